@@ -1,0 +1,120 @@
+/*
+ * MGPBD ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, serial fp64 CPU implementation of one MGPBD frame (Algorithm 1,
+ * PAPER.md:203-227) and of every step on its hot path.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.  It shares no code,
+ * header, table or constant generator with the CUDA library (paper_2505_13390_b200/csrc).
+ *
+ * Every function cites the passage it follows (PAPER.md line; SURVEY.md §8(c) reading id).
+ * Parity status per function is listed in DESIGN.md §"Oracle pins".  "parity unpinned":
+ * the *partition* produced by orc_aggregate is unpinned w.r.t. the paper (its visiting order
+ * is unstated; reading c2) — its invariants are pinned by tests.
+ */
+#ifndef MGPBD_ORACLE_H
+#define MGPBD_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+    double theta;            /* SOC threshold, PAPER.md:250 (0.1) */
+    int32_t min_coarse;      /* coarsen while n >= this, PAPER.md:241 (400) */
+    int32_t max_levels;      /* 16 (reading c7) */
+    double stall_ratio;      /* 0.9 (reading c7) */
+    int32_t setup_interval;  /* 20 */
+    int32_t bootstrap_sweeps;/* 20 */
+    int32_t power_iters;     /* 100 (reading c9) */
+    double lambda_min_est;   /* 0.1 */
+    int32_t smoother_sweeps; /* 2 */
+    int32_t pcg_iters;       /* 10 (reading c10) */
+    double omega_relax;      /* 0.1 tet / 0.25 cloth */
+    double gravity[3];       /* (0,-9.8,0) */
+    uint64_t seed;           /* 1 */
+} orc_config;
+
+void orc_config_default(orc_config* c);
+
+/* ---- hash (reading c0) ---- */
+uint64_t orc_mix64(uint64_t z);
+uint64_t orc_key(uint64_t seed, int stream, int level, uint64_t i);
+double orc_uniform(uint64_t seed, int stream, int level, uint64_t i);
+
+/* ---- constraints (a1) ---- */
+void orc_rest_distance(int32_t m, const int32_t* verts, const double* X, double* rest_len);
+int orc_rest_arap(int32_t m, const int32_t* verts, const double* X, double* Dm_inv, double* vol);
+void orc_eval_distance(int32_t m, const int32_t* verts, const double* x, const double* rest_len,
+                       double* C, double* g /* m*2*3 */);
+void orc_polar(const double* F /*9 row-major*/, double* R /*9*/);
+void orc_eval_arap(int32_t m, const int32_t* verts, const double* x, const double* Dm_inv,
+                   double* C, double* g /* m*4*3 */);
+
+/* ---- pattern + assembly (a2) ---- */
+int64_t orc_pattern(int32_t m, int kind, const int32_t* verts, int32_t n_verts,
+                    int64_t* rowptr /* m+1 or NULL */, int32_t* col /* nnz or NULL */);
+void orc_assemble(int32_t m, int kind, const int32_t* verts, const double* w, const double* g,
+                  const double* alpha_tilde, const int64_t* rowptr, const int32_t* col, double* val);
+void orc_rhs(int32_t m, const double* C, const double* alpha_tilde, const double* lambda, double* b);
+void orc_apply_dx(int32_t m, int kind, const int32_t* verts, int32_t n_verts, const double* w,
+                  const double* g, const double* dlambda, double* dx /* 3*n_verts */);
+
+/* ---- sparse helpers ---- */
+void orc_spmv(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+              const double* x, double* y);
+
+/* ---- setup (a3-a8) ---- */
+void orc_soc(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, double theta,
+             uint8_t* strong);
+int32_t orc_aggregate(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                      const uint8_t* strong, uint64_t seed, int level, int32_t* agg);
+int32_t orc_colour(int32_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed,
+                   int32_t* colour);
+void orc_gs_bootstrap(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                      const int32_t* colour, int32_t sweeps, uint64_t seed, double* B);
+void orc_prolongator(int32_t n, const int32_t* agg, int32_t n_agg, const double* B, double* P,
+                     double* B_next);
+int64_t orc_galerkin(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                     const int32_t* agg, const double* P, int32_t n_agg,
+                     int64_t* crowptr, int32_t* ccol, double* cval /* all NULL => count only */);
+double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                 int32_t iters, uint64_t seed, int level);
+int orc_cholesky(int32_t n, const double* A /* dense n*n */, double* L /* n*n */);
+void orc_chol_solve(int32_t n, const double* L, const double* b, double* x);
+
+/* ---- hierarchy / solve (a6-a11) ---- */
+typedef struct orc_hier orc_hier;
+orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                         const orc_config* cfg);
+int orc_hier_refresh(orc_hier* h, const double* val0); /* new A_0 values: Galerkin + coarse factor */
+void orc_hier_free(orc_hier* h);
+int orc_hier_levels(const orc_hier* h);
+void orc_hier_level_size(const orc_hier* h, int l, int32_t* n, int64_t* nnz);
+void orc_hier_get_level(const orc_hier* h, int l, int64_t* rowptr, int32_t* col, double* val);
+void orc_hier_get_agg(const orc_hier* h, int l, int32_t* agg);
+void orc_hier_get_P(const orc_hier* h, int l, double* P);
+double orc_hier_omega(const orc_hier* h, int l);
+void orc_hier_get_B0(const orc_hier* h, double* B);
+int32_t orc_hier_n_colours(const orc_hier* h);
+void orc_vcycle(const orc_hier* h, const double* b, double* x);
+int orc_pcg(const orc_hier* h, const double* b, int32_t iters, double* x, double* rz_trace);
+
+/* ---- simulation (Algorithm 1) ---- */
+typedef struct orc_sim orc_sim;
+orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* verts,
+                        const double* rest_pos, const double* pos, const double* vel,
+                        const double* inv_mass, const double* compliance, const orc_config* cfg);
+int orc_sim_step(orc_sim* s, double dt, int32_t n_iters);
+void orc_sim_mark_stale(orc_sim* s);
+void orc_sim_get(const orc_sim* s, double* x, double* v, double* lambda);
+void orc_sim_set(orc_sim* s, const double* x, const double* v);
+const orc_hier* orc_sim_hier(const orc_sim* s);
+int64_t orc_sim_nnz(const orc_sim* s);
+void orc_sim_get_A(const orc_sim* s, int64_t* rowptr, int32_t* col, double* val);
+void orc_sim_get_b_norms(const orc_sim* s, double* out, int32_t n);
+void orc_sim_free(orc_sim* s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

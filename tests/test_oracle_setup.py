@@ -1,0 +1,288 @@
+"""Pins of the oracle's AMG setup: SOC, aggregation, colouring, GS bootstrap,
+prolongator, Galerkin, power method and the coarsest Cholesky."""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from paper_2505_13390_b200 import scenes
+from _util import csr_from_dense_diaglast, dense
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+def random_spd_pattern(n, deg, seed):
+    rng = np.random.default_rng(seed)
+    A = np.zeros((n, n))
+    for i in range(n):
+        for j in rng.choice(n, size=deg, replace=False):
+            if i != j:
+                v = rng.normal()
+                A[i, j] = A[j, i] = v
+    A += np.diag(np.abs(A).sum(1) + 1.0)
+    return A
+
+
+@pytest.fixture(scope="module")
+def cloth_frame(O):
+    """cloth32 frame-0 system assembled by the oracle's own Alg.1 first iteration."""
+    sc = scenes.cloth(32, dt=3e-3)
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    return sc, sim.A()
+
+
+@pytest.fixture(scope="module")
+def bar_frame(O):
+    sc = scenes.make("bar3k")
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    return sc, sim.A()
+
+
+def test_soc_hand_example_and_limits(O):
+    g = GOLD["soc_3x3"]
+    r, c, v = csr_from_dense_diaglast(np.array(g["A"], float))
+    s = O.soc(r, c, v, 0.1)
+    kept = sorted([[i, int(c[e])] for i in range(3) for e in range(r[i], r[i + 1]) if s[e]])
+    assert kept == sorted(g["strong_pairs"])
+    A = random_spd_pattern(30, 4, 0)
+    r, c, v = csr_from_dense_diaglast(A)
+    s0 = O.soc(r, c, v, 0.0)
+    assert all(s0[e] == (c[e] != i) for i in range(30) for e in range(r[i], r[i + 1]))
+    assert O.soc(r, c, v, 1e9).sum() == 0
+    s = O.soc(r, c, v, 0.3)
+    S = dense(r, c, s.astype(float))
+    assert np.array_equal(S, S.T)
+
+
+def mis2_parallel_rounds(n, adj, prio):
+    """Independent pin: lexicographically-first MIS of S^2 by parallel rounds (Luby/Blelloch-style):
+    an undecided node joins when it has the smallest priority among undecided nodes within distance 2;
+    nodes within distance 2 of a new member become decided."""
+    d2 = [set() for _ in range(n)]
+    for i in range(n):
+        for j in adj[i]:
+            d2[i].add(j)
+            d2[i] |= adj[j]
+        d2[i].discard(i)
+    state = np.zeros(n, int)  # 0 undecided, 1 in, 2 out
+    while (state == 0).any():
+        new = [i for i in range(n) if state[i] == 0 and all(state[j] != 0 or prio[j] > prio[i] for j in d2[i])]
+        for i in new:
+            state[i] = 1
+        for i in new:
+            for j in d2[i]:
+                if state[j] == 0:
+                    state[j] = 2
+    return state == 1
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_aggregation_equals_parallel_mis2_and_invariants(O, seed):
+    A = random_spd_pattern(60, 3, seed)
+    r, c, v = csr_from_dense_diaglast(A)
+    s = O.soc(r, c, v, 0.1)
+    agg, na = O.aggregate(r, c, v, s, seed=7, level=2)
+    n = 60
+    adj = [set(int(c[e]) for e in range(r[i], r[i + 1]) if s[e]) for i in range(n)]
+    prio = {i: (O.key(7, 1, 2, i), i) for i in range(n)}
+    seeds = mis2_parallel_rounds(n, adj, prio)
+    # ids are the rank of the seed by node index
+    seed_ids = np.cumsum(seeds) - 1
+    assert na == seeds.sum()
+    assert sorted(set(agg.tolist())) == list(range(na))             # a partition into na aggregates
+    for i in range(n):
+        if seeds[i]:
+            assert agg[i] == seed_ids[i]
+            for j in adj[i]:
+                assert agg[j] == seed_ids[i]                        # pass 1 claims S-neighbours
+    p1 = np.full(n, -1)
+    for i in range(n):
+        if seeds[i]:
+            p1[i] = seed_ids[i]
+            for j in adj[i]:
+                p1[j] = seed_ids[i]
+    for i in range(n):                                              # pass 2: strongest neighbour
+        if p1[i] < 0:
+            cand = [(abs(A[i, j]), -p1[j]) for j in adj[i] if p1[j] >= 0]
+            best = max(cand)
+            assert agg[i] == -best[1]
+
+
+def test_aggregation_partition_on_cloth(O, cloth_frame):
+    sc, (r, c, v) = cloth_frame
+    s = O.soc(r, c, v, 0.1)
+    agg, na = O.aggregate(r, c, v, s)
+    assert agg.min() == 0 and agg.max() == na - 1 and len(np.unique(agg)) == na
+
+
+def jp_colouring(n, adj, prio):
+    """Independent pin: Jones-Plassmann rounds in the same priority order."""
+    colour = -np.ones(n, int)
+    while (colour < 0).any():
+        ready = [i for i in range(n) if colour[i] < 0 and all(colour[j] >= 0 for j in adj[i] if prio[j] < prio[i])]
+        snap = colour.copy()
+        for i in ready:
+            used = {snap[j] for j in adj[i] if prio[j] < prio[i]}
+            k = 0
+            while k in used:
+                k += 1
+            colour[i] = k
+    return colour
+
+
+def test_colouring_equals_jones_plassmann(O, bar_frame):
+    sc, (r, c, v) = bar_frame
+    n = r.shape[0] - 1
+    sub = 600
+    # restrict to the leading principal block to keep the pure-python pin fast
+    A = dense(r, c, v)[:sub, :sub]
+    r2, c2, v2 = csr_from_dense_diaglast(A)
+    col, nc = O.colour(r2, c2, seed=1)
+    adj = [set(int(x) for x in c2[r2[i]:r2[i + 1]] if x != i) for i in range(sub)]
+    prio = {i: (O.key(1, 2, 0, i), i) for i in range(sub)}
+    assert np.array_equal(col, jp_colouring(sub, adj, prio))
+    assert nc == col.max() + 1
+    for i in range(sub):
+        assert all(col[j] != col[i] for j in adj[i])
+
+
+def test_gs_bootstrap_equals_library_triangular_solves(O, bar_frame):
+    sc, (r, c, v) = bar_frame
+    n = r.shape[0] - 1
+    col, _ = O.colour(r, c, 1)
+    B = O.gs_bootstrap(r, c, v, col, sweeps=3, seed=1)
+    # independent: GS sweep = forward substitution (D+L) x_new = -U x_old in (colour, index) order
+    A = sp.csr_matrix(dense(r, c, v))
+    perm = np.lexsort((np.arange(n), col))
+    Ap = A[perm][:, perm]
+    x = scenes.hash_uniform(1, 3, 0, np.arange(n)) * np.abs(v).max()
+    x = x[perm]
+    Lw = sp.tril(Ap, 0, format="csr"); Up = sp.triu(Ap, 1, format="csr")
+    for _ in range(3):
+        x = spla.spsolve_triangular(Lw, -(Up @ x), lower=True)
+    assert np.allclose(B[perm], x, rtol=1e-10, atol=1e-12 * np.abs(x).max())
+
+
+def test_gs_bootstrap_quality_and_fallback(O, cloth_frame):
+    sc, (r, c, v) = cloth_frame
+    n = r.shape[0] - 1
+    col, _ = O.colour(r, c, 1)
+    A = sp.csr_matrix(dense(r, c, v))
+    x0 = scenes.hash_uniform(1, 3, 0, np.arange(n)) * np.abs(v).max()
+    B = O.gs_bootstrap(r, c, v, col, sweeps=20, seed=1)
+    ratio0 = np.linalg.norm(A @ x0) / np.linalg.norm(x0)
+    ratio = np.linalg.norm(A @ B) / np.linalg.norm(B)
+    assert ratio <= 0.1 * ratio0
+    ri, ci, vi = csr_from_dense_diaglast(np.eye(50))                # identity: GS annihilates x
+    B = O.gs_bootstrap(ri, ci, vi, np.zeros(50, np.int32), 20, 1)
+    assert np.array_equal(B, np.ones(50))                           # SPEC.md:279, 312 fallback
+
+
+def test_prolongator_hand_cases_and_orthonormality(O):
+    for cse in GOLD["prolongator"]["cases"]:
+        agg = np.array(cse["agg"], np.int32)
+        P, Bn = O.prolongator(agg, int(agg.max()) + 1, np.array(cse["B"], float))
+        assert np.allclose(P, cse["P"], rtol=1e-15) and np.allclose(Bn, cse["B_next"], rtol=1e-15)
+    rng = np.random.default_rng(0)
+    agg = rng.integers(0, 7, 40).astype(np.int32)
+    agg[:7] = np.arange(7)
+    B = rng.normal(size=40)
+    P, Bn = O.prolongator(agg, 7, B)
+    Pm = np.zeros((40, 7)); Pm[np.arange(40), agg] = P
+    assert np.allclose(Pm.T @ Pm, np.eye(7), atol=1e-12)          # P^T P = I
+    assert np.allclose(Pm @ Bn, B, atol=1e-12)                     # P B_{l+1} = B (QR)
+    Bz = B.copy(); Bz[agg == 3] = 0.0                              # zero-norm aggregate
+    P, Bn = O.prolongator(agg, 7, Bz)
+    k = (agg == 3).sum()
+    assert Bn[3] == 0.0 and np.allclose(P[agg == 3], 1 / np.sqrt(k))
+
+
+def test_galerkin_special_cases_and_dense(O):
+    A = random_spd_pattern(50, 4, 3)
+    r, c, v = csr_from_dense_diaglast(A)
+    cr, cc, cv = O.galerkin(r, c, v, np.arange(50, dtype=np.int32), np.ones(50), 50)   # P = I
+    assert np.array_equal(dense(cr, cc, cv), A)
+    cr, cc, cv = O.galerkin(r, c, v, np.zeros(50, np.int32), np.ones(50), 1)           # one all-ones column
+    assert np.isclose(cv[0], A.sum(), rtol=1e-13)
+    rng = np.random.default_rng(5)
+    for t in range(10):
+        n = int(rng.integers(20, 200)); na = int(rng.integers(1, n // 3 + 1))
+        A = random_spd_pattern(n, 3, 100 + t)
+        r, c, v = csr_from_dense_diaglast(A)
+        agg = rng.integers(0, na, n).astype(np.int32); agg[:na] = np.arange(na)
+        P = rng.normal(size=n)
+        cr, cc, cv = O.galerkin(r, c, v, agg, P, na)
+        Pm = np.zeros((n, na)); Pm[np.arange(n), agg] = P
+        Ad = Pm.T @ A @ Pm
+        Ac = dense(cr, cc, cv)
+        assert np.abs(Ac - Ad).max() <= 1e-12 * np.abs(Ad).max()
+        for a in range(na):                                          # diag last, off-diags ascending
+            row = cc[cr[a]:cr[a + 1]]
+            assert row[-1] == a and np.all(np.diff(row[:-1]) > 0)
+        # pattern = structural product pattern
+        S = (np.abs(Pm).T @ (A != 0).astype(float) @ (Pm != 0).astype(float)) != 0
+        assert np.array_equal(S, Ac != 0) or np.array_equal(S, dense(cr, cc, np.ones_like(cv)) != 0)
+
+
+def test_power_method(O):
+    g = GOLD["power_method"]
+    r, c, v = csr_from_dense_diaglast(np.diag(g["diag"]).astype(float) * 1.0)
+    # D^-1 A = I for a diagonal matrix: lambda = 1; so scale D: use A = diag(d) with D = I trick below
+    assert np.isclose(O.power(r, c, v, 100), 1.0, rtol=1e-12)
+    # diag(1,2,5) as D^-1 A: A = [[1,0,0],[0,2,0],[0,0,5]] with unit diagonal D is impossible in CSR
+    # diag-last form, so pin with A = D^{1/2} M D^{1/2}: embed M = Q diag(1,2,5) Q^T, D = I
+    rng = np.random.default_rng(0)
+    Q = np.linalg.qr(rng.normal(size=(3, 3)))[0]
+    M = Q @ np.diag(g["diag"]) @ Q.T
+    Dh = np.diag(np.diag(M))
+    r, c, v = csr_from_dense_diaglast(M)
+    lam = O.power(r, c, v, 200)
+    ev = np.linalg.eigvals(np.linalg.solve(Dh, M)).real.max()       # library eigen-solver
+    assert np.isclose(lam, ev, rtol=1e-3)
+    for t in range(3):
+        A = random_spd_pattern(80, 5, 200 + t)
+        r, c, v = csr_from_dense_diaglast(A)
+        d = np.sqrt(np.diag(A))
+        ev = np.linalg.eigvalsh(A / np.outer(d, d)).max()
+        # SPEC.md:88 asks 1e-3 at 200 iterations; small spectral gaps need more: pin the limit
+        assert np.isclose(O.power(r, c, v, 5000), ev, rtol=1e-6)
+    for cse in GOLD["omega"]["cases"]:
+        assert np.isclose(2.0 / (cse["lmax"] + 0.1), cse["omega"], rtol=1e-15)
+
+
+def test_cholesky_vs_library(O):
+    A = random_spd_pattern(120, 6, 9)
+    L, rc = O.cholesky(A)
+    assert rc == 0 and np.allclose(L, np.linalg.cholesky(A), rtol=1e-12, atol=1e-14)
+    b = np.random.default_rng(1).normal(size=120)
+    assert np.allclose(O.chol_solve(L, b), np.linalg.solve(A, b), rtol=1e-10)
+    _, rc = O.cholesky(-np.eye(3))
+    assert rc != 0
+
+
+def test_hierarchy_invariants_cloth_and_table1(O, cloth_frame):
+    sc, (r, c, v) = cloth_frame
+    h = O.Hierarchy(r, c, v)
+    L = h.n_levels
+    assert L >= 2
+    for l in range(L - 1):
+        n, _ = h.level_size(l)
+        agg, P = h.agg(l), h.P(l)
+        na = h.level_size(l + 1)[0]
+        Pm = sp.csr_matrix((P, (np.arange(n), agg)), shape=(n, na))
+        assert np.allclose((Pm.T @ Pm).toarray(), np.eye(na), atol=1e-10)
+        Al = sp.csr_matrix(dense(*h.level(l)))
+        Ac = dense(*h.level(l + 1))
+        assert np.abs(Ac - (Pm.T @ Al @ Pm).toarray()).max() <= 1e-12 * np.abs(Ac).max()
+        assert np.array_equal(Ac, Ac.T) or np.abs(Ac - Ac.T).max() <= 1e-14 * np.abs(Ac).max()
+        np.linalg.cholesky(Ac)
+        assert 0 < h.omega(l) < 2
+    assert h.level_size(L - 1)[0] < 400
+    t = GOLD["table1"]
+    # loose consistency with Table 1 (cloth C = 1.046, nl = 5): C close to 1, nl small
+    assert 1.0 <= h.operator_complexity() < 1.1 and t["nl_min"] <= L <= t["nl_max"]

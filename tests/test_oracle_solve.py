@@ -1,0 +1,219 @@
+"""Pins of the oracle's V-cycle, MGPCG and Algorithm-1 frame."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2505_13390_b200 import scenes
+from _util import csr_from_dense_diaglast, dense
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def bar_sys(O):
+    sc = scenes.make("bar3k")
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    return r, c, v, dense(r, c, v)
+
+
+def test_single_level_vcycle_is_dense_solve(O):
+    sc = scenes.make("bar_small")                      # 96 rows < 400: one level (c7)
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    h = O.Hierarchy(r, c, v)
+    assert h.n_levels == 1
+    b = np.random.default_rng(0).normal(size=96)
+    A = dense(r, c, v)
+    assert np.allclose(h.vcycle(b), np.linalg.solve(A, b), rtol=1e-10)
+    x, rc, _ = h.pcg(b, 1)                              # exact after one PCG iteration
+    assert rc == 0 and np.allclose(x, np.linalg.solve(A, b), rtol=1e-9)
+
+
+def test_vcycle_linear_symmetric_zero(O, bar_sys):
+    r, c, v, A = bar_sys
+    h = O.Hierarchy(r, c, v)
+    assert h.n_levels >= 2
+    rng = np.random.default_rng(1)
+    n = A.shape[0]
+    assert np.array_equal(h.vcycle(np.zeros(n)), np.zeros(n))
+    for _ in range(10):
+        u, w = rng.normal(size=n), rng.normal(size=n)
+        a, b = rng.normal(size=2)
+        lhs = h.vcycle(a * u + b * w)
+        rhs = a * h.vcycle(u) + b * h.vcycle(w)
+        assert np.linalg.norm(lhs - rhs) <= 1e-10 * np.linalg.norm(lhs)
+        Mu, Mw = h.vcycle(u), h.vcycle(w)
+        assert abs(Mu @ w - u @ Mw) <= 1e-8 * abs(Mu @ w) + 1e-8 * np.linalg.norm(Mu) * np.linalg.norm(w) * 1e-3
+        assert u @ Mu > 0                                                           # SPD preconditioner
+
+
+def test_vcycle_two_level_matches_dense_definition(O, bar_sys):
+    """Dense re-derivation of one two-level V-cycle from the level matrices and P."""
+    r, c, v, A = bar_sys
+    cfg = O.default_config(max_levels=2)
+    h = O.Hierarchy(r, c, v, cfg)
+    assert h.n_levels == 2
+    n = A.shape[0]
+    agg, P, w = h.agg(0), h.P(0), h.omega(0)
+    Pm = np.zeros((n, agg.max() + 1)); Pm[np.arange(n), agg] = P
+    Ac = Pm.T @ A @ Pm
+    Dinv = 1.0 / np.diag(A)
+    b = np.random.default_rng(2).normal(size=n)
+    x = np.zeros(n)
+    for _ in range(2):
+        x = x + w * Dinv * (b - A @ x)
+    x = x + Pm @ np.linalg.solve(Ac, Pm.T @ (b - A @ x))
+    for _ in range(2):
+        x = x + w * Dinv * (b - A @ x)
+    assert np.allclose(h.vcycle(b), x, rtol=1e-9, atol=1e-12 * np.abs(x).max())
+
+
+def test_pcg_finite_termination_and_monotone_A_norm(O, bar_sys):
+    r, c, v, A = bar_sys
+    h = O.Hierarchy(r, c, v)
+    b = np.random.default_rng(3).normal(size=A.shape[0])
+    xs = np.linalg.solve(A, b)
+    errs = []
+    for K in range(1, 41, 3):
+        x, rc, _ = h.pcg(b, K)
+        assert rc == 0
+        e = x - xs
+        errs.append(np.sqrt(e @ A @ e))
+    assert all(errs[i + 1] <= errs[i] * (1 + 1e-9) for i in range(len(errs) - 1))   # monotone in A-norm
+    x, rc, _ = h.pcg(b, 300)
+    assert np.linalg.norm(A @ x - b) <= 1e-3 * np.linalg.norm(b)
+    # CG finite termination on a tiny SPD system forced into several levels (K >> n): dense solution
+    sc = scenes.make("bar_small")
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    A = dense(r, c, v)
+    h = O.Hierarchy(r, c, v, O.default_config(min_coarse=20))
+    assert h.n_levels >= 2
+    b = np.random.default_rng(5).normal(size=A.shape[0])
+    x, rc, _ = h.pcg(b, 400)
+    assert np.linalg.norm(A @ x - b) <= 1e-8 * np.linalg.norm(b)
+
+
+def test_pcg_identity(O):
+    r, c, v = csr_from_dense_diaglast(np.eye(500))    # all-singleton stall => one dense level
+    h = O.Hierarchy(r, c, v)
+    b = np.random.default_rng(4).normal(size=500)
+    x, rc, _ = h.pcg(b, 1)
+    assert rc == 0 and np.allclose(x, b, rtol=1e-14)
+
+
+def _python_frame(O, sc, n_iters, omega, gravity=(0, -9.8, 0)):
+    """Algorithm 1 with a dense direct solve in place of MGPCG."""
+    x = sc.pos.copy(); v = sc.vel.copy(); w = sc.inv_mass
+    x_old = x.copy()
+    v[w > 0] += sc.dt * np.asarray(gravity)
+    x = x + sc.dt * v
+    lam = np.zeros(sc.n_cons)
+    at = sc.compliance / sc.dt ** 2
+    rowptr, col = O.pattern(sc.verts, sc.n_verts)
+    rest = O.rest_distance(sc.verts, sc.rest_pos) if sc.kind == 2 else O.rest_arap(sc.verts, sc.rest_pos)[0]
+    for _ in range(n_iters):
+        Cv, g = (O.eval_distance if sc.kind == 2 else O.eval_arap)(sc.verts, x, rest)
+        A = dense(rowptr, col, O.assemble(sc.verts, w, g, at, rowptr, col))
+        dl = np.linalg.solve(A, -Cv - at * lam)
+        dx = O.apply_dx(sc.verts, sc.n_verts, w, g, dl)
+        lam += dl
+        x = x + omega * dx
+    return x, (x - x_old) / sc.dt, lam
+
+
+@pytest.mark.parametrize("name", ["cloth4", "bar_small"])
+def test_frame_equals_dense_direct_frame(O, name):
+    sc = scenes.cloth(4, dt=3e-3) if name == "cloth4" else scenes.make(name)
+    cfg = O.default_config(omega_relax=sc.omega_relax, pcg_iters=3)
+    sim = O.Sim(sc, cfg)
+    assert sim.step(sc.dt, 4) == 0
+    x, v, lam = sim.state()
+    xr, vr, lr = _python_frame(O, sc, 4, sc.omega_relax)
+    assert np.allclose(lam, lr, rtol=1e-9, atol=1e-12 * np.abs(lr).max())
+    assert np.allclose(x - sc.pos, xr - sc.pos, rtol=1e-9, atol=1e-12 * np.abs(xr - sc.pos).max())
+
+
+def test_single_constraint_closed_form_eq4_eq5(O):
+    """One distance constraint: the hierarchy is one 1x1 level, so each outer iteration is exactly
+    Eq. 4 (dlambda = -(C + at lambda)/(w_a + w_b + at)) followed by Eq. 5."""
+    g = GOLD["single_constraint_xpbd"]
+    X = np.array([[0, 0, 0], [1, 0, 0]], float)
+    x0 = np.array([[0, 0, 0], [2, 0, 0]], float)          # stretch 1
+    sc = scenes.Scene("edge", 2, np.array([[0, 1]], np.int32), X, x0, np.zeros_like(X),
+                      np.ones(2), np.zeros(1), 1.0, 1.0)
+    cfg = O.default_config(omega_relax=1.0, gravity=(0, 0, 0), pcg_iters=1)
+    sim = O.Sim(sc, cfg)
+    sim.step(1.0, 1)
+    x, v, lam = sim.state()
+    assert np.isclose(lam[0], g["dlambda"], rtol=1e-15)
+    assert np.allclose(x, [[g["move"], 0, 0], [2 - g["move"], 0, 0]], rtol=1e-15)
+    # compliant case, two iterations, omega = 0.5, masses (1, 3)
+    alpha, dt, om = 0.3, 0.5, 0.5
+    sc = scenes.Scene("edge", 2, np.array([[0, 1]], np.int32), X, x0, np.zeros_like(X),
+                      np.array([1.0, 1 / 3.0]), np.array([alpha]), dt, om)
+    sim = O.Sim(sc, O.default_config(omega_relax=om, gravity=(0, 0, 0), pcg_iters=2))
+    sim.step(dt, 2)
+    x, _, lam = sim.state()
+    at = alpha / dt ** 2
+    xa, xb, l = x0[0].copy(), x0[1].copy(), 0.0
+    for _ in range(2):
+        d = xa - xb; L = np.linalg.norm(d); u = d / L
+        dl = -((L - 1.0) + at * l) / (1.0 + 1 / 3.0 + at)           # Eq. 4
+        xa = xa + om * 1.0 * u * dl; xb = xb - om * (1 / 3.0) * u * dl   # Eq. 5
+        l += dl
+    assert np.isclose(lam[0], l, rtol=1e-13) and np.allclose(x, [xa, xb], rtol=1e-13)
+
+
+def test_rest_state_identity_and_pins(O):
+    for sc in [scenes.cloth(8, jitter=0.0), scenes.kuhn_block(4, 2, 2, 0.05, squash=1.0, twist_deg=0.0, jitter=0.0)]:
+        cfg = O.default_config(omega_relax=sc.omega_relax, gravity=(0, 0, 0))
+        sim = O.Sim(sc, cfg)
+        sim.step(sc.dt, 3)
+        x, v, lam = sim.state()
+        assert np.abs(x - sc.pos).max() <= 1e-12 and np.abs(lam).max() <= 1e-9
+    sc = scenes.cloth(8)
+    sim = O.Sim(sc)
+    for _ in range(3):
+        sim.step(sc.dt, 3)
+    x, v, _ = sim.state()
+    pinned = sc.inv_mass == 0
+    assert np.array_equal(x[pinned], sc.pos[pinned]) and np.all(v[pinned] == 0)
+
+
+def test_semi_euler_free_fall(O):
+    g = GOLD["semi_euler"]
+    X = np.array([[0, 0, 0], [1, 0, 0]], float)
+    sc = scenes.Scene("edge", 2, np.array([[0, 1]], np.int32), X, X.copy(), np.zeros_like(X),
+                      np.ones(2), np.array([1e300]), g["dt"], 1.0)
+    sim = O.Sim(sc, O.default_config(omega_relax=0.0))
+    sim.step(g["dt"], 1)
+    x, _, _ = sim.state()
+    assert np.allclose(x - X, [[0, g["dy"], 0]] * 2, rtol=1e-12)
+
+
+def test_lambda_fixed_point(O):
+    """At convergence of the outer loop lambda = -alpha_tilde^-1 C."""
+    sc = scenes.cloth(4, dt=0.02, stiffness=1e3)
+    sim = O.Sim(sc, O.default_config(omega_relax=1.0, pcg_iters=5, gravity=(0, -9.8, 0)))
+    sim.step(sc.dt, 60)
+    x, _, lam = sim.state()
+    Cv, _ = O.eval_distance(sc.verts, x, O.rest_distance(sc.verts, sc.rest_pos))
+    at = sc.compliance / sc.dt ** 2
+    assert np.allclose(lam, -Cv / at, rtol=1e-6, atol=1e-9 * np.abs(lam).max())
+
+
+def test_deterministic(O):
+    sc = scenes.make("cloth16")
+    outs = []
+    for _ in range(2):
+        sim = O.Sim(sc)
+        sim.step(sc.dt, sc.n_iters)
+        outs.append(sim.state())
+    assert all(np.array_equal(a, b) for a, b in zip(*outs))
