@@ -1,0 +1,298 @@
+#!/usr/bin/env python
+"""Benchmark of the MGPBD hot path (BASELINE.json metric: ms/frame @20 AMG-PCG iterations on the
+1.67M-tet block, plus level-0 CSR-pass HBM GB/s).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+                  [--precision fp32|fp64]
+
+One step = one frame of Algorithm 1 (20 outer iterations x 10 MGPCG iterations, lazy setup every 20
+frames, so a 20-frame window holds exactly one setup).  Rank 0 prints one JSON line.
+--impl reference times the CPU oracle (the tier's reference arm) on a bounded slab of the same
+workload and scales by constraint count (time per iteration is linear in size).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ms/frame @20 AMG-PCG iters (1.7M-tet block) at 1/2/4/8 B200; SpMV HBM GB/s"
+UNIT = "ms/frame"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{index}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1])); smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def slab_scene(full_name, cells):
+    from paper_2505_13390_b200 import scenes
+    if full_name.startswith("block"):
+        return scenes.kuhn_block(cells, 64, 32, 0.01, dt=3e-3, squash=0.7, twist_deg=45.0 * cells / 136.0,
+                                 n_iters=20, name=f"blockslab{cells}")
+    raise ValueError(full_name)
+
+
+def oracle_frame_ms(sc, frames=1):
+    """Oracle wall time of `frames` frames of sc, setup amortised over setup_interval (1 core)."""
+    import oracle as O
+    sim = O.Sim(sc)
+    t0 = time.perf_counter()
+    for _ in range(frames):
+        sim.step(sc.dt, sc.n_iters)
+    total = (time.perf_counter() - t0) * 1e3
+    r, c, v = sim.A()
+    t1 = time.perf_counter()
+    O.Hierarchy(r, c, v, sim.cfg)
+    ts = (time.perf_counter() - t1) * 1e3                 # one setup, timed alone
+    setups = (frames + sim.cfg.setup_interval - 1) // sim.cfg.setup_interval
+    amort = (total - setups * ts + frames * ts / sim.cfg.setup_interval) / frames
+    return amort, total / frames, ts
+
+
+def config_dict(sc, args, extra=None):
+    d = {"workload": sc.name, "n_cons": sc.n_cons, "n_verts": sc.n_verts, "n_iters": sc.n_iters,
+         "pcg_iters": sc.pcg_iters, "setup_interval": 20, "precision": args.precision,
+         "accumulation": "fp64", "l2": "inputs larger than L2 (level-0 matrix streamed from HBM every pass)",
+         "parallelism": f"replicas x{args.gpus}" if args.gpus > 1 else "single GPU"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_2505_13390_b200 import scenes
+    full = scenes.make(args.config) if not args.config.startswith("block1.67M") else None
+    m_full = 1671168 if args.config == "block1.67M" else full.n_cons
+    cells = 2
+    sc = slab_scene("block", cells) if args.config.startswith("block") else full
+    scale = m_full / sc.n_cons
+    import oracle as O
+    sim = O.Sim(sc)
+    times = []
+    for k in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        sim.step(sc.dt, sc.n_iters)
+        dt_ms = (time.perf_counter() - t0) * 1e3
+        if k >= args.warmup:
+            times.append(dt_ms)
+    ms = statistics.mean(times) * scale
+    sample = (f"oracle frames of {sc.name} ({sc.n_cons} tets, {args.steps} timed frames after {args.warmup} "
+              f"warm-up, one setup per 20 frames), scaled x{scale:.1f} by constraint count to {args.config}")
+    out = {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": args.config, "n_cons": m_full, "n_iters": 20, "pcg_iters": 10,
+                      "precision": "fp64 (oracle)", "sample": sc.name},
+           "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_2505_13390_b200 import mgpbd, scenes
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    sc = scenes.make(args.config)
+    prec = 1 if args.precision == "fp32" else 0
+    stream = torch.cuda.Stream()
+    ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=1)
+    for _ in range(args.warmup):
+        ctx.step(sc.dt, sc.n_iters)
+    st0 = ctx.stats()
+    levels = [(int(st0.n[l]), int(st0.nnz[l])) for l in range(st0.n_levels)]
+
+    def barrier():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    l0_ms = l0_bytes = 0.0
+    launches = 0
+    frames_ms, setup_ms = [], []
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.step(sc.dt, sc.n_iters)
+            s = ctx.stats()
+            l0_ms += s.l0_pass_ms
+            l0_bytes += s.l0_pass_bytes
+            launches += s.kernel_launches
+            frames_ms.append(s.ms_frame)
+            if s.setup_ran:
+                setup_ms.append(s.ms_setup)
+        e1.record(stream)
+        barrier()
+    t_ms = e0.elapsed_time(e1)
+    if dist:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+        ll = torch.tensor([launches], device="cuda", dtype=torch.int64)
+        dist.all_reduce(ll)
+        launches = int(ll.item())
+    ms_per_step = t_ms / args.steps
+    value = ms_per_step / world      # replicas: each step advances `world` blocks by one frame
+
+    # e2e: through the public API with host buffers (pinned), H2D of the state + D2H of the result
+    n, m = sc.n_verts, sc.n_cons
+    pos_h = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+    vel_h = torch.empty((n, 3), dtype=torch.float64, pin_memory=True).numpy()
+    lam_h = torch.empty((m,), dtype=torch.float64, pin_memory=True).numpy()
+    ctx.positions(pos_h)
+    vel_h[:] = ctx.velocities()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ctx.set_state(pos_h, vel_h)
+        ctx.step(sc.dt, sc.n_iters)
+        ctx.positions(pos_h)
+        vel_h[:] = ctx.velocities()
+        ctx.lambdas(lam_h)
+    barrier()
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    if dist:
+        tt = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_ms = float(tt.item())
+
+    peak, peak_kind = measured_peaks()
+    achieved = (l0_bytes / 1e9) / (l0_ms / 1e3) if l0_ms > 0 else None
+    clocks = clk.summary()
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if prec else "f64", "data": "synthetic",
+        "config": config_dict(sc, args, {
+            "nnz_A0": levels[0][1] if levels else None, "levels": levels,
+            "op_complexity": st0.op_complexity,
+            "ms_setup_frame_extra": (statistics.mean(setup_ms) if setup_ms else None),
+            "setups_in_window": len(setup_ms),
+            "ms_frame_median": statistics.median(frames_ms)}),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "kernel": "level-0 CSR passes (k_pass: omega-Jacobi / residual*P / SpMV+dot)",
+                     "peak_kind": peak_kind, "l0_pass_share_of_step": (l0_ms / t_ms) if t_ms else None},
+        "e2e": {"value": e2e_ms / world, "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * n * 8,
+                "d2h_bytes_per_step": (2 * 3 * n + m) * 8},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cells = args.cpu_slab
+        sc_s = slab_scene(args.config, cells) if args.config.startswith("block") else sc
+        amort, raw, ts = oracle_frame_ms(sc_s, 1)
+        scale = sc.n_cons / sc_s.n_cons
+        out["cpu_baseline"] = {
+            "value": amort * scale, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"one oracle frame (20 outer x 10 PCG, fp64, 1 core) of {sc_s.name} ({sc_s.n_cons} tets): "
+                       f"{raw:.0f} ms incl. one {ts:.0f} ms setup, setup amortised /20, scaled x{scale:.1f} by "
+                       f"constraint count")}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    ctx.close()
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="block1.67M")
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-slab", type=int, default=8, help="x-slabs of the block the oracle sample uses")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

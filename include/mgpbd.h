@@ -1,0 +1,168 @@
+/*
+ * mgpbd.h — C-ABI of libmgpbd.so, the B200-native (sm_100a) hot path of MGPBD (arXiv 2505.13390).
+ *
+ * One frame of PAPER.md Algorithm 1: predict, then n_iters outer iterations of
+ * {evaluate C and grad C; re-assemble A = grad C M^-1 grad C^T + alpha_tilde into the fixed CSR
+ * pattern; b = -C - alpha_tilde lambda (Eq. 3); lazily rebuild the
+ * UA-AMG hierarchy; Galerkin A_{l+1} = P^T A_l P (Eq. 6,
+ * PAPER.md:309); MGPCG with one V-cycle per iteration; dx = M^-1 grad C^T
+ * dlambda (Eq. 5); lambda += dlambda; x += omega dx}, then v = (x - x_old)/dt.
+ * Every step runs in this library's own CUDA kernels on the device; there is no CPU fallback.
+ *
+ * Conventions (all functions):
+ *  - Ownership: input pointers are HOST memory borrowed for the duration of the call and copied.
+ *    Output buffers are caller-owned host memory.  The context owns all device memory and frees it
+ *    in mgpbd_destroy.
+ *  - Errors: functions return an mgpbd_status and never throw across the ABI; the context keeps a
+ *    last-error string (mgpbd_last_error).  Argument errors leave the state unchanged.  Solver
+ *    errors (indefinite preconditioner, non-finite values) are raised from device flags at the end
+ *    of mgpbd_step; the state is then the completed (possibly polluted) frame.
+ *  - Numbering: user numbering (constraint order and vertex order as passed to mgpbd_create) is
+ *    preserved at the boundary; the level-l matrices returned by the test hooks are CSR with
+ *    off-diagonals in ascending column order and the diagonal last in every row.
+ *  - Threading: one context per host thread; all work is enqueued on cfg.stream (NULL = a stream
+ *    the context creates) and every call returns after synchronising that stream.
+ */
+#ifndef MGPBD_H
+#define MGPBD_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MGPBD_API __attribute__((visibility("default")))
+#else
+#define MGPBD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mgpbd_ctx mgpbd_ctx; /* opaque; owns all device memory */
+
+typedef enum {
+    MGPBD_OK = 0,
+    MGPBD_E_ARG = -1,        /* invalid argument (state unchanged) */
+    MGPBD_E_CUDA = -2,       /* CUDA runtime error (message in mgpbd_last_error) */
+    MGPBD_E_NCCL = -3,       /* multi-GPU communication error */
+    MGPBD_E_OOM = -4,        /* device allocation failed */
+    MGPBD_E_INDEFINITE = -5, /* <z,r> <= 0 with r != 0 in PCG, or non-SPD coarsest */
+    MGPBD_E_NONFINITE = -6,  /* NaN/Inf reached the right-hand side or the PCG scalars */
+    MGPBD_E_STALL = -7       /* coarsening stalled with a coarsest level too large to invert */
+} mgpbd_status;
+
+typedef enum { MGPBD_DISTANCE = 2, MGPBD_TET_ARAP = 4 } mgpbd_kind; /* value = cardinality */
+
+typedef struct {
+    int32_t n_verts;
+    const double* rest_pos; /* 3*n_verts, xyz interleaved (rest shape: L or D_m, V) */
+    const double* pos;      /* 3*n_verts initial positions; NULL = rest_pos */
+    const double* vel;      /* 3*n_verts initial velocities; NULL = 0 */
+} mgpbd_mesh;
+
+typedef struct {
+    mgpbd_kind kind;        /* MGPBD_DISTANCE (cloth) or MGPBD_TET_ARAP (Eq. 8) */
+    int32_t n_cons;         /* m = number of constraints = rows of A */
+    const int32_t* verts;   /* kind*n_cons vertex ids, constraint-major */
+} mgpbd_constraints;
+
+typedef struct {
+    int32_t precision;        /* 0: fp64 everywhere; 1: fp32 storage of A, h, P and level vectors
+                                 with fp64 accumulation, fp64 setup, fp64 scalars and coarsest solve */
+    double theta;             /* SOC threshold theta_s, 0.1 */
+    int32_t k_nullspace;      /* near-kernel vectors per aggregate; only 1 is implemented (reading c1) */
+    int32_t min_coarse;       /* coarsen while n_l >= min_coarse, 400 */
+    int32_t max_levels;       /* 16 */
+    double stall_ratio;       /* stop coarsening when n_{l+1}/n_l > stall_ratio, 0.9 */
+    int32_t setup_interval;   /* lazy setup every k frames, 20 */
+    int32_t bootstrap_sweeps; /* GS sweeps on A x = 0, 20 */
+    int32_t power_iters;      /* power-method iterations for lambda_max(D^-1 A), 100 */
+    double lambda_min_est;    /* user estimate of lambda_min, 0.1 */
+    int32_t smoother_sweeps;  /* pre = post omega-Jacobi sweeps, 2 */
+    int32_t pcg_iters;        /* fixed MGPCG iterations per outer iteration (reading c10), 10 */
+    double omega_relax;       /* x += omega dx: 0.1 tets, 0.25 cloth */
+    double gravity[3];        /* (0, -9.8, 0) */
+    uint64_t seed;            /* hash seed (reading c0), 1 */
+    int32_t device;           /* CUDA device ordinal */
+    void* stream;             /* cudaStream_t, NULL = context-owned stream */
+    int32_t max_dense_coarse; /* largest coarsest level inverted densely, 8192 */
+    int32_t rank, world;      /* multi-GPU row partition; world must be 1 in this build */
+    int32_t profile;          /* 1: record CUDA events around the level-0 matrix passes */
+} mgpbd_config;
+
+#define MGPBD_MAX_LEVELS 16
+#define MGPBD_MAX_ITERS 256
+
+typedef struct {
+    int32_t n_levels;
+    int64_t n[MGPBD_MAX_LEVELS], nnz[MGPBD_MAX_LEVELS];
+    double op_complexity;              /* sum nnz_l / nnz_0 (Table 1 "C") */
+    double omega[MGPBD_MAX_LEVELS];    /* omega-Jacobi weight per level (coarsest: 0) */
+    int32_t n_colours;                 /* colours of the level-0 GS bootstrap */
+    int32_t setup_ran;                 /* setup ran in the last frame */
+    int32_t n_b;                       /* outer iterations recorded in b_norm */
+    double b_norm[MGPBD_MAX_ITERS];    /* ||b||_2 per outer iteration of the last frame */
+    int64_t frame;                     /* frames stepped so far */
+    /* profile == 1 only: summed CUDA-event time of the level-0 matrix-pass kernels (smoother
+       sweeps, residual, PCG SpMV) in the last frame, their launch count and algorithmic bytes */
+    double l0_pass_ms;
+    int64_t l0_pass_launches;
+    double l0_pass_bytes;
+    double ms_setup;                   /* CUDA-event time of the setup in the last frame */
+    double ms_frame;                   /* CUDA-event time of the last frame */
+    int64_t kernel_launches;           /* this library's kernel launches in the last frame */
+} mgpbd_stats;
+
+/* Fill *cfg with the defaults listed above.  Never fails for a non-NULL cfg. */
+MGPBD_API mgpbd_status mgpbd_config_default(mgpbd_config* cfg);
+
+/* Create a context: validates inputs, uploads them, computes rest data (L, or D_m^-1 and V) and the
+ * fixed CSR pattern of A ((i,j) stored iff constraints i, j share a vertex; sorted
+ * off-diagonals, diagonal last) on the device.  inv_mass: n_verts inverse masses, 0 = pinned.
+ * compliance: per-constraint alpha (NOT divided by dt^2; alpha_tilde = alpha/dt^2 per step).
+ * Errors: MGPBD_E_ARG (NULL pointers, vertex ids out of range, repeated vertex in a constraint,
+ * negative mass/compliance, degenerate rest tet, bad config), MGPBD_E_CUDA/OOM. */
+MGPBD_API mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
+                          const double* inv_mass, const double* compliance,
+                          const mgpbd_config* cfg, mgpbd_ctx** out);
+
+/* Mark the hierarchy stale: it is rebuilt at ite 0 of the next mgpbd_step (Alg. 1 l.7). */
+MGPBD_API mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx);
+
+/* One frame of Algorithm 1 with n_iters outer iterations (1..MGPBD_MAX_ITERS) and time step dt > 0.
+ * Setup runs at ite 0 when frame % setup_interval == 0 or the hierarchy is stale.  Synchronises at
+ * the end and checks the device flags (MGPBD_E_INDEFINITE / MGPBD_E_NONFINITE). */
+MGPBD_API mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters);
+
+/* Upload a new state (3*n_verts each; vel may be NULL = unchanged). */
+MGPBD_API mgpbd_status mgpbd_set_state(mgpbd_ctx* ctx, const double* pos, const double* vel);
+
+/* Read back positions / velocities (3*n_verts doubles) and lambda (n_cons doubles, user order). */
+MGPBD_API mgpbd_status mgpbd_get_positions(mgpbd_ctx* ctx, double* out);
+MGPBD_API mgpbd_status mgpbd_get_velocities(mgpbd_ctx* ctx, double* out);
+MGPBD_API mgpbd_status mgpbd_get_lambda(mgpbd_ctx* ctx, double* out);
+MGPBD_API mgpbd_status mgpbd_get_stats(mgpbd_ctx* ctx, mgpbd_stats* out);
+
+/* ---- test hooks (hierarchy as built by the last setup; level l in user numbering) ---- */
+MGPBD_API mgpbd_status mgpbd_get_level_sizes(mgpbd_ctx* ctx, int32_t l, int64_t* n, int64_t* nnz);
+/* CSR of level l (rowptr n+1, cols nnz, vals nnz as fp64): current values of the hot loop. */
+MGPBD_API mgpbd_status mgpbd_get_level(mgpbd_ctx* ctx, int32_t l, int64_t* rowptr, int32_t* cols, double* vals);
+/* Level-l prolongator values P_i (n_l doubles, one per row; column = aggregate of row i). */
+MGPBD_API mgpbd_status mgpbd_get_prolongator(mgpbd_ctx* ctx, int32_t l, double* p_vals);
+/* Level-l aggregate index per node (n_l int32). */
+MGPBD_API mgpbd_status mgpbd_get_aggregates(mgpbd_ctx* ctx, int32_t l, int32_t* out);
+/* Level-0 near-kernel vector B after the GS bootstrap (n_0 doubles). */
+MGPBD_API mgpbd_status mgpbd_get_near_kernel(mgpbd_ctx* ctx, double* out);
+/* Run the setup on caller-given level-0 values (nnz doubles in the pattern's CSR order), then the
+ * Galerkin refresh and coarse inversion on the same values (identical-input-bits tests). */
+MGPBD_API mgpbd_status mgpbd_debug_setup_from(mgpbd_ctx* ctx, const double* A0_values);
+/* Apply one V-cycle / K MGPCG iterations of the current hierarchy to host b (n_0) -> host x. */
+MGPBD_API mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x);
+MGPBD_API mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x);
+
+MGPBD_API const char* mgpbd_last_error(const mgpbd_ctx* ctx);
+MGPBD_API void mgpbd_destroy(mgpbd_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MGPBD_H */

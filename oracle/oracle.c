@@ -287,42 +287,52 @@ int64_t orc_pattern(int32_t m, int kind, const int32_t* verts, int32_t n_verts, 
 /* A = grad C M^-1 grad C^T + alpha_tilde (Eq. 3):
  * A_ii = sum_k w_{v_k} |g_{i,k}|^2 + alpha_tilde_i;
  * A_ij = sum over ALL shared vertices v (ascending id) of w_v g_{i,v} . g_{j,v} (reading c14). */
+static void assemble_row(int32_t i, int kind, const int32_t* verts, const double* w, const double* g,
+                         const double* alpha_tilde, const int64_t* rowptr, const int32_t* col, double* val) {
+    const int32_t* vi = verts + (int64_t)i * kind;
+    const double* gi = g + (int64_t)i * kind * 3;
+    for (int64_t e = rowptr[i]; e < rowptr[i + 1] - 1; ++e) {
+        int32_t j = col[e];
+        const int32_t* vj = verts + (int64_t)j * kind;
+        const double* gj = g + (int64_t)j * kind * 3;
+        /* shared vertices in ascending vertex id */
+        int32_t sv[4]; int ki[4], kj[4], ns = 0;
+        for (int a = 0; a < kind; ++a)
+            for (int b = 0; b < kind; ++b)
+                if (vi[a] == vj[b]) { sv[ns] = vi[a]; ki[ns] = a; kj[ns] = b; ++ns; }
+        for (int a = 0; a < ns; ++a)
+            for (int b = a + 1; b < ns; ++b)
+                if (sv[b] < sv[a]) {
+                    int32_t t = sv[a]; sv[a] = sv[b]; sv[b] = t;
+                    int u = ki[a]; ki[a] = ki[b]; ki[b] = u;
+                    u = kj[a]; kj[a] = kj[b]; kj[b] = u;
+                }
+        double s = 0.0;
+        for (int a = 0; a < ns; ++a) {
+            const double* x1 = gi + 3 * ki[a];
+            const double* x2 = gj + 3 * kj[a];
+            s += w[sv[a]] * (x1[0] * x2[0] + x1[1] * x2[1] + x1[2] * x2[2]);
+        }
+        val[e] = s;
+    }
+    double d = 0.0;
+    for (int k = 0; k < kind; ++k) {
+        const double* x1 = gi + 3 * k;
+        d += w[vi[k]] * (x1[0] * x1[0] + x1[1] * x1[1] + x1[2] * x1[2]);
+    }
+    val[rowptr[i + 1] - 1] = d + alpha_tilde[i];
+}
+
 void orc_assemble(int32_t m, int kind, const int32_t* verts, const double* w, const double* g,
                   const double* alpha_tilde, const int64_t* rowptr, const int32_t* col, double* val) {
-    for (int32_t i = 0; i < m; ++i) {
-        const int32_t* vi = verts + (int64_t)i * kind;
-        const double* gi = g + (int64_t)i * kind * 3;
-        for (int64_t e = rowptr[i]; e < rowptr[i + 1] - 1; ++e) {
-            int32_t j = col[e];
-            const int32_t* vj = verts + (int64_t)j * kind;
-            const double* gj = g + (int64_t)j * kind * 3;
-            /* shared vertices in ascending vertex id */
-            int32_t sv[4]; int ki[4], kj[4], ns = 0;
-            for (int a = 0; a < kind; ++a)
-                for (int b = 0; b < kind; ++b)
-                    if (vi[a] == vj[b]) { sv[ns] = vi[a]; ki[ns] = a; kj[ns] = b; ++ns; }
-            for (int a = 0; a < ns; ++a)
-                for (int b = a + 1; b < ns; ++b)
-                    if (sv[b] < sv[a]) {
-                        int32_t t = sv[a]; sv[a] = sv[b]; sv[b] = t;
-                        int u = ki[a]; ki[a] = ki[b]; ki[b] = u;
-                        u = kj[a]; kj[a] = kj[b]; kj[b] = u;
-                    }
-            double s = 0.0;
-            for (int a = 0; a < ns; ++a) {
-                const double* x1 = gi + 3 * ki[a];
-                const double* x2 = gj + 3 * kj[a];
-                s += w[sv[a]] * (x1[0] * x2[0] + x1[1] * x2[1] + x1[2] * x2[2]);
-            }
-            val[e] = s;
-        }
-        double d = 0.0;
-        for (int k = 0; k < kind; ++k) {
-            const double* x1 = gi + 3 * k;
-            d += w[vi[k]] * (x1[0] * x1[0] + x1[1] * x1[1] + x1[2] * x1[2]);
-        }
-        val[rowptr[i + 1] - 1] = d + alpha_tilde[i];
-    }
+    for (int32_t i = 0; i < m; ++i) assemble_row(i, kind, verts, w, g, alpha_tilde, rowptr, col, val);
+}
+
+/* The same definition restricted to the listed rows (sampled full-size parity checks). */
+void orc_assemble_rows(int32_t nrows, const int32_t* rows, int kind, const int32_t* verts, const double* w,
+                       const double* g, const double* alpha_tilde, const int64_t* rowptr, const int32_t* col,
+                       double* val) {
+    for (int32_t t = 0; t < nrows; ++t) assemble_row(rows[t], kind, verts, w, g, alpha_tilde, rowptr, col, val);
 }
 
 /* b = -C - alpha_tilde lambda (Eq. 3; Alg. 1 l.6). */

@@ -55,6 +55,9 @@ int64_t orc_pattern(int32_t m, int kind, const int32_t* verts, int32_t n_verts,
                     int64_t* rowptr /* m+1 or NULL */, int32_t* col /* nnz or NULL */);
 void orc_assemble(int32_t m, int kind, const int32_t* verts, const double* w, const double* g,
                   const double* alpha_tilde, const int64_t* rowptr, const int32_t* col, double* val);
+void orc_assemble_rows(int32_t nrows, const int32_t* rows, int kind, const int32_t* verts, const double* w,
+                       const double* g, const double* alpha_tilde, const int64_t* rowptr, const int32_t* col,
+                       double* val);
 void orc_rhs(int32_t m, const double* C, const double* alpha_tilde, const double* lambda, double* b);
 void orc_apply_dx(int32_t m, int kind, const int32_t* verts, int32_t n_verts, const double* w,
                   const double* g, const double* dlambda, double* dx /* 3*n_verts */);

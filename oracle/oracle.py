@@ -52,6 +52,7 @@ def lib():
             "orc_eval_arap": (None, [i32, P, P, P, P, P]),
             "orc_pattern": (i64, [i32, C.c_int, P, i32, P, P]),
             "orc_assemble": (None, [i32, C.c_int, P, P, P, P, P, P, P]),
+            "orc_assemble_rows": (None, [i32, P, C.c_int, P, P, P, P, P, P, P]),
             "orc_rhs": (None, [i32, P, P, P, P]),
             "orc_apply_dx": (None, [i32, C.c_int, P, i32, P, P, P, P]),
             "orc_spmv": (None, [i32, P, P, P, P, P]),
@@ -183,6 +184,18 @@ def assemble(verts, w, g, alpha_tilde, rowptr, col):
     rowptr, col = _c(rowptr, np.int64), _c(col, np.int32)
     val = np.empty(col.shape[0])
     lib().orc_assemble(m, kind, _p(verts), _p(w), _p(g), _p(at), _p(rowptr), _p(col), _p(val))
+    return val
+
+
+def assemble_rows(rows, verts, w, g, alpha_tilde, rowptr, col):
+    """Rows `rows` of A (values at those rows' CSR positions of a full-size array; others NaN)."""
+    verts = _c(verts, np.int32)
+    m, kind = verts.shape
+    rows = _c(rows, np.int32)
+    w, g, at = _c(w, np.float64), _c(g, np.float64), _c(alpha_tilde, np.float64)
+    rowptr, col = _c(rowptr, np.int64), _c(col, np.int32)
+    val = np.full(col.shape[0], np.nan)
+    lib().orc_assemble_rows(rows.shape[0], _p(rows), kind, _p(verts), _p(w), _p(g), _p(at), _p(rowptr), _p(col), _p(val))
     return val
 
 

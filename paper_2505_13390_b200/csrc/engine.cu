@@ -1,0 +1,715 @@
+// Host orchestration of one MGPBD frame (Algorithm 1) and the extern "C" ABI of mgpbd.h.
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/mgpbd.h"
+#include "common.cuh"
+#include "mesh.cuh"
+#include "setup.cuh"
+#include "solve.cuh"
+#include "util.cuh"
+
+namespace mgpbd {
+
+static int choose_vl(int64_t n, int64_t nnz) {
+    double avg = n ? (double)nnz / (double)n : 1.0;
+    int vl = 2;
+    while (vl < 32 && vl * 1.5 < avg) vl *= 2;
+    return vl < 4 ? 4 : vl;
+}
+
+struct EngineBase {
+    virtual ~EngineBase() = default;
+    virtual void step(double dt, int32_t n_iters) = 0;
+    virtual void set_state(const double* pos, const double* vel) = 0;
+    virtual void get_positions(double* out) = 0;
+    virtual void get_velocities(double* out) = 0;
+    virtual void get_lambda(double* out) = 0;
+    virtual void get_stats(mgpbd_stats* st) = 0;
+    virtual void level_sizes(int l, int64_t* n, int64_t* nnz) = 0;
+    virtual void get_level(int l, int64_t* rowptr, int32_t* col, double* val) = 0;
+    virtual void get_prolongator(int l, double* p) = 0;
+    virtual void get_aggregates(int l, int32_t* a) = 0;
+    virtual void get_near_kernel(double* b) = 0;
+    virtual void debug_setup_from(const double* vals) = 0;
+    virtual void debug_vcycle(const double* b, double* x) = 0;
+    virtual void debug_pcg(const double* b, int32_t iters, double* x) = 0;
+    bool stale = true;
+};
+
+template <class T>
+class Engine : public EngineBase {
+   public:
+    struct Level {
+        int32_t n = 0;
+        int64_t nnz = 0;
+        DBuf<int64_t> rowptr_own;
+        DBuf<int32_t> col_own;
+        const int64_t* rowptr = nullptr;
+        const int32_t* col = nullptr;
+        DBuf<T> val, dinv;            // hot values
+        DBuf<double> val64, dinv64;   // setup values
+        // towards level+1
+        DBuf<int32_t> agg;
+        int32_t n_agg = 0;
+        DBuf<double> P64;
+        DBuf<T> P;
+        DBuf<int64_t> mptr;
+        DBuf<int32_t> mlist;
+        GalerkinPlan plan;
+        DBuf<T> tval;
+        DBuf<double> tval64;
+        double omega = 0.0;
+        // V-cycle vectors
+        DBuf<T> vb, vz, vx, vy, vt;
+        int vl = 32, grid = 1;
+        Csr<T> hot() const {
+            Csr<T> c;
+            c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = val.p; c.dinv = dinv.p; c.vl = vl; c.grid = grid;
+            return c;
+        }
+        Csr<double> setup_csr() const {
+            Csr<double> c;
+            c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = val64.p; c.dinv = dinv64.p; c.vl = vl; c.grid = grid;
+            return c;
+        }
+    };
+
+    mgpbd_config cfg;
+    cudaStream_t st = nullptr;
+    bool own_stream = false;
+    int kind = 2, kc = 2;
+    int32_t nv = 0, m = 0;
+    DBuf<int32_t> verts;
+    DBuf<double> x, v, x_old, w, sqrtw, alpha, rest, vol, lambda;
+    DBuf<int64_t> vptr, rowptr0;
+    DBuf<int32_t> vlist, col0;
+    int64_t nnz0 = 0;
+    DBuf<T> h, b0;
+    DBuf<double> h64, b64;
+    std::vector<std::unique_ptr<Level>> L;
+    int nL = 0;
+    bool have_hier = false;
+    DBuf<double> Ainv, inv_work;
+    DBuf<T> r, p, q, xs;
+    DBuf<double> scal, parts1, parts2, bn, B0, pw_v, pw_w, pw_ss;
+    DBuf<int> flags;
+    int32_t ncolours = 0;
+    int64_t frame = 0;
+    int setup_ran = 0;
+    int n_b = 0;
+    double ms_setup = 0, ms_frame = 0;
+    // profiling of the level-0 matrix passes
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    double l0_ms = 0, l0_bytes = 0;
+    int64_t l0_launches = 0;
+    double l0_bytes_acc = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pairs;
+    int64_t launches_last = 0;
+
+    Engine(const mgpbd_mesh* mesh, const mgpbd_constraints* cons, const double* inv_mass, const double* comp,
+           const mgpbd_config* c) {
+        cfg = *c;
+        MG_CK(cudaSetDevice(cfg.device));
+        if (cfg.stream) st = (cudaStream_t)cfg.stream;
+        else { MG_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); own_stream = true; }
+        kind = cons->kind; kc = (int)kind;
+        nv = mesh->n_verts; m = cons->n_cons;
+        verts.resize((size_t)m * kc);
+        h2d(verts.p, cons->verts, (size_t)m * kc, st);
+        size_t n3 = 3 * (size_t)nv;
+        x.resize(n3); v.resize(n3); x_old.resize(n3); w.resize(nv); sqrtw.resize(nv);
+        DBuf<double> X;
+        X.resize(n3);
+        h2d(X.p, mesh->rest_pos, n3, st);
+        h2d(x.p, mesh->pos ? mesh->pos : mesh->rest_pos, n3, st);
+        if (mesh->vel) h2d(v.p, mesh->vel, n3, st);
+        else MG_CK(cudaMemsetAsync(v.p, 0, n3 * sizeof(double), st));
+        h2d(w.p, inv_mass, nv, st);
+        sqrt_vec(nv, w.p, sqrtw.p, st);
+        alpha.resize(m);
+        h2d(alpha.p, comp, m, st);
+        lambda.resize(m);
+        MG_CK(cudaMemsetAsync(lambda.p, 0, sizeof(double) * (m ? m : 1), st));
+        if (kind == 2) {
+            rest.resize(m);
+            rest_distance(verts.p, X.p, m, rest.p, st);
+        } else {
+            rest.resize(9 * (size_t)m); vol.resize(m);
+            DBuf<int32_t> bad;
+            bad.resize(1);
+            MG_CK(cudaMemsetAsync(bad.p, 0, sizeof(int32_t), st));
+            rest_arap(verts.p, X.p, m, rest.p, vol.p, bad.p, st);
+            if (read_scalar(bad.p, st)) throw Error(MGPBD_E_ARG, "degenerate rest tetrahedron");
+        }
+        build_incidence(verts.p, m, kc, nv, vptr, vlist, st);
+        build_pattern(verts.p, m, kc, nv, vptr.p, vlist.p, rowptr0, col0, st);
+        nnz0 = read_scalar(rowptr0.p + m, st);
+        h.resize((size_t)m * kc * 3); b0.resize(m);
+        r.resize(m); p.resize(m); q.resize(m); xs.resize(m);
+        scal.resize(2 * 4096); flags.resize(8); bn.resize(MGPBD_MAX_ITERS);
+        parts1.resize(148 * 8); parts2.resize(148 * 8);
+        pw_ss.resize(4);
+        MG_CK(cudaMemsetAsync(flags.p, 0, 8 * sizeof(int), st));
+        // level 0 skeleton (pattern fixed for the context's lifetime)
+        L.clear();
+        L.emplace_back(new Level());
+        Level& l0 = *L[0];
+        l0.n = m; l0.nnz = nnz0; l0.rowptr = rowptr0.p; l0.col = col0.p;
+        l0.val.resize(nnz0); l0.dinv.resize(m);
+        l0.vl = choose_vl(m, nnz0); l0.grid = pass_grid(m, l0.vl);
+        alloc_vectors(l0);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+
+    ~Engine() override {
+        for (auto e : ev_pool) cudaEventDestroy(e);
+        if (own_stream && st) cudaStreamDestroy(st);
+    }
+
+    void alloc_vectors(Level& lv) {
+        lv.vb.resize(lv.n); lv.vz.resize(lv.n); lv.vx.resize(lv.n); lv.vy.resize(lv.n); lv.vt.resize(lv.n);
+    }
+
+    cudaEvent_t ev() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            MG_CK(cudaEventCreate(&e));
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+
+    // Algorithmic bytes of one level-0 CSR pass (matrix stream + per-row vectors), see DESIGN.md.
+    double pass_bytes(int mode) const {
+        const double s = sizeof(T);
+        double mat = (double)nnz0 * (s + 4) + 8.0 * (m + 1);
+        double vec;
+        switch (mode) {
+            case PASS_JACOBI: vec = 4 * s; break;          // x (gathered once), b, dinv, y
+            case PASS_JACOBI_DOT: vec = 5 * s; break;      // + r
+            case PASS_RESID_P: vec = 4 * s; break;         // x, b, P, t
+            case PASS_SPMV_DOT: vec = 2 * s; break;        // x, y
+            default: vec = 3 * s; break;
+        }
+        return mat + vec * (double)m;
+    }
+
+    void l0_pass(int mode, const T* xin, const T* b, T* y, const T* aux, double omega) {
+        const Level& l0 = *L[0];
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (cfg.profile) { e0 = ev(); MG_CK(cudaEventRecord(e0, st)); }
+        csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
+        if (cfg.profile) {
+            e1 = ev();
+            MG_CK(cudaEventRecord(e1, st));
+            prof_pairs.emplace_back(e0, e1);
+            l0_launches++;
+            l0_bytes_acc += pass_bytes(mode);
+        }
+    }
+
+    void pass(int l, int mode, const T* xin, const T* b, T* y, const T* aux, double omega) {
+        if (l == 0) l0_pass(mode, xin, b, y, aux, omega);
+        else csr_pass<T>(mode, L[l]->hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
+    }
+
+    // ------------------------------------------------------------------ setup (Fig. setup-pipline)
+    void setup() {
+        Level& l0 = *L[0];
+        L.resize(1);
+        nL = 1;
+        B0.resize(m);
+        DBuf<double> B, Bn;
+        const int maxl = std::min<int>(cfg.max_levels, MGPBD_MAX_LEVELS);
+        pw_v.resize(m); pw_w.resize(m);
+        for (int l = 0; l + 1 < maxl; ++l) {
+            Level& a = *L[l];
+            if (a.n < cfg.min_coarse) break;
+            DBuf<uint8_t> strong;
+            strong.resize(a.nnz);
+            soc(a.n, a.rowptr, a.col, a.val64.p, cfg.theta, strong.p, st);
+            a.agg.resize(a.n);
+            int32_t na = aggregate(a.n, a.rowptr, a.col, a.val64.p, strong.p, cfg.seed, l, a.agg.p, st);
+            if ((double)na > cfg.stall_ratio * (double)a.n) break;
+            if (l == 0) {
+                DBuf<int32_t> col_;
+                col_.resize(a.n);
+                ncolours = colour(a.n, a.rowptr, a.col, cfg.seed, col_.p, st);
+                B.resize(a.n);
+                gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed, B.p, st);
+                d2d(B0.p, B.p, a.n, st);
+            }
+            a.n_agg = na;
+            DBuf<int32_t> cnt;
+            group_by_key(a.agg.p, a.n, na, a.mptr, a.mlist, cnt, st, true);
+            a.P64.resize(a.n);
+            Bn.resize(na);
+            prolongator(na, a.mptr.p, a.mlist.p, B.p, a.P64.p, Bn.p, st);
+            L.emplace_back(new Level());
+            Level& c = *L[l + 1];
+            Level& a2 = *L[l];  // re-bind after emplace (unique_ptr: stable)
+            galerkin_symbolic(a2.n, a2.rowptr, a2.col, a2.agg.p, a2.mptr.p, a2.mlist.p, na, a2.plan, c.rowptr_own,
+                              c.col_own, st);
+            c.n = na;
+            c.nnz = read_scalar(c.rowptr_own.p + na, st);
+            c.rowptr = c.rowptr_own.p; c.col = c.col_own.p;
+            c.vl = choose_vl(c.n, c.nnz); c.grid = pass_grid(c.n, c.vl);
+            c.val64.resize(c.nnz); c.dinv64.resize(c.n);
+            a2.tval64.resize(a2.plan.T);
+            galerkin_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, a2.P64.p, na, c.rowptr, c.nnz,
+                                     a2.tval64.p, c.val64.p, c.dinv64.p, st);
+            double lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
+            a2.omega = 2.0 / (lam + cfg.lambda_min_est);
+            B.swap(Bn);
+            nL = l + 2;
+        }
+        Level& cl = *L[nL - 1];
+        if (cl.n > cfg.max_dense_coarse)
+            throw Error(MGPBD_E_STALL, "coarsening stalled: coarsest level has " + std::to_string(cl.n) +
+                                           " rows (> max_dense_coarse)");
+        // hot buffers
+        for (int l = 0; l < nL; ++l) {
+            Level& a = *L[l];
+            if (l > 0) { a.val.resize(a.nnz); a.dinv.resize(a.n); alloc_vectors(a); }
+            if (l + 1 < nL) {
+                a.P.resize(a.n);
+                convert<double, T>(a.P64.p, a.P.p, a.n, st);
+                a.tval.resize(a.plan.T);
+            }
+        }
+        Ainv.resize((size_t)cl.n * cl.n);
+        inv_work.resize((size_t)cl.n * cl.n);
+        have_hier = true;
+        stale = false;
+        (void)l0;
+        MG_CK(cudaStreamSynchronize(st));
+    }
+
+    // Galerkin values of all coarse levels from the current level-0 values + coarsest inverse.
+    void refresh() {
+        for (int l = 0; l + 1 < nL; ++l) {
+            Level& a = *L[l];
+            Level& c = *L[l + 1];
+            galerkin_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.P.p, a.n_agg, c.rowptr, c.nnz, a.tval.p, c.val.p,
+                                c.dinv.p, st);
+        }
+        coarse_invert<T>(L[nL - 1]->hot(), inv_work.p, Ainv.p, flags.p, st);
+    }
+
+    // ------------------------------------------------------------------ V-cycle
+    // x_out = V(b) at level l, x = 0 start; at l = 0 with dot_r != nullptr the last post sweep also
+    // produces the partials of r.z and r.r.
+    void vcycle(int l, const T* b, T* x_out, const T* dot_r) {
+        Level& a = *L[l];
+        if (l == nL - 1) {
+            coarse_gemv<T>(a.n, Ainv.p, b, x_out, st);
+            return;
+        }
+        const int nu = cfg.smoother_sweeps;
+        T* cur = a.vx.p;
+        T* nxt = a.vy.p;
+        vec_jacobi0<T>(a.n, a.dinv.p, b, a.omega, cur, st);
+        for (int sw = 1; sw < nu; ++sw) {
+            pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.omega);
+            std::swap(cur, nxt);
+        }
+        pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
+        Level& c = *L[l + 1];
+        restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
+        vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+        prolong_add<T>(a.n, a.agg.p, a.P.p, c.vz.p, cur, st);
+        for (int sw = 0; sw < nu; ++sw) {
+            const bool last = sw == nu - 1;
+            T* dst = last ? x_out : (cur == a.vx.p ? a.vy.p : a.vx.p);
+            if (last && dot_r) pass(l, PASS_JACOBI_DOT, cur, b, dst, dot_r, a.omega);
+            else pass(l, PASS_JACOBI, cur, b, dst, nullptr, a.omega);
+            cur = dst;
+        }
+    }
+
+    // ------------------------------------------------------------------ MGPCG
+    void pcg(int32_t iters, int ite) {
+        Level& l0 = *L[0];
+        MG_CK(cudaMemsetAsync(xs.p, 0, sizeof(T) * m, st));
+        d2d(r.p, b0.p, m, st);
+        MG_CK(cudaMemsetAsync(p.p, 0, sizeof(T) * m, st));
+        T* z = l0.vz.p;
+        for (int k = 0; k < iters; ++k) {
+            const int tag = ite * 4096 + k;
+            if (nL == 1) {
+                vcycle(0, r.p, z, nullptr);
+                dot_parts<T>(m, r.p, z, parts1.p, l0.grid, st);
+                dot_parts<T>(m, r.p, r.p, parts2.p, l0.grid, st);
+            } else {
+                vcycle(0, r.p, z, r.p);
+            }
+            pcg_finalize_rz(parts1.p, parts2.p, l0.grid, scal.p, k, flags.p, tag, st);
+            pcg_update_p<T>(m, z, p.p, scal.p, k, st);
+            l0_pass(PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
+            pcg_finalize_pq(parts1.p, l0.grid, scal.p, k, flags.p, tag, st);
+            pcg_update_xr<T>(m, p.p, q.p, xs.p, r.p, scal.p, k, st);
+        }
+    }
+
+    void assemble_hot(double dt) {
+        Level& l0 = *L[0];
+        eval_constraints<T>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h.p, b0.p, st);
+        assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st);
+    }
+
+    void assemble_setup(double dt) {
+        Level& l0 = *L[0];
+        l0.val64.resize(nnz0);
+        l0.dinv64.resize(m);
+        if (std::is_same<T, double>::value) {
+            d2d(l0.val64.p, (const double*)l0.val.p, nnz0, st);
+            d2d(l0.dinv64.p, (const double*)l0.dinv.p, m, st);
+        } else {
+            h64.resize((size_t)m * kc * 3); b64.resize(m);
+            eval_constraints<double>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h64.p, b64.p, st);
+            assemble<double>(kind, m, verts.p, h64.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val64.p, l0.dinv64.p, st);
+        }
+    }
+
+    // ------------------------------------------------------------------ Algorithm 1
+    void step(double dt, int32_t n_iters) override {
+        ev_used = 0;
+        l0_launches = 0;
+        l0_bytes_acc = 0;
+        setup_ran = 0;
+        prof_pairs.clear();
+        g_kernel_launches = 0;
+        cudaEvent_t f0 = ev(), f1, s0 = nullptr, s1 = nullptr;
+        MG_CK(cudaEventRecord(f0, st));
+        MG_CK(cudaMemsetAsync(flags.p, 0, 8 * sizeof(int), st));
+        predict(nv, x.p, v.p, x_old.p, w.p, dt, cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], st);  // l.1
+        MG_CK(cudaMemsetAsync(lambda.p, 0, sizeof(double) * m, st));                                // l.2
+        for (int ite = 0; ite < n_iters; ++ite) {                                                    // l.3
+            assemble_hot(dt);                                                                        // l.4-6
+            dot_parts<T>(m, b0.p, b0.p, parts2.p, L[0]->grid, st);
+            finalize_sum(parts2.p, L[0]->grid, bn.p + ite, st);
+            if (ite == 0 && (stale || !have_hier || frame % cfg.setup_interval == 0)) {            // l.7
+                s0 = ev();
+                MG_CK(cudaEventRecord(s0, st));
+                assemble_setup(dt);
+                setup();
+                s1 = ev();
+                MG_CK(cudaEventRecord(s1, st));
+                setup_ran = 1;
+            }
+            refresh();                                                                               // Eq. 6
+            pcg(cfg.pcg_iters, ite);                                                                 // l.8
+            update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, cfg.omega_relax, x.p, st);  // l.9, l.11
+            lambda_add<T>(m, lambda.p, xs.p, st);                                                    // l.10
+        }
+        velocity(nv, x.p, x_old.p, v.p, dt, st);                                                     // l.17
+        f1 = ev();
+        MG_CK(cudaEventRecord(f1, st));
+        MG_CK(cudaStreamSynchronize(st));
+        launches_last = g_kernel_launches;
+        frame++;
+        n_b = n_iters;
+        float ms = 0;
+        MG_CK(cudaEventElapsedTime(&ms, f0, f1));
+        ms_frame = ms;
+        ms_setup = 0;
+        if (s0) { MG_CK(cudaEventElapsedTime(&ms, s0, s1)); ms_setup = ms; }
+        if (cfg.profile) {
+            double tot = 0;
+            for (auto& pr : prof_pairs) {
+                MG_CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+                tot += ms;
+            }
+            l0_ms = tot;
+            l0_bytes = l0_bytes_acc;
+        }
+        int hf[4];
+        d2h(hf, flags.p, 4, st);
+        MG_CK(cudaStreamSynchronize(st));
+        if (hf[1]) throw Error(MGPBD_E_NONFINITE, "non-finite PCG scalar at (frame " + std::to_string(frame - 1) +
+                                                      ", ite " + std::to_string(hf[3] / 4096) + ", pcg " +
+                                                      std::to_string(hf[3] % 4096) + ")");
+        if (hf[0]) throw Error(MGPBD_E_INDEFINITE, "indefinite preconditioner or non-SPD coarsest at (frame " +
+                                                       std::to_string(frame - 1) + ", tag " + std::to_string(hf[2]) + ")");
+    }
+
+    void set_state(const double* pos, const double* vel) override {
+        if (pos) h2d(x.p, pos, 3 * (size_t)nv, st);
+        if (vel) h2d(v.p, vel, 3 * (size_t)nv, st);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void get_positions(double* out) override { d2h(out, x.p, 3 * (size_t)nv, st); MG_CK(cudaStreamSynchronize(st)); }
+    void get_velocities(double* out) override { d2h(out, v.p, 3 * (size_t)nv, st); MG_CK(cudaStreamSynchronize(st)); }
+    void get_lambda(double* out) override { d2h(out, lambda.p, m, st); MG_CK(cudaStreamSynchronize(st)); }
+
+    void get_stats(mgpbd_stats* s) override {
+        std::memset(s, 0, sizeof(*s));
+        s->n_levels = have_hier ? nL : 0;
+        double tot = 0;
+        for (int l = 0; l < s->n_levels; ++l) {
+            s->n[l] = L[l]->n; s->nnz[l] = L[l]->nnz; tot += (double)L[l]->nnz;
+            s->omega[l] = L[l]->omega;
+        }
+        s->op_complexity = s->n_levels ? tot / (double)nnz0 : 0.0;
+        s->n_colours = ncolours;
+        s->setup_ran = setup_ran;
+        s->n_b = n_b;
+        if (n_b) d2h(s->b_norm, bn.p, n_b, st);
+        MG_CK(cudaStreamSynchronize(st));
+        for (int i = 0; i < n_b; ++i) s->b_norm[i] = std::sqrt(s->b_norm[i]);
+        s->frame = frame;
+        s->l0_pass_ms = l0_ms;
+        s->l0_pass_launches = cfg.profile ? l0_launches : 0;
+        s->l0_pass_bytes = l0_bytes;
+        s->ms_setup = ms_setup;
+        s->ms_frame = ms_frame;
+        s->kernel_launches = launches_last;
+    }
+
+    void check_level(int l) {
+        if (l == 0) return;  // the level-0 pattern exists from mgpbd_create on
+        if (!have_hier || l < 0 || l >= nL) throw Error(MGPBD_E_ARG, "level out of range (or no hierarchy yet)");
+    }
+    void level_sizes(int l, int64_t* n, int64_t* nnz) override {
+        check_level(l);
+        *n = L[l]->n; *nnz = L[l]->nnz;
+    }
+
+    void get_level(int l, int64_t* rp, int32_t* cl, double* vals) override {
+        check_level(l);
+        Level& a = *L[l];
+        if (rp) d2h(rp, a.rowptr, (size_t)a.n + 1, st);
+        if (cl) d2h(cl, a.col, a.nnz, st);
+        if (vals) {
+            std::vector<T> tmp(a.nnz);
+            d2h(tmp.data(), a.val.p, a.nnz, st);
+            MG_CK(cudaStreamSynchronize(st));
+            for (int64_t k = 0; k < a.nnz; ++k) vals[k] = (double)tmp[k];
+        }
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void get_prolongator(int l, double* pv) override {
+        check_level(l);
+        if (!have_hier || l >= nL - 1) throw Error(MGPBD_E_ARG, "coarsest level has no prolongator");
+        d2h(pv, L[l]->P64.p, L[l]->n, st);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void get_aggregates(int l, int32_t* ag) override {
+        check_level(l);
+        if (!have_hier || l >= nL - 1) throw Error(MGPBD_E_ARG, "coarsest level has no aggregates");
+        d2h(ag, L[l]->agg.p, L[l]->n, st);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void get_near_kernel(double* bout) override {
+        if (!have_hier || nL < 2) throw Error(MGPBD_E_ARG, "no bootstrapped near kernel (single-level hierarchy)");
+        d2h(bout, B0.p, m, st);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void debug_setup_from(const double* vals) override {
+        Level& l0 = *L[0];
+        l0.val64.resize(nnz0); l0.dinv64.resize(m);
+        h2d(l0.val64.p, vals, nnz0, st);
+        diag_inv<double>(m, rowptr0.p, l0.val64.p, l0.dinv64.p, st);
+        convert<double, T>(l0.val64.p, l0.val.p, nnz0, st);
+        diag_inv<T>(m, rowptr0.p, l0.val.p, l0.dinv.p, st);
+        setup();
+        refresh();
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void debug_vcycle(const double* b, double* xo) override {
+        if (!have_hier) throw Error(MGPBD_E_ARG, "no hierarchy");
+        DBuf<double> tmp;
+        tmp.resize(m);
+        h2d(tmp.p, b, m, st);
+        convert<double, T>(tmp.p, r.p, m, st);
+        vcycle(0, r.p, L[0]->vz.p, nullptr);
+        convert<T, double>(L[0]->vz.p, tmp.p, m, st);
+        d2h(xo, tmp.p, m, st);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+    void debug_pcg(const double* b, int32_t iters, double* xo) override {
+        if (!have_hier) throw Error(MGPBD_E_ARG, "no hierarchy");
+        DBuf<double> tmp;
+        tmp.resize(m);
+        h2d(tmp.p, b, m, st);
+        convert<double, T>(tmp.p, b0.p, m, st);
+        MG_CK(cudaMemsetAsync(flags.p, 0, 8 * sizeof(int), st));
+        pcg(iters, 0);
+        convert<T, double>(xs.p, tmp.p, m, st);
+        d2h(xo, tmp.p, m, st);
+        MG_CK(cudaStreamSynchronize(st));
+    }
+};
+
+}  // namespace mgpbd
+
+// ============================================================================ C ABI
+struct mgpbd_ctx {
+    std::unique_ptr<mgpbd::EngineBase> eng;
+    std::string err;
+};
+
+using mgpbd::Error;
+
+template <class F>
+static mgpbd_status guarded(mgpbd_ctx* ctx, F&& f) {
+    if (!ctx) return MGPBD_E_ARG;
+    try {
+        f();
+        return MGPBD_OK;
+    } catch (const Error& e) {
+        ctx->err = e.what();
+        return (mgpbd_status)e.status;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return MGPBD_E_CUDA;
+    }
+}
+
+extern "C" {
+
+mgpbd_status mgpbd_config_default(mgpbd_config* c) {
+    if (!c) return MGPBD_E_ARG;
+    std::memset(c, 0, sizeof(*c));
+    c->precision = 0;
+    c->theta = 0.1;
+    c->k_nullspace = 1;
+    c->min_coarse = 400;
+    c->max_levels = 16;
+    c->stall_ratio = 0.9;
+    c->setup_interval = 20;
+    c->bootstrap_sweeps = 20;
+    c->power_iters = 100;
+    c->lambda_min_est = 0.1;
+    c->smoother_sweeps = 2;
+    c->pcg_iters = 10;
+    c->omega_relax = 0.1;
+    c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0;
+    c->seed = 1;
+    c->device = 0;
+    c->stream = nullptr;
+    c->max_dense_coarse = 2048;
+    c->rank = 0; c->world = 1;
+    c->profile = 0;
+    return MGPBD_OK;
+}
+
+static std::string g_create_err;
+
+mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons, const double* inv_mass,
+                          const double* compliance, const mgpbd_config* cfg, mgpbd_ctx** out) {
+    if (!out) return MGPBD_E_ARG;
+    *out = nullptr;
+    auto fail = [&](const std::string& m) { g_create_err = m; return MGPBD_E_ARG; };
+    if (!mesh || !cons || !inv_mass || !compliance || !cfg) return fail("NULL argument");
+    if (!mesh->rest_pos || mesh->n_verts <= 0) return fail("bad mesh");
+    if (cons->kind != MGPBD_DISTANCE && cons->kind != MGPBD_TET_ARAP) return fail("bad constraint kind");
+    if (cons->n_cons <= 0 || !cons->verts) return fail("bad constraint set");
+    if ((int64_t)cons->n_cons * cons->kind >= ((int64_t)1 << 31)) return fail("too many constraints");
+    if (cfg->precision != 0 && cfg->precision != 1) return fail("precision must be 0 (fp64) or 1 (fp32)");
+    if (cfg->k_nullspace != 1) return fail("only k_nullspace = 1 is implemented (reading c1)");
+    if (cfg->world != 1) return fail("world > 1 is not supported by this build");
+    if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > 4096 || cfg->setup_interval < 1 ||
+        cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
+        cfg->max_dense_coarse < 1)
+        return fail("bad config");
+    const int kc = cons->kind;
+    for (int64_t j = 0; j < cons->n_cons; ++j) {
+        for (int a = 0; a < kc; ++a) {
+            int32_t va = cons->verts[j * kc + a];
+            if (va < 0 || va >= mesh->n_verts) return fail("vertex id out of range in constraint " + std::to_string(j));
+            for (int b = a + 1; b < kc; ++b)
+                if (cons->verts[j * kc + b] == va) return fail("repeated vertex in constraint " + std::to_string(j));
+        }
+        if (!(compliance[j] >= 0.0)) return fail("negative compliance");
+    }
+    for (int32_t i = 0; i < mesh->n_verts; ++i)
+        if (!(inv_mass[i] >= 0.0)) return fail("negative inverse mass");
+    auto* ctx = new mgpbd_ctx();
+    try {
+        if (cfg->precision == 1) ctx->eng.reset(new mgpbd::Engine<float>(mesh, cons, inv_mass, compliance, cfg));
+        else ctx->eng.reset(new mgpbd::Engine<double>(mesh, cons, inv_mass, compliance, cfg));
+    } catch (const Error& e) {
+        g_create_err = e.what();
+        delete ctx;
+        return (mgpbd_status)e.status;
+    } catch (const std::exception& e) {
+        g_create_err = e.what();
+        delete ctx;
+        return MGPBD_E_CUDA;
+    }
+    *out = ctx;
+    return MGPBD_OK;
+}
+
+mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx) {
+    return guarded(ctx, [&] { ctx->eng->stale = true; });
+}
+
+mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters) {
+    if (ctx && (!(dt > 0.0) || n_iters < 1 || n_iters > MGPBD_MAX_ITERS)) {
+        ctx->err = "dt must be > 0 and 1 <= n_iters <= MGPBD_MAX_ITERS";
+        return MGPBD_E_ARG;
+    }
+    return guarded(ctx, [&] { ctx->eng->step(dt, n_iters); });
+}
+
+mgpbd_status mgpbd_set_state(mgpbd_ctx* ctx, const double* pos, const double* vel) {
+    return guarded(ctx, [&] { ctx->eng->set_state(pos, vel); });
+}
+mgpbd_status mgpbd_get_positions(mgpbd_ctx* ctx, double* out) {
+    if (ctx && !out) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_positions(out); });
+}
+mgpbd_status mgpbd_get_velocities(mgpbd_ctx* ctx, double* out) {
+    if (ctx && !out) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_velocities(out); });
+}
+mgpbd_status mgpbd_get_lambda(mgpbd_ctx* ctx, double* out) {
+    if (ctx && !out) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_lambda(out); });
+}
+mgpbd_status mgpbd_get_stats(mgpbd_ctx* ctx, mgpbd_stats* out) {
+    if (ctx && !out) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_stats(out); });
+}
+mgpbd_status mgpbd_get_level_sizes(mgpbd_ctx* ctx, int32_t l, int64_t* n, int64_t* nnz) {
+    if (ctx && (!n || !nnz)) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->level_sizes(l, n, nnz); });
+}
+mgpbd_status mgpbd_get_level(mgpbd_ctx* ctx, int32_t l, int64_t* rowptr, int32_t* cols, double* vals) {
+    return guarded(ctx, [&] { ctx->eng->get_level(l, rowptr, cols, vals); });
+}
+mgpbd_status mgpbd_get_prolongator(mgpbd_ctx* ctx, int32_t l, double* p) {
+    if (ctx && !p) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_prolongator(l, p); });
+}
+mgpbd_status mgpbd_get_aggregates(mgpbd_ctx* ctx, int32_t l, int32_t* out) {
+    if (ctx && !out) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_aggregates(l, out); });
+}
+mgpbd_status mgpbd_get_near_kernel(mgpbd_ctx* ctx, double* out) {
+    if (ctx && !out) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_near_kernel(out); });
+}
+mgpbd_status mgpbd_debug_setup_from(mgpbd_ctx* ctx, const double* vals) {
+    if (ctx && !vals) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->debug_setup_from(vals); });
+}
+mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x) {
+    if (ctx && (!b || !x)) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->debug_vcycle(b, x); });
+}
+mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x) {
+    if (ctx && (!b || !x || iters < 0 || iters > 4096)) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->debug_pcg(b, iters, x); });
+}
+const char* mgpbd_last_error(const mgpbd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+void mgpbd_destroy(mgpbd_ctx* ctx) { delete ctx; }
+
+}  // extern "C"

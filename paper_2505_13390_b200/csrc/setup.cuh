@@ -1,0 +1,59 @@
+// AMG setup kernels and the Galerkin product (a7).
+// Setup always runs on fp64 values; the numeric Galerkin product is templated on the hot precision.
+#pragma once
+#include "common.cuh"
+#include "solve.cuh"
+
+namespace mgpbd {
+
+// Filter: strong[e] = (col != i) && |A_ij| >= theta sqrt(|A_ii||A_jj|)
+void soc(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, double theta, uint8_t* strong,
+         cudaStream_t s);
+
+// Aggregate (readings c2/c3): priority-order standard aggregation computed as
+// MIS-2 rounds + membership + leftover pass.  Returns n_agg; agg[i] in [0, n_agg).
+int32_t aggregate(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, const uint8_t* strong,
+                  uint64_t seed, int level, int32_t* agg, cudaStream_t s);
+
+// Greedy first-fit colouring in priority order (reading c5) by Jones-Plassmann rounds.
+int32_t colour(int32_t n, const int64_t* rowptr, const int32_t* col, uint64_t seed, int32_t* colours, cudaStream_t s);
+
+// Near-kernel bootstrap: `sweeps` colour-major GS sweeps on A x = 0.
+void gs_bootstrap(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, const int32_t* colours,
+                  int32_t ncolours, int32_t sweeps, uint64_t seed, double* B, cudaStream_t s);
+
+// Inject (k = 1): P_i = B_i / ||B_agg(i)||, B_next[a] = ||B_a|| (members ascending).
+void prolongator(int32_t n_agg, const int64_t* mptr, const int32_t* mlist, const double* B, double* P,
+                 double* B_next, cudaStream_t s);
+
+// Galerkin symbolic structures for fine level -> coarse level.
+struct GalerkinPlan {
+    DBuf<uint16_t> gperm;   // per fine nnz: row-relative entry index at sorted position (agg(col), col)
+    DBuf<int64_t> tptr;     // fine rows + 1: first t-entry (segment) of each row
+    DBuf<int64_t> tstart;   // T + 1: absolute sorted position where segment t starts
+    DBuf<int32_t> trow;     // T: fine row of segment t
+    DBuf<int32_t> tagg;     // T: coarse column of segment t
+    DBuf<int64_t> lptr;     // coarse nnz + 1: ranges into llist
+    DBuf<int32_t> llist;    // T: segments grouped by coarse nnz, ascending
+    int64_t T = 0;
+};
+
+// Builds plan + coarse pattern (crowptr/ccol, off-diagonals ascending, diagonal last).
+void galerkin_symbolic(int32_t n, const int64_t* rowptr, const int32_t* col, const int32_t* agg,
+                       const int64_t* mptr, const int32_t* mlist, int32_t n_agg, GalerkinPlan& plan,
+                       DBuf<int64_t>& crowptr, DBuf<int32_t>& ccol, cudaStream_t s);
+
+// Numeric Galerkin (Eq. 6): cval = P^T A P over the cached plan; cdinv = 1/diag.
+template <class T>
+void galerkin_numeric(const GalerkinPlan& plan, const int64_t* rowptr, const int32_t* col, const T* val,
+                      const T* P, int32_t n_agg, const int64_t* crowptr, int64_t cnnz, T* tval, T* cval, T* cdinv,
+                      cudaStream_t s);
+
+template <class T>
+void diag_inv(int32_t n, const int64_t* rowptr, const T* val, T* dinv, cudaStream_t s);
+
+// lambda_max(D^-1 A) by the power method (reading c9); returns lambda (host sync).
+double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
+                    double* parts, double* ss, cudaStream_t s);
+
+}  // namespace mgpbd

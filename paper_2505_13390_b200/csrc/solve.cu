@@ -1,0 +1,348 @@
+// Hot-loop kernels of the MGPCG solve (see solve.cuh).
+#include "solve.cuh"
+
+namespace mgpbd {
+namespace {
+
+constexpr int PB = 256;  // threads per block of the CSR passes
+
+inline int vgrid(int64_t n) {
+    int64_t g = (n + PB - 1) / PB;
+    return (int)(g < 148 * 8 ? (g > 0 ? g : 1) : 148 * 8);
+}
+
+// One fused pass over a CSR matrix, VL lanes per row, grid-stride over rows with a warp-uniform loop
+// (so the fixed-order sub-warp butterfly is always executed by full warps).
+template <class T, int VL, int MODE>
+__global__ void __launch_bounds__(PB) k_pass(int32_t n, const int64_t* __restrict__ rowptr,
+                                             const int32_t* __restrict__ col, const T* __restrict__ val,
+                                             const T* __restrict__ dinv, const T* __restrict__ x,
+                                             const T* __restrict__ b, T* __restrict__ y,
+                                             const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                             double* __restrict__ parts2) {
+    constexpr int RPW = 32 / VL;  // rows per warp
+    const int lane = threadIdx.x & 31;
+    const int sub = lane % VL, rid = lane / VL;
+    const int64_t gw = ((int64_t)blockIdx.x * PB + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * PB) >> 5;
+    double acc1 = 0.0, acc2 = 0.0;
+    for (int64_t r0 = gw * RPW; r0 < n; r0 += nw * RPW) {
+        const int64_t i = r0 + rid;
+        const bool valid = i < n;
+        double s = 0.0;
+        if (valid) {
+            const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+#pragma unroll 4
+            for (int64_t e = e0 + sub; e < e1; e += VL) s += (double)val[e] * (double)x[col[e]];
+        }
+        s = group_sum<VL>(s);
+        if (valid && sub == 0) {
+            if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
+                T yi = (T)((double)x[i] + omega * (double)dinv[i] * ((double)b[i] - s));
+                y[i] = yi;
+                if (MODE == PASS_JACOBI_DOT) {
+                    double r = (double)aux[i];
+                    acc1 += r * (double)yi;
+                    acc2 += r * r;
+                }
+            } else if (MODE == PASS_RESID_P) {
+                y[i] = (T)((double)aux[i] * ((double)b[i] - s));
+            } else if (MODE == PASS_SPMV_DOT) {
+                T yi = (T)s;
+                y[i] = yi;
+                acc1 += (double)x[i] * (double)yi;
+            } else if (MODE == PASS_POWER) {
+                T yi = (T)((double)dinv[i] * s);
+                y[i] = yi;
+                acc1 += (double)yi * (double)yi;
+            }
+        }
+    }
+    if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
+        __shared__ double sh[32];
+        double t1 = block_sum<PB>(acc1, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t1;
+        if (MODE == PASS_JACOBI_DOT) {
+            double t2 = block_sum<PB>(acc2, sh);
+            if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
+        }
+    }
+}
+
+template <class T, int MODE>
+void launch_pass_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                      double* parts2, cudaStream_t s) {
+#define MG_P(VL) k_pass<T, VL, MODE><<<A.grid, PB, 0, s>>>(A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2)
+    switch (A.vl) {
+        case 2: MG_P(2); break;
+        case 4: MG_P(4); break;
+        case 8: MG_P(8); break;
+        case 16: MG_P(16); break;
+        default: MG_P(32); break;
+    }
+#undef MG_P
+    MG_LAUNCH_CHECK();
+}
+
+template <class T>
+__global__ void k_jacobi0(int32_t n, const T* __restrict__ dinv, const T* __restrict__ b, double omega, T* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = (T)(omega * (double)dinv[i] * (double)b[i]);
+}
+
+// bc[a] = sum_{i in a, ascending} t[i]  (warp per aggregate, fixed-order butterfly)
+template <class T>
+__global__ void k_restrict(int32_t nc, const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
+                           const T* __restrict__ t, T* __restrict__ bc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t a = gw; a < nc; a += nw) {
+        double s = 0.0;
+        for (int64_t e = mptr[a] + lane; e < mptr[a + 1]; e += 32) s += (double)t[mlist[e]];
+        s = group_sum<32>(s);
+        if (lane == 0) bc[a] = (T)s;
+    }
+}
+
+template <class T>
+__global__ void k_prolong(int32_t n, const int32_t* __restrict__ agg, const T* __restrict__ P, const T* __restrict__ e,
+                          T* __restrict__ x) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = (T)((double)x[i] + (double)P[i] * (double)e[agg[i]]);
+}
+
+template <class T>
+__global__ void k_pcg_p(int32_t n, const T* __restrict__ z, T* __restrict__ p, const double* __restrict__ scal, int k) {
+    double beta = 0.0;
+    if (k > 0) {
+        double prev = scal[2 * (k - 1)];
+        beta = prev != 0.0 ? scal[2 * k] / prev : 0.0;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (T)((double)z[i] + beta * (double)p[i]);
+}
+
+template <class T>
+__global__ void k_pcg_xr(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
+                         T* __restrict__ r, const double* __restrict__ scal, int k) {
+    double pq = scal[2 * k + 1];
+    double alpha = pq != 0.0 ? scal[2 * k] / pq : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = (T)((double)x[i] + alpha * (double)p[i]);
+        r[i] = (T)((double)r[i] - alpha * (double)q[i]);
+    }
+}
+
+template <class T>
+__global__ void k_dot(int32_t n, const T* __restrict__ a, const T* __restrict__ b, double* __restrict__ parts) {
+    __shared__ double sh[32];
+    double v = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v += (double)a[i] * (double)b[i];
+    v = block_sum<PB>(v, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = v;
+}
+
+template <class T>
+__global__ void k_scale(int32_t n, const T* __restrict__ w, T* __restrict__ v, const double* __restrict__ ss) {
+    double lam = sqrt(*ss);
+    double inv = lam > 0.0 ? 1.0 / lam : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = (T)((double)w[i] * inv);
+}
+
+__global__ void k_fin_rz(const double* __restrict__ prz, const double* __restrict__ prr, int np, double* scal, int k,
+                         int* flags, int tag) {
+    __shared__ double sh[32];
+    double a = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < np; i += 1024) { a += prz[i]; c += prr[i]; }
+    a = block_sum<1024>(a, sh);
+    c = block_sum<1024>(c, sh);
+    if (threadIdx.x == 0) {
+        scal[2 * k] = a;
+        if (!isfinite(a) || !isfinite(c)) {
+            if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+        } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
+            if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+        }
+    }
+}
+__global__ void k_fin_pq(const double* __restrict__ p, int np, double* scal, int k, int* flags, int tag) {
+    __shared__ double sh[32];
+    double a = 0.0;
+    for (int i = threadIdx.x; i < np; i += 1024) a += p[i];
+    a = block_sum<1024>(a, sh);
+    if (threadIdx.x == 0) {
+        scal[2 * k + 1] = a;
+        if (!isfinite(a)) {
+            if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+        }
+    }
+}
+
+// Gauss-Jordan in-place inversion of the dense SPD coarsest matrix, one CTA.
+template <class T>
+__global__ void __launch_bounds__(1024) k_coarse_inv(int32_t n, const int64_t* __restrict__ rowptr,
+                                                     const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                     double* __restrict__ gwork, double* __restrict__ Ainv,
+                                                     int* flags, int use_smem) {
+    extern __shared__ double smem[];
+    double* W = use_smem ? smem : gwork;
+    const int64_t nn = (int64_t)n * n;
+    for (int64_t k = threadIdx.x; k < nn; k += blockDim.x) W[k] = 0.0;
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x)
+        for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) W[(int64_t)i * n + col[e]] = (double)val[e];
+    __syncthreads();
+    __shared__ double piv_s;
+    for (int32_t k = 0; k < n; ++k) {
+        if (threadIdx.x == 0) {
+            double p = W[(int64_t)k * n + k];
+            if (!(p > 0.0)) {
+                if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = -1;
+                p = (p == 0.0 || !isfinite(p)) ? 1.0 : p;
+            }
+            piv_s = p;
+        }
+        __syncthreads();
+        const double ip = 1.0 / piv_s;
+        for (int64_t t = threadIdx.x; t < nn; t += blockDim.x) {
+            int32_t i = (int32_t)(t / n), j = (int32_t)(t % n);
+            if (i != k && j != k) W[t] -= W[(int64_t)i * n + k] * W[(int64_t)k * n + j] * ip;
+        }
+        __syncthreads();
+        for (int32_t t = threadIdx.x; t < n; t += blockDim.x) {
+            if (t != k) {
+                W[(int64_t)k * n + t] *= ip;
+                W[(int64_t)t * n + k] = -W[(int64_t)t * n + k] * ip;
+            }
+        }
+        if (threadIdx.x == 0) W[(int64_t)k * n + k] = ip;
+        __syncthreads();
+    }
+    for (int64_t k = threadIdx.x; k < nn; k += blockDim.x) Ainv[k] = W[k];
+}
+
+template <class T>
+__global__ void k_coarse_gemv(int32_t n, const double* __restrict__ Ainv, const T* __restrict__ b, T* __restrict__ x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < n; i += nw) {
+        double s = 0.0;
+        for (int32_t j = lane; j < n; j += 32) s += Ainv[i * n + j] * (double)b[j];
+        s = group_sum<32>(s);
+        if (lane == 0) x[i] = (T)s;
+    }
+}
+
+}  // namespace
+
+int pass_grid(int32_t n, int vl) {
+    int rows_per_block = PB / vl;
+    int64_t g = ((int64_t)n + rows_per_block - 1) / rows_per_block;
+    if (g < 1) g = 1;
+    return (int)(g < 148 * 8 ? g : 148 * 8);
+}
+
+template <class T>
+void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+              double* parts2, cudaStream_t s) {
+    if (A.n == 0) return;
+    switch (mode) {
+        case PASS_JACOBI: launch_pass_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case PASS_JACOBI_DOT: launch_pass_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case PASS_RESID_P: launch_pass_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case PASS_SPMV_DOT: launch_pass_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case PASS_POWER: launch_pass_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        default: throw Error(-1, "bad pass mode");
+    }
+}
+
+template <class T>
+void vec_jacobi0(int32_t n, const T* dinv, const T* b, double omega, T* y, cudaStream_t s) {
+    if (!n) return;
+    k_jacobi0<T><<<vgrid(n), PB, 0, s>>>(n, dinv, b, omega, y);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, const T* t, T* bc, cudaStream_t s) {
+    if (!nc) return;
+    int g = (int)std::min<int64_t>(((int64_t)nc * 32 + PB - 1) / PB, 148 * 8);
+    k_restrict<T><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void prolong_add(int32_t n, const int32_t* agg, const T* P, const T* e, T* x, cudaStream_t s) {
+    if (!n) return;
+    k_prolong<T><<<vgrid(n), PB, 0, s>>>(n, agg, P, e, x);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaStream_t s) {
+    if (!n) return;
+    k_pcg_p<T><<<vgrid(n), PB, 0, s>>>(n, z, p, scal, k);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void pcg_update_xr(int32_t n, const T* p, const T* q, T* x, T* r, const double* scal, int k, cudaStream_t s) {
+    if (!n) return;
+    k_pcg_xr<T><<<vgrid(n), PB, 0, s>>>(n, p, q, x, r, scal, k);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void dot_parts(int32_t n, const T* a, const T* b, double* parts, int grid, cudaStream_t s) {
+    k_dot<T><<<grid, PB, 0, s>>>(n, a, b, parts);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void scale_by_inv_sqrt(int32_t n, const T* w, T* v, const double* ss, cudaStream_t s) {
+    if (!n) return;
+    k_scale<T><<<vgrid(n), PB, 0, s>>>(n, w, v, ss);
+    MG_LAUNCH_CHECK();
+}
+void pcg_finalize_rz(const double* prz, const double* prr, int np, double* scal, int k, int* flags, int tag,
+                     cudaStream_t s) {
+    k_fin_rz<<<1, 1024, 0, s>>>(prz, prr, np, scal, k, flags, tag);
+    MG_LAUNCH_CHECK();
+}
+void pcg_finalize_pq(const double* p, int np, double* scal, int k, int* flags, int tag, cudaStream_t s) {
+    k_fin_pq<<<1, 1024, 0, s>>>(p, np, scal, k, flags, tag);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cudaStream_t s) {
+    size_t bytes = (size_t)A.n * A.n * sizeof(double);
+    int use_smem = bytes <= 160 * 1024;
+    size_t smem = use_smem ? bytes : 0;
+    if (smem > 48 * 1024)
+        MG_CK(cudaFuncSetAttribute(k_coarse_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_coarse_inv<T><<<1, 1024, smem, s>>>(A.n, A.rowptr, A.col, A.val, work, Ainv, flags, use_smem);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s) {
+    if (!n) return;
+    int g = (int)std::min<int64_t>(((int64_t)n * 32 + PB - 1) / PB, 148 * 8);
+    k_coarse_gemv<T><<<g, PB, 0, s>>>(n, Ainv, b, x);
+    MG_LAUNCH_CHECK();
+}
+
+#define MG_INST(T)                                                                                            \
+    template void csr_pass<T>(int, const Csr<T>&, const T*, const T*, T*, const T*, double, double*, double*,  \
+                              cudaStream_t);                                                                   \
+    template void vec_jacobi0<T>(int32_t, const T*, const T*, double, T*, cudaStream_t);                       \
+    template void restrict_members<T>(int32_t, const int64_t*, const int32_t*, const T*, T*, cudaStream_t);    \
+    template void prolong_add<T>(int32_t, const int32_t*, const T*, const T*, T*, cudaStream_t);               \
+    template void pcg_update_p<T>(int32_t, const T*, T*, const double*, int, cudaStream_t);                    \
+    template void pcg_update_xr<T>(int32_t, const T*, const T*, T*, T*, const double*, int, cudaStream_t);     \
+    template void dot_parts<T>(int32_t, const T*, const T*, double*, int, cudaStream_t);                       \
+    template void scale_by_inv_sqrt<T>(int32_t, const T*, T*, const double*, cudaStream_t);                    \
+    template void coarse_invert<T>(const Csr<T>&, double*, double*, int*, cudaStream_t);                       \
+    template void coarse_gemv<T>(int32_t, const double*, const T*, T*, cudaStream_t);
+MG_INST(float)
+MG_INST(double)
+#undef MG_INST
+
+}  // namespace mgpbd

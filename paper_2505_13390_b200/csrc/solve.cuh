@@ -1,0 +1,61 @@
+// Hot-loop kernels: fused CSR passes (omega-Jacobi sweep, residual*P, SpMV+dot, power step),
+// aggregate restriction, prolongation, PCG vector updates, coarsest dense inverse + GEMV
+// (SURVEY.md §8(a) rows a8-a11).
+#pragma once
+#include "common.cuh"
+
+namespace mgpbd {
+
+template <class T>
+struct Csr {
+    int32_t n = 0;
+    int64_t nnz = 0;
+    const int64_t* rowptr = nullptr;
+    const int32_t* col = nullptr;
+    const T* val = nullptr;
+    const T* dinv = nullptr;
+    int vl = 32;     // lanes per row
+    int grid = 1;    // fixed grid (=> fixed partial count => deterministic reductions)
+};
+
+enum PassMode {
+    PASS_JACOBI = 0,      // y = x + omega dinv (b - A x)
+    PASS_JACOBI_DOT = 1,  // same, plus partials of sum aux_i*y_i and sum aux_i^2 (aux = PCG r)
+    PASS_RESID_P = 2,     // y = aux * (b - A x)   (aux = P: restriction input)
+    PASS_SPMV_DOT = 3,    // y = A x, partials of sum x_i*y_i
+    PASS_POWER = 4,       // y = dinv (A x), partials of sum y_i^2
+    PASS_JACOBI0_FIRST = 5
+};
+
+int pass_grid(int32_t n, int vl);
+
+template <class T>
+void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
+              double* parts, double* parts2, cudaStream_t s);
+
+template <class T> void vec_jacobi0(int32_t n, const T* dinv, const T* b, double omega, T* y, cudaStream_t s);
+template <class T> void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, const T* t,
+                                         T* bc, cudaStream_t s);
+template <class T> void prolong_add(int32_t n, const int32_t* agg, const T* P, const T* e, T* x, cudaStream_t s);
+// p = z + beta p with beta = rz[k]/rz[k-1] (0 if k == 0 or rz[k-1] == 0)
+template <class T> void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaStream_t s);
+// alpha = rz[k]/pq[k] (0 if pq == 0); x += alpha p; r -= alpha q
+template <class T> void pcg_update_xr(int32_t n, const T* p, const T* q, T* x, T* r, const double* scal, int k,
+                                      cudaStream_t s);
+template <class T> void dot_parts(int32_t n, const T* a, const T* b, double* parts, int grid, cudaStream_t s);
+// power method normalisation: v = w / sqrt(scal[0])
+template <class T> void scale_by_inv_sqrt(int32_t n, const T* w, T* v, const double* ss, cudaStream_t s);
+
+// PCG scalar layout in the device scalar array: rz[k] at 2k, pq[k] at 2k+1; flags int array:
+// flags[0] indefinite, flags[1] non-finite (first occurrence iteration in flags[2..3]).
+void pcg_finalize_rz(const double* parts_rz, const double* parts_rr, int np, double* scal, int k, int* flags,
+                     int tag, cudaStream_t s);
+void pcg_finalize_pq(const double* parts, int np, double* scal, int k, int* flags, int tag, cudaStream_t s);
+
+// Coarsest level: dense inverse by Gauss-Jordan (SPD, no pivoting; reading c8) of the CSR values,
+// then GEMV x = Ainv b.
+template <class T>
+void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cudaStream_t s);
+template <class T> void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s);
+
+}  // namespace mgpbd

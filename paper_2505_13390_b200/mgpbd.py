@@ -1,0 +1,227 @@
+"""Thin ctypes binding of libmgpbd.so (include/mgpbd.h).  Argument marshalling only: every step
+of the MGPBD frame runs in the library's CUDA kernels.  There is no CPU fallback: if the library is
+missing or no CUDA device is present, calls fail loudly."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmgpbd.so")
+
+OK, E_ARG, E_CUDA, E_NCCL, E_OOM, E_INDEFINITE, E_NONFINITE, E_STALL = 0, -1, -2, -3, -4, -5, -6, -7
+DISTANCE, TET_ARAP = 2, 4
+MAX_LEVELS, MAX_ITERS = 16, 256
+
+SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgpbd_step", "mgpbd_set_state",
+           "mgpbd_get_positions", "mgpbd_get_velocities", "mgpbd_get_lambda", "mgpbd_get_stats",
+           "mgpbd_get_level_sizes", "mgpbd_get_level", "mgpbd_get_prolongator", "mgpbd_get_aggregates",
+           "mgpbd_get_near_kernel", "mgpbd_debug_setup_from", "mgpbd_debug_vcycle", "mgpbd_debug_pcg",
+           "mgpbd_last_error", "mgpbd_destroy"]
+
+
+class MgpbdError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"mgpbd status {status}: {msg}")
+        self.status = status
+
+
+class Mesh(C.Structure):
+    _fields_ = [("n_verts", C.c_int32), ("rest_pos", C.c_void_p), ("pos", C.c_void_p), ("vel", C.c_void_p)]
+
+
+class Constraints(C.Structure):
+    _fields_ = [("kind", C.c_int), ("n_cons", C.c_int32), ("verts", C.c_void_p)]
+
+
+class Config(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("theta", C.c_double), ("k_nullspace", C.c_int32),
+                ("min_coarse", C.c_int32), ("max_levels", C.c_int32), ("stall_ratio", C.c_double),
+                ("setup_interval", C.c_int32), ("bootstrap_sweeps", C.c_int32), ("power_iters", C.c_int32),
+                ("lambda_min_est", C.c_double), ("smoother_sweeps", C.c_int32), ("pcg_iters", C.c_int32),
+                ("omega_relax", C.c_double), ("gravity", C.c_double * 3), ("seed", C.c_uint64),
+                ("device", C.c_int32), ("stream", C.c_void_p), ("max_dense_coarse", C.c_int32),
+                ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("n_levels", C.c_int32), ("n", C.c_int64 * MAX_LEVELS), ("nnz", C.c_int64 * MAX_LEVELS),
+                ("op_complexity", C.c_double), ("omega", C.c_double * MAX_LEVELS), ("n_colours", C.c_int32),
+                ("setup_ran", C.c_int32), ("n_b", C.c_int32), ("b_norm", C.c_double * MAX_ITERS),
+                ("frame", C.c_int64), ("l0_pass_ms", C.c_double), ("l0_pass_launches", C.c_int64),
+                ("l0_pass_bytes", C.c_double), ("ms_setup", C.c_double), ("ms_frame", C.c_double),
+                ("kernel_launches", C.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libmgpbd.so (built in-tree by build.py).  Raises if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2505_13390_b200.build` "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+        sig = {
+            "mgpbd_config_default": (C.c_int, [P]),
+            "mgpbd_create": (C.c_int, [P, P, P, P, P, P]),
+            "mgpbd_setup_hierarchy": (C.c_int, [P]),
+            "mgpbd_step": (C.c_int, [P, f64, i32]),
+            "mgpbd_set_state": (C.c_int, [P, P, P]),
+            "mgpbd_get_positions": (C.c_int, [P, P]),
+            "mgpbd_get_velocities": (C.c_int, [P, P]),
+            "mgpbd_get_lambda": (C.c_int, [P, P]),
+            "mgpbd_get_stats": (C.c_int, [P, P]),
+            "mgpbd_get_level_sizes": (C.c_int, [P, i32, P, P]),
+            "mgpbd_get_level": (C.c_int, [P, i32, P, P, P]),
+            "mgpbd_get_prolongator": (C.c_int, [P, i32, P]),
+            "mgpbd_get_aggregates": (C.c_int, [P, i32, P]),
+            "mgpbd_get_near_kernel": (C.c_int, [P, P]),
+            "mgpbd_debug_setup_from": (C.c_int, [P, P]),
+            "mgpbd_debug_vcycle": (C.c_int, [P, P, P]),
+            "mgpbd_debug_pcg": (C.c_int, [P, P, i32, P]),
+            "mgpbd_last_error": (C.c_char_p, [P]),
+            "mgpbd_destroy": (None, [P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def config_default(**kw) -> Config:
+    c = Config()
+    lib().mgpbd_config_default(C.byref(c))
+    for k, v in kw.items():
+        if k == "gravity":
+            c.gravity[:] = list(v)
+        else:
+            setattr(c, k, v)
+    return c
+
+
+class Context:
+    """One MGPBD simulation on one GPU (mgpbd_create ... mgpbd_destroy)."""
+
+    def __init__(self, kind, verts, rest_pos, inv_mass, compliance, pos=None, vel=None, cfg: Config | None = None,
+                 **cfg_kw):
+        L = lib()
+        self.cfg = cfg or config_default(**cfg_kw)
+        self.verts = np.ascontiguousarray(verts, np.int32)
+        self.m = int(self.verts.shape[0])
+        self.rest = np.ascontiguousarray(rest_pos, np.float64)
+        self.n = int(self.rest.shape[0])
+        self._pos = None if pos is None else np.ascontiguousarray(pos, np.float64)
+        self._vel = None if vel is None else np.ascontiguousarray(vel, np.float64)
+        w = np.ascontiguousarray(inv_mass, np.float64)
+        a = np.ascontiguousarray(compliance, np.float64)
+        mesh = Mesh(self.n, _p(self.rest), _p(self._pos), _p(self._vel))
+        cons = Constraints(int(kind), self.m, _p(self.verts))
+        h = C.c_void_p()
+        st = L.mgpbd_create(C.byref(mesh), C.byref(cons), _p(w), _p(a), C.byref(self.cfg), C.byref(h))
+        if st != OK:
+            raise MgpbdError(st, L.mgpbd_last_error(None).decode())
+        self.h = h
+
+    @classmethod
+    def from_scene(cls, sc, **cfg_kw):
+        cfg_kw.setdefault("omega_relax", sc.omega_relax)
+        cfg_kw.setdefault("pcg_iters", sc.pcg_iters)
+        return cls(sc.kind, sc.verts, sc.rest_pos, sc.inv_mass, sc.compliance, pos=sc.pos, vel=sc.vel, **cfg_kw)
+
+    def _ck(self, st):
+        if st != OK:
+            raise MgpbdError(st, lib().mgpbd_last_error(self.h).decode())
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().mgpbd_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def setup_hierarchy(self):
+        self._ck(lib().mgpbd_setup_hierarchy(self.h))
+
+    def step(self, dt, n_iters):
+        self._ck(lib().mgpbd_step(self.h, float(dt), int(n_iters)))
+
+    def set_state(self, pos, vel=None):
+        pos = np.ascontiguousarray(pos, np.float64)
+        vel = None if vel is None else np.ascontiguousarray(vel, np.float64)
+        self._ck(lib().mgpbd_set_state(self.h, _p(pos), _p(vel)))
+
+    def positions(self, out=None):
+        out = np.empty((self.n, 3)) if out is None else out
+        self._ck(lib().mgpbd_get_positions(self.h, _p(out)))
+        return out
+
+    def velocities(self):
+        out = np.empty((self.n, 3))
+        self._ck(lib().mgpbd_get_velocities(self.h, _p(out)))
+        return out
+
+    def lambdas(self, out=None):
+        out = np.empty(self.m) if out is None else out
+        self._ck(lib().mgpbd_get_lambda(self.h, _p(out)))
+        return out
+
+    def stats(self) -> Stats:
+        s = Stats()
+        self._ck(lib().mgpbd_get_stats(self.h, C.byref(s)))
+        return s
+
+    def level_size(self, l):
+        n = C.c_int64(); nnz = C.c_int64()
+        self._ck(lib().mgpbd_get_level_sizes(self.h, l, C.byref(n), C.byref(nnz)))
+        return n.value, nnz.value
+
+    def level(self, l):
+        n, nnz = self.level_size(l)
+        r = np.empty(n + 1, np.int64); c = np.empty(nnz, np.int32); v = np.empty(nnz)
+        self._ck(lib().mgpbd_get_level(self.h, l, _p(r), _p(c), _p(v)))
+        return r, c, v
+
+    def prolongator(self, l):
+        n, _ = self.level_size(l)
+        out = np.empty(n)
+        self._ck(lib().mgpbd_get_prolongator(self.h, l, _p(out)))
+        return out
+
+    def aggregates(self, l):
+        n, _ = self.level_size(l)
+        out = np.empty(n, np.int32)
+        self._ck(lib().mgpbd_get_aggregates(self.h, l, _p(out)))
+        return out
+
+    def near_kernel(self):
+        out = np.empty(self.m)
+        self._ck(lib().mgpbd_get_near_kernel(self.h, _p(out)))
+        return out
+
+    def debug_setup_from(self, vals):
+        vals = np.ascontiguousarray(vals, np.float64)
+        self._ck(lib().mgpbd_debug_setup_from(self.h, _p(vals)))
+
+    def debug_vcycle(self, b):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty_like(b)
+        self._ck(lib().mgpbd_debug_vcycle(self.h, _p(b), _p(x)))
+        return x
+
+    def debug_pcg(self, b, iters):
+        b = np.ascontiguousarray(b, np.float64)
+        x = np.empty_like(b)
+        self._ck(lib().mgpbd_debug_pcg(self.h, _p(b), int(iters), _p(x)))
+        return x

@@ -1,0 +1,196 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle, element by element on identical
+seeded inputs.  Tolerances: patterns, aggregates, colour-independent integer
+results bit-exact; fp64 values <= 1e-12 relative per stage on identical inputs; whole frame fp64
+<= 1e-6 relative, fp32 <= 1e-3 relative (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2505_13390_b200 import mgpbd, scenes
+
+pytestmark = pytest.mark.gpu
+
+SMALL = ["cloth16", "bar_small", "bar3k", "cloth64"]
+
+
+def make_scene(name):
+    if name == "cloth64":
+        return scenes.cloth(64, dt=3e-3, n_iters=5)
+    return scenes.make(name)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def ctx_for(sc, precision=0, **kw):
+    return mgpbd.Context.from_scene(sc, precision=precision, **kw)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_pattern_bit_exact(name):
+    sc = make_scene(name)
+    ctx = ctx_for(sc)
+    r, c, _ = ctx.level(0)
+    ro, co = O.pattern(sc.verts, sc.n_verts)
+    assert np.array_equal(r, ro) and np.array_equal(c, co)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_assembly_and_rhs_fp64(name):
+    sc = make_scene(name)
+    ctx = ctx_for(sc)
+    ctx.step(sc.dt, 1)
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = ctx.level(0)
+    ro, co, vo = sim.A()
+    assert np.array_equal(r, ro) and np.array_equal(c, co)
+    scale = np.abs(vo).max()
+    assert np.abs(v - vo).max() <= 1e-12 * scale
+    # bitwise symmetric (canonical shared-vertex order on the device as well)
+    n = r.shape[0] - 1
+    rows = np.repeat(np.arange(n), np.diff(r))
+    import scipy.sparse as sp
+    A = sp.csr_matrix((v, (rows, c)), shape=(n, n))
+    assert (A != A.T).nnz == 0
+    st = ctx.stats()
+    assert np.isclose(st.b_norm[0], sim.b_norms(1)[0], rtol=1e-12)
+
+
+def oracle_setup(sc, ctx=None):
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    return r, c, v, O.Hierarchy(r, c, v)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_setup_identical_input_bits(name):
+    """Setup on the oracle's own A_0 bits: aggregates and patterns bit-exact, P/B/omega/levels to 1e-12."""
+    sc = make_scene(name)
+    r, c, v, h = oracle_setup(sc)
+    ctx = ctx_for(sc)
+    ctx.debug_setup_from(v)
+    st = ctx.stats()
+    assert st.n_levels == h.n_levels
+    if h.n_levels > 1:
+        assert st.n_colours == h.n_colours
+        assert rel(ctx.near_kernel(), h.B0()) <= 1e-10
+    for l in range(h.n_levels):
+        rg, cg, vg = ctx.level(l)
+        ro, co, vo = h.level(l)
+        assert np.array_equal(rg, ro) and np.array_equal(cg, co), l
+        assert np.abs(vg - vo).max() <= 1e-12 * np.abs(vo).max(), l
+        if l + 1 < h.n_levels:
+            assert np.array_equal(ctx.aggregates(l), h.agg(l)), l
+            assert np.abs(ctx.prolongator(l) - h.P(l)).max() <= 1e-12, l
+            assert np.isclose(st.omega[l], h.omega(l), rtol=1e-10), l
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_vcycle_and_pcg_identical_hierarchy(name):
+    sc = make_scene(name)
+    r, c, v, h = oracle_setup(sc)
+    ctx = ctx_for(sc)
+    ctx.debug_setup_from(v)
+    rng = np.random.default_rng(0)
+    b = rng.normal(size=sc.n_cons)
+    assert rel(ctx.debug_vcycle(b), h.vcycle(b)) <= 1e-11
+    for K in (1, 3, 10):
+        xg = ctx.debug_pcg(b, K)
+        xo, rc, _ = h.pcg(b, K)
+        assert rc == 0
+        assert rel(xg, xo) <= 1e-9, K
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_frame_fp64(name):
+    sc = make_scene(name)
+    ctx = ctx_for(sc)
+    sim = O.Sim(sc)
+    ctx.step(sc.dt, sc.n_iters)
+    assert sim.step(sc.dt, sc.n_iters) == 0
+    xo, vo, lo = sim.state()
+    xg, vg, lg = ctx.positions(), ctx.velocities(), ctx.lambdas()
+    assert rel(lg, lo) <= 1e-6
+    assert rel(xg - sc.pos, xo - sc.pos) <= 1e-6 and rel(xg, xo) <= 1e-6
+    assert rel(vg, vo) <= 1e-6
+    st = ctx.stats()
+    assert np.allclose(st.b_norm[:sc.n_iters], sim.b_norms(sc.n_iters), rtol=1e-6)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_frame_fp32(name):
+    sc = make_scene(name)
+    ctx = ctx_for(sc, precision=1)
+    sim = O.Sim(sc)
+    ctx.step(sc.dt, sc.n_iters)
+    sim.step(sc.dt, sc.n_iters)
+    xo, _, lo = sim.state()
+    xg, lg = ctx.positions(), ctx.lambdas()
+    assert rel(lg, lo) <= 1e-3
+    assert rel(xg - sc.pos, xo - sc.pos) <= 1e-3
+
+
+def test_three_frames_lazy_setup_and_stale():
+    sc = scenes.make("cloth16")
+    ctx = ctx_for(sc, setup_interval=2)
+    sim = O.Sim(sc, O.default_config(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters, setup_interval=2))
+    ran = []
+    for f in range(3):
+        ctx.step(sc.dt, 4)
+        sim.step(sc.dt, 4)
+        ran.append(ctx.stats().setup_ran)
+    assert ran == [1, 0, 1]
+    ctx.setup_hierarchy(); sim.mark_stale()
+    ctx.step(sc.dt, 4); sim.step(sc.dt, 4)
+    assert ctx.stats().setup_ran == 1
+    xo, _, lo = sim.state()
+    assert rel(ctx.lambdas(), lo) <= 1e-6 and rel(ctx.positions(), xo) <= 1e-6
+
+
+def test_single_constraint_closed_form():
+    X = np.array([[0, 0, 0], [1, 0, 0]], float)
+    x0 = np.array([[0, 0, 0], [2, 0, 0]], float)
+    ctx = mgpbd.Context(2, np.array([[0, 1]], np.int32), X, np.ones(2), np.zeros(1), pos=x0,
+                        omega_relax=1.0, gravity=(0, 0, 0), pcg_iters=1)
+    ctx.step(1.0, 1)
+    assert np.isclose(ctx.lambdas()[0], -0.5, rtol=1e-15)            # Eq. 4
+    assert np.allclose(ctx.positions(), [[0.5, 0, 0], [1.5, 0, 0]], rtol=1e-15)   # Eq. 5
+
+
+def test_rest_state_and_pins():
+    sc = scenes.cloth(8, jitter=0.0)
+    ctx = ctx_for(sc, gravity=(0, 0, 0))
+    ctx.step(sc.dt, 3)
+    assert np.abs(ctx.positions() - sc.pos).max() <= 1e-12
+    sc = scenes.make("bar3k")
+    ctx = ctx_for(sc)
+    for _ in range(2):
+        ctx.step(sc.dt, 3)
+    pinned = sc.inv_mass == 0
+    assert np.array_equal(ctx.positions()[pinned], sc.pos[pinned])
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_deterministic(precision):
+    sc = scenes.make("bar3k")
+    outs = []
+    for _ in range(2):
+        ctx = ctx_for(sc, precision=precision)
+        ctx.step(sc.dt, 3)
+        outs.append((ctx.positions(), ctx.lambdas()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_step_argument_errors():
+    sc = scenes.make("cloth16")
+    ctx = ctx_for(sc)
+    with pytest.raises(mgpbd.MgpbdError):
+        ctx.step(0.0, 1)
+    with pytest.raises(mgpbd.MgpbdError):
+        ctx.step(sc.dt, 0)
+    with pytest.raises(mgpbd.MgpbdError):
+        ctx.aggregates(0)          # no hierarchy before the first step
