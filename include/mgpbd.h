@@ -77,6 +77,8 @@ typedef struct {
     int32_t bootstrap_sweeps; /* GS sweeps on A x = 0, 20 */
     int32_t power_iters;      /* power-method iterations for lambda_max(D^-1 A), 100 */
     double lambda_min_est;    /* user estimate of lambda_min, 0.1 */
+    double lambda_safety;     /* omega = 2/(lambda_safety*lambda_max + lambda_min_est), 1.1: keeps the
+                                 lazily-set omega below 2/lambda_max as A drifts (reading c9) */
     int32_t smoother_sweeps;  /* pre = post omega-Jacobi sweeps, 2 */
     int32_t pcg_iters;        /* fixed MGPCG iterations per outer iteration (reading c10), 10 */
     double omega_relax;       /* x += omega dx: 0.1 tets, 0.25 cloth */
@@ -110,6 +112,8 @@ typedef struct {
     double ms_setup;                   /* CUDA-event time of the setup in the last frame */
     double ms_frame;                   /* CUDA-event time of the last frame */
     int64_t kernel_launches;           /* this library's kernel launches in the last frame */
+    int32_t indefinite_events;         /* PCG iterations of the last frame with <z,r> <= 0 (r != 0):
+                                          the lazily-set omega went stale; setup re-runs next frame */
 } mgpbd_stats;
 
 /* Fill *cfg with the defaults listed above.  Never fails for a non-NULL cfg. */

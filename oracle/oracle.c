@@ -19,7 +19,7 @@ static void* xcalloc(size_t n, size_t s) { void* p = calloc(n ? n : 1, s ? s : 1
 void orc_config_default(orc_config* c) {
     c->theta = 0.1; c->min_coarse = 400; c->max_levels = 16; c->stall_ratio = 0.9;
     c->setup_interval = 20; c->bootstrap_sweeps = 20; c->power_iters = 100;
-    c->lambda_min_est = 0.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
+    c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -654,7 +654,7 @@ static int factor_coarsest(orc_hier* h) {
 
 /* Setup pipeline (§4.1): per level Filter -> Aggregate -> Inject -> Galerkin;
  * the level-0 near kernel comes from the GS bootstrap (§4.3), coarser ones from R (c6); omega_l
- * = 2/(lambda_max(D^-1 A_l) + lambda_min_est) (§4.5); stop when n < min_coarse (c7). */
+ * = 2/(s lambda_max(D^-1 A_l) + lambda_min_est) (§4.5; safety s, reading c9); stop when n < min_coarse (c7). */
 orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
                          const orc_config* cfg) {
     orc_hier* h = xcalloc(1, sizeof(orc_hier));
@@ -701,7 +701,7 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
         c->val = xmalloc(sizeof(double) * (size_t)c->nnz);
         orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, c->col, c->val);
         double lam = orc_power(a->n, a->rowptr, a->col, a->val, cfg->power_iters, cfg->seed, l);
-        a->omega = 2.0 / (lam + cfg->lambda_min_est);
+        a->omega = 2.0 / (cfg->lambda_safety * lam + cfg->lambda_min_est);
         h->L = l + 2;
     }
     free(B);
@@ -773,8 +773,8 @@ static double dot(int32_t n, const double* a, const double* b) {
 }
 
 /* MGPCG (Alg. 1 l.8) with a fixed iteration count (reading c10), x_0 = 0.
- * Guards: alpha = 0 if p.q == 0; beta = 0 if the previous r.z == 0.  Returns -5 if <z,r> < 0 or
- * (<z,r> == 0 and r != 0) ever occurs, else 0. */
+ * Guards: alpha = 0 if p.q == 0; beta = 0 if the previous r.z == 0.  Returns the number of
+ * iterations with <z,r> < 0 or (<z,r> == 0 and r != 0) (indefinite preconditioner). */
 int orc_pcg(const orc_hier* h, const double* b, int32_t iters, double* x, double* rz_trace) {
     const orc_level* a = &h->lv[0];
     int32_t n = a->n;
@@ -789,7 +789,7 @@ int orc_pcg(const orc_hier* h, const double* b, int32_t iters, double* x, double
         orc_vcycle(h, r, z);
         double rz = dot(n, r, z);
         if (rz_trace) rz_trace[k] = rz;
-        if (rz < 0.0 || (rz == 0.0 && dot(n, r, r) > 0.0)) rc = -5;
+        if (rz < 0.0 || (rz == 0.0 && dot(n, r, r) > 0.0)) rc++;
         double beta = (k == 0 || rz_old == 0.0) ? 0.0 : rz / rz_old;
         for (int32_t i = 0; i < n; ++i) p[i] = z[i] + beta * p[i];
         orc_spmv(n, a->rowptr, a->col, a->val, p, q);
@@ -818,6 +818,7 @@ struct orc_sim {
     orc_config cfg;
     double b_norm[1024];
     int32_t n_b;
+    int32_t n_indef;  /* PCG iterations with <z,r> <= 0 (r != 0) in the last frame */
 };
 
 orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* verts,
@@ -859,9 +860,12 @@ orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* ver
 /* One frame (Algorithm 1).  Setup runs at ite 0 of frames with frame % setup_interval == 0, or
  * when marked stale (reading c13); Galerkin values are refreshed every iteration.
  * The outer break (l.12) is disabled: fixed n_iters (reading c11).  Collision (l.16) is out of
- * scope.  Returns 0, or -5 on PCG indefiniteness / non-SPD coarsest matrix. */
+ * scope.  A PCG iteration with <z,r> <= 0 (the lazily-set omega of PAPER.md:320 no longer below
+ * 2/lambda_max) is counted and marks the hierarchy stale, so setup re-runs at ite 0 of the next
+ * frame (reading c13).  Returns 0, or -5 if a coarsest matrix is not SPD. */
 int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
     int rc = 0;
+    s->n_indef = 0;
     int32_t n = s->n, m = s->m;
     /* l.1 semiEuler: x_old = x; v += dt g (w > 0); x = x~ = x + dt v;  l.2 lambda = 0 */
     for (int32_t v = 0; v < n; ++v)
@@ -885,18 +889,19 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
             s->stale = 0;
             if (factor_coarsest(s->h) != 0) rc = -5;
         } else if (orc_hier_refresh(s->h, s->val) != 0) rc = -5;
-        int prc = orc_pcg(s->h, s->b, s->cfg.pcg_iters, s->dl, NULL);                            /* l.8 */
-        if (prc) rc = prc;
+        s->n_indef += orc_pcg(s->h, s->b, s->cfg.pcg_iters, s->dl, NULL);                         /* l.8 */
         orc_apply_dx(m, s->kind, s->verts, n, s->w, s->g, s->dl, s->dx);                         /* l.9 */
         for (int32_t j = 0; j < m; ++j) s->lambda[j] += s->dl[j];                               /* l.10 */
         for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->x[k] += s->cfg.omega_relax * s->dx[k];  /* l.11 */
     }
     for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->v[k] = (s->x[k] - s->x_old[k]) / dt;      /* l.17 */
     s->frame++;
+    if (s->n_indef) s->stale = 1;
     return rc;
 }
 
 void orc_sim_mark_stale(orc_sim* s) { s->stale = 1; }
+int32_t orc_sim_indefinite_events(const orc_sim* s) { return s->n_indef; }
 void orc_sim_get(const orc_sim* s, double* x, double* v, double* lambda) {
     if (x) memcpy(x, s->x, sizeof(double) * 3 * (size_t)s->n);
     if (v) memcpy(v, s->v, sizeof(double) * 3 * (size_t)s->n);

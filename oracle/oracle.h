@@ -27,6 +27,7 @@ typedef struct {
     int32_t bootstrap_sweeps;/* 20 */
     int32_t power_iters;     /* 100 (reading c9) */
     double lambda_min_est;   /* 0.1 */
+    double lambda_safety;    /* omega = 2/(safety*lambda_max + lambda_min_est); 1.1 (reading c9) */
     int32_t smoother_sweeps; /* 2 */
     int32_t pcg_iters;       /* 10 (reading c10) */
     double omega_relax;      /* 0.1 tet / 0.25 cloth */
@@ -109,6 +110,7 @@ orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* ver
                         const double* inv_mass, const double* compliance, const orc_config* cfg);
 int orc_sim_step(orc_sim* s, double dt, int32_t n_iters);
 void orc_sim_mark_stale(orc_sim* s);
+int32_t orc_sim_indefinite_events(const orc_sim* s);
 void orc_sim_get(const orc_sim* s, double* x, double* v, double* lambda);
 void orc_sim_set(orc_sim* s, const double* x, const double* v);
 const orc_hier* orc_sim_hier(const orc_sim* s);

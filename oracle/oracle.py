@@ -25,7 +25,7 @@ class Config(C.Structure):
     _fields_ = [("theta", C.c_double), ("min_coarse", C.c_int32), ("max_levels", C.c_int32),
                 ("stall_ratio", C.c_double), ("setup_interval", C.c_int32),
                 ("bootstrap_sweeps", C.c_int32), ("power_iters", C.c_int32),
-                ("lambda_min_est", C.c_double), ("smoother_sweeps", C.c_int32),
+                ("lambda_min_est", C.c_double), ("lambda_safety", C.c_double), ("smoother_sweeps", C.c_int32),
                 ("pcg_iters", C.c_int32), ("omega_relax", C.c_double),
                 ("gravity", C.c_double * 3), ("seed", C.c_uint64)]
 
@@ -81,6 +81,7 @@ def lib():
             "orc_sim_create": (P, [C.c_int, i32, i32, P, P, P, P, P, P, P]),
             "orc_sim_step": (C.c_int, [P, f64, i32]),
             "orc_sim_mark_stale": (None, [P]),
+            "orc_sim_indefinite_events": (i32, [P]),
             "orc_sim_get": (None, [P, P, P, P]),
             "orc_sim_set": (None, [P, P, P]),
             "orc_sim_hier": (P, [P]),
@@ -400,6 +401,9 @@ class Sim:
 
     def mark_stale(self):
         lib().orc_sim_mark_stale(self.s)
+
+    def indefinite_events(self) -> int:
+        return int(lib().orc_sim_indefinite_events(self.s))
 
     def state(self):
         x = np.empty((self.n, 3)); v = np.empty((self.n, 3)); lam = np.empty(self.m)

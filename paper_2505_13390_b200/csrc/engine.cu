@@ -110,6 +110,7 @@ class Engine : public EngineBase {
     double l0_bytes_acc = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pairs;
     int64_t launches_last = 0;
+    int32_t indef_events = 0;
 
     Engine(const mgpbd_mesh* mesh, const mgpbd_constraints* cons, const double* inv_mass, const double* comp,
            const mgpbd_config* c) {
@@ -264,7 +265,7 @@ class Engine : public EngineBase {
             galerkin_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, a2.P64.p, na, c.rowptr, c.nnz,
                                      a2.tval64.p, c.val64.p, c.dinv64.p, st);
             double lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
-            a2.omega = 2.0 / (lam + cfg.lambda_min_est);
+            a2.omega = 2.0 / (cfg.lambda_safety * lam + cfg.lambda_min_est);
             B.swap(Bn);
             nL = l + 2;
         }
@@ -428,14 +429,17 @@ class Engine : public EngineBase {
             l0_ms = tot;
             l0_bytes = l0_bytes_acc;
         }
-        int hf[4];
-        d2h(hf, flags.p, 4, st);
+        int hf[6];
+        d2h(hf, flags.p, 6, st);
         MG_CK(cudaStreamSynchronize(st));
+        // <z,r> <= 0: the lazily-set omega is no longer below 2/lambda_max -> re-run the setup at ite 0
+        // of the next frame (reading c13); counted, not an error.
+        indef_events = hf[4];
+        if (indef_events) stale = true;
         if (hf[1]) throw Error(MGPBD_E_NONFINITE, "non-finite PCG scalar at (frame " + std::to_string(frame - 1) +
                                                       ", ite " + std::to_string(hf[3] / 4096) + ", pcg " +
                                                       std::to_string(hf[3] % 4096) + ")");
-        if (hf[0]) throw Error(MGPBD_E_INDEFINITE, "indefinite preconditioner or non-SPD coarsest at (frame " +
-                                                       std::to_string(frame - 1) + ", tag " + std::to_string(hf[2]) + ")");
+        if (hf[5]) throw Error(MGPBD_E_INDEFINITE, "non-SPD coarsest matrix in frame " + std::to_string(frame - 1));
     }
 
     void set_state(const double* pos, const double* vel) override {
@@ -469,6 +473,7 @@ class Engine : public EngineBase {
         s->ms_setup = ms_setup;
         s->ms_frame = ms_frame;
         s->kernel_launches = launches_last;
+        s->indefinite_events = indef_events;
     }
 
     void check_level(int l) {
@@ -586,6 +591,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->bootstrap_sweeps = 20;
     c->power_iters = 100;
     c->lambda_min_est = 0.1;
+    c->lambda_safety = 1.1;
     c->smoother_sweeps = 2;
     c->pcg_iters = 10;
     c->omega_relax = 0.1;

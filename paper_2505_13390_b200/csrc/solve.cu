@@ -165,6 +165,7 @@ __global__ void k_fin_rz(const double* __restrict__ prz, const double* __restric
             if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
         } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
             if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+            atomicAdd(&flags[4], 1);
         }
     }
 }
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(1024) k_coarse_inv(int32_t n, const int64_t* _
         if (threadIdx.x == 0) {
             double p = W[(int64_t)k * n + k];
             if (!(p > 0.0)) {
-                if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = -1;
+                flags[5] = 1;
                 p = (p == 0.0 || !isfinite(p)) ? 1.0 : p;
             }
             piv_s = p;

@@ -40,7 +40,8 @@ class Config(C.Structure):
     _fields_ = [("precision", C.c_int32), ("theta", C.c_double), ("k_nullspace", C.c_int32),
                 ("min_coarse", C.c_int32), ("max_levels", C.c_int32), ("stall_ratio", C.c_double),
                 ("setup_interval", C.c_int32), ("bootstrap_sweeps", C.c_int32), ("power_iters", C.c_int32),
-                ("lambda_min_est", C.c_double), ("smoother_sweeps", C.c_int32), ("pcg_iters", C.c_int32),
+                ("lambda_min_est", C.c_double), ("lambda_safety", C.c_double), ("smoother_sweeps", C.c_int32),
+                ("pcg_iters", C.c_int32),
                 ("omega_relax", C.c_double), ("gravity", C.c_double * 3), ("seed", C.c_uint64),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("max_dense_coarse", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32)]
@@ -52,7 +53,7 @@ class Stats(C.Structure):
                 ("setup_ran", C.c_int32), ("n_b", C.c_int32), ("b_norm", C.c_double * MAX_ITERS),
                 ("frame", C.c_int64), ("l0_pass_ms", C.c_double), ("l0_pass_launches", C.c_int64),
                 ("l0_pass_bytes", C.c_double), ("ms_setup", C.c_double), ("ms_frame", C.c_double),
-                ("kernel_launches", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("indefinite_events", C.c_int32)]
 
 
 _lib = None

@@ -177,6 +177,9 @@ def make(name: str) -> Scene:
     if name == "bar3k":          # 20x5x5 cells = 3000 tets (multi-level)
         return kuhn_block(20, 5, 5, 0.05, dt=10e-3, squash=1.0, twist_deg=90.0, n_iters=5,
                           name=name)
+    if name == "block_small":    # 24x12x6 cells = 10,368 tets: the block's deformation at desk size
+        return kuhn_block(24, 12, 6, 0.01, dt=3e-3, squash=0.7, twist_deg=45.0 * 24 / 136, n_iters=5,
+                          name=name)
     if name == "bar50k":         # 60x12x12 cells = 51,840 tets, 5:1:1 (bar twist PAPER.md:330)
         return kuhn_block(60, 12, 12, 1.0 / 60.0, dt=10e-3, squash=1.0, twist_deg=90.0,
                           n_iters=20, name=name)

@@ -10,7 +10,7 @@ from paper_2505_13390_b200 import mgpbd, scenes
 
 pytestmark = pytest.mark.gpu
 
-SMALL = ["cloth16", "bar_small", "bar3k", "cloth64"]
+SMALL = ["cloth16", "bar_small", "bar3k", "cloth64", "block_small"]
 
 
 def make_scene(name):
@@ -119,6 +119,24 @@ def test_frame_fp64(name):
     assert rel(vg, vo) <= 1e-6
     st = ctx.stats()
     assert np.allclose(st.b_norm[:sc.n_iters], sim.b_norms(sc.n_iters), rtol=1e-6)
+    assert st.indefinite_events == sim.indefinite_events()
+
+
+def test_bar3k_multiframe_indefinite_resetup_fp64():
+    """The bar-twist release drifts lambda_max(D^-1 A) past the lazily-set omega; both sides detect
+    <z,r> <= 0 identically and re-run the setup at the next frame (reading c13)."""
+    sc = scenes.make("bar3k")
+    ctx = ctx_for(sc)
+    sim = O.Sim(sc)
+    ev_g, ev_o, ran = [], [], []
+    for f in range(4):
+        ctx.step(sc.dt, 20)
+        sim.step(sc.dt, 20)
+        st = ctx.stats()
+        ev_g.append(st.indefinite_events); ev_o.append(sim.indefinite_events()); ran.append(st.setup_ran)
+    assert ev_g == ev_o
+    xo, _, lo = sim.state()
+    assert rel(ctx.lambdas(), lo) <= 1e-6 and rel(ctx.positions() - sc.pos, xo - sc.pos) <= 1e-6
 
 
 @pytest.mark.parametrize("name", SMALL)
