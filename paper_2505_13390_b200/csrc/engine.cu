@@ -1,5 +1,8 @@
 // Host orchestration of one MGPBD frame (Algorithm 1) and the extern "C" ABI of mgpbd.h.
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -65,17 +68,21 @@ class Engine : public EngineBase {
         double omega = 0.0;
         // V-cycle vectors
         DBuf<T> vb, vz, vx, vy, vt;
-        int vl = 32, grid = 1;
-        Csr<T> hot() const {
-            Csr<T> c;
-            c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = val.p; c.dinv = dinv.p; c.vl = vl; c.grid = grid;
+        int vl = 32, grid = 1, vlr = 0, tile_nnz = 0;
+        void configure(cudaStream_t s) {
+            vl = choose_vl(n, nnz);
+            tile_config(n, nnz, rowptr, vlr, grid, tile_nnz, s);
+            if (vlr == 0) grid = pass_grid(n, vl);
+        }
+        template <class U>
+        Csr<U> view(const U* v, const U* d) const {
+            Csr<U> c;
+            c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = v; c.dinv = d;
+            c.vl = vl; c.grid = grid; c.vlr = vlr; c.tile_nnz = tile_nnz;
             return c;
         }
-        Csr<double> setup_csr() const {
-            Csr<double> c;
-            c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = val64.p; c.dinv = dinv64.p; c.vl = vl; c.grid = grid;
-            return c;
-        }
+        Csr<T> hot() const { return view<T>(val.p, dinv.p); }
+        Csr<double> setup_csr() const { return view<double>(val64.p, dinv64.p); }
     };
 
     mgpbd_config cfg;
@@ -162,7 +169,7 @@ class Engine : public EngineBase {
         Level& l0 = *L[0];
         l0.n = m; l0.nnz = nnz0; l0.rowptr = rowptr0.p; l0.col = col0.p;
         l0.val.resize(nnz0); l0.dinv.resize(m);
-        l0.vl = choose_vl(m, nnz0); l0.grid = pass_grid(m, l0.vl);
+        l0.configure(st);
         alloc_vectors(l0);
         MG_CK(cudaStreamSynchronize(st));
     }
@@ -228,22 +235,27 @@ class Engine : public EngineBase {
         DBuf<double> B, Bn;
         const int maxl = std::min<int>(cfg.max_levels, MGPBD_MAX_LEVELS);
         pw_v.resize(m); pw_w.resize(m);
+        trace(nullptr);
         for (int l = 0; l + 1 < maxl; ++l) {
             Level& a = *L[l];
             if (a.n < cfg.min_coarse) break;
             DBuf<uint8_t> strong;
             strong.resize(a.nnz);
             soc(a.n, a.rowptr, a.col, a.val64.p, cfg.theta, strong.p, st);
+            trace("soc", l);
             a.agg.resize(a.n);
             int32_t na = aggregate(a.n, a.rowptr, a.col, a.val64.p, strong.p, cfg.seed, l, a.agg.p, st);
+            trace("aggregate", l);
             if ((double)na > cfg.stall_ratio * (double)a.n) break;
             if (l == 0) {
                 DBuf<int32_t> col_;
                 col_.resize(a.n);
                 ncolours = colour(a.n, a.rowptr, a.col, cfg.seed, col_.p, st);
+                trace("colour", l);
                 B.resize(a.n);
                 gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed, B.p, st);
                 d2d(B0.p, B.p, a.n, st);
+                trace("gs_bootstrap", l);
             }
             a.n_agg = na;
             DBuf<int32_t> cnt;
@@ -251,21 +263,25 @@ class Engine : public EngineBase {
             a.P64.resize(a.n);
             Bn.resize(na);
             prolongator(na, a.mptr.p, a.mlist.p, B.p, a.P64.p, Bn.p, st);
+            trace("members+prolongator", l);
             L.emplace_back(new Level());
             Level& c = *L[l + 1];
             Level& a2 = *L[l];  // re-bind after emplace (unique_ptr: stable)
             galerkin_symbolic(a2.n, a2.rowptr, a2.col, a2.agg.p, a2.mptr.p, a2.mlist.p, na, a2.plan, c.rowptr_own,
                               c.col_own, st);
+            trace("galerkin_symbolic", l);
             c.n = na;
             c.nnz = read_scalar(c.rowptr_own.p + na, st);
             c.rowptr = c.rowptr_own.p; c.col = c.col_own.p;
-            c.vl = choose_vl(c.n, c.nnz); c.grid = pass_grid(c.n, c.vl);
+            c.configure(st);
             c.val64.resize(c.nnz); c.dinv64.resize(c.n);
             a2.tval64.resize(a2.plan.T);
             galerkin_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, a2.P64.p, na, c.rowptr, c.nnz,
                                      a2.tval64.p, c.val64.p, c.dinv64.p, st);
+            trace("galerkin_numeric", l);
             double lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
             a2.omega = 2.0 / (cfg.lambda_safety * lam + cfg.lambda_min_est);
+            trace("power", l);
             B.swap(Bn);
             nL = l + 2;
         }
@@ -284,11 +300,25 @@ class Engine : public EngineBase {
             }
         }
         Ainv.resize((size_t)cl.n * cl.n);
-        inv_work.resize((size_t)cl.n * cl.n);
+        inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
         have_hier = true;
         stale = false;
         (void)l0;
         MG_CK(cudaStreamSynchronize(st));
+        trace("hot buffers");
+    }
+
+    // MGPBD_TRACE=1: host wall time of the setup phases (stream synchronised at every mark).
+    bool tracing = std::getenv("MGPBD_TRACE") != nullptr;
+    std::chrono::steady_clock::time_point tr0;
+    void trace(const char* what, int l = -1) {
+        if (!tracing) return;
+        MG_CK(cudaStreamSynchronize(st));
+        auto now = std::chrono::steady_clock::now();
+        if (what)
+            std::fprintf(stderr, "[mgpbd trace] %-22s l=%2d %10.2f ms\n", what, l,
+                         std::chrono::duration<double, std::milli>(now - tr0).count());
+        tr0 = now;
     }
 
     // Galerkin values of all coarse levels from the current level-0 values + coarsest inverse.

@@ -69,6 +69,106 @@ __global__ void __launch_bounds__(PB) k_pass(int32_t n, const int64_t* __restric
     }
 }
 
+// Row-tile CSR pass: a CTA takes R = 256/VLR consecutive rows (a contiguous nnz range), streams
+// val/col/x[col] for the whole tile with coalesced, independent loads (many in flight per thread),
+// keeps the fp64 products in shared memory, then VLR lanes per row reduce them in fixed order.
+template <class T, int VLR, int MODE>
+__global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restrict__ rowptr,
+                                             const int32_t* __restrict__ col, const T* __restrict__ val,
+                                             const T* __restrict__ dinv, const T* __restrict__ x,
+                                             const T* __restrict__ b, T* __restrict__ y,
+                                             const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                             double* __restrict__ parts2) {
+    extern __shared__ double prod[];
+    constexpr int R = PB / VLR;
+    const int rr = threadIdx.x / VLR, ln = threadIdx.x % VLR;
+    const int64_t ntiles = ((int64_t)n + R - 1) / R;
+    double acc1 = 0.0, acc2 = 0.0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t r0 = tile * R;
+        const int64_t r1 = r0 + R < n ? r0 + R : n;
+        const int64_t e0 = rowptr[r0];
+        const int ne = (int)(rowptr[r1] - e0);
+        const T* __restrict__ vt = val + e0;
+        const int32_t* __restrict__ ct = col + e0;
+#pragma unroll 4
+        for (int k = threadIdx.x; k < ne; k += PB) prod[k] = (double)vt[k] * (double)x[ct[k]];
+        __syncthreads();
+        const int64_t i = r0 + rr;
+        double s = 0.0;
+        if (i < r1) {
+            const int a = (int)(rowptr[i] - e0), z = (int)(rowptr[i + 1] - e0);
+            for (int k = a + ln; k < z; k += VLR) s += prod[k];
+        }
+        s = group_sum<VLR>(s);
+        if (ln == 0 && i < r1) {
+            if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
+                T yi = (T)((double)x[i] + omega * (double)dinv[i] * ((double)b[i] - s));
+                y[i] = yi;
+                if (MODE == PASS_JACOBI_DOT) {
+                    double r = (double)aux[i];
+                    acc1 += r * (double)yi;
+                    acc2 += r * r;
+                }
+            } else if (MODE == PASS_RESID_P) {
+                y[i] = (T)((double)aux[i] * ((double)b[i] - s));
+            } else if (MODE == PASS_SPMV_DOT) {
+                T yi = (T)s;
+                y[i] = yi;
+                acc1 += (double)x[i] * (double)yi;
+            } else if (MODE == PASS_POWER) {
+                T yi = (T)((double)dinv[i] * s);
+                y[i] = yi;
+                acc1 += (double)yi * (double)yi;
+            }
+        }
+        __syncthreads();
+    }
+    if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
+        __shared__ double sh[32];
+        double t1 = block_sum<PB>(acc1, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t1;
+        if (MODE == PASS_JACOBI_DOT) {
+            double t2 = block_sum<PB>(acc2, sh);
+            if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
+        }
+    }
+}
+
+template <class T, int MODE, int VLR>
+void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                 double* parts2, cudaStream_t s) {
+    static bool attr_set = false;
+    const size_t smem = (size_t)A.tile_nnz * sizeof(double);
+    if (smem > 48 * 1024 && !attr_set) {
+        MG_CK(cudaFuncSetAttribute(k_tile<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
+    MG_LAUNCH_CHECK();
+}
+
+template <class T, int MODE>
+void launch_tile_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                      double* parts2, cudaStream_t s) {
+    switch (A.vlr) {
+        case 1: launch_tile<T, MODE, 1>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 2: launch_tile<T, MODE, 2>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 4: launch_tile<T, MODE, 4>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 8: launch_tile<T, MODE, 8>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 16: launch_tile<T, MODE, 16>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        default: launch_tile<T, MODE, 32>(A, x, b, y, aux, omega, parts, parts2, s); break;
+    }
+}
+
+__global__ void k_max_tile(int32_t n, int R, const int64_t* __restrict__ rowptr, int32_t* out) {
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t r0 = t * R;
+    if (r0 >= n) return;
+    int64_t r1 = r0 + R < n ? r0 + R : n;
+    atomicMax(out, (int32_t)(rowptr[r1] - rowptr[r0]));
+}
+
 template <class T, int MODE>
 void launch_pass_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                       double* parts2, cudaStream_t s) {
@@ -225,6 +325,110 @@ __global__ void __launch_bounds__(1024) k_coarse_inv(int32_t n, const int64_t* _
     for (int64_t k = threadIdx.x; k < nn; k += blockDim.x) Ainv[k] = W[k];
 }
 
+// ---- blocked Gauss-Jordan (block size GJB) for coarsest levels too large for one CTA's smem.
+// Step k (block K = [k0, k0+bs)): P = W_KK^-1; R = P W_K,: ; C = W_:,K (old);
+// W_ij -= C_i R_j (i,j not in K); W_Kj = R_j; W_iK = -C_i P; W_KK = P.  SPD => no pivoting.
+constexpr int GJB = 32;
+
+template <class T>
+__global__ void k_dense_load(int32_t n, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                             const T* __restrict__ val, double* __restrict__ W) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = gw; i < n; i += nw) {
+        for (int32_t j = lane; j < n; j += 32) W[i * n + j] = 0.0;
+        __syncwarp();
+        for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) W[i * n + col[e]] = (double)val[e];
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_gj_diag(int32_t n, const double* __restrict__ W, int32_t k0, int32_t bs,
+                                                  double* __restrict__ P, int* flags) {
+    __shared__ double S[GJB * GJB];
+    __shared__ double piv;
+    const int t = threadIdx.x;
+    if (t < bs * bs) S[t] = W[(int64_t)(k0 + t / bs) * n + k0 + t % bs];
+    __syncthreads();
+    for (int k = 0; k < bs; ++k) {
+        if (t == 0) {
+            double p = S[k * bs + k];
+            if (!(p > 0.0)) { flags[5] = 1; p = (p == 0.0 || !isfinite(p)) ? 1.0 : p; }
+            piv = p;
+        }
+        __syncthreads();
+        const double ip = 1.0 / piv;
+        double upd = 0.0;
+        const int i = t / bs, j = t % bs;
+        if (t < bs * bs && i != k && j != k) upd = S[i * bs + j] - S[i * bs + k] * S[k * bs + j] * ip;
+        __syncthreads();
+        if (t < bs * bs) {
+            if (i != k && j != k) S[t] = upd;
+            else if (i == k && j != k) S[t] = S[t] * ip;
+            else if (i != k && j == k) S[t] = -S[t] * ip;
+            else S[t] = ip;
+        }
+        __syncthreads();
+    }
+    if (t < bs * bs) P[t] = S[t];
+}
+
+// R[t][j] = sum_s P[t][s] W[k0+s][j] (j not in K);  C[i][t] = W[i][k0+t] (i not in K)
+__global__ void k_gj_panel(int32_t n, const double* __restrict__ W, int32_t k0, int32_t bs, const double* __restrict__ P,
+                           double* __restrict__ C, double* __restrict__ R) {
+    const int64_t tot = (int64_t)n * bs;
+    for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < 2 * tot; q += (int64_t)gridDim.x * blockDim.x) {
+        if (q < tot) {
+            const int32_t t = (int32_t)(q / n), j = (int32_t)(q % n);
+            if (j >= k0 && j < k0 + bs) continue;
+            double s = 0.0;
+            for (int u = 0; u < bs; ++u) s += P[t * bs + u] * W[(int64_t)(k0 + u) * n + j];
+            R[(int64_t)t * n + j] = s;
+        } else {
+            const int64_t q2 = q - tot;
+            const int32_t i = (int32_t)(q2 / bs), t = (int32_t)(q2 % bs);
+            if (i >= k0 && i < k0 + bs) continue;
+            C[(int64_t)i * bs + t] = W[(int64_t)i * n + k0 + t];
+        }
+    }
+}
+
+// 32x32 output tile per CTA (32x8 threads, 4 outputs each)
+__global__ void __launch_bounds__(256) k_gj_update(int32_t n, double* __restrict__ W, int32_t k0, int32_t bs,
+                                                   const double* __restrict__ P, const double* __restrict__ C,
+                                                   const double* __restrict__ R) {
+    __shared__ double Cs[32][GJB + 1];
+    __shared__ double Rs[GJB][32 + 1];
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int32_t i0 = blockIdx.y * 32, j0 = blockIdx.x * 32;
+    for (int r = ty; r < 32; r += 8) {
+        const int32_t i = i0 + r;
+        Cs[r][tx] = (i < n && tx < bs && !(i >= k0 && i < k0 + bs)) ? C[(int64_t)i * bs + tx] : 0.0;
+        const int32_t j = j0 + tx;
+        if (r < bs) Rs[r][tx] = (j < n && !(j >= k0 && j < k0 + bs)) ? R[(int64_t)r * n + j] : 0.0;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const int32_t i = i0 + r, j = j0 + tx;
+        if (i >= n || j >= n) continue;
+        const bool iK = i >= k0 && i < k0 + bs, jK = j >= k0 && j < k0 + bs;
+        double* w = &W[(int64_t)i * n + j];
+        if (!iK && !jK) {
+            double s = 0.0;
+            for (int t = 0; t < bs; ++t) s += Cs[r][t] * Rs[t][tx];
+            *w -= s;
+        } else if (iK && !jK) {
+            *w = R[(int64_t)(i - k0) * n + j];
+        } else if (!iK && jK) {
+            double s = 0.0;
+            for (int t = 0; t < bs; ++t) s += Cs[r][t] * P[t * bs + (j - k0)];
+            *w = -s;
+        } else {
+            *w = P[(i - k0) * bs + (j - k0)];
+        }
+    }
+}
+
 template <class T>
 __global__ void k_coarse_gemv(int32_t n, const double* __restrict__ Ainv, const T* __restrict__ b, T* __restrict__ x) {
     const int lane = threadIdx.x & 31;
@@ -240,6 +444,28 @@ __global__ void k_coarse_gemv(int32_t n, const double* __restrict__ Ainv, const 
 
 }  // namespace
 
+void tile_config(int32_t n, int64_t nnz, const int64_t* rowptr, int& vlr, int& grid, int& tile_nnz, cudaStream_t s) {
+    const double avg = n ? (double)nnz / n : 1.0;
+    vlr = 1;
+    while (vlr < 32 && vlr * 2 <= avg / 8.0) vlr *= 2;
+    const int R = PB / vlr;
+    const int64_t ntiles = ((int64_t)n + R - 1) / R;
+    grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, 148 * 8));
+    int32_t* d;
+    MG_CK(cudaMallocAsync(&d, sizeof(int32_t), s));
+    MG_CK(cudaMemsetAsync(d, 0, sizeof(int32_t), s));
+    if (n) {
+        k_max_tile<<<(int)((ntiles + 255) / 256), 256, 0, s>>>(n, R, rowptr, d);
+        MG_LAUNCH_CHECK();
+    }
+    int32_t h = 0;
+    MG_CK(cudaMemcpyAsync(&h, d, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    MG_CK(cudaFreeAsync(d, s));
+    MG_CK(cudaStreamSynchronize(s));
+    tile_nnz = std::max(1, h);
+    if ((size_t)tile_nnz * sizeof(double) > 200 * 1024) vlr = 0;  // fall back to the warp-per-row kernel
+}
+
 int pass_grid(int32_t n, int vl) {
     int rows_per_block = PB / vl;
     int64_t g = ((int64_t)n + rows_per_block - 1) / rows_per_block;
@@ -251,6 +477,17 @@ template <class T>
 void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
               double* parts2, cudaStream_t s) {
     if (A.n == 0) return;
+    if (A.vlr > 0) {
+        switch (mode) {
+            case PASS_JACOBI: launch_tile_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_JACOBI_DOT: launch_tile_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_RESID_P: launch_tile_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_SPMV_DOT: launch_tile_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_POWER: launch_tile_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            default: throw Error(-1, "bad pass mode");
+        }
+        return;
+    }
     switch (mode) {
         case PASS_JACOBI: launch_pass_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
         case PASS_JACOBI_DOT: launch_pass_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
@@ -314,13 +551,33 @@ void pcg_finalize_pq(const double* p, int np, double* scal, int k, int* flags, i
 }
 template <class T>
 void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cudaStream_t s) {
-    size_t bytes = (size_t)A.n * A.n * sizeof(double);
-    int use_smem = bytes <= 160 * 1024;
-    size_t smem = use_smem ? bytes : 0;
-    if (smem > 48 * 1024)
-        MG_CK(cudaFuncSetAttribute(k_coarse_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_coarse_inv<T><<<1, 1024, smem, s>>>(A.n, A.rowptr, A.col, A.val, work, Ainv, flags, use_smem);
+    const int32_t n = A.n;
+    size_t bytes = (size_t)n * n * sizeof(double);
+    if (bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
+        if (bytes > 48 * 1024)
+            MG_CK(cudaFuncSetAttribute(k_coarse_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        k_coarse_inv<T><<<1, 1024, bytes, s>>>(n, A.rowptr, A.col, A.val, work, Ainv, flags, 1);
+        MG_LAUNCH_CHECK();
+        return;
+    }
+    // blocked Gauss-Jordan in place on Ainv; work holds P (GJB^2), C (n*GJB), R (GJB*n)
+    double* P = work;
+    double* Cb = work + GJB * GJB;
+    double* Rb = Cb + (size_t)n * GJB;
+    k_dense_load<T><<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, 148 * 8), 256, 0, s>>>(n, A.rowptr, A.col,
+                                                                                                   A.val, Ainv);
     MG_LAUNCH_CHECK();
+    const dim3 ug((n + 31) / 32, (n + 31) / 32);
+    for (int32_t k0 = 0; k0 < n; k0 += GJB) {
+        const int32_t bs = std::min<int32_t>(GJB, n - k0);
+        k_gj_diag<<<1, 1024, 0, s>>>(n, Ainv, k0, bs, P, flags);
+        MG_LAUNCH_CHECK();
+        k_gj_panel<<<(int)std::min<int64_t>((2 * (int64_t)n * bs + 255) / 256, 148 * 8), 256, 0, s>>>(n, Ainv, k0, bs, P,
+                                                                                                   Cb, Rb);
+        MG_LAUNCH_CHECK();
+        k_gj_update<<<ug, 256, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
+        MG_LAUNCH_CHECK();
+    }
 }
 template <class T>
 void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s) {

@@ -14,9 +14,15 @@ struct Csr {
     const int32_t* col = nullptr;
     const T* val = nullptr;
     const T* dinv = nullptr;
-    int vl = 32;     // lanes per row
+    int vl = 32;     // lanes per row (warp-per-row kernel)
     int grid = 1;    // fixed grid (=> fixed partial count => deterministic reductions)
+    int vlr = 0;     // > 0: row-tile kernel with 256/vlr rows per tile and vlr reduce lanes per row
+    int tile_nnz = 0;  // max nnz of a tile (shared-memory products)
 };
+
+// Choose the row-tile configuration of a level (vlr, fixed grid, max tile nnz); vlr = 0 if the tile
+// would not fit in shared memory.
+void tile_config(int32_t n, int64_t nnz, const int64_t* rowptr, int& vlr, int& grid, int& tile_nnz, cudaStream_t s);
 
 enum PassMode {
     PASS_JACOBI = 0,      // y = x + omega dinv (b - A x)
