@@ -69,16 +69,27 @@ class Engine : public EngineBase {
         // V-cycle vectors
         DBuf<T> vb, vz, vx, vy, vt;
         int vl = 32, grid = 1, vlr = 0, tile_nnz = 0;
+        int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0;
+        DBuf<int32_t> win_lo, win_len;
         void configure(cudaStream_t s) {
             vl = choose_vl(n, nnz);
             tile_config(n, nnz, rowptr, vlr, grid, tile_nnz, s);
             if (vlr == 0) grid = pass_grid(n, vl);
+            band_rows = 0;
+            if (!std::getenv("MGPBD_NO_BAND"))
+                band_config<T>(n, rowptr, col, vlr, win_lo, win_len, band_rows, band_grid, prod_cap, band_win, s);
         }
         template <class U>
         Csr<U> view(const U* v, const U* d) const {
             Csr<U> c;
             c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = v; c.dinv = d;
             c.vl = vl; c.grid = grid; c.vlr = vlr; c.tile_nnz = tile_nnz;
+            c.nparts = grid;
+            if (std::is_same<U, T>::value && band_rows) {
+                c.band_rows = band_rows; c.band_grid = band_grid; c.prod_cap = prod_cap; c.band_win = band_win;
+                c.win_lo = win_lo.p; c.win_len = win_len.p;
+                c.nparts = band_grid;
+            }
             return c;
         }
         Csr<T> hot() const { return view<T>(val.p, dinv.p); }
@@ -379,10 +390,10 @@ class Engine : public EngineBase {
             } else {
                 vcycle(0, r.p, z, r.p);
             }
-            pcg_finalize_rz(parts1.p, parts2.p, l0.grid, scal.p, k, flags.p, tag, st);
+            pcg_finalize_rz(parts1.p, parts2.p, l0.hot().nparts, scal.p, k, flags.p, tag, st);
             pcg_update_p<T>(m, z, p.p, scal.p, k, st);
             l0_pass(PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
-            pcg_finalize_pq(parts1.p, l0.grid, scal.p, k, flags.p, tag, st);
+            pcg_finalize_pq(parts1.p, l0.hot().nparts, scal.p, k, flags.p, tag, st);
             pcg_update_xr<T>(m, p.p, q.p, xs.p, r.p, scal.p, k, st);
         }
     }

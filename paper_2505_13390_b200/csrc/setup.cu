@@ -621,7 +621,7 @@ double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int leve
     scale_by_inv_sqrt<double>(n, v, v, ss, s);
     for (int it = 0; it < iters; ++it) {
         csr_pass<double>(PASS_POWER, A, v, nullptr, w, nullptr, 0.0, parts, nullptr, s);
-        finalize_sum(parts, A.grid, ss, s);
+        finalize_sum(parts, A.nparts, ss, s);
         scale_by_inv_sqrt<double>(n, w, v, ss, s);
     }
     double lam2 = read_scalar(ss, s);

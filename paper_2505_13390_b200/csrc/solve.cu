@@ -1,6 +1,10 @@
 // Hot-loop kernels of the MGPCG solve (see solve.cuh).
 #include "solve.cuh"
 
+#include <cstdint>
+
+#include "util.cuh"
+
 namespace mgpbd {
 namespace {
 
@@ -133,6 +137,141 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restric
             if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
         }
     }
+}
+
+// Band-staged row-tile pass (level 0 of mesh-ordered matrices).  One 1024-thread CTA per SM walks
+// "band tiles" of C consecutive rows; for each it stages the window x[lo, lo+len) that those rows
+// touch into shared memory (one coalesced copy), then processes sub-tiles of 1024/VLR rows: stream
+// val/col with independent coalesced loads, gather x from the shared window (no L1 line fan-out),
+// products (PT = T) into shared memory, fixed-order VLR-lane row reductions.  The epilogue's per-row
+// loads are issued before the stream so their latency overlaps it.
+constexpr int BB = 1024;
+template <class T, int VLR, int MODE>
+__global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
+                                                const int32_t* __restrict__ win_len, int prod_cap,
+                                                const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                                const T* __restrict__ val, const T* __restrict__ dinv,
+                                                const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
+                                                const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                                double* __restrict__ parts2) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* prod = reinterpret_cast<T*>(smraw);
+    T* xs = prod + prod_cap;
+    constexpr int R = BB / VLR;
+    const int rr = threadIdx.x / VLR, ln = threadIdx.x % VLR;
+    const int32_t nband = (n + C - 1) / C;
+    double acc1 = 0.0, acc2 = 0.0;
+    for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
+        const int32_t lo = win_lo[bt], len = win_len[bt];
+        const int32_t c0 = bt * C, c1 = c0 + C < n ? c0 + C : n;
+        __syncthreads();
+        for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
+        __syncthreads();
+        for (int32_t r0 = c0; r0 < c1; r0 += R) {
+            const int32_t r1 = r0 + R < c1 ? r0 + R : c1;
+            const int32_t i = r0 + rr;
+            const bool own = i < r1;
+            // per-row operands first: their latency overlaps the stream below
+            int64_t ra = 0, rz = 0;
+            double bi = 0.0, di = 0.0, ai = 0.0;
+            if (own) {
+                ra = rowptr[i];
+                rz = rowptr[i + 1];
+                if (ln == 0) {
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) bi = (double)b[i];
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) di = (double)dinv[i];
+                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) ai = (double)aux[i];
+                }
+            }
+            const int64_t e0 = rowptr[r0];
+            const int ne = (int)(rowptr[r1] - e0);
+            const T* __restrict__ vt = val + e0;
+            const int32_t* __restrict__ ct = col + e0;
+#pragma unroll 4
+            for (int k = threadIdx.x; k < ne; k += BB) prod[k] = (T)((double)vt[k] * (double)xs[ct[k] - lo]);
+            __syncthreads();
+            double s = 0.0;
+            if (own)
+                for (int k = (int)(ra - e0) + ln; k < (int)(rz - e0); k += VLR) s += (double)prod[k];
+            s = group_sum<VLR>(s);
+            if (own && ln == 0) {
+                if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
+                    T yi = (T)((double)xs[i - lo] + omega * di * (bi - s));
+                    y[i] = yi;
+                    if (MODE == PASS_JACOBI_DOT) { acc1 += ai * (double)yi; acc2 += ai * ai; }
+                } else if (MODE == PASS_RESID_P) {
+                    y[i] = (T)(ai * (bi - s));
+                } else if (MODE == PASS_SPMV_DOT) {
+                    T yi = (T)s;
+                    y[i] = yi;
+                    acc1 += (double)xs[i - lo] * (double)yi;
+                } else if (MODE == PASS_POWER) {
+                    T yi = (T)(di * s);
+                    y[i] = yi;
+                    acc1 += (double)yi * (double)yi;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
+        __shared__ double sh[32];
+        double t1 = block_sum<BB>(acc1, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t1;
+        if (MODE == PASS_JACOBI_DOT) {
+            double t2 = block_sum<BB>(acc2, sh);
+            if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
+        }
+    }
+}
+
+template <class T, int MODE, int VLR>
+void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                 double* parts2, cudaStream_t s) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        MG_CK(cudaFuncSetAttribute(k_band<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr_set = true;
+    }
+    const size_t smem = ((size_t)A.prod_cap + A.band_win) * sizeof(T);
+    k_band<T, VLR, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.prod_cap, A.rowptr,
+                                                      A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
+    MG_LAUNCH_CHECK();
+}
+
+template <class T, int MODE>
+void launch_band_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                      double* parts2, cudaStream_t s) {
+    switch (A.vlr) {
+        case 1: launch_band<T, MODE, 1>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 2: launch_band<T, MODE, 2>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 4: launch_band<T, MODE, 4>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 8: launch_band<T, MODE, 8>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 16: launch_band<T, MODE, 16>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        default: launch_band<T, MODE, 32>(A, x, b, y, aux, omega, parts, parts2, s); break;
+    }
+}
+
+// per band tile: the column window [min col, max col] of its rows (diagonal-last CSR)
+__global__ void k_band_windows(int32_t n, int32_t C, const int64_t* __restrict__ rowptr,
+                               const int32_t* __restrict__ col, int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t a = rowptr[i], z = rowptr[i + 1];
+    int32_t mn = i, mx = i;
+    if (z - a > 1) {
+        mn = min(mn, col[a]);
+        mx = max(mx, col[z - 2]);
+    }
+    atomicMin(&lo[i / C], mn);
+    atomicMax(&hi[i / C], mx);
+}
+__global__ void k_band_len(int32_t nb, int32_t* __restrict__ lo, const int32_t* __restrict__ hi, int32_t* len,
+                           int32_t* maxlen) {
+    int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nb) return;
+    len[t] = hi[t] - lo[t] + 1;
+    atomicMax(maxlen, len[t]);
 }
 
 template <class T, int MODE, int VLR>
@@ -466,6 +605,58 @@ void tile_config(int32_t n, int64_t nnz, const int64_t* rowptr, int& vlr, int& g
     if ((size_t)tile_nnz * sizeof(double) > 200 * 1024) vlr = 0;  // fall back to the warp-per-row kernel
 }
 
+namespace {
+__global__ void k_rowlen_max2(int32_t n, const int64_t* __restrict__ rowptr, int32_t* out) {
+    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) atomicMax(out, (int32_t)(rowptr[i + 1] - rowptr[i]));
+}
+}  // namespace
+
+template <class T>
+bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
+                 int& C, int& grid, int& prod_cap, int& win, cudaStream_t s) {
+    C = 0;
+    if (n < 4096 || vlr <= 0) return false;
+    DBuf<int32_t> tmp, hi;
+    tmp.resize(2);
+    MG_CK(cudaMemsetAsync(tmp.p, 0, 2 * sizeof(int32_t), s));
+    k_rowlen_max2<<<ceil_div(n, 256), 256, 0, s>>>(n, rowptr, tmp.p);
+    MG_LAUNCH_CHECK();
+    int32_t maxrow = 0;
+    MG_CK(cudaMemcpyAsync(&maxrow, tmp.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    MG_CK(cudaStreamSynchronize(s));
+    const int R = BB / vlr;
+    prod_cap = R * maxrow;
+    const size_t budget = 227 * 1024 - 1024;
+    if ((size_t)prod_cap * sizeof(T) >= budget) return false;
+    for (int32_t c = ((n + 147) / 148 + R - 1) / R * R; c >= R; c = (c / 2 + R - 1) / R * R) {
+        const int32_t nb = (n + c - 1) / c;
+        lo.resize(nb); hi.resize(nb); len.resize(nb);
+        fill_i32(lo.p, INT32_MAX, nb, s);
+        fill_i32(hi.p, -1, nb, s);
+        k_band_windows<<<ceil_div(n, 256), 256, 0, s>>>(n, c, rowptr, col, lo.p, hi.p);
+        MG_LAUNCH_CHECK();
+        MG_CK(cudaMemsetAsync(tmp.p + 1, 0, sizeof(int32_t), s));
+        k_band_len<<<ceil_div(nb, 256), 256, 0, s>>>(nb, lo.p, hi.p, len.p, tmp.p + 1);
+        MG_LAUNCH_CHECK();
+        int32_t mw = 0;
+        MG_CK(cudaMemcpyAsync(&mw, tmp.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        MG_CK(cudaStreamSynchronize(s));
+        if ((size_t)(prod_cap + mw) * sizeof(T) <= budget) {
+            C = c;
+            win = mw;
+            grid = nb < 148 ? nb : 148;
+            return true;
+        }
+        if (c == R) break;
+    }
+    return false;
+}
+template bool band_config<float>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
+                                 int&, int&, int&, cudaStream_t);
+template bool band_config<double>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
+                                  int&, int&, int&, cudaStream_t);
+
 int pass_grid(int32_t n, int vl) {
     int rows_per_block = PB / vl;
     int64_t g = ((int64_t)n + rows_per_block - 1) / rows_per_block;
@@ -477,6 +668,17 @@ template <class T>
 void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
               double* parts2, cudaStream_t s) {
     if (A.n == 0) return;
+    if (A.band_rows > 0) {
+        switch (mode) {
+            case PASS_JACOBI: launch_band_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_JACOBI_DOT: launch_band_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_RESID_P: launch_band_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_SPMV_DOT: launch_band_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_POWER: launch_band_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            default: throw Error(-1, "bad pass mode");
+        }
+        return;
+    }
     if (A.vlr > 0) {
         switch (mode) {
             case PASS_JACOBI: launch_tile_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;

@@ -16,9 +16,20 @@ struct Csr {
     const T* dinv = nullptr;
     int vl = 32;     // lanes per row (warp-per-row kernel)
     int grid = 1;    // fixed grid (=> fixed partial count => deterministic reductions)
+    int nparts = 1;  // number of per-CTA partials a dot-producing pass writes
     int vlr = 0;     // > 0: row-tile kernel with 256/vlr rows per tile and vlr reduce lanes per row
     int tile_nnz = 0;  // max nnz of a tile (shared-memory products)
+    // band-staged kernel (band_rows > 0): band tiles of band_rows rows, x window per band tile
+    int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0;
+    const int32_t* win_lo = nullptr;
+    const int32_t* win_len = nullptr;
 };
+
+// Band configuration for the band-staged pass: returns false (and C = 0) if the column window of even
+// the smallest band tile does not fit in shared memory next to the product buffer.
+template <class T>
+bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
+                 int& C, int& grid, int& prod_cap, int& win, cudaStream_t s);
 
 // Choose the row-tile configuration of a level (vlr, fixed grid, max tile nnz); vlr = 0 if the tile
 // would not fit in shared memory.
