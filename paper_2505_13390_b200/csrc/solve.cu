@@ -228,12 +228,12 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
 template <class T, int MODE, int VLR>
 void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                  double* parts2, cudaStream_t s) {
-    static bool attr_set = false;
-    if (!attr_set) {
-        MG_CK(cudaFuncSetAttribute(k_band<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr_set = true;
-    }
+    static size_t attr_set = 48 * 1024;
     const size_t smem = ((size_t)A.prod_cap + A.band_win) * sizeof(T);
+    if (smem > attr_set) {
+        MG_CK(cudaFuncSetAttribute(k_band<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = smem;
+    }
     k_band<T, VLR, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.prod_cap, A.rowptr,
                                                       A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
     MG_LAUNCH_CHECK();
@@ -277,11 +277,11 @@ __global__ void k_band_len(int32_t nb, int32_t* __restrict__ lo, const int32_t* 
 template <class T, int MODE, int VLR>
 void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                  double* parts2, cudaStream_t s) {
-    static bool attr_set = false;
+    static size_t attr_set = 48 * 1024;
     const size_t smem = (size_t)A.tile_nnz * sizeof(double);
-    if (smem > 48 * 1024 && !attr_set) {
-        MG_CK(cudaFuncSetAttribute(k_tile<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        attr_set = true;
+    if (smem > attr_set) {
+        MG_CK(cudaFuncSetAttribute(k_tile<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = smem;
     }
     k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
     MG_LAUNCH_CHECK();
@@ -627,7 +627,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     MG_CK(cudaStreamSynchronize(s));
     const int R = BB / vlr;
     prod_cap = R * maxrow;
-    const size_t budget = 227 * 1024 - 1024;
+    const size_t budget = 227 * 1024 - 2048;  // leave room for the kernel's static shared memory
     if ((size_t)prod_cap * sizeof(T) >= budget) return false;
     for (int32_t c = ((n + 147) / 148 + R - 1) / R * R; c >= R; c = (c / 2 + R - 1) / R * R) {
         const int32_t nb = (n + c - 1) / c;
