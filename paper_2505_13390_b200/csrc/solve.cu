@@ -146,6 +146,7 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restric
 // products (PT = T) into shared memory, fixed-order VLR-lane row reductions.  The epilogue's per-row
 // loads are issued before the stream so their latency overlaps it.
 constexpr int BB = 1024;
+constexpr int BAND_EPT = 12;  // stream elements per thread per sub-tile (sub-tile nnz <= BAND_EPT*BB)
 template <class T, int VLR, int MODE>
 __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
                                                 const int32_t* __restrict__ win_len, int prod_cap,
@@ -167,28 +168,52 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
         __syncthreads();
         for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
         __syncthreads();
-        for (int32_t r0 = c0; r0 < c1; r0 += R) {
-            const int32_t r1 = r0 + R < c1 ? r0 + R : c1;
+        // software pipeline: the next sub-tile's stream and row operands are loaded into registers
+        // while the current sub-tile is reduced (one CTA per SM, so nothing else hides the latency)
+        T pv[BAND_EPT];
+        int32_t pc[BAND_EPT];
+        int32_t nr0 = c0, nr1 = 0;
+        int64_t ne0 = 0, nra = 0, nrz = 0;
+        int nne = 0;
+        double nbi = 0.0, ndi = 0.0, nai = 0.0;
+        auto fetch = [&](int32_t r0) {
+            nr0 = r0;
+            nr1 = r0 + R < c1 ? r0 + R : c1;
+            ne0 = rowptr[r0];
+            nne = (int)(rowptr[nr1] - ne0);
+#pragma unroll
+            for (int j = 0; j < BAND_EPT; ++j) {
+                const int idx = threadIdx.x + j * BB;
+                const bool in = idx < nne;
+                pv[j] = in ? val[ne0 + idx] : (T)0;
+                pc[j] = in ? col[ne0 + idx] : lo;
+            }
             const int32_t i = r0 + rr;
-            const bool own = i < r1;
-            // per-row operands first: their latency overlaps the stream below
-            int64_t ra = 0, rz = 0;
-            double bi = 0.0, di = 0.0, ai = 0.0;
-            if (own) {
-                ra = rowptr[i];
-                rz = rowptr[i + 1];
+            if (i < nr1) {
+                nra = rowptr[i];
+                nrz = rowptr[i + 1];
                 if (ln == 0) {
-                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) bi = (double)b[i];
-                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) di = (double)dinv[i];
-                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) ai = (double)aux[i];
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) nbi = (double)b[i];
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) ndi = (double)dinv[i];
+                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) nai = (double)aux[i];
                 }
             }
-            const int64_t e0 = rowptr[r0];
-            const int ne = (int)(rowptr[r1] - e0);
-            const T* __restrict__ vt = val + e0;
-            const int32_t* __restrict__ ct = col + e0;
-#pragma unroll 4
-            for (int k = threadIdx.x; k < ne; k += BB) prod[k] = (T)((double)vt[k] * (double)xs[ct[k] - lo]);
+        };
+        fetch(c0);
+        while (nr0 < c1) {
+            const int32_t r0 = nr0, r1 = nr1;
+            const int64_t e0 = ne0, ra = nra, rz = nrz;
+            const int ne = nne;
+            const double bi = nbi, di = ndi, ai = nai;
+            const int32_t i = r0 + rr;
+            const bool own = i < r1;
+#pragma unroll
+            for (int j = 0; j < BAND_EPT; ++j) {
+                const int idx = threadIdx.x + j * BB;
+                if (idx < ne) prod[idx] = (T)((double)pv[j] * (double)xs[pc[j] - lo]);
+            }
+            if (r0 + R < c1) fetch(r0 + R);
+            else nr0 = c1;
             __syncthreads();
             double s = 0.0;
             if (own)
@@ -628,7 +653,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     const int R = BB / vlr;
     prod_cap = R * maxrow;
     const size_t budget = 227 * 1024 - 2048;  // leave room for the kernel's static shared memory
-    if ((size_t)prod_cap * sizeof(T) >= budget) return false;
+    if ((size_t)prod_cap * sizeof(T) >= budget || prod_cap > BAND_EPT * BB) return false;
     for (int32_t c = ((n + 147) / 148 + R - 1) / R * R; c >= R; c = (c / 2 + R - 1) / R * R) {
         const int32_t nb = (n + c - 1) / c;
         lo.resize(nb); hi.resize(nb); len.resize(nb);
