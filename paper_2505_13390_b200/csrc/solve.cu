@@ -2,6 +2,7 @@
 #include "solve.cuh"
 
 #include <cstdint>
+#include <type_traits>
 
 #include "util.cuh"
 
@@ -146,7 +147,7 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restric
 // products (PT = T) into shared memory, fixed-order VLR-lane row reductions.  The epilogue's per-row
 // loads are issued before the stream so their latency overlaps it.
 constexpr int BB = 1024;
-constexpr int BAND_EPT = 12;  // stream elements per thread per sub-tile (sub-tile nnz <= BAND_EPT*BB)
+constexpr int BAND_EPT = 12;  // stream elements per thread per sub-tile (sub-tile nnz + 6 <= BAND_EPT*BB)
 template <class T, int VLR, int MODE>
 __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
                                                 const int32_t* __restrict__ win_len, int prod_cap,
@@ -170,10 +171,13 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
         __syncthreads();
         // software pipeline: the next sub-tile's stream and row operands are loaded into registers
         // while the current sub-tile is reduced (one CTA per SM, so nothing else hides the latency)
-        T pv[BAND_EPT];
-        int32_t pc[BAND_EPT];
+        // the stream is read as 16-byte vectors of 4 elements from the 4-aligned start below e0
+        constexpr int NV = BAND_EPT / 4;
+        using V4 = typename std::conditional<sizeof(T) == 4, float4, double4>::type;
+        V4 pv[NV];
+        int4 pc[NV];
         int32_t nr0 = c0, nr1 = 0;
-        int64_t ne0 = 0, nra = 0, nrz = 0;
+        int64_t ne0 = 0, nra = 0, nrz = 0, na0 = 0;
         int nne = 0;
         double nbi = 0.0, ndi = 0.0, nai = 0.0;
         auto fetch = [&](int32_t r0) {
@@ -181,12 +185,14 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
             nr1 = r0 + R < c1 ? r0 + R : c1;
             ne0 = rowptr[r0];
             nne = (int)(rowptr[nr1] - ne0);
+            na0 = ne0 & ~(int64_t)3;
+            const int nvec = (int)((ne0 + nne - na0 + 3) >> 2);
+            const V4* v4 = reinterpret_cast<const V4*>(val + na0);
+            const int4* c4 = reinterpret_cast<const int4*>(col + na0);
 #pragma unroll
-            for (int j = 0; j < BAND_EPT; ++j) {
-                const int idx = threadIdx.x + j * BB;
-                const bool in = idx < nne;
-                pv[j] = in ? val[ne0 + idx] : (T)0;
-                pc[j] = in ? col[ne0 + idx] : lo;
+            for (int j = 0; j < NV; ++j) {
+                const int q = threadIdx.x + j * BB;
+                if (q < nvec) { pv[j] = v4[q]; pc[j] = c4[q]; }
             }
             const int32_t i = r0 + rr;
             if (i < nr1) {
@@ -204,21 +210,26 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
             const int32_t r0 = nr0, r1 = nr1;
             const int64_t e0 = ne0, ra = nra, rz = nrz;
             const int ne = nne;
+            const int off = (int)(e0 - na0);  // 0..3 leading elements of the first vector outside the tile
             const double bi = nbi, di = ndi, ai = nai;
             const int32_t i = r0 + rr;
             const bool own = i < r1;
 #pragma unroll
-            for (int j = 0; j < BAND_EPT; ++j) {
-                const int idx = threadIdx.x + j * BB;
-                if (idx < ne) prod[idx] = (T)((double)pv[j] * (double)xs[pc[j] - lo]);
+            for (int j = 0; j < NV; ++j) {
+                const int base = 4 * (threadIdx.x + j * BB) - off;
+                // products in the storage precision T (fp32 variant: FMUL, no conversions)
+                if (base >= 0 && base < ne) prod[base] = pv[j].x * xs[pc[j].x - lo];
+                if (base + 1 >= 0 && base + 1 < ne) prod[base + 1] = pv[j].y * xs[pc[j].y - lo];
+                if (base + 2 >= 0 && base + 2 < ne) prod[base + 2] = pv[j].z * xs[pc[j].z - lo];
+                if (base + 3 >= 0 && base + 3 < ne) prod[base + 3] = pv[j].w * xs[pc[j].w - lo];
             }
             if (r0 + R < c1) fetch(r0 + R);
             else nr0 = c1;
             __syncthreads();
-            double s = 0.0;
+            T sl = (T)0;  // per-lane partial in T, the cross-lane sum in fp64
             if (own)
-                for (int k = (int)(ra - e0) + ln; k < (int)(rz - e0); k += VLR) s += (double)prod[k];
-            s = group_sum<VLR>(s);
+                for (int k = (int)(ra - e0) + ln; k < (int)(rz - e0); k += VLR) sl += prod[k];
+            double s = group_sum<VLR>((double)sl);
             if (own && ln == 0) {
                 if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
                     T yi = (T)((double)xs[i - lo] + omega * di * (bi - s));
@@ -653,7 +664,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     const int R = BB / vlr;
     prod_cap = R * maxrow;
     const size_t budget = 227 * 1024 - 2048;  // leave room for the kernel's static shared memory
-    if ((size_t)prod_cap * sizeof(T) >= budget || prod_cap > BAND_EPT * BB) return false;
+    if ((size_t)prod_cap * sizeof(T) >= budget || prod_cap + 6 > BAND_EPT * BB) return false;
     for (int32_t c = ((n + 147) / 148 + R - 1) / R * R; c >= R; c = (c / 2 + R - 1) / R * R) {
         const int32_t nb = (n + c - 1) / c;
         lo.resize(nb); hi.resize(nb); len.resize(nb);
