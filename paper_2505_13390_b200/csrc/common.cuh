@@ -48,7 +48,8 @@ struct DBuf {
         if (m > cap) {
             if (p) MG_CK(cudaFree(p));
             p = nullptr;
-            MG_CK(cudaMalloc(&p, (m ? m : 1) * sizeof(T)));
+            // +16 elements: vectorised streams may read up to one 32-byte vector past the end
+            MG_CK(cudaMalloc(&p, (m + 16) * sizeof(T)));
             cap = m;
         }
         n = m;

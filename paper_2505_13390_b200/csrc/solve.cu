@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
                                                 double* __restrict__ parts2) {
     extern __shared__ __align__(16) unsigned char smraw[];
     T* prod = reinterpret_cast<T*>(smraw);
-    T* xs = prod + prod_cap;
+    T* xs = prod + prod_cap + 8;  // prod holds up to 3 leading + 3 trailing vector lanes beyond the tile
     constexpr int R = BB / VLR;
     const int rr = threadIdx.x / VLR, ln = threadIdx.x % VLR;
     const int32_t nband = (n + C - 1) / C;
@@ -214,21 +214,30 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
             const double bi = nbi, di = ndi, ai = nai;
             const int32_t i = r0 + rr;
             const bool own = i < r1;
+            const int nvec = (ne + off + 3) >> 2;
 #pragma unroll
             for (int j = 0; j < NV; ++j) {
-                const int base = 4 * (threadIdx.x + j * BB) - off;
-                // products in the storage precision T (fp32 variant: FMUL, no conversions)
-                if (base >= 0 && base < ne) prod[base] = pv[j].x * xs[pc[j].x - lo];
-                if (base + 1 >= 0 && base + 1 < ne) prod[base + 1] = pv[j].y * xs[pc[j].y - lo];
-                if (base + 2 >= 0 && base + 2 < ne) prod[base + 2] = pv[j].z * xs[pc[j].z - lo];
-                if (base + 3 >= 0 && base + 3 < ne) prod[base + 3] = pv[j].w * xs[pc[j].w - lo];
+                const int q = threadIdx.x + j * BB;
+                if (q < nvec) {
+                    // products in the storage precision T (fp32 variant: FMUL, no conversions); prod is
+                    // indexed from the aligned start so each thread writes one 16-byte vector.  Elements
+                    // outside [e0, e0+ne) are gathered at a clamped column and never read back.
+                    const int32_t c0x = min(max(pc[j].x - lo, 0), len - 1), c0y = min(max(pc[j].y - lo, 0), len - 1);
+                    const int32_t c0z = min(max(pc[j].z - lo, 0), len - 1), c0w = min(max(pc[j].w - lo, 0), len - 1);
+                    V4 pr;
+                    pr.x = pv[j].x * xs[c0x];
+                    pr.y = pv[j].y * xs[c0y];
+                    pr.z = pv[j].z * xs[c0z];
+                    pr.w = pv[j].w * xs[c0w];
+                    reinterpret_cast<V4*>(prod)[q] = pr;
+                }
             }
             if (r0 + R < c1) fetch(r0 + R);
             else nr0 = c1;
             __syncthreads();
             T sl = (T)0;  // per-lane partial in T, the cross-lane sum in fp64
             if (own)
-                for (int k = (int)(ra - e0) + ln; k < (int)(rz - e0); k += VLR) sl += prod[k];
+                for (int k = (int)(ra - e0) + off + ln; k < (int)(rz - e0) + off; k += VLR) sl += prod[k];
             double s = group_sum<VLR>((double)sl);
             if (own && ln == 0) {
                 if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
@@ -265,7 +274,7 @@ template <class T, int MODE, int VLR>
 void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                  double* parts2, cudaStream_t s) {
     static size_t attr_set = 48 * 1024;
-    const size_t smem = ((size_t)A.prod_cap + A.band_win) * sizeof(T);
+    const size_t smem = ((size_t)A.prod_cap + 8 + A.band_win) * sizeof(T);
     if (smem > attr_set) {
         MG_CK(cudaFuncSetAttribute(k_band<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
@@ -678,7 +687,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
         int32_t mw = 0;
         MG_CK(cudaMemcpyAsync(&mw, tmp.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         MG_CK(cudaStreamSynchronize(s));
-        if ((size_t)(prod_cap + mw) * sizeof(T) <= budget) {
+        if ((size_t)(prod_cap + 8 + mw) * sizeof(T) <= budget) {
             C = c;
             win = mw;
             grid = nb < 148 ? nb : 148;
