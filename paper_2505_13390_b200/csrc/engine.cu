@@ -69,7 +69,7 @@ class Engine : public EngineBase {
         // V-cycle vectors
         DBuf<T> vb, vz, vx, vy, vt;
         int vl = 32, grid = 1, vlr = 0, tile_nnz = 0;
-        int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0;
+        int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0, row_vl = 0;
         DBuf<int32_t> win_lo, win_len;
         void configure(cudaStream_t s) {
             vl = choose_vl(n, nnz);
@@ -77,7 +77,8 @@ class Engine : public EngineBase {
             if (vlr == 0) grid = pass_grid(n, vl);
             band_rows = 0;
             if (!std::getenv("MGPBD_NO_BAND"))
-                band_config<T>(n, rowptr, col, vlr, win_lo, win_len, band_rows, band_grid, prod_cap, band_win, s);
+                band_config<T>(n, rowptr, col, vlr, win_lo, win_len, band_rows, band_grid, prod_cap, band_win, row_vl,
+                               s);
         }
         template <class U>
         Csr<U> view(const U* v, const U* d) const {
@@ -87,6 +88,7 @@ class Engine : public EngineBase {
             c.nparts = grid;
             if (std::is_same<U, T>::value && band_rows) {
                 c.band_rows = band_rows; c.band_grid = band_grid; c.prod_cap = prod_cap; c.band_win = band_win;
+                c.row_vl = row_vl;
                 c.win_lo = win_lo.p; c.win_len = win_len.p;
                 c.nparts = band_grid;
             }

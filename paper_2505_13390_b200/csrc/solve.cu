@@ -270,6 +270,128 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
     }
 }
 
+// Band-staged row pass without block barriers: after the shared x window of a band tile is staged,
+// every VL-lane group owns rows (warp-uniform stepping so the fixed-order butterfly always runs on
+// full warps) and keeps the NEXT row's val/col chunks and per-row operands in flight in registers
+// while it reduces the current one.  Rows have at most ROWCH*VL entries (checked at configuration).
+constexpr int ROWCH = 6;
+template <class T, int VL, int MODE>
+__global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
+                                                const int32_t* __restrict__ win_len,
+                                                const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                                const T* __restrict__ val, const T* __restrict__ dinv,
+                                                const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
+                                                const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                                double* __restrict__ parts2) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* xs = reinterpret_cast<T*>(smraw);
+    constexpr int SPW = 32 / VL;              // row groups per warp
+    constexpr int NSLOT = (BB / 32) * SPW;    // rows in flight per CTA step
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / VL, sl = lane % VL;
+    const int32_t nband = (n + C - 1) / C;
+    double acc1 = 0.0, acc2 = 0.0;
+    struct Row {
+        int32_t i;
+        int len;
+        T v[ROWCH];
+        int32_t c[ROWCH];
+        double bi, di, ai;
+    };
+    for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
+        const int32_t lo = win_lo[bt], len = win_len[bt];
+        const int32_t c0 = bt * C, c1 = c0 + C < n ? c0 + C : n;
+        __syncthreads();
+        for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
+        __syncthreads();
+        auto load = [&](int32_t wbase, Row& R) {
+            R.i = wbase + sub;
+            R.len = 0;
+            if (R.i < c1) {
+                const int64_t e0 = rowptr[R.i];
+                R.len = (int)(rowptr[R.i + 1] - e0);
+#pragma unroll
+                for (int j = 0; j < ROWCH; ++j) {
+                    const int k = sl + j * VL;
+                    const bool in = k < R.len;
+                    R.v[j] = in ? val[e0 + k] : (T)0;
+                    R.c[j] = in ? col[e0 + k] : lo;
+                }
+                if (sl == 0) {
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.bi = (double)b[R.i];
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) R.di = (double)dinv[R.i];
+                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.ai = (double)aux[R.i];
+                }
+            }
+        };
+        Row A, B;
+        int32_t wb = c0 + warp * SPW;  // warp-uniform base row of this warp's current step
+        load(wb, A);
+        load(wb + NSLOT, B);
+        for (; wb < c1; wb += NSLOT) {
+            T sl_ = (T)0;
+#pragma unroll
+            for (int j = 0; j < ROWCH; ++j)
+                if (sl + j * VL < A.len) sl_ += A.v[j] * xs[A.c[j] - lo];
+            const double s = group_sum<VL>((double)sl_);
+            if (A.i < c1 && sl == 0) {
+                const int32_t i = A.i;
+                if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
+                    T yi = (T)((double)xs[i - lo] + omega * A.di * (A.bi - s));
+                    y[i] = yi;
+                    if (MODE == PASS_JACOBI_DOT) { acc1 += A.ai * (double)yi; acc2 += A.ai * A.ai; }
+                } else if (MODE == PASS_RESID_P) {
+                    y[i] = (T)(A.ai * (A.bi - s));
+                } else if (MODE == PASS_SPMV_DOT) {
+                    T yi = (T)s;
+                    y[i] = yi;
+                    acc1 += (double)xs[i - lo] * (double)yi;
+                } else if (MODE == PASS_POWER) {
+                    T yi = (T)(A.di * s);
+                    y[i] = yi;
+                    acc1 += (double)yi * (double)yi;
+                }
+            }
+            A = B;
+            load(wb + 2 * NSLOT, B);
+        }
+    }
+    if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
+        __shared__ double sh[32];
+        double t1 = block_sum<BB>(acc1, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t1;
+        if (MODE == PASS_JACOBI_DOT) {
+            double t2 = block_sum<BB>(acc2, sh);
+            if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
+        }
+    }
+}
+
+template <class T, int MODE, int VL>
+void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                 double* parts2, cudaStream_t s) {
+    static size_t attr_set = 48 * 1024;
+    const size_t smem = (size_t)A.band_win * sizeof(T);
+    if (smem > attr_set) {
+        MG_CK(cudaFuncSetAttribute(k_rows<T, VL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_set = smem;
+    }
+    k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col, A.val,
+                                                     A.dinv, x, b, y, aux, omega, parts, parts2);
+    MG_LAUNCH_CHECK();
+}
+
+template <class T, int MODE>
+void launch_rows_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+                      double* parts2, cudaStream_t s) {
+    switch (A.row_vl) {
+        case 4: launch_rows<T, MODE, 4>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 8: launch_rows<T, MODE, 8>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 16: launch_rows<T, MODE, 16>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        default: launch_rows<T, MODE, 32>(A, x, b, y, aux, omega, parts, parts2, s); break;
+    }
+}
+
 template <class T, int MODE, int VLR>
 void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                  double* parts2, cudaStream_t s) {
@@ -659,8 +781,9 @@ __global__ void k_rowlen_max2(int32_t n, const int64_t* __restrict__ rowptr, int
 
 template <class T>
 bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
-                 int& C, int& grid, int& prod_cap, int& win, cudaStream_t s) {
+                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, cudaStream_t s) {
     C = 0;
+    row_vl = 0;
     if (n < 4096 || vlr <= 0) return false;
     DBuf<int32_t> tmp, hi;
     tmp.resize(2);
@@ -691,6 +814,12 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
             C = c;
             win = mw;
             grid = nb < 148 ? nb : 148;
+            // barrier-free row kernel: VL lanes per row, rows of at most ROWCH*VL entries
+            const double avg = (double)read_scalar(rowptr + n, s) / n;
+            int v = 4;
+            while (v < 32 && v * 5 < avg) v *= 2;
+            while (v < 32 && maxrow > ROWCH * v) v *= 2;
+            if (maxrow <= ROWCH * v && !std::getenv("MGPBD_NO_ROWS")) row_vl = v;
             return true;
         }
         if (c == R) break;
@@ -698,9 +827,9 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     return false;
 }
 template bool band_config<float>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
-                                 int&, int&, int&, cudaStream_t);
+                                 int&, int&, int&, int&, cudaStream_t);
 template bool band_config<double>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
-                                  int&, int&, int&, cudaStream_t);
+                                  int&, int&, int&, int&, cudaStream_t);
 
 int pass_grid(int32_t n, int vl) {
     int rows_per_block = PB / vl;
@@ -713,6 +842,17 @@ template <class T>
 void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
               double* parts2, cudaStream_t s) {
     if (A.n == 0) return;
+    if (A.band_rows > 0 && A.row_vl > 0) {
+        switch (mode) {
+            case PASS_JACOBI: launch_rows_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_JACOBI_DOT: launch_rows_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_RESID_P: launch_rows_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_SPMV_DOT: launch_rows_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_POWER: launch_rows_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            default: throw Error(-1, "bad pass mode");
+        }
+        return;
+    }
     if (A.band_rows > 0) {
         switch (mode) {
             case PASS_JACOBI: launch_band_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;

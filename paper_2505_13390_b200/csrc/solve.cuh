@@ -21,6 +21,7 @@ struct Csr {
     int tile_nnz = 0;  // max nnz of a tile (shared-memory products)
     // band-staged kernel (band_rows > 0): band tiles of band_rows rows, x window per band tile
     int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0;
+    int row_vl = 0;  // > 0: barrier-free band row kernel with row_vl lanes per row
     const int32_t* win_lo = nullptr;
     const int32_t* win_len = nullptr;
 };
@@ -29,7 +30,7 @@ struct Csr {
 // the smallest band tile does not fit in shared memory next to the product buffer.
 template <class T>
 bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
-                 int& C, int& grid, int& prod_cap, int& win, cudaStream_t s);
+                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, cudaStream_t s);
 
 // Choose the row-tile configuration of a level (vlr, fixed grid, max tile nnz); vlr = 0 if the tile
 // would not fit in shared memory.
