@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
 // every VL-lane group owns rows (warp-uniform stepping so the fixed-order butterfly always runs on
 // full warps) and keeps the NEXT row's val/col chunks and per-row operands in flight in registers
 // while it reduces the current one.  Rows have at most ROWCH*VL entries (checked at configuration).
-constexpr int ROWCH = 6;
+constexpr int ROWCH = 5;
 template <class T, int VL, int MODE>
 __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
                                                 const int32_t* __restrict__ win_len,
@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
         int len;
         T v[ROWCH];
         int32_t c[ROWCH];
-        double bi, di, ai;
+        T bi, di, ai;  // storage precision (registers); widened to fp64 in the epilogue
     };
     for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
         const int32_t lo = win_lo[bt], len = win_len[bt];
@@ -318,16 +318,17 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                     R.c[j] = in ? col[e0 + k] : lo;
                 }
                 if (sl == 0) {
-                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.bi = (double)b[R.i];
-                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) R.di = (double)dinv[R.i];
-                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.ai = (double)aux[R.i];
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.bi = b[R.i];
+                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) R.di = dinv[R.i];
+                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.ai = aux[R.i];
                 }
             }
         };
-        Row A, B;
+        Row A, B, D;
         int32_t wb = c0 + warp * SPW;  // warp-uniform base row of this warp's current step
         load(wb, A);
         load(wb + NSLOT, B);
+        load(wb + 2 * NSLOT, D);
         for (; wb < c1; wb += NSLOT) {
             T sl_ = (T)0;
 #pragma unroll
@@ -336,24 +337,26 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
             const double s = group_sum<VL>((double)sl_);
             if (A.i < c1 && sl == 0) {
                 const int32_t i = A.i;
+                const double bi = (double)A.bi, di = (double)A.di, ai = (double)A.ai;
                 if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
-                    T yi = (T)((double)xs[i - lo] + omega * A.di * (A.bi - s));
+                    T yi = (T)((double)xs[i - lo] + omega * di * (bi - s));
                     y[i] = yi;
-                    if (MODE == PASS_JACOBI_DOT) { acc1 += A.ai * (double)yi; acc2 += A.ai * A.ai; }
+                    if (MODE == PASS_JACOBI_DOT) { acc1 += ai * (double)yi; acc2 += ai * ai; }
                 } else if (MODE == PASS_RESID_P) {
-                    y[i] = (T)(A.ai * (A.bi - s));
+                    y[i] = (T)(ai * (bi - s));
                 } else if (MODE == PASS_SPMV_DOT) {
                     T yi = (T)s;
                     y[i] = yi;
                     acc1 += (double)xs[i - lo] * (double)yi;
                 } else if (MODE == PASS_POWER) {
-                    T yi = (T)(A.di * s);
+                    T yi = (T)(di * s);
                     y[i] = yi;
                     acc1 += (double)yi * (double)yi;
                 }
             }
             A = B;
-            load(wb + 2 * NSLOT, B);
+            B = D;
+            load(wb + 3 * NSLOT, D);
         }
     }
     if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
