@@ -71,6 +71,7 @@ class Engine : public EngineBase {
         int vl = 32, grid = 1, vlr = 0, tile_nnz = 0;
         int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0, row_vl = 0;
         DBuf<int32_t> win_lo, win_len;
+        DBuf<uint16_t> col16;
         void configure(cudaStream_t s) {
             vl = choose_vl(n, nnz);
             tile_config(n, nnz, rowptr, vlr, grid, tile_nnz, s);
@@ -78,7 +79,7 @@ class Engine : public EngineBase {
             band_rows = 0;
             if (!std::getenv("MGPBD_NO_BAND"))
                 band_config<T>(n, rowptr, col, vlr, win_lo, win_len, band_rows, band_grid, prod_cap, band_win, row_vl,
-                               s);
+                               col16, s);
         }
         template <class U>
         Csr<U> view(const U* v, const U* d) const {
@@ -89,6 +90,7 @@ class Engine : public EngineBase {
             if (std::is_same<U, T>::value && band_rows) {
                 c.band_rows = band_rows; c.band_grid = band_grid; c.prod_cap = prod_cap; c.band_win = band_win;
                 c.row_vl = row_vl;
+                c.col16 = col16.p;
                 c.win_lo = win_lo.p; c.win_len = win_len.p;
                 c.nparts = band_grid;
             }
@@ -208,7 +210,8 @@ class Engine : public EngineBase {
     // Algorithmic bytes of one level-0 CSR pass (matrix stream + per-row vectors), see DESIGN.md.
     double pass_bytes(int mode) const {
         const double s = sizeof(T);
-        double mat = (double)nnz0 * (s + 4) + 8.0 * (m + 1);
+        const double cb = (L[0]->band_rows > 0 && L[0]->row_vl > 0) ? 2.0 : 4.0;  // col16 hot copy or int32
+        double mat = (double)nnz0 * (s + cb) + 8.0 * (m + 1);
         double vec;
         switch (mode) {
             case PASS_JACOBI: vec = 4 * s; break;          // x (gathered once), b, dinv, y

@@ -275,10 +275,22 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
 // full warps) and keeps the NEXT row's val/col chunks and per-row operands in flight in registers
 // while it reduces the current one.  Rows have at most ROWCH*VL entries (checked at configuration).
 constexpr int ROWCH = 5;
+// col16[e] = col[e] - win_lo[band tile of the row]: the hot copy of the level-0 column indices.
+__global__ void k_col16(int32_t n, int32_t C, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                        const int32_t* __restrict__ win_lo, uint16_t* __restrict__ col16) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w0; i < n; i += nw) {
+        const int32_t lo = win_lo[i / C];
+        for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) col16[e] = (uint16_t)(col[e] - lo);
+    }
+}
+
 template <class T, int VL, int MODE>
 __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
                                                 const int32_t* __restrict__ win_len,
-                                                const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                                const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ col,
                                                 const T* __restrict__ val, const T* __restrict__ dinv,
                                                 const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
                                                 const T* __restrict__ aux, double omega, double* __restrict__ parts,
@@ -295,7 +307,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
         int32_t i;
         int len;
         T v[ROWCH];
-        int32_t c[ROWCH];
+        uint16_t c[ROWCH];  // window-relative column
         T bi, di, ai;  // storage precision (registers); widened to fp64 in the epilogue
     };
     for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
@@ -315,7 +327,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                     const int k = sl + j * VL;
                     const bool in = k < R.len;
                     R.v[j] = in ? val[e0 + k] : (T)0;
-                    R.c[j] = in ? col[e0 + k] : lo;
+                    R.c[j] = in ? col[e0 + k] : (uint16_t)0;
                 }
                 if (sl == 0) {
                     if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.bi = b[R.i];
@@ -333,7 +345,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
             T sl_ = (T)0;
 #pragma unroll
             for (int j = 0; j < ROWCH; ++j)
-                if (sl + j * VL < A.len) sl_ += A.v[j] * xs[A.c[j] - lo];
+                if (sl + j * VL < A.len) sl_ += A.v[j] * xs[A.c[j]];
             const double s = group_sum<VL>((double)sl_);
             if (A.i < c1 && sl == 0) {
                 const int32_t i = A.i;
@@ -379,8 +391,8 @@ void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         MG_CK(cudaFuncSetAttribute(k_rows<T, VL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col, A.val,
-                                                     A.dinv, x, b, y, aux, omega, parts, parts2);
+    k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col16,
+                                                     A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
     MG_LAUNCH_CHECK();
 }
 
@@ -784,7 +796,7 @@ __global__ void k_rowlen_max2(int32_t n, const int64_t* __restrict__ rowptr, int
 
 template <class T>
 bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
-                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, cudaStream_t s) {
+                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, DBuf<uint16_t>& col16, cudaStream_t s) {
     C = 0;
     row_vl = 0;
     if (n < 4096 || vlr <= 0) return false;
@@ -822,7 +834,15 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
             int v = 4;
             while (v < 32 && v * 5 < avg) v *= 2;
             while (v < 32 && maxrow > ROWCH * v) v *= 2;
-            if (maxrow <= ROWCH * v && !std::getenv("MGPBD_NO_ROWS")) row_vl = v;
+            if (maxrow <= ROWCH * v && mw <= 65536 && !std::getenv("MGPBD_NO_ROWS")) {
+                row_vl = v;
+                const int64_t nnz = read_scalar(rowptr + n, s);
+                col16.resize(nnz);
+                k_col16<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, 148 * 16), 256, 0, s>>>(n, c, rowptr, col,
+                                                                                                     lo.p, col16.p);
+                MG_LAUNCH_CHECK();
+                MG_CK(cudaStreamSynchronize(s));
+            }
             return true;
         }
         if (c == R) break;
@@ -830,9 +850,9 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     return false;
 }
 template bool band_config<float>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
-                                 int&, int&, int&, int&, cudaStream_t);
+                                 int&, int&, int&, int&, DBuf<uint16_t>&, cudaStream_t);
 template bool band_config<double>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
-                                  int&, int&, int&, int&, cudaStream_t);
+                                  int&, int&, int&, int&, DBuf<uint16_t>&, cudaStream_t);
 
 int pass_grid(int32_t n, int vl) {
     int rows_per_block = PB / vl;

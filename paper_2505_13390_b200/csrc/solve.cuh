@@ -24,13 +24,15 @@ struct Csr {
     int row_vl = 0;  // > 0: barrier-free band row kernel with row_vl lanes per row
     const int32_t* win_lo = nullptr;
     const int32_t* win_len = nullptr;
+    const uint16_t* col16 = nullptr;  // window-relative column offsets (hot copy, row kernel)
 };
 
 // Band configuration for the band-staged pass: returns false (and C = 0) if the column window of even
-// the smallest band tile does not fit in shared memory next to the product buffer.
+// the smallest band tile does not fit in shared memory next to the product buffer.  With the row
+// kernel (row_vl > 0) it also builds col16, the 16-bit window-relative copy of the column indices.
 template <class T>
 bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
-                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, cudaStream_t s);
+                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, DBuf<uint16_t>& col16, cudaStream_t s);
 
 // Choose the row-tile configuration of a level (vlr, fixed grid, max tile nnz); vlr = 0 if the tile
 // would not fit in shared memory.
