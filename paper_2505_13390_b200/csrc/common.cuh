@@ -100,6 +100,13 @@ __device__ __forceinline__ double group_sum(double v) {
     return v;
 }
 
+template <int VL, class U>
+__device__ __forceinline__ U group_sum_t(U v) {
+#pragma unroll
+    for (int o = VL / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, VL);
+    return v;
+}
+
 // Deterministic block sum of per-thread values (fixed tree); result valid in thread 0.
 template <int BS>
 __device__ __forceinline__ double block_sum(double v, double* sh) {

@@ -336,17 +336,13 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                 }
             }
         };
-        Row A, B, D;
-        int32_t wb = c0 + warp * SPW;  // warp-uniform base row of this warp's current step
-        load(wb, A);
-        load(wb + NSLOT, B);
-        load(wb + 2 * NSLOT, D);
-        for (; wb < c1; wb += NSLOT) {
-            T sl_ = (T)0;
+        auto process = [&](const Row& A) {
+            T part = (T)0;
 #pragma unroll
             for (int j = 0; j < ROWCH; ++j)
-                if (sl + j * VL < A.len) sl_ += A.v[j] * xs[A.c[j]];
-            const double s = group_sum<VL>((double)sl_);
+                if (sl + j * VL < A.len) part += A.v[j] * xs[A.c[j]];
+            // lane partials and the butterfly in the storage precision, the row sum in fp64
+            const double s = (double)group_sum_t<VL>(part);
             if (A.i < c1 && sl == 0) {
                 const int32_t i = A.i;
                 const double bi = (double)A.bi, di = (double)A.di, ai = (double)A.ai;
@@ -366,9 +362,24 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                     acc1 += (double)yi * (double)yi;
                 }
             }
-            A = B;
-            B = D;
-            load(wb + 3 * NSLOT, D);
+        };
+        // three rows in flight per group, rotated in place (no register copies)
+        Row A, B, D;
+        int32_t wb = c0 + warp * SPW;  // warp-uniform base row of this warp's current step
+        load(wb, A);
+        load(wb + NSLOT, B);
+        load(wb + 2 * NSLOT, D);
+        // single-exit loop with a warp-uniform trip count (rows past c1 are empty), so the butterfly
+        // needs no divergence handling
+        const int nsteps = wb < c1 ? (c1 - wb + NSLOT - 1) / NSLOT : 0;
+        for (int t = 0; t < nsteps; t += 3) {
+            process(A);
+            load(wb + 3 * NSLOT, A);
+            process(B);
+            load(wb + 4 * NSLOT, B);
+            process(D);
+            load(wb + 5 * NSLOT, D);
+            wb += 3 * NSLOT;
         }
     }
     if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
