@@ -296,7 +296,9 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                                                 const T* __restrict__ aux, double omega, double* __restrict__ parts,
                                                 double* __restrict__ parts2) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    T* xs = reinterpret_cast<T*>(smraw);
+    // shared: [row offsets of the band tile, int32 relative to its first nonzero][x window]
+    int32_t* rp = reinterpret_cast<int32_t*>(smraw);
+    T* xs = reinterpret_cast<T*>(smraw + (((size_t)(C + 1) * sizeof(int32_t) + 15) & ~(size_t)15));
     constexpr int SPW = 32 / VL;              // row groups per warp
     constexpr int NSLOT = (BB / 32) * SPW;    // rows in flight per CTA step
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -313,21 +315,25 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
     for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
         const int32_t lo = win_lo[bt], len = win_len[bt];
         const int32_t c0 = bt * C, c1 = c0 + C < n ? c0 + C : n;
+        const int64_t ebase = rowptr[c0];
         __syncthreads();
         for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
+        for (int32_t k = threadIdx.x; k <= c1 - c0; k += BB) rp[k] = (int32_t)(rowptr[c0 + k] - ebase);
         __syncthreads();
+        const T* __restrict__ vb = val + ebase;
+        const uint16_t* __restrict__ cb = col + ebase;
         auto load = [&](int32_t wbase, Row& R) {
             R.i = wbase + sub;
             R.len = 0;
             if (R.i < c1) {
-                const int64_t e0 = rowptr[R.i];
-                R.len = (int)(rowptr[R.i + 1] - e0);
+                const int32_t e0 = rp[R.i - c0];  // shared-memory row offsets: no dependent global load
+                R.len = rp[R.i - c0 + 1] - e0;
 #pragma unroll
                 for (int j = 0; j < ROWCH; ++j) {
                     const int k = sl + j * VL;
                     const bool in = k < R.len;
-                    R.v[j] = in ? val[e0 + k] : (T)0;
-                    R.c[j] = in ? col[e0 + k] : (uint16_t)0;
+                    R.v[j] = in ? vb[e0 + k] : (T)0;
+                    R.c[j] = in ? cb[e0 + k] : (uint16_t)0;
                 }
                 if (sl == 0) {
                     if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.bi = b[R.i];
@@ -397,7 +403,7 @@ template <class T, int MODE, int VL>
 void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                  double* parts2, cudaStream_t s) {
     static size_t attr_set = 48 * 1024;
-    const size_t smem = (size_t)A.band_win * sizeof(T);
+    const size_t smem = ((((size_t)A.band_rows + 1) * sizeof(int32_t) + 15) & ~(size_t)15) + (size_t)A.band_win * sizeof(T);
     if (smem > attr_set) {
         MG_CK(cudaFuncSetAttribute(k_rows<T, VL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
@@ -836,16 +842,20 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
         int32_t mw = 0;
         MG_CK(cudaMemcpyAsync(&mw, tmp.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         MG_CK(cudaStreamSynchronize(s));
-        if ((size_t)(prod_cap + 8 + mw) * sizeof(T) <= budget) {
+        // barrier-free row kernel: VL lanes per row, rows of at most ROWCH*VL entries; its shared
+        // memory holds the band tile's row offsets and the x window
+        const double avg = (double)read_scalar(rowptr + n, s) / n;
+        int v = 4;
+        while (v < 32 && v * 5 < avg) v *= 2;
+        while (v < 32 && maxrow > ROWCH * v) v *= 2;
+        const bool rows_fit = maxrow <= ROWCH * v && mw <= 65536 && !std::getenv("MGPBD_NO_ROWS") &&
+                              (((size_t)(c + 1) * 4 + 15) & ~(size_t)15) + (size_t)mw * sizeof(T) <= budget;
+        const bool band_fit = (size_t)(prod_cap + 8 + mw) * sizeof(T) <= budget;
+        if (rows_fit || band_fit) {
             C = c;
             win = mw;
             grid = nb < 148 ? nb : 148;
-            // barrier-free row kernel: VL lanes per row, rows of at most ROWCH*VL entries
-            const double avg = (double)read_scalar(rowptr + n, s) / n;
-            int v = 4;
-            while (v < 32 && v * 5 < avg) v *= 2;
-            while (v < 32 && maxrow > ROWCH * v) v *= 2;
-            if (maxrow <= ROWCH * v && mw <= 65536 && !std::getenv("MGPBD_NO_ROWS")) {
+            if (rows_fit) {
                 row_vl = v;
                 const int64_t nnz = read_scalar(rowptr + n, s);
                 col16.resize(nnz);
