@@ -296,9 +296,13 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                                                 const T* __restrict__ aux, double omega, double* __restrict__ parts,
                                                 double* __restrict__ parts2) {
     extern __shared__ __align__(16) unsigned char smraw[];
-    // shared: [row offsets of the band tile, int32 relative to its first nonzero][x window]
+    // shared: [row offsets of the band tile, int32 relative to its first nonzero]
+    //         [per-row operands b, dinv, aux of the band tile (storage precision)] [x window]
     int32_t* rp = reinterpret_cast<int32_t*>(smraw);
-    T* xs = reinterpret_cast<T*>(smraw + (((size_t)(C + 1) * sizeof(int32_t) + 15) & ~(size_t)15));
+    T* ob = reinterpret_cast<T*>(smraw + (((size_t)(C + 1) * sizeof(int32_t) + 15) & ~(size_t)15));
+    T* od = ob + C;
+    T* oa = od + C;
+    T* xs = oa + C;
     constexpr int SPW = 32 / VL;              // row groups per warp
     constexpr int NSLOT = (BB / 32) * SPW;    // rows in flight per CTA step
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -310,8 +314,10 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
         int len;
         T v[ROWCH];
         uint16_t c[ROWCH];  // window-relative column
-        T bi, di, ai;  // storage precision (registers); widened to fp64 in the epilogue
     };
+    constexpr bool NB = MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P;
+    constexpr bool ND = MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER;
+    constexpr bool NA = MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P;
     for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
         const int32_t lo = win_lo[bt], len = win_len[bt];
         const int32_t c0 = bt * C, c1 = c0 + C < n ? c0 + C : n;
@@ -319,6 +325,11 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
         __syncthreads();
         for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
         for (int32_t k = threadIdx.x; k <= c1 - c0; k += BB) rp[k] = (int32_t)(rowptr[c0 + k] - ebase);
+        for (int32_t k = threadIdx.x; k < c1 - c0; k += BB) {
+            if (NB) ob[k] = b[c0 + k];
+            if (ND) od[k] = dinv[c0 + k];
+            if (NA) oa[k] = aux[c0 + k];
+        }
         __syncthreads();
         const T* __restrict__ vb = val + ebase;
         const uint16_t* __restrict__ cb = col + ebase;
@@ -335,11 +346,6 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
                     R.v[j] = in ? vb[e0 + k] : (T)0;
                     R.c[j] = in ? cb[e0 + k] : (uint16_t)0;
                 }
-                if (sl == 0) {
-                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.bi = b[R.i];
-                    if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER) R.di = dinv[R.i];
-                    if (MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P) R.ai = aux[R.i];
-                }
             }
         };
         auto process = [&](const Row& A) {
@@ -351,7 +357,8 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
             const double s = (double)group_sum_t<VL>(part);
             if (A.i < c1 && sl == 0) {
                 const int32_t i = A.i;
-                const double bi = (double)A.bi, di = (double)A.di, ai = (double)A.ai;
+                const double bi = NB ? (double)ob[i - c0] : 0.0, di = ND ? (double)od[i - c0] : 0.0,
+                             ai = NA ? (double)oa[i - c0] : 0.0;
                 if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
                     T yi = (T)((double)xs[i - lo] + omega * di * (bi - s));
                     y[i] = yi;
@@ -403,7 +410,8 @@ template <class T, int MODE, int VL>
 void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                  double* parts2, cudaStream_t s) {
     static size_t attr_set = 48 * 1024;
-    const size_t smem = ((((size_t)A.band_rows + 1) * sizeof(int32_t) + 15) & ~(size_t)15) + (size_t)A.band_win * sizeof(T);
+    const size_t smem = ((((size_t)A.band_rows + 1) * sizeof(int32_t) + 15) & ~(size_t)15) +
+                        ((size_t)3 * A.band_rows + A.band_win) * sizeof(T);
     if (smem > attr_set) {
         MG_CK(cudaFuncSetAttribute(k_rows<T, VL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
@@ -828,8 +836,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     const int R = BB / vlr;
     prod_cap = R * maxrow;
     const size_t budget = 227 * 1024 - 2048;  // leave room for the kernel's static shared memory
-    if ((size_t)prod_cap * sizeof(T) >= budget || prod_cap + 6 > BAND_EPT * BB) return false;
-    for (int32_t c = ((n + 147) / 148 + R - 1) / R * R; c >= R; c = (c / 2 + R - 1) / R * R) {
+    auto windows = [&](int32_t c) {
         const int32_t nb = (n + c - 1) / c;
         lo.resize(nb); hi.resize(nb); len.resize(nb);
         fill_i32(lo.p, INT32_MAX, nb, s);
@@ -842,28 +849,42 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
         int32_t mw = 0;
         MG_CK(cudaMemcpyAsync(&mw, tmp.p + 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
         MG_CK(cudaStreamSynchronize(s));
-        // barrier-free row kernel: VL lanes per row, rows of at most ROWCH*VL entries; its shared
-        // memory holds the band tile's row offsets and the x window
+        return mw;
+    };
+    // 1) barrier-free row kernel: VL lanes per row (rows of at most ROWCH*VL entries); shared memory
+    //    holds the band tile's row offsets, its per-row operands and the x window.  Band tiles are
+    //    sized so every CTA gets the same whole number of them (k per SM).
+    {
         const double avg = (double)read_scalar(rowptr + n, s) / n;
         int v = 4;
         while (v < 32 && v * 5 < avg) v *= 2;
         while (v < 32 && maxrow > ROWCH * v) v *= 2;
-        const bool rows_fit = maxrow <= ROWCH * v && mw <= 65536 && !std::getenv("MGPBD_NO_ROWS") &&
-                              (((size_t)(c + 1) * 4 + 15) & ~(size_t)15) + (size_t)mw * sizeof(T) <= budget;
-        const bool band_fit = (size_t)(prod_cap + 8 + mw) * sizeof(T) <= budget;
-        if (rows_fit || band_fit) {
-            C = c;
-            win = mw;
-            grid = nb < 148 ? nb : 148;
-            if (rows_fit) {
-                row_vl = v;
-                const int64_t nnz = read_scalar(rowptr + n, s);
-                col16.resize(nnz);
-                k_col16<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, 148 * 16), 256, 0, s>>>(n, c, rowptr, col,
-                                                                                                     lo.p, col16.p);
-                MG_LAUNCH_CHECK();
-                MG_CK(cudaStreamSynchronize(s));
+        if (maxrow <= ROWCH * v && !std::getenv("MGPBD_NO_ROWS")) {
+            for (int k = 1; k <= 64; ++k) {
+                const int32_t c = (int32_t)(((int64_t)n + 148 * k - 1) / (148 * k));
+                const int32_t mw = windows(c);
+                const size_t need = (((size_t)(c + 1) * 4 + 15) & ~(size_t)15) + ((size_t)3 * c + mw) * sizeof(T);
+                if (mw <= 65536 && need <= budget) {
+                    const int32_t nb = (n + c - 1) / c;
+                    C = c; win = mw; grid = nb < 148 ? nb : 148; row_vl = v;
+                    const int64_t nnz = read_scalar(rowptr + n, s);
+                    col16.resize(nnz);
+                    k_col16<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, 148 * 16), 256, 0, s>>>(
+                        n, c, rowptr, col, lo.p, col16.p);
+                    MG_LAUNCH_CHECK();
+                    MG_CK(cudaStreamSynchronize(s));
+                    return true;
+                }
             }
+        }
+    }
+    // 2) band kernel with a shared product buffer
+    if ((size_t)prod_cap * sizeof(T) >= budget || prod_cap + 6 > BAND_EPT * BB) return false;
+    for (int32_t c = ((n + 147) / 148 + R - 1) / R * R; c >= R; c = (c / 2 + R - 1) / R * R) {
+        const int32_t mw = windows(c);
+        if ((size_t)(prod_cap + 8 + mw) * sizeof(T) <= budget) {
+            const int32_t nb = (n + c - 1) / c;
+            C = c; win = mw; grid = nb < 148 ? nb : 148;
             return true;
         }
         if (c == R) break;
