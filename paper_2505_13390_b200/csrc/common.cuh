@@ -35,6 +35,17 @@ extern thread_local int64_t g_kernel_launches;
 
 constexpr int kWarp = 32;
 
+// Stream on which the current thread's context allocates (stream-ordered allocation from the
+// device's default memory pool, whose release threshold the context raises so that setup-time
+// temporaries are recycled instead of being mapped/unmapped every setup).  nullptr = cudaMalloc.
+extern thread_local cudaStream_t g_alloc_stream;
+
+inline void dev_free(void* p) {
+    if (!p) return;
+    if (g_alloc_stream) cudaFreeAsync(p, g_alloc_stream);
+    else cudaFree(p);
+}
+
 // Growable device buffer (owns memory; never shrinks).
 template <class T>
 struct DBuf {
@@ -43,19 +54,20 @@ struct DBuf {
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
-    ~DBuf() { if (p) cudaFree(p); }
+    ~DBuf() { dev_free(p); }
     void resize(size_t m) {
         if (m > cap) {
-            if (p) MG_CK(cudaFree(p));
+            dev_free(p);
             p = nullptr;
             // +16 elements: vectorised streams may read up to one 32-byte vector past the end
-            MG_CK(cudaMalloc(&p, (m + 16) * sizeof(T)));
+            if (g_alloc_stream) MG_CK(cudaMallocAsync(&p, (m + 16) * sizeof(T), g_alloc_stream));
+            else MG_CK(cudaMalloc(&p, (m + 16) * sizeof(T)));
             cap = m;
         }
         n = m;
     }
     void swap(DBuf& o) { std::swap(p, o.p); std::swap(n, o.n); std::swap(cap, o.cap); }
-    void free_all() { if (p) cudaFree(p); p = nullptr; n = cap = 0; }
+    void free_all() { dev_free(p); p = nullptr; n = cap = 0; }
     T* get() const { return p; }
     size_t bytes() const { return n * sizeof(T); }
 };

@@ -40,6 +40,7 @@ struct EngineBase {
     virtual void debug_setup_from(const double* vals) = 0;
     virtual void debug_vcycle(const double* b, double* x) = 0;
     virtual void debug_pcg(const double* b, int32_t iters, double* x) = 0;
+    virtual void bind() = 0;  // make this context's device/stream current for the calling thread
     bool stale = true;
 };
 
@@ -140,6 +141,12 @@ class Engine : public EngineBase {
         MG_CK(cudaSetDevice(cfg.device));
         if (cfg.stream) st = (cudaStream_t)cfg.stream;
         else { MG_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); own_stream = true; }
+        // stream-ordered allocations from the default pool, retained across setups
+        cudaMemPool_t pool;
+        MG_CK(cudaDeviceGetDefaultMemPool(&pool, cfg.device));
+        uint64_t keep = UINT64_MAX;
+        MG_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        g_alloc_stream = st;
         kind = cons->kind; kc = (int)kind;
         nv = mesh->n_verts; m = cons->n_cons;
         verts.resize((size_t)m * kc);
@@ -191,8 +198,11 @@ class Engine : public EngineBase {
 
     ~Engine() override {
         for (auto e : ev_pool) cudaEventDestroy(e);
+        cudaStreamSynchronize(st);
+        g_alloc_stream = nullptr;  // members are freed after this body: plain cudaFree from here on
         if (own_stream && st) cudaStreamDestroy(st);
     }
+    void bind() override { cudaSetDevice(cfg.device); g_alloc_stream = st; }
 
     void alloc_vectors(Level& lv) {
         lv.vb.resize(lv.n); lv.vz.resize(lv.n); lv.vx.resize(lv.n); lv.vy.resize(lv.n); lv.vt.resize(lv.n);
@@ -611,6 +621,7 @@ template <class F>
 static mgpbd_status guarded(mgpbd_ctx* ctx, F&& f) {
     if (!ctx) return MGPBD_E_ARG;
     try {
+        ctx->eng->bind();
         f();
         return MGPBD_OK;
     } catch (const Error& e) {
@@ -762,6 +773,10 @@ mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, dou
     return guarded(ctx, [&] { ctx->eng->debug_pcg(b, iters, x); });
 }
 const char* mgpbd_last_error(const mgpbd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
-void mgpbd_destroy(mgpbd_ctx* ctx) { delete ctx; }
+void mgpbd_destroy(mgpbd_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->eng) ctx->eng->bind();
+    delete ctx;
+}
 
 }  // extern "C"

@@ -4,6 +4,7 @@
 namespace mgpbd {
 
 thread_local int64_t g_kernel_launches = 0;
+thread_local cudaStream_t g_alloc_stream = nullptr;
 
 namespace {
 constexpr int SB = 1024;      // threads per scan block
