@@ -197,6 +197,7 @@ class Engine : public EngineBase {
     }
 
     ~Engine() override {
+        invalidate_graphs();
         for (auto e : ev_pool) cudaEventDestroy(e);
         cudaStreamSynchronize(st);
         g_alloc_stream = nullptr;  // members are freed after this body: plain cudaFree from here on
@@ -233,15 +234,43 @@ class Engine : public EngineBase {
         return mat + vec * (double)m;
     }
 
+    // ---- CUDA graphs: the solve part of each outer iteration (Galerkin refresh, coarsest inverse,
+    // MGPCG, update) is captured once per hierarchy and replayed; graph i owns its profiling events.
+    struct IterGraph {
+        cudaGraphExec_t exec = nullptr;
+        bool seen = false;  // first use runs eagerly (kernel attributes are set outside capture)
+        std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+        int64_t launches = 0, l0_launches = 0;
+        double l0_bytes = 0;
+    };
+    std::vector<IterGraph> graphs;
+    IterGraph* capturing = nullptr;
+    bool use_graphs = std::getenv("MGPBD_NO_GRAPH") == nullptr;
+
+    void invalidate_graphs() {
+        for (auto& g : graphs) {
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+            for (auto& pr : g.ev) { cudaEventDestroy(pr.first); cudaEventDestroy(pr.second); }
+        }
+        graphs.clear();
+    }
+
+    cudaEvent_t prof_event() {
+        if (!capturing) return ev();
+        cudaEvent_t e;
+        MG_CK(cudaEventCreate(&e));
+        return e;
+    }
+
     void l0_pass(int mode, const T* xin, const T* b, T* y, const T* aux, double omega) {
         const Level& l0 = *L[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (cfg.profile) { e0 = ev(); MG_CK(cudaEventRecord(e0, st)); }
+        if (cfg.profile) { e0 = prof_event(); MG_CK(cudaEventRecord(e0, st)); }
         csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
         if (cfg.profile) {
-            e1 = ev();
+            e1 = prof_event();
             MG_CK(cudaEventRecord(e1, st));
-            prof_pairs.emplace_back(e0, e1);
+            (capturing ? capturing->ev : prof_pairs).emplace_back(e0, e1);
             l0_launches++;
             l0_bytes_acc += pass_bytes(mode);
         }
@@ -327,6 +356,7 @@ class Engine : public EngineBase {
         }
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
+        invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
         stale = false;
         (void)l0;
@@ -433,6 +463,48 @@ class Engine : public EngineBase {
         }
     }
 
+    void iter_body(int ite) {
+        refresh();                                                                                   // Eq. 6
+        pcg(cfg.pcg_iters, ite);                                                                     // l.8
+        update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, cfg.omega_relax, x.p, st);  // l.9, l.11
+        lambda_add<T>(m, lambda.p, xs.p, st);                                                        // l.10
+    }
+
+    void run_iter(int ite) {
+        if (!use_graphs) { iter_body(ite); return; }
+        if ((int)graphs.size() <= ite) graphs.resize(ite + 1);
+        IterGraph& g = graphs[ite];
+        if (!g.seen) {  // first use after a (re)build: eager
+            g.seen = true;
+            iter_body(ite);
+            return;
+        }
+        if (!g.exec) {
+            const int64_t kl = g_kernel_launches, l0l = l0_launches;
+            const double l0b = l0_bytes_acc;
+            capturing = &g;
+            MG_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+            iter_body(ite);
+            cudaGraph_t graph;
+            const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+            capturing = nullptr;
+            MG_CK(ec);
+            MG_CK(cudaGraphInstantiate(&g.exec, graph, 0));
+            MG_CK(cudaGraphDestroy(graph));
+            g.launches = g_kernel_launches - kl;
+            g.l0_launches = l0_launches - l0l;
+            g.l0_bytes = l0_bytes_acc - l0b;
+            g_kernel_launches = kl; l0_launches = l0l; l0_bytes_acc = l0b;  // counted at replay
+        }
+        MG_CK(cudaGraphLaunch(g.exec, st));
+        g_kernel_launches += g.launches;
+        if (cfg.profile) {
+            l0_launches += g.l0_launches;
+            l0_bytes_acc += g.l0_bytes;
+            for (auto& pr : g.ev) prof_pairs.push_back(pr);
+        }
+    }
+
     // ------------------------------------------------------------------ Algorithm 1
     void step(double dt, int32_t n_iters) override {
         ev_used = 0;
@@ -459,10 +531,7 @@ class Engine : public EngineBase {
                 MG_CK(cudaEventRecord(s1, st));
                 setup_ran = 1;
             }
-            refresh();                                                                               // Eq. 6
-            pcg(cfg.pcg_iters, ite);                                                                 // l.8
-            update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, cfg.omega_relax, x.p, st);  // l.9, l.11
-            lambda_add<T>(m, lambda.p, xs.p, st);                                                    // l.10
+            run_iter(ite);  // Eq. 6 refresh, l.8 MGPCG, l.9-11 update
         }
         velocity(nv, x.p, x_old.p, v.p, dt, st);                                                     // l.17
         f1 = ev();

@@ -205,6 +205,24 @@ def test_deterministic(precision):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+@pytest.mark.parametrize("precision", [0, 1])
+def test_graph_replay_equals_eager(precision, monkeypatch):
+    """The captured CUDA graphs replay exactly the eager launch sequence (bitwise)."""
+    sc = scenes.make("block_small")
+    outs = []
+    for no_graph in ("1", None):
+        if no_graph:
+            monkeypatch.setenv("MGPBD_NO_GRAPH", "1")
+        else:
+            monkeypatch.delenv("MGPBD_NO_GRAPH", raising=False)
+        ctx = ctx_for(sc, precision=precision, setup_interval=2)
+        for _ in range(3):
+            ctx.step(sc.dt, 4)
+        outs.append((ctx.positions(), ctx.lambdas()))
+        ctx.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
 def test_step_argument_errors():
     sc = scenes.make("cloth16")
     ctx = ctx_for(sc)
