@@ -86,6 +86,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def traffic_per_launch():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the level-0 pass, from the committed
+    ncu --set full capture summary (profiles/ncu_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        try:
+            return json.load(open(p)).get("bytes_per_launch")
+        except Exception:
+            return None
+    return None
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -172,7 +184,7 @@ def run_ours(args):
     sc = scenes.make(args.config)
     prec = 1 if args.precision == "fp32" else 0
     stream = torch.cuda.Stream()
-    ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=1)
+    ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=0)
     for _ in range(args.warmup):
         ctx.step(sc.dt, sc.n_iters)
     st0 = ctx.stats()
@@ -183,8 +195,8 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    l0_ms = l0_bytes = 0.0
     launches = 0
+    indef = 0
     frames_ms, setup_ms = [], []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -194,15 +206,26 @@ def run_ours(args):
         for _ in range(args.steps):
             ctx.step(sc.dt, sc.n_iters)
             s = ctx.stats()
-            l0_ms += s.l0_pass_ms
-            l0_bytes += s.l0_pass_bytes
             launches += s.kernel_launches
+            indef += s.indefinite_events
             frames_ms.append(s.ms_frame)
             if s.setup_ran:
                 setup_ms.append(s.ms_setup)
         e1.record(stream)
         barrier()
     t_ms = e0.elapsed_time(e1)
+    # roofline of the dominant kernel: the same frames again with CUDA events around every level-0
+    # CSR pass (the per-iteration graphs are bypassed while profiling; kernels are identical)
+    ctx.set_profiling(True)
+    l0_ms = l0_bytes = 0.0
+    prof_frames_ms = 0.0
+    for _ in range(args.profile_frames):
+        ctx.step(sc.dt, sc.n_iters)
+        s = ctx.stats()
+        l0_ms += s.l0_pass_ms
+        l0_bytes += s.l0_pass_bytes
+        prof_frames_ms += s.ms_frame - s.ms_setup
+    ctx.set_profiling(False)
     if dist:
         tt = torch.tensor([t_ms], device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -247,11 +270,13 @@ def run_ours(args):
             "op_complexity": st0.op_complexity,
             "ms_setup_frame_extra": (statistics.mean(setup_ms) if setup_ms else None),
             "setups_in_window": len(setup_ms),
+            "indefinite_events_in_window": indef,
             "ms_frame_median": statistics.median(frames_ms)}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
-                     "kernel": "level-0 CSR passes (k_pass: omega-Jacobi / residual*P / SpMV+dot)",
-                     "peak_kind": peak_kind, "l0_pass_share_of_step": (l0_ms / t_ms) if t_ms else None},
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic_per_launch(),
+                     "kernel": "level-0 CSR passes (k_rows: omega-Jacobi / residual*P / SpMV+dot / Jacobi+r.z)",
+                     "peak_kind": peak_kind, "profiled_frames": args.profile_frames,
+                     "l0_pass_share_of_frame": (l0_ms / prof_frames_ms) if prof_frames_ms else None},
         "e2e": {"value": e2e_ms / world, "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * n * 8,
                 "d2h_bytes_per_step": (2 * 3 * n + m) * 8},
         "gpu_launches": launches,
@@ -285,6 +310,7 @@ def main():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-slab", type=int, default=8, help="x-slabs of the block the oracle sample uses")
+    ap.add_argument("--profile-frames", type=int, default=2, help="frames timed per level-0 pass for the roofline")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)

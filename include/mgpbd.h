@@ -137,6 +137,11 @@ MGPBD_API mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx);
  * the end and checks the device flags (MGPBD_E_INDEFINITE / MGPBD_E_NONFINITE). */
 MGPBD_API mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters);
 
+/* Enable (1) / disable (0) CUDA-event timing of the level-0 matrix passes (mgpbd_stats.l0_pass_*).
+ * While enabled the per-iteration CUDA graphs are not used: the same kernels launch eagerly between
+ * event records.  Errors: MGPBD_E_ARG for a NULL context. */
+MGPBD_API mgpbd_status mgpbd_set_profiling(mgpbd_ctx* ctx, int32_t on);
+
 /* Upload a new state (3*n_verts each; vel may be NULL = unchanged). */
 MGPBD_API mgpbd_status mgpbd_set_state(mgpbd_ctx* ctx, const double* pos, const double* vel);
 

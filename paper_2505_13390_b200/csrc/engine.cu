@@ -41,6 +41,7 @@ struct EngineBase {
     virtual void debug_vcycle(const double* b, double* x) = 0;
     virtual void debug_pcg(const double* b, int32_t iters, double* x) = 0;
     virtual void bind() = 0;  // make this context's device/stream current for the calling thread
+    virtual void set_profiling(int on) = 0;
     bool stale = true;
 };
 
@@ -470,8 +471,10 @@ class Engine : public EngineBase {
         lambda_add<T>(m, lambda.p, xs.p, st);                                                        // l.10
     }
 
+    void set_profiling(int on) override { cfg.profile = on ? 1 : 0; }
+
     void run_iter(int ite) {
-        if (!use_graphs) { iter_body(ite); return; }
+        if (!use_graphs || cfg.profile) { iter_body(ite); return; }  // events need eager launches
         if ((int)graphs.size() <= ite) graphs.resize(ite + 1);
         IterGraph& g = graphs[ite];
         if (!g.seen) {  // first use after a (re)build: eager
@@ -789,6 +792,10 @@ mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters) {
         return MGPBD_E_ARG;
     }
     return guarded(ctx, [&] { ctx->eng->step(dt, n_iters); });
+}
+
+mgpbd_status mgpbd_set_profiling(mgpbd_ctx* ctx, int32_t on) {
+    return guarded(ctx, [&] { ctx->eng->set_profiling(on); });
 }
 
 mgpbd_status mgpbd_set_state(mgpbd_ctx* ctx, const double* pos, const double* vel) {

@@ -16,6 +16,7 @@ DISTANCE, TET_ARAP = 2, 4
 MAX_LEVELS, MAX_ITERS = 16, 256
 
 SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgpbd_step", "mgpbd_set_state",
+           "mgpbd_set_profiling",
            "mgpbd_get_positions", "mgpbd_get_velocities", "mgpbd_get_lambda", "mgpbd_get_stats",
            "mgpbd_get_level_sizes", "mgpbd_get_level", "mgpbd_get_prolongator", "mgpbd_get_aggregates",
            "mgpbd_get_near_kernel", "mgpbd_debug_setup_from", "mgpbd_debug_vcycle", "mgpbd_debug_pcg",
@@ -74,6 +75,7 @@ def lib():
             "mgpbd_setup_hierarchy": (C.c_int, [P]),
             "mgpbd_step": (C.c_int, [P, f64, i32]),
             "mgpbd_set_state": (C.c_int, [P, P, P]),
+            "mgpbd_set_profiling": (C.c_int, [P, i32]),
             "mgpbd_get_positions": (C.c_int, [P, P]),
             "mgpbd_get_velocities": (C.c_int, [P, P]),
             "mgpbd_get_lambda": (C.c_int, [P, P]),
@@ -157,6 +159,9 @@ class Context:
 
     def step(self, dt, n_iters):
         self._ck(lib().mgpbd_step(self.h, float(dt), int(n_iters)))
+
+    def set_profiling(self, on: bool):
+        self._ck(lib().mgpbd_set_profiling(self.h, 1 if on else 0))
 
     def set_state(self, pos, vel=None):
         pos = np.ascontiguousarray(pos, np.float64)
