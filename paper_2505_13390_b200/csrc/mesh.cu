@@ -1,5 +1,6 @@
 // Constraint-side kernels of the MGPBD hot path (see mesh.cuh).
 #include <climits>
+#include <type_traits>
 
 #include "mesh.cuh"
 #include "util.cuh"
@@ -286,6 +287,55 @@ __global__ void k_eval_arap(int32_t m, const int32_t* __restrict__ verts, const 
 }
 
 // ----------------------------------------------------------------------------- assembly
+__device__ __forceinline__ void load_iv(const int4& v, int (&o)[4]) { o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w; }
+__device__ __forceinline__ void load_iv(const int2& v, int (&o)[2]) { o[0] = v.x; o[1] = v.y; }
+
+// one constraint's scaled-gradient record (KC slots x 3) with 16-/8-byte vector loads
+template <class T, int KC>
+__device__ __forceinline__ void load_record(const T* __restrict__ p, T (&o)[KC][3]) {
+    constexpr int N = KC * 3;
+    T tmp[N];
+    if constexpr (sizeof(T) == 4 && KC == 4) {
+        const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float4 v = q[k];
+            tmp[4 * k] = v.x; tmp[4 * k + 1] = v.y; tmp[4 * k + 2] = v.z; tmp[4 * k + 3] = v.w;
+        }
+    } else {
+        using V2 = typename std::conditional<sizeof(T) == 4, float2, double2>::type;
+        const V2* q = reinterpret_cast<const V2*>(p);
+#pragma unroll
+        for (int k = 0; k < N / 2; ++k) {
+            const V2 v = q[k];
+            tmp[2 * k] = v.x; tmp[2 * k + 1] = v.y;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < KC; ++k)
+#pragma unroll
+        for (int r = 0; r < 3; ++r) o[k][r] = tmp[3 * k + r];
+}
+
+// ascending vertex order of a constraint's slots (compare-exchange network, static indices)
+template <class T, int KC>
+__device__ __forceinline__ void sort_slots(int (&v)[KC], T (&hh)[KC][3]) {
+    auto cx = [&](int a, int b) {
+        const bool sw = v[b] < v[a];
+        const int ta = v[a], tb = v[b];
+        v[a] = sw ? tb : ta;
+        v[b] = sw ? ta : tb;
+#pragma unroll
+        for (int r = 0; r < 3; ++r) {
+            const T xa = hh[a][r], xb = hh[b][r];
+            hh[a][r] = sw ? xb : xa;
+            hh[b][r] = sw ? xa : xb;
+        }
+    };
+    if constexpr (KC == 4) { cx(0, 1); cx(2, 3); cx(0, 2); cx(1, 3); cx(1, 2); }
+    else cx(0, 1);
+}
+
 // Sub-warp (VL lanes) per row.  A_ij = sum over shared vertices (ascending vertex id) of
 // h_{i,v} . h_{j,v}; A_ii = sum_k |h_{i,k}|^2 + alpha_i/dt^2 (reading c14).
 template <class T, int KC, int VL>
@@ -296,40 +346,42 @@ __global__ void __launch_bounds__(256) k_assemble(int32_t m, const int32_t* __re
     const int sub = threadIdx.x % VL;
     const int64_t gsub = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VL;
     const int64_t nsub = (int64_t)gridDim.x * blockDim.x / VL;
+    using IV = typename std::conditional<KC == 4, int4, int2>::type;
     for (int64_t i = gsub; i < m; i += nsub) {
         int vi[KC];
-        double hi[KC][3];
-        for (int k = 0; k < KC; ++k) {
-            vi[k] = verts[i * KC + k];
-            for (int r = 0; r < 3; ++r) hi[k][r] = (double)h[(i * KC + k) * 3 + r];
+        T hi[KC][3];
+        {
+            const IV v4 = reinterpret_cast<const IV*>(verts)[i];
+            load_iv(v4, vi);
+            load_record<T, KC>(h + i * KC * 3, hi);
         }
-        // ascending vertex order of row i's vertices
-        int ord[KC];
-        for (int k = 0; k < KC; ++k) ord[k] = k;
-        for (int a = 1; a < KC; ++a)
-            for (int c = a; c > 0 && vi[ord[c]] < vi[ord[c - 1]]; --c) { int t = ord[c]; ord[c] = ord[c - 1]; ord[c - 1] = t; }
+        // diagonal (slot order), before the rows' vertices are sorted
+        double d = 0.0;
+#pragma unroll
+        for (int k = 0; k < KC; ++k)
+            d += (double)hi[k][0] * hi[k][0] + (double)hi[k][1] * hi[k][1] + (double)hi[k][2] * hi[k][2];
+        // ascending vertex order of row i's vertices: compare-exchange network with static indices
+        // (keeps vi/hi in registers)
+        sort_slots<T, KC>(vi, hi);
         const int64_t e0 = rowptr[i], e1 = rowptr[i + 1] - 1;
         for (int64_t e = e0 + sub; e < e1; e += VL) {
             const int32_t j = col[e];
             int vj[KC];
-            for (int k = 0; k < KC; ++k) vj[k] = verts[(int64_t)j * KC + k];
+            T hj[KC][3];
+            load_iv(reinterpret_cast<const IV*>(verts)[j], vj);
+            load_record<T, KC>(h + (int64_t)j * KC * 3, hj);  // whole record, 16-byte vectors
             double s = 0.0;
 #pragma unroll
             for (int t = 0; t < KC; ++t) {
-                const int a = ord[t];
 #pragma unroll
                 for (int q = 0; q < KC; ++q) {
-                    if (vj[q] == vi[a]) {
-                        const T* hj = h + ((int64_t)j * KC + q) * 3;
-                        s += hi[a][0] * (double)hj[0] + hi[a][1] * (double)hj[1] + hi[a][2] * (double)hj[2];
-                    }
+                    if (vj[q] == vi[t])
+                        s += (double)hi[t][0] * hj[q][0] + (double)hi[t][1] * hj[q][1] + (double)hi[t][2] * hj[q][2];
                 }
             }
             val[e] = (T)s;
         }
         if (sub == 0) {
-            double d = 0.0;
-            for (int k = 0; k < KC; ++k) d += hi[k][0] * hi[k][0] + hi[k][1] * hi[k][1] + hi[k][2] * hi[k][2];
             d += alpha[i] / dt2;
             val[e1] = (T)d;
             dinv[i] = (T)(1.0 / (double)(T)d);
