@@ -87,8 +87,12 @@ typedef struct {
     int32_t device;           /* CUDA device ordinal */
     void* stream;             /* cudaStream_t, NULL = context-owned stream */
     int32_t max_dense_coarse; /* largest coarsest level inverted densely, 8192 */
-    int32_t rank, world;      /* multi-GPU row partition; world must be 1 in this build */
+    int32_t rank, world;      /* row partition of level 0 over `world` ranks, 0 <= rank < world */
     int32_t profile;          /* 1: record CUDA events around the level-0 matrix passes */
+    const void* nccl_id;      /* world > 1: 128-byte ncclUniqueId shared by all ranks (mgpbd_nccl_unique_id on
+                                 rank 0, broadcast by the caller); one process and one GPU per rank */
+    void* vgroup;             /* alternative to nccl_id: a virtual-ranks group (mgpbd_vgroup_create) — `world`
+                                 contexts in one process, one host thread each, all on one GPU (tests) */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16
@@ -114,6 +118,9 @@ typedef struct {
     int64_t kernel_launches;           /* this library's kernel launches in the last frame */
     int32_t indefinite_events;         /* PCG iterations of the last frame with <z,r> <= 0 (r != 0):
                                           the lazily-set omega went stale; setup re-runs next frame */
+    int32_t rank, world;               /* partitioned run: this rank / number of ranks (1 otherwise) */
+    int32_t row_begin, row_end;        /* level-0 rows this rank owns */
+    int64_t halo_rows;                 /* level-0 x entries received per halo exchange */
 } mgpbd_stats;
 
 /* Fill *cfg with the defaults listed above.  Never fails for a non-NULL cfg. */
@@ -167,6 +174,23 @@ MGPBD_API mgpbd_status mgpbd_debug_setup_from(mgpbd_ctx* ctx, const double* A0_v
 /* Apply one V-cycle / K MGPCG iterations of the current hierarchy to host b (n_0) -> host x. */
 MGPBD_API mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x);
 MGPBD_API mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x);
+
+/* ---- multi-GPU (row-partitioned level 0; coarse levels and setup replicated) ----
+ * Every rank calls every function with the same inputs.  Per level-0 matrix pass the rank exchanges
+ * the halo of x with the ranks owning the rows its rows reference; dots, the level-1 restriction, the
+ * level-1 Galerkin values and dlambda are summed over ranks.  get_positions/get_lambda return the
+ * global arrays on every rank; get_level(0) values are current only for the rank's own rows. */
+/* Write a fresh 128-byte NCCL unique id (host call; rank 0 creates it, the caller broadcasts it). */
+MGPBD_API mgpbd_status mgpbd_nccl_unique_id(void* out128);
+/* Virtual ranks: a group for `world` contexts created in one process (one host thread per context). */
+MGPBD_API mgpbd_status mgpbd_vgroup_create(int32_t world, void** out);
+MGPBD_API void mgpbd_vgroup_destroy(void* group);
+/* Host-only partition logic (no device work): bounds[world+1] = row blocks balanced by nonzeros. */
+MGPBD_API mgpbd_status mgpbd_partition_rows(const int64_t* rowptr, int32_t n, int32_t world, int32_t* bounds);
+/* Host-only halo plan: recv[(q*world+p)*2 + {0,1}] = [a, b) rows rank q receives from rank p, given each
+ * rank's referenced column window [minc[q], maxc[q]]. */
+MGPBD_API mgpbd_status mgpbd_halo_plan(const int32_t* bounds, const int32_t* minc, const int32_t* maxc,
+                                       int32_t world, int32_t* recv);
 
 MGPBD_API const char* mgpbd_last_error(const mgpbd_ctx* ctx);
 MGPBD_API void mgpbd_destroy(mgpbd_ctx* ctx);

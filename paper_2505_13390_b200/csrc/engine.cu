@@ -14,6 +14,7 @@
 #include "setup.cuh"
 #include "solve.cuh"
 #include "util.cuh"
+#include "comm.cuh"
 
 namespace mgpbd {
 
@@ -74,22 +75,35 @@ class Engine : public EngineBase {
         int band_rows = 0, band_grid = 0, prod_cap = 0, band_win = 0, row_vl = 0;
         DBuf<int32_t> win_lo, win_len;
         DBuf<uint16_t> col16;
+        // rows this rank processes in the hot loop (partitioned level 0); coarse levels: all rows
+        int32_t own0 = 0, own1 = -1;
+        int32_t own_n() const { return (own1 < 0 ? n : own1) - own0; }
         void configure(cudaStream_t s) {
+            const int32_t nl = own_n();
             vl = choose_vl(n, nnz);
-            tile_config(n, nnz, rowptr, vlr, grid, tile_nnz, s);
+            tile_config(n, nnz, rowptr, vlr, grid, tile_nnz, s);  // full-range tiling (replicated setup)
+            if (nl != n) {  // the owned range is tiled from own0: size shared memory for both tilings
+                int vlr2 = 0, grid2 = 0, tn2 = 0;
+                tile_config(nl, nnz, rowptr + own0, vlr2, grid2, tn2, s);
+                tile_nnz = std::max(tile_nnz, tn2);
+                if (vlr2 == 0 || tile_nnz * 8 > 200 * 1024) vlr = 0;
+            }
             if (vlr == 0) grid = pass_grid(n, vl);
             band_rows = 0;
             if (!std::getenv("MGPBD_NO_BAND"))
-                band_config<T>(n, rowptr, col, vlr, win_lo, win_len, band_rows, band_grid, prod_cap, band_win, row_vl,
-                               col16, s);
+                band_config<T>(own0, nl, rowptr, col, vlr, win_lo, win_len, band_rows, band_grid, prod_cap, band_win,
+                               row_vl, col16, s);
         }
+        // hot == true: this rank's rows with the band kernels; false: all rows (replicated setup)
         template <class U>
-        Csr<U> view(const U* v, const U* d) const {
+        Csr<U> view(const U* v, const U* d, bool hot_rows) const {
             Csr<U> c;
-            c.n = n; c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = v; c.dinv = d;
+            c.row0 = hot_rows ? own0 : 0;
+            c.n = hot_rows ? own_n() : n;
+            c.nnz = nnz; c.rowptr = rowptr; c.col = col; c.val = v; c.dinv = d;
             c.vl = vl; c.grid = grid; c.vlr = vlr; c.tile_nnz = tile_nnz;
             c.nparts = grid;
-            if (std::is_same<U, T>::value && band_rows) {
+            if (hot_rows && band_rows) {
                 c.band_rows = band_rows; c.band_grid = band_grid; c.prod_cap = prod_cap; c.band_win = band_win;
                 c.row_vl = row_vl;
                 c.col16 = col16.p;
@@ -98,8 +112,8 @@ class Engine : public EngineBase {
             }
             return c;
         }
-        Csr<T> hot() const { return view<T>(val.p, dinv.p); }
-        Csr<double> setup_csr() const { return view<double>(val64.p, dinv64.p); }
+        Csr<T> hot() const { return view<T>(val.p, dinv.p, true); }
+        Csr<double> setup_csr() const { return view<double>(val64.p, dinv64.p, false); }
     };
 
     mgpbd_config cfg;
@@ -135,6 +149,42 @@ class Engine : public EngineBase {
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pairs;
     int64_t launches_last = 0;
     int32_t indef_events = 0;
+    // partitioned level 0 (world > 1): rows [r0, r1) of this rank, halo transfers
+    std::unique_ptr<Comm> comm;
+    bool dist = false;
+    int32_t r0 = 0, r1 = 0;
+    int64_t nnz_own = 0, halo_elems = 0;
+    std::vector<Comm::Xfer> xfers;
+    int64_t tb0 = 0, te0 = -1;  // Galerkin segments of the owned rows (level 0 -> 1)
+    DBuf<double> dsc;           // rank-local dot results before the allreduce
+
+    void setup_partition() {
+        if (cfg.vgroup) comm = make_virtual_comm(static_cast<VirtualGroup*>(cfg.vgroup), cfg.rank);
+        else comm = make_nccl_comm(cfg.nccl_id, cfg.rank, cfg.world, cfg.device);
+        dist = true;
+        const int W = cfg.world, me = cfg.rank;
+        std::vector<int64_t> hrp((size_t)m + 1);
+        d2h(hrp.data(), rowptr0.p, (size_t)m + 1, st);
+        MG_CK(cudaStreamSynchronize(st));
+        const std::vector<int32_t> bounds = partition_rows(hrp.data(), m, W);
+        std::vector<int32_t> mn(W), mx(W);
+        for (int q = 0; q < W; ++q) row_range_window(rowptr0.p, col0.p, bounds[q], bounds[q + 1], &mn[q], &mx[q], st);
+        const auto plan = halo_plan(bounds, mn, mx);
+        r0 = bounds[me];
+        r1 = bounds[me + 1];
+        nnz_own = hrp[r1] - hrp[r0];
+        xfers.clear();
+        halo_elems = 0;
+        for (int p = 0; p < W; ++p) {
+            if (p == me) continue;
+            Comm::Xfer x{p, plan[p][me], plan[me][p]};
+            if (x.send.size() || x.recv.size()) xfers.push_back(x);
+            halo_elems += x.recv.size();
+        }
+        dsc.resize(4);
+    }
+    int32_t lo0(int l) const { return (l == 0) ? r0 : 0; }
+    int32_t cnt(int l) const { return (l == 0) ? r1 - r0 : L[l]->n; }
 
     Engine(const mgpbd_mesh* mesh, const mgpbd_constraints* cons, const double* inv_mass, const double* comp,
            const mgpbd_config* c) {
@@ -180,6 +230,8 @@ class Engine : public EngineBase {
         build_incidence(verts.p, m, kc, nv, vptr, vlist, st);
         build_pattern(verts.p, m, kc, nv, vptr.p, vlist.p, rowptr0, col0, st);
         nnz0 = read_scalar(rowptr0.p + m, st);
+        r0 = 0; r1 = m; nnz_own = nnz0;
+        if (cfg.world > 1 || cfg.vgroup) setup_partition();
         h.resize((size_t)m * kc * 3); b0.resize(m);
         r.resize(m); p.resize(m); q.resize(m); xs.resize(m);
         scal.resize(2 * 4096); flags.resize(8); bn.resize(MGPBD_MAX_ITERS);
@@ -192,8 +244,11 @@ class Engine : public EngineBase {
         Level& l0 = *L[0];
         l0.n = m; l0.nnz = nnz0; l0.rowptr = rowptr0.p; l0.col = col0.p;
         l0.val.resize(nnz0); l0.dinv.resize(m);
+        l0.own0 = r0; l0.own1 = r1;
         l0.configure(st);
         alloc_vectors(l0);
+        MG_CK(cudaMemsetAsync(l0.vt.p, 0, sizeof(T) * m, st));  // restriction input: zero outside the owned rows
+        if (use_graphs && dist && !comm->graph_capturable()) use_graphs = false;
         MG_CK(cudaStreamSynchronize(st));
     }
 
@@ -223,7 +278,8 @@ class Engine : public EngineBase {
     double pass_bytes(int mode) const {
         const double s = sizeof(T);
         const double cb = (L[0]->band_rows > 0 && L[0]->row_vl > 0) ? 2.0 : 4.0;  // col16 hot copy or int32
-        double mat = (double)nnz0 * (s + cb) + 8.0 * (m + 1);
+        const double mrows = (double)(r1 - r0);
+        double mat = (double)nnz_own * (s + cb) + 8.0 * (mrows + 1);
         double vec;
         switch (mode) {
             case PASS_JACOBI: vec = 4 * s; break;          // x (gathered once), b, dinv, y
@@ -232,7 +288,7 @@ class Engine : public EngineBase {
             case PASS_SPMV_DOT: vec = 2 * s; break;        // x, y
             default: vec = 3 * s; break;
         }
-        return mat + vec * (double)m;
+        return mat + vec * mrows;
     }
 
     // ---- CUDA graphs: the solve part of each outer iteration (Galerkin refresh, coarsest inverse,
@@ -278,7 +334,11 @@ class Engine : public EngineBase {
     }
 
     void pass(int l, int mode, const T* xin, const T* b, T* y, const T* aux, double omega) {
-        if (l == 0) l0_pass(mode, xin, b, y, aux, omega);
+        if (l == 0) {
+            // partitioned level 0: bring the halo columns of x from the owning ranks first
+            if (dist) comm->exchange(const_cast<T*>(xin), sizeof(T), xfers, st);
+            l0_pass(mode, xin, b, y, aux, omega);
+        }
         else csr_pass<T>(mode, L[l]->hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
     }
 
@@ -355,6 +415,12 @@ class Engine : public EngineBase {
                 a.tval.resize(a.plan.T);
             }
         }
+        if (dist && nL > 1) {  // level-0 Galerkin segments of the owned rows; the others stay zero
+            Level& a = *L[0];
+            tb0 = read_scalar(a.plan.tptr.p + r0, st);
+            te0 = read_scalar(a.plan.tptr.p + r1, st);
+            MG_CK(cudaMemsetAsync(a.tval.p, 0, sizeof(T) * (a.plan.T ? a.plan.T : 1), st));
+        }
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
         invalidate_graphs();  // buffers of the hierarchy changed
@@ -383,6 +449,13 @@ class Engine : public EngineBase {
         for (int l = 0; l + 1 < nL; ++l) {
             Level& a = *L[l];
             Level& c = *L[l + 1];
+            if (l == 0 && dist) {  // this rank's fine rows only, then sum the partial coarse values
+                galerkin_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.P.p, a.n_agg, c.rowptr, c.nnz, a.tval.p,
+                                    c.val.p, nullptr, st, tb0, te0);
+                comm->allreduce(c.val.p, (size_t)c.nnz, st);
+                diag_inv<T>(c.n, c.rowptr, c.val.p, c.dinv.p, st);
+                continue;
+            }
             galerkin_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.P.p, a.n_agg, c.rowptr, c.nnz, a.tval.p, c.val.p,
                                 c.dinv.p, st);
         }
@@ -401,7 +474,8 @@ class Engine : public EngineBase {
         const int nu = cfg.smoother_sweeps;
         T* cur = a.vx.p;
         T* nxt = a.vy.p;
-        vec_jacobi0<T>(a.n, a.dinv.p, b, a.omega, cur, st);
+        const int32_t o = lo0(l), cn = cnt(l);  // rows this rank updates at this level
+        vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.omega, cur + o, st);
         for (int sw = 1; sw < nu; ++sw) {
             pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.omega);
             std::swap(cur, nxt);
@@ -409,8 +483,9 @@ class Engine : public EngineBase {
         pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
         Level& c = *L[l + 1];
         restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
+        if (l == 0 && dist) comm->allreduce(c.vb.p, (size_t)c.n, st);  // partial sums of split aggregates
         vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
-        prolong_add<T>(a.n, a.agg.p, a.P.p, c.vz.p, cur, st);
+        prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
         for (int sw = 0; sw < nu; ++sw) {
             const bool last = sw == nu - 1;
             T* dst = last ? x_out : (cur == a.vx.p ? a.vy.p : a.vx.p);
@@ -427,6 +502,8 @@ class Engine : public EngineBase {
         d2d(r.p, b0.p, m, st);
         MG_CK(cudaMemsetAsync(p.p, 0, sizeof(T) * m, st));
         T* z = l0.vz.p;
+        const int32_t o = r0, cn = r1 - r0;
+        if (dist && nL == 1) throw Error(MGPBD_E_ARG, "a partitioned solve needs at least two levels");
         for (int k = 0; k < iters; ++k) {
             const int tag = ite * 4096 + k;
             if (nL == 1) {
@@ -436,25 +513,40 @@ class Engine : public EngineBase {
             } else {
                 vcycle(0, r.p, z, r.p);
             }
-            pcg_finalize_rz(parts1.p, parts2.p, l0.hot().nparts, scal.p, k, flags.p, tag, st);
-            pcg_update_p<T>(m, z, p.p, scal.p, k, st);
-            l0_pass(PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
-            pcg_finalize_pq(parts1.p, l0.hot().nparts, scal.p, k, flags.p, tag, st);
-            pcg_update_xr<T>(m, p.p, q.p, xs.p, r.p, scal.p, k, st);
+            const int np = nL == 1 ? l0.grid : l0.hot().nparts;
+            if (dist) {  // rank-local sums -> allreduce -> checks on the global values
+                finalize_sum(parts1.p, np, dsc.p, st);
+                finalize_sum(parts2.p, np, dsc.p + 1, st);
+                comm->allreduce(dsc.p, 2, st);
+                pcg_commit_rz(dsc.p, scal.p, k, flags.p, tag, st);
+            } else {
+                pcg_finalize_rz(parts1.p, parts2.p, np, scal.p, k, flags.p, tag, st);
+            }
+            pcg_update_p<T>(cn, z + o, p.p + o, scal.p, k, st);
+            pass(0, PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
+            if (dist) {
+                finalize_sum(parts1.p, l0.hot().nparts, dsc.p + 2, st);
+                comm->allreduce(dsc.p + 2, 1, st);
+                pcg_commit_pq(dsc.p + 2, scal.p, k, flags.p, tag, st);
+            } else {
+                pcg_finalize_pq(parts1.p, l0.hot().nparts, scal.p, k, flags.p, tag, st);
+            }
+            pcg_update_xr<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, st);
         }
     }
 
     void assemble_hot(double dt) {
         Level& l0 = *L[0];
         eval_constraints<T>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h.p, b0.p, st);
-        assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st);
+        // (all constraints are evaluated on every rank: h of the halo constraints is needed locally)
+        assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st, r0, r1);
     }
 
     void assemble_setup(double dt) {
         Level& l0 = *L[0];
         l0.val64.resize(nnz0);
         l0.dinv64.resize(m);
-        if (std::is_same<T, double>::value) {
+        if (std::is_same<T, double>::value && !dist) {
             d2d(l0.val64.p, (const double*)l0.val.p, nnz0, st);
             d2d(l0.dinv64.p, (const double*)l0.dinv.p, m, st);
         } else {
@@ -467,6 +559,7 @@ class Engine : public EngineBase {
     void iter_body(int ite) {
         refresh();                                                                                   // Eq. 6
         pcg(cfg.pcg_iters, ite);                                                                     // l.8
+        if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
         update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, cfg.omega_relax, x.p, st);  // l.9, l.11
         lambda_add<T>(m, lambda.p, xs.p, st);                                                        // l.10
     }
@@ -602,6 +695,11 @@ class Engine : public EngineBase {
         s->ms_frame = ms_frame;
         s->kernel_launches = launches_last;
         s->indefinite_events = indef_events;
+        s->rank = dist ? comm->rank() : 0;
+        s->world = dist ? comm->world() : 1;
+        s->row_begin = r0;
+        s->row_end = r1;
+        s->halo_rows = halo_elems;
     }
 
     void check_level(int l) {
@@ -731,6 +829,8 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->max_dense_coarse = 2048;
     c->rank = 0; c->world = 1;
     c->profile = 0;
+    c->nccl_id = nullptr;
+    c->vgroup = nullptr;
     return MGPBD_OK;
 }
 
@@ -748,7 +848,8 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if ((int64_t)cons->n_cons * cons->kind >= ((int64_t)1 << 31)) return fail("too many constraints");
     if (cfg->precision != 0 && cfg->precision != 1) return fail("precision must be 0 (fp64) or 1 (fp32)");
     if (cfg->k_nullspace != 1) return fail("only k_nullspace = 1 is implemented (reading c1)");
-    if (cfg->world != 1) return fail("world > 1 is not supported by this build");
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail("bad rank/world");
+    if (cfg->world > 1 && !cfg->nccl_id && !cfg->vgroup) return fail("world > 1 needs nccl_id or vgroup");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > 4096 || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
         cfg->max_dense_coarse < 1)
@@ -848,6 +949,41 @@ mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, dou
     if (ctx && (!b || !x || iters < 0 || iters > 4096)) return MGPBD_E_ARG;
     return guarded(ctx, [&] { ctx->eng->debug_pcg(b, iters, x); });
 }
+mgpbd_status mgpbd_nccl_unique_id(void* out128) {
+    if (!out128) return MGPBD_E_ARG;
+    try {
+        mgpbd::nccl_unique_id(out128);
+    } catch (const Error& e) {
+        g_create_err = e.what();
+        return (mgpbd_status)e.status;
+    }
+    return MGPBD_OK;
+}
+mgpbd_status mgpbd_vgroup_create(int32_t world, void** out) {
+    if (!out || world < 1 || world > 8) return MGPBD_E_ARG;
+    *out = mgpbd::vgroup_create(world);
+    return MGPBD_OK;
+}
+void mgpbd_vgroup_destroy(void* g) { mgpbd::vgroup_destroy(static_cast<mgpbd::VirtualGroup*>(g)); }
+mgpbd_status mgpbd_partition_rows(const int64_t* rowptr, int32_t n, int32_t world, int32_t* bounds) {
+    if (!rowptr || !bounds || n < 0 || world < 1) return MGPBD_E_ARG;
+    const std::vector<int32_t> b = mgpbd::partition_rows(rowptr, n, world);
+    std::memcpy(bounds, b.data(), sizeof(int32_t) * b.size());
+    return MGPBD_OK;
+}
+mgpbd_status mgpbd_halo_plan(const int32_t* bounds, const int32_t* minc, const int32_t* maxc, int32_t world,
+                             int32_t* recv) {
+    if (!bounds || !minc || !maxc || !recv || world < 1) return MGPBD_E_ARG;
+    std::vector<int32_t> b(bounds, bounds + world + 1), mn(minc, minc + world), mx(maxc, maxc + world);
+    const auto plan = mgpbd::halo_plan(b, mn, mx);
+    for (int q = 0; q < world; ++q)
+        for (int p = 0; p < world; ++p) {
+            recv[(q * world + p) * 2] = plan[q][p].a;
+            recv[(q * world + p) * 2 + 1] = plan[q][p].b;
+        }
+    return MGPBD_OK;
+}
+
 const char* mgpbd_last_error(const mgpbd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 void mgpbd_destroy(mgpbd_ctx* ctx) {
     if (!ctx) return;

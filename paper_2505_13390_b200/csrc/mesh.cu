@@ -339,7 +339,7 @@ __device__ __forceinline__ void sort_slots(int (&v)[KC], T (&hh)[KC][3]) {
 // Sub-warp (VL lanes) per row.  A_ij = sum over shared vertices (ascending vertex id) of
 // h_{i,v} . h_{j,v}; A_ii = sum_k |h_{i,k}|^2 + alpha_i/dt^2 (reading c14).
 template <class T, int KC, int VL>
-__global__ void __launch_bounds__(256) k_assemble(int32_t m, const int32_t* __restrict__ verts, const T* __restrict__ h,
+__global__ void __launch_bounds__(256) k_assemble(int32_t row0, int32_t m, const int32_t* __restrict__ verts, const T* __restrict__ h,
                                                   const double* __restrict__ alpha, double dt2,
                                                   const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                   T* __restrict__ val, T* __restrict__ dinv) {
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) k_assemble(int32_t m, const int32_t* __re
     const int64_t gsub = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / VL;
     const int64_t nsub = (int64_t)gridDim.x * blockDim.x / VL;
     using IV = typename std::conditional<KC == 4, int4, int2>::type;
-    for (int64_t i = gsub; i < m; i += nsub) {
+    for (int64_t i = row0 + gsub; i < m; i += nsub) {  // rows [row0, m)
         int vi[KC];
         T hi[KC][3];
         {
@@ -516,12 +516,14 @@ void eval_constraints(int kind, int32_t m, const int32_t* verts, const double* x
 
 template <class T>
 void assemble(int kind, int32_t m, const int32_t* verts, const T* h, const double* alpha, double dt,
-              const int64_t* rowptr, const int32_t* col, int vl, T* val, T* dinv, cudaStream_t s) {
-    if (!m) return;
+              const int64_t* rowptr, const int32_t* col, int vl, T* val, T* dinv, cudaStream_t s, int32_t row0,
+              int32_t row1) {
+    if (row1 < 0) row1 = m;
+    if (row1 <= row0) return;
     double dt2 = dt * dt;
-    int64_t threads = (int64_t)m * vl;
+    int64_t threads = (int64_t)(row1 - row0) * vl;
     int grid = (int)std::min<int64_t>((threads + 255) / 256, 148 * 16);
-#define MG_ASM(KC, VL) k_assemble<T, KC, VL><<<grid, 256, 0, s>>>(m, verts, h, alpha, dt2, rowptr, col, val, dinv)
+#define MG_ASM(KC, VL) k_assemble<T, KC, VL><<<grid, 256, 0, s>>>(row0, row1, verts, h, alpha, dt2, rowptr, col, val, dinv)
     if (kind == 2) {
         if (vl <= 4) MG_ASM(2, 4); else if (vl <= 8) MG_ASM(2, 8); else MG_ASM(2, 16);
     } else {
@@ -565,7 +567,7 @@ void sqrt_vec(int32_t n, const double* w, double* out, cudaStream_t s) {
     template void eval_constraints<T>(int, int32_t, const int32_t*, const double*, const double*, const double*, \
                                       const double*, double, const double*, T*, T*, cudaStream_t);           \
     template void assemble<T>(int, int32_t, const int32_t*, const T*, const double*, double, const int64_t*,  \
-                              const int32_t*, int, T*, T*, cudaStream_t);                                    \
+                              const int32_t*, int, T*, T*, cudaStream_t, int32_t, int32_t);                  \
     template void update_positions<T>(int32_t, int, const int64_t*, const int32_t*, const T*, const double*,  \
                                       const T*, double, double*, cudaStream_t);                              \
     template void lambda_add<T>(int32_t, double*, const T*, cudaStream_t);

@@ -26,7 +26,8 @@ void eval_constraints(int kind, int32_t m, const int32_t* verts, const double* x
 // Numeric re-assembly (Alg. 1 l.5) into the fixed pattern; also dinv = 1/A_ii.
 template <class T>
 void assemble(int kind, int32_t m, const int32_t* verts, const T* h, const double* alpha, double dt,
-              const int64_t* rowptr, const int32_t* col, int vl, T* val, T* dinv, cudaStream_t s);
+              const int64_t* rowptr, const int32_t* col, int vl, T* val, T* dinv, cudaStream_t s, int32_t row0 = 0,
+              int32_t row1 = -1);  // rows [row0, row1) (default: all m)
 
 void predict(int32_t n, double* x, double* v, double* x_old, const double* w, double dt,
              double gx, double gy, double gz, cudaStream_t s);

@@ -592,16 +592,20 @@ void galerkin_symbolic(int32_t n, const int64_t* rowptr, const int32_t* col, con
 
 template <class T>
 void galerkin_numeric(const GalerkinPlan& plan, const int64_t* rowptr, const int32_t* col, const T* val, const T* P,
-                      int32_t n_agg, const int64_t* crowptr, int64_t cnnz, T* tval, T* cval, T* cdinv, cudaStream_t s) {
-    if (plan.T) {
-        k_gal1<T><<<g1(plan.T), 256, 0, s>>>(plan.T, plan.tstart.p, plan.trow.p, rowptr, col, plan.gperm.p, val, P, tval);
+                      int32_t n_agg, const int64_t* crowptr, int64_t cnnz, T* tval, T* cval, T* cdinv, cudaStream_t s,
+                      int64_t t_begin, int64_t t_end) {
+    if (t_end < 0) t_end = plan.T;
+    if (t_end > t_begin) {
+        const int64_t nt = t_end - t_begin;
+        k_gal1<T><<<g1(nt), 256, 0, s>>>(nt, plan.tstart.p + t_begin, plan.trow.p + t_begin, rowptr, col,
+                                        plan.gperm.p, val, P, tval + t_begin);
         MG_LAUNCH_CHECK();
     }
     if (cnnz) {
         k_gal2<T><<<g1(cnnz), 256, 0, s>>>(cnnz, plan.lptr.p, plan.llist.p, tval, cval);
         MG_LAUNCH_CHECK();
     }
-    diag_inv<T>(n_agg, crowptr, cval, cdinv, s);
+    if (cdinv) diag_inv<T>(n_agg, crowptr, cval, cdinv, s);
 }
 
 template <class T>
@@ -630,7 +634,8 @@ double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int leve
 
 #define MG_INST(T)                                                                                             \
     template void galerkin_numeric<T>(const GalerkinPlan&, const int64_t*, const int32_t*, const T*, const T*,  \
-                                      int32_t, const int64_t*, int64_t, T*, T*, T*, cudaStream_t);             \
+                                      int32_t, const int64_t*, int64_t, T*, T*, T*, cudaStream_t, int64_t,     \
+                                      int64_t);                                                                \
     template void diag_inv<T>(int32_t, const int64_t*, const T*, T*, cudaStream_t);
 MG_INST(float)
 MG_INST(double)

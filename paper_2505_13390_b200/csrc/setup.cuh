@@ -47,7 +47,8 @@ void galerkin_symbolic(int32_t n, const int64_t* rowptr, const int32_t* col, con
 template <class T>
 void galerkin_numeric(const GalerkinPlan& plan, const int64_t* rowptr, const int32_t* col, const T* val,
                       const T* P, int32_t n_agg, const int64_t* crowptr, int64_t cnnz, T* tval, T* cval, T* cdinv,
-                      cudaStream_t s);
+                      cudaStream_t s, int64_t t_begin = 0, int64_t t_end = -1);
+// (segments [t_begin, t_end) only — the others keep their tval; cdinv == nullptr skips 1/diag)
 
 template <class T>
 void diag_inv(int32_t n, const int64_t* rowptr, const T* val, T* dinv, cudaStream_t s);

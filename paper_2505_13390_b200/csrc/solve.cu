@@ -19,7 +19,7 @@ inline int vgrid(int64_t n) {
 // One fused pass over a CSR matrix, VL lanes per row, grid-stride over rows with a warp-uniform loop
 // (so the fixed-order sub-warp butterfly is always executed by full warps).
 template <class T, int VL, int MODE>
-__global__ void __launch_bounds__(PB) k_pass(int32_t n, const int64_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(PB) k_pass(int32_t row0, int32_t n, const int64_t* __restrict__ rowptr,
                                              const int32_t* __restrict__ col, const T* __restrict__ val,
                                              const T* __restrict__ dinv, const T* __restrict__ x,
                                              const T* __restrict__ b, T* __restrict__ y,
@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(PB) k_pass(int32_t n, const int64_t* __restric
     const int64_t gw = ((int64_t)blockIdx.x * PB + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * PB) >> 5;
     double acc1 = 0.0, acc2 = 0.0;
-    for (int64_t r0 = gw * RPW; r0 < n; r0 += nw * RPW) {
+    for (int64_t r0 = row0 + gw * RPW; r0 < n; r0 += nw * RPW) {  // rows [row0, n)
         const int64_t i = r0 + rid;
         const bool valid = i < n;
         double s = 0.0;
@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(PB) k_pass(int32_t n, const int64_t* __restric
 // val/col/x[col] for the whole tile with coalesced, independent loads (many in flight per thread),
 // keeps the fp64 products in shared memory, then VLR lanes per row reduce them in fixed order.
 template <class T, int VLR, int MODE>
-__global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restrict__ rowptr,
+__global__ void __launch_bounds__(PB) k_tile(int32_t row0, int32_t n, const int64_t* __restrict__ rowptr,
                                              const int32_t* __restrict__ col, const T* __restrict__ val,
                                              const T* __restrict__ dinv, const T* __restrict__ x,
                                              const T* __restrict__ b, T* __restrict__ y,
@@ -87,10 +87,10 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restric
     extern __shared__ double prod[];
     constexpr int R = PB / VLR;
     const int rr = threadIdx.x / VLR, ln = threadIdx.x % VLR;
-    const int64_t ntiles = ((int64_t)n + R - 1) / R;
+    const int64_t ntiles = ((int64_t)n - row0 + R - 1) / R;  // rows [row0, n)
     double acc1 = 0.0, acc2 = 0.0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t r0 = tile * R;
+        const int64_t r0 = row0 + tile * R;
         const int64_t r1 = r0 + R < n ? r0 + R : n;
         const int64_t e0 = rowptr[r0];
         const int ne = (int)(rowptr[r1] - e0);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t n, const int64_t* __restric
 constexpr int BB = 1024;
 constexpr int BAND_EPT = 12;  // stream elements per thread per sub-tile (sub-tile nnz + 6 <= BAND_EPT*BB)
 template <class T, int VLR, int MODE>
-__global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
+__global__ void __launch_bounds__(BB, 1) k_band(int32_t row0, int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
                                                 const int32_t* __restrict__ win_len, int prod_cap,
                                                 const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                 const T* __restrict__ val, const T* __restrict__ dinv,
@@ -161,11 +161,11 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
     T* xs = prod + prod_cap + 8;  // prod holds up to 3 leading + 3 trailing vector lanes beyond the tile
     constexpr int R = BB / VLR;
     const int rr = threadIdx.x / VLR, ln = threadIdx.x % VLR;
-    const int32_t nband = (n + C - 1) / C;
+    const int32_t nband = (n - row0 + C - 1) / C;  // rows [row0, n)
     double acc1 = 0.0, acc2 = 0.0;
     for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
         const int32_t lo = win_lo[bt], len = win_len[bt];
-        const int32_t c0 = bt * C, c1 = c0 + C < n ? c0 + C : n;
+        const int32_t c0 = row0 + bt * C, c1 = c0 + C < n ? c0 + C : n;
         __syncthreads();
         for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
         __syncthreads();
@@ -276,19 +276,21 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t n, int32_t C, const int3
 // while it reduces the current one.  Rows have at most ROWCH*VL entries (checked at configuration).
 constexpr int ROWCH = 5;
 // col16[e] = col[e] - win_lo[band tile of the row]: the hot copy of the level-0 column indices.
-__global__ void k_col16(int32_t n, int32_t C, const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-                        const int32_t* __restrict__ win_lo, uint16_t* __restrict__ col16) {
+__global__ void k_col16(int32_t row0, int32_t n, int32_t C, const int64_t* __restrict__ rowptr,
+                        const int32_t* __restrict__ col, const int32_t* __restrict__ win_lo,
+                        uint16_t* __restrict__ col16) {
     const int lane = threadIdx.x & 31;
     const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t i = w0; i < n; i += nw) {
-        const int32_t lo = win_lo[i / C];
+    for (int64_t li = w0; li < n; li += nw) {
+        const int64_t i = row0 + li;
+        const int32_t lo = win_lo[li / C];
         for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) col16[e] = (uint16_t)(col[e] - lo);
     }
 }
 
 template <class T, int VL, int MODE>
-__global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
+__global__ void __launch_bounds__(BB, 1) k_rows(int32_t row0, int32_t n, int32_t C, const int32_t* __restrict__ win_lo,
                                                 const int32_t* __restrict__ win_len,
                                                 const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ col,
                                                 const T* __restrict__ val, const T* __restrict__ dinv,
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
     constexpr int NSLOT = (BB / 32) * SPW;    // rows in flight per CTA step
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int sub = lane / VL, sl = lane % VL;
-    const int32_t nband = (n + C - 1) / C;
+    const int32_t nband = (n - row0 + C - 1) / C;  // rows [row0, n)
     double acc1 = 0.0, acc2 = 0.0;
     struct Row {
         int32_t i;
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t n, int32_t C, const int3
     constexpr bool NA = MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P;
     for (int32_t bt = blockIdx.x; bt < nband; bt += gridDim.x) {
         const int32_t lo = win_lo[bt], len = win_len[bt];
-        const int32_t c0 = bt * C, c1 = c0 + C < n ? c0 + C : n;
+        const int32_t c0 = row0 + bt * C, c1 = c0 + C < n ? c0 + C : n;
         const int64_t ebase = rowptr[c0];
         __syncthreads();
         for (int32_t k = threadIdx.x; k < len; k += BB) xs[k] = x[lo + k];
@@ -416,7 +418,7 @@ void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         MG_CK(cudaFuncSetAttribute(k_rows<T, VL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col16,
+    k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.row0, A.row0 + A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col16,
                                                      A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
     MG_LAUNCH_CHECK();
 }
@@ -441,7 +443,7 @@ void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         MG_CK(cudaFuncSetAttribute(k_band<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    k_band<T, VLR, MODE><<<A.band_grid, BB, smem, s>>>(A.n, A.band_rows, A.win_lo, A.win_len, A.prod_cap, A.rowptr,
+    k_band<T, VLR, MODE><<<A.band_grid, BB, smem, s>>>(A.row0, A.row0 + A.n, A.band_rows, A.win_lo, A.win_len, A.prod_cap, A.rowptr,
                                                       A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
     MG_LAUNCH_CHECK();
 }
@@ -460,18 +462,19 @@ void launch_band_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* au
 }
 
 // per band tile: the column window [min col, max col] of its rows (diagonal-last CSR)
-__global__ void k_band_windows(int32_t n, int32_t C, const int64_t* __restrict__ rowptr,
+__global__ void k_band_windows(int32_t row0, int32_t n, int32_t C, const int64_t* __restrict__ rowptr,
                                const int32_t* __restrict__ col, int32_t* __restrict__ lo, int32_t* __restrict__ hi) {
-    int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+    int32_t li = blockIdx.x * blockDim.x + threadIdx.x;
+    if (li >= n) return;
+    const int32_t i = row0 + li;
     const int64_t a = rowptr[i], z = rowptr[i + 1];
     int32_t mn = i, mx = i;
     if (z - a > 1) {
         mn = min(mn, col[a]);
         mx = max(mx, col[z - 2]);
     }
-    atomicMin(&lo[i / C], mn);
-    atomicMax(&hi[i / C], mx);
+    atomicMin(&lo[li / C], mn);
+    atomicMax(&hi[li / C], mx);
 }
 __global__ void k_band_len(int32_t nb, int32_t* __restrict__ lo, const int32_t* __restrict__ hi, int32_t* len,
                            int32_t* maxlen) {
@@ -490,7 +493,7 @@ void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         MG_CK(cudaFuncSetAttribute(k_tile<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
+    k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
     MG_LAUNCH_CHECK();
 }
 
@@ -518,7 +521,7 @@ __global__ void k_max_tile(int32_t n, int R, const int64_t* __restrict__ rowptr,
 template <class T, int MODE>
 void launch_pass_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
                       double* parts2, cudaStream_t s) {
-#define MG_P(VL) k_pass<T, VL, MODE><<<A.grid, PB, 0, s>>>(A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2)
+#define MG_P(VL) k_pass<T, VL, MODE><<<A.grid, PB, 0, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2)
     switch (A.vl) {
         case 2: MG_P(2); break;
         case 4: MG_P(4); break;
@@ -820,15 +823,16 @@ __global__ void k_rowlen_max2(int32_t n, const int64_t* __restrict__ rowptr, int
 }  // namespace
 
 template <class T>
-bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
-                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, DBuf<uint16_t>& col16, cudaStream_t s) {
+bool band_config(int32_t row0, int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo,
+                 DBuf<int32_t>& len, int& C, int& grid, int& prod_cap, int& win, int& row_vl, DBuf<uint16_t>& col16,
+                 cudaStream_t s) {
     C = 0;
     row_vl = 0;
     if (n < 4096 || vlr <= 0) return false;
     DBuf<int32_t> tmp, hi;
     tmp.resize(2);
     MG_CK(cudaMemsetAsync(tmp.p, 0, 2 * sizeof(int32_t), s));
-    k_rowlen_max2<<<ceil_div(n, 256), 256, 0, s>>>(n, rowptr, tmp.p);
+    k_rowlen_max2<<<ceil_div(n, 256), 256, 0, s>>>(n, rowptr + row0, tmp.p);
     MG_LAUNCH_CHECK();
     int32_t maxrow = 0;
     MG_CK(cudaMemcpyAsync(&maxrow, tmp.p, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
@@ -841,7 +845,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
         lo.resize(nb); hi.resize(nb); len.resize(nb);
         fill_i32(lo.p, INT32_MAX, nb, s);
         fill_i32(hi.p, -1, nb, s);
-        k_band_windows<<<ceil_div(n, 256), 256, 0, s>>>(n, c, rowptr, col, lo.p, hi.p);
+        k_band_windows<<<ceil_div(n, 256), 256, 0, s>>>(row0, n, c, rowptr, col, lo.p, hi.p);
         MG_LAUNCH_CHECK();
         MG_CK(cudaMemsetAsync(tmp.p + 1, 0, sizeof(int32_t), s));
         k_band_len<<<ceil_div(nb, 256), 256, 0, s>>>(nb, lo.p, hi.p, len.p, tmp.p + 1);
@@ -855,7 +859,7 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     //    holds the band tile's row offsets, its per-row operands and the x window.  Band tiles are
     //    sized so every CTA gets the same whole number of them (k per SM).
     {
-        const double avg = (double)read_scalar(rowptr + n, s) / n;
+        const double avg = (double)(read_scalar(rowptr + row0 + n, s) - read_scalar(rowptr + row0, s)) / n;
         int v = 4;
         while (v < 32 && v * 5 < avg) v *= 2;
         while (v < 32 && maxrow > ROWCH * v) v *= 2;
@@ -867,10 +871,10 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
                 if (mw <= 65536 && need <= budget) {
                     const int32_t nb = (n + c - 1) / c;
                     C = c; win = mw; grid = nb < 148 ? nb : 148; row_vl = v;
-                    const int64_t nnz = read_scalar(rowptr + n, s);
+                    const int64_t nnz = read_scalar(rowptr + row0 + n, s);  // global positions up to the range end
                     col16.resize(nnz);
                     k_col16<<<(int)std::min<int64_t>(((int64_t)n * 32 + 255) / 256, 148 * 16), 256, 0, s>>>(
-                        n, c, rowptr, col, lo.p, col16.p);
+                        row0, n, c, rowptr, col, lo.p, col16.p);
                     MG_LAUNCH_CHECK();
                     MG_CK(cudaStreamSynchronize(s));
                     return true;
@@ -891,10 +895,65 @@ bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, 
     }
     return false;
 }
-template bool band_config<float>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
-                                 int&, int&, int&, int&, DBuf<uint16_t>&, cudaStream_t);
-template bool band_config<double>(int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&, int&,
-                                  int&, int&, int&, int&, DBuf<uint16_t>&, cudaStream_t);
+template bool band_config<float>(int32_t, int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&, DBuf<int32_t>&,
+                                 int&, int&, int&, int&, int&, DBuf<uint16_t>&, cudaStream_t);
+template bool band_config<double>(int32_t, int32_t, const int64_t*, const int32_t*, int, DBuf<int32_t>&,
+                                  DBuf<int32_t>&, int&, int&, int&, int&, int&, DBuf<uint16_t>&, cudaStream_t);
+
+namespace {
+__global__ void k_commit_rz(const double* __restrict__ d2, double* scal, int k, int* flags, int tag) {
+    const double a = d2[0], c = d2[1];
+    scal[2 * k] = a;
+    if (!isfinite(a) || !isfinite(c)) {
+        if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+    } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
+        if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+        atomicAdd(&flags[4], 1);
+    }
+}
+__global__ void k_commit_pq(const double* __restrict__ d1, double* scal, int k, int* flags, int tag) {
+    const double a = d1[0];
+    scal[2 * k + 1] = a;
+    if (!isfinite(a)) {
+        if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+    }
+}
+__global__ void k_range_window(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int32_t a,
+                               int32_t b, int32_t* out) {
+    int32_t i = a + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= b) return;
+    const int64_t e0 = rowptr[i], e1 = rowptr[i + 1];
+    int32_t mn = i, mx = i;
+    if (e1 - e0 > 1) { mn = min(mn, col[e0]); mx = max(mx, col[e1 - 2]); }
+    atomicMin(&out[0], mn);
+    atomicMax(&out[1], mx);
+}
+}  // namespace
+
+void pcg_commit_rz(const double* d2, double* scal, int k, int* flags, int tag, cudaStream_t s) {
+    k_commit_rz<<<1, 1, 0, s>>>(d2, scal, k, flags, tag);
+    MG_LAUNCH_CHECK();
+}
+void pcg_commit_pq(const double* d1, double* scal, int k, int* flags, int tag, cudaStream_t s) {
+    k_commit_pq<<<1, 1, 0, s>>>(d1, scal, k, flags, tag);
+    MG_LAUNCH_CHECK();
+}
+void row_range_window(const int64_t* rowptr, const int32_t* col, int32_t a, int32_t b, int32_t* lo, int32_t* hi,
+                      cudaStream_t s) {
+    DBuf<int32_t> d;
+    d.resize(2);
+    int32_t init[2] = {INT32_MAX, -1};
+    h2d(d.p, init, 2, s);
+    if (b > a) {
+        k_range_window<<<ceil_div(b - a, 256), 256, 0, s>>>(rowptr, col, a, b, d.p);
+        MG_LAUNCH_CHECK();
+    }
+    int32_t out[2];
+    d2h(out, d.p, 2, s);
+    MG_CK(cudaStreamSynchronize(s));
+    *lo = out[0] == INT32_MAX ? a : out[0];
+    *hi = out[1] < 0 ? a - 1 : out[1];
+}
 
 int pass_grid(int32_t n, int vl) {
     int rows_per_block = PB / vl;

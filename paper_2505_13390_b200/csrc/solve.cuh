@@ -8,6 +8,7 @@ namespace mgpbd {
 
 template <class T>
 struct Csr {
+    int32_t row0 = 0;  // first row processed (global index); rows [row0, row0 + n)
     int32_t n = 0;
     int64_t nnz = 0;
     const int64_t* rowptr = nullptr;
@@ -31,8 +32,17 @@ struct Csr {
 // the smallest band tile does not fit in shared memory next to the product buffer.  With the row
 // kernel (row_vl > 0) it also builds col16, the 16-bit window-relative copy of the column indices.
 template <class T>
-bool band_config(int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo, DBuf<int32_t>& len,
-                 int& C, int& grid, int& prod_cap, int& win, int& row_vl, DBuf<uint16_t>& col16, cudaStream_t s);
+bool band_config(int32_t row0, int32_t n, const int64_t* rowptr, const int32_t* col, int vlr, DBuf<int32_t>& lo,
+                 DBuf<int32_t>& len, int& C, int& grid, int& prod_cap, int& win, int& row_vl, DBuf<uint16_t>& col16,
+                 cudaStream_t s);
+
+// PCG scalar commit for a partitioned solve: d2 = (r.z, r.r) or d1 = (p.q) already summed over ranks.
+void pcg_commit_rz(const double* d2, double* scal, int k, int* flags, int tag, cudaStream_t s);
+void pcg_commit_pq(const double* d1, double* scal, int k, int* flags, int tag, cudaStream_t s);
+
+// Column window [min col, max col] referenced by rows [a, b) (diagonal-last CSR); host result.
+void row_range_window(const int64_t* rowptr, const int32_t* col, int32_t a, int32_t b, int32_t* lo, int32_t* hi,
+                      cudaStream_t s);
 
 // Choose the row-tile configuration of a level (vlr, fixed grid, max tile nnz); vlr = 0 if the tile
 // would not fit in shared memory.

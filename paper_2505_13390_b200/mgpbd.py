@@ -20,7 +20,8 @@ SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgp
            "mgpbd_get_positions", "mgpbd_get_velocities", "mgpbd_get_lambda", "mgpbd_get_stats",
            "mgpbd_get_level_sizes", "mgpbd_get_level", "mgpbd_get_prolongator", "mgpbd_get_aggregates",
            "mgpbd_get_near_kernel", "mgpbd_debug_setup_from", "mgpbd_debug_vcycle", "mgpbd_debug_pcg",
-           "mgpbd_last_error", "mgpbd_destroy"]
+           "mgpbd_last_error", "mgpbd_destroy", "mgpbd_nccl_unique_id", "mgpbd_vgroup_create",
+           "mgpbd_vgroup_destroy", "mgpbd_partition_rows", "mgpbd_halo_plan"]
 
 
 class MgpbdError(RuntimeError):
@@ -45,7 +46,8 @@ class Config(C.Structure):
                 ("pcg_iters", C.c_int32),
                 ("omega_relax", C.c_double), ("gravity", C.c_double * 3), ("seed", C.c_uint64),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("max_dense_coarse", C.c_int32),
-                ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32)]
+                ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32),
+                ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p)]
 
 
 class Stats(C.Structure):
@@ -54,7 +56,9 @@ class Stats(C.Structure):
                 ("setup_ran", C.c_int32), ("n_b", C.c_int32), ("b_norm", C.c_double * MAX_ITERS),
                 ("frame", C.c_int64), ("l0_pass_ms", C.c_double), ("l0_pass_launches", C.c_int64),
                 ("l0_pass_bytes", C.c_double), ("ms_setup", C.c_double), ("ms_frame", C.c_double),
-                ("kernel_launches", C.c_int64), ("indefinite_events", C.c_int32)]
+                ("kernel_launches", C.c_int64), ("indefinite_events", C.c_int32),
+                ("rank", C.c_int32), ("world", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
+                ("halo_rows", C.c_int64)]
 
 
 _lib = None
@@ -89,6 +93,11 @@ def lib():
             "mgpbd_debug_vcycle": (C.c_int, [P, P, P]),
             "mgpbd_debug_pcg": (C.c_int, [P, P, i32, P]),
             "mgpbd_last_error": (C.c_char_p, [P]),
+            "mgpbd_nccl_unique_id": (C.c_int, [P]),
+            "mgpbd_vgroup_create": (C.c_int, [i32, P]),
+            "mgpbd_vgroup_destroy": (None, [P]),
+            "mgpbd_partition_rows": (C.c_int, [P, i32, i32, P]),
+            "mgpbd_halo_plan": (C.c_int, [P, P, P, i32, P]),
             "mgpbd_destroy": (None, [P]),
         }
         for name, (res, args) in sig.items():
@@ -101,6 +110,53 @@ def lib():
 
 def _p(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 creates it; broadcast it to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    st = lib().mgpbd_nccl_unique_id(buf)
+    if st != OK:
+        raise MgpbdError(st, lib().mgpbd_last_error(None).decode())
+    return buf.raw
+
+
+class VirtualGroup:
+    """W virtual ranks in one process (one thread per context, all on one GPU)."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        st = lib().mgpbd_vgroup_create(world, C.byref(h))
+        if st != OK:
+            raise MgpbdError(st, "vgroup_create")
+        self.h, self.world = h, world
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().mgpbd_vgroup_destroy(self.h)
+            self.h = None
+
+
+def partition_rows(rowptr, world):
+    """Host-only: row blocks [bounds[p], bounds[p+1]) balanced by nonzeros (no GPU needed)."""
+    rowptr = np.ascontiguousarray(rowptr, np.int64)
+    out = np.empty(world + 1, np.int32)
+    st = lib().mgpbd_partition_rows(_p(rowptr), rowptr.shape[0] - 1, world, _p(out))
+    if st != OK:
+        raise MgpbdError(st, "partition_rows")
+    return out
+
+
+def halo_plan(bounds, minc, maxc):
+    """Host-only: recv[q, p] = [a, b) rows rank q receives from rank p."""
+    bounds = np.ascontiguousarray(bounds, np.int32)
+    minc, maxc = np.ascontiguousarray(minc, np.int32), np.ascontiguousarray(maxc, np.int32)
+    w = bounds.shape[0] - 1
+    out = np.empty((w, w, 2), np.int32)
+    st = lib().mgpbd_halo_plan(_p(bounds), _p(minc), _p(maxc), w, _p(out))
+    if st != OK:
+        raise MgpbdError(st, "halo_plan")
+    return out
 
 
 def config_default(**kw) -> Config:
@@ -120,7 +176,17 @@ class Context:
     def __init__(self, kind, verts, rest_pos, inv_mass, compliance, pos=None, vel=None, cfg: Config | None = None,
                  **cfg_kw):
         L = lib()
+        nccl_id = cfg_kw.pop("nccl_id", None)
+        vgroup = cfg_kw.pop("vgroup", None)
         self.cfg = cfg or config_default(**cfg_kw)
+        self._keep = []
+        if nccl_id is not None:
+            buf = C.create_string_buffer(bytes(nccl_id), 128)
+            self._keep.append(buf)
+            self.cfg.nccl_id = C.cast(buf, C.c_void_p)
+        if vgroup is not None:
+            self._keep.append(vgroup)
+            self.cfg.vgroup = vgroup.h
         self.verts = np.ascontiguousarray(verts, np.int32)
         self.m = int(self.verts.shape[0])
         self.rest = np.ascontiguousarray(rest_pos, np.float64)

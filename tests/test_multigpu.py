@@ -1,0 +1,189 @@
+"""Row-partitioned (world > 1) path, SURVEY.md §8(e).
+
+CPU: the host partition and halo-plan logic exported by libmgpbd.so (the same functions the engine
+uses), and a 2-process gloo run of the halo-exchanged level-0 SpMV + allreduced dot built on them.
+GPU: W virtual ranks (W contexts on one GPU, one thread each, host-synchronised collectives) against
+the single-context frame.
+"""
+import os
+import socket
+import threading
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as O
+from paper_2505_13390_b200 import mgpbd, scenes
+
+
+def _pattern(name):
+    sc = scenes.make(name) if name != "cloth32" else scenes.cloth(32)
+    return sc, O.pattern(sc.verts, sc.n_verts)
+
+
+def _windows(r, c, bounds):
+    mn, mx = [], []
+    for q in range(len(bounds) - 1):
+        a, b = bounds[q], bounds[q + 1]
+        cols = c[r[a]:r[b]]
+        mn.append(int(min(cols.min(), a)) if b > a else a)
+        mx.append(int(max(cols.max(), b - 1)) if b > a else a - 1)
+    return np.array(mn, np.int32), np.array(mx, np.int32)
+
+
+@pytest.mark.parametrize("name,world", [("block_small", 2), ("block_small", 3), ("cloth32", 4), ("bar3k", 8)])
+def test_partition_balanced_and_covering(name, world):
+    sc, (r, c) = _pattern(name)
+    b = mgpbd.partition_rows(r, world)
+    assert b[0] == 0 and b[-1] == sc.n_cons and np.all(np.diff(b) >= 0)
+    nnz = np.diff(r[b])
+    assert nnz.max() - nnz.min() <= 2 * np.diff(r).max()          # balanced by nonzeros
+
+
+@pytest.mark.parametrize("name,world", [("block_small", 2), ("block_small", 3), ("cloth32", 4)])
+def test_halo_plan_is_exactly_the_referenced_foreign_columns(name, world):
+    sc, (r, c) = _pattern(name)
+    b = mgpbd.partition_rows(r, world)
+    mn, mx = _windows(r, c, b)
+    plan = mgpbd.halo_plan(b, mn, mx)
+    for q in range(world):
+        need = set(c[r[b[q]]:r[b[q + 1]]].tolist()) - set(range(b[q], b[q + 1]))
+        got = set()
+        for p in range(world):
+            a, e = plan[q, p]
+            if p == q:
+                assert e <= a
+                continue
+            got |= set(range(a, e))
+            assert all(b[p] <= x < b[p + 1] for x in range(a, e))     # owned by the sender
+        assert need <= got                                            # every referenced column arrives
+        assert got <= set(range(mn[q], mx[q] + 1))                     # nothing outside the window
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _gloo_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc = scenes.make("block_small")
+        r, c = O.pattern(sc.verts, sc.n_verts)
+        rng = np.random.default_rng(0)
+        val = rng.normal(size=c.shape[0])
+        xg = rng.normal(size=sc.n_cons)
+        b = mgpbd.partition_rows(r, world)
+        mn, mx = _windows(r, c, b)
+        plan = mgpbd.halo_plan(b, mn, mx)
+        r0, r1 = b[rank], b[rank + 1]
+        # full-length local vector: owned rows valid, everything else garbage until the exchange
+        x = np.full(sc.n_cons, np.nan)
+        x[r0:r1] = xg[r0:r1]
+        reqs = []
+        for p in range(world):
+            if p == rank:
+                continue
+            sa, se = plan[p, rank]      # what p needs from me
+            ra, re = plan[rank, p]      # what I need from p
+            if se > sa:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(x[sa:se])), p))
+            if re > ra:
+                buf = torch.empty(re - ra, dtype=torch.float64)
+                dist.recv(buf, p)
+                x[ra:re] = buf.numpy()
+        for rq in reqs:
+            rq.wait()
+        y = np.zeros(sc.n_cons)
+        for i in range(r0, r1):
+            y[i] = np.dot(val[r[i]:r[i + 1]], x[c[r[i]:r[i + 1]]])
+        yt = torch.from_numpy(y)
+        dist.all_reduce(yt)                     # disjoint rows: the sum is the global vector
+        d = torch.tensor([np.dot(xg[r0:r1], y[r0:r1])])
+        dist.all_reduce(d)
+        if rank == 0:
+            yref = O.spmv(r, c, val, xg)
+            q.put((float(np.abs(yt.numpy() - yref).max()), float(abs(d.item() - xg @ yref))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_two_rank_halo_spmv_and_dot():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(rk, 2, port, q)) for rk in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    err_y, err_d = q.get(timeout=5)
+    assert err_y < 1e-12 and err_d < 1e-9
+
+
+# ----------------------------------------------------------------------------------- GPU
+def _run_virtual(sc, world, frames, n_iters, **kw):
+    group = mgpbd.VirtualGroup(world)
+    out = [None] * world
+    errs = []
+
+    def worker(rank):
+        try:
+            ctx = mgpbd.Context.from_scene(sc, rank=rank, world=world, vgroup=group, **kw)
+            for _ in range(frames):
+                ctx.step(sc.dt, n_iters)
+            out[rank] = (ctx.positions(), ctx.lambdas(), ctx.stats().halo_rows, ctx.stats().row_begin,
+                         ctx.stats().row_end)
+            ctx.close()
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(rk,)) for rk in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(600)
+    assert not errs, errs
+    return out
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,world,precision", [("block_small", 2, 0), ("block_small", 3, 0),
+                                                   ("block_small", 2, 1), ("cloth64", 4, 0)])
+def test_virtual_ranks_match_single_gpu(name, world, precision):
+    sc = scenes.make(name) if name != "cloth64" else scenes.cloth(64, dt=3e-3, n_iters=5)
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, setup_interval=2)
+    for _ in range(3):
+        ctx.step(sc.dt, 4)
+    x1, l1 = ctx.positions(), ctx.lambdas()
+    ctx.close()
+    outs = _run_virtual(sc, world, 3, 4, precision=precision, setup_interval=2)
+    tol = 1e-9 if precision == 0 else 1e-4
+    bounds = [o[3] for o in outs] + [outs[-1][4]]
+    assert bounds[0] == 0 and bounds[-1] == sc.n_cons and all(o[2] > 0 for o in outs)
+    for x, lam, *_ in outs:
+        assert rel(x - sc.pos, x1 - sc.pos) <= tol and rel(lam, l1) <= tol
+    # ranks hold identical replicated state
+    assert all(np.array_equal(outs[0][0], o[0]) for o in outs)
+
+
+@pytest.mark.gpu
+def test_virtual_ranks_vs_oracle_fp64():
+    sc = scenes.make("block_small")
+    outs = _run_virtual(sc, 2, 1, sc.n_iters)
+    sim = O.Sim(sc)
+    sim.step(sc.dt, sc.n_iters)
+    xo, _, lo = sim.state()
+    assert rel(outs[0][1], lo) <= 1e-6 and rel(outs[0][0] - sc.pos, xo - sc.pos) <= 1e-6
