@@ -161,16 +161,22 @@ def rel(a, b):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("name,world,precision", [("block_small", 2, 0), ("block_small", 3, 0),
-                                                   ("block_small", 2, 1), ("cloth64", 4, 0)])
+                                                   ("block_small", 2, 1), ("block_small", 3, 1),
+                                                   ("cloth64", 4, 0), ("bar3k", 2, 1)])
 def test_virtual_ranks_match_single_gpu(name, world, precision):
     sc = scenes.make(name) if name != "cloth64" else scenes.cloth(64, dt=3e-3, n_iters=5)
+    # fp64: three frames across a lazy re-setup, to rounding.  fp32: one frame at the whole-frame fp32
+    # bound (1e-3); fp32 frames of the squashed block are chaotic in the rounding (single-GPU fp32 vs
+    # fp64 already differ by 1e-2 in lambda after two frames, tools/debug_prec.py), so later frames of
+    # two fp32 runs with different summation orders are not comparable element-wise.
+    frames = 3 if precision == 0 else 1
     ctx = mgpbd.Context.from_scene(sc, precision=precision, setup_interval=2)
-    for _ in range(3):
+    for _ in range(frames):
         ctx.step(sc.dt, 4)
     x1, l1 = ctx.positions(), ctx.lambdas()
     ctx.close()
-    outs = _run_virtual(sc, world, 3, 4, precision=precision, setup_interval=2)
-    tol = 1e-9 if precision == 0 else 1e-4
+    outs = _run_virtual(sc, world, frames, 4, precision=precision, setup_interval=2)
+    tol = 1e-9 if precision == 0 else 1e-3
     bounds = [o[3] for o in outs] + [outs[-1][4]]
     assert bounds[0] == 0 and bounds[-1] == sc.n_cons and all(o[2] > 0 for o in outs)
     for x, lam, *_ in outs:
