@@ -172,6 +172,9 @@ def run_reference(args):
 
 
 def run_ours(args):
+    # NCCL's banner / debug lines go to stderr: stdout carries exactly one JSON line
+    os.environ.setdefault("NCCL_DEBUG", "WARN")
+    os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import numpy as np
     import torch
     from paper_2505_13390_b200 import mgpbd, scenes
@@ -191,6 +194,8 @@ def run_ours(args):
         obj = [mgpbd.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
         part = dict(rank=rank, world=world, nccl_id=obj[0])
+    elif args.partitioned:
+        part = dict(rank=0, world=1, nccl_id=mgpbd.nccl_unique_id())   # partitioned path, 1-rank NCCL
     ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=0, **part)
     for _ in range(args.warmup):
         ctx.step(sc.dt, sc.n_iters)
@@ -317,6 +322,8 @@ def main():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-slab", type=int, default=8, help="x-slabs of the block the oracle sample uses")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="N=1 only: run the row-partitioned (NCCL) code path on a 1-rank communicator")
     ap.add_argument("--profile-frames", type=int, default=2, help="frames timed per level-0 pass for the roofline")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -90,7 +90,8 @@ typedef struct {
     int32_t rank, world;      /* row partition of level 0 over `world` ranks, 0 <= rank < world */
     int32_t profile;          /* 1: record CUDA events around the level-0 matrix passes */
     const void* nccl_id;      /* world > 1: 128-byte ncclUniqueId shared by all ranks (mgpbd_nccl_unique_id on
-                                 rank 0, broadcast by the caller); one process and one GPU per rank */
+                                 rank 0, broadcast by the caller); one process and one GPU per rank.  A non-NULL
+                                 id with world == 1 runs the partitioned code path on one rank */
     void* vgroup;             /* alternative to nccl_id: a virtual-ranks group (mgpbd_vgroup_create) — `world`
                                  contexts in one process, one host thread each, all on one GPU (tests) */
 } mgpbd_config;

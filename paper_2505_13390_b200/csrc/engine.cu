@@ -231,7 +231,7 @@ class Engine : public EngineBase {
         build_pattern(verts.p, m, kc, nv, vptr.p, vlist.p, rowptr0, col0, st);
         nnz0 = read_scalar(rowptr0.p + m, st);
         r0 = 0; r1 = m; nnz_own = nnz0;
-        if (cfg.world > 1 || cfg.vgroup) setup_partition();
+        if (cfg.world > 1 || cfg.vgroup || cfg.nccl_id) setup_partition();
         h.resize((size_t)m * kc * 3); b0.resize(m);
         r.resize(m); p.resize(m); q.resize(m); xs.resize(m);
         scal.resize(2 * 4096); flags.resize(8); bn.resize(MGPBD_MAX_ITERS);

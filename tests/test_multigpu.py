@@ -193,3 +193,27 @@ def test_virtual_ranks_vs_oracle_fp64():
     sim.step(sc.dt, sc.n_iters)
     xo, _, lo = sim.state()
     assert rel(outs[0][1], lo) <= 1e-6 and rel(outs[0][0] - sc.pos, xo - sc.pos) <= 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", [0, 1])
+def test_nccl_single_rank_partitioned_path(precision):
+    """The NCCL backend on a 1-rank communicator: the partitioned code path (halo plan, NCCL allreduce
+    of dots / restriction / Galerkin values / dlambda, captured into CUDA graphs) against the plain path."""
+    sc = scenes.make("block_small")
+    frames = 2 if precision == 0 else 1
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, setup_interval=2)
+    for _ in range(frames):
+        ctx.step(sc.dt, 4)
+    x1, l1 = ctx.positions(), ctx.lambdas()
+    ctx.close()
+    uid = mgpbd.nccl_unique_id()
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, setup_interval=2, rank=0, world=1, nccl_id=uid)
+    for _ in range(frames):
+        ctx.step(sc.dt, 4)
+    st = ctx.stats()
+    assert st.world == 1 and st.row_begin == 0 and st.row_end == sc.n_cons and st.halo_rows == 0
+    x, lam = ctx.positions(), ctx.lambdas()
+    ctx.close()
+    frames_tol = 1e-9 if precision == 0 else 1e-3
+    assert rel(x - sc.pos, x1 - sc.pos) <= frames_tol and rel(lam, l1) <= frames_tol
