@@ -94,6 +94,10 @@ typedef struct {
                                  id with world == 1 runs the partitioned code path on one rank */
     void* vgroup;             /* alternative to nccl_id: a virtual-ranks group (mgpbd_vgroup_create) — `world`
                                  contexts in one process, one host thread each, all on one GPU (tests) */
+    int32_t level0_operator;  /* hot level-0 matrix passes: 0 = stream the assembled CSR, 1 = matrix-free
+                                 A x = H (H^T x) + at x from the scaled gradients (SURVEY.md §8(f) f4,
+                                 PAPER.md:450); the CSR is assembled either way (Galerkin, diagonal).
+                                 Default 1 */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16

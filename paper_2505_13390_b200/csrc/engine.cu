@@ -15,6 +15,7 @@
 #include "solve.cuh"
 #include "util.cuh"
 #include "comm.cuh"
+#include "matfree.cuh"
 
 namespace mgpbd {
 
@@ -157,6 +158,11 @@ class Engine : public EngineBase {
     std::vector<Comm::Xfer> xfers;
     int64_t tb0 = 0, te0 = -1;  // Galerkin segments of the owned rows (level 0 -> 1)
     DBuf<double> dsc;           // rank-local dot results before the allreduce
+    // matrix-free level-0 operator (cfg.level0_operator == 1, matfree.cuh)
+    MatFree<T> mf;
+    DBuf<T> mf_hv, mf_at, mf_u;
+    bool mf_ready = false;      // h is current and belongs to the assembled level 0 (not debug values)
+    bool mf_on() const { return cfg.level0_operator == 1 && mf_ready; }
 
     void setup_partition() {
         if (cfg.vgroup) comm = make_virtual_comm(static_cast<VirtualGroup*>(cfg.vgroup), cfg.rank);
@@ -183,6 +189,29 @@ class Engine : public EngineBase {
         }
         dsc.resize(4);
     }
+    void setup_matfree() {
+        // vertices touched by this rank's rows: their incidences reference only owned or halo rows
+        std::vector<int32_t> hv_((size_t)(r1 - r0) * kc);
+        if (r1 > r0) d2h(hv_.data(), verts.p + (size_t)r0 * kc, hv_.size(), st);
+        std::vector<int64_t> hp((size_t)nv + 1);
+        d2h(hp.data(), vptr.p, (size_t)nv + 1, st);
+        MG_CK(cudaStreamSynchronize(st));
+        int32_t vmin = nv, vmax = -1;
+        for (int32_t q : hv_) { vmin = std::min(vmin, q); vmax = std::max(vmax, q); }
+        mf = MatFree<T>();
+        mf.kc = kc;
+        mf.row0 = r0; mf.row1 = r1;
+        mf.v0 = vmax < 0 ? 0 : vmin; mf.v1 = vmax < 0 ? 0 : vmax + 1;
+        mf.verts = verts.p; mf.h = h.p; mf.vptr = vptr.p; mf.vlist = vlist.p;
+        mf.ninc = hp[nv]; mf.e0 = hp[mf.v0]; mf.e1 = hp[mf.v1];
+        mf_hv.resize(3 * (size_t)mf.ninc); mf_at.resize(m); mf_u.resize(4 * (size_t)nv);
+        MG_CK(cudaMemsetAsync(mf_u.p, 0, sizeof(T) * 4 * (size_t)nv, st));
+        mf.hv = mf_hv.p; mf.at = mf_at.p; mf.u = mf_u.p;
+        mf.dinv = L[0]->dinv.p;
+        mf.grid = mf_grid(r1 - r0);
+    }
+    int l0_nparts() const { return mf_on() ? mf.grid : L[0]->hot().nparts; }
+
     int32_t lo0(int l) const { return (l == 0) ? r0 : 0; }
     int32_t cnt(int l) const { return (l == 0) ? r1 - r0 : L[l]->n; }
 
@@ -248,6 +277,7 @@ class Engine : public EngineBase {
         l0.configure(st);
         alloc_vectors(l0);
         MG_CK(cudaMemsetAsync(l0.vt.p, 0, sizeof(T) * m, st));  // restriction input: zero outside the owned rows
+        if (cfg.level0_operator == 1) setup_matfree();
         if (use_graphs && dist && !comm->graph_capturable()) use_graphs = false;
         MG_CK(cudaStreamSynchronize(st));
     }
@@ -280,6 +310,13 @@ class Engine : public EngineBase {
         const double cb = (L[0]->band_rows > 0 && L[0]->row_vl > 0) ? 2.0 : 4.0;  // col16 hot copy or int32
         const double mrows = (double)(r1 - r0);
         double mat = (double)nnz_own * (s + cb) + 8.0 * (mrows + 1);
+        if (mf_on()) {
+            // matrix-free: vertex gather (hv planes, vlist, vptr, u write) + row gather (verts, h, at,
+            // u read once per vertex); x is read by both kernels
+            const double nvr = (double)(mf.v1 - mf.v0), ne = (double)(mf.e1 - mf.e0);
+            mat = ne * (3 * s + 4) + 8.0 * (nvr + 1) + nvr * 4 * s                      // gather
+                  + mrows * (4.0 * kc + 3.0 * kc * s + s) + nvr * 4 * s + mrows * s;    // rows
+        }
         double vec;
         switch (mode) {
             case PASS_JACOBI: vec = 4 * s; break;          // x (gathered once), b, dinv, y
@@ -323,7 +360,8 @@ class Engine : public EngineBase {
         const Level& l0 = *L[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (cfg.profile) { e0 = prof_event(); MG_CK(cudaEventRecord(e0, st)); }
-        csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
+        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st);
+        else csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
         if (cfg.profile) {
             e1 = prof_event();
             MG_CK(cudaEventRecord(e1, st));
@@ -513,7 +551,7 @@ class Engine : public EngineBase {
             } else {
                 vcycle(0, r.p, z, r.p);
             }
-            const int np = nL == 1 ? l0.grid : l0.hot().nparts;
+            const int np = nL == 1 ? l0.grid : l0_nparts();
             if (dist) {  // rank-local sums -> allreduce -> checks on the global values
                 finalize_sum(parts1.p, np, dsc.p, st);
                 finalize_sum(parts2.p, np, dsc.p + 1, st);
@@ -525,11 +563,11 @@ class Engine : public EngineBase {
             pcg_update_p<T>(cn, z + o, p.p + o, scal.p, k, st);
             pass(0, PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
             if (dist) {
-                finalize_sum(parts1.p, l0.hot().nparts, dsc.p + 2, st);
+                finalize_sum(parts1.p, l0_nparts(), dsc.p + 2, st);
                 comm->allreduce(dsc.p + 2, 1, st);
                 pcg_commit_pq(dsc.p + 2, scal.p, k, flags.p, tag, st);
             } else {
-                pcg_finalize_pq(parts1.p, l0.hot().nparts, scal.p, k, flags.p, tag, st);
+                pcg_finalize_pq(parts1.p, l0_nparts(), scal.p, k, flags.p, tag, st);
             }
             pcg_update_xr<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, st);
         }
@@ -540,6 +578,10 @@ class Engine : public EngineBase {
         eval_constraints<T>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h.p, b0.p, st);
         // (all constraints are evaluated on every rank: h of the halo constraints is needed locally)
         assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st, r0, r1);
+        if (cfg.level0_operator == 1) {
+            mf_refresh<T>(mf, alpha.p, dt, st);
+            mf_ready = true;
+        }
     }
 
     void assemble_setup(double dt) {
@@ -743,6 +785,7 @@ class Engine : public EngineBase {
     }
     void debug_setup_from(const double* vals) override {
         Level& l0 = *L[0];
+        mf_ready = false;  // external A_0 values: h does not describe them, use the CSR passes
         l0.val64.resize(nnz0); l0.dinv64.resize(m);
         h2d(l0.val64.p, vals, nnz0, st);
         diag_inv<double>(m, rowptr0.p, l0.val64.p, l0.dinv64.p, st);
@@ -831,6 +874,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->profile = 0;
     c->nccl_id = nullptr;
     c->vgroup = nullptr;
+    c->level0_operator = 1;
     return MGPBD_OK;
 }
 
@@ -850,6 +894,7 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cfg->k_nullspace != 1) return fail("only k_nullspace = 1 is implemented (reading c1)");
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail("bad rank/world");
     if (cfg->world > 1 && !cfg->nccl_id && !cfg->vgroup) return fail("world > 1 needs nccl_id or vgroup");
+    if (cfg->level0_operator != 0 && cfg->level0_operator != 1) return fail("level0_operator must be 0 or 1");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > 4096 || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
         cfg->max_dense_coarse < 1)

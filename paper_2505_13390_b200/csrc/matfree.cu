@@ -1,0 +1,182 @@
+// Matrix-free level-0 operator, see matfree.cuh.
+#include <algorithm>
+
+#include "matfree.cuh"
+#include "record.cuh"
+#include "solve.cuh"
+
+namespace mgpbd {
+
+namespace {
+
+constexpr int MF_BS = 256;
+
+template <class T>
+struct alignas(4 * sizeof(T)) V4 {
+    T x, y, z, w;
+};
+
+// hv[plane][e] = h[vlist[e]][plane] for the incidences of vertices [v0, v1); at_i = alpha_i / dt^2.
+template <class T>
+__global__ void k_mf_refresh(int64_t e0, int64_t e1, int64_t ninc, const int32_t* __restrict__ vlist,
+                             const T* __restrict__ h, T* __restrict__ hv, int32_t r0, int32_t r1,
+                             const double* __restrict__ alpha, double dt2, T* __restrict__ at) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = e0 + tid; e < e1; e += nt) {
+        const T* p = h + (int64_t)vlist[e] * 3;
+        hv[e] = p[0];
+        hv[ninc + e] = p[1];
+        hv[2 * ninc + e] = p[2];
+    }
+    for (int64_t i = r0 + tid; i < r1; i += nt) at[i] = (T)(alpha[i] / dt2);
+}
+
+// u_v = sum over v's incidences of h_{j,s} x_j: G lanes per vertex, lane partials in incidence order
+// strided by G, fixed butterfly (deterministic).
+template <class T, int KC, int G>
+__global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, int64_t ninc,
+                                                      const int64_t* __restrict__ vptr,
+                                                      const int32_t* __restrict__ vlist, const T* __restrict__ hv,
+                                                      const T* __restrict__ x, V4<T>* __restrict__ u) {
+    constexpr int PER_WARP = 32 / G;
+    const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T* __restrict__ hx = hv;
+    const T* __restrict__ hy = hv + ninc;
+    const T* __restrict__ hz = hv + 2 * ninc;
+    // warp-uniform trip count: the butterfly below needs the whole warp
+    for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {
+        const int64_t v = base + sub;
+        T a0 = (T)0, a1 = (T)0, a2 = (T)0;
+        if (v < v1) {
+            const int64_t e1 = vptr[v + 1];
+            for (int64_t e = vptr[v] + sl; e < e1; e += G) {
+                const T xj = x[vlist[e] / KC];
+                a0 += hx[e] * xj;
+                a1 += hy[e] * xj;
+                a2 += hz[e] * xj;
+            }
+        }
+        a0 = group_sum_t<G>(a0);
+        a1 = group_sum_t<G>(a1);
+        a2 = group_sum_t<G>(a2);
+        if (v < v1 && sl == 0) u[v] = V4<T>{a0, a1, a2, (T)0};
+    }
+}
+
+// (A x)_i = sum_s h_{i,s} . u_{v_s} + at_i x_i in the storage precision, epilogue in fp64 exactly as
+// the CSR row kernels (solve.cu k_rows).
+template <class T, int KC, int MODE>
+__global__ void __launch_bounds__(MF_BS) k_mf_rows(int32_t row0, int32_t row1, const int32_t* __restrict__ verts,
+                                                   const T* __restrict__ h, const V4<T>* __restrict__ u,
+                                                   const T* __restrict__ at, const T* __restrict__ dinv,
+                                                   const T* __restrict__ x, const T* __restrict__ b,
+                                                   T* __restrict__ y, const T* __restrict__ aux, double omega,
+                                                   double* __restrict__ parts, double* __restrict__ parts2) {
+    using IV = typename std::conditional<KC == 4, int4, int2>::type;
+    double acc1 = 0.0, acc2 = 0.0;
+    const int32_t nt = gridDim.x * blockDim.x;
+    for (int32_t i = row0 + blockIdx.x * blockDim.x + threadIdx.x; i < row1; i += nt) {
+        int vi[KC];
+        T hi[KC][3];
+        load_iv(reinterpret_cast<const IV*>(verts)[i], vi);
+        load_record<T, KC>(h + (int64_t)i * KC * 3, hi);
+        const T xi = x[i];
+        T acc = at[i] * xi;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const V4<T> uu = u[vi[k]];
+            acc += hi[k][0] * uu.x + hi[k][1] * uu.y + hi[k][2] * uu.z;
+        }
+        const double s = (double)acc;
+        if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
+            const T yi = (T)((double)xi + omega * (double)dinv[i] * ((double)b[i] - s));
+            y[i] = yi;
+            if (MODE == PASS_JACOBI_DOT) {
+                const double ai = (double)aux[i];
+                acc1 += ai * (double)yi;
+                acc2 += ai * ai;
+            }
+        } else if (MODE == PASS_RESID_P) {
+            y[i] = (T)((double)aux[i] * ((double)b[i] - s));
+        } else if (MODE == PASS_SPMV_DOT) {
+            const T yi = (T)s;
+            y[i] = yi;
+            acc1 += (double)xi * (double)yi;
+        } else if (MODE == PASS_POWER) {
+            const T yi = (T)((double)dinv[i] * s);
+            y[i] = yi;
+            acc1 += (double)yi * (double)yi;
+        }
+    }
+    if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
+        __shared__ double sh[32];
+        const double t1 = block_sum<MF_BS>(acc1, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t1;
+        if (MODE == PASS_JACOBI_DOT) {
+            const double t2 = block_sum<MF_BS>(acc2, sh);
+            if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
+        }
+    }
+}
+
+template <class T, int KC>
+void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
+                double* parts, double* parts2, cudaStream_t s) {
+    if (A.v1 > A.v0) {
+        constexpr int G = KC == 4 ? 8 : 4;  // ~23 (tets) / ~6 (cloth) incidences per vertex
+        const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
+        const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * 16);
+        k_mf_vgather<T, KC, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, x,
+                                                      reinterpret_cast<V4<T>*>(A.u));
+        MG_LAUNCH_CHECK();
+    }
+    const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
+#define MG_MF(M)                                                                                            \
+    k_mf_rows<T, KC, M><<<A.grid, MF_BS, 0, s>>>(A.row0, A.row1, A.verts, A.h, u, A.at, A.dinv, x, b, y, aux, \
+                                                  omega, parts, parts2)
+    switch (mode) {
+        case PASS_JACOBI: MG_MF(PASS_JACOBI); break;
+        case PASS_JACOBI_DOT: MG_MF(PASS_JACOBI_DOT); break;
+        case PASS_RESID_P: MG_MF(PASS_RESID_P); break;
+        case PASS_SPMV_DOT: MG_MF(PASS_SPMV_DOT); break;
+        case PASS_POWER: MG_MF(PASS_POWER); break;
+        default: throw Error(-1, "mf_pass: bad mode");
+    }
+#undef MG_MF
+    MG_LAUNCH_CHECK();
+}
+
+}  // namespace
+
+int mf_grid(int32_t rows) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)rows + MF_BS - 1) / MF_BS, 148 * 8));
+}
+
+template <class T>
+void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, cudaStream_t s) {
+    const int64_t e0 = A.e0, e1 = A.e1;
+    const int64_t work = std::max<int64_t>(e1 - e0, A.row1 - A.row0);
+    if (work <= 0) return;
+    const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
+    k_mf_refresh<T><<<grid, 256, 0, s>>>(e0, e1, A.ninc, A.vlist, A.h, A.hv, A.row0, A.row1, alpha, dt * dt, A.at);
+    MG_LAUNCH_CHECK();
+}
+
+template <class T>
+void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
+             double* parts, double* parts2, cudaStream_t s) {
+    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s);
+    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s);
+}
+
+#define MG_INST(T)                                                                                           \
+    template void mf_refresh<T>(const MatFree<T>&, const double*, double, cudaStream_t);                     \
+    template void mf_pass<T>(int, const MatFree<T>&, const T*, const T*, T*, const T*, double, double*, double*, \
+                             cudaStream_t);
+MG_INST(float)
+MG_INST(double)
+#undef MG_INST
+
+}  // namespace mgpbd

@@ -1,0 +1,45 @@
+// Matrix-free level-0 operator (PAPER.md:450 names it as future work).
+//
+// With the scaled gradients h_{i,s} = sqrt(w_v) grad_v C_i (v = verts[i][s]) the dual matrix of
+// PAPER.md Eq. 4-5 is A = H H^T + diag(at), at_i = alpha_i / dt^2 (reading c14: the sum runs over every
+// shared vertex).  A x is evaluated in two gathers instead of streaming the assembled CSR:
+//   u_v     = sum_{(j,s): verts[j][s] = v} h_{j,s} x_j               (vertex gather, vertices [v0, v1))
+//   (A x)_i = sum_s h_{i,s} . u_{verts[i][s]} + at_i x_i              (constraint gather, rows [row0, row1))
+// followed by the same per-row epilogues as the CSR passes (PASS_* in solve.cuh).  The assembled CSR
+// is still built every outer iteration: the Galerkin refresh (Eq. 6) and the smoother diagonal use it.
+#pragma once
+#include "common.cuh"
+
+namespace mgpbd {
+
+template <class T>
+struct MatFree {
+    int kc = 4;                     // vertices per constraint (2 distance, 4 tetrahedron)
+    int32_t row0 = 0, row1 = 0;     // constraint rows this rank evaluates
+    int32_t v0 = 0, v1 = 0;         // vertices those rows touch
+    const int32_t* verts = nullptr; // m x kc
+    const T* h = nullptr;           // m x kc x 3
+    const int64_t* vptr = nullptr;  // vertex incidence CSR (nv + 1)
+    const int32_t* vlist = nullptr; // constraint*kc + slot, ascending per vertex
+    int64_t ninc = 0;               // vptr[nv]
+    int64_t e0 = 0, e1 = 0;         // vptr[v0], vptr[v1]
+    T* hv = nullptr;                // vertex-major copy of h: [x | y | z] planes of ninc values
+    T* at = nullptr;                // alpha_i / dt^2 (m)
+    T* u = nullptr;                 // 4 values per vertex (xyz, pad)
+    const T* dinv = nullptr;        // 1 / A_ii from the assembly
+    int grid = 1;                   // CTAs of the row kernel = number of dot partials
+};
+
+int mf_grid(int32_t rows);
+
+// Per outer iteration, after the constraint evaluation: hv (vertex-major h) and at.
+template <class T>
+void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, cudaStream_t s);
+
+// One level-0 pass of `mode` (PASS_JACOBI, PASS_JACOBI_DOT, PASS_RESID_P, PASS_SPMV_DOT, PASS_POWER);
+// same arguments and outputs as csr_pass, A.grid partials.
+template <class T>
+void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
+             double* parts, double* parts2, cudaStream_t s);
+
+}  // namespace mgpbd

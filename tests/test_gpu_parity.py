@@ -105,10 +105,11 @@ def test_vcycle_and_pcg_identical_hierarchy(name):
         assert rel(xg, xo) <= 1e-9, K
 
 
+@pytest.mark.parametrize("op", [0, 1], ids=["csr", "matfree"])
 @pytest.mark.parametrize("name", SMALL)
-def test_frame_fp64(name):
+def test_frame_fp64(name, op):
     sc = make_scene(name)
-    ctx = ctx_for(sc)
+    ctx = ctx_for(sc, level0_operator=op)
     sim = O.Sim(sc)
     ctx.step(sc.dt, sc.n_iters)
     assert sim.step(sc.dt, sc.n_iters) == 0
@@ -120,6 +121,38 @@ def test_frame_fp64(name):
     st = ctx.stats()
     assert np.allclose(st.b_norm[:sc.n_iters], sim.b_norms(sc.n_iters), rtol=1e-6)
     assert st.indefinite_events == sim.indefinite_events()
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_matrix_free_vcycle_and_pcg(name):
+    """Matrix-free level 0 (A x = H(H^T x) + at x from the scaled gradients) inside
+    the V-cycle and MGPCG, against the oracle's assembled-CSR hierarchy at the same state."""
+    sc = make_scene(name)
+    ctx = ctx_for(sc, level0_operator=1)
+    ctx.step(sc.dt, 1)                      # one outer iteration: setup and h at the same state
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    h = O.Hierarchy(r, c, v)
+    rng = np.random.default_rng(1)
+    b = rng.normal(size=sc.n_cons)
+    assert rel(ctx.debug_vcycle(b), h.vcycle(b)) <= 1e-10
+    for K in (1, 5):
+        xo, rc, _ = h.pcg(b, K)
+        assert rc == 0 and rel(ctx.debug_pcg(b, K), xo) <= 1e-8, K
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_matrix_free_equals_csr_frames(precision):
+    sc = scenes.make("block_small")
+    outs = []
+    for op in (0, 1):
+        ctx = ctx_for(sc, precision=precision, level0_operator=op)
+        ctx.step(sc.dt, sc.n_iters)
+        outs.append((ctx.positions() - sc.pos, ctx.lambdas()))
+        ctx.close()
+    tol = 1e-9 if precision == 0 else 1e-3
+    assert rel(outs[1][0], outs[0][0]) <= tol and rel(outs[1][1], outs[0][1]) <= tol
 
 
 def test_bar3k_multiframe_indefinite_resetup_fp64():
@@ -141,10 +174,11 @@ def test_bar3k_multiframe_indefinite_resetup_fp64():
     assert ctx.stats().setup_ran == 1      # early re-setup (frame 2 is not a multiple of 20)
 
 
+@pytest.mark.parametrize("op", [0, 1], ids=["csr", "matfree"])
 @pytest.mark.parametrize("name", SMALL)
-def test_frame_fp32(name):
+def test_frame_fp32(name, op):
     sc = make_scene(name)
-    ctx = ctx_for(sc, precision=1)
+    ctx = ctx_for(sc, precision=1, level0_operator=op)
     sim = O.Sim(sc)
     ctx.step(sc.dt, sc.n_iters)
     sim.step(sc.dt, sc.n_iters)
