@@ -16,6 +16,7 @@
 #include "util.cuh"
 #include "comm.cuh"
 #include "matfree.cuh"
+#include "vagal.cuh"
 
 namespace mgpbd {
 
@@ -161,7 +162,10 @@ class Engine : public EngineBase {
     // matrix-free level-0 operator (cfg.level0_operator == 1, matfree.cuh)
     MatFree<T> mf;
     DBuf<T> mf_hv, mf_at, mf_u;
-    bool mf_ready = false;      // h is current and belongs to the assembled level 0 (not debug values)
+    bool mf_ready = false;      // h is current and describes level 0 (false after debug_setup_from)
+    VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
+    bool va_ok = false;
+    double last_dt = 0.0;
     bool mf_on() const { return cfg.level0_operator == 1 && mf_ready; }
 
     void setup_partition() {
@@ -200,6 +204,7 @@ class Engine : public EngineBase {
         for (int32_t q : hv_) { vmin = std::min(vmin, q); vmax = std::max(vmax, q); }
         mf = MatFree<T>();
         mf.kc = kc;
+        mf.m = m;
         mf.row0 = r0; mf.row1 = r1;
         mf.v0 = vmax < 0 ? 0 : vmin; mf.v1 = vmax < 0 ? 0 : vmax + 1;
         mf.verts = verts.p; mf.h = h.p; mf.vptr = vptr.p; mf.vlist = vlist.p;
@@ -459,6 +464,12 @@ class Engine : public EngineBase {
             te0 = read_scalar(a.plan.tptr.p + r1, st);
             MG_CK(cudaMemsetAsync(a.tval.p, 0, sizeof(T) * (a.plan.T ? a.plan.T : 1), st));
         }
+        va_ok = false;
+        if (cfg.level0_operator == 1 && nL > 1) {
+            va_symbolic(nv, kc, vptr.p, vlist.p, L[0]->agg.p, L[0]->n_agg, L[1]->rowptr, L[1]->col, L[1]->nnz, va, st);
+            va_ok = true;
+            trace("va_symbolic");
+        }
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
         invalidate_graphs();  // buffers of the hierarchy changed
@@ -487,6 +498,10 @@ class Engine : public EngineBase {
         for (int l = 0; l + 1 < nL; ++l) {
             Level& a = *L[l];
             Level& c = *L[l + 1];
+            if (l == 0 && va_ok && mf_on()) {  // from h directly (replicated on every rank, no collective)
+                va_numeric<T>(va, kc, h.p, a.P.p, a.mptr.p, a.mlist.p, mf.at, a.n_agg, c.rowptr, c.val.p, c.dinv.p, st);
+                continue;
+            }
             if (l == 0 && dist) {  // this rank's fine rows only, then sum the partial coarse values
                 galerkin_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.P.p, a.n_agg, c.rowptr, c.nnz, a.tval.p,
                                     c.val.p, nullptr, st, tb0, te0);
@@ -577,10 +592,13 @@ class Engine : public EngineBase {
         Level& l0 = *L[0];
         eval_constraints<T>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h.p, b0.p, st);
         // (all constraints are evaluated on every rank: h of the halo constraints is needed locally)
-        assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st, r0, r1);
+        last_dt = dt;
         if (cfg.level0_operator == 1) {
-            mf_refresh<T>(mf, alpha.p, dt, st);
+            // matrix-free level 0: no assembled matrix in the hot loop (diagonal and A_1 from h)
+            mf_refresh<T>(mf, alpha.p, dt, l0.dinv.p, st);
             mf_ready = true;
+        } else {
+            assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st, r0, r1);
         }
     }
 
@@ -588,7 +606,7 @@ class Engine : public EngineBase {
         Level& l0 = *L[0];
         l0.val64.resize(nnz0);
         l0.dinv64.resize(m);
-        if (std::is_same<T, double>::value && !dist) {
+        if (std::is_same<T, double>::value && !dist && cfg.level0_operator == 0) {
             d2d(l0.val64.p, (const double*)l0.val.p, nnz0, st);
             d2d(l0.dinv64.p, (const double*)l0.dinv.p, m, st);
         } else {
@@ -669,6 +687,9 @@ class Engine : public EngineBase {
                 MG_CK(cudaEventRecord(s1, st));
                 setup_ran = 1;
             }
+            if (cfg.level0_operator == 1 && nL < 2)  // single level: A_0 is the coarsest, inverted densely
+                assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, L[0]->vl, L[0]->val.p,
+                            L[0]->dinv.p, st, r0, r1);
             run_iter(ite);  // Eq. 6 refresh, l.8 MGPCG, l.9-11 update
         }
         velocity(nv, x.p, x_old.p, v.p, dt, st);                                                     // l.17
@@ -756,6 +777,8 @@ class Engine : public EngineBase {
     void get_level(int l, int64_t* rp, int32_t* cl, double* vals) override {
         check_level(l);
         Level& a = *L[l];
+        if (l == 0 && vals && cfg.level0_operator == 1 && last_dt > 0)  // not assembled in the hot loop
+            assemble<T>(kind, m, verts.p, h.p, alpha.p, last_dt, rowptr0.p, col0.p, a.vl, a.val.p, a.dinv.p, st);
         if (rp) d2h(rp, a.rowptr, (size_t)a.n + 1, st);
         if (cl) d2h(cl, a.col, a.nnz, st);
         if (vals) {

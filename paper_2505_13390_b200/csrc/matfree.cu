@@ -16,11 +16,14 @@ struct alignas(4 * sizeof(T)) V4 {
     T x, y, z, w;
 };
 
-// hv[plane][e] = h[vlist[e]][plane] for the incidences of vertices [v0, v1); at_i = alpha_i / dt^2.
-template <class T>
+// hv[plane][e] = h[vlist[e]][plane] for the incidences of vertices [v0, v1); at_i = alpha_i / dt^2 for
+// all rows; dinv_i = 1 / (sum_s |h_{i,s}|^2 + at_i) for rows [r0, r1) — the assembly's diagonal formula
+// (mesh.cu k_assemble), so the smoother does not need the assembled matrix.
+template <class T, int KC>
 __global__ void k_mf_refresh(int64_t e0, int64_t e1, int64_t ninc, const int32_t* __restrict__ vlist,
-                             const T* __restrict__ h, T* __restrict__ hv, int32_t r0, int32_t r1,
-                             const double* __restrict__ alpha, double dt2, T* __restrict__ at) {
+                             const T* __restrict__ h, T* __restrict__ hv, int32_t m, int32_t r0, int32_t r1,
+                             const double* __restrict__ alpha, double dt2, T* __restrict__ at,
+                             T* __restrict__ dinv) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = e0 + tid; e < e1; e += nt) {
         const T* p = h + (int64_t)vlist[e] * 3;
@@ -28,7 +31,20 @@ __global__ void k_mf_refresh(int64_t e0, int64_t e1, int64_t ninc, const int32_t
         hv[ninc + e] = p[1];
         hv[2 * ninc + e] = p[2];
     }
-    for (int64_t i = r0 + tid; i < r1; i += nt) at[i] = (T)(alpha[i] / dt2);
+    for (int64_t i = tid; i < m; i += nt) {
+        const double a = alpha[i] / dt2;
+        at[i] = (T)a;
+        if (i >= r0 && i < r1) {
+            T hi[KC][3];
+            load_record<T, KC>(h + i * KC * 3, hi);
+            double d = 0.0;
+#pragma unroll
+            for (int k = 0; k < KC; ++k)
+                d += (double)hi[k][0] * hi[k][0] + (double)hi[k][1] * hi[k][1] + (double)hi[k][2] * hi[k][2];
+            d += a;
+            dinv[i] = (T)(1.0 / (double)(T)d);
+        }
+    }
 }
 
 // u_v = sum over v's incidences of h_{j,s} x_j: G lanes per vertex, lane partials in incidence order
@@ -155,12 +171,16 @@ int mf_grid(int32_t rows) {
 }
 
 template <class T>
-void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, cudaStream_t s) {
-    const int64_t e0 = A.e0, e1 = A.e1;
-    const int64_t work = std::max<int64_t>(e1 - e0, A.row1 - A.row0);
+void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cudaStream_t s) {
+    const int64_t work = std::max<int64_t>(A.e1 - A.e0, A.m);
     if (work <= 0) return;
     const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
-    k_mf_refresh<T><<<grid, 256, 0, s>>>(e0, e1, A.ninc, A.vlist, A.h, A.hv, A.row0, A.row1, alpha, dt * dt, A.at);
+    if (A.kc == 4)
+        k_mf_refresh<T, 4><<<grid, 256, 0, s>>>(A.e0, A.e1, A.ninc, A.vlist, A.h, A.hv, A.m, A.row0, A.row1, alpha,
+                                                dt * dt, A.at, dinv);
+    else
+        k_mf_refresh<T, 2><<<grid, 256, 0, s>>>(A.e0, A.e1, A.ninc, A.vlist, A.h, A.hv, A.m, A.row0, A.row1, alpha,
+                                                dt * dt, A.at, dinv);
     MG_LAUNCH_CHECK();
 }
 
@@ -172,7 +192,7 @@ void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const 
 }
 
 #define MG_INST(T)                                                                                           \
-    template void mf_refresh<T>(const MatFree<T>&, const double*, double, cudaStream_t);                     \
+    template void mf_refresh<T>(const MatFree<T>&, const double*, double, T*, cudaStream_t);                     \
     template void mf_pass<T>(int, const MatFree<T>&, const T*, const T*, T*, const T*, double, double*, double*, \
                              cudaStream_t);
 MG_INST(float)

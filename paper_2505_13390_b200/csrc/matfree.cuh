@@ -15,6 +15,7 @@ namespace mgpbd {
 template <class T>
 struct MatFree {
     int kc = 4;                     // vertices per constraint (2 distance, 4 tetrahedron)
+    int32_t m = 0;                  // constraints
     int32_t row0 = 0, row1 = 0;     // constraint rows this rank evaluates
     int32_t v0 = 0, v1 = 0;         // vertices those rows touch
     const int32_t* verts = nullptr; // m x kc
@@ -32,9 +33,10 @@ struct MatFree {
 
 int mf_grid(int32_t rows);
 
-// Per outer iteration, after the constraint evaluation: hv (vertex-major h) and at.
+// Per outer iteration, after the constraint evaluation: hv (vertex-major h), at (all rows) and the
+// diagonal inverse dinv of the owned rows.
 template <class T>
-void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, cudaStream_t s);
+void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cudaStream_t s);
 
 // One level-0 pass of `mode` (PASS_JACOBI, PASS_JACOBI_DOT, PASS_RESID_P, PASS_SPMV_DOT, PASS_POWER);
 // same arguments and outputs as csr_pass, A.grid partials.

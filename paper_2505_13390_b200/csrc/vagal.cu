@@ -1,0 +1,223 @@
+// Level-0 -> level-1 Galerkin product from the scaled gradients, see vagal.cuh.
+#include <algorithm>
+
+#include "setup.cuh"
+#include "util.cuh"
+#include "vagal.cuh"
+
+namespace mgpbd {
+
+namespace {
+
+template <class T>
+struct alignas(4 * sizeof(T)) G4 {
+    T x, y, z, w;
+};
+
+inline int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 32)); }
+
+// per vertex: incidences re-sorted by aggregate (stable: codes stay ascending inside an aggregate),
+// number of distinct aggregates
+__global__ void k_va_sort(int32_t nv, int kc, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vlist,
+                          const int32_t* __restrict__ agg, int32_t* __restrict__ vlist2, int32_t* __restrict__ pcnt) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        const int64_t e0 = vptr[v], e1 = vptr[v + 1];
+        for (int64_t e = e0; e < e1; ++e) vlist2[e] = vlist[e];
+        for (int64_t a = e0 + 1; a < e1; ++a) {
+            const int32_t c = vlist2[a];
+            const int32_t ka = agg[c / kc];
+            int64_t b = a - 1;
+            while (b >= e0) {
+                const int32_t cb = vlist2[b];
+                if (agg[cb / kc] <= ka) break;
+                vlist2[b + 1] = cb;
+                --b;
+            }
+            vlist2[b + 1] = c;
+        }
+        int32_t pc = 0, prev = -1;
+        for (int64_t e = e0; e < e1; ++e) {
+            const int32_t k = agg[vlist2[e] / kc];
+            if (k != prev) { ++pc; prev = k; }
+        }
+        pcnt[v] = pc;
+    }
+}
+
+// pair starts / aggregates, and k_v^2 products per vertex
+__global__ void k_va_pairs(int32_t nv, int kc, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vlist2,
+                           const int32_t* __restrict__ agg, const int64_t* __restrict__ vpp,
+                           int32_t* __restrict__ pstart, int32_t* __restrict__ pagg, int32_t* __restrict__ ccnt) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        const int64_t e0 = vptr[v], e1 = vptr[v + 1];
+        int64_t p = vpp[v];
+        int32_t prev = -1;
+        for (int64_t e = e0; e < e1; ++e) {
+            const int32_t k = agg[vlist2[e] / kc];
+            if (k != prev) { pstart[p] = (int32_t)e; pagg[p] = k; ++p; prev = k; }
+        }
+        const int32_t kv = (int32_t)(vpp[v + 1] - vpp[v]);
+        ccnt[v] = kv * kv;
+    }
+}
+
+// position of (a, b) in the coarse CSR (off-diagonals ascending, diagonal last); -1 if absent
+__device__ __forceinline__ int64_t coarse_pos(const int64_t* __restrict__ crowptr, const int32_t* __restrict__ ccol,
+                                              int32_t a, int32_t b) {
+    const int64_t r0 = crowptr[a], r1 = crowptr[a + 1];
+    if (a == b) return r1 - 1;
+    int64_t lo = r0, hi = r1 - 1;  // off-diagonal range [r0, r1-1)
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ccol[mid] < b) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < r1 - 1 && ccol[lo] == b) ? lo : -1;
+}
+
+__global__ void k_va_contrib(int32_t nv, const int64_t* __restrict__ vpp, const int64_t* __restrict__ coff,
+                             const int32_t* __restrict__ pagg, const int64_t* __restrict__ crowptr,
+                             const int32_t* __restrict__ ccol, int32_t* __restrict__ key, int2* __restrict__ pq,
+                             int32_t* __restrict__ bad) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        const int64_t p0 = vpp[v], p1 = vpp[v + 1];
+        int64_t idx = coff[v];
+        for (int64_t p = p0; p < p1; ++p)
+            for (int64_t q = p0; q < p1; ++q, ++idx) {
+                const int64_t pos = coarse_pos(crowptr, ccol, pagg[p], pagg[q]);
+                if (pos < 0) { atomicExch(bad, 1); key[idx] = 0; }
+                else key[idx] = (int32_t)pos;
+                pq[idx] = make_int2((int32_t)p, (int32_t)q);
+            }
+    }
+}
+
+__global__ void k_va_permute(int64_t n, const int32_t* __restrict__ list, const int2* __restrict__ in,
+                             int2* __restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = in[list[k]];
+}
+
+__global__ void k_va_erow(int32_t n, const int64_t* __restrict__ crowptr, int32_t* __restrict__ erow) {
+    for (int32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x)
+        for (int64_t k = crowptr[a]; k < crowptr[a + 1]; ++k) erow[k] = a;
+}
+
+// G_p = sum over the pair's incidences of P_j h_{j,s} (fp64 sum, incidence order)
+template <class T, int KC>
+__global__ void k_va_g(int64_t npairs, const int32_t* __restrict__ pstart, const int32_t* __restrict__ vlist2,
+                       const T* __restrict__ h, const T* __restrict__ P, G4<T>* __restrict__ G) {
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
+        double g0 = 0.0, g1_ = 0.0, g2 = 0.0;
+        for (int32_t e = pstart[p]; e < pstart[p + 1]; ++e) {
+            const int32_t code = vlist2[e];
+            const double pj = (double)P[code / KC];
+            const T* hh = h + (int64_t)code * 3;
+            g0 += pj * (double)hh[0];
+            g1_ += pj * (double)hh[1];
+            g2 += pj * (double)hh[2];
+        }
+        G[p] = G4<T>{(T)g0, (T)g1_, (T)g2, (T)0};
+    }
+}
+
+template <class T>
+__global__ void k_va_dterm(int32_t n_agg, const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
+                           const T* __restrict__ P, const T* __restrict__ at, double* __restrict__ dterm) {
+    for (int32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n_agg; a += gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = mptr[a]; k < mptr[a + 1]; ++k) {
+            const int32_t i = mlist[k];
+            const double pi = (double)P[i];
+            s += pi * pi * (double)at[i];
+        }
+        dterm[a] = s;
+    }
+}
+
+template <class T>
+__global__ void k_va_a1(int64_t cnnz, const int64_t* __restrict__ cptr, const int2* __restrict__ cpq,
+                        const G4<T>* __restrict__ G, const int32_t* __restrict__ erow,
+                        const int64_t* __restrict__ crowptr, const double* __restrict__ dterm, T* __restrict__ cval) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnnz; k += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t c = cptr[k]; c < cptr[k + 1]; ++c) {
+            const int2 pq = cpq[c];
+            const G4<T> a = G[pq.x], b = G[pq.y];
+            s += (double)a.x * (double)b.x + (double)a.y * (double)b.y + (double)a.z * (double)b.z;
+        }
+        const int32_t r = erow[k];
+        if (k == crowptr[r + 1] - 1) s += dterm[r];
+        cval[k] = (T)s;
+    }
+}
+
+}  // namespace
+
+void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg, int32_t n_agg,
+                 const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s) {
+    const int64_t ninc = read_scalar(vptr + nv, s);
+    plan.cnnz = cnnz;
+    plan.vlist2.resize(ninc);
+    DBuf<int32_t> pcnt, pagg, ccnt, key, clist, cnt;
+    DBuf<int64_t> vpp, coff;
+    DBuf<int2> pq;
+    pcnt.resize(nv);
+    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, plan.vlist2.p, pcnt.p);
+    MG_LAUNCH_CHECK();
+    vpp.resize((size_t)nv + 1);
+    scan_exclusive<int32_t>(pcnt.p, vpp.p, nv, s);
+    plan.npairs = read_scalar(vpp.p + nv, s);
+    plan.pstart.resize(plan.npairs + 1);
+    pagg.resize(plan.npairs);
+    ccnt.resize(nv);
+    k_va_pairs<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, plan.vlist2.p, agg, vpp.p, plan.pstart.p, pagg.p, ccnt.p);
+    MG_LAUNCH_CHECK();
+    const int32_t ninc32 = (int32_t)ninc;
+    MG_CK(cudaMemcpyAsync(plan.pstart.p + plan.npairs, &ninc32, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+    coff.resize((size_t)nv + 1);
+    scan_exclusive<int32_t>(ccnt.p, coff.p, nv, s);
+    plan.ncontrib = read_scalar(coff.p + nv, s);
+    key.resize(plan.ncontrib);
+    pq.resize(plan.ncontrib);
+    DBuf<int32_t> bad;
+    bad.resize(1);
+    MG_CK(cudaMemsetAsync(bad.p, 0, sizeof(int32_t), s));
+    k_va_contrib<<<g1(nv), 256, 0, s>>>(nv, vpp.p, coff.p, pagg.p, crowptr, ccol, key.p, pq.p, bad.p);
+    MG_LAUNCH_CHECK();
+    if (read_scalar(bad.p, s)) throw Error(-1, "va_symbolic: product outside the coarse pattern");
+    group_by_key(key.p, plan.ncontrib, cnnz, plan.cptr, clist, cnt, s, true);
+    plan.cpq.resize(plan.ncontrib);
+    k_va_permute<<<g1(plan.ncontrib), 256, 0, s>>>(plan.ncontrib, clist.p, pq.p, plan.cpq.p);
+    MG_LAUNCH_CHECK();
+    plan.erow.resize(cnnz);
+    k_va_erow<<<g1(n_agg), 256, 0, s>>>(n_agg, crowptr, plan.erow.p);
+    MG_LAUNCH_CHECK();
+    plan.dterm.resize(n_agg);
+    plan.G.resize((size_t)plan.npairs * 4 * sizeof(double));  // either hot type (allocated outside capture)
+    MG_CK(cudaStreamSynchronize(s));  // temporaries are freed on return
+}
+
+template <class T>
+void va_numeric(VaPlan& plan, int kc, const T* h, const T* P, const int64_t* mptr, const int32_t* mlist,
+                const T* at, int32_t n_agg, const int64_t* crowptr, T* cval, T* cdinv, cudaStream_t s) {
+    G4<T>* G = reinterpret_cast<G4<T>*>(plan.G.p);
+    if (plan.npairs) {
+        if (kc == 4) k_va_g<T, 4><<<g1(plan.npairs), 256, 0, s>>>(plan.npairs, plan.pstart.p, plan.vlist2.p, h, P, G);
+        else k_va_g<T, 2><<<g1(plan.npairs), 256, 0, s>>>(plan.npairs, plan.pstart.p, plan.vlist2.p, h, P, G);
+        MG_LAUNCH_CHECK();
+    }
+    k_va_dterm<T><<<g1(n_agg), 256, 0, s>>>(n_agg, mptr, mlist, P, at, plan.dterm.p);
+    MG_LAUNCH_CHECK();
+    k_va_a1<T><<<g1(plan.cnnz), 256, 0, s>>>(plan.cnnz, plan.cptr.p, plan.cpq.p, G, plan.erow.p, crowptr,
+                                             plan.dterm.p, cval);
+    MG_LAUNCH_CHECK();
+    diag_inv<T>(n_agg, crowptr, cval, cdinv, s);
+}
+
+template void va_numeric<float>(VaPlan&, int, const float*, const float*, const int64_t*, const int32_t*,
+                                const float*, int32_t, const int64_t*, float*, float*, cudaStream_t);
+template void va_numeric<double>(VaPlan&, int, const double*, const double*, const int64_t*, const int32_t*,
+                                 const double*, int32_t, const int64_t*, double*, double*, cudaStream_t);
+
+}  // namespace mgpbd

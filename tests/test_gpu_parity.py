@@ -142,6 +142,24 @@ def test_matrix_free_vcycle_and_pcg(name):
         assert rc == 0 and rel(ctx.debug_pcg(b, K), xo) <= 1e-8, K
 
 
+@pytest.mark.parametrize("name", ["bar3k", "cloth64", "block_small"])
+def test_galerkin_from_gradients_level1(name):
+    """With the matrix-free level 0 the Eq. 6 refresh of A_1 = P^T A_0 P is computed from the scaled
+    gradients (vertex-aggregate sums, csrc/vagal.cu); it must equal the oracle's explicit product."""
+    sc = make_scene(name)
+    ctx = ctx_for(sc, level0_operator=1)
+    ctx.step(sc.dt, 1)
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    h = O.Hierarchy(r, c, v)
+    assert h.n_levels > 1
+    rg, cg, vg = ctx.level(1)
+    ro, co, vo = h.level(1)
+    assert np.array_equal(rg, ro) and np.array_equal(cg, co)
+    assert np.abs(vg - vo).max() <= 1e-12 * np.abs(vo).max()
+
+
 @pytest.mark.parametrize("precision", [0, 1])
 def test_matrix_free_equals_csr_frames(precision):
     sc = scenes.make("block_small")
