@@ -17,6 +17,7 @@
 #include "comm.cuh"
 #include "matfree.cuh"
 #include "vagal.cuh"
+#include "coarse.cuh"
 
 namespace mgpbd {
 
@@ -166,6 +167,12 @@ class Engine : public EngineBase {
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
     double last_dt = 0.0;
+    // levels >= 1 of the V-cycle as one persistent kernel (coarse.cuh); MGPBD_NO_COARSE_KERNEL=1 disables
+    CoarseCycle<T> ccyc;
+    bool ccyc_ok = false;
+    bool use_coarse_kernel = std::getenv("MGPBD_NO_COARSE_KERNEL") == nullptr;
+    DBuf<unsigned long long> ctrace;
+    int ccyc_from = std::getenv("MGPBD_COARSE_FROM") ? std::atoi(std::getenv("MGPBD_COARSE_FROM")) : 1;
     bool mf_on() const { return cfg.level0_operator == 1 && mf_ready; }
 
     void setup_partition() {
@@ -472,6 +479,26 @@ class Engine : public EngineBase {
         }
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
+        ccyc_ok = false;
+        if (use_coarse_kernel && ccyc_from >= 1 && nL >= ccyc_from + 2) {
+            ccyc = CoarseCycle<T>();
+            ccyc.K = nL - ccyc_from;
+            ccyc.nu = cfg.smoother_sweeps;
+            ccyc.Ainv = Ainv.p;
+            if (std::getenv("MGPBD_TRACE_COARSE")) {
+                ctrace.resize(64);
+                MG_CK(cudaMemsetAsync(ctrace.p, 0, 64 * sizeof(unsigned long long), st));
+                ccyc.trace = ctrace.p;
+            }
+            for (int l = ccyc_from; l < nL; ++l) {
+                Level& a = *L[l];
+                CoarseLevel<T>& c = ccyc.L[l - ccyc_from];
+                c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p; c.omega = a.omega;
+                if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_agg = a.n_agg; }
+                c.t = a.vt.p; c.b = a.vb.p; c.z = a.vz.p; c.x = a.vx.p; c.y = a.vy.p;
+            }
+            ccyc_ok = true;
+        }
         invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
         stale = false;
@@ -522,6 +549,10 @@ class Engine : public EngineBase {
         Level& a = *L[l];
         if (l == nL - 1) {
             coarse_gemv<T>(a.n, Ainv.p, b, x_out, st);
+            return;
+        }
+        if (l == ccyc_from && ccyc_ok && b == a.vb.p && x_out == a.vz.p) {
+            coarse_vcycle<T>(ccyc, st);
             return;
         }
         const int nu = cfg.smoother_sweeps;
@@ -697,6 +728,14 @@ class Engine : public EngineBase {
         MG_CK(cudaEventRecord(f1, st));
         MG_CK(cudaStreamSynchronize(st));
         launches_last = g_kernel_launches;
+        if (ccyc.trace) {  // phase times of the last coarse V-cycle (MGPBD_TRACE_COARSE)
+            unsigned long long tt[64];
+            d2h(tt, ctrace.p, 64, st);
+            MG_CK(cudaStreamSynchronize(st));
+            std::fprintf(stderr, "[mgpbd coarse] K=%d phases (us):", ccyc.K);
+            for (int k = 1; k < 64 && tt[k] > tt[k - 1]; ++k) std::fprintf(stderr, " %.2f", (tt[k] - tt[k - 1]) * 1e-3);
+            std::fprintf(stderr, "\n");
+        }
         frame++;
         n_b = n_iters;
         float ms = 0;
