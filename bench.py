@@ -86,13 +86,15 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def traffic_per_launch():
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the level-0 pass, from the committed
-    ncu --set full capture summary (profiles/ncu_traffic.json), or None."""
+def traffic_per_launch(op=1):
+    """dram__bytes_read.sum + dram__bytes_write.sum per level-0 pass (both kernels of the matrix-free
+    pass, or the CSR k_rows pass for op=0), from the committed ncu --set full capture summary
+    (profiles/ncu_traffic.json), or None."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(p):
         try:
-            return json.load(open(p)).get("bytes_per_launch")
+            d = json.load(open(p))
+            return d.get("bytes_per_launch") if op == 1 else d.get("previous_csr_k_rows_bytes_per_launch")
         except Exception:
             return None
     return None
@@ -196,7 +198,8 @@ def run_ours(args):
         part = dict(rank=rank, world=world, nccl_id=obj[0])
     elif args.partitioned:
         part = dict(rank=0, world=1, nccl_id=mgpbd.nccl_unique_id())   # partitioned path, 1-rank NCCL
-    ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=0, **part)
+    ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=0,
+                                   level0_operator=args.level0_operator, **part)
     for _ in range(args.warmup):
         ctx.step(sc.dt, sc.n_iters)
     st0 = ctx.stats()
@@ -285,8 +288,10 @@ def run_ours(args):
             "indefinite_events_in_window": indef,
             "ms_frame_median": statistics.median(frames_ms)}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic_per_launch(),
-                     "kernel": "level-0 CSR passes (k_rows: omega-Jacobi / residual*P / SpMV+dot / Jacobi+r.z)",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic_per_launch(args.level0_operator),
+                     "kernel": ("level-0 matrix-free passes (k_mf_vgather + k_mf_rows: omega-Jacobi / residual*P / "
+                                "SpMV+dot / Jacobi+r.z)") if args.level0_operator == 1 else
+                               "level-0 CSR passes (k_rows: omega-Jacobi / residual*P / SpMV+dot / Jacobi+r.z)",
                      "peak_kind": peak_kind, "profiled_frames": args.profile_frames,
                      "l0_pass_share_of_frame": (l0_ms / prof_frames_ms) if prof_frames_ms else None},
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * n * 8,
@@ -322,6 +327,8 @@ def main():
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-slab", type=int, default=8, help="x-slabs of the block the oracle sample uses")
+    ap.add_argument("--level0-operator", type=int, default=1, choices=[0, 1],
+                    help="1: matrix-free level 0 (default), 0: assembled-CSR level-0 passes")
     ap.add_argument("--partitioned", action="store_true",
                     help="N=1 only: run the row-partitioned (NCCL) code path on a 1-rank communicator")
     ap.add_argument("--profile-frames", type=int, default=2, help="frames timed per level-0 pass for the roofline")

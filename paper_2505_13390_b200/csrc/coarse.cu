@@ -198,7 +198,7 @@ __device__ __forceinline__ void dense_solve(const Lanes& w, int32_t n, const dou
 
 template <class T>
 __device__ __forceinline__ bool fused_level(const CoarseLevel<T>& L) {
-    return L.n_agg < 1500;  // small level: one phase (warp per aggregate) beats two
+    return L.n_agg < 500;  // small level: one phase (warp per aggregate) beats two
 }
 
 template <class T>
@@ -272,15 +272,33 @@ __global__ void __launch_bounds__(CB, 2) k_coarse_vcycle(const __grid_constant__
     // ---- up
     for (int k = K - 2; k >= 0; --k) {
         const CoarseLevel<T>& L = sc.L[k];
-        pre_rows(w, L, p);
-        grid.sync(); mark();
-        const T* __restrict__ cu = cur[k];
+        T* __restrict__ cu = cur[k];
         const T* __restrict__ zc = sc.L[k + 1].z;
         const T* __restrict__ P = L.P;
         const int32_t* __restrict__ agg = L.agg;
         T* dst = nu == 1 ? L.z : (cu == L.x ? L.y : L.x);
-        // post sweep 1 with the prolongation x_j + P_j z_c[agg_j] evaluated on the fly
-        sweep(w, L, p, [&](int32_t j) { return (T)((double)cu[j] + (double)P[j] * (double)zc[agg[j]]); }, dst);
+        if (L.n >= 32768) {
+            // large level: materialise x += P z_c[agg] (row-local; static operands loaded before the
+            // barrier), then a plain sweep — cheaper than three extra gathers per nonzero
+            const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+            const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+            int32_t a0 = 0;
+            double x0 = 0.0, p0 = 0.0;
+            if (tid < L.n) { a0 = agg[tid]; x0 = (double)cu[tid]; p0 = (double)P[tid]; }
+            grid.sync(); mark();
+            for (int64_t i = tid; i < L.n; i += nt) {
+                if (i != tid) { a0 = agg[i]; x0 = (double)cu[i]; p0 = (double)P[i]; }
+                cu[i] = (T)(x0 + p0 * (double)zc[a0]);
+            }
+            pre_rows(w, L, p);
+            grid.sync(); mark();
+            sweep(w, L, p, [&](int32_t j) { return cu[j]; }, dst);
+        } else {
+            pre_rows(w, L, p);
+            grid.sync(); mark();
+            // post sweep 1 with the prolongation x_j + P_j z_c[agg_j] evaluated on the fly
+            sweep(w, L, p, [&](int32_t j) { return (T)((double)cu[j] + (double)P[j] * (double)zc[agg[j]]); }, dst);
+        }
         for (int s = 2; s <= nu; ++s) {
             pre_rows(w, L, p);
             grid.sync(); mark();

@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
 // (A x)_i = sum_s h_{i,s} . u_{v_s} + at_i x_i in the storage precision, epilogue in fp64 exactly as
 // the CSR row kernels (solve.cu k_rows).
 template <class T, int KC, int MODE>
-__global__ void __launch_bounds__(MF_BS) k_mf_rows(int32_t row0, int32_t row1, const int32_t* __restrict__ verts,
+__global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, int32_t row1, const int32_t* __restrict__ verts,
                                                    const T* __restrict__ h, const V4<T>* __restrict__ u,
                                                    const T* __restrict__ at, const T* __restrict__ dinv,
                                                    const T* __restrict__ x, const T* __restrict__ b,
@@ -141,7 +141,7 @@ template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
                 double* parts, double* parts2, cudaStream_t s) {
     if (A.v1 > A.v0) {
-        constexpr int G = KC == 4 ? 8 : 4;  // ~23 (tets) / ~6 (cloth) incidences per vertex
+        constexpr int G = KC == 4 ? 4 : 2;  // ~23 (tets) / ~6 (cloth) incidences per vertex
         const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
         const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * 16);
         k_mf_vgather<T, KC, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, x,
