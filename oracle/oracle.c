@@ -20,6 +20,7 @@ void orc_config_default(orc_config* c) {
     c->theta = 0.1; c->min_coarse = 400; c->max_levels = 16; c->stall_ratio = 0.9;
     c->setup_interval = 20; c->bootstrap_sweeps = 20; c->power_iters = 100;
     c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
+    c->smoother = 0; c->cheb_lower = 0.25;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -622,6 +623,7 @@ typedef struct {
     int32_t n; int64_t nnz;
     int64_t* rowptr; int32_t* col; double* val;
     int32_t* agg; int32_t n_agg; double* P; double omega;
+    double cheb_theta, cheb_delta;  /* Chebyshev interval (reading c20) */
 } orc_level;
 
 struct orc_hier {
@@ -702,6 +704,11 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
         orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, c->col, c->val);
         double lam = orc_power(a->n, a->rowptr, a->col, a->val, cfg->power_iters, cfg->seed, l);
         a->omega = 2.0 / (cfg->lambda_safety * lam + cfg->lambda_min_est);
+        {   /* Chebyshev interval [cheb_lower*hi, hi], hi = safety*lambda_max (reading c20) */
+            const double hi = cfg->lambda_safety * lam, lo = cfg->cheb_lower * hi;
+            a->cheb_theta = 0.5 * (hi + lo);
+            a->cheb_delta = 0.5 * (hi - lo);
+        }
         h->L = l + 2;
     }
     free(B);
@@ -745,6 +752,44 @@ static void jacobi(const orc_level* a, const double* b, double* x, double* tmp) 
     for (int32_t i = 0; i < a->n; ++i) x[i] += a->omega * (b[i] - tmp[i]) / a->val[a->rowptr[i + 1] - 1];
 }
 
+/* Chebyshev smoother (lazily set parameters PAPER.md:320; reading c20): `sweeps` steps
+ * of the Chebyshev iteration for A x = b preconditioned by D = diag(A) on the interval
+ * [lo, hi] of D^-1 A (Saad, Iterative Methods for Sparse Linear Systems, 2nd ed., Alg. 12.1):
+ *   theta = (hi+lo)/2, delta = (hi-lo)/2, sigma = theta/delta, rho_0 = 1/sigma,
+ *   step 0:  r = D^-1 (b - A x),  d = r / theta,                                   x += d
+ *   step k:  r = D^-1 (b - A x),  rho_k = 1/(2 sigma - rho_{k-1}),
+ *            d = rho_k rho_{k-1} d + (2 rho_k / delta) r,                            x += d        */
+static void chebyshev(const orc_level* a, int sweeps, const double* b, double* x, double* tmp, double* d) {
+    const double theta = a->cheb_theta, delta = a->cheb_delta, sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    for (int k = 0; k < sweeps; ++k) {
+        orc_spmv(a->n, a->rowptr, a->col, a->val, x, tmp);
+        const double rho_new = k == 0 ? rho : 1.0 / (2.0 * sigma - rho);
+        for (int32_t i = 0; i < a->n; ++i) {
+            const double r = (b[i] - tmp[i]) / a->val[a->rowptr[i + 1] - 1];
+            d[i] = k == 0 ? r / theta : rho_new * rho * d[i] + (2.0 * rho_new / delta) * r;
+            x[i] += d[i];
+        }
+        rho = rho_new;
+    }
+}
+
+static void smooth(const orc_hier* h, const orc_level* a, const double* b, double* x, double* tmp, double* d) {
+    if (h->cfg.smoother == 1) chebyshev(a, h->cfg.smoother_sweeps, b, x, tmp, d);
+    else for (int s = 0; s < h->cfg.smoother_sweeps; ++s) jacobi(a, b, x, tmp);
+}
+
+void orc_hier_cheb(const orc_hier* h, int l, double* theta, double* delta) {
+    *theta = h->lv[l].cheb_theta; *delta = h->lv[l].cheb_delta;
+}
+void orc_hier_smooth(const orc_hier* h, int l, const double* b, double* x) {
+    const orc_level* a = &h->lv[l];
+    double* tmp = xmalloc(sizeof(double) * (size_t)a->n);
+    double* d = xmalloc(sizeof(double) * (size_t)a->n);
+    smooth(h, a, b, x, tmp, d);
+    free(tmp); free(d);
+}
+
 /* V-cycle from x = 0: nu pre-sweeps, r = b - A x, b_c = P^T r, recurse,
  * x += P e, nu post-sweeps; coarsest level solved by the dense Cholesky factor (c8). */
 static void vcycle_level(const orc_hier* h, int l, const double* b, double* x) {
@@ -752,16 +797,17 @@ static void vcycle_level(const orc_hier* h, int l, const double* b, double* x) {
     if (l == h->L - 1) { orc_chol_solve(a->n, h->Lc, b, x); return; }
     int32_t n = a->n, nc = a->n_agg;
     double* tmp = xmalloc(sizeof(double) * (size_t)n);
+    double* d = xmalloc(sizeof(double) * (size_t)n);
     for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
-    for (int s = 0; s < h->cfg.smoother_sweeps; ++s) jacobi(a, b, x, tmp);
+    smooth(h, a, b, x, tmp, d);
     orc_spmv(n, a->rowptr, a->col, a->val, x, tmp);
     double* bc = xcalloc((size_t)nc, sizeof(double));
     double* ec = xmalloc(sizeof(double) * (size_t)nc);
     for (int32_t i = 0; i < n; ++i) bc[a->agg[i]] += a->P[i] * (b[i] - tmp[i]);
     vcycle_level(h, l + 1, bc, ec);
     for (int32_t i = 0; i < n; ++i) x[i] += a->P[i] * ec[a->agg[i]];
-    for (int s = 0; s < h->cfg.smoother_sweeps; ++s) jacobi(a, b, x, tmp);
-    free(tmp); free(bc); free(ec);
+    smooth(h, a, b, x, tmp, d);
+    free(tmp); free(d); free(bc); free(ec);
 }
 
 void orc_vcycle(const orc_hier* h, const double* b, double* x) { vcycle_level(h, 0, b, x); }

@@ -33,6 +33,8 @@ typedef struct {
     double omega_relax;      /* 0.1 tet / 0.25 cloth */
     double gravity[3];       /* (0,-9.8,0) */
     uint64_t seed;           /* 1 */
+    int32_t smoother;        /* 0 omega-Jacobi, 1 Chebyshev (reading c20) */
+    double cheb_lower;       /* Chebyshev interval [cheb_lower*hi, hi], hi = safety*lambda_max; 0.25 (c20) */
 } orc_config;
 
 void orc_config_default(orc_config* c);
@@ -98,6 +100,10 @@ void orc_hier_get_level(const orc_hier* h, int l, int64_t* rowptr, int32_t* col,
 void orc_hier_get_agg(const orc_hier* h, int l, int32_t* agg);
 void orc_hier_get_P(const orc_hier* h, int l, double* P);
 double orc_hier_omega(const orc_hier* h, int l);
+/* Chebyshev interval centre theta and half-width delta of level l (reading c20) */
+void orc_hier_cheb(const orc_hier* h, int l, double* theta, double* delta);
+/* one smoothing pass (the level's configured smoother, cfg.smoother_sweeps steps) on A x = b */
+void orc_hier_smooth(const orc_hier* h, int l, const double* b, double* x);
 void orc_hier_get_B0(const orc_hier* h, double* B);
 int32_t orc_hier_n_colours(const orc_hier* h);
 void orc_vcycle(const orc_hier* h, const double* b, double* x);

@@ -27,7 +27,8 @@ class Config(C.Structure):
                 ("bootstrap_sweeps", C.c_int32), ("power_iters", C.c_int32),
                 ("lambda_min_est", C.c_double), ("lambda_safety", C.c_double), ("smoother_sweeps", C.c_int32),
                 ("pcg_iters", C.c_int32), ("omega_relax", C.c_double),
-                ("gravity", C.c_double * 3), ("seed", C.c_uint64)]
+                ("gravity", C.c_double * 3), ("seed", C.c_uint64), ("smoother", C.c_int32),
+                ("cheb_lower", C.c_double)]
 
 
 _lib = None
@@ -74,6 +75,8 @@ def lib():
             "orc_hier_get_agg": (None, [P, C.c_int, P]),
             "orc_hier_get_P": (None, [P, C.c_int, P]),
             "orc_hier_omega": (f64, [P, C.c_int]),
+            "orc_hier_cheb": (None, [P, C.c_int, P, P]),
+            "orc_hier_smooth": (None, [P, C.c_int, P, P]),
             "orc_hier_get_B0": (None, [P, P]),
             "orc_hier_n_colours": (i32, [P]),
             "orc_vcycle": (None, [P, P, P]),
@@ -344,6 +347,18 @@ class Hierarchy:
 
     def omega(self, l) -> float:
         return float(lib().orc_hier_omega(self.h, l))
+
+    def cheb(self, l):
+        """(theta, delta) of level l's Chebyshev interval (reading c20)."""
+        t, d = C.c_double(), C.c_double()
+        lib().orc_hier_cheb(self.h, l, C.byref(t), C.byref(d))
+        return t.value, d.value
+
+    def smooth(self, l, b, x0):
+        """One pre/post smoothing pass (configured smoother) at level l, from x0."""
+        x = _c(x0, np.float64).copy()
+        lib().orc_hier_smooth(self.h, l, _p(_c(b, np.float64)), _p(x))
+        return x
 
     def B0(self):
         n, _ = self.level_size(0)

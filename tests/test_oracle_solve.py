@@ -217,3 +217,98 @@ def test_deterministic(O):
         sim.step(sc.dt, sc.n_iters)
         outs.append(sim.state())
     assert all(np.array_equal(a, b) for a, b in zip(*outs))
+
+
+# ------------------------------------------------------------------ Chebyshev smoother (reading c20)
+def _cheb_T(k, z):
+    return np.cos(k * np.arccos(z)) if abs(z) <= 1 else np.cosh(k * np.arccosh(abs(z))) * np.sign(z) ** k
+
+
+def _tridiag(n, c):
+    A = np.eye(n) - c * (np.eye(n, k=1) + np.eye(n, k=-1))
+    return A, 1.0 - 2.0 * c * np.cos(np.arange(1, n + 1) * np.pi / (n + 1))
+
+
+@pytest.mark.parametrize("sweeps", [1, 2, 3])
+def test_chebyshev_residual_is_the_scaled_chebyshev_polynomial(O, sweeps):
+    """A = tridiag(-c, 1, -c) has D = I and eigenpairs (1 - 2c cos(k pi/(n+1)), sin).  From x = 0 with
+    b = an eigenvector v (eigenvalue lam), s Chebyshev steps on [lo, hi] leave the residual
+    T_s((theta - lam)/delta) / T_s(theta/delta) * v — the defining property of the Chebyshev iteration
+    (Saad, Alg. 12.1) — and the interval is hi = safety * lambda_max(D^-1 A), lo = 0.25 hi (c20)."""
+    n, c = 500, 0.45
+    A, lam = _tridiag(n, c)
+    r, cc, v = csr_from_dense_diaglast(A)
+    cfg = O.default_config(smoother=1, smoother_sweeps=sweeps, power_iters=3000)
+    h = O.Hierarchy(r, cc, v, cfg)
+    assert h.n_levels >= 2
+    theta, delta = h.cheb(0)
+    hi, lo = theta + delta, theta - delta
+    # power method from below, tiny spectral gap at the top: 1e-3 (its own pin is in test_oracle_setup)
+    assert 0 <= 1.1 * lam.max() - hi <= 1e-3 * hi and abs(lo - 0.25 * hi) <= 1e-12 * hi
+    i = np.arange(1, n + 1)
+    for k in (1, 7, 60, 250, 499):
+        vk = np.sin(k * i * np.pi / (n + 1))
+        x = h.smooth(0, vk, np.zeros(n))
+        res = vk - A @ x
+        want = _cheb_T(sweeps, (theta - lam[k - 1]) / delta) / _cheb_T(sweeps, theta / delta)
+        assert np.allclose(res, want * vk, rtol=1e-9, atol=1e-11), k
+
+
+def test_chebyshev_one_step_is_jacobi_with_one_over_theta(O):
+    """s = 1: x = D^-1 b / theta (the Chebyshev iteration's first step is damped Jacobi)."""
+    n = 500
+    A, _ = _tridiag(n, 0.3)
+    A = A * np.linspace(1.0, 3.0, n)[:, None] ** 0.5 * np.linspace(1.0, 3.0, n)[None, :] ** 0.5  # D != I
+    r, c, v = csr_from_dense_diaglast(A)
+    h = O.Hierarchy(r, c, v, O.default_config(smoother=1, smoother_sweeps=1))
+    theta, _ = h.cheb(0)
+    b = np.random.default_rng(4).normal(size=n)
+    assert np.allclose(h.smooth(0, b, np.zeros(n)), b / np.diag(A) / theta, rtol=1e-14)
+
+
+def test_chebyshev_vcycle_linear_symmetric_and_pcg(O, bar_sys):
+    """The Chebyshev V-cycle is a symmetric positive definite linear operator (identical pre/post
+    polynomials in D^-1 A) and MGPCG with it converges."""
+    r, c, v, A = bar_sys
+    h = O.Hierarchy(r, c, v, O.default_config(smoother=1))
+    rng = np.random.default_rng(6)
+    n = A.shape[0]
+    for _ in range(5):
+        u, w = rng.normal(size=n), rng.normal(size=n)
+        a, bb = rng.normal(size=2)
+        lhs = h.vcycle(a * u + bb * w)
+        assert np.linalg.norm(lhs - a * h.vcycle(u) - bb * h.vcycle(w)) <= 1e-10 * np.linalg.norm(lhs)
+        Mu, Mw = h.vcycle(u), h.vcycle(w)
+        assert abs(Mu @ w - u @ Mw) <= 1e-9 * np.linalg.norm(Mu) * np.linalg.norm(w)
+        assert u @ Mu > 0
+    b = rng.normal(size=n)
+    x, rc, _ = h.pcg(b, 300)
+    assert rc == 0 and np.linalg.norm(A @ x - b) <= 1e-3 * np.linalg.norm(b)
+
+
+def test_chebyshev_two_level_matches_dense_definition(O, bar_sys):
+    """Dense re-derivation of a two-level Chebyshev V-cycle: x_{k+1} = x_k + d_k with
+    d_0 = D^-1 r_0 / theta, d_k = rho_k rho_{k-1} d_{k-1} + 2 rho_k / delta D^-1 r_k."""
+    r, c, v, A = bar_sys
+    h = O.Hierarchy(r, c, v, O.default_config(max_levels=2, smoother=1))
+    n = A.shape[0]
+    agg, P = h.agg(0), h.P(0)
+    theta, delta = h.cheb(0)
+    Pm = np.zeros((n, agg.max() + 1)); Pm[np.arange(n), agg] = P
+    Ac = Pm.T @ A @ Pm
+    Dinv = 1.0 / np.diag(A)
+
+    def cheb(x, b):
+        sigma = theta / delta
+        rho = 1 / sigma
+        d = Dinv * (b - A @ x) / theta
+        x = x + d
+        rho_new = 1 / (2 * sigma - rho)
+        d = rho_new * rho * d + 2 * rho_new / delta * Dinv * (b - A @ x)
+        return x + d
+
+    b = np.random.default_rng(7).normal(size=n)
+    x = cheb(np.zeros(n), b)
+    x = x + Pm @ np.linalg.solve(Ac, Pm.T @ (b - A @ x))
+    x = cheb(x, b)
+    assert np.allclose(h.vcycle(b), x, rtol=1e-9, atol=1e-12 * np.abs(x).max())
