@@ -79,7 +79,7 @@ typedef struct {
     double lambda_min_est;    /* user estimate of lambda_min, 0.1 */
     double lambda_safety;     /* omega = 2/(lambda_safety*lambda_max + lambda_min_est), 1.1: keeps the
                                  lazily-set omega below 2/lambda_max as A drifts (reading c9) */
-    int32_t smoother_sweeps;  /* pre = post omega-Jacobi sweeps, 2 */
+    int32_t smoother_sweeps;  /* pre = post smoother steps, 2 (1..8) */
     int32_t pcg_iters;        /* fixed MGPCG iterations per outer iteration (reading c10), 10 */
     double omega_relax;       /* x += omega dx: 0.1 tets, 0.25 cloth */
     double gravity[3];        /* (0, -9.8, 0) */
@@ -98,6 +98,10 @@ typedef struct {
                                  A x = H (H^T x) + at x from the scaled gradients (SURVEY.md §8(f) f4,
                                  PAPER.md:450); the CSR is assembled either way (Galerkin, diagonal).
                                  Default 1 */
+    int32_t smoother;         /* V-cycle smoother: 0 = omega-Jacobi (default), 1 = Chebyshev
+                                 (smoother_sweeps steps = polynomial degree; reading c20) */
+    double cheb_lower;        /* Chebyshev interval [cheb_lower * hi, hi] of D^-1 A, hi = lambda_safety *
+                                 lambda_max (power method, lazily at setup: PAPER.md:320); 0.25 */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16

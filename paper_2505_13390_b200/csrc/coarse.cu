@@ -93,17 +93,22 @@ __device__ __forceinline__ void pre_rows(const Lanes& w, const CoarseLevel<T>& L
     pre_row(w, L, i < L.n, i, p);
 }
 
-// One omega-Jacobi sweep y = x + omega D^-1 (b - A x) over all rows, x given by xf(j) (materialised
-// vector or an on-the-fly expression).
-template <class T, class XF>
-__device__ __forceinline__ void sweep(const Lanes& w, const CoarseLevel<T>& L, Pre<T>& p, XF xf, T* __restrict__ out) {
+// One smoother step over all rows: y = x + alpha (x - xprev) + omega D^-1 (b - A x), x given by xf(j)
+// (materialised vector or an on-the-fly expression), xprev by xpf(i) (row-local; unused if alpha = 0).
+template <class T, class XF, class XPF>
+__device__ __forceinline__ void sweep(const Lanes& w, const CoarseLevel<T>& L, Pre<T>& p, XF xf, XPF xpf, double omega,
+                                      double alpha, T* __restrict__ out) {
     for (int64_t base = w.gw * RPW; base < L.n; base += w.nw * RPW) {  // warp-uniform trip count
         const int64_t i = base + w.sub;
         const bool valid = i < L.n;
         if (base != w.gw * RPW) pre_row(w, L, valid, i, p);
         const double s = row_sum(w, L, p, xf);
-        if (valid && w.sl == 0)
-            out[i] = (T)((double)xf((int32_t)i) + L.omega * (double)L.dinv[i] * ((double)L.b[i] - s));
+        if (valid && w.sl == 0) {
+            const double xi = (double)xf((int32_t)i);
+            double y = xi + omega * (double)L.dinv[i] * ((double)L.b[i] - s);
+            if (alpha != 0.0) y += alpha * (xi - (double)xpf((int32_t)i));
+            out[i] = (T)y;
+        }
     }
 }
 
@@ -232,24 +237,29 @@ __global__ void __launch_bounds__(CB, 2) k_coarse_vcycle(const __grid_constant__
     if (K > 1) pre_rows(w, sc.L[0], p);
     for (int k = 0; k + 1 < K; ++k) {
         const CoarseLevel<T>& L = sc.L[k];
-        // pre-smoothing: sweep 1 (x = omega D^-1 b) evaluated on the fly inside sweep 2
+        const T* __restrict__ b = L.b;
+        const T* __restrict__ d = L.dinv;
+        const double om0 = L.sm_omega[0];
+        auto x1f = [&](int32_t j) { return (T)(om0 * (double)d[j] * (double)b[j]); };  // step 0 from x = 0
+        auto zero = [&](int32_t) { return (T)0; };
         T* cu = L.x;
         T* ot = L.y;
         if (nu >= 2) {
-            const T* __restrict__ b = L.b;
-            const T* __restrict__ d = L.dinv;
-            const double om = L.omega;
-            sweep(w, L, p, [&](int32_t j) { return (T)(om * (double)d[j] * (double)b[j]); }, L.x);
-            for (int s = 2; s < nu; ++s) {
+            // pre-smoothing: step 0 (x_1 = omega_0 D^-1 b) evaluated on the fly inside step 1 (x_0 = 0)
+            sweep(w, L, p, x1f, zero, L.sm_omega[1], L.sm_alpha[1], L.x);
+            for (int s = 2; s < nu; ++s) {  // step s: x_{s+1} written over x_{s-1} (row-local read first)
                 pre_rows(w, L, p);
                 grid.sync(); mark();
                 const T* __restrict__ src = cu;
-                sweep(w, L, p, [&](int32_t j) { return src[j]; }, ot);
+                T* __restrict__ prv = ot;
+                if (s == 2) sweep(w, L, p, [&](int32_t j) { return src[j]; }, x1f, L.sm_omega[s], L.sm_alpha[s], ot);
+                else sweep(w, L, p, [&](int32_t j) { return src[j]; }, [&](int32_t i) { return prv[i]; },
+                           L.sm_omega[s], L.sm_alpha[s], ot);
                 T* t = cu; cu = ot; ot = t;
             }
         } else {
             for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < L.n; i += (int64_t)gridDim.x * blockDim.x)
-                L.x[i] = (T)(L.omega * (double)L.dinv[i] * (double)L.b[i]);
+                L.x[i] = x1f((int32_t)i);
         }
         cur[k] = cu;
         if (fused_level(L)) {
@@ -273,13 +283,15 @@ __global__ void __launch_bounds__(CB, 2) k_coarse_vcycle(const __grid_constant__
     for (int k = K - 2; k >= 0; --k) {
         const CoarseLevel<T>& L = sc.L[k];
         T* __restrict__ cu = cur[k];
+        T* ot = cu == L.x ? L.y : L.x;
         const T* __restrict__ zc = sc.L[k + 1].z;
         const T* __restrict__ P = L.P;
         const int32_t* __restrict__ agg = L.agg;
-        T* dst = nu == 1 ? L.z : (cu == L.x ? L.y : L.x);
-        if (L.n >= 32768) {
-            // large level: materialise x += P z_c[agg] (row-local; static operands loaded before the
-            // barrier), then a plain sweep — cheaper than three extra gathers per nonzero
+        const bool mat = L.n >= 32768;
+        auto zero = [&](int32_t) { return (T)0; };
+        if (mat) {
+            // large level: materialise x_0 = x + P z_c[agg] (row-local; static operands loaded before
+            // the barrier) — cheaper than three extra gathers per nonzero in the next step
             const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
             const int64_t nt = (int64_t)gridDim.x * blockDim.x;
             int32_t a0 = 0;
@@ -290,21 +302,25 @@ __global__ void __launch_bounds__(CB, 2) k_coarse_vcycle(const __grid_constant__
                 if (i != tid) { a0 = agg[i]; x0 = (double)cu[i]; p0 = (double)P[i]; }
                 cu[i] = (T)(x0 + p0 * (double)zc[a0]);
             }
-            pre_rows(w, L, p);
-            grid.sync(); mark();
-            sweep(w, L, p, [&](int32_t j) { return cu[j]; }, dst);
-        } else {
-            pre_rows(w, L, p);
-            grid.sync(); mark();
-            // post sweep 1 with the prolongation x_j + P_j z_c[agg_j] evaluated on the fly
-            sweep(w, L, p, [&](int32_t j) { return (T)((double)cu[j] + (double)P[j] * (double)zc[agg[j]]); }, dst);
         }
-        for (int s = 2; s <= nu; ++s) {
+        // x_0 of the post-smoothing: materialised, or the prolongation evaluated on the fly
+        auto x0f = [&](int32_t j) { return mat ? cu[j] : (T)((double)cu[j] + (double)P[j] * (double)zc[agg[j]]); };
+        pre_rows(w, L, p);
+        grid.sync(); mark();
+        T* src = nu == 1 ? L.z : ot;
+        sweep(w, L, p, x0f, zero, L.sm_omega[0], 0.0, src);  // step 0 (alpha_0 = 0)
+        T* prv = cu;                                          // buffer of x_{s-1}
+        for (int s = 1; s < nu; ++s) {
             pre_rows(w, L, p);
             grid.sync(); mark();
-            const T* __restrict__ src = dst;
-            dst = s == nu ? L.z : (src == L.x ? L.y : L.x);
-            sweep(w, L, p, [&](int32_t j) { return src[j]; }, dst);
+            T* out = s == nu - 1 ? L.z : prv;                  // over x_{s-1} (row-local read first)
+            const T* __restrict__ xs = src;
+            const T* __restrict__ xp = prv;
+            if (s == 1) sweep(w, L, p, [&](int32_t j) { return xs[j]; }, x0f, L.sm_omega[s], L.sm_alpha[s], out);
+            else sweep(w, L, p, [&](int32_t j) { return xs[j]; }, [&](int32_t i) { return xp[i]; }, L.sm_omega[s],
+                       L.sm_alpha[s], out);
+            prv = src;
+            src = out;
         }
     }
 }

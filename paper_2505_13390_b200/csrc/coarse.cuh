@@ -8,6 +8,8 @@
 //   coarsest: z = A_c^-1 b (dense fp64 inverse)                                          | barrier
 //   up:   [sweep 1 with the prolongation x_j + P_j z_c[agg_j] evaluated on the fly]      | barrier
 //         [sweep 2 -> z]                                                                  | barrier
+// Smoother steps are the general x_{k+1} = x_k + alpha_k (x_k - x_{k-1}) + omega_k D^-1 (b - A x_k)
+// (omega-Jacobi: alpha = 0; Chebyshev: three-term recurrence).
 // Same operators, smoothing schedule and arithmetic precision as the per-level kernels (solve.cu);
 // only the summation order inside a row differs.
 #pragma once
@@ -22,7 +24,11 @@ struct CoarseLevel {
     const int32_t* col = nullptr;
     const T* val = nullptr;
     const T* dinv = nullptr;
-    double omega = 0.0;
+    double omega = 0.0;             // (unused by the cycle; the per-step coefficients below)
+    // smoother step k (k < nu): x_{k+1} = x_k + alpha_k (x_k - x_{k-1}) + omega_k D^-1 (b - A x_k);
+    // omega-Jacobi: omega_k = omega, alpha_k = 0; Chebyshev: the three-term recurrence (reading c20)
+    double sm_omega[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    double sm_alpha[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     // towards the next level (unused on the coarsest)
     const int32_t* agg = nullptr;
     const T* P = nullptr;

@@ -72,6 +72,7 @@ class Engine : public EngineBase {
         DBuf<T> tval;
         DBuf<double> tval64;
         double omega = 0.0;
+        double sm_omega[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sm_alpha[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // set_smoother
         // V-cycle vectors
         DBuf<T> vb, vz, vx, vy, vt;
         int vl = 32, grid = 1, vlr = 0, tile_nnz = 0;
@@ -368,12 +369,13 @@ class Engine : public EngineBase {
         return e;
     }
 
-    void l0_pass(int mode, const T* xin, const T* b, T* y, const T* aux, double omega) {
+    void l0_pass(int mode, const T* xin, const T* b, T* y, const T* aux, double omega, double alpha = 0.0,
+                 const T* xprev = nullptr) {
         const Level& l0 = *L[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (cfg.profile) { e0 = prof_event(); MG_CK(cudaEventRecord(e0, st)); }
-        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st);
-        else csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
+        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
+        else csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
         if (cfg.profile) {
             e1 = prof_event();
             MG_CK(cudaEventRecord(e1, st));
@@ -383,13 +385,39 @@ class Engine : public EngineBase {
         }
     }
 
-    void pass(int l, int mode, const T* xin, const T* b, T* y, const T* aux, double omega) {
+    // alpha/xprev: the Chebyshev momentum of a smoother step (solve.cuh); 0 / nullptr otherwise
+    void pass(int l, int mode, const T* xin, const T* b, T* y, const T* aux, double omega, double alpha = 0.0,
+              const T* xprev = nullptr) {
         if (l == 0) {
             // partitioned level 0: bring the halo columns of x from the owning ranks first
             if (dist) comm->exchange(const_cast<T*>(xin), sizeof(T), xfers, st);
-            l0_pass(mode, xin, b, y, aux, omega);
+            l0_pass(mode, xin, b, y, aux, omega, alpha, xprev);
         }
-        else csr_pass<T>(mode, L[l]->hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st);
+        else csr_pass<T>(mode, L[l]->hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
+    }
+
+    // Smoother coefficients of level a from lambda_max(D^-1 A) (lazily, at setup: PAPER.md:320).
+    // Step k: x_{k+1} = x_k + alpha_k (x_k - x_{k-1}) + omega_k D^-1 (b - A x_k).
+    //   omega-Jacobi: omega_k = 2/(s lambda + lambda_min_est), alpha_k = 0 (c9);
+    //   Chebyshev on [lo, hi] = [cheb_lower hi, s lambda] (reading c20, Saad Alg. 12.1 with
+    //   d_{k-1} = x_k - x_{k-1}): omega_0 = 1/theta, alpha_0 = 0, rho_0 = delta/theta,
+    //   rho_k = 1/(2 theta/delta - rho_{k-1}), alpha_k = rho_k rho_{k-1}, omega_k = 2 rho_k/delta.
+    void set_smoother(Level& a, double lam) {
+        a.omega = 2.0 / (cfg.lambda_safety * lam + cfg.lambda_min_est);
+        for (int k = 0; k < 8; ++k) { a.sm_omega[k] = a.omega; a.sm_alpha[k] = 0.0; }
+        if (cfg.smoother == 1) {
+            const double hi = cfg.lambda_safety * lam, lo = cfg.cheb_lower * hi;
+            const double theta = 0.5 * (hi + lo), delta = 0.5 * (hi - lo), sigma = theta / delta;
+            double rho = 1.0 / sigma;
+            a.sm_omega[0] = 1.0 / theta;
+            a.sm_alpha[0] = 0.0;
+            for (int k = 1; k < 8; ++k) {
+                const double rn = 1.0 / (2.0 * sigma - rho);
+                a.sm_alpha[k] = rn * rho;
+                a.sm_omega[k] = 2.0 * rn / delta;
+                rho = rn;
+            }
+        }
     }
 
     // ------------------------------------------------------------------ setup (Fig. setup-pipline)
@@ -446,7 +474,7 @@ class Engine : public EngineBase {
                                      a2.tval64.p, c.val64.p, c.dinv64.p, st);
             trace("galerkin_numeric", l);
             double lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
-            a2.omega = 2.0 / (cfg.lambda_safety * lam + cfg.lambda_min_est);
+            set_smoother(a2, lam);
             trace("power", l);
             B.swap(Bn);
             nL = l + 2;
@@ -494,6 +522,7 @@ class Engine : public EngineBase {
                 Level& a = *L[l];
                 CoarseLevel<T>& c = ccyc.L[l - ccyc_from];
                 c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p; c.omega = a.omega;
+                for (int k = 0; k < 8; ++k) { c.sm_omega[k] = a.sm_omega[k]; c.sm_alpha[k] = a.sm_alpha[k]; }
                 if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_agg = a.n_agg; }
                 c.t = a.vt.p; c.b = a.vb.p; c.z = a.vz.p; c.x = a.vx.p; c.y = a.vy.p;
             }
@@ -559,9 +588,9 @@ class Engine : public EngineBase {
         T* cur = a.vx.p;
         T* nxt = a.vy.p;
         const int32_t o = lo0(l), cn = cnt(l);  // rows this rank updates at this level
-        vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.omega, cur + o, st);
-        for (int sw = 1; sw < nu; ++sw) {
-            pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.omega);
+        vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.sm_omega[0], cur + o, st);  // step 0 from x = 0
+        for (int sw = 1; sw < nu; ++sw) {  // x_{sw+1} over x_{sw-1} (x_0 = 0: no xprev)
+            pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.sm_omega[sw], a.sm_alpha[sw], sw == 1 ? nullptr : nxt);
             std::swap(cur, nxt);
         }
         pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
@@ -572,9 +601,11 @@ class Engine : public EngineBase {
         prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
         for (int sw = 0; sw < nu; ++sw) {
             const bool last = sw == nu - 1;
-            T* dst = last ? x_out : (cur == a.vx.p ? a.vy.p : a.vx.p);
-            if (last && dot_r) pass(l, PASS_JACOBI_DOT, cur, b, dst, dot_r, a.omega);
-            else pass(l, PASS_JACOBI, cur, b, dst, nullptr, a.omega);
+            T* other = cur == a.vx.p ? a.vy.p : a.vx.p;  // holds x_{sw-1} for sw >= 1
+            T* dst = last ? x_out : other;
+            const T* xprev = sw == 0 ? nullptr : other;
+            if (last && dot_r) pass(l, PASS_JACOBI_DOT, cur, b, dst, dot_r, a.sm_omega[sw], a.sm_alpha[sw], xprev);
+            else pass(l, PASS_JACOBI, cur, b, dst, nullptr, a.sm_omega[sw], a.sm_alpha[sw], xprev);
             cur = dst;
         }
     }
@@ -937,6 +968,8 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->nccl_id = nullptr;
     c->vgroup = nullptr;
     c->level0_operator = 1;
+    c->smoother = 0;
+    c->cheb_lower = 0.25;
     return MGPBD_OK;
 }
 
@@ -957,6 +990,9 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail("bad rank/world");
     if (cfg->world > 1 && !cfg->nccl_id && !cfg->vgroup) return fail("world > 1 needs nccl_id or vgroup");
     if (cfg->level0_operator != 0 && cfg->level0_operator != 1) return fail("level0_operator must be 0 or 1");
+    if (cfg->smoother != 0 && cfg->smoother != 1) return fail("smoother must be 0 (omega-Jacobi) or 1 (Chebyshev)");
+    if (cfg->smoother_sweeps > 8) return fail("smoother_sweeps must be <= 8");
+    if (cfg->smoother == 1 && !(cfg->cheb_lower > 0.0 && cfg->cheb_lower < 1.0)) return fail("cheb_lower must be in (0, 1)");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > 4096 || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
         cfg->max_dense_coarse < 1)

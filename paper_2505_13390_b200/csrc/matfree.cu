@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
                                                    const T* __restrict__ at, const T* __restrict__ dinv,
                                                    const T* __restrict__ x, const T* __restrict__ b,
                                                    T* __restrict__ y, const T* __restrict__ aux, double omega,
+                                                   double alpha, const T* __restrict__ xprev,
                                                    double* __restrict__ parts, double* __restrict__ parts2) {
     using IV = typename std::conditional<KC == 4, int4, int2>::type;
     double acc1 = 0.0, acc2 = 0.0;
@@ -107,7 +108,9 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
         }
         const double s = (double)acc;
         if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
-            const T yi = (T)((double)xi + omega * (double)dinv[i] * ((double)b[i] - s));
+            double yd = (double)xi + omega * (double)dinv[i] * ((double)b[i] - s);
+            if (alpha != 0.0) yd += alpha * ((double)xi - (xprev ? (double)xprev[i] : 0.0));  // Chebyshev step
+            const T yi = (T)yd;
             y[i] = yi;
             if (MODE == PASS_JACOBI_DOT) {
                 const double ai = (double)aux[i];
@@ -139,7 +142,7 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 
 template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-                double* parts, double* parts2, cudaStream_t s) {
+                double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
     if (A.v1 > A.v0) {
         constexpr int G = KC == 4 ? 4 : 2;  // ~23 (tets) / ~6 (cloth) incidences per vertex
         const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
@@ -151,7 +154,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
     const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
 #define MG_MF(M)                                                                                            \
     k_mf_rows<T, KC, M><<<A.grid, MF_BS, 0, s>>>(A.row0, A.row1, A.verts, A.h, u, A.at, A.dinv, x, b, y, aux, \
-                                                  omega, parts, parts2)
+                                                  omega, alpha, xprev, parts, parts2)
     switch (mode) {
         case PASS_JACOBI: MG_MF(PASS_JACOBI); break;
         case PASS_JACOBI_DOT: MG_MF(PASS_JACOBI_DOT); break;
@@ -186,15 +189,15 @@ void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cu
 
 template <class T>
 void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-             double* parts, double* parts2, cudaStream_t s) {
-    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s);
-    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s);
+             double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
+    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev);
+    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev);
 }
 
 #define MG_INST(T)                                                                                           \
     template void mf_refresh<T>(const MatFree<T>&, const double*, double, T*, cudaStream_t);                     \
     template void mf_pass<T>(int, const MatFree<T>&, const T*, const T*, T*, const T*, double, double*, double*, \
-                             cudaStream_t);
+                             cudaStream_t, double, const T*);
 MG_INST(float)
 MG_INST(double)
 #undef MG_INST

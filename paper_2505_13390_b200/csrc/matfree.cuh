@@ -42,6 +42,6 @@ void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cu
 // same arguments and outputs as csr_pass, A.grid partials.
 template <class T>
 void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-             double* parts, double* parts2, cudaStream_t s);
+             double* parts, double* parts2, cudaStream_t s, double alpha = 0.0, const T* xprev = nullptr);
 
 }  // namespace mgpbd

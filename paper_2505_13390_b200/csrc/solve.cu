@@ -9,6 +9,17 @@
 namespace mgpbd {
 namespace {
 
+// Relaxation step of the smoother passes: y_i = x_i + omega D^-1 (b - A x)_i, plus the Chebyshev
+// momentum alpha (x_i - xprev_i) (xprev == nullptr: xprev = 0).  alpha = 0 is plain omega-Jacobi,
+// bit-identical to x_i + omega d_i (b_i - s).
+template <class T>
+__device__ __forceinline__ double relax(double xi, int64_t i, double omega, double alpha, const T* __restrict__ xprev,
+                                        double di, double bi, double s) {
+    double y = xi + omega * di * (bi - s);
+    if (alpha != 0.0) y += alpha * (xi - (xprev ? (double)xprev[i] : 0.0));
+    return y;
+}
+
 constexpr int PB = 256;  // threads per block of the CSR passes
 
 inline int vgrid(int64_t n) {
@@ -23,7 +34,7 @@ __global__ void __launch_bounds__(PB) k_pass(int32_t row0, int32_t n, const int6
                                              const int32_t* __restrict__ col, const T* __restrict__ val,
                                              const T* __restrict__ dinv, const T* __restrict__ x,
                                              const T* __restrict__ b, T* __restrict__ y,
-                                             const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                             const T* __restrict__ aux, double omega, double alpha, const T* __restrict__ xprev, double* __restrict__ parts,
                                              double* __restrict__ parts2) {
     constexpr int RPW = 32 / VL;  // rows per warp
     const int lane = threadIdx.x & 31;
@@ -43,7 +54,7 @@ __global__ void __launch_bounds__(PB) k_pass(int32_t row0, int32_t n, const int6
         s = group_sum<VL>(s);
         if (valid && sub == 0) {
             if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
-                T yi = (T)((double)x[i] + omega * (double)dinv[i] * ((double)b[i] - s));
+                T yi = (T)relax((double)x[i], i, omega, alpha, xprev, (double)dinv[i], (double)b[i], s);
                 y[i] = yi;
                 if (MODE == PASS_JACOBI_DOT) {
                     double r = (double)aux[i];
@@ -82,7 +93,7 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t row0, int32_t n, const int6
                                              const int32_t* __restrict__ col, const T* __restrict__ val,
                                              const T* __restrict__ dinv, const T* __restrict__ x,
                                              const T* __restrict__ b, T* __restrict__ y,
-                                             const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                             const T* __restrict__ aux, double omega, double alpha, const T* __restrict__ xprev, double* __restrict__ parts,
                                              double* __restrict__ parts2) {
     extern __shared__ double prod[];
     constexpr int R = PB / VLR;
@@ -108,7 +119,7 @@ __global__ void __launch_bounds__(PB) k_tile(int32_t row0, int32_t n, const int6
         s = group_sum<VLR>(s);
         if (ln == 0 && i < r1) {
             if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
-                T yi = (T)((double)x[i] + omega * (double)dinv[i] * ((double)b[i] - s));
+                T yi = (T)relax((double)x[i], i, omega, alpha, xprev, (double)dinv[i], (double)b[i], s);
                 y[i] = yi;
                 if (MODE == PASS_JACOBI_DOT) {
                     double r = (double)aux[i];
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t row0, int32_t n, int32_t
                                                 const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
                                                 const T* __restrict__ val, const T* __restrict__ dinv,
                                                 const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
-                                                const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                                const T* __restrict__ aux, double omega, double alpha, const T* __restrict__ xprev, double* __restrict__ parts,
                                                 double* __restrict__ parts2) {
     extern __shared__ __align__(16) unsigned char smraw[];
     T* prod = reinterpret_cast<T*>(smraw);
@@ -241,7 +252,7 @@ __global__ void __launch_bounds__(BB, 1) k_band(int32_t row0, int32_t n, int32_t
             double s = group_sum<VLR>((double)sl);
             if (own && ln == 0) {
                 if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
-                    T yi = (T)((double)xs[i - lo] + omega * di * (bi - s));
+                    T yi = (T)relax((double)xs[i - lo], i, omega, alpha, xprev, di, bi, s);
                     y[i] = yi;
                     if (MODE == PASS_JACOBI_DOT) { acc1 += ai * (double)yi; acc2 += ai * ai; }
                 } else if (MODE == PASS_RESID_P) {
@@ -295,7 +306,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t row0, int32_t n, int32_t
                                                 const int64_t* __restrict__ rowptr, const uint16_t* __restrict__ col,
                                                 const T* __restrict__ val, const T* __restrict__ dinv,
                                                 const T* __restrict__ x, const T* __restrict__ b, T* __restrict__ y,
-                                                const T* __restrict__ aux, double omega, double* __restrict__ parts,
+                                                const T* __restrict__ aux, double omega, double alpha, const T* __restrict__ xprev, double* __restrict__ parts,
                                                 double* __restrict__ parts2) {
     extern __shared__ __align__(16) unsigned char smraw[];
     // shared: [row offsets of the band tile, int32 relative to its first nonzero]
@@ -362,7 +373,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t row0, int32_t n, int32_t
                 const double bi = NB ? (double)ob[i - c0] : 0.0, di = ND ? (double)od[i - c0] : 0.0,
                              ai = NA ? (double)oa[i - c0] : 0.0;
                 if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
-                    T yi = (T)((double)xs[i - lo] + omega * di * (bi - s));
+                    T yi = (T)relax((double)xs[i - lo], i, omega, alpha, xprev, di, bi, s);
                     y[i] = yi;
                     if (MODE == PASS_JACOBI_DOT) { acc1 += ai * (double)yi; acc2 += ai * ai; }
                 } else if (MODE == PASS_RESID_P) {
@@ -409,7 +420,7 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t row0, int32_t n, int32_t
 }
 
 template <class T, int MODE, int VL>
-void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                  double* parts2, cudaStream_t s) {
     static size_t attr_set = 48 * 1024;
     const size_t smem = ((((size_t)A.band_rows + 1) * sizeof(int32_t) + 15) & ~(size_t)15) +
@@ -419,23 +430,23 @@ void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         attr_set = smem;
     }
     k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.row0, A.row0 + A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col16,
-                                                     A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
+                                                     A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2);
     MG_LAUNCH_CHECK();
 }
 
 template <class T, int MODE>
-void launch_rows_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_rows_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                       double* parts2, cudaStream_t s) {
     switch (A.row_vl) {
-        case 4: launch_rows<T, MODE, 4>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 8: launch_rows<T, MODE, 8>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 16: launch_rows<T, MODE, 16>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        default: launch_rows<T, MODE, 32>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 4: launch_rows<T, MODE, 4>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 8: launch_rows<T, MODE, 8>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 16: launch_rows<T, MODE, 16>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        default: launch_rows<T, MODE, 32>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
     }
 }
 
 template <class T, int MODE, int VLR>
-void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                  double* parts2, cudaStream_t s) {
     static size_t attr_set = 48 * 1024;
     const size_t smem = ((size_t)A.prod_cap + 8 + A.band_win) * sizeof(T);
@@ -444,20 +455,20 @@ void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         attr_set = smem;
     }
     k_band<T, VLR, MODE><<<A.band_grid, BB, smem, s>>>(A.row0, A.row0 + A.n, A.band_rows, A.win_lo, A.win_len, A.prod_cap, A.rowptr,
-                                                      A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
+                                                      A.col, A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2);
     MG_LAUNCH_CHECK();
 }
 
 template <class T, int MODE>
-void launch_band_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_band_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                       double* parts2, cudaStream_t s) {
     switch (A.vlr) {
-        case 1: launch_band<T, MODE, 1>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 2: launch_band<T, MODE, 2>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 4: launch_band<T, MODE, 4>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 8: launch_band<T, MODE, 8>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 16: launch_band<T, MODE, 16>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        default: launch_band<T, MODE, 32>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 1: launch_band<T, MODE, 1>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 2: launch_band<T, MODE, 2>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 4: launch_band<T, MODE, 4>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 8: launch_band<T, MODE, 8>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 16: launch_band<T, MODE, 16>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        default: launch_band<T, MODE, 32>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
     }
 }
 
@@ -485,7 +496,7 @@ __global__ void k_band_len(int32_t nb, int32_t* __restrict__ lo, const int32_t* 
 }
 
 template <class T, int MODE, int VLR>
-void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                  double* parts2, cudaStream_t s) {
     static size_t attr_set = 48 * 1024;
     const size_t smem = (size_t)A.tile_nnz * sizeof(double);
@@ -493,20 +504,20 @@ void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, do
         MG_CK(cudaFuncSetAttribute(k_tile<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_set = smem;
     }
-    k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2);
+    k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2);
     MG_LAUNCH_CHECK();
 }
 
 template <class T, int MODE>
-void launch_tile_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_tile_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                       double* parts2, cudaStream_t s) {
     switch (A.vlr) {
-        case 1: launch_tile<T, MODE, 1>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 2: launch_tile<T, MODE, 2>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 4: launch_tile<T, MODE, 4>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 8: launch_tile<T, MODE, 8>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case 16: launch_tile<T, MODE, 16>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        default: launch_tile<T, MODE, 32>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case 1: launch_tile<T, MODE, 1>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 2: launch_tile<T, MODE, 2>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 4: launch_tile<T, MODE, 4>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 8: launch_tile<T, MODE, 8>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case 16: launch_tile<T, MODE, 16>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        default: launch_tile<T, MODE, 32>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
     }
 }
 
@@ -519,9 +530,9 @@ __global__ void k_max_tile(int32_t n, int R, const int64_t* __restrict__ rowptr,
 }
 
 template <class T, int MODE>
-void launch_pass_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
+void launch_pass_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                       double* parts2, cudaStream_t s) {
-#define MG_P(VL) k_pass<T, VL, MODE><<<A.grid, PB, 0, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, parts, parts2)
+#define MG_P(VL) k_pass<T, VL, MODE><<<A.grid, PB, 0, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2)
     switch (A.vl) {
         case 2: MG_P(2); break;
         case 4: MG_P(4); break;
@@ -964,47 +975,47 @@ int pass_grid(int32_t n, int vl) {
 
 template <class T>
 void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double* parts,
-              double* parts2, cudaStream_t s) {
+              double* parts2, cudaStream_t s, double alpha, const T* xprev) {
     if (A.n == 0) return;
     if (A.band_rows > 0 && A.row_vl > 0) {
         switch (mode) {
-            case PASS_JACOBI: launch_rows_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_JACOBI_DOT: launch_rows_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_RESID_P: launch_rows_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_SPMV_DOT: launch_rows_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_POWER: launch_rows_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_JACOBI: launch_rows_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_JACOBI_DOT: launch_rows_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_RESID_P: launch_rows_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_SPMV_DOT: launch_rows_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_POWER: launch_rows_mode<T, PASS_POWER>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
             default: throw Error(-1, "bad pass mode");
         }
         return;
     }
     if (A.band_rows > 0) {
         switch (mode) {
-            case PASS_JACOBI: launch_band_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_JACOBI_DOT: launch_band_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_RESID_P: launch_band_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_SPMV_DOT: launch_band_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_POWER: launch_band_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_JACOBI: launch_band_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_JACOBI_DOT: launch_band_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_RESID_P: launch_band_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_SPMV_DOT: launch_band_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_POWER: launch_band_mode<T, PASS_POWER>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
             default: throw Error(-1, "bad pass mode");
         }
         return;
     }
     if (A.vlr > 0) {
         switch (mode) {
-            case PASS_JACOBI: launch_tile_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_JACOBI_DOT: launch_tile_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_RESID_P: launch_tile_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_SPMV_DOT: launch_tile_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-            case PASS_POWER: launch_tile_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+            case PASS_JACOBI: launch_tile_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_JACOBI_DOT: launch_tile_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_RESID_P: launch_tile_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_SPMV_DOT: launch_tile_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+            case PASS_POWER: launch_tile_mode<T, PASS_POWER>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
             default: throw Error(-1, "bad pass mode");
         }
         return;
     }
     switch (mode) {
-        case PASS_JACOBI: launch_pass_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case PASS_JACOBI_DOT: launch_pass_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case PASS_RESID_P: launch_pass_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case PASS_SPMV_DOT: launch_pass_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, parts, parts2, s); break;
-        case PASS_POWER: launch_pass_mode<T, PASS_POWER>(A, x, b, y, aux, omega, parts, parts2, s); break;
+        case PASS_JACOBI: launch_pass_mode<T, PASS_JACOBI>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case PASS_JACOBI_DOT: launch_pass_mode<T, PASS_JACOBI_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case PASS_RESID_P: launch_pass_mode<T, PASS_RESID_P>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case PASS_SPMV_DOT: launch_pass_mode<T, PASS_SPMV_DOT>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
+        case PASS_POWER: launch_pass_mode<T, PASS_POWER>(A, x, b, y, aux, omega, alpha, xprev, parts, parts2, s); break;
         default: throw Error(-1, "bad pass mode");
     }
 }
@@ -1100,7 +1111,7 @@ void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s
 
 #define MG_INST(T)                                                                                            \
     template void csr_pass<T>(int, const Csr<T>&, const T*, const T*, T*, const T*, double, double*, double*,  \
-                              cudaStream_t);                                                                   \
+                              cudaStream_t, double, const T*);                                                 \
     template void vec_jacobi0<T>(int32_t, const T*, const T*, double, T*, cudaStream_t);                       \
     template void restrict_members<T>(int32_t, const int64_t*, const int32_t*, const T*, T*, cudaStream_t);    \
     template void prolong_add<T>(int32_t, const int32_t*, const T*, const T*, T*, cudaStream_t);               \

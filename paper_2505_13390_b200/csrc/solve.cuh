@@ -61,7 +61,9 @@ int pass_grid(int32_t n, int vl);
 
 template <class T>
 void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-              double* parts, double* parts2, cudaStream_t s);
+              double* parts, double* parts2, cudaStream_t s, double alpha = 0.0, const T* xprev = nullptr);
+// (PASS_JACOBI / PASS_JACOBI_DOT with alpha != 0: y = x + alpha (x - xprev) + omega D^-1 (b - A x),
+//  the Chebyshev three-term step; xprev == nullptr means xprev = 0)
 
 template <class T> void vec_jacobi0(int32_t n, const T* dinv, const T* b, double omega, T* y, cudaStream_t s);
 template <class T> void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, const T* t,

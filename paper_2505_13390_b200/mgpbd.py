@@ -47,7 +47,8 @@ class Config(C.Structure):
                 ("omega_relax", C.c_double), ("gravity", C.c_double * 3), ("seed", C.c_uint64),
                 ("device", C.c_int32), ("stream", C.c_void_p), ("max_dense_coarse", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32),
-                ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32)]
+                ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32),
+                ("smoother", C.c_int32), ("cheb_lower", C.c_double)]
 
 
 class Stats(C.Structure):
