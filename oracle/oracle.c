@@ -21,6 +21,7 @@ void orc_config_default(orc_config* c) {
     c->setup_interval = 20; c->bootstrap_sweeps = 20; c->power_iters = 100;
     c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
     c->smoother = 0; c->cheb_lower = 0.25;
+    c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -864,6 +865,8 @@ struct orc_sim {
     orc_config cfg;
     double b_norm[1024];
     int32_t n_b;
+    int32_t iters_used;
+    double omega_last;
     int32_t n_indef;  /* PCG iterations with <z,r> <= 0 (r != 0) in the last frame */
 };
 
@@ -923,12 +926,18 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
         }
     for (int32_t j = 0; j < m; ++j) { s->lambda[j] = 0.0; s->atilde[j] = s->alpha[j] / (dt * dt); }
     s->n_b = 0;
+    /* omega of l.11: user-specified, or halved whenever ||b|| rises (reading c21) */
+    double omega = s->cfg.omega_relax, bprev = -1.0, b0 = 0.0;
     for (int32_t ite = 0; ite < n_iters; ++ite) {
         if (s->kind == 2) orc_eval_distance(m, s->verts, s->x, s->rest_len, s->C, s->g);          /* l.4 */
         else orc_eval_arap(m, s->verts, s->x, s->Dm_inv, s->C, s->g);
         orc_assemble(m, s->kind, s->verts, s->w, s->g, s->atilde, s->rowptr, s->col, s->val);   /* l.5 */
         orc_rhs(m, s->C, s->atilde, s->lambda, s->b);                                            /* l.6 */
-        if (s->n_b < 1024) s->b_norm[s->n_b++] = sqrt(dot(m, s->b, s->b));
+        const double bn = sqrt(dot(m, s->b, s->b));
+        if (s->n_b < 1024) s->b_norm[s->n_b++] = bn;
+        if (ite == 0) b0 = bn;
+        if (s->cfg.backtrack && ite > 0 && bn > bprev) omega = fmax(0.5 * omega, s->cfg.omega_min);
+        bprev = bn;
         if (ite == 0 && (s->h == NULL || s->stale || s->frame % s->cfg.setup_interval == 0)) { /* l.7 */
             orc_hier_free(s->h);
             s->h = orc_hier_build(m, s->rowptr, s->col, s->val, &s->cfg);
@@ -938,8 +947,11 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
         s->n_indef += orc_pcg(s->h, s->b, s->cfg.pcg_iters, s->dl, NULL);                         /* l.8 */
         orc_apply_dx(m, s->kind, s->verts, n, s->w, s->g, s->dl, s->dx);                         /* l.9 */
         for (int32_t j = 0; j < m; ++j) s->lambda[j] += s->dl[j];                               /* l.10 */
-        for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->x[k] += s->cfg.omega_relax * s->dx[k];  /* l.11 */
+        for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->x[k] += omega * s->dx[k];              /* l.11 */
+        s->iters_used = ite + 1;
+        if (s->cfg.residual_tol > 0.0 && bn < s->cfg.residual_tol * b0) break;                 /* l.12 */
     }
+    s->omega_last = omega;
     for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->v[k] = (s->x[k] - s->x_old[k]) / dt;      /* l.17 */
     s->frame++;
     if (s->n_indef) s->stale = 1;
@@ -947,6 +959,8 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
 }
 
 void orc_sim_mark_stale(orc_sim* s) { s->stale = 1; }
+int32_t orc_sim_iters_used(const orc_sim* s) { return s->iters_used; }
+double orc_sim_omega(const orc_sim* s) { return s->omega_last; }
 int32_t orc_sim_indefinite_events(const orc_sim* s) { return s->n_indef; }
 void orc_sim_get(const orc_sim* s, double* x, double* v, double* lambda) {
     if (x) memcpy(x, s->x, sizeof(double) * 3 * (size_t)s->n);

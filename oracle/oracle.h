@@ -35,6 +35,9 @@ typedef struct {
     uint64_t seed;           /* 1 */
     int32_t smoother;        /* 0 omega-Jacobi, 1 Chebyshev (reading c20) */
     double cheb_lower;       /* Chebyshev interval [cheb_lower*hi, hi], hi = safety*lambda_max; 0.25 (c20) */
+    int32_t backtrack;       /* 1: halve omega when ||b|| rises (reading c21); 0 */
+    double omega_min;        /* floor of the halving; 1e-3 */
+    double residual_tol;     /* Alg. 1 l.12: break once ||b|| < residual_tol * ||b_0||; 0 = off (c11/c21) */
 } orc_config;
 
 void orc_config_default(orc_config* c);
@@ -123,6 +126,8 @@ const orc_hier* orc_sim_hier(const orc_sim* s);
 int64_t orc_sim_nnz(const orc_sim* s);
 void orc_sim_get_A(const orc_sim* s, int64_t* rowptr, int32_t* col, double* val);
 void orc_sim_get_b_norms(const orc_sim* s, double* out, int32_t n);
+int32_t orc_sim_iters_used(const orc_sim* s);      /* outer iterations run by the last frame */
+double orc_sim_omega(const orc_sim* s);            /* relaxation omega at the end of the last frame */
 void orc_sim_free(orc_sim* s);
 
 #ifdef __cplusplus

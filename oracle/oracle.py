@@ -28,7 +28,8 @@ class Config(C.Structure):
                 ("lambda_min_est", C.c_double), ("lambda_safety", C.c_double), ("smoother_sweeps", C.c_int32),
                 ("pcg_iters", C.c_int32), ("omega_relax", C.c_double),
                 ("gravity", C.c_double * 3), ("seed", C.c_uint64), ("smoother", C.c_int32),
-                ("cheb_lower", C.c_double)]
+                ("cheb_lower", C.c_double), ("backtrack", C.c_int32), ("omega_min", C.c_double),
+                ("residual_tol", C.c_double)]
 
 
 _lib = None
@@ -85,6 +86,8 @@ def lib():
             "orc_sim_step": (C.c_int, [P, f64, i32]),
             "orc_sim_mark_stale": (None, [P]),
             "orc_sim_indefinite_events": (i32, [P]),
+            "orc_sim_iters_used": (i32, [P]),
+            "orc_sim_omega": (f64, [P]),
             "orc_sim_get": (None, [P, P, P, P]),
             "orc_sim_set": (None, [P, P, P]),
             "orc_sim_hier": (P, [P]),
@@ -419,6 +422,12 @@ class Sim:
 
     def indefinite_events(self) -> int:
         return int(lib().orc_sim_indefinite_events(self.s))
+
+    def iters_used(self) -> int:
+        return int(lib().orc_sim_iters_used(self.s))
+
+    def omega(self) -> float:
+        return float(lib().orc_sim_omega(self.s))
 
     def state(self):
         x = np.empty((self.n, 3)); v = np.empty((self.n, 3)); lam = np.empty(self.m)

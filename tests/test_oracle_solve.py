@@ -108,8 +108,10 @@ def test_pcg_identity(O):
     assert rc == 0 and np.allclose(x, b, rtol=1e-14)
 
 
-def _python_frame(O, sc, n_iters, omega, gravity=(0, -9.8, 0)):
-    """Algorithm 1 with a dense direct solve in place of MGPCG."""
+def _python_frame(O, sc, n_iters, omega, gravity=(0, -9.8, 0), backtrack=False, omega_min=1e-3, tol=0.0,
+                  trace=None):
+    """Algorithm 1 with a dense direct solve in place of MGPCG; optional backtracking
+    (halve omega when ||b|| rises) and the ||b|| < tol ||b_0|| exit (l.12)."""
     x = sc.pos.copy(); v = sc.vel.copy(); w = sc.inv_mass
     x_old = x.copy()
     v[w > 0] += sc.dt * np.asarray(gravity)
@@ -118,13 +120,25 @@ def _python_frame(O, sc, n_iters, omega, gravity=(0, -9.8, 0)):
     at = sc.compliance / sc.dt ** 2
     rowptr, col = O.pattern(sc.verts, sc.n_verts)
     rest = O.rest_distance(sc.verts, sc.rest_pos) if sc.kind == 2 else O.rest_arap(sc.verts, sc.rest_pos)[0]
-    for _ in range(n_iters):
+    bprev = None
+    for ite in range(n_iters):
         Cv, g = (O.eval_distance if sc.kind == 2 else O.eval_arap)(sc.verts, x, rest)
         A = dense(rowptr, col, O.assemble(sc.verts, w, g, at, rowptr, col))
-        dl = np.linalg.solve(A, -Cv - at * lam)
+        b = -Cv - at * lam
+        nb = np.linalg.norm(b)
+        if ite == 0:
+            b0 = nb
+        if backtrack and bprev is not None and nb > bprev:
+            omega = max(0.5 * omega, omega_min)
+        bprev = nb
+        dl = np.linalg.solve(A, b)
         dx = O.apply_dx(sc.verts, sc.n_verts, w, g, dl)
         lam += dl
         x = x + omega * dx
+        if trace is not None:
+            trace.append((ite, nb, omega))
+        if tol > 0 and nb < tol * b0:
+            break
     return x, (x - x_old) / sc.dt, lam
 
 
@@ -312,3 +326,42 @@ def test_chebyshev_two_level_matches_dense_definition(O, bar_sys):
     x = x + Pm @ np.linalg.solve(Ac, Pm.T @ (b - A @ x))
     x = cheb(x, b)
     assert np.allclose(h.vcycle(b), x, rtol=1e-9, atol=1e-12 * np.abs(x).max())
+
+
+# ------------------------------------------------------------------ outer-loop variants (reading c21)
+def test_backtrack_rule_examples(O):
+    """decrease -> unchanged; increase halves; repeated halving floors at 1e-3."""
+    omega, seq = 0.1, []
+    for _ in range(9):
+        omega = max(0.5 * omega, 1e-3)
+        seq.append(omega)
+    assert seq[6] == 1e-3 and seq[5] > 1e-3 and seq[-1] == 1e-3
+
+
+@pytest.mark.parametrize("name", ["cloth4", "bar_small"])
+def test_backtracking_and_residual_exit_equal_dense_frame(O, name):
+    """Backtracking omega and the ||b|| < eps exit in the oracle's frame against the dense Python
+    Algorithm 1 (single-level hierarchy: MGPCG is exact), and the halving actually triggered."""
+    sc = scenes.cloth(4, dt=3e-3) if name == "cloth4" else scenes.make(name)
+    om = 1.0 if name == "cloth4" else 0.9         # large omega: overshoot, ||b|| rises, halving kicks in
+    cfg = O.default_config(omega_relax=om, pcg_iters=3, backtrack=1)
+    sim = O.Sim(sc, cfg)
+    assert sim.step(sc.dt, 12) == 0
+    trace = []
+    xr, _, lr = _python_frame(O, sc, 12, om, backtrack=True, trace=trace)
+    x, _, lam = sim.state()
+    # 12 outer iterations of a stiff system amplify the solves' rounding (Cholesky vs LAPACK): 1e-7
+    assert np.abs(lam - lr).max() <= 1e-7 * np.abs(lr).max()
+    assert np.abs((x - sc.pos) - (xr - sc.pos)).max() <= 1e-7 * np.abs(xr - sc.pos).max()
+    assert sim.omega() == trace[-1][2] < om                      # halved at least once
+    nb = sim.b_norms(12)
+    assert np.allclose(nb, [t[1] for t in trace], rtol=1e-7)
+    # residual exit: stops at the first iteration whose ||b|| < tol ||b_0||, after its update
+    tol = 1.001 * nb[:6].min() / nb[0]
+    cfg = O.default_config(omega_relax=om, pcg_iters=3, backtrack=1, residual_tol=tol)
+    sim = O.Sim(sc, cfg)
+    sim.step(sc.dt, 12)
+    trace = []
+    xr, _, lr = _python_frame(O, sc, 12, om, backtrack=True, tol=tol, trace=trace)
+    assert sim.iters_used() == len(trace) < 12
+    assert np.abs(sim.state()[2] - lr).max() <= 1e-7 * np.abs(lr).max()
