@@ -102,6 +102,11 @@ typedef struct {
                                  (smoother_sweeps steps = polynomial degree; reading c20) */
     double cheb_lower;        /* Chebyshev interval [cheb_lower * hi, hi] of D^-1 A, hi = lambda_safety *
                                  lambda_max (power method, lazily at setup: PAPER.md:320); 0.25 */
+    int32_t backtrack;        /* 1: halve the relaxation omega (floor omega_min) whenever ||b|| of an outer
+                                 iteration exceeds the previous one (reading c21); 0 */
+    double omega_min;         /* 1e-3 */
+    double residual_tol;      /* Alg. 1 l.12: stop the frame after the first outer iteration with
+                                 ||b|| < residual_tol * ||b_0|| (one host read per iteration); 0 = off */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16
@@ -130,6 +135,7 @@ typedef struct {
     int32_t rank, world;               /* partitioned run: this rank / number of ranks (1 otherwise) */
     int32_t row_begin, row_end;        /* level-0 rows this rank owns */
     int64_t halo_rows;                 /* level-0 x entries received per halo exchange */
+    double omega_relax;                /* relaxation omega at the end of the last frame (backtracking) */
 } mgpbd_stats;
 
 /* Fill *cfg with the defaults listed above.  Never fails for a non-NULL cfg. */

@@ -168,6 +168,8 @@ class Engine : public EngineBase {
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
     double last_dt = 0.0;
+    DBuf<double> omega_dev;     // relaxation omega of Alg. 1 l.11 (device scalar: backtracking, c21)
+    double omega_last = 0.0;
     // levels >= 1 of the V-cycle as one persistent kernel (coarse.cuh); MGPBD_NO_COARSE_KERNEL=1 disables
     CoarseCycle<T> ccyc;
     bool ccyc_ok = false;
@@ -682,7 +684,7 @@ class Engine : public EngineBase {
         refresh();                                                                                   // Eq. 6
         pcg(cfg.pcg_iters, ite);                                                                     // l.8
         if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
-        update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, cfg.omega_relax, x.p, st);  // l.9, l.11
+        update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);  // l.9, l.11
         lambda_add<T>(m, lambda.p, xs.p, st);                                                        // l.10
     }
 
@@ -735,11 +737,15 @@ class Engine : public EngineBase {
         MG_CK(cudaEventRecord(f0, st));
         MG_CK(cudaMemsetAsync(flags.p, 0, 8 * sizeof(int), st));
         predict(nv, x.p, v.p, x_old.p, w.p, dt, cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], st);  // l.1
+        omega_dev.resize(1);
+        h2d(omega_dev.p, &cfg.omega_relax, 1, st);  // user omega; halved below if backtracking
         MG_CK(cudaMemsetAsync(lambda.p, 0, sizeof(double) * m, st));                                // l.2
+        int32_t iters_run = 0;
         for (int ite = 0; ite < n_iters; ++ite) {                                                    // l.3
             assemble_hot(dt);                                                                        // l.4-6
             dot_parts<T>(m, b0.p, b0.p, parts2.p, L[0]->grid, st);
             finalize_sum(parts2.p, L[0]->grid, bn.p + ite, st);
+            if (cfg.backtrack) backtrack_omega(bn.p, ite, omega_dev.p, cfg.omega_min, st);
             if (ite == 0 && (stale || !have_hier || frame % cfg.setup_interval == 0)) {            // l.7
                 s0 = ev();
                 MG_CK(cudaEventRecord(s0, st));
@@ -753,6 +759,14 @@ class Engine : public EngineBase {
                 assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, L[0]->vl, L[0]->val.p,
                             L[0]->dinv.p, st, r0, r1);
             run_iter(ite);  // Eq. 6 refresh, l.8 MGPCG, l.9-11 update
+            iters_run = ite + 1;
+            if (cfg.residual_tol > 0.0) {  // l.12: ||b|| < eps, eps = residual_tol ||b_0|| (reading c21)
+                double b2[2];
+                d2h(b2, bn.p, 1, st);
+                d2h(b2 + 1, bn.p + ite, 1, st);
+                MG_CK(cudaStreamSynchronize(st));
+                if (b2[1] < cfg.residual_tol * cfg.residual_tol * b2[0]) break;
+            }
         }
         velocity(nv, x.p, x_old.p, v.p, dt, st);                                                     // l.17
         f1 = ev();
@@ -768,7 +782,8 @@ class Engine : public EngineBase {
             std::fprintf(stderr, "\n");
         }
         frame++;
-        n_b = n_iters;
+        n_b = iters_run;
+        d2h(&omega_last, omega_dev.p, 1, st);
         float ms = 0;
         MG_CK(cudaEventElapsedTime(&ms, f0, f1));
         ms_frame = ms;
@@ -833,6 +848,7 @@ class Engine : public EngineBase {
         s->row_begin = r0;
         s->row_end = r1;
         s->halo_rows = halo_elems;
+        s->omega_relax = omega_last;
     }
 
     void check_level(int l) {
@@ -970,6 +986,9 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->level0_operator = 1;
     c->smoother = 0;
     c->cheb_lower = 0.25;
+    c->backtrack = 0;
+    c->omega_min = 1e-3;
+    c->residual_tol = 0.0;
     return MGPBD_OK;
 }
 
@@ -992,6 +1011,8 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cfg->level0_operator != 0 && cfg->level0_operator != 1) return fail("level0_operator must be 0 or 1");
     if (cfg->smoother != 0 && cfg->smoother != 1) return fail("smoother must be 0 (omega-Jacobi) or 1 (Chebyshev)");
     if (cfg->smoother_sweeps > 8) return fail("smoother_sweeps must be <= 8");
+    if (cfg->backtrack != 0 && cfg->backtrack != 1) return fail("backtrack must be 0 or 1");
+    if (!(cfg->omega_min > 0.0) || !(cfg->residual_tol >= 0.0)) return fail("bad omega_min / residual_tol");
     if (cfg->smoother == 1 && !(cfg->cheb_lower > 0.0 && cfg->cheb_lower < 1.0)) return fail("cheb_lower must be in (0, 1)");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > 4096 || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||

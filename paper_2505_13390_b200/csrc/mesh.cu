@@ -380,7 +380,7 @@ __global__ void k_predict(int32_t n, double* __restrict__ x, double* __restrict_
 template <class T>
 __global__ void k_update(int32_t n, int kc, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vlist,
                          const T* __restrict__ h, const double* __restrict__ sqrtw, const T* __restrict__ dl,
-                         double omega, double* __restrict__ x) {
+                         const double* __restrict__ omega_p, double* __restrict__ x) {
     int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= n) return;
     double s0 = 0, s1 = 0, s2 = 0;
@@ -391,7 +391,7 @@ __global__ void k_update(int32_t n, int kc, const int64_t* __restrict__ vptr, co
         double d = (double)dl[j];
         s0 += (double)hh[0] * d; s1 += (double)hh[1] * d; s2 += (double)hh[2] * d;
     }
-    double sw = sqrtw[v];
+    const double sw = sqrtw[v], omega = *omega_p;
     x[3 * v] += omega * (sw * s0);
     x[3 * v + 1] += omega * (sw * s1);
     x[3 * v + 2] += omega * (sw * s2);
@@ -512,7 +512,7 @@ void predict(int32_t n, double* x, double* v, double* x_old, const double* w, do
 }
 template <class T>
 void update_positions(int32_t n, int kc, const int64_t* vptr, const int32_t* vlist, const T* h, const double* sqrtw,
-                      const T* dl, double omega, double* x, cudaStream_t s) {
+                      const T* dl, const double* omega, double* x, cudaStream_t s) {
     if (!n) return;
     k_update<T><<<grid1d(n, 128), 128, 0, s>>>(n, kc, vptr, vlist, h, sqrtw, dl, omega, x);
     MG_LAUNCH_CHECK();
@@ -523,6 +523,16 @@ void lambda_add(int32_t m, double* lambda, const T* dl, cudaStream_t s) {
     k_lambda_add<T><<<grid1d(m), 256, 0, s>>>(m, lambda, dl);
     MG_LAUNCH_CHECK();
 }
+// Backtracking relaxation (reading c21): omega /= 2 (floored at omega_min) when the
+// squared residual norm of outer iteration ite exceeds that of ite - 1.  One thread; graph-safe.
+__global__ void k_backtrack(const double* __restrict__ bn2, int ite, double* __restrict__ omega, double omega_min) {
+    if (ite > 0 && bn2[ite] > bn2[ite - 1]) *omega = fmax(0.5 * *omega, omega_min);
+}
+void backtrack_omega(const double* bn2, int ite, double* omega, double omega_min, cudaStream_t s) {
+    k_backtrack<<<1, 1, 0, s>>>(bn2, ite, omega, omega_min);
+    MG_LAUNCH_CHECK();
+}
+
 void velocity(int32_t n, const double* x, const double* x_old, double* v, double dt, cudaStream_t s) {
     if (!n) return;
     k_velocity<<<grid1d(3 * (int64_t)n), 256, 0, s>>>(3 * n, x, x_old, v, dt);
@@ -540,7 +550,7 @@ void sqrt_vec(int32_t n, const double* w, double* out, cudaStream_t s) {
     template void assemble<T>(int, int32_t, const int32_t*, const T*, const double*, double, const int64_t*,  \
                               const int32_t*, int, T*, T*, cudaStream_t, int32_t, int32_t);                  \
     template void update_positions<T>(int32_t, int, const int64_t*, const int32_t*, const T*, const double*,  \
-                                      const T*, double, double*, cudaStream_t);                              \
+                                      const T*, const double*, double*, cudaStream_t);                       \
     template void lambda_add<T>(int32_t, double*, const T*, cudaStream_t);
 MG_INST(float)
 MG_INST(double)

@@ -33,9 +33,11 @@ void predict(int32_t n, double* x, double* v, double* x_old, const double* w, do
              double gx, double gy, double gz, cudaStream_t s);
 template <class T>
 void update_positions(int32_t n, int kc, const int64_t* vptr, const int32_t* vlist, const T* h,
-                      const double* sqrtw, const T* dl, double omega, double* x, cudaStream_t s);
+                      const double* sqrtw, const T* dl, const double* omega, double* x, cudaStream_t s);
 template <class T>
 void lambda_add(int32_t m, double* lambda, const T* dl, cudaStream_t s);
+// omega *= 1/2 (>= omega_min) if ||b_ite||^2 > ||b_{ite-1}||^2 (device scalars; reading c21)
+void backtrack_omega(const double* bn2, int ite, double* omega, double omega_min, cudaStream_t s);
 void velocity(int32_t n, const double* x, const double* x_old, double* v, double dt, cudaStream_t s);
 void sqrt_vec(int32_t n, const double* w, double* out, cudaStream_t s);
 

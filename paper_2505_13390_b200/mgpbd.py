@@ -48,7 +48,8 @@ class Config(C.Structure):
                 ("device", C.c_int32), ("stream", C.c_void_p), ("max_dense_coarse", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32),
                 ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32),
-                ("smoother", C.c_int32), ("cheb_lower", C.c_double)]
+                ("smoother", C.c_int32), ("cheb_lower", C.c_double), ("backtrack", C.c_int32),
+                ("omega_min", C.c_double), ("residual_tol", C.c_double)]
 
 
 class Stats(C.Structure):
@@ -59,7 +60,7 @@ class Stats(C.Structure):
                 ("l0_pass_bytes", C.c_double), ("ms_setup", C.c_double), ("ms_frame", C.c_double),
                 ("kernel_launches", C.c_int64), ("indefinite_events", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
-                ("halo_rows", C.c_int64)]
+                ("halo_rows", C.c_int64), ("omega_relax", C.c_double)]
 
 
 _lib = None
