@@ -223,7 +223,9 @@ class Engine : public EngineBase {
         MG_CK(cudaMemsetAsync(mf_u.p, 0, sizeof(T) * 4 * (size_t)nv, st));
         mf.hv = mf_hv.p; mf.at = mf_at.p; mf.u = mf_u.p;
         mf.dinv = L[0]->dinv.p;
-        mf.grid = mf_grid(r1 - r0);
+        mf.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
+        mf.grid = mf.tma ? mf_grid_tma(r0, r1, (int)sizeof(T), kc) : mf_grid(r1 - r0);
+
     }
     int l0_nparts() const { return mf_on() ? mf.grid : L[0]->hot().nparts; }
 

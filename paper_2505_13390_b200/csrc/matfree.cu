@@ -1,5 +1,6 @@
 // Matrix-free level-0 operator, see matfree.cuh.
 #include <algorithm>
+#include <vector>
 
 #include "matfree.cuh"
 #include "record.cuh"
@@ -140,6 +141,152 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
     }
 }
 
+// ---------------------------------------------------------------------------------------------
+// TMA-pipelined row kernel: persistent CTAs stream 256-row tiles of the constraint records (vertex
+// ids, h) and per-row operands into shared memory with 1-D bulk copies (cp.async.bulk, completion on
+// an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
+constexpr int MF_R = 256;       // rows per tile (= threads per CTA)
+constexpr int MF_STAGES = 3;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <class T, int KC>
+struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 256)
+    static constexpr uint32_t H = 0;
+    static constexpr uint32_t V = H + MF_R * KC * 3 * sizeof(T);
+    static constexpr uint32_t X = V + MF_R * KC * sizeof(int32_t);
+    static constexpr uint32_t AT = X + MF_R * sizeof(T);
+    static constexpr uint32_t D = AT + MF_R * sizeof(T);
+    static constexpr uint32_t B = D + MF_R * sizeof(T);
+    static constexpr uint32_t AUX = B + MF_R * sizeof(T);
+    static constexpr uint32_t XP = AUX + MF_R * sizeof(T);
+    static constexpr uint32_t BYTES = XP + MF_R * sizeof(T);
+};
+
+template <class T, int KC, int MODE>
+__global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1, int32_t tbase, int32_t ntiles,
+                                                      const int32_t* __restrict__ verts, const T* __restrict__ h,
+                                                      const V4<T>* __restrict__ u, const T* __restrict__ at,
+                                                      const T* __restrict__ dinv, const T* __restrict__ x,
+                                                      const T* __restrict__ b, T* __restrict__ y,
+                                                      const T* __restrict__ aux, double omega, double alpha,
+                                                      const T* __restrict__ xprev, double* __restrict__ parts,
+                                                      double* __restrict__ parts2) {
+    using LY = TileLayout<T, KC>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[MF_STAGES];
+    constexpr bool ND = MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER;
+    constexpr bool NB = MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P;
+    constexpr bool NA = MODE == PASS_JACOBI_DOT || MODE == PASS_RESID_P;
+    const bool NP = (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) && alpha != 0.0 && xprev != nullptr;
+    const int t = threadIdx.x;
+    if (t == 0) {
+        for (int k = 0; k < MF_STAGES; ++k) mbar_init(&bars[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // tile j of this CTA = blockIdx.x + j * gridDim.x; rows [tbase + tile*R, +R) clipped to row1
+    auto issue = [&](int j) {
+        const int tile = blockIdx.x + j * gridDim.x;
+        unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
+        const int32_t i0 = tbase + tile * MF_R;
+        const int32_t rows = min(MF_R, row1 - i0);
+        auto rnd = [](uint32_t by) { return (by + 15u) & ~15u; };
+        const uint32_t bh = rnd(rows * KC * 3 * sizeof(T)), bv = rnd(rows * KC * sizeof(int32_t)),
+                       bs = rnd(rows * sizeof(T));
+        uint32_t tot = bh + bv + 2 * bs + (ND ? bs : 0) + (NB ? bs : 0) + (NA ? bs : 0) + (NP ? bs : 0);
+        uint64_t* bar = &bars[j % MF_STAGES];
+        mbar_expect_tx(bar, tot);
+        bulk_g2s(st + LY::H, h + (int64_t)i0 * KC * 3, bh, bar);
+        bulk_g2s(st + LY::V, verts + (int64_t)i0 * KC, bv, bar);
+        bulk_g2s(st + LY::X, x + i0, bs, bar);
+        bulk_g2s(st + LY::AT, at + i0, bs, bar);
+        if (ND) bulk_g2s(st + LY::D, dinv + i0, bs, bar);
+        if (NB) bulk_g2s(st + LY::B, b + i0, bs, bar);
+        if (NA) bulk_g2s(st + LY::AUX, aux + i0, bs, bar);
+        if (NP) bulk_g2s(st + LY::XP, xprev + i0, bs, bar);
+    };
+    const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (t == 0)
+        for (int j = 0; j < MF_STAGES && j < my_tiles; ++j) issue(j);
+    double acc1 = 0.0, acc2 = 0.0;
+    for (int j = 0; j < my_tiles; ++j) {
+        mbar_wait(&bars[j % MF_STAGES], (uint32_t)((j / MF_STAGES) & 1));
+        const unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
+        const int32_t i = tbase + (blockIdx.x + j * gridDim.x) * MF_R + t;
+        if (i >= row0 && i < row1) {
+            int vi[KC];
+            T hi[KC][3];
+            {
+                const int32_t* sv = reinterpret_cast<const int32_t*>(st + LY::V) + t * KC;
+#pragma unroll
+                for (int k = 0; k < KC; ++k) vi[k] = sv[k];
+                load_record<T, KC>(reinterpret_cast<const T*>(st + LY::H) + t * KC * 3, hi);
+            }
+            const T xi = reinterpret_cast<const T*>(st + LY::X)[t];
+            T acc = reinterpret_cast<const T*>(st + LY::AT)[t] * xi;
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const V4<T> uu = u[vi[k]];
+                acc += hi[k][0] * uu.x + hi[k][1] * uu.y + hi[k][2] * uu.z;
+            }
+            const double s = (double)acc;
+            const double di = ND ? (double)reinterpret_cast<const T*>(st + LY::D)[t] : 0.0;
+            const double bi = NB ? (double)reinterpret_cast<const T*>(st + LY::B)[t] : 0.0;
+            const double ai = NA ? (double)reinterpret_cast<const T*>(st + LY::AUX)[t] : 0.0;
+            if (MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT) {
+                double yd = (double)xi + omega * di * (bi - s);
+                if (alpha != 0.0)
+                    yd += alpha * ((double)xi - (NP ? (double)reinterpret_cast<const T*>(st + LY::XP)[t] : 0.0));
+                const T yi = (T)yd;
+                y[i] = yi;
+                if (MODE == PASS_JACOBI_DOT) { acc1 += ai * (double)yi; acc2 += ai * ai; }
+            } else if (MODE == PASS_RESID_P) {
+                y[i] = (T)(ai * (bi - s));
+            } else if (MODE == PASS_SPMV_DOT) {
+                const T yi = (T)s;
+                y[i] = yi;
+                acc1 += (double)xi * (double)yi;
+            } else if (MODE == PASS_POWER) {
+                const T yi = (T)(di * s);
+                y[i] = yi;
+                acc1 += (double)yi * (double)yi;
+            }
+        }
+        __syncthreads();  // every thread is done with this stage: refill it
+        if (t == 0 && j + MF_STAGES < my_tiles) issue(j + MF_STAGES);
+    }
+    if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
+        __shared__ double sh[32];
+        const double t1 = block_sum<MF_R>(acc1, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t1;
+        if (MODE == PASS_JACOBI_DOT) {
+            const double t2 = block_sum<MF_R>(acc2, sh);
+            if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
+        }
+    }
+}
+
 template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
                 double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
@@ -152,6 +299,34 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         MG_LAUNCH_CHECK();
     }
     const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
+    if (A.tma) {
+        const int32_t tbase = A.row0 & ~3;  // 16-B aligned vector offsets
+        const int32_t ntiles = (A.row1 - tbase + MF_R - 1) / MF_R;
+        const size_t smem = (size_t)MF_STAGES * TileLayout<T, KC>::BYTES;
+#define MG_MFT(M)                                                                                               \
+    {                                                                                                           \
+        static bool attr = false;                                                                               \
+        if (!attr) {                                                                                            \
+            MG_CK(cudaFuncSetAttribute(k_mf_rows_tma<T, KC, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
+                                       (int)smem));                                                             \
+            attr = true;                                                                                        \
+        }                                                                                                       \
+        k_mf_rows_tma<T, KC, M><<<A.grid, MF_R, smem, s>>>(A.row0, A.row1, tbase, ntiles, A.verts, A.h, u, A.at, \
+                                                            A.dinv, x, b, y, aux, omega, alpha, xprev, parts,   \
+                                                            parts2);                                            \
+    }
+        switch (mode) {
+            case PASS_JACOBI: MG_MFT(PASS_JACOBI); break;
+            case PASS_JACOBI_DOT: MG_MFT(PASS_JACOBI_DOT); break;
+            case PASS_RESID_P: MG_MFT(PASS_RESID_P); break;
+            case PASS_SPMV_DOT: MG_MFT(PASS_SPMV_DOT); break;
+            case PASS_POWER: MG_MFT(PASS_POWER); break;
+            default: throw Error(-1, "mf_pass: bad mode");
+        }
+#undef MG_MFT
+        MG_LAUNCH_CHECK();
+        return;
+    }
 #define MG_MF(M)                                                                                            \
     k_mf_rows<T, KC, M><<<A.grid, MF_BS, 0, s>>>(A.row0, A.row1, A.verts, A.h, u, A.at, A.dinv, x, b, y, aux, \
                                                   omega, alpha, xprev, parts, parts2)
@@ -171,6 +346,17 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 
 int mf_grid(int32_t rows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)rows + MF_BS - 1) / MF_BS, 148 * 8));
+}
+
+int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc) {
+    const int32_t tbase = row0 & ~3;
+    const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + MF_R - 1) / MF_R);
+    const size_t stage = (size_t)MF_R * ((size_t)kc * 3 * tsize + (size_t)kc * 4 + 6 * (size_t)tsize);
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (MF_STAGES * stage + 1024)));
+    int dev = 0, sms = 148;
+    MG_CK(cudaGetDevice(&dev));
+    MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return (int)std::min<int64_t>(ntiles, (int64_t)sms * per_sm);
 }
 
 template <class T>

@@ -8,6 +8,8 @@
 // followed by the same per-row epilogues as the CSR passes (PASS_* in solve.cuh).  The assembled CSR
 // is still built every outer iteration: the Galerkin refresh (Eq. 6) and the smoother diagonal use it.
 #pragma once
+#include <vector>
+
 #include "common.cuh"
 
 namespace mgpbd {
@@ -29,9 +31,13 @@ struct MatFree {
     T* u = nullptr;                 // 4 values per vertex (xyz, pad)
     const T* dinv = nullptr;        // 1 / A_ii from the assembly
     int grid = 1;                   // CTAs of the row kernel = number of dot partials
+    bool tma = false;               // TMA-pipelined row kernel (persistent CTAs, bulk copies)
 };
 
 int mf_grid(int32_t rows);
+// persistent grid of the TMA row kernel for rows [row0, row1) (T of tsize bytes, kc vertices)
+int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc);
+
 
 // Per outer iteration, after the constraint evaluation: hv (vertex-major h), at (all rows) and the
 // diagonal inverse dinv of the owned rows.
