@@ -164,6 +164,13 @@ class Engine : public EngineBase {
     // matrix-free level-0 operator (cfg.level0_operator == 1, matfree.cuh)
     MatFree<T> mf;
     DBuf<T> mf_hv, mf_at, mf_u;
+    // fp64 matrix-free operator for the setup's level-0 power method (reading c18: setup in fp64)
+    MatFree<double> mf64;
+    DBuf<double> mf64_hv, mf64_at, mf64_u;
+    bool mf64_ok = false;
+    // Jones-Plassmann colouring of A_0's pattern (reading c5): depends only on the fixed pattern
+    DBuf<int32_t> colours0;
+    bool colours_cached = false;
     bool mf_ready = false;      // h is current and describes level 0 (false after debug_setup_from)
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
@@ -223,6 +230,18 @@ class Engine : public EngineBase {
         MG_CK(cudaMemsetAsync(mf_u.p, 0, sizeof(T) * 4 * (size_t)nv, st));
         mf.hv = mf_hv.p; mf.at = mf_at.p; mf.u = mf_u.p;
         mf.dinv = L[0]->dinv.p;
+        if (!dist) {  // fp64 twin on the same geometry (h64 / dinv64 of the setup assembly)
+            mf64 = MatFree<double>();
+            mf64.kc = kc; mf64.m = m; mf64.row0 = 0; mf64.row1 = m; mf64.v0 = 0; mf64.v1 = nv;
+            mf64.verts = verts.p; mf64.vptr = vptr.p; mf64.vlist = vlist.p;
+            mf64.ninc = hp[nv]; mf64.e0 = 0; mf64.e1 = hp[nv];
+            mf64_hv.resize(3 * (size_t)mf64.ninc); mf64_at.resize(m); mf64_u.resize(4 * (size_t)nv);
+            MG_CK(cudaMemsetAsync(mf64_u.p, 0, sizeof(double) * 4 * (size_t)nv, st));
+            mf64.hv = mf64_hv.p; mf64.at = mf64_at.p; mf64.u = mf64_u.p;
+            mf64.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
+            mf64.grid = mf64.tma ? mf_grid_tma(0, m, 8, kc) : mf_grid(m);
+            mf64_ok = true;
+        }
         mf.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
         mf.grid = mf.tma ? mf_grid_tma(r0, r1, (int)sizeof(T), kc) : mf_grid(r1 - r0);
 
@@ -446,10 +465,13 @@ class Engine : public EngineBase {
             trace("aggregate", l);
             if ((double)na > cfg.stall_ratio * (double)a.n) break;
             if (l == 0) {
-                DBuf<int32_t> col_;
-                col_.resize(a.n);
-                ncolours = colour(a.n, a.rowptr, a.col, cfg.seed, col_.p, st);
-                trace("colour", l);
+                if (!colours_cached) {  // pattern fixed for the context lifetime: colour once
+                    colours0.resize(a.n);
+                    ncolours = colour(a.n, a.rowptr, a.col, cfg.seed, colours0.p, st);
+                    colours_cached = true;
+                    trace("colour", l);
+                }
+                const DBuf<int32_t>& col_ = colours0;
                 B.resize(a.n);
                 gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed, B.p, st);
                 d2d(B0.p, B.p, a.n, st);
@@ -477,7 +499,22 @@ class Engine : public EngineBase {
             galerkin_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, a2.P64.p, na, c.rowptr, c.nnz,
                                      a2.tval64.p, c.val64.p, c.dinv64.p, st);
             trace("galerkin_numeric", l);
-            double lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
+            double lam;
+            if (l == 0 && mf64_ok && mf_ready && h64.n) {
+                // level 0 through the fp64 matrix-free operator (2 gathers instead of the 1.4 GB CSR)
+                mf64.h = h64.p;
+                mf64.dinv = a2.dinv64.p;
+                mf_refresh<double>(mf64, alpha.p, last_dt, a2.dinv64.p, st);
+                lam = power_method_op(
+                    m, a2.grid,
+                    [&](const double* xv, double* yv, double* pp) {
+                        mf_pass<double>(PASS_POWER, mf64, xv, nullptr, yv, nullptr, 0.0, pp, nullptr, st);
+                        return mf64.grid;
+                    },
+                    cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
+            } else {
+                lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
+            }
             set_smoother(a2, lam);
             trace("power", l);
             B.swap(Bn);

@@ -615,21 +615,32 @@ void diag_inv(int32_t n, const int64_t* rowptr, const T* val, T* dinv, cudaStrea
     MG_LAUNCH_CHECK();
 }
 
-double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
-                    double* parts, double* ss, cudaStream_t s) {
-    const int32_t n = A.n;
+double power_method_op(int32_t n, int dot_grid, const std::function<int(const double*, double*, double*)>& apply,
+                       int32_t iters, uint64_t seed, int level, double* v, double* w, double* parts, double* ss,
+                       cudaStream_t s) {
     k_power_init<<<g1(n), 256, 0, s>>>(n, hkey_base(seed, 4, level), v);
     MG_LAUNCH_CHECK();
-    dot_parts<double>(n, v, v, parts, A.grid, s);
-    finalize_sum(parts, A.grid, ss, s);
+    dot_parts<double>(n, v, v, parts, dot_grid, s);
+    finalize_sum(parts, dot_grid, ss, s);
     scale_by_inv_sqrt<double>(n, v, v, ss, s);
     for (int it = 0; it < iters; ++it) {
-        csr_pass<double>(PASS_POWER, A, v, nullptr, w, nullptr, 0.0, parts, nullptr, s);
-        finalize_sum(parts, A.nparts, ss, s);
+        const int np = apply(v, w, parts);
+        finalize_sum(parts, np, ss, s);
         scale_by_inv_sqrt<double>(n, w, v, ss, s);
     }
     double lam2 = read_scalar(ss, s);
     return iters > 0 ? sqrt(lam2) : 0.0;
+}
+
+double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
+                    double* parts, double* ss, cudaStream_t s) {
+    return power_method_op(
+        A.n, A.grid,
+        [&](const double* x, double* y, double* pp) {
+            csr_pass<double>(PASS_POWER, A, x, nullptr, y, nullptr, 0.0, pp, nullptr, s);
+            return A.nparts;
+        },
+        iters, seed, level, v, w, parts, ss, s);
 }
 
 #define MG_INST(T)                                                                                             \

@@ -1,6 +1,8 @@
 // AMG setup kernels and the Galerkin product (a7).
 // Setup always runs on fp64 values; the numeric Galerkin product is templated on the hot precision.
 #pragma once
+#include <functional>
+
 #include "common.cuh"
 #include "solve.cuh"
 
@@ -54,6 +56,11 @@ template <class T>
 void diag_inv(int32_t n, const int64_t* rowptr, const T* val, T* dinv, cudaStream_t s);
 
 // lambda_max(D^-1 A) by the power method (reading c9); returns lambda (host sync).
+// Same iteration with the operator given as apply(v, w, parts): w = D^-1 A v and the partials of
+// |w|^2; returns the number of partials written.  (Level 0 uses the matrix-free operator.)
+double power_method_op(int32_t n, int dot_grid, const std::function<int(const double*, double*, double*)>& apply,
+                       int32_t iters, uint64_t seed, int level, double* v, double* w, double* parts, double* ss,
+                       cudaStream_t s);
 double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
                     double* parts, double* ss, cudaStream_t s);
 
