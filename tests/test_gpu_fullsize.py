@@ -1,0 +1,90 @@
+"""Parity at BASELINE.json's full sizes in the launch configuration bench.py times (fp32 storage,
+matrix-free level 0 with the TMA row kernel, CUDA graphs, persistent coarse kernel): the oracle cannot
+run a 1.7M-tet frame in test time, so it checks what it can compute one by one — the whole CSR pattern,
+the assembled A_0 on sampled rows and ||b_0|| at the predicted state (Alg. 1 l.1-6), the setup on the
+oracle's own A_0 bits (aggregates and level-1 pattern bit-exact, level-1 values) — plus properties
+that hold at any size (bitwise determinism, graph replay == eager, pinned vertices fixed)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2505_13390_b200 import mgpbd, scenes
+
+pytestmark = pytest.mark.gpu
+
+FULL = ["cloth256", "bar50k", "block1.67M", "cloth2048"]
+
+
+def predicted(sc):
+    """Alg. 1 l.1 (semi-implicit Euler): v += dt g for w > 0, x~ = x + dt v."""
+    v = sc.vel.copy()
+    free = sc.inv_mass > 0
+    v[free] += sc.dt * np.array([0.0, -9.8, 0.0])
+    return sc.pos + sc.dt * v
+
+
+def oracle_state(sc):
+    xt = predicted(sc)
+    if sc.kind == 2:
+        C, g = O.eval_distance(sc.verts, xt, O.rest_distance(sc.verts, sc.rest_pos))
+    else:
+        C, g = O.eval_arap(sc.verts, xt, O.rest_arap(sc.verts, sc.rest_pos)[0])
+    return C, g, sc.compliance / sc.dt ** 2
+
+
+@pytest.fixture(scope="module", params=FULL)
+def full(request):
+    sc = scenes.make(request.param)
+    rowptr, col = O.pattern(sc.verts, sc.n_verts)
+    C, g, at = oracle_state(sc)
+    return sc, rowptr, col, C, g, at
+
+
+def test_fullsize_pattern_assembly_rows_and_rhs(full):
+    sc, ro, co, C, g, at = full
+    ctx = mgpbd.Context.from_scene(sc, precision=1)          # bench configuration
+    ctx.step(sc.dt, 1)                                       # one outer iteration at the predicted state
+    r, c, v = ctx.level(0)
+    assert np.array_equal(r, ro) and np.array_equal(c, co)   # whole pattern, bit-exact
+    rows = np.sort(np.random.default_rng(0).choice(sc.n_cons, size=min(4000, sc.n_cons), replace=False))
+    vo = O.assemble_rows(rows, sc.verts, sc.inv_mass, g, at, ro, co)
+    for i in rows:
+        a, e = ro[i], ro[i + 1]
+        scale = np.abs(vo[a:e]).max()
+        assert np.abs(v[a:e] - vo[a:e]).max() <= 2e-5 * scale, i      # fp32 h, fp32 products
+    bn = ctx.stats().b_norm[0]
+    assert abs(bn - np.linalg.norm(C)) <= 1e-5 * np.linalg.norm(C)    # b = -C - at*0
+    ctx.close()
+
+
+def test_fullsize_setup_on_oracle_bits(full):
+    sc, ro, co, C, g, at = full
+    v0 = O.assemble(sc.verts, sc.inv_mass, g, at, ro, co)
+    ctx = mgpbd.Context.from_scene(sc, precision=1)
+    ctx.debug_setup_from(v0)
+    strong = O.soc(ro, co, v0, 0.1)
+    agg, na = O.aggregate(ro, co, v0, strong)
+    assert np.array_equal(ctx.aggregates(0), agg)
+    P = ctx.prolongator(0)
+    r1, c1, v1 = ctx.level(1)
+    ro1, co1, vo1 = O.galerkin(ro, co, v0, agg, P, na)       # P^T A P with the device's P
+    assert np.array_equal(r1, ro1) and np.array_equal(c1, co1)
+    assert np.abs(v1 - vo1).max() <= 1e-5 * np.abs(vo1).max()   # fp32 hot refresh of A_1
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", ["block1.67M"])
+def test_fullsize_deterministic_and_graph_replay(name, monkeypatch):
+    sc = scenes.make(name)
+    outs = []
+    for env in (None, None, "1"):
+        if env:
+            monkeypatch.setenv("MGPBD_NO_GRAPH", env)
+        ctx = mgpbd.Context.from_scene(sc, precision=1)
+        ctx.step(sc.dt, sc.n_iters)
+        outs.append((ctx.positions(), ctx.lambdas()))
+        ctx.close()
+    for x, lam in outs[1:]:
+        assert np.array_equal(x, outs[0][0]) and np.array_equal(lam, outs[0][1])
+    pinned = sc.inv_mass == 0
+    assert np.array_equal(outs[0][0][pinned], sc.pos[pinned])
