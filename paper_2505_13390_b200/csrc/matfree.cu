@@ -67,12 +67,30 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
         const int64_t v = base + sub;
         T a0 = (T)0, a1 = (T)0, a2 = (T)0;
         if (v < v1) {
-            const int64_t e1 = vptr[v + 1];
-            for (int64_t e = vptr[v] + sl; e < e1; e += G) {
-                const T xj = x[vlist[e] / KC];
-                a0 += hx[e] * xj;
-                a1 += hy[e] * xj;
-                a2 += hz[e] * xj;
+            // chunks of UN incidences per lane: all index/h loads, then all x gathers, then the FMAs,
+            // so a chunk costs two dependent round trips instead of two per incidence
+            constexpr int UN = 4;
+            const int64_t e0 = vptr[v], e1 = vptr[v + 1];
+            for (int64_t eb = e0 + sl; eb < e1; eb += G * UN) {
+                int32_t cj[UN];
+                T px[UN], py[UN], pz[UN], xv[UN];
+#pragma unroll
+                for (int q = 0; q < UN; ++q) {
+                    const int64_t e = eb + q * G;
+                    const bool in = e < e1;
+                    cj[q] = in ? vlist[e] / KC : -1;
+                    px[q] = in ? hx[e] : (T)0;
+                    py[q] = in ? hy[e] : (T)0;
+                    pz[q] = in ? hz[e] : (T)0;
+                }
+#pragma unroll
+                for (int q = 0; q < UN; ++q) xv[q] = cj[q] >= 0 ? x[cj[q]] : (T)0;
+#pragma unroll
+                for (int q = 0; q < UN; ++q) {
+                    a0 += px[q] * xv[q];
+                    a1 += py[q] * xv[q];
+                    a2 += pz[q] * xv[q];
+                }
             }
         }
         a0 = group_sum_t<G>(a0);
