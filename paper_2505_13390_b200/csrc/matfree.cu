@@ -55,6 +55,9 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
                                                       const int64_t* __restrict__ vptr,
                                                       const int32_t* __restrict__ vlist, const T* __restrict__ hv,
                                                       const T* __restrict__ x, V4<T>* __restrict__ u) {
+    // programmatic dependent launch: the row kernel may start streaming its static operands now; it
+    // waits (griddepcontrol.wait) for this grid's u before gathering it
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr int PER_WARP = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -247,6 +250,9 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
     const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
     if (t == 0)
         for (int j = 0; j < MF_STAGES && j < my_tiles; ++j) issue(j);
+    // everything above reads only data of earlier kernels; u comes from the vertex gather launched
+    // just before this grid (programmatic dependent launch): wait for it before the first gather
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     double acc1 = 0.0, acc2 = 0.0;
     for (int j = 0; j < my_tiles; ++j) {
         mbar_wait(&bars[j % MF_STAGES], (uint32_t)((j / MF_STAGES) & 1));
@@ -329,9 +335,19 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
                                        (int)smem));                                                             \
             attr = true;                                                                                        \
         }                                                                                                       \
-        k_mf_rows_tma<T, KC, M><<<A.grid, MF_R, smem, s>>>(A.row0, A.row1, tbase, ntiles, A.verts, A.h, u, A.at, \
-                                                            A.dinv, x, b, y, aux, omega, alpha, xprev, parts,   \
-                                                            parts2);                                            \
+        cudaLaunchConfig_t lc = {};                                                                             \
+        lc.gridDim = dim3(A.grid);                                                                              \
+        lc.blockDim = dim3(MF_R);                                                                               \
+        lc.dynamicSmemBytes = smem;                                                                             \
+        lc.stream = s;                                                                                          \
+        cudaLaunchAttribute la[1];                                                                              \
+        la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                          \
+        la[0].val.programmaticStreamSerializationAllowed = 1;                                                   \
+        lc.attrs = la;                                                                                          \
+        lc.numAttrs = 1;                                                                                        \
+        MG_CK(cudaLaunchKernelEx(&lc, k_mf_rows_tma<T, KC, M>, A.row0, A.row1, tbase, ntiles, A.verts, A.h, u,   \
+                                 (const T*)A.at, (const T*)A.dinv, x, b, y, aux, omega, alpha, xprev, parts,    \
+                                 parts2));                                                                      \
     }
         switch (mode) {
             case PASS_JACOBI: MG_MFT(PASS_JACOBI); break;
