@@ -1,0 +1,352 @@
+// Shared-memory-resident persistent coarse V-cycle, see coarse_res.cuh.
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "coarse_res.cuh"
+#include "comm.cuh"
+#include "tma.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mgpbd {
+
+namespace {
+
+constexpr int RB = 1024;  // threads per CTA (one CTA per SM)
+constexpr int RSVL = 8;   // lanes per row
+constexpr int RSCH = 5;   // nonzeros per lane per chunk
+constexpr int RRPW = 32 / RSVL;
+constexpr int RCHUNK = RSVL * RSCH;
+constexpr int RWARPS = RB / 32;
+
+// one CTA's slices of one level in shared memory (offsets point at element r0 / e0 / a0 / m0)
+template <class T>
+struct Slice {
+    const unsigned char* sm;
+    ResLevel d;
+    __device__ int64_t rp(int64_t i) const { return reinterpret_cast<const int64_t*>(sm + d.o_rp)[i - d.r0]; }
+    __device__ int32_t col(int64_t e) const { return reinterpret_cast<const int32_t*>(sm + d.o_col)[e - d.e0]; }
+    __device__ T val(int64_t e) const { return reinterpret_cast<const T*>(sm + d.o_val)[e - d.e0]; }
+    __device__ T dinv(int64_t i) const { return reinterpret_cast<const T*>(sm + d.o_dinv)[i - d.r0]; }
+    __device__ T P(int64_t i) const { return reinterpret_cast<const T*>(sm + d.o_P)[i - d.r0]; }
+    __device__ int32_t agg(int64_t i) const { return reinterpret_cast<const int32_t*>(sm + d.o_agg)[i - d.r0]; }
+    __device__ int64_t mp(int64_t a) const { return reinterpret_cast<const int64_t*>(sm + d.o_mp)[a - d.a0]; }
+    __device__ int32_t ml(int64_t e) const { return reinterpret_cast<const int32_t*>(sm + d.o_ml)[e - d.m0]; }
+    __device__ const double* dense_rows() const { return reinterpret_cast<const double*>(sm + d.o_val); }
+};
+
+struct Lanes {
+    int lane, sub, sl, warp;
+    __device__ Lanes() {
+        lane = threadIdx.x & 31;
+        sub = lane / RSVL;
+        sl = lane % RSVL;
+        warp = threadIdx.x >> 5;
+    }
+};
+
+// sum_k A_ik x(col_k) for row i (owned by this CTA; matrix from shared memory); warp-wide butterfly
+template <class T, class XF>
+__device__ __forceinline__ double row_sum(const Lanes& w, const Slice<T>& S, bool valid, int64_t i, XF xf) {
+    const int64_t a = valid ? S.rp(i) : 0, e = valid ? S.rp(i + 1) : 0;
+    const int maxlen = __reduce_max_sync(0xffffffffu, (int)(e - a));
+    T part = (T)0;
+    for (int off = 0; off < maxlen; off += RCHUNK) {
+        int32_t c[RSCH];
+        T v[RSCH], xv[RSCH];
+#pragma unroll
+        for (int q = 0; q < RSCH; ++q) {
+            const int64_t k = a + off + q * RSVL + w.sl;
+            const bool in = k < e;
+            c[q] = in ? S.col(k) : -1;
+            v[q] = in ? S.val(k) : (T)0;
+        }
+#pragma unroll
+        for (int q = 0; q < RSCH; ++q) xv[q] = c[q] >= 0 ? xf(c[q]) : (T)0;
+#pragma unroll
+        for (int q = 0; q < RSCH; ++q) part += v[q] * xv[q];
+    }
+    return (double)group_sum_t<RSVL>(part);
+}
+
+// smoother step over this CTA's rows: y = x + alpha (x - xprev) + omega D^-1 (b - A x)
+template <class T, class XF, class XPF>
+__device__ __forceinline__ void sweep(const Lanes& w, const CoarseLevel<T>& L, const Slice<T>& S, XF xf, XPF xpf,
+                                      double omega, double alpha, T* __restrict__ out) {
+    for (int64_t base = S.d.r0 + w.warp * RRPW; base < S.d.r1; base += RWARPS * RRPW) {  // warp-uniform
+        const int64_t i = base + w.sub;
+        const bool valid = i < S.d.r1;
+        const double s = row_sum(w, S, valid, i, xf);
+        if (valid && w.sl == 0) {
+            const double xi = (double)xf((int32_t)i);
+            double y = xi + omega * (double)S.dinv(i) * ((double)L.b[i] - s);
+            if (alpha != 0.0) y += alpha * (xi - (double)xpf((int32_t)i));
+            out[i] = (T)y;
+        }
+    }
+}
+
+template <class T>
+__device__ __forceinline__ void resid(const Lanes& w, const CoarseLevel<T>& L, const Slice<T>& S,
+                                      const T* __restrict__ x) {
+    for (int64_t base = S.d.r0 + w.warp * RRPW; base < S.d.r1; base += RWARPS * RRPW) {
+        const int64_t i = base + w.sub;
+        const bool valid = i < S.d.r1;
+        const double s = row_sum(w, S, valid, i, [&](int32_t j) { return x[j]; });
+        if (valid && w.sl == 0) L.t[i] = (T)((double)S.P(i) * ((double)L.b[i] - s));
+    }
+}
+
+template <class T>
+__device__ __forceinline__ void restrict_t(const Lanes& w, const CoarseLevel<T>& L, const Slice<T>& S,
+                                           T* __restrict__ bnext) {
+    for (int64_t base = S.d.a0 + w.warp * RRPW; base < S.d.a1; base += RWARPS * RRPW) {
+        const int64_t a = base + w.sub;
+        double s = 0.0;
+        if (a < S.d.a1) {
+            const int64_t m1 = S.mp(a + 1);
+            for (int64_t e = S.mp(a) + w.sl; e < m1; e += RSVL) s += (double)L.t[S.ml(e)];
+        }
+        s = group_sum<RSVL>(s);
+        if (a < S.d.a1 && w.sl == 0) bnext[a] = (T)s;
+    }
+}
+
+template <class T>
+__device__ __forceinline__ void dense_solve(const Lanes& w, int32_t n, const Slice<T>& S, const T* __restrict__ b,
+                                            T* __restrict__ x) {
+    const double* A = S.dense_rows();
+    for (int64_t i = S.d.r0 + w.warp; i < S.d.r1; i += RWARPS) {
+        double s = 0.0;
+        for (int32_t j = w.lane; j < n; j += 32) s += A[(i - S.d.r0) * n + j] * (double)b[j];
+        s = group_sum<32>(s);
+        if (w.lane == 0) x[i] = (T)s;
+    }
+}
+
+template <class T>
+__global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_constant__ CoarseCycle<T> c,
+                                                             const __grid_constant__ ResPlan plan) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bar;
+    __shared__ CoarseCycle<T> sc;
+    __shared__ ResLevel slv[16];  // this CTA's slice descriptors (read after every barrier)
+    const Lanes w;
+    const int cta = blockIdx.x;
+    {
+        const int* src = reinterpret_cast<const int*>(&c);
+        int* dst = reinterpret_cast<int*>(&sc);
+        for (int k = threadIdx.x; k < (int)(sizeof(CoarseCycle<T>) / sizeof(int)); k += blockDim.x) dst[k] = src[k];
+        const int* ls = reinterpret_cast<const int*>(plan.lv + (size_t)cta * 16);
+        int* ld = reinterpret_cast<int*>(slv);
+        for (int k = threadIdx.x; k < (int)(16 * sizeof(ResLevel) / sizeof(int)); k += blockDim.x) ld[k] = ls[k];
+    }
+    if (threadIdx.x == 0) {  // this CTA's slices of every level -> shared memory
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&bar, plan.txbytes[cta]);
+        const ResCopy* cp = plan.copies + (size_t)cta * RES_MAXC;
+        for (int k = 0; k < plan.ncopies[cta]; ++k) bulk_g2s(smem + cp[k].dst, cp[k].src, cp[k].bytes, &bar);
+    }
+    __syncthreads();
+    mbar_wait(&bar, 0);
+    int tix = 0;
+    auto mark = [&]() {
+        if (c.trace && blockIdx.x == 0 && threadIdx.x == 0 && tix < 64) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            c.trace[tix] = t;
+        }
+        ++tix;
+    };
+    mark();
+    const int K = sc.K, nu = sc.nu;
+    auto slice = [&](int k) { return Slice<T>{smem, slv[k]}; };
+    T* cur[16];
+    // ---- down
+    for (int k = 0; k + 1 < K; ++k) {
+        const CoarseLevel<T>& L = sc.L[k];
+        const Slice<T> S = slice(k);
+        const T* __restrict__ b = L.b;
+        const T* __restrict__ d = L.dinv;
+        const double om0 = L.sm_omega[0];
+        auto x1f = [&](int32_t j) { return (T)(om0 * (double)d[j] * (double)b[j]); };
+        auto zero = [&](int32_t) { return (T)0; };
+        T* cu = L.x;
+        T* ot = L.y;
+        if (nu >= 2) {
+            sweep(w, L, S, x1f, zero, L.sm_omega[1], L.sm_alpha[1], L.x);
+            for (int s = 2; s < nu; ++s) {
+                grid.sync(); mark();
+                const T* __restrict__ src = cu;
+                T* __restrict__ prv = ot;
+                if (s == 2) sweep(w, L, S, [&](int32_t j) { return src[j]; }, x1f, L.sm_omega[s], L.sm_alpha[s], ot);
+                else sweep(w, L, S, [&](int32_t j) { return src[j]; }, [&](int32_t i) { return prv[i]; },
+                           L.sm_omega[s], L.sm_alpha[s], ot);
+                T* t = cu; cu = ot; ot = t;
+            }
+        } else {
+            for (int64_t i = S.d.r0 + threadIdx.x; i < S.d.r1; i += blockDim.x) L.x[i] = x1f((int32_t)i);
+        }
+        cur[k] = cu;
+        grid.sync(); mark();
+        resid(w, L, S, cu);
+        grid.sync(); mark();
+        restrict_t(w, L, S, sc.L[k + 1].b);
+        grid.sync(); mark();
+    }
+    // ---- coarsest
+    dense_solve(w, sc.L[K - 1].n, slice(K - 1), sc.L[K - 1].b, sc.L[K - 1].z);
+    // ---- up
+    for (int k = K - 2; k >= 0; --k) {
+        const CoarseLevel<T>& L = sc.L[k];
+        const Slice<T> S = slice(k);
+        T* __restrict__ cu = cur[k];
+        T* ot = cu == L.x ? L.y : L.x;
+        const T* __restrict__ zc = sc.L[k + 1].z;
+        const T* __restrict__ P = L.P;
+        const int32_t* __restrict__ agg = L.agg;
+        const bool mat = L.n >= 32768;
+        auto zero = [&](int32_t) { return (T)0; };
+        grid.sync(); mark();
+        if (mat) {  // materialise x_0 = x + P z_c[agg] over the owned rows (shared-memory P, agg)
+            for (int64_t i = S.d.r0 + threadIdx.x; i < S.d.r1; i += blockDim.x)
+                cu[i] = (T)((double)cu[i] + (double)S.P(i) * (double)zc[S.agg(i)]);
+            grid.sync(); mark();
+        }
+        auto x0f = [&](int32_t j) { return mat ? cu[j] : (T)((double)cu[j] + (double)P[j] * (double)zc[agg[j]]); };
+        T* src = nu == 1 ? L.z : ot;
+        sweep(w, L, S, x0f, zero, L.sm_omega[0], 0.0, src);
+        T* prv = cu;
+        for (int s = 1; s < nu; ++s) {
+            grid.sync(); mark();
+            T* out = s == nu - 1 ? L.z : prv;
+            const T* __restrict__ xs = src;
+            const T* __restrict__ xp = prv;
+            if (s == 1) sweep(w, L, S, [&](int32_t j) { return xs[j]; }, x0f, L.sm_omega[s], L.sm_alpha[s], out);
+            else sweep(w, L, S, [&](int32_t j) { return xs[j]; }, [&](int32_t i) { return xp[i]; }, L.sm_omega[s],
+                       L.sm_alpha[s], out);
+            prv = src;
+            src = out;
+        }
+    }
+}
+
+}  // namespace
+
+template <class T>
+bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vector<ResLevel>& lv,
+                     std::vector<ResCopy>& copies, std::vector<int32_t>& ncopies, std::vector<uint32_t>& tx,
+                     uint32_t& smem, cudaStream_t s) {
+    const int K = c.K;
+    if (K < 2 || K > 16) return false;
+    std::vector<std::vector<int32_t>> rb(K), ab(K);
+    std::vector<std::vector<int64_t>> rp(K), mp(K);
+    for (int k = 0; k < K; ++k) {
+        const CoarseLevel<T>& L = c.L[k];
+        if (k + 1 < K) {
+            rp[k].resize((size_t)L.n + 1);
+            d2h(rp[k].data(), L.rowptr, (size_t)L.n + 1, s);
+            mp[k].resize((size_t)L.n_agg + 1);
+            d2h(mp[k].data(), L.mptr, (size_t)L.n_agg + 1, s);
+        }
+    }
+    MG_CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < K; ++k) {
+        const CoarseLevel<T>& L = c.L[k];
+        if (k + 1 < K) {
+            rb[k] = partition_rows(rp[k].data(), L.n, G);             // rows balanced by nonzeros
+            ab[k] = partition_rows(mp[k].data(), L.n_agg, G);         // aggregates balanced by members
+        } else {
+            rb[k].resize(G + 1);
+            for (int g = 0; g <= G; ++g) rb[k][g] = (int32_t)((int64_t)L.n * g / G);
+        }
+    }
+    lv.assign((size_t)G * 16, ResLevel());
+    copies.assign((size_t)G * RES_MAXC, ResCopy{nullptr, 0, 0});
+    ncopies.assign(G, 0);
+    tx.assign(G, 0);
+    smem = 0;
+    for (int g = 0; g < G; ++g) {
+        uint32_t cursor = 0;
+        int nc = 0;
+        auto add = [&](uint32_t& off, const void* base, int64_t elem_off, size_t esz, size_t count) -> bool {
+            const uintptr_t src = reinterpret_cast<uintptr_t>(base) + (uintptr_t)(elem_off * (int64_t)esz);
+            const uintptr_t al = src & ~(uintptr_t)15;
+            const uint32_t lead = (uint32_t)(src - al);
+            const uint32_t dst = (cursor + 15u) & ~15u;
+            off = dst + lead;
+            const size_t bytes = count * esz;
+            if (bytes == 0) { cursor = dst; return true; }
+            const uint32_t nb = (uint32_t)((lead + bytes + 15) & ~(size_t)15);
+            if (nc >= RES_MAXC) return false;
+            copies[(size_t)g * RES_MAXC + nc++] = ResCopy{reinterpret_cast<const void*>(al), dst, nb};
+            cursor = dst + nb;
+            tx[g] += nb;
+            return true;
+        };
+        for (int k = 0; k < K; ++k) {
+            const CoarseLevel<T>& L = c.L[k];
+            ResLevel& d = lv[(size_t)g * 16 + k];
+            d.r0 = rb[k][g]; d.r1 = rb[k][g + 1];
+            const int64_t rows = d.r1 - d.r0;
+            bool ok = true;
+            if (k + 1 < K) {
+                d.e0 = rp[k][d.r0];
+                const int64_t nnz = rp[k][d.r1] - d.e0;
+                d.a0 = ab[k][g]; d.a1 = ab[k][g + 1];
+                d.m0 = mp[k][d.a0];
+                const int64_t mem = mp[k][d.a1] - d.m0;
+                ok = ok && add(d.o_rp, L.rowptr, d.r0, 8, (size_t)rows + 1);
+                ok = ok && add(d.o_col, L.col, d.e0, 4, (size_t)nnz);
+                ok = ok && add(d.o_val, L.val, d.e0, sizeof(T), (size_t)nnz);
+                ok = ok && add(d.o_dinv, L.dinv, d.r0, sizeof(T), (size_t)rows);
+                ok = ok && add(d.o_P, L.P, d.r0, sizeof(T), (size_t)rows);
+                ok = ok && add(d.o_agg, L.agg, d.r0, 4, (size_t)rows);
+                ok = ok && add(d.o_mp, L.mptr, d.a0, 8, (size_t)(d.a1 - d.a0) + 1);
+                ok = ok && add(d.o_ml, L.mlist, d.m0, 4, (size_t)mem);
+            } else {
+                ok = ok && add(d.o_val, c.Ainv, (int64_t)d.r0 * L.n, 8, (size_t)rows * L.n);
+            }
+            if (!ok) return false;
+        }
+        ncopies[g] = nc;
+        smem = std::max(smem, cursor);
+        if (cursor > smem_cap) return false;
+    }
+    return true;
+}
+
+template <class T>
+void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s) {
+    static size_t attr = 0;
+    if (plan.smem > attr) {
+        MG_CK(cudaFuncSetAttribute(k_coarse_vcycle_res<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
+        attr = plan.smem;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(plan.G);
+    cfg.blockDim = dim3(RB);
+    cfg.dynamicSmemBytes = plan.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr_[1];
+    attr_[0].id = cudaLaunchAttributeCooperative;
+    attr_[0].val.cooperative = 1;
+    cfg.attrs = attr_;
+    cfg.numAttrs = 1;
+    MG_CK(cudaLaunchKernelEx(&cfg, k_coarse_vcycle_res<T>, c, plan));
+    MG_LAUNCH_CHECK();
+}
+
+#define MG_INST(T)                                                                                             \
+    template bool coarse_res_plan<T>(const CoarseCycle<T>&, int, uint32_t, std::vector<ResLevel>&,             \
+                                     std::vector<ResCopy>&, std::vector<int32_t>&, std::vector<uint32_t>&,     \
+                                     uint32_t&, cudaStream_t);                                                 \
+    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t);
+MG_INST(float)
+MG_INST(double)
+#undef MG_INST
+
+}  // namespace mgpbd

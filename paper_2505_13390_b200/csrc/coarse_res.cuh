@@ -1,0 +1,51 @@
+// Shared-memory-resident variant of the persistent coarse V-cycle (coarse.cuh).
+//
+// One CTA per SM owns a contiguous, nnz-balanced row range of every coarse level and a member-balanced
+// aggregate range; at kernel start it copies its slices of the static data (CSR offsets, columns and
+// values, D^-1, P, aggregate ids, member lists, its rows of the coarsest inverse) into shared memory
+// with 1-D bulk copies.  Every phase then reads the matrix from shared memory and only gathers vectors
+// from L2: one dependent round trip per row wave instead of two.  Used when the slices fit (the block
+// hierarchies do); otherwise the global-memory kernel runs.
+#pragma once
+#include <vector>
+
+#include "coarse.cuh"
+
+namespace mgpbd {
+
+struct ResLevel {        // one CTA's share of one coarse level
+    int32_t r0 = 0, r1 = 0;  // owned rows
+    int32_t a0 = 0, a1 = 0;  // owned aggregates (towards the next level)
+    int64_t e0 = 0;          // rowptr[r0]
+    int64_t m0 = 0;          // mptr[a0]
+    // shared-memory byte offsets of element r0 / e0 / a0 / m0 of each slice
+    uint32_t o_rp = 0, o_col = 0, o_val = 0, o_dinv = 0, o_P = 0, o_agg = 0, o_mp = 0, o_ml = 0;
+};
+struct ResCopy {
+    const void* src;     // 16-byte aligned
+    uint32_t dst;        // shared-memory byte offset, 16-byte aligned
+    uint32_t bytes;      // multiple of 16
+};
+
+constexpr int RES_MAXC = 64;  // bulk copies per CTA
+
+struct ResPlan {
+    int G = 0;                       // CTAs (one per SM)
+    uint32_t smem = 0;               // dynamic shared memory per CTA
+    const ResLevel* lv = nullptr;    // [G][16]
+    const ResCopy* copies = nullptr; // [G][RES_MAXC]
+    const int32_t* ncopies = nullptr;
+    const uint32_t* txbytes = nullptr;
+};
+
+// Host: build the plan for cycle `c` (host copies of each level's rowptr / mptr are downloaded).
+// Returns false if some CTA's slices exceed `smem_cap` bytes (then the global kernel is used).
+template <class T>
+bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vector<ResLevel>& lv,
+                     std::vector<ResCopy>& copies, std::vector<int32_t>& ncopies, std::vector<uint32_t>& tx,
+                     uint32_t& smem, cudaStream_t s);
+
+template <class T>
+void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s);
+
+}  // namespace mgpbd

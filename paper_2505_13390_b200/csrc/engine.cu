@@ -18,6 +18,7 @@
 #include "matfree.cuh"
 #include "vagal.cuh"
 #include "coarse.cuh"
+#include "coarse_res.cuh"
 
 namespace mgpbd {
 
@@ -182,6 +183,14 @@ class Engine : public EngineBase {
     bool ccyc_ok = false;
     bool use_coarse_kernel = std::getenv("MGPBD_NO_COARSE_KERNEL") == nullptr;
     DBuf<unsigned long long> ctrace;
+    // shared-memory-resident variant of the coarse kernel (coarse_res.cuh); MGPBD_NO_RES_COARSE=1 disables
+    ResPlan res_plan;
+    DBuf<ResLevel> res_lv;
+    DBuf<ResCopy> res_cp;
+    DBuf<int32_t> res_nc;
+    DBuf<uint32_t> res_tx;
+    bool res_ok = false;
+    bool use_res = std::getenv("MGPBD_NO_RES_COARSE") == nullptr;
     int ccyc_from = std::getenv("MGPBD_COARSE_FROM") ? std::atoi(std::getenv("MGPBD_COARSE_FROM")) : 1;
     bool mf_on() const { return cfg.level0_operator == 1 && mf_ready; }
 
@@ -568,6 +577,30 @@ class Engine : public EngineBase {
                 c.t = a.vt.p; c.b = a.vb.p; c.z = a.vz.p; c.x = a.vx.p; c.y = a.vy.p;
             }
             ccyc_ok = true;
+            res_ok = false;
+            if (use_res) {
+                int sms = 148;
+                MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
+                std::vector<ResLevel> lv;
+                std::vector<ResCopy> cp;
+                std::vector<int32_t> nc;
+                std::vector<uint32_t> tx;
+                uint32_t smem = 0;
+                const uint32_t cap = 220u * 1024u;  // 227 KB minus the static descriptor copy
+                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st)) {
+                    res_lv.resize(lv.size()); h2d(res_lv.p, lv.data(), lv.size(), st);
+                    res_cp.resize(cp.size()); h2d(res_cp.p, cp.data(), cp.size(), st);
+                    res_nc.resize(nc.size()); h2d(res_nc.p, nc.data(), nc.size(), st);
+                    res_tx.resize(tx.size()); h2d(res_tx.p, tx.data(), tx.size(), st);
+                    res_plan.G = sms;
+                    res_plan.smem = smem;
+                    res_plan.lv = res_lv.p;
+                    res_plan.copies = res_cp.p;
+                    res_plan.ncopies = res_nc.p;
+                    res_plan.txbytes = res_tx.p;
+                    res_ok = true;
+                }
+            }
         }
         invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
@@ -622,7 +655,8 @@ class Engine : public EngineBase {
             return;
         }
         if (l == ccyc_from && ccyc_ok && b == a.vb.p && x_out == a.vz.p) {
-            coarse_vcycle<T>(ccyc, st);
+            if (res_ok) coarse_vcycle_res<T>(ccyc, res_plan, st);
+            else coarse_vcycle<T>(ccyc, st);
             return;
         }
         const int nu = cfg.smoother_sweeps;

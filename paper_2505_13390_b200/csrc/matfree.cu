@@ -3,6 +3,7 @@
 #include <vector>
 
 #include "matfree.cuh"
+#include "tma.cuh"
 #include "record.cuh"
 #include "solve.cuh"
 
@@ -168,28 +169,6 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 // an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
 constexpr int MF_R = 256;       // rows per tile (= threads per CTA)
 constexpr int MF_STAGES = 3;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
-    asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
-        "r"(phase)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
 
 template <class T, int KC>
 struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 256)
