@@ -284,3 +284,24 @@ def test_step_argument_errors():
         ctx.step(sc.dt, 0)
     with pytest.raises(mgpbd.MgpbdError):
         ctx.aggregates(0)          # no hierarchy before the first step
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_coarse_kernel_variants_agree(precision, monkeypatch):
+    """The shared-memory-resident coarse V-cycle (default), the global-memory coarse kernel and the
+    per-level kernels apply the same operators (summation order differs only inside restrictions)."""
+    sc = scenes.make("block_small")
+    outs = []
+    for env in ({}, {"MGPBD_NO_RES_COARSE": "1"}, {"MGPBD_NO_COARSE_KERNEL": "1"}):
+        for k in ("MGPBD_NO_RES_COARSE", "MGPBD_NO_COARSE_KERNEL"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        ctx = ctx_for(sc, precision=precision, setup_interval=2)
+        for _ in range(2):
+            ctx.step(sc.dt, 4)
+        outs.append((ctx.positions() - sc.pos, ctx.lambdas()))
+        ctx.close()
+    tol = 1e-9 if precision == 0 else 1e-3
+    for x, lam in outs[1:]:
+        assert rel(x, outs[0][0]) <= tol and rel(lam, outs[0][1]) <= tol
