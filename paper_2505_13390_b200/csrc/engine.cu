@@ -630,6 +630,7 @@ class Engine : public EngineBase {
             Level& c = *L[l + 1];
             if (l == 0 && va_ok && mf_on()) {  // from h directly (replicated on every rank, no collective)
                 va_numeric<T>(va, kc, h.p, a.P.p, a.mptr.p, a.mlist.p, mf.at, a.n_agg, c.rowptr, c.val.p, c.dinv.p, st);
+                mark_stage(1);
                 continue;
             }
             if (l == 0 && dist) {  // this rank's fine rows only, then sum the partial coarse values
@@ -642,6 +643,7 @@ class Engine : public EngineBase {
             galerkin_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.P.p, a.n_agg, c.rowptr, c.nnz, a.tval.p, c.val.p,
                                 c.dinv.p, st);
         }
+        mark_stage(2);
         coarse_invert<T>(L[nL - 1]->hot(), inv_work.p, Ainv.p, flags.p, st);
     }
 
@@ -701,7 +703,9 @@ class Engine : public EngineBase {
                 dot_parts<T>(m, r.p, z, parts1.p, l0.grid, st);
                 dot_parts<T>(m, r.p, r.p, parts2.p, l0.grid, st);
             } else {
+                if (k == 0) mark_stage(6);
                 vcycle(0, r.p, z, r.p);
+                if (k == 0) mark_stage(7);
             }
             const int np = nL == 1 ? l0.grid : l0_nparts();
             if (dist) {  // rank-local sums -> allreduce -> checks on the global values
@@ -713,7 +717,9 @@ class Engine : public EngineBase {
                 pcg_finalize_rz(parts1.p, parts2.p, np, scal.p, k, flags.p, tag, st);
             }
             pcg_update_p<T>(cn, z + o, p.p + o, scal.p, k, st);
+            if (k == 0) mark_stage(8);
             pass(0, PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
+            if (k == 0) mark_stage(9);
             if (dist) {
                 finalize_sum(parts1.p, l0_nparts(), dsc.p + 2, st);
                 comm->allreduce(dsc.p + 2, 1, st);
@@ -753,12 +759,25 @@ class Engine : public EngineBase {
         }
     }
 
+    // stage timestamps of one outer iteration (MGPBD_TRACE_STAGES=1; printed at frame end)
+    bool trace_stages = std::getenv("MGPBD_TRACE_STAGES") != nullptr;
+    DBuf<unsigned long long> stamps;
+    void mark_stage(int idx) {
+        if (!trace_stages) return;
+        if (stamps.n < 32) stamps.resize(32);
+        stamp(stamps.p, idx, st);
+    }
+
     void iter_body(int ite) {
+        mark_stage(0);
         refresh();                                                                                   // Eq. 6
+        mark_stage(3);
         pcg(cfg.pcg_iters, ite);                                                                     // l.8
+        mark_stage(4);
         if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
         update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);  // l.9, l.11
         lambda_add<T>(m, lambda.p, xs.p, st);                                                        // l.10
+        mark_stage(5);
     }
 
     void set_profiling(int on) override { cfg.profile = on ? 1 : 0; }
@@ -846,6 +865,16 @@ class Engine : public EngineBase {
         MG_CK(cudaEventRecord(f1, st));
         MG_CK(cudaStreamSynchronize(st));
         launches_last = g_kernel_launches;
+        if (trace_stages && stamps.n) {  // stage times of the last outer iteration
+            unsigned long long tt[10];
+            d2h(tt, stamps.p, 10, st);
+            MG_CK(cudaStreamSynchronize(st));
+            auto us = [&](int a, int b) { return (double)(tt[b] - tt[a]) * 1e-3; };
+            std::fprintf(stderr,
+                         "[mgpbd stages] refresh: VA %.1f levels %.1f coarsest-inverse %.1f | pcg %.1f (first "
+                         "iteration: V-cycle %.1f, p-update %.1f, SpMV %.1f) | update %.1f us\n",
+                         us(0, 1), us(1, 2), us(2, 3), us(3, 4), us(6, 7), us(7, 8), us(8, 9), us(4, 5));
+        }
         if (ccyc.trace) {  // phase times of the last coarse V-cycle (MGPBD_TRACE_COARSE)
             unsigned long long tt[64];
             d2h(tt, ctrace.p, 64, st);

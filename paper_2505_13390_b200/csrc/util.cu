@@ -205,4 +205,14 @@ void group_by_key(const int32_t* key, int64_t n, int64_t nk, DBuf<int64_t>& ptr,
     if (sort) sort_segments_i32(ptr.p, list.p, nk, s);
 }
 
+__global__ void k_stamp(unsigned long long* buf, int idx) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    buf[idx] = t;
+}
+void stamp(unsigned long long* buf, int idx, cudaStream_t s) {
+    k_stamp<<<1, 1, 0, s>>>(buf, idx);
+    MG_LAUNCH_CHECK();
+}
+
 }  // namespace mgpbd

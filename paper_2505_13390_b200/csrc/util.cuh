@@ -36,4 +36,7 @@ void sort_segments_i32(const int64_t* ptr, int32_t* keys, int64_t nseg, cudaStre
 void group_by_key(const int32_t* key, int64_t n, int64_t nk, DBuf<int64_t>& ptr, DBuf<int32_t>& list,
                   DBuf<int32_t>& tmp_cnt, cudaStream_t s, bool sort = true);
 
+// Diagnostics: buf[idx] = %globaltimer (one thread; graph-capturable; MGPBD_TRACE_STAGES).
+void stamp(unsigned long long* buf, int idx, cudaStream_t s);
+
 }  // namespace mgpbd
