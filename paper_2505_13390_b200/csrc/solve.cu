@@ -1,10 +1,15 @@
 // Hot-loop kernels of the MGPCG solve (see solve.cuh).
 #include "solve.cuh"
 
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include <cstdint>
 #include <type_traits>
 
 #include "util.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mgpbd {
 namespace {
@@ -789,6 +794,118 @@ __global__ void __launch_bounds__(256) k_gj_update(int32_t n, double* __restrict
     }
 }
 
+// Blocked Gauss-Jordan inverse as ONE cooperative kernel (one grid barrier per 32-wide panel instead of
+// three launches).  Ping-pong between two n x n buffers so no tile reads a value another CTA writes in
+// the same panel.  Every CTA inverts the 32x32 pivot block itself (warp 0, register-resident columns,
+// pivots broadcast by shuffles), then updates its 32x32 output tiles:
+//   i,j outside K: W' = W - C R,  i in K: W' = R,  j in K: W' = -C P,  both: W' = P
+// with P = (W_KK)^-1, C = W_{:,K}, R = P W_{K,:}.
+constexpr int GJT = 256;
+template <class T>
+__global__ void __launch_bounds__(GJT) k_gj_coop(int32_t n, const int64_t* __restrict__ rowptr,
+                                                 const int32_t* __restrict__ col, const T* __restrict__ val,
+                                                 double* __restrict__ W0, double* __restrict__ W1, int* flags) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double Ps[32][33];
+    __shared__ double Ks[32][33];  // W_old[K rows][J cols]
+    __shared__ double Cs[32][33];  // W_old[I rows][K cols]
+    __shared__ double Rs[32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int npan = (n + 31) / 32;
+    double* cur = (npan % 2 == 0) ? W0 : W1;  // the buffer that holds the inverse after npan swaps is W0
+    double* nxt = (npan % 2 == 0) ? W1 : W0;
+    {
+        const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        for (int64_t i = gw; i < n; i += nw) {
+            for (int32_t j = lane; j < n; j += 32) cur[i * n + j] = 0.0;
+            __syncwarp();
+            for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) cur[i * n + col[e]] = (double)val[e];
+        }
+    }
+    grid.sync();
+    for (int pnl = 0; pnl < npan; ++pnl) {
+        const int32_t k0 = pnl * 32, bs = min(32, n - k0);
+        {   // P = inverse of the pivot block (identity-padded to 32 x 32), Gauss-Jordan by the whole CTA:
+            // 4 entries per thread, the old row k / column k read before the barrier of each step
+            for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
+                const int i = q >> 5, j = q & 31;
+                Ps[i][j] = (i < bs && j < bs) ? cur[(int64_t)(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
+            }
+            __syncthreads();
+            for (int k = 0; k < 32; ++k) {
+                double pv = Ps[k][k];
+                if (!(pv > 0.0)) {
+                    if (blockIdx.x == 0 && threadIdx.x == 0) flags[5] = 1;
+                    pv = (pv == 0.0 || !isfinite(pv)) ? 1.0 : pv;
+                }
+                const double ip = 1.0 / pv;
+                double nv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = threadIdx.x + u * GJT, i = q >> 5, j = q & 31;
+                    const double sij = Ps[i][j], sik = Ps[i][k], skj = Ps[k][j];
+                    nv[u] = i == k ? (j == k ? ip : skj * ip) : (j == k ? -sik * ip : sij - sik * skj * ip);
+                }
+                __syncthreads();
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int q = threadIdx.x + u * GJT;
+                    Ps[q >> 5][q & 31] = nv[u];
+                }
+                __syncthreads();
+            }
+            (void)warp;
+            (void)lane;
+        }
+        const int nt = npan * npan;
+        for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+            const int I = tile / npan, J = tile % npan;
+            const int32_t i0 = I * 32, j0 = J * 32;
+            const bool iK = I == pnl, jK = J == pnl;
+            for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
+                const int r = q >> 5, c = q & 31;
+                if (!jK) Ks[r][c] = (r < bs && j0 + c < n) ? cur[(int64_t)(k0 + r) * n + j0 + c] : 0.0;
+                if (!iK) Cs[r][c] = (i0 + r < n && c < bs) ? cur[(int64_t)(i0 + r) * n + k0 + c] : 0.0;
+            }
+            __syncthreads();
+            if (!jK) {
+                for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
+                    const int t = q >> 5, c = q & 31;
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int u = 0; u < 32; ++u) acc += Ps[t][u] * Ks[u][c];
+                    Rs[t][c] = acc;
+                }
+            }
+            __syncthreads();
+            for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
+                const int r = q >> 5, c = q & 31;
+                const int32_t i = i0 + r, j = j0 + c;
+                if (i >= n || j >= n) continue;
+                double v;
+                if (iK && jK) v = Ps[r][c];
+                else if (iK) v = Rs[r][c];
+                else if (jK) {
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int t = 0; t < 32; ++t) acc += Cs[r][t] * Ps[t][c];
+                    v = -acc;
+                } else {
+                    double acc = 0.0;
+#pragma unroll 8
+                    for (int t = 0; t < 32; ++t) acc += Cs[r][t] * Rs[t][c];
+                    v = cur[(int64_t)i * n + j] - acc;
+                }
+                nxt[(int64_t)i * n + j] = v;
+            }
+            __syncthreads();
+        }
+        grid.sync();
+        double* t = cur; cur = nxt; nxt = t;
+    }
+}
+
 template <class T>
 __global__ void k_coarse_gemv(int32_t n, const double* __restrict__ Ainv, const T* __restrict__ b, T* __restrict__ x) {
     const int lane = threadIdx.x & 31;
@@ -1079,6 +1196,30 @@ void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cuda
         if (bytes > 48 * 1024)
             MG_CK(cudaFuncSetAttribute(k_coarse_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
         k_coarse_inv<T><<<1, 1024, bytes, s>>>(n, A.rowptr, A.col, A.val, work, Ainv, flags, 1);
+        MG_LAUNCH_CHECK();
+        return;
+    }
+    static const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
+    if (coop) {  // one cooperative launch; work is the second n x n buffer
+        static int grid = 0;
+        if (!grid) {
+            int dev = 0, sms = 0, occ = 0;
+            MG_CK(cudaGetDevice(&dev));
+            MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gj_coop<T>, GJT, 0));
+            grid = sms * std::max(1, std::min(occ, 2));
+        }
+        const int npan = (n + 31) / 32;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(std::min(grid, npan * npan));
+        cfg.blockDim = dim3(GJT);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        MG_CK(cudaLaunchKernelEx(&cfg, k_gj_coop<T>, n, A.rowptr, A.col, A.val, Ainv, work, flags));
         MG_LAUNCH_CHECK();
         return;
     }
