@@ -109,13 +109,28 @@ __global__ void k_va_g(int64_t npairs, const int32_t* __restrict__ pstart, const
                        const T* __restrict__ h, const T* __restrict__ P, G4<T>* __restrict__ G) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
         double g0 = 0.0, g1_ = 0.0, g2 = 0.0;
-        for (int32_t e = pstart[p]; e < pstart[p + 1]; ++e) {
-            const int32_t code = vlist2[e];
-            const double pj = (double)P[code / KC];
-            const T* hh = h + (int64_t)code * 3;
-            g0 += pj * (double)hh[0];
-            g1_ += pj * (double)hh[1];
-            g2 += pj * (double)hh[2];
+        const int32_t e0 = pstart[p], e1 = pstart[p + 1];
+        // chunks of 4 incidences: all index loads, then all P / h gathers, then the sums (in order)
+        for (int32_t eb = e0; eb < e1; eb += 4) {
+            int32_t code[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) code[q] = eb + q < e1 ? vlist2[eb + q] : -1;
+            double pj[4], hx[4], hy[4], hz[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const bool in = code[q] >= 0;
+                const T* hh = h + (int64_t)(in ? code[q] : 0) * 3;
+                pj[q] = in ? (double)P[code[q] / KC] : 0.0;
+                hx[q] = in ? (double)hh[0] : 0.0;
+                hy[q] = in ? (double)hh[1] : 0.0;
+                hz[q] = in ? (double)hh[2] : 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                g0 += pj[q] * hx[q];
+                g1_ += pj[q] * hy[q];
+                g2 += pj[q] * hz[q];
+            }
         }
         G[p] = G4<T>{(T)g0, (T)g1_, (T)g2, (T)0};
     }
@@ -141,10 +156,22 @@ __global__ void k_va_a1(int64_t cnnz, const int64_t* __restrict__ cptr, const in
                         const int64_t* __restrict__ crowptr, const double* __restrict__ dterm, T* __restrict__ cval) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnnz; k += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
-        for (int64_t c = cptr[k]; c < cptr[k + 1]; ++c) {
-            const int2 pq = cpq[c];
-            const G4<T> a = G[pq.x], b = G[pq.y];
-            s += (double)a.x * (double)b.x + (double)a.y * (double)b.y + (double)a.z * (double)b.z;
+        const int64_t c0 = cptr[k], c1 = cptr[k + 1];
+        // chunks of 4 products: all (p, q) loads, then all G gathers, then the sums (in order)
+        for (int64_t cb = c0; cb < c1; cb += 4) {
+            int2 pq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pq[u] = cb + u < c1 ? cpq[cb + u] : make_int2(-1, -1);
+            G4<T> a[4], b[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool in = pq[u].x >= 0;
+                a[u] = in ? G[pq[u].x] : G4<T>{(T)0, (T)0, (T)0, (T)0};
+                b[u] = in ? G[pq[u].y] : G4<T>{(T)0, (T)0, (T)0, (T)0};
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                s += (double)a[u].x * (double)b[u].x + (double)a[u].y * (double)b[u].y + (double)a[u].z * (double)b[u].z;
         }
         const int32_t r = erow[k];
         if (k == crowptr[r + 1] - 1) s += dterm[r];
