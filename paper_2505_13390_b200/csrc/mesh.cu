@@ -243,7 +243,7 @@ __global__ void k_eval_distance(int32_t m, const int32_t* __restrict__ verts, co
 // ARAP (Eq. 8, literal squared form, reading c15): C = ||F - R||_F^2, G = 2(F - R) D_m^-T,
 // grad_{1..3} = columns of G, grad_0 = -sum; h_k = sqrt(w_{v_k}) grad_k.
 template <class T>
-__global__ void k_eval_arap(int32_t m, const int32_t* __restrict__ verts, const double* __restrict__ x,
+__global__ void __launch_bounds__(128, 8) k_eval_arap(int32_t m, const int32_t* __restrict__ verts, const double* __restrict__ x,
                             const double* __restrict__ Dminv, const double* __restrict__ sqrtw,
                             const double* __restrict__ alpha, double dt2, const double* __restrict__ lambda,
                             T* __restrict__ h, T* __restrict__ b) {
