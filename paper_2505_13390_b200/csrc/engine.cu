@@ -713,10 +713,10 @@ class Engine : public EngineBase {
                 finalize_sum(parts2.p, np, dsc.p + 1, st);
                 comm->allreduce(dsc.p, 2, st);
                 pcg_commit_rz(dsc.p, scal.p, k, flags.p, tag, st);
+                pcg_update_p<T>(cn, z + o, p.p + o, scal.p, k, st);
             } else {
-                pcg_finalize_rz(parts1.p, parts2.p, np, scal.p, k, flags.p, tag, st);
+                pcg_update_p_fin<T>(cn, z + o, p.p + o, scal.p, k, parts1.p, parts2.p, np, flags.p, tag, st);
             }
-            pcg_update_p<T>(cn, z + o, p.p + o, scal.p, k, st);
             if (k == 0) mark_stage(8);
             pass(0, PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
             if (k == 0) mark_stage(9);
@@ -724,10 +724,11 @@ class Engine : public EngineBase {
                 finalize_sum(parts1.p, l0_nparts(), dsc.p + 2, st);
                 comm->allreduce(dsc.p + 2, 1, st);
                 pcg_commit_pq(dsc.p + 2, scal.p, k, flags.p, tag, st);
+                pcg_update_xr<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, st);
             } else {
-                pcg_finalize_pq(parts1.p, l0_nparts(), scal.p, k, flags.p, tag, st);
+                pcg_update_xr_fin<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, parts1.p, l0_nparts(),
+                                     flags.p, tag, st);
             }
-            pcg_update_xr<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, st);
         }
     }
 

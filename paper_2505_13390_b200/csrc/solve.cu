@@ -4,6 +4,7 @@
 #include <cooperative_groups.h>
 #include <cstdlib>
 
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -599,6 +600,67 @@ __global__ void k_pcg_xr(int32_t n, const T* __restrict__ p, const T* __restrict
     }
 }
 
+// Finalisation of <r,z> (and <r,r>) fused into the p update: every CTA reduces the partials in the same
+// fixed order (identical value everywhere), CTA 0 publishes the scalar and raises the flags of
+// k_fin_rz; saves one launch per PCG iteration.
+template <class T>
+__global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ p, double* __restrict__ scal, int k,
+                            const double* __restrict__ prz, const double* __restrict__ prr, int np, int* flags,
+                            int tag) {
+    __shared__ double sh[32];
+    __shared__ double rz_s;
+    double a = 0.0, c = 0.0;
+    for (int i = threadIdx.x; i < np; i += PB) { a += prz[i]; c += prr[i]; }
+    a = block_sum<PB>(a, sh);
+    c = block_sum<PB>(c, sh);
+    if (threadIdx.x == 0) {
+        rz_s = a;
+        if (blockIdx.x == 0) {
+            scal[2 * k] = a;
+            if (!isfinite(a) || !isfinite(c)) {
+                if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+            } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
+                if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+                atomicAdd(&flags[4], 1);
+            }
+        }
+    }
+    __syncthreads();
+    double beta = 0.0;
+    if (k > 0) {
+        const double prev = scal[2 * (k - 1)];
+        beta = prev != 0.0 ? rz_s / prev : 0.0;
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = (T)((double)z[i] + beta * (double)p[i]);
+}
+
+// <p,q> finalisation fused into the x / r update (see k_pcg_p_fin)
+template <class T>
+__global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
+                             T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
+                             int np, int* flags, int tag) {
+    __shared__ double sh[32];
+    __shared__ double pq_s;
+    double a = 0.0;
+    for (int i = threadIdx.x; i < np; i += PB) a += ppq[i];
+    a = block_sum<PB>(a, sh);
+    if (threadIdx.x == 0) {
+        pq_s = a;
+        if (blockIdx.x == 0) {
+            scal[2 * k + 1] = a;
+            if (!isfinite(a))
+                if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+        }
+    }
+    __syncthreads();
+    const double alpha = pq_s != 0.0 ? scal[2 * k] / pq_s : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = (T)((double)x[i] + alpha * (double)p[i]);
+        r[i] = (T)((double)r[i] - alpha * (double)q[i]);
+    }
+}
+
 template <class T>
 __global__ void k_dot(int32_t n, const T* __restrict__ a, const T* __restrict__ b, double* __restrict__ parts) {
     __shared__ double sh[32];
@@ -1163,6 +1225,18 @@ void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaSt
     MG_LAUNCH_CHECK();
 }
 template <class T>
+void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const double* prz, const double* prr, int np,
+                      int* flags, int tag, cudaStream_t s) {
+    k_pcg_p_fin<T><<<vgrid(std::max<int32_t>(n, 1)), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
+void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
+                       int* flags, int tag, cudaStream_t s) {
+    k_pcg_xr_fin<T><<<vgrid(std::max<int32_t>(n, 1)), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag);
+    MG_LAUNCH_CHECK();
+}
+template <class T>
 void pcg_update_xr(int32_t n, const T* p, const T* q, T* x, T* r, const double* scal, int k, cudaStream_t s) {
     if (!n) return;
     k_pcg_xr<T><<<vgrid(n), PB, 0, s>>>(n, p, q, x, r, scal, k);
@@ -1258,6 +1332,10 @@ void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s
     template void prolong_add<T>(int32_t, const int32_t*, const T*, const T*, T*, cudaStream_t);               \
     template void pcg_update_p<T>(int32_t, const T*, T*, const double*, int, cudaStream_t);                    \
     template void pcg_update_xr<T>(int32_t, const T*, const T*, T*, T*, const double*, int, cudaStream_t);     \
+    template void pcg_update_p_fin<T>(int32_t, const T*, T*, double*, int, const double*, const double*, int,  \
+                                      int*, int, cudaStream_t);                                               \
+    template void pcg_update_xr_fin<T>(int32_t, const T*, const T*, T*, T*, double*, int, const double*, int,  \
+                                       int*, int, cudaStream_t);                                              \
     template void dot_parts<T>(int32_t, const T*, const T*, double*, int, cudaStream_t);                       \
     template void scale_by_inv_sqrt<T>(int32_t, const T*, T*, const double*, cudaStream_t);                    \
     template void coarse_invert<T>(const Csr<T>&, double*, double*, int*, cudaStream_t);                       \

@@ -71,6 +71,14 @@ template <class T> void restrict_members(int32_t nc, const int64_t* mptr, const 
 template <class T> void prolong_add(int32_t n, const int32_t* agg, const T* P, const T* e, T* x, cudaStream_t s);
 // p = z + beta p with beta = rz[k]/rz[k-1] (0 if k == 0 or rz[k-1] == 0)
 template <class T> void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaStream_t s);
+// single-GPU variants with the dot finalisation fused in (same flags / scal semantics as the
+// pcg_finalize_* + pcg_update_* pairs)
+template <class T>
+void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const double* prz, const double* prr, int np,
+                      int* flags, int tag, cudaStream_t s);
+template <class T>
+void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
+                       int* flags, int tag, cudaStream_t s);
 // alpha = rz[k]/pq[k] (0 if pq == 0); x += alpha p; r -= alpha q
 template <class T> void pcg_update_xr(int32_t n, const T* p, const T* q, T* x, T* r, const double* scal, int k,
                                       cudaStream_t s);
