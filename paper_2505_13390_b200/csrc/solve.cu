@@ -556,18 +556,30 @@ __global__ void k_jacobi0(int32_t n, const T* __restrict__ dinv, const T* __rest
         y[i] = (T)(omega * (double)dinv[i] * (double)b[i]);
 }
 
-// bc[a] = sum_{i in a, ascending} t[i]  (warp per aggregate, fixed-order butterfly)
+// bc[a] = sum_{i in a, ascending} t[i]: 8 lanes per aggregate, each lane's members in chunks of 4 with
+// all list loads issued before the t gathers; lane partials + fixed-order butterfly (deterministic)
 template <class T>
 __global__ void k_restrict(int32_t nc, const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
                            const T* __restrict__ t, T* __restrict__ bc) {
-    const int lane = threadIdx.x & 31;
+    constexpr int G = 8, PER = 32 / G, UN = 4;
+    const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t a = gw; a < nc; a += nw) {
+    for (int64_t base = gw * PER; base < nc; base += nw * PER) {  // warp-uniform trip count
+        const int64_t a = base + sub;
         double s = 0.0;
-        for (int64_t e = mptr[a] + lane; e < mptr[a + 1]; e += 32) s += (double)t[mlist[e]];
-        s = group_sum<32>(s);
-        if (lane == 0) bc[a] = (T)s;
+        if (a < nc) {
+            const int64_t m0 = mptr[a], m1 = mptr[a + 1];
+            for (int64_t eb = m0 + sl; eb < m1; eb += G * UN) {
+                int32_t mi[UN];
+#pragma unroll
+                for (int q = 0; q < UN; ++q) mi[q] = eb + q * G < m1 ? mlist[eb + q * G] : -1;
+#pragma unroll
+                for (int q = 0; q < UN; ++q) s += mi[q] >= 0 ? (double)t[mi[q]] : 0.0;
+            }
+        }
+        s = group_sum<G>(s);
+        if (a < nc && sl == 0) bc[a] = (T)s;
     }
 }
 
