@@ -625,6 +625,7 @@ typedef struct {
     int64_t* rowptr; int32_t* col; double* val;
     int32_t* agg; int32_t n_agg; double* P; double omega;
     double cheb_theta, cheb_delta;  /* Chebyshev interval (reading c20) */
+    int32_t* gs_order;              /* multicolour GS: nodes sorted by (colour, index) (reading c22) */
 } orc_level;
 
 struct orc_hier {
@@ -638,7 +639,7 @@ struct orc_hier {
 };
 
 static void level_free(orc_level* v) {
-    free(v->rowptr); free(v->col); free(v->val); free(v->agg); free(v->P);
+    free(v->rowptr); free(v->col); free(v->val); free(v->agg); free(v->P); free(v->gs_order);
     memset(v, 0, sizeof *v);
 }
 
@@ -705,6 +706,16 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
         orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, c->col, c->val);
         double lam = orc_power(a->n, a->rowptr, a->col, a->val, cfg->power_iters, cfg->seed, l);
         a->omega = 2.0 / (cfg->lambda_safety * lam + cfg->lambda_min_est);
+        if (cfg->smoother == 2) {  /* multicolour GS order of this level (reading c22) */
+            int32_t* colour = xmalloc(sizeof(int32_t) * (size_t)a->n);
+            orc_colour(a->n, a->rowptr, a->col, cfg->seed, colour);
+            ci_pair* ord = xmalloc(sizeof(ci_pair) * (size_t)a->n);
+            for (int32_t i = 0; i < a->n; ++i) { ord[i].c = colour[i]; ord[i].i = i; }
+            qsort(ord, (size_t)a->n, sizeof(ci_pair), cmp_ci);
+            a->gs_order = xmalloc(sizeof(int32_t) * (size_t)a->n);
+            for (int32_t i = 0; i < a->n; ++i) a->gs_order[i] = ord[i].i;
+            free(ord); free(colour);
+        }
         {   /* Chebyshev interval [cheb_lower*hi, hi], hi = safety*lambda_max (reading c20) */
             const double hi = cfg->lambda_safety * lam, lo = cfg->cheb_lower * hi;
             a->cheb_theta = 0.5 * (hi + lo);
@@ -775,19 +786,37 @@ static void chebyshev(const orc_level* a, int sweeps, const double* b, double* x
     }
 }
 
-static void smooth(const orc_hier* h, const orc_level* a, const double* b, double* x, double* tmp, double* d) {
+/* Multicolour Gauss-Seidel ("parallel GS"; reading c22): one sweep updates the nodes in
+ * (colour, index) order — forward for pre-smoothing, reversed for post-smoothing, so the V-cycle stays
+ * symmetric: x_i = (b_i - sum_{j != i} A_ij x_j) / A_ii with the latest x. */
+static void gauss_seidel(const orc_level* a, int sweeps, int backward, const double* b, double* x) {
+    for (int s = 0; s < sweeps; ++s)
+        for (int32_t t = 0; t < a->n; ++t) {
+            const int32_t i = a->gs_order[backward ? a->n - 1 - t : t];
+            double acc = 0.0, dg = 0.0;
+            for (int64_t e = a->rowptr[i]; e < a->rowptr[i + 1]; ++e) {
+                if (a->col[e] == i) dg = a->val[e];
+                else acc += a->val[e] * x[a->col[e]];
+            }
+            x[i] = (b[i] - acc) / dg;
+        }
+}
+
+static void smooth(const orc_hier* h, const orc_level* a, const double* b, double* x, double* tmp, double* d,
+                   int post) {
     if (h->cfg.smoother == 1) chebyshev(a, h->cfg.smoother_sweeps, b, x, tmp, d);
+    else if (h->cfg.smoother == 2) gauss_seidel(a, h->cfg.smoother_sweeps, post, b, x);
     else for (int s = 0; s < h->cfg.smoother_sweeps; ++s) jacobi(a, b, x, tmp);
 }
 
 void orc_hier_cheb(const orc_hier* h, int l, double* theta, double* delta) {
     *theta = h->lv[l].cheb_theta; *delta = h->lv[l].cheb_delta;
 }
-void orc_hier_smooth(const orc_hier* h, int l, const double* b, double* x) {
+void orc_hier_smooth(const orc_hier* h, int l, const double* b, double* x, int post) {
     const orc_level* a = &h->lv[l];
     double* tmp = xmalloc(sizeof(double) * (size_t)a->n);
     double* d = xmalloc(sizeof(double) * (size_t)a->n);
-    smooth(h, a, b, x, tmp, d);
+    smooth(h, a, b, x, tmp, d, post);
     free(tmp); free(d);
 }
 
@@ -800,14 +829,14 @@ static void vcycle_level(const orc_hier* h, int l, const double* b, double* x) {
     double* tmp = xmalloc(sizeof(double) * (size_t)n);
     double* d = xmalloc(sizeof(double) * (size_t)n);
     for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
-    smooth(h, a, b, x, tmp, d);
+    smooth(h, a, b, x, tmp, d, 0);
     orc_spmv(n, a->rowptr, a->col, a->val, x, tmp);
     double* bc = xcalloc((size_t)nc, sizeof(double));
     double* ec = xmalloc(sizeof(double) * (size_t)nc);
     for (int32_t i = 0; i < n; ++i) bc[a->agg[i]] += a->P[i] * (b[i] - tmp[i]);
     vcycle_level(h, l + 1, bc, ec);
     for (int32_t i = 0; i < n; ++i) x[i] += a->P[i] * ec[a->agg[i]];
-    smooth(h, a, b, x, tmp, d);
+    smooth(h, a, b, x, tmp, d, 1);
     free(tmp); free(d); free(bc); free(ec);
 }
 

@@ -77,7 +77,7 @@ def lib():
             "orc_hier_get_P": (None, [P, C.c_int, P]),
             "orc_hier_omega": (f64, [P, C.c_int]),
             "orc_hier_cheb": (None, [P, C.c_int, P, P]),
-            "orc_hier_smooth": (None, [P, C.c_int, P, P]),
+            "orc_hier_smooth": (None, [P, C.c_int, P, P, C.c_int]),
             "orc_hier_get_B0": (None, [P, P]),
             "orc_hier_n_colours": (i32, [P]),
             "orc_vcycle": (None, [P, P, P]),
@@ -357,10 +357,10 @@ class Hierarchy:
         lib().orc_hier_cheb(self.h, l, C.byref(t), C.byref(d))
         return t.value, d.value
 
-    def smooth(self, l, b, x0):
-        """One pre/post smoothing pass (configured smoother) at level l, from x0."""
+    def smooth(self, l, b, x0, post=False):
+        """One pre (post=False) or post smoothing pass (configured smoother) at level l, from x0."""
         x = _c(x0, np.float64).copy()
-        lib().orc_hier_smooth(self.h, l, _p(_c(b, np.float64)), _p(x))
+        lib().orc_hier_smooth(self.h, l, _p(_c(b, np.float64)), _p(x), int(post))
         return x
 
     def B0(self):

@@ -365,3 +365,41 @@ def test_backtracking_and_residual_exit_equal_dense_frame(O, name):
     xr, _, lr = _python_frame(O, sc, 12, om, backtrack=True, tol=tol, trace=trace)
     assert sim.iters_used() == len(trace) < 12
     assert np.abs(sim.state()[2] - lr).max() <= 1e-7 * np.abs(lr).max()
+
+
+# ------------------------------------------------------------------ multicolour GS smoother (reading c22)
+def test_gs_sweep_is_the_permuted_triangular_solve(O, bar_sys):
+    """One forward multicolour GS sweep = solve (D + L_p) x' = b - U_p x in the (colour, index) order;
+    the backward (post) sweep = (D + U_p) x' = b - L_p x (the order reversed)."""
+    import scipy.linalg as sl
+    r, c, v, A = bar_sys
+    h = O.Hierarchy(r, c, v, O.default_config(smoother=2, smoother_sweeps=1))
+    colours, _ = O.colour(r, c)
+    order = np.lexsort((np.arange(A.shape[0]), colours))        # by colour, then index
+    Ap = A[np.ix_(order, order)]
+    rng = np.random.default_rng(8)
+    b, x0 = rng.normal(size=A.shape[0]), rng.normal(size=A.shape[0])
+    Lw, Up = np.tril(Ap), np.triu(Ap, 1)
+    want = np.empty_like(b)
+    want[order] = sl.solve_triangular(Lw, b[order] - Up @ x0[order], lower=True)
+    assert np.allclose(h.smooth(0, b, x0), want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
+    Uw, Lp = np.triu(Ap), np.tril(Ap, -1)
+    want[order] = sl.solve_triangular(Uw, b[order] - Lp @ x0[order], lower=False)
+    assert np.allclose(h.smooth(0, b, x0, post=True), want, rtol=1e-10, atol=1e-12 * np.abs(want).max())
+
+
+def test_gs_vcycle_symmetric_positive_and_pcg(O, bar_sys):
+    """Forward pre-sweeps and reversed post-sweeps make the GS V-cycle a symmetric positive definite
+    preconditioner (identical pre- and post-smoothers keep the cycle symmetric)."""
+    r, c, v, A = bar_sys
+    h = O.Hierarchy(r, c, v, O.default_config(smoother=2))
+    rng = np.random.default_rng(9)
+    n = A.shape[0]
+    for _ in range(5):
+        u, w = rng.normal(size=n), rng.normal(size=n)
+        Mu, Mw = h.vcycle(u), h.vcycle(w)
+        assert abs(Mu @ w - u @ Mw) <= 1e-9 * np.linalg.norm(Mu) * np.linalg.norm(w)
+        assert u @ Mu > 0
+    b = rng.normal(size=n)
+    x, rc, _ = h.pcg(b, 300)
+    assert rc == 0 and np.linalg.norm(A @ x - b) <= 1e-3 * np.linalg.norm(b)
