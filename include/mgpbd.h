@@ -99,7 +99,9 @@ typedef struct {
                                  PAPER.md:450); the CSR is assembled either way (Galerkin, diagonal).
                                  Default 1 */
     int32_t smoother;         /* V-cycle smoother: 0 = omega-Jacobi (default), 1 = Chebyshev
-                                 (smoother_sweeps steps = polynomial degree; reading c20) */
+                                 (smoother_sweeps steps = polynomial degree; reading c20), 2 = multicolour
+                                 Gauss-Seidel (forward pre / reversed post sweeps; reading c22; needs
+                                 level0_operator = 0 and one rank) */
     double cheb_lower;        /* Chebyshev interval [cheb_lower * hi, hi] of D^-1 A, hi = lambda_safety *
                                  lambda_max (power method, lazily at setup: PAPER.md:320); 0.25 */
     int32_t backtrack;        /* 1: halve the relaxation omega (floor omega_min) whenever ||b|| of an outer

@@ -74,6 +74,10 @@ class Engine : public EngineBase {
         DBuf<double> tval64;
         double omega = 0.0;
         double sm_omega[8] = {0, 0, 0, 0, 0, 0, 0, 0}, sm_alpha[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // set_smoother
+        // multicolour GS smoother (smoother = 2): rows grouped by colour
+        DBuf<int64_t> gs_ptr;
+        DBuf<int32_t> gs_list;
+        int gs_ncol = 0;
         // V-cycle vectors
         DBuf<T> vb, vz, vx, vy, vt;
         int vl = 32, grid = 1, vlr = 0, tile_nnz = 0;
@@ -487,6 +491,14 @@ class Engine : public EngineBase {
                 trace("gs_bootstrap", l);
             }
             a.n_agg = na;
+            if (cfg.smoother == 2) {  // multicolour GS order of this level (reading c22)
+                DBuf<int32_t> cl, cnt_;
+                const int32_t* cols = nullptr;
+                if (l == 0) { cols = colours0.p; a.gs_ncol = ncolours; }
+                else { cl.resize(a.n); a.gs_ncol = colour(a.n, a.rowptr, a.col, cfg.seed, cl.p, st); cols = cl.p; }
+                group_by_key(cols, a.n, a.gs_ncol, a.gs_ptr, a.gs_list, cnt_, st, true);
+                MG_CK(cudaStreamSynchronize(st));
+            }
             DBuf<int32_t> cnt;
             group_by_key(a.agg.p, a.n, na, a.mptr, a.mlist, cnt, st, true);
             a.P64.resize(a.n);
@@ -558,7 +570,7 @@ class Engine : public EngineBase {
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
         ccyc_ok = false;
-        if (use_coarse_kernel && ccyc_from >= 1 && nL >= ccyc_from + 2) {
+        if (use_coarse_kernel && cfg.smoother != 2 && ccyc_from >= 1 && nL >= ccyc_from + 2) {
             ccyc = CoarseCycle<T>();
             ccyc.K = nL - ccyc_from;
             ccyc.nu = cfg.smoother_sweeps;
@@ -665,6 +677,23 @@ class Engine : public EngineBase {
         T* cur = a.vx.p;
         T* nxt = a.vy.p;
         const int32_t o = lo0(l), cn = cnt(l);  // rows this rank updates at this level
+        if (cfg.smoother == 2) {  // multicolour GS: forward pre-sweeps, reversed post-sweeps (c22)
+            const Csr<T> A = a.hot();
+            MG_CK(cudaMemsetAsync(cur, 0, sizeof(T) * a.n, st));
+            for (int sw = 0; sw < nu; ++sw) gs_sweep<T>(A, a.gs_ptr.p, a.gs_list.p, a.gs_ncol, false, b, cur, st);
+            pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
+            Level& c = *L[l + 1];
+            restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
+            vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+            prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
+            for (int sw = 0; sw < nu; ++sw) gs_sweep<T>(A, a.gs_ptr.p, a.gs_list.p, a.gs_ncol, true, b, cur, st);
+            d2d(x_out, cur, a.n, st);
+            if (dot_r) {  // the partials of r.z and r.r the PCG finalisation expects
+                dot_parts<T>(a.n, dot_r, x_out, parts1.p, l0_nparts(), st);
+                dot_parts<T>(a.n, dot_r, dot_r, parts2.p, l0_nparts(), st);
+            }
+            return;
+        }
         vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.sm_omega[0], cur + o, st);  // step 0 from x = 0
         for (int sw = 1; sw < nu; ++sw) {  // x_{sw+1} over x_{sw-1} (x_0 = 0: no xprev)
             pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.sm_omega[sw], a.sm_alpha[sw], sw == 1 ? nullptr : nxt);
@@ -1112,7 +1141,10 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail("bad rank/world");
     if (cfg->world > 1 && !cfg->nccl_id && !cfg->vgroup) return fail("world > 1 needs nccl_id or vgroup");
     if (cfg->level0_operator != 0 && cfg->level0_operator != 1) return fail("level0_operator must be 0 or 1");
-    if (cfg->smoother != 0 && cfg->smoother != 1) return fail("smoother must be 0 (omega-Jacobi) or 1 (Chebyshev)");
+    if (cfg->smoother < 0 || cfg->smoother > 2)
+        return fail("smoother must be 0 (omega-Jacobi), 1 (Chebyshev) or 2 (multicolour Gauss-Seidel)");
+    if (cfg->smoother == 2 && (cfg->level0_operator != 0 || cfg->world > 1 || cfg->vgroup || cfg->nccl_id))
+        return fail("the Gauss-Seidel smoother needs level0_operator = 0 and one rank");
     if (cfg->smoother_sweeps > 8) return fail("smoother_sweeps must be <= 8");
     if (cfg->backtrack != 0 && cfg->backtrack != 1) return fail("backtrack must be 0 or 1");
     if (!(cfg->omega_min > 0.0) || !(cfg->residual_tol >= 0.0)) return fail("bad omega_min / residual_tol");

@@ -673,6 +673,28 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
     }
 }
 
+// One colour of a multicolour Gauss-Seidel sweep (reading c22): for the rows of colour c
+// (mutually independent), x_i = (b_i - sum_{j != i} A_ij x_j) / A_ii in place; warp per row, diagonal
+// last in every row; products in T, row sum in fp64.
+template <class T>
+__global__ void k_gs_colour_smooth(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                   const T* __restrict__ val, const int64_t* __restrict__ gs_ptr,
+                                   const int32_t* __restrict__ gs_list, int c, const T* __restrict__ b,
+                                   T* __restrict__ x) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t r0 = gs_ptr[c], r1 = gs_ptr[c + 1];
+    for (int64_t t = r0 + gw; t < r1; t += nw) {
+        const int32_t i = gs_list[t];
+        const int64_t a = rowptr[i], e = rowptr[i + 1] - 1;
+        T part = (T)0;
+        for (int64_t k = a + lane; k < e; k += 32) part += val[k] * x[col[k]];
+        const double sum = group_sum<32>((double)part);
+        if (lane == 0) x[i] = (T)(((double)b[i] - sum) / (double)val[e]);
+    }
+}
+
 template <class T>
 __global__ void k_dot(int32_t n, const T* __restrict__ a, const T* __restrict__ b, double* __restrict__ parts) {
     __shared__ double sh[32];
@@ -1231,6 +1253,15 @@ void prolong_add(int32_t n, const int32_t* agg, const T* P, const T* e, T* x, cu
     MG_LAUNCH_CHECK();
 }
 template <class T>
+void gs_sweep(const Csr<T>& A, const int64_t* gs_ptr, const int32_t* gs_list, int ncol, bool backward, const T* b, T* x,
+              cudaStream_t s) {
+    for (int t = 0; t < ncol; ++t) {
+        const int c = backward ? ncol - 1 - t : t;
+        k_gs_colour_smooth<T><<<148 * 4, PB, 0, s>>>(A.rowptr, A.col, A.val, gs_ptr, gs_list, c, b, x);
+        MG_LAUNCH_CHECK();
+    }
+}
+template <class T>
 void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaStream_t s) {
     if (!n) return;
     k_pcg_p<T><<<vgrid(n), PB, 0, s>>>(n, z, p, scal, k);
@@ -1343,6 +1374,7 @@ void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s
     template void restrict_members<T>(int32_t, const int64_t*, const int32_t*, const T*, T*, cudaStream_t);    \
     template void prolong_add<T>(int32_t, const int32_t*, const T*, const T*, T*, cudaStream_t);               \
     template void pcg_update_p<T>(int32_t, const T*, T*, const double*, int, cudaStream_t);                    \
+    template void gs_sweep<T>(const Csr<T>&, const int64_t*, const int32_t*, int, bool, const T*, T*, cudaStream_t); \
     template void pcg_update_xr<T>(int32_t, const T*, const T*, T*, T*, const double*, int, cudaStream_t);     \
     template void pcg_update_p_fin<T>(int32_t, const T*, T*, double*, int, const double*, const double*, int,  \
                                       int*, int, cudaStream_t);                                               \

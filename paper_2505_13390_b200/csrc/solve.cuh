@@ -71,6 +71,10 @@ template <class T> void restrict_members(int32_t nc, const int64_t* mptr, const 
 template <class T> void prolong_add(int32_t n, const int32_t* agg, const T* P, const T* e, T* x, cudaStream_t s);
 // p = z + beta p with beta = rz[k]/rz[k-1] (0 if k == 0 or rz[k-1] == 0)
 template <class T> void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaStream_t s);
+// one multicolour Gauss-Seidel sweep in place (colours 0..ncol-1, or reversed), rows grouped by colour
+template <class T>
+void gs_sweep(const Csr<T>& A, const int64_t* gs_ptr, const int32_t* gs_list, int ncol, bool backward, const T* b, T* x,
+              cudaStream_t s);
 // single-GPU variants with the dot finalisation fused in (same flags / scal semantics as the
 // pcg_finalize_* + pcg_update_* pairs)
 template <class T>
