@@ -80,7 +80,7 @@ typedef struct {
     double lambda_safety;     /* omega = 2/(lambda_safety*lambda_max + lambda_min_est), 1.1: keeps the
                                  lazily-set omega below 2/lambda_max as A drifts (reading c9) */
     int32_t smoother_sweeps;  /* pre = post smoother steps, 2 (1..8) */
-    int32_t pcg_iters;        /* fixed MGPCG iterations per outer iteration (reading c10), 10 */
+    int32_t pcg_iters;        /* MGPCG iterations per outer iteration (reading c10), 10 (<= 4090) */
     double omega_relax;       /* x += omega dx: 0.1 tets, 0.25 cloth */
     double gravity[3];        /* (0, -9.8, 0) */
     uint64_t seed;            /* hash seed (reading c0), 1 */
@@ -109,6 +109,9 @@ typedef struct {
     double omega_min;         /* 1e-3 */
     double residual_tol;      /* Alg. 1 l.12: stop the frame after the first outer iteration with
                                  ||b|| < residual_tol * ||b_0|| (one host read per iteration); 0 = off */
+    double pcg_tol;           /* MGPCG convergence exit: the solve stops (remaining iterations become no-ops,
+                                 decided on the device) at the first iteration k with ||r_k|| <= pcg_tol *
+                                 ||b||; 0 = off: exactly pcg_iters iterations (reading c10) */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16

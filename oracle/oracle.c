@@ -21,7 +21,7 @@ void orc_config_default(orc_config* c) {
     c->setup_interval = 20; c->bootstrap_sweeps = 20; c->power_iters = 100;
     c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
     c->smoother = 0; c->cheb_lower = 0.25;
-    c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0;
+    c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0; c->pcg_tol = 0.0;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -861,7 +861,11 @@ int orc_pcg(const orc_hier* h, const double* b, int32_t iters, double* x, double
     int rc = 0;
     for (int32_t i = 0; i < n; ++i) { x[i] = 0.0; r[i] = b[i]; }
     double rz_old = 0.0;
+    const double tol = h->cfg.pcg_tol, bb = dot(n, b, b);
     for (int32_t k = 0; k < iters; ++k) {
+        /* optional convergence exit (reading c10: off by default): stop before iteration k once the
+         * residual r_k meets ||r_k|| <= pcg_tol ||b|| */
+        if (tol > 0.0 && sqrt(dot(n, r, r)) <= tol * sqrt(bb)) break;
         orc_vcycle(h, r, z);
         double rz = dot(n, r, z);
         if (rz_trace) rz_trace[k] = rz;

@@ -38,6 +38,7 @@ typedef struct {
     int32_t backtrack;       /* 1: halve omega when ||b|| rises (reading c21); 0 */
     double omega_min;        /* floor of the halving; 1e-3 */
     double residual_tol;     /* Alg. 1 l.12: break once ||b|| < residual_tol * ||b_0||; 0 = off (c11/c21) */
+    double pcg_tol;          /* MGPCG stops once ||r_k|| <= pcg_tol ||b||; 0 = off, fixed pcg_iters (c10) */
 } orc_config;
 
 void orc_config_default(orc_config* c);

@@ -29,7 +29,7 @@ class Config(C.Structure):
                 ("pcg_iters", C.c_int32), ("omega_relax", C.c_double),
                 ("gravity", C.c_double * 3), ("seed", C.c_uint64), ("smoother", C.c_int32),
                 ("cheb_lower", C.c_double), ("backtrack", C.c_int32), ("omega_min", C.c_double),
-                ("residual_tol", C.c_double)]
+                ("residual_tol", C.c_double), ("pcg_tol", C.c_double)]
 
 
 _lib = None

@@ -720,6 +720,7 @@ class Engine : public EngineBase {
     void pcg(int32_t iters, int ite) {
         Level& l0 = *L[0];
         MG_CK(cudaMemsetAsync(xs.p, 0, sizeof(T) * m, st));
+        pcg_begin(scal.p, cfg.pcg_tol, st);  // convergence exit state (pcg_tol; off by default)
         d2d(r.p, b0.p, m, st);
         MG_CK(cudaMemsetAsync(p.p, 0, sizeof(T) * m, st));
         T* z = l0.vz.p;
@@ -1121,6 +1122,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->backtrack = 0;
     c->omega_min = 1e-3;
     c->residual_tol = 0.0;
+    c->pcg_tol = 0.0;
     return MGPBD_OK;
 }
 
@@ -1149,7 +1151,8 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cfg->backtrack != 0 && cfg->backtrack != 1) return fail("backtrack must be 0 or 1");
     if (!(cfg->omega_min > 0.0) || !(cfg->residual_tol >= 0.0)) return fail("bad omega_min / residual_tol");
     if (cfg->smoother == 1 && !(cfg->cheb_lower > 0.0 && cfg->cheb_lower < 1.0)) return fail("cheb_lower must be in (0, 1)");
-    if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > 4096 || cfg->setup_interval < 1 ||
+    if (!(cfg->pcg_tol >= 0.0)) return fail("pcg_tol must be >= 0");
+    if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > mgpbd::SC_KMAX || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
         cfg->max_dense_coarse < 1)
         return fail("bad config");

@@ -590,8 +590,20 @@ __global__ void k_prolong(int32_t n, const int32_t* __restrict__ agg, const T* _
         x[i] = (T)((double)x[i] + (double)P[i] * (double)e[agg[i]]);
 }
 
+// Convergence exit of MGPCG (pcg_tol > 0): true if the solve is frozen at iteration k, i.e. it was
+// already converged or ||r_k||^2 = rr <= tol^2 ||b||^2 (||b||^2 = rr at k = 0).  The caller publishes
+// ||b||^2 and the flag (one thread) and every thread takes the same decision.
+__device__ __forceinline__ bool pcg_converged(const double* scal, int k, double rr) {
+    if (scal[SC_DONE] != 0.0) return true;
+    const double tol = scal[SC_TOL];
+    if (!(tol > 0.0)) return false;
+    const double b2 = k == 0 ? rr : scal[SC_B2];
+    return rr <= tol * tol * b2;
+}
+
 template <class T>
 __global__ void k_pcg_p(int32_t n, const T* __restrict__ z, T* __restrict__ p, const double* __restrict__ scal, int k) {
+    if (scal[SC_DONE] != 0.0) return;  // converged (pcg_tol): the remaining iterations change nothing
     double beta = 0.0;
     if (k > 0) {
         double prev = scal[2 * (k - 1)];
@@ -604,6 +616,7 @@ __global__ void k_pcg_p(int32_t n, const T* __restrict__ z, T* __restrict__ p, c
 template <class T>
 __global__ void k_pcg_xr(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
                          T* __restrict__ r, const double* __restrict__ scal, int k) {
+    if (scal[SC_DONE] != 0.0) return;
     double pq = scal[2 * k + 1];
     double alpha = pq != 0.0 ? scal[2 * k] / pq : 0.0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -625,9 +638,20 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
     for (int i = threadIdx.x; i < np; i += PB) { a += prz[i]; c += prr[i]; }
     a = block_sum<PB>(a, sh);
     c = block_sum<PB>(c, sh);
+    __shared__ int conv;
+    if (threadIdx.x == 0) conv = pcg_converged(scal, k, c) ? 1 : 0;
+    __syncthreads();
+    if (conv) {  // converged: publish the flag, no event checks, no update
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (k == 0) scal[SC_B2] = c;
+            scal[SC_DONE] = 1.0;
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         rz_s = a;
         if (blockIdx.x == 0) {
+            if (k == 0) scal[SC_B2] = c;
             scal[2 * k] = a;
             if (!isfinite(a) || !isfinite(c)) {
                 if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
@@ -652,6 +676,7 @@ template <class T>
 __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
                              T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
                              int np, int* flags, int tag) {
+    if (scal[SC_DONE] != 0.0) return;
     __shared__ double sh[32];
     __shared__ double pq_s;
     double a = 0.0;
@@ -721,6 +746,9 @@ __global__ void k_fin_rz(const double* __restrict__ prz, const double* __restric
     a = block_sum<1024>(a, sh);
     c = block_sum<1024>(c, sh);
     if (threadIdx.x == 0) {
+        const bool conv = pcg_converged(scal, k, c);
+        if (k == 0) scal[SC_B2] = c;
+        if (conv) { scal[SC_DONE] = 1.0; return; }
         scal[2 * k] = a;
         if (!isfinite(a) || !isfinite(c)) {
             if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
@@ -1127,6 +1155,9 @@ template bool band_config<double>(int32_t, int32_t, const int64_t*, const int32_
 namespace {
 __global__ void k_commit_rz(const double* __restrict__ d2, double* scal, int k, int* flags, int tag) {
     const double a = d2[0], c = d2[1];
+    const bool conv = pcg_converged(scal, k, c);
+    if (k == 0) scal[SC_B2] = c;
+    if (conv) { scal[SC_DONE] = 1.0; return; }
     scal[2 * k] = a;
     if (!isfinite(a) || !isfinite(c)) {
         if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
@@ -1154,6 +1185,14 @@ __global__ void k_range_window(const int64_t* __restrict__ rowptr, const int32_t
 }
 }  // namespace
 
+__global__ void k_pcg_begin(double* scal, double tol) {
+    scal[SC_TOL] = tol;
+    scal[SC_DONE] = 0.0;
+}
+void pcg_begin(double* scal, double tol, cudaStream_t s) {
+    k_pcg_begin<<<1, 1, 0, s>>>(scal, tol);
+    MG_LAUNCH_CHECK();
+}
 void pcg_commit_rz(const double* d2, double* scal, int k, int* flags, int tag, cudaStream_t s) {
     k_commit_rz<<<1, 1, 0, s>>>(d2, scal, k, flags, tag);
     MG_LAUNCH_CHECK();

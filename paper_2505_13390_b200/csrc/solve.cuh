@@ -38,6 +38,12 @@ bool band_config(int32_t row0, int32_t n, const int64_t* rowptr, const int32_t* 
 
 // PCG scalar commit for a partitioned solve: d2 = (r.z, r.r) or d1 = (p.q) already summed over ranks.
 void pcg_commit_rz(const double* d2, double* scal, int k, int* flags, int tag, cudaStream_t s);
+// PCG scalar slots of `scal` (2 * 4096 doubles; iteration k uses 2k, 2k + 1 for k < SC_KMAX): the
+// optional convergence exit (pcg_tol > 0): tolerance, ||b||^2, and the "converged" flag that freezes
+// the remaining iterations (their updates are skipped, so the result equals an early exit).
+constexpr int SC_KMAX = 4090;
+constexpr int SC_TOL = 8189, SC_B2 = 8190, SC_DONE = 8191;
+void pcg_begin(double* scal, double tol, cudaStream_t s);
 void pcg_commit_pq(const double* d1, double* scal, int k, int* flags, int tag, cudaStream_t s);
 
 // Column window [min col, max col] referenced by rows [a, b) (diagonal-last CSR); host result.

@@ -49,7 +49,7 @@ class Config(C.Structure):
                 ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32),
                 ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32),
                 ("smoother", C.c_int32), ("cheb_lower", C.c_double), ("backtrack", C.c_int32),
-                ("omega_min", C.c_double), ("residual_tol", C.c_double)]
+                ("omega_min", C.c_double), ("residual_tol", C.c_double), ("pcg_tol", C.c_double)]
 
 
 class Stats(C.Structure):

@@ -56,3 +56,28 @@ def test_defaults_are_the_literal_loop():
     ctx.step(sc.dt, 4)
     st = ctx.stats()
     assert st.n_b == 4 and st.omega_relax == sc.omega_relax
+
+
+@pytest.mark.parametrize("name", ["bar3k", "block_small"])
+def test_pcg_tolerance_exit(name):
+    """pcg_tol > 0: the device freezes MGPCG at the first iteration k with ||r_k|| <= pcg_tol ||b||
+    (the oracle breaks there) — identical hierarchies, fp64."""
+    sc = scenes.make(name)
+    sim = O.Sim(sc)
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    import scipy.sparse as sp
+    n = r.shape[0] - 1
+    A = sp.csr_matrix((v, c, r), shape=(n, n))
+    b = A @ np.random.default_rng(3).normal(size=n)      # in the range of A: the residual decreases
+    h = O.Hierarchy(r, c, v)
+    res = [np.linalg.norm(b - A @ h.pcg(b, K)[0]) / np.linalg.norm(b) for K in range(0, 8)]
+    assert res[6] < min(res[:6])
+    tol = np.sqrt(res[6] * min(res[:6]))                  # reached first at K = 6
+    ho = O.Hierarchy(r, c, v, O.default_config(pcg_tol=tol))
+    xo, _, _ = ho.pcg(b, 30)
+    ctx = mgpbd.Context.from_scene(sc, pcg_tol=tol)
+    ctx.debug_setup_from(v)
+    xg = ctx.debug_pcg(b, 30)
+    assert rel(xg, xo) <= 1e-9
+    assert np.linalg.norm(b - A @ xg) <= tol * np.linalg.norm(b) * (1 + 1e-9)

@@ -403,3 +403,22 @@ def test_gs_vcycle_symmetric_positive_and_pcg(O, bar_sys):
     b = rng.normal(size=n)
     x, rc, _ = h.pcg(b, 300)
     assert rc == 0 and np.linalg.norm(A @ x - b) <= 1e-3 * np.linalg.norm(b)
+
+
+def test_pcg_tolerance_exit(O, bar_sys):
+    """pcg_tol > 0 (off by default, reading c10): MGPCG stops before the first
+    iteration k with ||r_k|| <= pcg_tol ||b|| — the result equals the fixed-count solve truncated at
+    that k, and meets the tolerance."""
+    r, c, v, A = bar_sys
+    n = A.shape[0]
+    b = A @ np.random.default_rng(11).normal(size=n)     # in the range of A: the residual decreases
+    h = O.Hierarchy(r, c, v)
+    res = [np.linalg.norm(b - A @ h.pcg(b, K)[0]) / np.linalg.norm(b) for K in range(0, 41)]
+    assert res[8] < min(res[:8])
+    tol = np.sqrt(res[8] * min(res[:8]))
+    K = next(k for k in range(41) if res[k] <= tol)
+    assert K == 8
+    ht = O.Hierarchy(r, c, v, O.default_config(pcg_tol=tol))
+    xt, _, _ = ht.pcg(b, 40)
+    assert np.array_equal(xt, h.pcg(b, K)[0])
+    assert np.linalg.norm(b - A @ xt) <= tol * np.linalg.norm(b) * (1 + 1e-12)
