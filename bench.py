@@ -234,12 +234,15 @@ def run_ours(args):
     ctx.set_profiling(True)
     l0_ms = l0_bytes = 0.0
     prof_frames_ms = 0.0
+    phases = {"assemble": 0.0, "galerkin_refresh": 0.0, "vcycle": 0.0, "pcg_other": 0.0, "update": 0.0}
     for _ in range(args.profile_frames):
         ctx.step(sc.dt, sc.n_iters)
         s = ctx.stats()
         l0_ms += s.l0_pass_ms
         l0_bytes += s.l0_pass_bytes
         prof_frames_ms += s.ms_frame - s.ms_setup
+        for k, v in zip(phases, (s.ms_assemble, s.ms_galerkin, s.ms_vcycle, s.ms_pcg_other, s.ms_update)):
+            phases[k] += v / max(args.profile_frames, 1)
     ctx.set_profiling(False)
     if dist:
         tt = torch.tensor([t_ms], device="cuda")
@@ -296,6 +299,8 @@ def run_ours(args):
                      "l0_pass_share_of_frame": (l0_ms / prof_frames_ms) if prof_frames_ms else None},
         "e2e": {"value": e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * n * 8,
                 "d2h_bytes_per_step": (2 * 3 * n + m) * 8},
+        "phase_ms_per_frame": {**{k: round(v, 3) for k, v in phases.items()},
+                               "note": "profiled (eager) frames; graphs are faster"},
         "gpu_launches": launches,
         "clocks": clocks,
     }

@@ -141,6 +141,10 @@ typedef struct {
     int32_t row_begin, row_end;        /* level-0 rows this rank owns */
     int64_t halo_rows;                 /* level-0 x entries received per halo exchange */
     double omega_relax;                /* relaxation omega at the end of the last frame (backtracking) */
+    /* phase times of the last frame in ms (recorded only with profile = 1, i.e. eager launches; else 0):
+       constraint evaluation + assembly / matrix-free refresh, Galerkin refresh + coarsest inverse,
+       V-cycles, the rest of MGPCG, position / lambda update */
+    double ms_assemble, ms_galerkin, ms_vcycle, ms_pcg_other, ms_update;
 } mgpbd_stats;
 
 /* Fill *cfg with the defaults listed above.  Never fails for a non-NULL cfg. */

@@ -156,6 +156,21 @@ class Engine : public EngineBase {
     int64_t l0_launches = 0;
     double l0_bytes_acc = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_pairs;
+    // phase times of the last frame (profile = 1, eager launches): assemble, Galerkin refresh, V-cycle,
+    // whole MGPCG, update
+    enum { PH_ASM, PH_GAL, PH_VC, PH_PCG, PH_UPD, PH_N };
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ph_pairs[PH_N];
+    double ph_ms[PH_N] = {0, 0, 0, 0, 0};
+    template <class F>
+    void timed(int ph, F&& f) {
+        if (!cfg.profile || capturing) { f(); return; }
+        cudaEvent_t e0 = ev();
+        MG_CK(cudaEventRecord(e0, st));
+        f();
+        cudaEvent_t e1 = ev();
+        MG_CK(cudaEventRecord(e1, st));
+        ph_pairs[ph].emplace_back(e0, e1);
+    }
     int64_t launches_last = 0;
     int32_t indef_events = 0;
     // partitioned level 0 (world > 1): rows [r0, r1) of this rank, halo transfers
@@ -734,7 +749,7 @@ class Engine : public EngineBase {
                 dot_parts<T>(m, r.p, r.p, parts2.p, l0.grid, st);
             } else {
                 if (k == 0) mark_stage(6);
-                vcycle(0, r.p, z, r.p);
+                timed(PH_VC, [&] { vcycle(0, r.p, z, r.p); });
                 if (k == 0) mark_stage(7);
             }
             const int np = nL == 1 ? l0.grid : l0_nparts();
@@ -801,13 +816,15 @@ class Engine : public EngineBase {
 
     void iter_body(int ite) {
         mark_stage(0);
-        refresh();                                                                                   // Eq. 6
+        timed(PH_GAL, [&] { refresh(); });                                                           // Eq. 6
         mark_stage(3);
-        pcg(cfg.pcg_iters, ite);                                                                     // l.8
+        timed(PH_PCG, [&] { pcg(cfg.pcg_iters, ite); });                                             // l.8
         mark_stage(4);
-        if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
-        update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);  // l.9, l.11
-        lambda_add<T>(m, lambda.p, xs.p, st);                                                        // l.10
+        timed(PH_UPD, [&] {
+            if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
+            update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);  // l.9, l.11
+            lambda_add<T>(m, lambda.p, xs.p, st);                                                    // l.10
+        });
         mark_stage(5);
     }
 
@@ -855,6 +872,7 @@ class Engine : public EngineBase {
         l0_bytes_acc = 0;
         setup_ran = 0;
         prof_pairs.clear();
+        for (auto& v_ : ph_pairs) v_.clear();
         g_kernel_launches = 0;
         cudaEvent_t f0 = ev(), f1, s0 = nullptr, s1 = nullptr;
         MG_CK(cudaEventRecord(f0, st));
@@ -865,7 +883,7 @@ class Engine : public EngineBase {
         MG_CK(cudaMemsetAsync(lambda.p, 0, sizeof(double) * m, st));                                // l.2
         int32_t iters_run = 0;
         for (int ite = 0; ite < n_iters; ++ite) {                                                    // l.3
-            assemble_hot(dt);                                                                        // l.4-6
+            timed(PH_ASM, [&] { assemble_hot(dt); });                                                // l.4-6
             dot_parts<T>(m, b0.p, b0.p, parts2.p, L[0]->grid, st);
             finalize_sum(parts2.p, L[0]->grid, bn.p + ite, st);
             if (cfg.backtrack) backtrack_omega(bn.p, ite, omega_dev.p, cfg.omega_min, st);
@@ -930,6 +948,16 @@ class Engine : public EngineBase {
             }
             l0_ms = tot;
             l0_bytes = l0_bytes_acc;
+            for (int ph = 0; ph < PH_N; ++ph) {
+                double t = 0;
+                for (auto& pr : ph_pairs[ph]) {
+                    MG_CK(cudaEventElapsedTime(&ms, pr.first, pr.second));
+                    t += ms;
+                }
+                ph_ms[ph] = t;
+            }
+        } else {
+            for (double& t : ph_ms) t = 0;
         }
         int hf[6];
         d2h(hf, flags.p, 6, st);
@@ -982,6 +1010,11 @@ class Engine : public EngineBase {
         s->row_end = r1;
         s->halo_rows = halo_elems;
         s->omega_relax = omega_last;
+        s->ms_assemble = ph_ms[PH_ASM];
+        s->ms_galerkin = ph_ms[PH_GAL];
+        s->ms_vcycle = ph_ms[PH_VC];
+        s->ms_pcg_other = ph_ms[PH_PCG] - ph_ms[PH_VC];
+        s->ms_update = ph_ms[PH_UPD];
     }
 
     void check_level(int l) {

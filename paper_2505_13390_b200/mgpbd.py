@@ -60,7 +60,9 @@ class Stats(C.Structure):
                 ("l0_pass_bytes", C.c_double), ("ms_setup", C.c_double), ("ms_frame", C.c_double),
                 ("kernel_launches", C.c_int64), ("indefinite_events", C.c_int32),
                 ("rank", C.c_int32), ("world", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
-                ("halo_rows", C.c_int64), ("omega_relax", C.c_double)]
+                ("halo_rows", C.c_int64), ("omega_relax", C.c_double), ("ms_assemble", C.c_double),
+                ("ms_galerkin", C.c_double), ("ms_vcycle", C.c_double), ("ms_pcg_other", C.c_double),
+                ("ms_update", C.c_double)]
 
 
 _lib = None

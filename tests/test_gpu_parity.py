@@ -305,3 +305,19 @@ def test_coarse_kernel_variants_agree(precision, monkeypatch):
     tol = 1e-9 if precision == 0 else 1e-3
     for x, lam in outs[1:]:
         assert rel(x, outs[0][0]) <= tol and rel(lam, outs[0][1]) <= tol
+
+
+def test_phase_times_cover_the_frame():
+    """stats.ms_* (profile = 1): the phases add up to the frame (minus setup and small glue)."""
+    sc = scenes.make("block_small")
+    ctx = ctx_for(sc, precision=1)
+    ctx.set_profiling(True)
+    for _ in range(2):
+        ctx.step(sc.dt, sc.n_iters)
+    st = ctx.stats()
+    parts = st.ms_assemble + st.ms_galerkin + st.ms_vcycle + st.ms_pcg_other + st.ms_update
+    assert min(st.ms_assemble, st.ms_galerkin, st.ms_vcycle, st.ms_pcg_other, st.ms_update) > 0
+    assert 0.6 * (st.ms_frame - st.ms_setup) <= parts <= st.ms_frame - st.ms_setup
+    ctx.set_profiling(False)
+    ctx.step(sc.dt, sc.n_iters)
+    assert ctx.stats().ms_vcycle == 0.0
