@@ -88,3 +88,37 @@ def test_fullsize_deterministic_and_graph_replay(name, monkeypatch):
         assert np.array_equal(x, outs[0][0]) and np.array_equal(lam, outs[0][1])
     pinned = sc.inv_mass == 0
     assert np.array_equal(outs[0][0][pinned], sc.pos[pinned])
+
+
+def test_fullsize_two_virtual_ranks_match_one_context():
+    """The row-partitioned path at full size (block1.67M fp32, two virtual ranks on one GPU: halo
+    exchange, TMA row kernel from a non-zero first row, replicated coarse kernels) against one context."""
+    import threading
+    sc = scenes.make("block1.67M")
+    ctx = mgpbd.Context.from_scene(sc, precision=1)
+    ctx.step(sc.dt, 4)
+    x1, l1 = ctx.positions(), ctx.lambdas()
+    ctx.close()
+    group = mgpbd.VirtualGroup(2)
+    out, errs = [None, None], []
+
+    def worker(rank):
+        try:
+            c = mgpbd.Context.from_scene(sc, precision=1, rank=rank, world=2, vgroup=group)
+            c.step(sc.dt, 4)
+            out[rank] = (c.positions(), c.lambdas(), c.stats().halo_rows)
+            c.close()
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(900)
+    assert not errs, errs
+    for x, lam, halo in out:
+        assert halo > 0
+        assert np.linalg.norm(lam - l1) <= 1e-3 * np.linalg.norm(l1)
+        assert np.linalg.norm((x - sc.pos) - (x1 - sc.pos)) <= 1e-3 * np.linalg.norm(x1 - sc.pos)
+    assert np.array_equal(out[0][1], out[1][1])
