@@ -742,7 +742,7 @@ class Engine : public EngineBase {
         const int32_t o = r0, cn = r1 - r0;
         if (dist && nL == 1) throw Error(MGPBD_E_ARG, "a partitioned solve needs at least two levels");
         for (int k = 0; k < iters; ++k) {
-            const int tag = ite * 4096 + k;
+            const int tag = k;  // + flags[7] (outer iteration) * 4096, added on the device
             if (nL == 1) {
                 vcycle(0, r.p, z, nullptr);
                 dot_parts<T>(m, r.p, z, parts1.p, l0.grid, st);
@@ -830,10 +830,13 @@ class Engine : public EngineBase {
 
     void set_profiling(int on) override { cfg.profile = on ? 1 : 0; }
 
+    // One graph serves every outer iteration (the iteration index reaches the kernels through flags[7]),
+    // so after a setup only the second outer iteration pays the capture + instantiation.
     void run_iter(int ite) {
+        set_outer_index(flags.p, ite, st);
         if (!use_graphs || cfg.profile) { iter_body(ite); return; }  // events need eager launches
-        if ((int)graphs.size() <= ite) graphs.resize(ite + 1);
-        IterGraph& g = graphs[ite];
+        if (graphs.empty()) graphs.resize(1);
+        IterGraph& g = graphs[0];
         if (!g.seen) {  // first use after a (re)build: eager
             g.seen = true;
             iter_body(ite);

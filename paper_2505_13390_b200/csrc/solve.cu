@@ -654,9 +654,9 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
             if (k == 0) scal[SC_B2] = c;
             scal[2 * k] = a;
             if (!isfinite(a) || !isfinite(c)) {
-                if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+                if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = flags[7] * 4096 + tag;
             } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
-                if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+                if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = flags[7] * 4096 + tag;
                 atomicAdd(&flags[4], 1);
             }
         }
@@ -687,7 +687,7 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
         if (blockIdx.x == 0) {
             scal[2 * k + 1] = a;
             if (!isfinite(a))
-                if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+                if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = flags[7] * 4096 + tag;
         }
     }
     __syncthreads();
@@ -751,9 +751,9 @@ __global__ void k_fin_rz(const double* __restrict__ prz, const double* __restric
         if (conv) { scal[SC_DONE] = 1.0; return; }
         scal[2 * k] = a;
         if (!isfinite(a) || !isfinite(c)) {
-            if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+            if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = flags[7] * 4096 + tag;
         } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
-            if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+            if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = flags[7] * 4096 + tag;
             atomicAdd(&flags[4], 1);
         }
     }
@@ -766,7 +766,7 @@ __global__ void k_fin_pq(const double* __restrict__ p, int np, double* scal, int
     if (threadIdx.x == 0) {
         scal[2 * k + 1] = a;
         if (!isfinite(a)) {
-            if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+            if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = flags[7] * 4096 + tag;
         }
     }
 }
@@ -1160,9 +1160,9 @@ __global__ void k_commit_rz(const double* __restrict__ d2, double* scal, int k, 
     if (conv) { scal[SC_DONE] = 1.0; return; }
     scal[2 * k] = a;
     if (!isfinite(a) || !isfinite(c)) {
-        if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+        if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = flags[7] * 4096 + tag;
     } else if (a < 0.0 || (a == 0.0 && c > 0.0)) {
-        if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = tag;
+        if (atomicCAS(&flags[0], 0, 1) == 0) flags[2] = flags[7] * 4096 + tag;
         atomicAdd(&flags[4], 1);
     }
 }
@@ -1170,7 +1170,7 @@ __global__ void k_commit_pq(const double* __restrict__ d1, double* scal, int k, 
     const double a = d1[0];
     scal[2 * k + 1] = a;
     if (!isfinite(a)) {
-        if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = tag;
+        if (atomicCAS(&flags[1], 0, 1) == 0) flags[3] = flags[7] * 4096 + tag;
     }
 }
 __global__ void k_range_window(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col, int32_t a,
@@ -1185,6 +1185,11 @@ __global__ void k_range_window(const int64_t* __restrict__ rowptr, const int32_t
 }
 }  // namespace
 
+__global__ void k_set_int(int* p, int v) { *p = v; }
+void set_outer_index(int* flags, int ite, cudaStream_t s) {
+    k_set_int<<<1, 1, 0, s>>>(flags + 7, ite);
+    MG_LAUNCH_CHECK();
+}
 __global__ void k_pcg_begin(double* scal, double tol) {
     scal[SC_TOL] = tol;
     scal[SC_DONE] = 0.0;

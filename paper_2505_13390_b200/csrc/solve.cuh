@@ -44,6 +44,9 @@ void pcg_commit_rz(const double* d2, double* scal, int k, int* flags, int tag, c
 constexpr int SC_KMAX = 4090;
 constexpr int SC_TOL = 8189, SC_B2 = 8190, SC_DONE = 8191;
 void pcg_begin(double* scal, double tol, cudaStream_t s);
+// flags[7] = outer-iteration index (written eagerly before each outer iteration, so the captured
+// iteration graph is the same for every ite; the flag kernels report ite * 4096 + pcg iteration)
+void set_outer_index(int* flags, int ite, cudaStream_t s);
 void pcg_commit_pq(const double* d1, double* scal, int k, int* flags, int tag, cudaStream_t s);
 
 // Column window [min col, max col] referenced by rows [a, b) (diagonal-last CSR); host result.
