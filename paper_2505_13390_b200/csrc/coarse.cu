@@ -327,15 +327,14 @@ __global__ void __launch_bounds__(CB, 2) k_coarse_vcycle(const __grid_constant__
 
 template <class T>
 int coarse_grid() {
-    static int g = 0;
-    if (!g) {
+    static const int g = [] {  // thread-safe one-time initialisation
         int dev = 0, sms = 0, occ = 0;
         MG_CK(cudaGetDevice(&dev));
         MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_coarse_vcycle<T>, CB, 0));
         if (occ < 1) throw Error(-1, "coarse_vcycle: kernel does not fit on an SM");
-        g = sms * std::min(occ, 4);
-    }
+        return sms * std::min(occ, 4);
+    }();
     return g;
 }
 

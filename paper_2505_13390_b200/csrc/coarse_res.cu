@@ -6,6 +6,7 @@
 #include "coarse_res.cuh"
 #include "comm.cuh"
 #include "tma.cuh"
+#include "util.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -321,11 +322,7 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
 
 template <class T>
 void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s) {
-    static size_t attr = 0;
-    if (plan.smem > attr) {
-        MG_CK(cudaFuncSetAttribute(k_coarse_vcycle_res<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem));
-        attr = plan.smem;
-    }
+    ensure_dyn_smem((const void*)k_coarse_vcycle_res<T>, plan.smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.G);
     cfg.blockDim = dim3(RB);

@@ -4,6 +4,7 @@
 
 #include "matfree.cuh"
 #include "tma.cuh"
+#include "util.cuh"
 #include "record.cuh"
 #include "solve.cuh"
 
@@ -308,12 +309,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         const size_t smem = (size_t)MF_STAGES * TileLayout<T, KC>::BYTES;
 #define MG_MFT(M)                                                                                               \
     {                                                                                                           \
-        static bool attr = false;                                                                               \
-        if (!attr) {                                                                                            \
-            MG_CK(cudaFuncSetAttribute(k_mf_rows_tma<T, KC, M>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                                       (int)smem));                                                             \
-            attr = true;                                                                                        \
-        }                                                                                                       \
+        ensure_dyn_smem((const void*)k_mf_rows_tma<T, KC, M>, smem);                                           \
         cudaLaunchConfig_t lc = {};                                                                             \
         lc.gridDim = dim3(A.grid);                                                                              \
         lc.blockDim = dim3(MF_R);                                                                               \

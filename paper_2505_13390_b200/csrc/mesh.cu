@@ -457,8 +457,8 @@ void build_pattern(const int32_t* verts, int32_t m, int kc, int32_t nv, const in
     if (per_warp * wpb > 200 * 1024) throw Error(-1, "vertex degree too large for the pattern kernel");
     size_t smem = per_warp * wpb;
     if (smem > 48 * 1024) {
-        MG_CK(cudaFuncSetAttribute(k_pattern<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        MG_CK(cudaFuncSetAttribute(k_pattern<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ensure_dyn_smem((const void*)k_pattern<0>, smem);
+        ensure_dyn_smem((const void*)k_pattern<1>, smem);
     }
     DBuf<int32_t> cnt;
     cnt.resize(m);

@@ -539,7 +539,7 @@ void galerkin_symbolic(int32_t n, const int64_t* rowptr, const int32_t* col, con
     while (wpb > 1 && (size_t)maxlen * 8 * wpb > 160 * 1024) wpb >>= 1;
     size_t smem = (size_t)maxlen * 8 * wpb;
     if (smem > 200 * 1024) throw Error(-7, "row too long for the Galerkin plan");
-    if (smem > 48 * 1024) MG_CK(cudaFuncSetAttribute(k_gsort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (smem > 48 * 1024) ensure_dyn_smem((const void*)k_gsort, smem);
     plan.gperm.resize(nnz);
     DBuf<int32_t> nseg;
     nseg.resize(n);
@@ -565,8 +565,8 @@ void galerkin_symbolic(int32_t n, const int64_t* rowptr, const int32_t* col, con
     size_t csm = (size_t)maxc * 8 * cw;
     if (csm > 200 * 1024) throw Error(-7, "coarse row candidate list too long");
     if (csm > 48 * 1024) {
-        MG_CK(cudaFuncSetAttribute(k_crow<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
-        MG_CK(cudaFuncSetAttribute(k_crow<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm));
+        ensure_dyn_smem((const void*)k_crow<0>, csm);
+        ensure_dyn_smem((const void*)k_crow<1>, csm);
     }
     DBuf<int32_t> ccnt;
     ccnt.resize(n_agg);

@@ -428,13 +428,9 @@ __global__ void __launch_bounds__(BB, 1) k_rows(int32_t row0, int32_t n, int32_t
 template <class T, int MODE, int VL>
 void launch_rows(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                  double* parts2, cudaStream_t s) {
-    static size_t attr_set = 48 * 1024;
     const size_t smem = ((((size_t)A.band_rows + 1) * sizeof(int32_t) + 15) & ~(size_t)15) +
                         ((size_t)3 * A.band_rows + A.band_win) * sizeof(T);
-    if (smem > attr_set) {
-        MG_CK(cudaFuncSetAttribute(k_rows<T, VL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = smem;
-    }
+    ensure_dyn_smem((const void*)k_rows<T, VL, MODE>, smem);
     k_rows<T, VL, MODE><<<A.band_grid, BB, smem, s>>>(A.row0, A.row0 + A.n, A.band_rows, A.win_lo, A.win_len, A.rowptr, A.col16,
                                                      A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2);
     MG_LAUNCH_CHECK();
@@ -454,12 +450,8 @@ void launch_rows_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* au
 template <class T, int MODE, int VLR>
 void launch_band(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                  double* parts2, cudaStream_t s) {
-    static size_t attr_set = 48 * 1024;
     const size_t smem = ((size_t)A.prod_cap + 8 + A.band_win) * sizeof(T);
-    if (smem > attr_set) {
-        MG_CK(cudaFuncSetAttribute(k_band<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = smem;
-    }
+    ensure_dyn_smem((const void*)k_band<T, VLR, MODE>, smem);
     k_band<T, VLR, MODE><<<A.band_grid, BB, smem, s>>>(A.row0, A.row0 + A.n, A.band_rows, A.win_lo, A.win_len, A.prod_cap, A.rowptr,
                                                       A.col, A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2);
     MG_LAUNCH_CHECK();
@@ -504,12 +496,8 @@ __global__ void k_band_len(int32_t nb, int32_t* __restrict__ lo, const int32_t* 
 template <class T, int MODE, int VLR>
 void launch_tile(const Csr<T>& A, const T* x, const T* b, T* y, const T* aux, double omega, double alpha, const T* xprev, double* parts,
                  double* parts2, cudaStream_t s) {
-    static size_t attr_set = 48 * 1024;
     const size_t smem = (size_t)A.tile_nnz * sizeof(double);
-    if (smem > attr_set) {
-        MG_CK(cudaFuncSetAttribute(k_tile<T, VLR, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_set = smem;
-    }
+    ensure_dyn_smem((const void*)k_tile<T, VLR, MODE>, smem);
     k_tile<T, VLR, MODE><<<A.grid, PB, smem, s>>>(A.row0, A.row0 + A.n, A.rowptr, A.col, A.val, A.dinv, x, b, y, aux, omega, alpha, xprev, parts, parts2);
     MG_LAUNCH_CHECK();
 }
@@ -1355,21 +1343,20 @@ void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cuda
     size_t bytes = (size_t)n * n * sizeof(double);
     if (bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
         if (bytes > 48 * 1024)
-            MG_CK(cudaFuncSetAttribute(k_coarse_inv<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            ensure_dyn_smem((const void*)k_coarse_inv<T>, bytes);
         k_coarse_inv<T><<<1, 1024, bytes, s>>>(n, A.rowptr, A.col, A.val, work, Ainv, flags, 1);
         MG_LAUNCH_CHECK();
         return;
     }
     static const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
     if (coop) {  // one cooperative launch; work is the second n x n buffer
-        static int grid = 0;
-        if (!grid) {
+        static const int grid = [] {  // thread-safe one-time initialisation
             int dev = 0, sms = 0, occ = 0;
             MG_CK(cudaGetDevice(&dev));
             MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
             MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gj_coop<T>, GJT, 0));
-            grid = sms * std::max(1, std::min(occ, 2));
-        }
+            return sms * std::max(1, std::min(occ, 2));
+        }();
         const int npan = (n + 31) / 32;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(std::min(grid, npan * npan));

@@ -1,6 +1,9 @@
 // Deterministic scans, reductions and small helper kernels.
 #include "util.cuh"
 
+#include <mutex>
+#include <unordered_map>
+
 namespace mgpbd {
 
 thread_local int64_t g_kernel_launches = 0;
@@ -213,6 +216,17 @@ __global__ void k_stamp(unsigned long long* buf, int idx) {
 void stamp(unsigned long long* buf, int idx, cudaStream_t s) {
     k_stamp<<<1, 1, 0, s>>>(buf, idx);
     MG_LAUNCH_CHECK();
+}
+
+void ensure_dyn_smem(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> set;
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& cur = set[kernel];
+    if (bytes > cur && bytes > 48 * 1024) {
+        MG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        cur = bytes;
+    }
 }
 
 }  // namespace mgpbd

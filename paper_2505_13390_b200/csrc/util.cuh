@@ -36,6 +36,10 @@ void sort_segments_i32(const int64_t* ptr, int32_t* keys, int64_t nseg, cudaStre
 void group_by_key(const int32_t* key, int64_t n, int64_t nk, DBuf<int64_t>& ptr, DBuf<int32_t>& list,
                   DBuf<int32_t>& tmp_cnt, cudaStream_t s, bool sort = true);
 
+// Raise a kernel's dynamic shared-memory limit to at least `bytes` (thread-safe: contexts of virtual
+// ranks launch from several host threads; the attribute is only ever raised).
+void ensure_dyn_smem(const void* kernel, size_t bytes);
+
 // Diagnostics: buf[idx] = %globaltimer (one thread; graph-capturable; MGPBD_TRACE_STAGES).
 void stamp(unsigned long long* buf, int idx, cudaStream_t s);
 
