@@ -1284,7 +1284,7 @@ mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x) {
     return guarded(ctx, [&] { ctx->eng->debug_vcycle(b, x); });
 }
 mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x) {
-    if (ctx && (!b || !x || iters < 0 || iters > 4096)) return MGPBD_E_ARG;
+    if (ctx && (!b || !x || iters < 0 || iters > mgpbd::SC_KMAX)) return MGPBD_E_ARG;
     return guarded(ctx, [&] { ctx->eng->debug_pcg(b, iters, x); });
 }
 mgpbd_status mgpbd_nccl_unique_id(void* out128) {
