@@ -1,12 +1,13 @@
 #!/usr/bin/env python
 """Benchmark of the MGPBD hot path (BASELINE.json metric: ms/frame @20 AMG-PCG iterations on the
-1.67M-tet block, plus level-0 CSR-pass HBM GB/s).
+1.67M-tet block, plus the HBM GB/s of the level-0 matrix pass).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
-                  [--precision fp32|fp64]
+                  [--precision fp32|fp64] [--level0-operator 0|1] [--partitioned]
 
-One step = one frame of Algorithm 1 (20 outer iterations x 10 MGPCG iterations, lazy setup every 20
-frames, so a 20-frame window holds exactly one setup).  Rank 0 prints one JSON line.
+One step = one frame of Algorithm 1 (20 outer iterations x 10 MGPCG iterations; the lazy setup runs
+every 20 frames and after an indefinite PCG step, reading c13, and its cost is inside the timed
+frames).  Rank 0 prints one JSON line.
 --impl reference times the CPU oracle (the tier's reference arm) on a bounded slab of the same
 workload and scales by constraint count (time per iteration is linear in size).
 """
