@@ -321,3 +321,37 @@ def test_phase_times_cover_the_frame():
     ctx.set_profiling(False)
     ctx.step(sc.dt, sc.n_iters)
     assert ctx.stats().ms_vcycle == 0.0
+
+
+def test_single_tet_closed_form():
+    """One ARAP tetrahedron: A is 1x1, so the first outer iteration is Eq. 4,
+    dlambda = -(C + at lambda) / (sum_k w_k |grad_k C|^2 + at), then Eq. 5 — against the oracle."""
+    X = np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]], float) * 0.1
+    x0 = X.copy(); x0[3] += [0.02, -0.01, 0.03]
+    w = np.array([0.0, 2.0, 3.0, 4.0])
+    comp = np.array([1e-6])
+    ctx = mgpbd.Context(4, np.array([[0, 1, 2, 3]], np.int32), X, w, comp, pos=x0, gravity=(0, 0, 0),
+                        omega_relax=1.0, pcg_iters=1)
+    ctx.step(1e-2, 1)
+    Cv, g = O.eval_arap(np.array([[0, 1, 2, 3]], np.int32), x0, O.rest_arap(np.array([[0, 1, 2, 3]], np.int32), X)[0])
+    at = comp[0] / 1e-4
+    dl = -Cv[0] / ((w[:, None] * g[0] ** 2).sum() + at)
+    assert np.isclose(ctx.lambdas()[0], dl, rtol=1e-11)
+    assert np.allclose(ctx.positions(), x0 + (w[:, None] * g[0]) * dl, rtol=1e-11, atol=1e-15)
+
+
+def test_all_pinned_block():
+    """Every vertex pinned: A = diag(at), positions never move and lambda = -C / at after one iteration."""
+    sc = scenes.make("bar_small")
+    w = np.zeros_like(sc.inv_mass)
+    ctx = mgpbd.Context(sc.kind, sc.verts, sc.rest_pos, w, sc.compliance, pos=sc.pos, pcg_iters=2)
+    ctx.step(sc.dt, 1)
+    assert np.array_equal(ctx.positions(), sc.pos)
+    Cv, _ = O.eval_arap(sc.verts, sc.pos, O.rest_arap(sc.verts, sc.rest_pos)[0])
+    assert np.allclose(ctx.lambdas(), -Cv / (sc.compliance / sc.dt ** 2), rtol=1e-10)
+
+
+def test_degenerate_rest_tet_rejected():
+    X = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0], [0, 1, 0]], float)   # collinear -> zero volume
+    with pytest.raises(mgpbd.MgpbdError):
+        mgpbd.Context(4, np.array([[0, 1, 2, 3]], np.int32), X, np.ones(4), np.ones(1))
