@@ -198,6 +198,10 @@ MGPBD_API mgpbd_status mgpbd_debug_setup_from(mgpbd_ctx* ctx, const double* A0_v
 /* Apply one V-cycle / K MGPCG iterations of the current hierarchy to host b (n_0) -> host x. */
 MGPBD_API mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x);
 MGPBD_API mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x);
+/* Measurement hook: `reps` (1..4096) level-0 SpMV+dot passes of the hot operator on the current state,
+ * captured as one CUDA graph and timed with events around its replay (no launch gaps).  *ms = device
+ * time, *bytes = the passes' algorithmic bytes.  Needs a stepped context and one rank; E_ARG otherwise. */
+MGPBD_API mgpbd_status mgpbd_pass_burst(mgpbd_ctx* ctx, int32_t reps, double* ms, double* bytes);
 
 /* ---- multi-GPU (row-partitioned level 0; coarse levels and setup replicated) ----
  * Every rank calls every function with the same inputs.  Per level-0 matrix pass the rank exchanges

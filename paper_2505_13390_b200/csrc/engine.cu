@@ -45,6 +45,7 @@ struct EngineBase {
     virtual void debug_setup_from(const double* vals) = 0;
     virtual void debug_vcycle(const double* b, double* x) = 0;
     virtual void debug_pcg(const double* b, int32_t iters, double* x) = 0;
+    virtual void pass_burst(int32_t reps, double* ms, double* bytes) = 0;
     virtual void bind() = 0;  // make this context's device/stream current for the calling thread
     virtual void set_profiling(int on) = 0;
     bool stale = true;
@@ -1084,6 +1085,40 @@ class Engine : public EngineBase {
         d2h(xo, tmp.p, m, st);
         MG_CK(cudaStreamSynchronize(st));
     }
+    // `reps` level-0 SpMV+dot passes (the hot operator on the current state) captured into one CUDA
+    // graph and timed with events around its launch (after one warm-up replay): the pass rate without
+    // launch gaps.  Returns the device time of the replay and the passes' algorithmic bytes.
+    void pass_burst(int32_t reps, double* ms, double* bytes) override {
+        if (!have_hier || (cfg.level0_operator == 1 && !mf_ready)) throw Error(MGPBD_E_ARG, "no current state");
+        if (dist) throw Error(MGPBD_E_ARG, "pass_burst: one rank only");
+        cudaGraph_t graph;
+        cudaGraphExec_t exec;
+        const bool prof = cfg.profile;
+        cfg.profile = 0;
+        MG_CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        for (int k = 0; k < reps; ++k) l0_pass(PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
+        const cudaError_t ec = cudaStreamEndCapture(st, &graph);
+        cfg.profile = prof;
+        MG_CK(ec);
+        MG_CK(cudaGraphInstantiate(&exec, graph, 0));
+        MG_CK(cudaGraphDestroy(graph));
+        cudaEvent_t e0, e1;
+        MG_CK(cudaEventCreate(&e0));
+        MG_CK(cudaEventCreate(&e1));
+        MG_CK(cudaGraphLaunch(exec, st));  // warm-up
+        MG_CK(cudaEventRecord(e0, st));
+        MG_CK(cudaGraphLaunch(exec, st));
+        MG_CK(cudaEventRecord(e1, st));
+        MG_CK(cudaEventSynchronize(e1));
+        float t = 0;
+        MG_CK(cudaEventElapsedTime(&t, e0, e1));
+        *ms = t;
+        *bytes = pass_bytes(PASS_SPMV_DOT) * reps;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaGraphExecDestroy(exec);
+    }
+
     void debug_pcg(const double* b, int32_t iters, double* xo) override {
         if (!have_hier) throw Error(MGPBD_E_ARG, "no hierarchy");
         DBuf<double> tmp;
@@ -1286,6 +1321,10 @@ mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x) {
 mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x) {
     if (ctx && (!b || !x || iters < 0 || iters > mgpbd::SC_KMAX)) return MGPBD_E_ARG;
     return guarded(ctx, [&] { ctx->eng->debug_pcg(b, iters, x); });
+}
+mgpbd_status mgpbd_pass_burst(mgpbd_ctx* ctx, int32_t reps, double* ms, double* bytes) {
+    if (ctx && (reps < 1 || reps > 4096 || !ms || !bytes)) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->pass_burst(reps, ms, bytes); });
 }
 mgpbd_status mgpbd_nccl_unique_id(void* out128) {
     if (!out128) return MGPBD_E_ARG;

@@ -20,6 +20,7 @@ SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgp
            "mgpbd_get_positions", "mgpbd_get_velocities", "mgpbd_get_lambda", "mgpbd_get_stats",
            "mgpbd_get_level_sizes", "mgpbd_get_level", "mgpbd_get_prolongator", "mgpbd_get_aggregates",
            "mgpbd_get_near_kernel", "mgpbd_debug_setup_from", "mgpbd_debug_vcycle", "mgpbd_debug_pcg",
+           "mgpbd_pass_burst",
            "mgpbd_last_error", "mgpbd_destroy", "mgpbd_nccl_unique_id", "mgpbd_vgroup_create",
            "mgpbd_vgroup_destroy", "mgpbd_partition_rows", "mgpbd_halo_plan"]
 
@@ -96,6 +97,7 @@ def lib():
             "mgpbd_debug_setup_from": (C.c_int, [P, P]),
             "mgpbd_debug_vcycle": (C.c_int, [P, P, P]),
             "mgpbd_debug_pcg": (C.c_int, [P, P, i32, P]),
+            "mgpbd_pass_burst": (C.c_int, [P, i32, P, P]),
             "mgpbd_last_error": (C.c_char_p, [P]),
             "mgpbd_nccl_unique_id": (C.c_int, [P]),
             "mgpbd_vgroup_create": (C.c_int, [i32, P]),
@@ -295,6 +297,12 @@ class Context:
         x = np.empty_like(b)
         self._ck(lib().mgpbd_debug_vcycle(self.h, _p(b), _p(x)))
         return x
+
+    def pass_burst(self, reps):
+        """(device ms, algorithmic bytes) of `reps` level-0 passes replayed as one CUDA graph."""
+        ms, by = C.c_double(), C.c_double()
+        self._ck(lib().mgpbd_pass_burst(self.h, int(reps), C.byref(ms), C.byref(by)))
+        return ms.value, by.value
 
     def debug_pcg(self, b, iters):
         b = np.ascontiguousarray(b, np.float64)

@@ -355,3 +355,16 @@ def test_degenerate_rest_tet_rejected():
     X = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0], [0, 1, 0]], float)   # collinear -> zero volume
     with pytest.raises(mgpbd.MgpbdError):
         mgpbd.Context(4, np.array([[0, 1, 2, 3]], np.int32), X, np.ones(4), np.ones(1))
+
+
+def test_pass_burst_hook():
+    sc = scenes.make("block_small")
+    ctx = ctx_for(sc, precision=1)
+    with pytest.raises(mgpbd.MgpbdError):
+        ctx.pass_burst(4)                      # no state before the first step
+    ctx.step(sc.dt, 2)
+    ms, by = ctx.pass_burst(8)
+    assert ms > 0 and by > 8 * sc.n_cons * 4
+    x_before = ctx.positions()
+    ctx.step(sc.dt, 2)                         # the context keeps working after the hook
+    assert np.isfinite(ctx.positions()).all() and not np.array_equal(ctx.positions(), x_before)
