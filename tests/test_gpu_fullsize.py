@@ -122,3 +122,33 @@ def test_fullsize_two_virtual_ranks_match_one_context():
         assert np.linalg.norm(lam - l1) <= 1e-3 * np.linalg.norm(l1)
         assert np.linalg.norm((x - sc.pos) - (x1 - sc.pos)) <= 1e-3 * np.linalg.norm(x1 - sc.pos)
     assert np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.fixture(scope="module")
+def block_oracle_hierarchy():
+    sc = scenes.make("block1.67M")
+    ro, co = O.pattern(sc.verts, sc.n_verts)
+    C, g, at = oracle_state(sc)
+    v0 = O.assemble(sc.verts, sc.inv_mass, g, at, ro, co)
+    return sc, ro, co, v0, O.Hierarchy(ro, co, v0)       # ~1 min of oracle setup on one core
+
+
+@pytest.mark.parametrize("precision,tol_v", [(1, 1e-4), (0, 1e-10)])
+def test_fullsize_vcycle_and_pcg_on_oracle_hierarchy(block_oracle_hierarchy, precision, tol_v):
+    """block1.67M: the whole setup on the oracle's A_0 bits (levels, omegas) and the V-cycle / 5-step
+    MGPCG of the device hierarchy (resident coarse kernel, cooperative coarsest inverse) against the
+    oracle's, in fp32 (the bench configuration) and fp64."""
+    sc, ro, co, v0, h = block_oracle_hierarchy
+    ctx = mgpbd.Context.from_scene(sc, precision=precision)
+    ctx.debug_setup_from(v0)
+    st = ctx.stats()
+    assert st.n_levels == h.n_levels
+    for l in range(h.n_levels - 1):
+        assert st.n[l] == h.level_size(l)[0]
+        assert np.isclose(st.omega[l], h.omega(l), rtol=1e-9), l
+    b = np.random.default_rng(0).normal(size=sc.n_cons)
+    zg, zo = ctx.debug_vcycle(b), h.vcycle(b)
+    assert np.linalg.norm(zg - zo) <= tol_v * np.linalg.norm(zo)
+    xg, (xo, rc, _) = ctx.debug_pcg(b, 5), h.pcg(b, 5)
+    assert rc == 0 and np.linalg.norm(xg - xo) <= 100 * tol_v * np.linalg.norm(xo)
+    ctx.close()
