@@ -368,3 +368,22 @@ def test_pass_burst_hook():
     x_before = ctx.positions()
     ctx.step(sc.dt, 2)                         # the context keeps working after the hook
     assert np.isfinite(ctx.positions()).all() and not np.array_equal(ctx.positions(), x_before)
+
+
+@pytest.mark.parametrize("precision", [0, 1])
+def test_tma_and_register_row_kernels_agree(precision, monkeypatch):
+    """The TMA-pipelined matrix-free row kernel and the register-streaming one (MGPBD_NO_TMA) compute
+    the same rows (only the dot partials' grid differs)."""
+    sc = scenes.make("block_small")
+    outs = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("MGPBD_NO_TMA", env)
+        else:
+            monkeypatch.delenv("MGPBD_NO_TMA", raising=False)
+        ctx = ctx_for(sc, precision=precision)
+        ctx.step(sc.dt, 4)
+        outs.append((ctx.positions() - sc.pos, ctx.lambdas()))
+        ctx.close()
+    tol = 1e-9 if precision == 0 else 1e-3
+    assert rel(outs[1][0], outs[0][0]) <= tol and rel(outs[1][1], outs[0][1]) <= tol
