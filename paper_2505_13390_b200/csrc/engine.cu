@@ -137,7 +137,7 @@ class Engine : public EngineBase {
     DBuf<int32_t> vlist, col0;
     int64_t nnz0 = 0;
     DBuf<T> h, b0;
-    DBuf<double> h64, b64;
+    DBuf<double> h64, b64, at64;
     std::vector<std::unique_ptr<Level>> L;
     int nL = 0;
     bool have_hier = false;
@@ -195,6 +195,7 @@ class Engine : public EngineBase {
     bool mf_ready = false;      // h is current and describes level 0 (false after debug_setup_from)
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
+    bool va_off = std::getenv("MGPBD_NO_VA_SETUP") != nullptr;  // CSR Galerkin at setup (comparison)
     double last_dt = 0.0;
     DBuf<double> omega_dev;     // relaxation omega of Alg. 1 l.11 (device scalar: backtracking, c21)
     double omega_last = 0.0;
@@ -481,6 +482,7 @@ class Engine : public EngineBase {
         DBuf<double> B, Bn;
         const int maxl = std::min<int>(cfg.max_levels, MGPBD_MAX_LEVELS);
         pw_v.resize(m); pw_w.resize(m);
+        bool va_built = false;
         trace(nullptr);
         for (int l = 0; l + 1 < maxl; ++l) {
             Level& a = *L[l];
@@ -524,18 +526,39 @@ class Engine : public EngineBase {
             L.emplace_back(new Level());
             Level& c = *L[l + 1];
             Level& a2 = *L[l];  // re-bind after emplace (unique_ptr: stable)
-            galerkin_symbolic(a2.n, a2.rowptr, a2.col, a2.agg.p, a2.mptr.p, a2.mlist.p, na, a2.plan, c.rowptr_own,
-                              c.col_own, st);
-            trace("galerkin_symbolic", l);
+            // matrix-free level 0: P^T A_0 P from the fp64 gradients (vertex-aggregate form, vagal.cuh) — no
+            // CSR Galerkin plan over the 1.4 GB level-0 pattern; the VA plan is the hot loop's as well
+            const bool va_setup = l == 0 && cfg.level0_operator == 1 && mf_ready && h64.n && !va_off;
+            if (va_setup) {
+                GalerkinPlan& gp = a2.plan;  // not used: drop a CSR plan left by an earlier setup
+                gp.gperm.free_all(); gp.tptr.free_all(); gp.tstart.free_all(); gp.trow.free_all();
+                gp.tagg.free_all(); gp.lptr.free_all(); gp.llist.free_all(); gp.T = 0;
+                va_coarse_pattern(nv, kc, vptr.p, vlist.p, a2.agg.p, na, c.rowptr_own, c.col_own, st);
+                trace("va_pattern", l);
+            } else {
+                galerkin_symbolic(a2.n, a2.rowptr, a2.col, a2.agg.p, a2.mptr.p, a2.mlist.p, na, a2.plan, c.rowptr_own,
+                                  c.col_own, st);
+                trace("galerkin_symbolic", l);
+            }
             c.n = na;
             c.nnz = read_scalar(c.rowptr_own.p + na, st);
             c.rowptr = c.rowptr_own.p; c.col = c.col_own.p;
             c.configure(st);
             c.val64.resize(c.nnz); c.dinv64.resize(c.n);
-            a2.tval64.resize(a2.plan.T);
-            galerkin_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, a2.P64.p, na, c.rowptr, c.nnz,
-                                     a2.tval64.p, c.val64.p, c.dinv64.p, st);
-            trace("galerkin_numeric", l);
+            if (va_setup) {
+                va_symbolic(nv, kc, vptr.p, vlist.p, a2.agg.p, na, c.rowptr, c.col, c.nnz, va, st);
+                at64.resize(m);
+                va_at(m, alpha.p, last_dt, at64.p, st);
+                va_numeric<double>(va, kc, h64.p, a2.P64.p, a2.mptr.p, a2.mlist.p, at64.p, na, c.rowptr, c.val64.p,
+                                   c.dinv64.p, st);
+                va_built = true;
+                trace("va_symbolic+numeric", l);
+            } else {
+                a2.tval64.resize(a2.plan.T);
+                galerkin_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, a2.P64.p, na, c.rowptr, c.nnz,
+                                         a2.tval64.p, c.val64.p, c.dinv64.p, st);
+                trace("galerkin_numeric", l);
+            }
             double lam;
             if (l == 0 && mf64_ok && mf_ready && h64.n) {
                 // level 0 through the fp64 matrix-free operator (2 gathers instead of the 1.4 GB CSR)
@@ -571,14 +594,14 @@ class Engine : public EngineBase {
                 a.tval.resize(a.plan.T);
             }
         }
-        if (dist && nL > 1) {  // level-0 Galerkin segments of the owned rows; the others stay zero
+        if (dist && nL > 1 && !va_built) {  // level-0 Galerkin segments of the owned rows; the others stay zero
             Level& a = *L[0];
             tb0 = read_scalar(a.plan.tptr.p + r0, st);
             te0 = read_scalar(a.plan.tptr.p + r1, st);
             MG_CK(cudaMemsetAsync(a.tval.p, 0, sizeof(T) * (a.plan.T ? a.plan.T : 1), st));
         }
-        va_ok = false;
-        if (cfg.level0_operator == 1 && nL > 1) {
+        va_ok = va_built && nL > 1;
+        if (!va_ok && cfg.level0_operator == 1 && nL > 1) {
             va_symbolic(nv, kc, vptr.p, vlist.p, L[0]->agg.p, L[0]->n_agg, L[1]->rowptr, L[1]->col, L[1]->nnz, va, st);
             va_ok = true;
             trace("va_symbolic");

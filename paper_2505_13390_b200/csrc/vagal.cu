@@ -179,7 +179,94 @@ __global__ void k_va_a1(int64_t cnnz, const int64_t* __restrict__ cptr, const in
     }
 }
 
+__global__ void k_pat_count(int32_t nv, const int64_t* __restrict__ vpp, const int32_t* __restrict__ pagg,
+                            int32_t* __restrict__ cnt) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        const int64_t p0 = vpp[v], p1 = vpp[v + 1];
+        const int32_t kv = (int32_t)(p1 - p0);
+        for (int64_t p = p0; p < p1; ++p) atomicAdd(&cnt[pagg[p]], kv);
+    }
+}
+// candidates of row a: every b that shares a vertex with a (order within a row fixed later by a sort)
+__global__ void k_pat_fill(int32_t nv, const int64_t* __restrict__ vpp, const int32_t* __restrict__ pagg,
+                           const int64_t* __restrict__ ptr, int32_t* __restrict__ cur, int32_t* __restrict__ cand) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        const int64_t p0 = vpp[v], p1 = vpp[v + 1];
+        const int32_t kv = (int32_t)(p1 - p0);
+        for (int64_t p = p0; p < p1; ++p) {
+            const int32_t a = pagg[p];
+            const int64_t base = ptr[a] + atomicAdd(&cur[a], kv);
+            for (int64_t q = p0; q < p1; ++q) cand[base + (q - p0)] = pagg[q];
+        }
+    }
+}
+// per row: unique sorted candidates except a, then a (diagonal last); count pass (out == nullptr) or fill
+__global__ void k_pat_unique(int32_t n, const int64_t* __restrict__ ptr, const int32_t* __restrict__ cand,
+                             int32_t* __restrict__ ucnt, const int64_t* __restrict__ crowptr, int32_t* __restrict__ out) {
+    for (int32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+        int64_t o = out ? crowptr[a] : 0;
+        int32_t u = 0, prev = -1;
+        for (int64_t k = ptr[a]; k < ptr[a + 1]; ++k) {
+            const int32_t b = cand[k];
+            if (b == prev || b == a) { prev = b; continue; }
+            prev = b;
+            if (out) out[o++] = b;
+            ++u;
+        }
+        if (out) out[o] = a;
+        else ucnt[a] = u + 1;
+    }
+}
+__global__ void k_va_at(int32_t m, const double* __restrict__ alpha, double dt2, double* __restrict__ at) {
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) at[i] = alpha[i] / dt2;
+}
+
 }  // namespace
+
+void va_coarse_pattern(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg,
+                       int32_t n_agg, DBuf<int64_t>& crowptr, DBuf<int32_t>& ccol, cudaStream_t s) {
+    const int64_t ninc = read_scalar(vptr + nv, s);
+    DBuf<int32_t> vl2, pcnt, pst, pagg, ccnt, cnt, cur, cand, ucnt;
+    DBuf<int64_t> vpp, ptr;
+    vl2.resize(ninc);
+    pcnt.resize(nv);
+    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, vl2.p, pcnt.p);
+    MG_LAUNCH_CHECK();
+    vpp.resize((size_t)nv + 1);
+    scan_exclusive<int32_t>(pcnt.p, vpp.p, nv, s);
+    const int64_t npairs = read_scalar(vpp.p + nv, s);
+    pst.resize(npairs + 1); pagg.resize(npairs); ccnt.resize(nv);
+    k_va_pairs<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vl2.p, agg, vpp.p, pst.p, pagg.p, ccnt.p);
+    MG_LAUNCH_CHECK();
+    cnt.resize(n_agg);
+    MG_CK(cudaMemsetAsync(cnt.p, 0, sizeof(int32_t) * (size_t)n_agg, s));
+    k_pat_count<<<g1(nv), 256, 0, s>>>(nv, vpp.p, pagg.p, cnt.p);
+    MG_LAUNCH_CHECK();
+    ptr.resize((size_t)n_agg + 1);
+    scan_exclusive<int32_t>(cnt.p, ptr.p, n_agg, s);
+    const int64_t ncand = read_scalar(ptr.p + n_agg, s);
+    cand.resize(ncand);
+    cur.resize(n_agg);
+    MG_CK(cudaMemsetAsync(cur.p, 0, sizeof(int32_t) * (size_t)n_agg, s));
+    k_pat_fill<<<g1(nv), 256, 0, s>>>(nv, vpp.p, pagg.p, ptr.p, cur.p, cand.p);
+    MG_LAUNCH_CHECK();
+    sort_segments_i32(ptr.p, cand.p, n_agg, s);
+    ucnt.resize(n_agg);
+    k_pat_unique<<<g1(n_agg), 256, 0, s>>>(n_agg, ptr.p, cand.p, ucnt.p, nullptr, nullptr);
+    MG_LAUNCH_CHECK();
+    crowptr.resize((size_t)n_agg + 1);
+    scan_exclusive<int32_t>(ucnt.p, crowptr.p, n_agg, s);
+    ccol.resize(read_scalar(crowptr.p + n_agg, s));
+    k_pat_unique<<<g1(n_agg), 256, 0, s>>>(n_agg, ptr.p, cand.p, nullptr, crowptr.p, ccol.p);
+    MG_LAUNCH_CHECK();
+    MG_CK(cudaStreamSynchronize(s));  // temporaries are freed on return
+}
+
+void va_at(int32_t m, const double* alpha, double dt, double* at, cudaStream_t s) {
+    if (!m) return;
+    k_va_at<<<g1(m), 256, 0, s>>>(m, alpha, dt * dt, at);
+    MG_LAUNCH_CHECK();
+}
 
 void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg, int32_t n_agg,
                  const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s) {

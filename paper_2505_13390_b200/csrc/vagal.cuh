@@ -23,7 +23,17 @@ struct VaPlan {
     DBuf<double> dterm;     // n_agg: sum_{i in a} P_i^2 at_i
 };
 
-// Setup time, after aggregation and galerkin_symbolic of level 0.
+// Setup time: the coarse pattern of A_1 = P^T A_0 P from the mesh alone — (a, b) is an entry iff some
+// vertex is touched by members of both aggregates (reading c14: A_ij != 0 iff constraints i, j share a
+// vertex) — off-diagonals ascending, diagonal last; replaces galerkin_symbolic of level 0 when the
+// hot loop is matrix-free.
+void va_coarse_pattern(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg,
+                       int32_t n_agg, DBuf<int64_t>& crowptr, DBuf<int32_t>& ccol, cudaStream_t s);
+
+// at_i = alpha_i / dt^2 (fp64, all rows) for the setup-time product
+void va_at(int32_t m, const double* alpha, double dt, double* at, cudaStream_t s);
+
+// Setup time, after aggregation and the coarse pattern of level 1.
 void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg, int32_t n_agg,
                  const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s);
 

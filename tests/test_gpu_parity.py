@@ -160,6 +160,30 @@ def test_galerkin_from_gradients_level1(name):
     assert np.abs(vg - vo).max() <= 1e-12 * np.abs(vo).max()
 
 
+@pytest.mark.parametrize("name", ["cloth64", "bar3k", "block_small"])
+def test_setup_galerkin_vertex_aggregate_equals_csr(name, monkeypatch):
+    """In matrix-free mode the setup's A_1 = P^T A_0 P (pattern and fp64 values) comes from the gradients
+    (csrc/vagal.cu va_coarse_pattern + va_numeric) instead of the CSR Galerkin plan; the hierarchy it
+    builds must be the one the CSR product builds (MGPBD_NO_VA_SETUP=1)."""
+    sc = make_scene(name)
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("MGPBD_NO_VA_SETUP", "1")
+        ctx = ctx_for(sc, level0_operator=1)
+        ctx.step(sc.dt, 1)   # setup at the first outer iteration, then the hot refreshes
+        nl = ctx.stats().n_levels
+        out.append((nl, [ctx.aggregates(l) for l in range(nl - 1)], [ctx.level(l) for l in range(1, nl)]))
+        ctx.close()
+    (n0, a0, m0), (n1, a1, m1) = out
+    assert n0 == n1 and n0 > 1
+    for x, y in zip(a0, a1):
+        assert np.array_equal(x, y)
+    for (r0_, c0_, v0_), (r1_, c1_, v1_) in zip(m0, m1):
+        assert np.array_equal(r0_, r1_) and np.array_equal(c0_, c1_)
+        assert np.abs(v0_ - v1_).max() <= 1e-12 * np.abs(v1_).max()
+
+
 @pytest.mark.parametrize("precision", [0, 1])
 def test_matrix_free_equals_csr_frames(precision):
     sc = scenes.make("block_small")
