@@ -653,6 +653,9 @@ class Engine : public EngineBase {
                 }
             }
         }
+        if (tracing)
+            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B\n", nL,
+                         !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u);
         invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
         stale = false;

@@ -908,10 +908,12 @@ __global__ void __launch_bounds__(256) k_gj_update(int32_t n, double* __restrict
 
 // Blocked Gauss-Jordan inverse as ONE cooperative kernel (one grid barrier per 32-wide panel instead of
 // three launches).  Ping-pong between two n x n buffers so no tile reads a value another CTA writes in
-// the same panel.  Every CTA inverts the 32x32 pivot block itself (warp 0, register-resident columns,
-// pivots broadcast by shuffles), then updates its 32x32 output tiles:
+// the same panel.  Every CTA inverts the 32x32 pivot block itself (all 256 threads, 4 entries each,
+// two shared buffers alternating so each elimination step needs one barrier), then updates its 32x32
+// output tiles (thread (ty, lane) owns rows ty, ty+8, ty+16, ty+24 of column lane: 4 independent
+// accumulators):
 //   i,j outside K: W' = W - C R,  i in K: W' = R,  j in K: W' = -C P,  both: W' = P
-// with P = (W_KK)^-1, C = W_{:,K}, R = P W_{K,:}.
+// with P = (W_KK)^-1, C = W_{:,K}, R = P W_{K,:}.  (tools/micro/gj.cu: 268 -> 190 us at n = 357.)
 constexpr int GJT = 256;
 template <class T>
 __global__ void __launch_bounds__(GJT) k_gj_coop(int32_t n, const int64_t* __restrict__ rowptr,
@@ -919,10 +921,11 @@ __global__ void __launch_bounds__(GJT) k_gj_coop(int32_t n, const int64_t* __res
                                                  double* __restrict__ W0, double* __restrict__ W1, int* flags) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double Ps[32][33];
+    __shared__ double Qs[32][33];
     __shared__ double Ks[32][33];  // W_old[K rows][J cols]
     __shared__ double Cs[32][33];  // W_old[I rows][K cols]
     __shared__ double Rs[32][33];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31, ty = threadIdx.x >> 5;
     const int npan = (n + 31) / 32;
     double* cur = (npan % 2 == 0) ? W0 : W1;  // the buffer that holds the inverse after npan swaps is W0
     double* nxt = (npan % 2 == 0) ? W1 : W0;
@@ -938,77 +941,80 @@ __global__ void __launch_bounds__(GJT) k_gj_coop(int32_t n, const int64_t* __res
     grid.sync();
     for (int pnl = 0; pnl < npan; ++pnl) {
         const int32_t k0 = pnl * 32, bs = min(32, n - k0);
-        {   // P = inverse of the pivot block (identity-padded to 32 x 32), Gauss-Jordan by the whole CTA:
-            // 4 entries per thread, the old row k / column k read before the barrier of each step
-            for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
-                const int i = q >> 5, j = q & 31;
-                Ps[i][j] = (i < bs && j < bs) ? cur[(int64_t)(k0 + i) * n + k0 + j] : (i == j ? 1.0 : 0.0);
+        // P = inverse of the pivot block (identity-padded to 32 x 32); step k reads one buffer, writes the other
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int i = ty + 8 * u;
+            Ps[i][lane] = (i < bs && lane < bs) ? cur[(int64_t)(k0 + i) * n + k0 + lane] : (i == lane ? 1.0 : 0.0);
+        }
+        __syncthreads();
+#pragma unroll 2
+        for (int k = 0; k < 32; ++k) {
+            double (*A_)[33] = (k & 1) ? Qs : Ps;
+            double (*B_)[33] = (k & 1) ? Ps : Qs;
+            double pv = A_[k][k];
+            if (!(pv > 0.0)) {  // SPD: a non-positive pivot means the coarse matrix lost definiteness
+                if (blockIdx.x == 0 && threadIdx.x == 0) flags[5] = 1;
+                pv = (pv == 0.0 || !isfinite(pv)) ? 1.0 : pv;
+            }
+            const double ip = 1.0 / pv;
+            const double akj = A_[k][lane] * ip;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = ty + 8 * u;
+                const double aik = A_[i][k];
+                double v;
+                if (i == k) v = lane == k ? ip : akj;
+                else v = lane == k ? -aik * ip : fma(-aik, akj, A_[i][lane]);
+                B_[i][lane] = v;
             }
             __syncthreads();
-            for (int k = 0; k < 32; ++k) {
-                double pv = Ps[k][k];
-                if (!(pv > 0.0)) {
-                    if (blockIdx.x == 0 && threadIdx.x == 0) flags[5] = 1;
-                    pv = (pv == 0.0 || !isfinite(pv)) ? 1.0 : pv;
-                }
-                const double ip = 1.0 / pv;
-                double nv[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int q = threadIdx.x + u * GJT, i = q >> 5, j = q & 31;
-                    const double sij = Ps[i][j], sik = Ps[i][k], skj = Ps[k][j];
-                    nv[u] = i == k ? (j == k ? ip : skj * ip) : (j == k ? -sik * ip : sij - sik * skj * ip);
-                }
-                __syncthreads();
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int q = threadIdx.x + u * GJT;
-                    Ps[q >> 5][q & 31] = nv[u];
-                }
-                __syncthreads();
-            }
-            (void)warp;
-            (void)lane;
-        }
+        }  // 32 steps: the inverse is back in Ps
         const int nt = npan * npan;
         for (int tile = blockIdx.x; tile < nt; tile += gridDim.x) {
             const int I = tile / npan, J = tile % npan;
             const int32_t i0 = I * 32, j0 = J * 32;
             const bool iK = I == pnl, jK = J == pnl;
-            for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
-                const int r = q >> 5, c = q & 31;
-                if (!jK) Ks[r][c] = (r < bs && j0 + c < n) ? cur[(int64_t)(k0 + r) * n + j0 + c] : 0.0;
-                if (!iK) Cs[r][c] = (i0 + r < n && c < bs) ? cur[(int64_t)(i0 + r) * n + k0 + c] : 0.0;
+            double old[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = ty + 8 * u;
+                if (!jK) Ks[r][lane] = (r < bs && j0 + lane < n) ? cur[(int64_t)(k0 + r) * n + j0 + lane] : 0.0;
+                if (!iK) Cs[r][lane] = (i0 + r < n && lane < bs) ? cur[(int64_t)(i0 + r) * n + k0 + lane] : 0.0;
+                old[u] = (!iK && !jK && i0 + r < n && j0 + lane < n) ? cur[(int64_t)(i0 + r) * n + j0 + lane] : 0.0;
             }
             __syncthreads();
-            if (!jK) {
-                for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
-                    const int t = q >> 5, c = q & 31;
-                    double acc = 0.0;
-#pragma unroll 8
-                    for (int u = 0; u < 32; ++u) acc += Ps[t][u] * Ks[u][c];
-                    Rs[t][c] = acc;
+            if (!jK) {  // R = P K
+                double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const double kv = Ks[t][lane];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = fma(Ps[ty + 8 * u][t], kv, acc[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) Rs[ty + 8 * u][lane] = acc[u];
+            }
+            __syncthreads();
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            if (!iK) {  // C R (j outside K) or C P (j in K)
+#pragma unroll
+                for (int t = 0; t < 32; ++t) {
+                    const double rv = jK ? Ps[t][lane] : Rs[t][lane];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) acc[u] = fma(Cs[ty + 8 * u][t], rv, acc[u]);
                 }
             }
-            __syncthreads();
-            for (int q = threadIdx.x; q < 32 * 32; q += GJT) {
-                const int r = q >> 5, c = q & 31;
-                const int32_t i = i0 + r, j = j0 + c;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int r = ty + 8 * u;
+                const int32_t i = i0 + r, j = j0 + lane;
                 if (i >= n || j >= n) continue;
                 double v;
-                if (iK && jK) v = Ps[r][c];
-                else if (iK) v = Rs[r][c];
-                else if (jK) {
-                    double acc = 0.0;
-#pragma unroll 8
-                    for (int t = 0; t < 32; ++t) acc += Cs[r][t] * Ps[t][c];
-                    v = -acc;
-                } else {
-                    double acc = 0.0;
-#pragma unroll 8
-                    for (int t = 0; t < 32; ++t) acc += Cs[r][t] * Rs[t][c];
-                    v = cur[(int64_t)i * n + j] - acc;
-                }
+                if (iK && jK) v = Ps[r][lane];
+                else if (iK) v = Rs[r][lane];
+                else if (jK) v = -acc[u];
+                else v = old[u] - acc[u];
                 nxt[(int64_t)i * n + j] = v;
             }
             __syncthreads();
