@@ -549,9 +549,12 @@ class Engine : public EngineBase {
                 va_symbolic(nv, kc, vptr.p, vlist.p, a2.agg.p, na, c.rowptr, c.col, c.nnz, va, st);
                 at64.resize(m);
                 va_at(m, alpha.p, last_dt, at64.p, st);
-                va_numeric<double>(va, kc, h64.p, a2.P64.p, a2.mptr.p, a2.mlist.p, at64.p, na, c.rowptr, c.val64.p,
+                va_numeric<double>(va, kc, h64.p, nullptr, a2.P64.p, a2.mptr.p, a2.mlist.p, at64.p, na, c.rowptr, c.val64.p,
                                    c.dinv64.p, st);
                 va_built = true;
+                if (tracing)
+                    std::fprintf(stderr, "[mgpbd trace] VA plan: %lld (vertex, aggregate) pairs, %lld products, %lld coarse entries\n",
+                                 (long long)va.npairs, (long long)va.ncontrib, (long long)va.cnnz);
                 trace("va_symbolic+numeric", l);
             } else {
                 a2.tval64.resize(a2.plan.T);
@@ -683,7 +686,8 @@ class Engine : public EngineBase {
             Level& a = *L[l];
             Level& c = *L[l + 1];
             if (l == 0 && va_ok && mf_on()) {  // from h directly (replicated on every rank, no collective)
-                va_numeric<T>(va, kc, h.p, a.P.p, a.mptr.p, a.mlist.p, mf.at, a.n_agg, c.rowptr, c.val.p, c.dinv.p, st);
+                va_numeric<T>(va, kc, h.p, (mf.e0 == 0 && mf.e1 == mf.ninc) ? (const T*)mf.hv : nullptr, a.P.p, a.mptr.p,
+                              a.mlist.p, mf.at, a.n_agg, c.rowptr, c.val.p, c.dinv.p, st);
                 mark_stage(1);
                 continue;
             }

@@ -19,21 +19,25 @@ inline int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n
 // per vertex: incidences re-sorted by aggregate (stable: codes stay ascending inside an aggregate),
 // number of distinct aggregates
 __global__ void k_va_sort(int32_t nv, int kc, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vlist,
-                          const int32_t* __restrict__ agg, int32_t* __restrict__ vlist2, int32_t* __restrict__ pcnt) {
+                          const int32_t* __restrict__ agg, int32_t* __restrict__ vlist2, int32_t* __restrict__ vpos,
+                          int32_t* __restrict__ pcnt) {
     for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
         const int64_t e0 = vptr[v], e1 = vptr[v + 1];
-        for (int64_t e = e0; e < e1; ++e) vlist2[e] = vlist[e];
+        for (int64_t e = e0; e < e1; ++e) { vlist2[e] = vlist[e]; if (vpos) vpos[e] = (int32_t)e; }
         for (int64_t a = e0 + 1; a < e1; ++a) {
             const int32_t c = vlist2[a];
+            const int32_t pa = vpos ? vpos[a] : 0;
             const int32_t ka = agg[c / kc];
             int64_t b = a - 1;
             while (b >= e0) {
                 const int32_t cb = vlist2[b];
                 if (agg[cb / kc] <= ka) break;
                 vlist2[b + 1] = cb;
+                if (vpos) vpos[b + 1] = vpos[b];
                 --b;
             }
             vlist2[b + 1] = c;
+            if (vpos) vpos[b + 1] = pa;
         }
         int32_t pc = 0, prev = -1;
         for (int64_t e = e0; e < e1; ++e) {
@@ -98,15 +102,23 @@ __global__ void k_va_permute(int64_t n, const int32_t* __restrict__ list, const 
         out[k] = in[list[k]];
 }
 
-__global__ void k_va_erow(int32_t n, const int64_t* __restrict__ crowptr, int32_t* __restrict__ erow) {
-    for (int32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x)
-        for (int64_t k = crowptr[a]; k < crowptr[a + 1]; ++k) erow[k] = a;
+// product range of every off-diagonal entry; empty for the diagonal (k_va_a1_diag computes it)
+__global__ void k_va_crange(int32_t n, const int64_t* __restrict__ crowptr, const int64_t* __restrict__ cptr,
+                            int2* __restrict__ crange) {
+    for (int32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n; a += gridDim.x * blockDim.x) {
+        const int64_t k1 = crowptr[a + 1] - 1;
+        for (int64_t k = crowptr[a]; k < k1; ++k) crange[k] = make_int2((int32_t)cptr[k], (int32_t)cptr[k + 1]);
+        crange[k1] = make_int2(0, 0);
+    }
 }
 
 // G_p = sum over the pair's incidences of P_j h_{j,s} (fp64 sum, incidence order)
-template <class T, int KC>
+// (HV: h read from the vertex-major copy hv of the matrix-free operator — the pair's incidences are
+// neighbours there, instead of one 12-byte record per constraint scattered over h)
+template <class T, int KC, bool HV>
 __global__ void k_va_g(int64_t npairs, const int32_t* __restrict__ pstart, const int32_t* __restrict__ vlist2,
-                       const T* __restrict__ h, const T* __restrict__ P, G4<T>* __restrict__ G) {
+                       const int32_t* __restrict__ vpos, const T* __restrict__ h, const T* __restrict__ hv,
+                       int64_t ninc, const T* __restrict__ P, G4<T>* __restrict__ G) {
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs; p += (int64_t)gridDim.x * blockDim.x) {
         double g0 = 0.0, g1_ = 0.0, g2 = 0.0;
         const int32_t e0 = pstart[p], e1 = pstart[p + 1];
@@ -116,14 +128,28 @@ __global__ void k_va_g(int64_t npairs, const int32_t* __restrict__ pstart, const
 #pragma unroll
             for (int q = 0; q < 4; ++q) code[q] = eb + q < e1 ? vlist2[eb + q] : -1;
             double pj[4], hx[4], hy[4], hz[4];
+            if (HV) {
+                int32_t pos[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const bool in = code[q] >= 0;
-                const T* hh = h + (int64_t)(in ? code[q] : 0) * 3;
-                pj[q] = in ? (double)P[code[q] / KC] : 0.0;
-                hx[q] = in ? (double)hh[0] : 0.0;
-                hy[q] = in ? (double)hh[1] : 0.0;
-                hz[q] = in ? (double)hh[2] : 0.0;
+                for (int q = 0; q < 4; ++q) pos[q] = eb + q < e1 ? vpos[eb + q] : 0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool in = code[q] >= 0;
+                    pj[q] = in ? (double)P[code[q] / KC] : 0.0;
+                    hx[q] = in ? (double)hv[pos[q]] : 0.0;
+                    hy[q] = in ? (double)hv[ninc + pos[q]] : 0.0;
+                    hz[q] = in ? (double)hv[2 * ninc + pos[q]] : 0.0;
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const bool in = code[q] >= 0;
+                    const T* hh = h + (int64_t)(in ? code[q] : 0) * 3;
+                    pj[q] = in ? (double)P[code[q] / KC] : 0.0;
+                    hx[q] = in ? (double)hh[0] : 0.0;
+                    hy[q] = in ? (double)hh[1] : 0.0;
+                    hz[q] = in ? (double)hh[2] : 0.0;
+                }
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -136,32 +162,19 @@ __global__ void k_va_g(int64_t npairs, const int32_t* __restrict__ pstart, const
     }
 }
 
+// Off-diagonal entries (A_1)_ab: one thread each over the entry's product range (chunks of 4: all
+// (p, q) loads, then all G gathers, then the sums in order).
 template <class T>
-__global__ void k_va_dterm(int32_t n_agg, const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
-                           const T* __restrict__ P, const T* __restrict__ at, double* __restrict__ dterm) {
-    for (int32_t a = blockIdx.x * blockDim.x + threadIdx.x; a < n_agg; a += gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int64_t k = mptr[a]; k < mptr[a + 1]; ++k) {
-            const int32_t i = mlist[k];
-            const double pi = (double)P[i];
-            s += pi * pi * (double)at[i];
-        }
-        dterm[a] = s;
-    }
-}
-
-template <class T>
-__global__ void k_va_a1(int64_t cnnz, const int64_t* __restrict__ cptr, const int2* __restrict__ cpq,
-                        const G4<T>* __restrict__ G, const int32_t* __restrict__ erow,
-                        const int64_t* __restrict__ crowptr, const double* __restrict__ dterm, T* __restrict__ cval) {
+__global__ void k_va_a1(int64_t cnnz, const int2* __restrict__ crange, const int2* __restrict__ cpq,
+                        const G4<T>* __restrict__ G, T* __restrict__ cval) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < cnnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int2 rg = crange[k];
+        if (rg.x == rg.y) continue;  // diagonal: k_va_a1_diag
         double s = 0.0;
-        const int64_t c0 = cptr[k], c1 = cptr[k + 1];
-        // chunks of 4 products: all (p, q) loads, then all G gathers, then the sums (in order)
-        for (int64_t cb = c0; cb < c1; cb += 4) {
+        for (int32_t cb = rg.x; cb < rg.y; cb += 4) {
             int2 pq[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) pq[u] = cb + u < c1 ? cpq[cb + u] : make_int2(-1, -1);
+            for (int u = 0; u < 4; ++u) pq[u] = cb + u < rg.y ? cpq[cb + u] : make_int2(-1, -1);
             G4<T> a[4], b[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -173,9 +186,54 @@ __global__ void k_va_a1(int64_t cnnz, const int64_t* __restrict__ cptr, const in
             for (int u = 0; u < 4; ++u)
                 s += (double)a[u].x * (double)b[u].x + (double)a[u].y * (double)b[u].y + (double)a[u].z * (double)b[u].z;
         }
-        const int32_t r = erow[k];
-        if (k == crowptr[r + 1] - 1) s += dterm[r];
         cval[k] = (T)s;
+    }
+}
+
+// Diagonal entries (A_1)_aa: one warp per aggregate (the diagonal collects a product from every vertex
+// the aggregate touches, ~10-50x the work of an off-diagonal entry; thread-per-entry left whole warps
+// waiting on it).  Lane-strided chunks of 4 products + the aggregate's sum_i P_i^2 at_i, fixed-order
+// butterfly (deterministic); writes the smoother's 1/(A_1)_aa as well.
+template <class T>
+__global__ void k_va_a1_diag(int32_t n_agg, const int64_t* __restrict__ cptr, const int2* __restrict__ cpq,
+                             const G4<T>* __restrict__ G, const int64_t* __restrict__ crowptr,
+                             const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
+                             const T* __restrict__ P, const T* __restrict__ at, T* __restrict__ cval,
+                             T* __restrict__ cdinv) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t a = gw; a < n_agg; a += nw) {
+        const int64_t k = crowptr[a + 1] - 1;
+        const int64_t c0 = cptr[k], c1 = cptr[k + 1];
+        double s = 0.0;
+        for (int64_t cb = c0 + lane; cb < c1; cb += 4 * 32) {
+            int2 pq[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pq[u] = cb + 32 * u < c1 ? cpq[cb + 32 * u] : make_int2(-1, -1);
+            G4<T> x[4], y[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const bool in = pq[u].x >= 0;
+                x[u] = in ? G[pq[u].x] : G4<T>{(T)0, (T)0, (T)0, (T)0};
+                y[u] = in ? G[pq[u].y] : G4<T>{(T)0, (T)0, (T)0, (T)0};
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                s += (double)x[u].x * (double)y[u].x + (double)x[u].y * (double)y[u].y + (double)x[u].z * (double)y[u].z;
+        }
+        for (int64_t e = mptr[a] + lane; e < mptr[a + 1]; e += 32) {  // sum_{i in a} P_i^2 at_i
+            const int32_t i = mlist[e];
+            const double pi = (double)P[i];
+            s += pi * pi * (double)at[i];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            const T d = (T)s;
+            cval[k] = d;
+            cdinv[a] = (T)(1.0 / (double)d);
+        }
     }
 }
 
@@ -230,7 +288,7 @@ void va_coarse_pattern(int32_t nv, int kc, const int64_t* vptr, const int32_t* v
     DBuf<int64_t> vpp, ptr;
     vl2.resize(ninc);
     pcnt.resize(nv);
-    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, vl2.p, pcnt.p);
+    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, vl2.p, nullptr, pcnt.p);
     MG_LAUNCH_CHECK();
     vpp.resize((size_t)nv + 1);
     scan_exclusive<int32_t>(pcnt.p, vpp.p, nv, s);
@@ -273,11 +331,13 @@ void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, 
     const int64_t ninc = read_scalar(vptr + nv, s);
     plan.cnnz = cnnz;
     plan.vlist2.resize(ninc);
+    plan.vpos.resize(ninc);
+    plan.ninc = ninc;
     DBuf<int32_t> pcnt, pagg, ccnt, key, clist, cnt;
     DBuf<int64_t> vpp, coff;
     DBuf<int2> pq;
     pcnt.resize(nv);
-    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, plan.vlist2.p, pcnt.p);
+    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, plan.vlist2.p, plan.vpos.p, pcnt.p);
     MG_LAUNCH_CHECK();
     vpp.resize((size_t)nv + 1);
     scan_exclusive<int32_t>(pcnt.p, vpp.p, nv, s);
@@ -304,34 +364,40 @@ void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, 
     plan.cpq.resize(plan.ncontrib);
     k_va_permute<<<g1(plan.ncontrib), 256, 0, s>>>(plan.ncontrib, clist.p, pq.p, plan.cpq.p);
     MG_LAUNCH_CHECK();
-    plan.erow.resize(cnnz);
-    k_va_erow<<<g1(n_agg), 256, 0, s>>>(n_agg, crowptr, plan.erow.p);
+    if (plan.ncontrib >= INT32_MAX) throw Error(-1, "va_symbolic: more than 2^31 products");
+    plan.crange.resize(cnnz);
+    k_va_crange<<<g1(n_agg), 256, 0, s>>>(n_agg, crowptr, plan.cptr.p, plan.crange.p);
     MG_LAUNCH_CHECK();
-    plan.dterm.resize(n_agg);
     plan.G.resize((size_t)plan.npairs * 4 * sizeof(double));  // either hot type (allocated outside capture)
     MG_CK(cudaStreamSynchronize(s));  // temporaries are freed on return
 }
 
 template <class T>
-void va_numeric(VaPlan& plan, int kc, const T* h, const T* P, const int64_t* mptr, const int32_t* mlist,
-                const T* at, int32_t n_agg, const int64_t* crowptr, T* cval, T* cdinv, cudaStream_t s) {
+void va_numeric(VaPlan& plan, int kc, const T* h, const T* hv, const T* P, const int64_t* mptr,
+                const int32_t* mlist, const T* at, int32_t n_agg, const int64_t* crowptr, T* cval, T* cdinv,
+                cudaStream_t s) {
     G4<T>* G = reinterpret_cast<G4<T>*>(plan.G.p);
     if (plan.npairs) {
-        if (kc == 4) k_va_g<T, 4><<<g1(plan.npairs), 256, 0, s>>>(plan.npairs, plan.pstart.p, plan.vlist2.p, h, P, G);
-        else k_va_g<T, 2><<<g1(plan.npairs), 256, 0, s>>>(plan.npairs, plan.pstart.p, plan.vlist2.p, h, P, G);
+#define MG_VAG(KC, HV)                                                                                      \
+    k_va_g<T, KC, HV><<<g1(plan.npairs), 256, 0, s>>>(plan.npairs, plan.pstart.p, plan.vlist2.p, plan.vpos.p, h, \
+                                                      hv, plan.ninc, P, G)
+        if (kc == 4) { if (hv) MG_VAG(4, true); else MG_VAG(4, false); }
+        else { if (hv) MG_VAG(2, true); else MG_VAG(2, false); }
+#undef MG_VAG
         MG_LAUNCH_CHECK();
     }
-    k_va_dterm<T><<<g1(n_agg), 256, 0, s>>>(n_agg, mptr, mlist, P, at, plan.dterm.p);
+    k_va_a1<T><<<g1(plan.cnnz), 256, 0, s>>>(plan.cnnz, plan.crange.p, plan.cpq.p, G, cval);
     MG_LAUNCH_CHECK();
-    k_va_a1<T><<<g1(plan.cnnz), 256, 0, s>>>(plan.cnnz, plan.cptr.p, plan.cpq.p, G, plan.erow.p, crowptr,
-                                             plan.dterm.p, cval);
-    MG_LAUNCH_CHECK();
-    diag_inv<T>(n_agg, crowptr, cval, cdinv, s);
+    if (n_agg) {
+        k_va_a1_diag<T><<<(int)std::min<int64_t>(((int64_t)n_agg * 32 + 255) / 256, 148 * 16), 256, 0, s>>>(
+            n_agg, plan.cptr.p, plan.cpq.p, G, crowptr, mptr, mlist, P, at, cval, cdinv);
+        MG_LAUNCH_CHECK();
+    }
 }
 
-template void va_numeric<float>(VaPlan&, int, const float*, const float*, const int64_t*, const int32_t*,
+template void va_numeric<float>(VaPlan&, int, const float*, const float*, const float*, const int64_t*, const int32_t*,
                                 const float*, int32_t, const int64_t*, float*, float*, cudaStream_t);
-template void va_numeric<double>(VaPlan&, int, const double*, const double*, const int64_t*, const int32_t*,
+template void va_numeric<double>(VaPlan&, int, const double*, const double*, const double*, const int64_t*, const int32_t*,
                                  const double*, int32_t, const int64_t*, double*, double*, cudaStream_t);
 
 }  // namespace mgpbd

@@ -5,22 +5,23 @@
 // diag(at) (reading c14) and the aggregate-wise prolongator (k = 1, reading c6):
 //   G_{a,v}  = sum_{i in a, v in verts(i)} P_i h_{i,v}                       (3-vector per (vertex, aggregate) pair)
 //   (A_1)_ab = sum_v G_{a,v} . G_{b,v}  +  [a == b] sum_{i in a} P_i^2 at_i
-// which is P^T A_0 P exactly (up to rounding order).  The pattern of A_1 is the one galerkin_symbolic
-// built; a setup-time plan maps every (v, a, b) product to its coarse entry.
+// which is P^T A_0 P exactly (up to rounding order).  The pattern of A_1 is the one va_coarse_pattern
+// (or galerkin_symbolic) built; a setup-time plan maps every (v, a, b) product to its coarse entry.
+// Off-diagonal entries: one thread each; diagonal entries (10-50x the products): one warp each.
 #pragma once
 #include "common.cuh"
 
 namespace mgpbd {
 
 struct VaPlan {
-    int64_t npairs = 0, ncontrib = 0, cnnz = 0;
+    int64_t npairs = 0, ncontrib = 0, cnnz = 0, ninc = 0;
     DBuf<int32_t> vlist2;   // incidence codes (constraint*kc + slot) per vertex sorted by (agg, code)
+    DBuf<int32_t> vpos;     // ninc: position in vlist (and in the matrix-free hv planes) of vlist2[e]
     DBuf<int32_t> pstart;   // npairs + 1: incidence range of (vertex, aggregate) pair p in vlist2
     DBuf<int64_t> cptr;     // cnnz + 1: products of coarse entry k
     DBuf<int2> cpq;         // ncontrib: (p, q) pair indices, grouped by coarse entry, ascending (v, p, q)
-    DBuf<int32_t> erow;     // cnnz: coarse row of entry k
+    DBuf<int2> crange;      // cnnz: product range of off-diagonal entry k in cpq; (0, 0) for diagonals
     DBuf<unsigned char> G;  // npairs x 4 values of the hot type
-    DBuf<double> dterm;     // n_agg: sum_{i in a} P_i^2 at_i
 };
 
 // Setup time: the coarse pattern of A_1 = P^T A_0 P from the mesh alone — (a, b) is an entry iff some
@@ -38,9 +39,11 @@ void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, 
                  const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s);
 
 // Every outer iteration: cval = A_1 values from the current h (m x kc x 3), P and at = alpha/dt^2 (all
-// m rows); cdinv = 1/diag.  No allocation (graph-capturable).
+// m rows); cdinv = 1/diag.  hv (optional, nullptr = read h): the matrix-free operator's vertex-major
+// copy of h over ALL incidences (single-rank layout).  No allocation (graph-capturable).
 template <class T>
-void va_numeric(VaPlan& plan, int kc, const T* h, const T* P, const int64_t* mptr, const int32_t* mlist,
-                const T* at, int32_t n_agg, const int64_t* crowptr, T* cval, T* cdinv, cudaStream_t s);
+void va_numeric(VaPlan& plan, int kc, const T* h, const T* hv, const T* P, const int64_t* mptr,
+                const int32_t* mlist, const T* at, int32_t n_agg, const int64_t* crowptr, T* cval, T* cdinv,
+                cudaStream_t s);
 
 }  // namespace mgpbd
