@@ -504,7 +504,16 @@ class Engine : public EngineBase {
                 }
                 const DBuf<int32_t>& col_ = colours0;
                 B.resize(a.n);
-                gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed, B.p, st);
+                GsOperator gop;
+                const bool gs_mf = cfg.level0_operator == 1 && mf_ready && h64.n && !va_off;
+                if (gs_mf) {  // the sweeps through H H^T + diag(at) (fp64 setup values)
+                    at64.resize(m);
+                    va_at(m, alpha.p, last_dt, at64.p, st);
+                    gop.kc = kc; gop.nv = nv; gop.verts = verts.p; gop.h = h64.p; gop.vptr = vptr.p;
+                    gop.vlist = vlist.p; gop.at = at64.p; gop.dinv = a.dinv64.p;
+                }
+                gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed, B.p, st,
+                             gs_mf ? &gop : nullptr);
                 d2d(B0.p, B.p, a.n, st);
                 trace("gs_bootstrap", l);
             }
@@ -547,8 +556,6 @@ class Engine : public EngineBase {
             c.val64.resize(c.nnz); c.dinv64.resize(c.n);
             if (va_setup) {
                 va_symbolic(nv, kc, vptr.p, vlist.p, a2.agg.p, na, c.rowptr, c.col, c.nnz, va, st);
-                at64.resize(m);
-                va_at(m, alpha.p, last_dt, at64.p, st);
                 va_numeric<double>(va, kc, h64.p, nullptr, a2.P64.p, a2.mptr.p, a2.mlist.p, at64.p, na, c.rowptr, c.val64.p,
                                    c.dinv64.p, st);
                 va_built = true;

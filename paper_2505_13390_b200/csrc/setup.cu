@@ -211,6 +211,52 @@ __global__ void k_gs_colour(int64_t cnt, const int32_t* __restrict__ rows, const
         if (lane == 0) x[i] = -s / val[e1];
     }
 }
+// u_v = sum over v's incidences (constraint j, slot s) of h_{j,s} x_j (fp64, incidence order)
+__global__ void k_gs_u(int32_t nv, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vlist, int kc,
+                       const double* __restrict__ h, const double* __restrict__ x, double* __restrict__ u) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
+        double a = 0.0, b = 0.0, c = 0.0;
+        for (int64_t e = vptr[v]; e < vptr[v + 1]; ++e) {
+            const int32_t code = vlist[e];
+            const double xj = x[code / kc];
+            a += h[(int64_t)code * 3] * xj;
+            b += h[(int64_t)code * 3 + 1] * xj;
+            c += h[(int64_t)code * 3 + 2] * xj;
+        }
+        u[3 * (int64_t)v] = a; u[3 * (int64_t)v + 1] = b; u[3 * (int64_t)v + 2] = c;
+    }
+}
+// one colour of a matrix-free GS sweep (b = 0), thread per row
+template <int KC>
+__global__ void k_gs_colour_mf(int64_t cnt, const int32_t* __restrict__ rows, const int32_t* __restrict__ verts,
+                               const double* __restrict__ h, const double* __restrict__ at,
+                               const double* __restrict__ dinv, double* __restrict__ x, double* __restrict__ u) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < cnt; t += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = rows[t];
+        int32_t v[KC];
+        double hh[KC][3];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            v[k] = verts[(int64_t)i * KC + k];
+#pragma unroll
+            for (int d = 0; d < 3; ++d) hh[k][d] = h[((int64_t)i * KC + k) * 3 + d];
+        }
+        const double xi = x[i];
+        double ax = at[i] * xi;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const double* uv = u + 3 * (int64_t)v[k];
+            ax += hh[k][0] * uv[0] + hh[k][1] * uv[1] + hh[k][2] * uv[2];
+        }
+        const double dx = -ax * dinv[i];
+        x[i] = xi + dx;
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            double* uv = u + 3 * (int64_t)v[k];
+            uv[0] += hh[k][0] * dx; uv[1] += hh[k][1] * dx; uv[2] += hh[k][2] * dx;
+        }
+    }
+}
 __global__ void k_fill_d(int32_t n, double* x, double v) {
     int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) x[i] = v;
@@ -486,7 +532,7 @@ int32_t colour(int32_t n, const int64_t* rowptr, const int32_t* col, uint64_t se
 }
 
 void gs_bootstrap(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, const int32_t* colours,
-                  int32_t ncolours, int32_t sweeps, uint64_t seed, double* B, cudaStream_t s) {
+                  int32_t ncolours, int32_t sweeps, uint64_t seed, double* B, cudaStream_t s, const GsOperator* op) {
     int64_t nnz = read_scalar(rowptr + n, s);
     DBuf<double> parts, mx;
     parts.resize(1024); mx.resize(2);
@@ -500,11 +546,25 @@ void gs_bootstrap(int32_t n, const int64_t* rowptr, const int32_t* col, const do
     std::vector<int64_t> hptr(ncolours + 1);
     d2h(hptr.data(), cptr.p, ncolours + 1, s);
     MG_CK(cudaStreamSynchronize(s));
+    DBuf<double> u;
+    if (op) {
+        u.resize(3 * (size_t)op->nv);
+        k_gs_u<<<g1(op->nv), 256, 0, s>>>(op->nv, op->vptr, op->vlist, op->kc, op->h, B, u.p);
+        MG_LAUNCH_CHECK();
+    }
     for (int sw = 0; sw < sweeps; ++sw)
         for (int c = 0; c < ncolours; ++c) {
             int64_t cntc = hptr[c + 1] - hptr[c];
             if (!cntc) continue;
-            k_gs_colour<<<gw(cntc), 256, 0, s>>>(cntc, clist.p + hptr[c], rowptr, col, val, B);
+            if (op) {
+                const int g = (int)std::min<int64_t>((cntc + 127) / 128, 148 * 16);
+                if (op->kc == 4)
+                    k_gs_colour_mf<4><<<g, 128, 0, s>>>(cntc, clist.p + hptr[c], op->verts, op->h, op->at, op->dinv, B, u.p);
+                else
+                    k_gs_colour_mf<2><<<g, 128, 0, s>>>(cntc, clist.p + hptr[c], op->verts, op->h, op->at, op->dinv, B, u.p);
+            } else {
+                k_gs_colour<<<gw(cntc), 256, 0, s>>>(cntc, clist.p + hptr[c], rowptr, col, val, B);
+            }
             MG_LAUNCH_CHECK();
         }
     dot_parts<double>(n, B, B, parts.p, 1024, s);
