@@ -1,8 +1,12 @@
 // AMG setup kernels and the Galerkin product (see setup.cuh).
 #include <climits>
+#include <cstdlib>
+#include <cooperative_groups.h>
 
 #include "setup.cuh"
 #include "util.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace mgpbd {
 namespace {
@@ -692,8 +696,88 @@ double power_method_op(int32_t n, int dot_grid, const std::function<int(const do
     return iters > 0 ? sqrt(lam2) : 0.0;
 }
 
+namespace {
+// The whole power method of a coarse level in one cooperative launch: per iteration one phase computing
+// w = D^-1 A v (warp per row) with per-CTA partials of |w|^2, a grid barrier, every CTA summing the
+// partials in the same fixed order, v = w / |w| over its rows, a barrier.  Same arithmetic as the
+// launch-per-step version (k_power_init, PASS_POWER, k_finalize_sum, k_scale); ~3 launches per
+// iteration (~1.4 ms per level at 100 iterations) become ~2 barriers per iteration.
+constexpr int PWT = 512;
+__device__ __forceinline__ double pw_total(const double* __restrict__ parts, int np, double* sh) {
+    double v = 0.0;
+    for (int i = threadIdx.x; i < np; i += PWT) v += parts[i];
+    return block_sum<PWT>(v, sh);
+}
+__global__ void __launch_bounds__(PWT) k_power_coop(int32_t n, const int64_t* __restrict__ rowptr,
+                                                    const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                    const double* __restrict__ dinv, int32_t iters, uint64_t base,
+                                                    double* __restrict__ v, double* __restrict__ w,
+                                                    double* __restrict__ parts, double* __restrict__ out) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[32];
+    __shared__ double inv_s;
+    const int lane = threadIdx.x & 31;
+    const int64_t tid = (int64_t)blockIdx.x * PWT + threadIdx.x, nt = (int64_t)gridDim.x * PWT;
+    const int64_t gw = tid >> 5, nw = nt >> 5;
+    double acc = 0.0;
+    for (int64_t i = tid; i < n; i += nt) {
+        const double x = hunit(hkey(base, (uint64_t)i));
+        v[i] = x;
+        acc += x * x;
+    }
+    double t = block_sum<PWT>(acc, sh);
+    if (threadIdx.x == 0) parts[blockIdx.x] = t;
+    grid.sync();
+    double ss = pw_total(parts, gridDim.x, sh);
+    if (threadIdx.x == 0) { const double lam = sqrt(ss); inv_s = lam > 0.0 ? 1.0 / lam : 0.0; }
+    __syncthreads();
+    for (int64_t i = tid; i < n; i += nt) v[i] = v[i] * inv_s;
+    grid.sync();
+    for (int32_t it = 0; it < iters; ++it) {
+        acc = 0.0;
+        for (int64_t i = gw; i < n; i += nw) {
+            double s = 0.0;
+            for (int64_t e = rowptr[i] + lane; e < rowptr[i + 1]; e += 32) s += val[e] * v[col[e]];
+            s = group_sum<32>(s);
+            if (lane == 0) {
+                const double wi = dinv[i] * s;
+                w[i] = wi;
+                acc += wi * wi;
+            }
+        }
+        t = block_sum<PWT>(acc, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t;
+        grid.sync();
+        ss = pw_total(parts, gridDim.x, sh);
+        if (threadIdx.x == 0) { const double lam = sqrt(ss); inv_s = lam > 0.0 ? 1.0 / lam : 0.0; }
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += nt) v[i] = w[i] * inv_s;
+        grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *out = ss;
+}
+}  // namespace
+
 double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
                     double* parts, double* ss, cudaStream_t s) {
+    if (A.n > 0 && A.n <= (1 << 18) && std::getenv("MGPBD_NO_POWER_COOP") == nullptr) {
+        static const int grid = [] {
+            int dev = 0, sms = 0, occ = 0;
+            MG_CK(cudaGetDevice(&dev));
+            MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+            MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_power_coop, PWT, 0));
+            return sms * std::max(1, std::min(occ, 2));
+        }();
+        // parts holds >= 1024 doubles (the engine's partial-sum buffer)
+        const int g = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(grid, 1024), ((int64_t)A.n * 32 + PWT - 1) / PWT));
+        const uint64_t base = hkey_base(seed, 4, level);
+        void* args[] = {(void*)&A.n, (void*)&A.rowptr, (void*)&A.col, (void*)&A.val, (void*)&A.dinv,
+                        (void*)&iters, (void*)&base, (void*)&v, (void*)&w, (void*)&parts, (void*)&ss};
+        MG_CK(cudaLaunchCooperativeKernel((const void*)k_power_coop, g, PWT, args, 0, s));
+        MG_LAUNCH_CHECK();
+        const double lam2 = read_scalar(ss, s);
+        return iters > 0 ? sqrt(lam2) : 0.0;
+    }
     return power_method_op(
         A.n, A.grid,
         [&](const double* x, double* y, double* pp) {
