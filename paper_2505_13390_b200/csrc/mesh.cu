@@ -129,7 +129,6 @@ __global__ void k_pattern(const int32_t* __restrict__ verts, int32_t m, int kc, 
 }
 
 // ----------------------------------------------------------------------------- eval
-__device__ __forceinline__ double sgn1(double x) { return x >= 0.0 ? 1.0 : -1.0; }
 
 // Polar rotation of F via the symmetric eigen-decomposition F^T F = V L V^T
 // (cyclic Jacobi), sigma = sqrt(L), U = F V / sigma (completed by cross products when rank-deficient),
@@ -154,9 +153,12 @@ __device__ void polar_rotation(const double F[9], double R[9]) {
             const int p = t == 2 ? 1 : 0, q = t == 0 ? 1 : 2;
             double apq = S[p * 3 + q];
             if (apq == 0.0) continue;
-            double th = (S[q * 3 + q] - S[p * 3 + p]) / (2.0 * apq);
-            double tt = sgn1(th) / (fabs(th) + sqrt(th * th + 1.0));
-            double c = 1.0 / sqrt(tt * tt + 1.0), s = tt * c;
+            // t = sgn(th) / (|th| + sqrt(th^2 + 1)), th = u / v, multiplied through by |v|: one divide and
+            // one square root instead of two divides (the kernel is bound by the special-function unit)
+            const double u = S[q * 3 + q] - S[p * 3 + p], v = 2.0 * apq;
+            const double sg = (u == 0.0) ? 1.0 : ((u > 0.0) == (v > 0.0) ? 1.0 : -1.0);  // sgn1(u / v)
+            double tt = sg * fabs(v) / (fabs(u) + sqrt(u * u + v * v));
+            double c = rsqrt(tt * tt + 1.0), s = tt * c;  // 1/sqrt(.) within an ulp, no fp64 divide
             // S <- J^T S J with J = rotation in (p,q)
             for (int k = 0; k < 3; ++k) {
                 double skp = S[k * 3 + p], skq = S[k * 3 + q];
@@ -190,9 +192,11 @@ __device__ void polar_rotation(const double F[9], double R[9]) {
         double u0 = F[0] * Vs[k] + F[1] * Vs[3 + k] + F[2] * Vs[6 + k];
         double u1 = F[3] * Vs[k] + F[4] * Vs[3 + k] + F[5] * Vs[6 + k];
         double u2 = F[6] * Vs[k] + F[7] * Vs[3 + k] + F[8] * Vs[6 + k];
-        double nu = sqrt(u0 * u0 + u1 * u1 + u2 * u2);
+        const double n2 = u0 * u0 + u1 * u1 + u2 * u2;
+        const double rn = n2 > 0.0 ? rsqrt(n2) : 0.0;  // one special-function op instead of sqrt + 3 divides
+        const double nu = n2 * rn;
         if (nu > 1e-14 * sg[0] && rank == k) {
-            U[k] = u0 / nu; U[3 + k] = u1 / nu; U[6 + k] = u2 / nu;
+            U[k] = u0 * rn; U[3 + k] = u1 * rn; U[6 + k] = u2 * rn;
             rank = k + 1;
         }
     }
@@ -279,9 +283,19 @@ __global__ void __launch_bounds__(128, 8) k_eval_arap(int32_t m, const int32_t* 
             for (int r = 0; r < 3; ++r)
                 g[1 + c][r] = 2.0 * (E[r * 3] * Dm[c * 3] + E[r * 3 + 1] * Dm[c * 3 + 1] + E[r * 3 + 2] * Dm[c * 3 + 2]);
         for (int r = 0; r < 3; ++r) g[0][r] = -(g[1][r] + g[2][r] + g[3][r]);
+        T o[12];
         for (int k = 0; k < 4; ++k) {
             double sw = sqrtw[vv[k]];
-            for (int r = 0; r < 3; ++r) hj[3 * k + r] = (T)(sw * g[k][r]);
+            for (int r = 0; r < 3; ++r) o[3 * k + r] = (T)(sw * g[k][r]);
+        }
+        if (sizeof(T) == 4) {  // 48-byte record as three 16-byte stores (full sectors, no partial writes)
+            float4* d = reinterpret_cast<float4*>(hj);
+            d[0] = make_float4((float)o[0], (float)o[1], (float)o[2], (float)o[3]);
+            d[1] = make_float4((float)o[4], (float)o[5], (float)o[6], (float)o[7]);
+            d[2] = make_float4((float)o[8], (float)o[9], (float)o[10], (float)o[11]);
+        } else {
+            double2* d = reinterpret_cast<double2*>(hj);
+            for (int k = 0; k < 6; ++k) d[k] = make_double2((double)o[2 * k], (double)o[2 * k + 1]);
         }
     }
     b[j] = (T)(-C - (alpha[j] / dt2) * lambda[j]);
