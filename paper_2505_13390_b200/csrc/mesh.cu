@@ -153,12 +153,15 @@ __device__ void polar_rotation(const double F[9], double R[9]) {
             const int p = t == 2 ? 1 : 0, q = t == 0 ? 1 : 2;
             double apq = S[p * 3 + q];
             if (apq == 0.0) continue;
-            // t = sgn(th) / (|th| + sqrt(th^2 + 1)), th = u / v, multiplied through by |v|: one divide and
-            // one square root instead of two divides (the kernel is bound by the special-function unit)
+            // t = sgn(th) / (|th| + sqrt(th^2 + 1)) with th = u / v, c = 1 / sqrt(1 + t^2), s = t c, written
+            // with w = |u| + sqrt(u^2 + v^2): t = sgn |v| / w, c = w / sqrt(w^2 + v^2), s = sgn |v| / sqrt(.) —
+            // one sqrt and one rsqrt per rotation instead of two divides and two square roots (the kernel
+            // is bound by the special-function unit)
             const double u = S[q * 3 + q] - S[p * 3 + p], v = 2.0 * apq;
-            const double sg = (u == 0.0) ? 1.0 : ((u > 0.0) == (v > 0.0) ? 1.0 : -1.0);  // sgn1(u / v)
-            double tt = sg * fabs(v) / (fabs(u) + sqrt(u * u + v * v));
-            double c = rsqrt(tt * tt + 1.0), s = tt * c;  // 1/sqrt(.) within an ulp, no fp64 divide
+            const double sg = (u == 0.0) ? 1.0 : ((u > 0.0) == (v > 0.0) ? 1.0 : -1.0);  // sgn(th), +1 at 0
+            const double w = fabs(u) + sqrt(u * u + v * v);
+            const double iq = rsqrt(w * w + v * v);
+            const double c = w * iq, s = sg * fabs(v) * iq;
             // S <- J^T S J with J = rotation in (p,q)
             for (int k = 0; k < 3; ++k) {
                 double skp = S[k * 3 + p], skq = S[k * 3 + q];
