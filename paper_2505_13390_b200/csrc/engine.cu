@@ -860,7 +860,10 @@ class Engine : public EngineBase {
         mark_stage(4);
         timed(PH_UPD, [&] {
             if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
-            update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);  // l.9, l.11
+            if (mf_on() && !dist && mf.e0 == 0 && mf.e1 == mf.ninc)  // hv covers every incidence
+                mf_update<T>(mf, xs.p, sqrtw.p, omega_dev.p, x.p, st);                       // l.9, l.11
+            else
+                update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);
             lambda_add<T>(m, lambda.p, xs.p, st);                                                    // l.10
         });
         mark_stage(5);

@@ -105,6 +105,63 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
     }
 }
 
+// Eq. 5 position update from the vertex-major gradients: x_v += omega sqrt(w_v) sum_{(j,s) at v}
+// h_{j,s} dl_j, G lanes per vertex over the vertex's contiguous incidences in hv (coalesced planes
+// instead of one scattered 12-byte record per incidence), fp64 lane partials, fixed butterfly.
+template <class T, int KC, int G>
+__global__ void __launch_bounds__(MF_BS) k_mf_update(int32_t v0, int32_t v1, int64_t ninc,
+                                                     const int64_t* __restrict__ vptr,
+                                                     const int32_t* __restrict__ vlist, const T* __restrict__ hv,
+                                                     const T* __restrict__ dl, const double* __restrict__ sqrtw,
+                                                     const double* __restrict__ omega_p, double* __restrict__ x) {
+    constexpr int PER_WARP = 32 / G;
+    const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const T* __restrict__ hx = hv;
+    const T* __restrict__ hy = hv + ninc;
+    const T* __restrict__ hz = hv + 2 * ninc;
+    for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {  // warp-uniform
+        const int64_t v = base + sub;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        if (v < v1) {
+            constexpr int UN = 4;
+            const int64_t e0 = vptr[v], e1 = vptr[v + 1];
+            for (int64_t eb = e0 + sl; eb < e1; eb += G * UN) {
+                int32_t cj[UN];
+                T px[UN], py[UN], pz[UN];
+                double dv[UN];
+#pragma unroll
+                for (int q = 0; q < UN; ++q) {
+                    const int64_t e = eb + q * G;
+                    const bool in = e < e1;
+                    cj[q] = in ? vlist[e] / KC : -1;
+                    px[q] = in ? hx[e] : (T)0;
+                    py[q] = in ? hy[e] : (T)0;
+                    pz[q] = in ? hz[e] : (T)0;
+                }
+#pragma unroll
+                for (int q = 0; q < UN; ++q) dv[q] = cj[q] >= 0 ? (double)dl[cj[q]] : 0.0;
+#pragma unroll
+                for (int q = 0; q < UN; ++q) {
+                    a0 += (double)px[q] * dv[q];
+                    a1 += (double)py[q] * dv[q];
+                    a2 += (double)pz[q] * dv[q];
+                }
+            }
+        }
+        a0 = group_sum<G>(a0);
+        a1 = group_sum<G>(a1);
+        a2 = group_sum<G>(a2);
+        if (v < v1 && sl == 0) {
+            const double sw = sqrtw[v], om = *omega_p;
+            x[3 * v] += om * (sw * a0);
+            x[3 * v + 1] += om * (sw * a1);
+            x[3 * v + 2] += om * (sw * a2);
+        }
+    }
+}
+
 // (A x)_i = sum_s h_{i,s} . u_{v_s} + at_i x_i in the storage precision, epilogue in fp64 exactly as
 // the CSR row kernels (solve.cu k_rows).
 template <class T, int KC, int MODE>
@@ -389,7 +446,21 @@ void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const 
     else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev);
 }
 
+template <class T>
+void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const double* omega, double* x, cudaStream_t s) {
+    if (A.v1 <= A.v0) return;
+    constexpr int G = 4;
+    const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
+    const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * 16);
+    if (A.kc == 4)
+        k_mf_update<T, 4, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, dl, sqrtw, omega, x);
+    else
+        k_mf_update<T, 2, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, dl, sqrtw, omega, x);
+    MG_LAUNCH_CHECK();
+}
+
 #define MG_INST(T)                                                                                           \
+    template void mf_update<T>(const MatFree<T>&, const T*, const double*, const double*, double*, cudaStream_t); \
     template void mf_refresh<T>(const MatFree<T>&, const double*, double, T*, cudaStream_t);                     \
     template void mf_pass<T>(int, const MatFree<T>&, const T*, const T*, T*, const T*, double, double*, double*, \
                              cudaStream_t, double, const T*);

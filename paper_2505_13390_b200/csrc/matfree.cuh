@@ -44,6 +44,11 @@ int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc);
 template <class T>
 void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cudaStream_t s);
 
+// Eq. 5 from the vertex-major copy hv: x_v += omega sqrt(w_v) sum_{(j,s) at v} h_{j,s} dl_j
+// for the vertices [v0, v1) (hv must be current: after mf_refresh of this outer iteration).
+template <class T>
+void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const double* omega, double* x, cudaStream_t s);
+
 // One level-0 pass of `mode` (PASS_JACOBI, PASS_JACOBI_DOT, PASS_RESID_P, PASS_SPMV_DOT, PASS_POWER);
 // same arguments and outputs as csr_pass, A.grid partials.
 template <class T>
