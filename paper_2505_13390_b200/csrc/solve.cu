@@ -785,9 +785,16 @@ __global__ void __launch_bounds__(1024) k_coarse_inv(int32_t n, const int64_t* _
         }
         __syncthreads();
         const double ip = 1.0 / piv_s;
-        for (int64_t t = threadIdx.x; t < nn; t += blockDim.x) {
-            int32_t i = (int32_t)(t / n), j = (int32_t)(t % n);
-            if (i != k && j != k) W[t] -= W[(int64_t)i * n + k] * W[(int64_t)k * n + j] * ip;
+        {   // warp per row, lanes over columns (no 64-bit index division: it dominated this loop)
+            const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+            const double* __restrict__ Wk = W + (int64_t)k * n;
+            for (int32_t i = warp; i < n; i += nw) {
+                if (i == k) continue;
+                double* Wi = W + (int64_t)i * n;
+                const double wik = Wi[k];
+                for (int32_t j = lane; j < n; j += 32)
+                    if (j != k) Wi[j] -= wik * Wk[j] * ip;
+            }
         }
         __syncthreads();
         for (int32_t t = threadIdx.x; t < n; t += blockDim.x) {
@@ -1347,14 +1354,16 @@ template <class T>
 void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cudaStream_t s) {
     const int32_t n = A.n;
     size_t bytes = (size_t)n * n * sizeof(double);
-    if (bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
+    static const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
+    // (the one-CTA scalar Gauss-Jordan in shared memory is n barrier-separated steps: 241 us at n = 102
+    // against ~40 us for the cooperative blocked kernel, so it only serves as the MGPBD_NO_GJ_COOP path)
+    if (!coop && bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
         if (bytes > 48 * 1024)
             ensure_dyn_smem((const void*)k_coarse_inv<T>, bytes);
         k_coarse_inv<T><<<1, 1024, bytes, s>>>(n, A.rowptr, A.col, A.val, work, Ainv, flags, 1);
         MG_LAUNCH_CHECK();
         return;
     }
-    static const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
     if (coop) {  // one cooperative launch; work is the second n x n buffer
         static const int grid = [] {  // thread-safe one-time initialisation
             int dev = 0, sms = 0, occ = 0;
