@@ -15,7 +15,7 @@ SOURCES = ["util.cu", "mesh.cu", "solve.cu", "setup.cu", "comm.cu", "matfree.cu"
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE,
-         "--expt-relaxed-constexpr"]
+         "--expt-relaxed-constexpr"] + os.environ.get("MGPBD_EXTRA_NVCC_FLAGS", "").split()  # tuning sweeps only
 
 
 def _stale() -> bool:

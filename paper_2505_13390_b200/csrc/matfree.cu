@@ -74,7 +74,10 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
         if (v < v1) {
             // chunks of UN incidences per lane: all index/h loads, then all x gathers, then the FMAs,
             // so a chunk costs two dependent round trips instead of two per incidence
-            constexpr int UN = 4;
+#ifndef MGPBD_VG_UN
+#define MGPBD_VG_UN 6  // swept on B200 (profiles/r1/sweep_level0_pass.txt): 6 > 4 > 8 > 2
+#endif
+            constexpr int UN = MGPBD_VG_UN;
             const int64_t e0 = vptr[v], e1 = vptr[v + 1];
             for (int64_t eb = e0 + sl; eb < e1; eb += G * UN) {
                 int32_t cj[UN];
@@ -226,7 +229,10 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 // ids, h) and per-row operands into shared memory with 1-D bulk copies (cp.async.bulk, completion on
 // an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
 constexpr int MF_R = 256;       // rows per tile (= threads per CTA)
-constexpr int MF_STAGES = 3;
+#ifndef MGPBD_MF_STAGES
+#define MGPBD_MF_STAGES 3
+#endif
+constexpr int MF_STAGES = MGPBD_MF_STAGES;  // ring depth (overridable at build time for tuning sweeps)
 
 template <class T, int KC>
 struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 256)
@@ -352,7 +358,10 @@ template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
                 double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
     if (A.v1 > A.v0) {
-        constexpr int G = KC == 4 ? 4 : 2;  // ~23 (tets) / ~6 (cloth) incidences per vertex
+#ifndef MGPBD_VG_G4
+#define MGPBD_VG_G4 4
+#endif
+        constexpr int G = KC == 4 ? MGPBD_VG_G4 : 2;  // ~23 (tets) / ~6 (cloth) incidences per vertex
         const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
         const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * 16);
         k_mf_vgather<T, KC, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, x,
