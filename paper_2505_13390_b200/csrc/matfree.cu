@@ -363,7 +363,10 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #endif
         constexpr int G = KC == 4 ? MGPBD_VG_G4 : 2;  // ~23 (tets) / ~6 (cloth) incidences per vertex
         const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
-        const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * 16);
+#ifndef MGPBD_VG_CTAS_PER_SM
+#define MGPBD_VG_CTAS_PER_SM 16
+#endif
+        const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
         k_mf_vgather<T, KC, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, x,
                                                       reinterpret_cast<V4<T>*>(A.u));
         MG_LAUNCH_CHECK();
