@@ -225,17 +225,20 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 }
 
 // ---------------------------------------------------------------------------------------------
-// TMA-pipelined row kernel: persistent CTAs stream 256-row tiles of the constraint records (vertex
+// TMA-pipelined row kernel: persistent CTAs stream MF_R-row tiles of the constraint records (vertex
 // ids, h) and per-row operands into shared memory with 1-D bulk copies (cp.async.bulk, completion on
 // an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
-constexpr int MF_R = 256;       // rows per tile (= threads per CTA)
+#ifndef MGPBD_MF_R
+#define MGPBD_MF_R 128  // swept on B200 (profiles/r1/sweep_level0_pass.txt): 128 rows, 3 stages, 6 CTAs/SM
+#endif
+constexpr int MF_R = MGPBD_MF_R;  // rows per tile (= threads per CTA)
 #ifndef MGPBD_MF_STAGES
 #define MGPBD_MF_STAGES 3
 #endif
 constexpr int MF_STAGES = MGPBD_MF_STAGES;  // ring depth (overridable at build time for tuning sweeps)
 
 template <class T, int KC>
-struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 256)
+struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 128 or 256)
     static constexpr uint32_t H = 0;
     static constexpr uint32_t V = H + MF_R * KC * 3 * sizeof(T);
     static constexpr uint32_t X = V + MF_R * KC * sizeof(int32_t);
