@@ -337,11 +337,27 @@ void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_
     MG_LAUNCH_CHECK();
 }
 
+template <class T>
+int coarse_res_blocks_per_sm(uint32_t smem) {
+    if (cudaFuncSetAttribute((const void*)k_coarse_vcycle_res<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_coarse_vcycle_res<T>, RB, smem) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return nb;
+}
+
 #define MG_INST(T)                                                                                             \
     template bool coarse_res_plan<T>(const CoarseCycle<T>&, int, uint32_t, std::vector<ResLevel>&,             \
                                      std::vector<ResCopy>&, std::vector<int32_t>&, std::vector<uint32_t>&,     \
                                      uint32_t&, cudaStream_t);                                                 \
-    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t);
+    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t);                \
+    template int coarse_res_blocks_per_sm<T>(uint32_t);
 MG_INST(float)
 MG_INST(double)
 #undef MG_INST

@@ -47,5 +47,9 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
 
 template <class T>
 void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s);
+// CTAs of k_coarse_vcycle_res<T> that fit on one SM with `smem` dynamic bytes (0: the resident plan
+// cannot be launched cooperatively at one CTA per SM; the caller falls back to the global kernel)
+template <class T>
+int coarse_res_blocks_per_sm(uint32_t smem);
 
 }  // namespace mgpbd

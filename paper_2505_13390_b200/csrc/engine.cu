@@ -648,7 +648,8 @@ class Engine : public EngineBase {
                 std::vector<uint32_t> tx;
                 uint32_t smem = 0;
                 const uint32_t cap = 220u * 1024u;  // 227 KB minus the static descriptor copy
-                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st)) {
+                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st) &&
+                    coarse_res_blocks_per_sm<T>(smem) >= 1) {  // else the global coarse kernel
                     res_lv.resize(lv.size()); h2d(res_lv.p, lv.data(), lv.size(), st);
                     res_cp.resize(cp.size()); h2d(res_cp.p, cp.data(), cp.size(), st);
                     res_nc.resize(nc.size()); h2d(res_nc.p, nc.data(), nc.size(), st);
