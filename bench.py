@@ -7,9 +7,11 @@
 
 One step = one frame of Algorithm 1 (20 outer iterations x 10 MGPCG iterations; the lazy setup runs
 every 20 frames and after an indefinite PCG step, reading c13, and its cost is inside the timed
-frames).  Rank 0 prints one JSON line.
---impl reference times the CPU oracle (the tier's reference arm) on a bounded slab of the same
-workload and scales by constraint count (time per iteration is linear in size).
+frames).  Rank 0 prints one JSON line.  `--gpus N` (N > 1) without torchrun re-launches itself under
+`torch.distributed.run` with N ranks; under torchrun WORLD_SIZE must equal N.
+--impl reference times the CPU oracle (the tier's reference arm) on the same workload: each step is
+one outer Algorithm-1 iteration of the full configuration after the frame-0 setup (timed on its own),
+and the value is setup/setup_interval + n_iters x the mean iteration time.
 """
 from __future__ import annotations
 
@@ -105,70 +107,87 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def slab_scene(full_name, cells):
-    from paper_2505_13390_b200 import scenes
-    if full_name.startswith("block"):
-        return scenes.kuhn_block(cells, 64, 32, 0.01, dt=3e-3, squash=0.7, twist_deg=45.0 * cells / 136.0,
-                                 n_iters=20, name=f"blockslab{cells}")
-    raise ValueError(full_name)
-
-
-def oracle_frame_ms(sc, frames=1):
-    """Oracle wall time of `frames` frames of sc, setup amortised over setup_interval (1 core)."""
+def oracle_at_config(sc, iters):
+    """The oracle (1 core, fp64) on the configured workload itself: frame 0 with `iters` outer
+    iterations (setup at ite 0, timed inside the oracle).  Returns (ms/frame = setup/setup_interval +
+    n_iters x mean iteration, mean iteration ms, setup ms, the Sim for the parity comparison)."""
     import oracle as O
-    sim = O.Sim(sc)
+    sim = O.Sim(sc)                      # pattern of A (creation, not part of a frame)
     t0 = time.perf_counter()
-    for _ in range(frames):
-        sim.step(sc.dt, sc.n_iters)
+    sim.step(sc.dt, iters)
     total = (time.perf_counter() - t0) * 1e3
-    r, c, v = sim.A()
-    t1 = time.perf_counter()
-    O.Hierarchy(r, c, v, sim.cfg)
-    ts = (time.perf_counter() - t1) * 1e3                 # one setup, timed alone
-    setups = (frames + sim.cfg.setup_interval - 1) // sim.cfg.setup_interval
-    amort = (total - setups * ts + frames * ts / sim.cfg.setup_interval) / frames
-    return amort, total / frames, ts
+    setup = sim.setup_ms()
+    per_iter = (total - setup) / iters
+    return setup / sim.cfg.setup_interval + sc.n_iters * per_iter, per_iter, setup, sim
 
 
-def config_dict(sc, args, extra=None):
+def frame_errors(ctx, sim, sc):
+    """GPU-vs-oracle error of the same frame: relative 2-norm and max-abs/max of lambda and of the
+    displacement x - x_start."""
+    import numpy as np
+    xo, _, lo = sim.state()
+    x, lam = ctx.positions(), ctx.lambdas()
+    dx, dxo = x - sc.pos, xo - sc.pos
+    return {"lambda_rel2": float(np.linalg.norm(lam - lo) / np.linalg.norm(lo)),
+            "lambda_maxabs_over_max": float(np.abs(lam - lo).max() / np.abs(lo).max()),
+            "dx_rel2": float(np.linalg.norm(dx - dxo) / np.linalg.norm(dxo)),
+            "dx_maxabs_over_max": float(np.abs(dx - dxo).max() / np.abs(dxo).max())}
+
+
+def config_dict(sc, args, world, extra=None):
     d = {"workload": sc.name, "n_cons": sc.n_cons, "n_verts": sc.n_verts, "n_iters": sc.n_iters,
          "pcg_iters": sc.pcg_iters, "setup_interval": 20, "precision": args.precision,
          "accumulation": "fp64", "l2": "inputs larger than L2 (level-0 matrix streamed from HBM every pass)",
-         "parallelism": (f"level-0 rows partitioned over {args.gpus} GPUs (NCCL halos + allreduce), coarse "
-                         f"levels replicated") if args.gpus > 1 else "single GPU"}
+         "parallelism": (f"level-0 rows partitioned over {world} GPUs (NCCL halos + allreduce), coarse "
+                         f"levels replicated") if world > 1 else "single GPU"}
     if extra:
         d.update(extra)
     return d
 
 
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle, as it stands, on the configured workload.  Each step is
+    one outer Algorithm-1 iteration (constraint evaluation, assembly, Galerkin refresh, 10 MGPCG
+    iterations, update) of the full configuration; frame 0's setup runs once before the warm-up steps
+    and is timed on its own."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2505_13390_b200 import scenes
-    full = scenes.make(args.config) if not args.config.startswith("block1.67M") else None
-    m_full = 1671168 if args.config == "block1.67M" else full.n_cons
-    cells = 2
-    sc = slab_scene("block", cells) if args.config.startswith("block") else full
-    scale = m_full / sc.n_cons
     import oracle as O
+    sc = scenes.make(args.config)
+    t0 = time.perf_counter()
     sim = O.Sim(sc)
+    t_create = (time.perf_counter() - t0) * 1e3
+    t0 = time.perf_counter()
+    sim.step(sc.dt, 1)                   # frame 0: predict, setup (timed inside), first outer iteration
+    first = (time.perf_counter() - t0) * 1e3
+    setup = sim.setup_ms()
     times = []
     for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        sim.step(sc.dt, sc.n_iters)
+        sim.step(sc.dt, 1)               # one outer iteration (setup_interval 20: no setup in frames 1..19)
         dt_ms = (time.perf_counter() - t0) * 1e3
+        if sim.setup_ms() > 0:           # an off-schedule setup (indefinite event / frame % 20): count apart
+            dt_ms -= sim.setup_ms()
         if k >= args.warmup:
             times.append(dt_ms)
-    ms = statistics.mean(times) * scale
-    sample = (f"oracle frames of {sc.name} ({sc.n_cons} tets, {args.steps} timed frames after {args.warmup} "
-              f"warm-up, one setup per 20 frames), scaled x{scale:.1f} by constraint count to {args.config}")
+    per_iter = statistics.mean(times)
+    ms = setup / sim.cfg.setup_interval + sc.n_iters * per_iter
+    sample = (f"oracle (fp64, 1 core) on the full {sc.name} ({sc.n_cons} constraints): each step = one outer "
+              f"Alg.-1 iteration ({args.steps} timed after {args.warmup} warm-up, mean {per_iter:.0f} ms); frame-0 "
+              f"setup {setup:.0f} ms timed once and amortised /{sim.cfg.setup_interval}; value = setup/20 + "
+              f"{sc.n_iters} x iteration (pattern creation {t_create:.0f} ms excluded)")
+    cores = 1
     out = {"impl": "reference", "metric": METRIC, "value": ms, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": args.config, "n_cons": m_full, "n_iters": 20, "pcg_iters": 10,
-                      "precision": "fp64 (oracle)", "sample": sc.name},
-           "cpu_baseline": {"value": ms, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "config": {"workload": sc.name, "n_cons": sc.n_cons, "n_verts": sc.n_verts, "n_iters": sc.n_iters,
+                      "pcg_iters": sc.pcg_iters, "setup_interval": 20, "precision": "fp64 (oracle)",
+                      "same_config": True},
+           "cpu_baseline": {"value": ms, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample,
+                            "measured_at_config": True, "iteration_ms": per_iter, "setup_ms": setup,
+                            "first_frame_ms": first},
            "e2e": {"value": ms, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
@@ -213,7 +232,7 @@ def run_ours(args):
 
     launches = 0
     indef = 0
-    frames_ms, setup_ms = [], []
+    frames_ms, setup_ms, steady_ms = [], [], []
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
@@ -227,6 +246,8 @@ def run_ours(args):
             frames_ms.append(s.ms_frame)
             if s.setup_ran:
                 setup_ms.append(s.ms_setup)
+            else:
+                steady_ms.append(s.ms_frame)
         e1.record(stream)
         barrier()
     t_ms = e0.elapsed_time(e1)
@@ -290,13 +311,15 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prec else "f64", "data": "synthetic",
-        "config": config_dict(sc, args, {
+        "config": config_dict(sc, args, world, {
             "nnz_A0": levels[0][1] if levels else None, "levels": levels,
             "op_complexity": st0.op_complexity,
             "ms_setup_frame_extra": (statistics.mean(setup_ms) if setup_ms else None),
             "setups_in_window": len(setup_ms),
             "indefinite_events_in_window": indef,
-            "ms_frame_median": statistics.median(frames_ms)}),
+            "ms_frame_median": statistics.median(frames_ms),
+            "ms_frame_steady_median": statistics.median(steady_ms) if steady_ms else None,
+            "sweep_criterion": "ms_frame_steady_median (frames without a setup) and ms_setup_frame_extra"}),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic_per_launch(args.level0_operator),
                      "kernel": ("level-0 matrix-free passes (k_mf_vgather + k_mf_rows: omega-Jacobi / residual*P / "
@@ -317,19 +340,25 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    ctx.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cells = args.cpu_slab
-        sc_s = slab_scene(args.config, cells) if args.config.startswith("block") else sc
-        amort, raw, ts = oracle_frame_ms(sc_s, 1)
-        scale = sc.n_cons / sc_s.n_cons
+        # the oracle on the configured workload itself (frame 0, setup + cpu_iters outer iterations),
+        # and the GPU's error on that same frame (a fresh context in the bench configuration)
+        ms_o, per_iter, setup, sim = oracle_at_config(sc, args.cpu_iters)
+        ctx0 = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream,
+                                        level0_operator=args.level0_operator)
+        ctx0.step(sc.dt, args.cpu_iters)
+        err = frame_errors(ctx0, sim, sc)
+        ctx0.close()
         out["cpu_baseline"] = {
-            "value": amort * scale, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": (f"one oracle frame (20 outer x 10 PCG, fp64, 1 core) of {sc_s.name} ({sc_s.n_cons} tets): "
-                       f"{raw:.0f} ms incl. one {ts:.0f} ms setup, setup amortised /20, scaled x{scale:.1f} by "
-                       f"constraint count")}
+            "value": ms_o, "unit": UNIT, "cores": 1, "kind": "oracle", "measured_at_config": True,
+            "iteration_ms": per_iter, "setup_ms": setup,
+            "sample": (f"oracle (fp64, 1 core) on the full {sc.name}: frame 0 with setup + {args.cpu_iters} of "
+                       f"{sc.n_iters} outer iterations timed ({setup:.0f} ms setup, {per_iter:.0f} ms per "
+                       f"iteration); value = setup/20 + {sc.n_iters} x iteration"),
+            "gpu_vs_oracle_same_frame": {"frame": 0, "outer_iterations": args.cpu_iters, **err}}
     if rank == 0:
         print(json.dumps(out), flush=True)
-    ctx.close()
     if dist:
         dist.destroy_process_group()
     return 0
@@ -344,19 +373,45 @@ def main():
     ap.add_argument("--config", default="block1.67M")
     ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-slab", type=int, default=8, help="x-slabs of the block the oracle sample uses")
+    ap.add_argument("--cpu-iters", type=int, default=1,
+                    help="outer iterations of the oracle's frame-0 sample at the full configuration")
     ap.add_argument("--level0-operator", type=int, default=1, choices=[0, 1],
                     help="1: matrix-free level 0 (default), 0: assembled-CSR level-0 passes")
     ap.add_argument("--partitioned", action="store_true",
                     help="N=1 only: run the row-partitioned (NCCL) code path on a 1-rank communicator")
     ap.add_argument("--profile-frames", type=int, default=2, help="frames timed per level-0 pass for the roofline")
+    ap.add_argument("--dry-run", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        return spawn(args.gpus)
+    if int(ws or 1) != args.gpus:
+        print(f"error: --gpus {args.gpus} but WORLD_SIZE={ws or 1}", file=sys.stderr)
+        return 2
+    if args.dry_run:  # launcher check only (tests): what each rank sees, no CUDA
+        rank, world, local = dist_env()
+        if rank == 0:
+            print(json.dumps({"dry_run": True, "n_gpus": world, "gpus_arg": args.gpus, "local_rank": local}),
+                  flush=True)
+        return 0
     return run_ours(args)
+
+
+def spawn(n):
+    """`--gpus N` without a launcher: run this script under torch.distributed.run with N ranks (one per
+    GPU, rendezvous on 127.0.0.1); rank 0's JSON line passes through."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 if __name__ == "__main__":

@@ -15,7 +15,7 @@
  *    in mgpbd_destroy.
  *  - Errors: functions return an mgpbd_status and never throw across the ABI; the context keeps a
  *    last-error string (mgpbd_last_error).  Argument errors leave the state unchanged.  Solver
- *    errors (indefinite preconditioner, non-finite values) are raised from device flags at the end
+ *    errors (non-SPD coarsest matrix, non-finite values) are raised from device flags at the end
  *    of mgpbd_step; the state is then the completed (possibly polluted) frame.
  *  - Numbering: user numbering (constraint order and vertex order as passed to mgpbd_create) is
  *    preserved at the boundary; the level-l matrices returned by the test hooks are CSR with
@@ -45,7 +45,10 @@ typedef enum {
     MGPBD_E_CUDA = -2,       /* CUDA runtime error (message in mgpbd_last_error) */
     MGPBD_E_NCCL = -3,       /* multi-GPU communication error */
     MGPBD_E_OOM = -4,        /* device allocation failed */
-    MGPBD_E_INDEFINITE = -5, /* <z,r> <= 0 with r != 0 in PCG, or non-SPD coarsest */
+    MGPBD_E_INDEFINITE = -5, /* the coarsest matrix of the hierarchy is not SPD (non-positive pivot in its
+                                dense inversion).  A PCG iteration with <z,r> <= 0 (r != 0) is
+                                NOT an error: it is counted in mgpbd_stats.indefinite_events, the frame
+                                completes, and with cfg.resetup_on_indef the setup re-runs at the next frame */
     MGPBD_E_NONFINITE = -6,  /* NaN/Inf reached the right-hand side or the PCG scalars */
     MGPBD_E_STALL = -7       /* coarsening stalled with a coarsest level too large to invert */
 } mgpbd_status;
@@ -112,6 +115,11 @@ typedef struct {
     double pcg_tol;           /* MGPCG convergence exit: the solve stops (remaining iterations become no-ops,
                                  decided on the device) at the first iteration k with ||r_k|| <= pcg_tol *
                                  ||b||; 0 = off: exactly pcg_iters iterations (reading c10) */
+    int32_t resetup_on_indef; /* 1 (default): a frame in which a PCG iteration saw <z,r> <= 0 marks the
+                                 hierarchy stale, so the setup re-runs at ite 0 of the next frame (reading
+                                 c13 extension); 0: the literal lazy schedule of PAPER.md:215
+                                 (setup only every setup_interval frames).  With lambda_safety = 1 this is
+                                 the paper's literal mode */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16
@@ -165,7 +173,9 @@ MGPBD_API mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx);
 
 /* One frame of Algorithm 1 with n_iters outer iterations (1..MGPBD_MAX_ITERS) and time step dt > 0.
  * Setup runs at ite 0 when frame % setup_interval == 0 or the hierarchy is stale.  Synchronises at
- * the end and checks the device flags (MGPBD_E_INDEFINITE / MGPBD_E_NONFINITE). */
+ * the end and checks the device flags: MGPBD_E_NONFINITE (NaN/Inf PCG scalar), MGPBD_E_INDEFINITE
+ * (non-SPD coarsest matrix).  <z,r> <= 0 in PCG is counted (mgpbd_stats.indefinite_events), not
+ * returned. */
 MGPBD_API mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters);
 
 /* Enable (1) / disable (0) CUDA-event timing of the level-0 matrix passes (mgpbd_stats.l0_pass_*).
@@ -198,6 +208,13 @@ MGPBD_API mgpbd_status mgpbd_debug_setup_from(mgpbd_ctx* ctx, const double* A0_v
 /* Apply one V-cycle / K MGPCG iterations of the current hierarchy to host b (n_0) -> host x. */
 MGPBD_API mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x);
 MGPBD_API mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x);
+/* Alg. 1 l.1-7 of the next frame without the solve: predict (positions become the
+ * predicted x~, velocities get dt g), lambda = 0, evaluate the constraints and refresh the hot level-0
+ * operator at x~ (matrix-free when configured), run the setup if one is due (frame % setup_interval
+ * == 0 or stale), then the Galerkin refresh and coarsest inverse — so debug_vcycle / debug_pcg apply
+ * exactly the operators mgpbd_step's first outer iteration uses.  The frame counter is not advanced.
+ * Errors: MGPBD_E_ARG for dt <= 0. */
+MGPBD_API mgpbd_status mgpbd_debug_prepare(mgpbd_ctx* ctx, double dt);
 /* Measurement hook: `reps` (1..4096) level-0 SpMV+dot passes of the hot operator on the current state,
  * captured as one CUDA graph and timed with events around its replay (no launch gaps).  *ms = device
  * time, *bytes = the passes' algorithmic bytes.  Needs a stepped context and one rank; E_ARG otherwise. */

@@ -5,11 +5,13 @@
  * follows the paper's definition or algorithm step by step; where the paper is silent the
  * SURVEY.md §8(c) reading (c0..c19, restated in DESIGN.md) is cited.
  */
+#define _POSIX_C_SOURCE 199309L
 #include "oracle.h"
 
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #define OMAX(a, b) ((a) > (b) ? (a) : (b))
 
@@ -22,6 +24,7 @@ void orc_config_default(orc_config* c) {
     c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
     c->smoother = 0; c->cheb_lower = 0.25;
     c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0; c->pcg_tol = 0.0;
+    c->resetup_on_indef = 1; c->k_nullspace = 1;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -901,7 +904,15 @@ struct orc_sim {
     int32_t iters_used;
     double omega_last;
     int32_t n_indef;  /* PCG iterations with <z,r> <= 0 (r != 0) in the last frame */
+    int32_t n_setups; /* setups run since creation */
+    double setup_ms;  /* wall time of the setup in the last frame (0 if none; timing only, bench.py) */
 };
+
+static double wall_ms(void) {
+    struct timespec t;
+    clock_gettime(CLOCK_MONOTONIC, &t);
+    return 1e3 * (double)t.tv_sec + 1e-6 * (double)t.tv_nsec;
+}
 
 orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* verts,
                         const double* rest_pos, const double* pos, const double* vel,
@@ -943,11 +954,13 @@ orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* ver
  * when marked stale (reading c13); Galerkin values are refreshed every iteration.
  * The outer break (l.12) is disabled: fixed n_iters (reading c11).  Collision (l.16) is out of
  * scope.  A PCG iteration with <z,r> <= 0 (the lazily-set omega of PAPER.md:320 no longer below
- * 2/lambda_max) is counted and marks the hierarchy stale, so setup re-runs at ite 0 of the next
- * frame (reading c13).  Returns 0, or -5 if a coarsest matrix is not SPD. */
+ * 2/lambda_max) is counted; with cfg.resetup_on_indef it marks the hierarchy stale, so setup re-runs
+ * at ite 0 of the next frame (reading c13); without it the schedule is the literal
+ * PAPER.md:215.  Returns 0, or -5 if a coarsest matrix is not SPD. */
 int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
     int rc = 0;
     s->n_indef = 0;
+    s->setup_ms = 0.0;
     int32_t n = s->n, m = s->m;
     /* l.1 semiEuler: x_old = x; v += dt g (w > 0); x = x~ = x + dt v;  l.2 lambda = 0 */
     for (int32_t v = 0; v < n; ++v)
@@ -972,9 +985,12 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
         if (s->cfg.backtrack && ite > 0 && bn > bprev) omega = fmax(0.5 * omega, s->cfg.omega_min);
         bprev = bn;
         if (ite == 0 && (s->h == NULL || s->stale || s->frame % s->cfg.setup_interval == 0)) { /* l.7 */
+            const double t0 = wall_ms();
             orc_hier_free(s->h);
             s->h = orc_hier_build(m, s->rowptr, s->col, s->val, &s->cfg);
             s->stale = 0;
+            s->n_setups++;
+            s->setup_ms = wall_ms() - t0;
             if (factor_coarsest(s->h) != 0) rc = -5;
         } else if (orc_hier_refresh(s->h, s->val) != 0) rc = -5;
         s->n_indef += orc_pcg(s->h, s->b, s->cfg.pcg_iters, s->dl, NULL);                         /* l.8 */
@@ -987,7 +1003,7 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
     s->omega_last = omega;
     for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->v[k] = (s->x[k] - s->x_old[k]) / dt;      /* l.17 */
     s->frame++;
-    if (s->n_indef) s->stale = 1;
+    if (s->n_indef && s->cfg.resetup_on_indef) s->stale = 1;
     return rc;
 }
 
@@ -995,6 +1011,8 @@ void orc_sim_mark_stale(orc_sim* s) { s->stale = 1; }
 int32_t orc_sim_iters_used(const orc_sim* s) { return s->iters_used; }
 double orc_sim_omega(const orc_sim* s) { return s->omega_last; }
 int32_t orc_sim_indefinite_events(const orc_sim* s) { return s->n_indef; }
+int32_t orc_sim_setups(const orc_sim* s) { return s->n_setups; }
+double orc_sim_setup_ms(const orc_sim* s) { return s->setup_ms; }
 void orc_sim_get(const orc_sim* s, double* x, double* v, double* lambda) {
     if (x) memcpy(x, s->x, sizeof(double) * 3 * (size_t)s->n);
     if (v) memcpy(v, s->v, sizeof(double) * 3 * (size_t)s->n);

@@ -39,6 +39,11 @@ typedef struct {
     double omega_min;        /* floor of the halving; 1e-3 */
     double residual_tol;     /* Alg. 1 l.12: break once ||b|| < residual_tol * ||b_0||; 0 = off (c11/c21) */
     double pcg_tol;          /* MGPCG stops once ||r_k|| <= pcg_tol ||b||; 0 = off, fixed pcg_iters (c10) */
+    int32_t resetup_on_indef;/* 1: a frame with a PCG iteration <z,r> <= 0 marks the hierarchy stale, so setup
+                                re-runs at ite 0 of the next frame (reading c13 extension); 0: the literal
+                                schedule of PAPER.md:215 (setup only every setup_interval frames).  Default 1 */
+    int32_t k_nullspace;     /* near-kernel vectors per aggregate ("six distinct B"; reading c1):
+                                1 (default) or up to 6 */
 } orc_config;
 
 void orc_config_default(orc_config* c);
@@ -122,6 +127,8 @@ orc_sim* orc_sim_create(int kind, int32_t n_verts, int32_t m, const int32_t* ver
 int orc_sim_step(orc_sim* s, double dt, int32_t n_iters);
 void orc_sim_mark_stale(orc_sim* s);
 int32_t orc_sim_indefinite_events(const orc_sim* s);
+int32_t orc_sim_setups(const orc_sim* s);          /* setups run since creation (Alg. 1 l.7) */
+double orc_sim_setup_ms(const orc_sim* s);         /* wall time of the last frame's setup (0 if none) */
 void orc_sim_get(const orc_sim* s, double* x, double* v, double* lambda);
 void orc_sim_set(orc_sim* s, const double* x, const double* v);
 const orc_hier* orc_sim_hier(const orc_sim* s);

@@ -16,8 +16,10 @@ def build(force: bool = False) -> str:
     """Compile the oracle: serial, fp64, -O2 -ffp-contract=off, no fast-math."""
     if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
             os.path.getmtime(SRC), os.path.getmtime(os.path.join(HERE, "oracle.h"))):
+        tmp = f"{LIB_PATH}.{os.getpid()}.tmp"  # replace atomically: a running process may map the old one
         subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-std=c11",
-                               "-fPIC", "-shared", "-o", LIB_PATH, SRC, "-lm"])
+                               "-fPIC", "-shared", "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, LIB_PATH)
     return LIB_PATH
 
 
@@ -29,7 +31,8 @@ class Config(C.Structure):
                 ("pcg_iters", C.c_int32), ("omega_relax", C.c_double),
                 ("gravity", C.c_double * 3), ("seed", C.c_uint64), ("smoother", C.c_int32),
                 ("cheb_lower", C.c_double), ("backtrack", C.c_int32), ("omega_min", C.c_double),
-                ("residual_tol", C.c_double), ("pcg_tol", C.c_double)]
+                ("residual_tol", C.c_double), ("pcg_tol", C.c_double), ("resetup_on_indef", C.c_int32),
+                ("k_nullspace", C.c_int32)]
 
 
 _lib = None
@@ -85,6 +88,8 @@ def lib():
             "orc_sim_create": (P, [C.c_int, i32, i32, P, P, P, P, P, P, P]),
             "orc_sim_step": (C.c_int, [P, f64, i32]),
             "orc_sim_mark_stale": (None, [P]),
+            "orc_sim_setups": (C.c_int32, [P]),
+            "orc_sim_setup_ms": (C.c_double, [P]),
             "orc_sim_indefinite_events": (i32, [P]),
             "orc_sim_iters_used": (i32, [P]),
             "orc_sim_omega": (f64, [P]),
@@ -422,6 +427,13 @@ class Sim:
 
     def indefinite_events(self) -> int:
         return int(lib().orc_sim_indefinite_events(self.s))
+
+    def setups(self) -> int:
+        return int(lib().orc_sim_setups(self.s))
+
+    def setup_ms(self) -> float:
+        """Wall time of the last frame's setup (timing for bench.py; 0 if no setup ran)."""
+        return float(lib().orc_sim_setup_ms(self.s))
 
     def iters_used(self) -> int:
         return int(lib().orc_sim_iters_used(self.s))

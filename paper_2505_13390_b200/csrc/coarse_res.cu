@@ -339,11 +339,7 @@ void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_
 
 template <class T>
 int coarse_res_blocks_per_sm(uint32_t smem) {
-    if (cudaFuncSetAttribute((const void*)k_coarse_vcycle_res<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess) {
-        (void)cudaGetLastError();
-        return 0;
-    }
+    if (!try_raise_dyn_smem((const void*)k_coarse_vcycle_res<T>, smem)) return 0;  // raise-only (util.cu)
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_coarse_vcycle_res<T>, RB, smem) != cudaSuccess) {
         (void)cudaGetLastError();

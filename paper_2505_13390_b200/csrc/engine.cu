@@ -45,6 +45,7 @@ struct EngineBase {
     virtual void debug_setup_from(const double* vals) = 0;
     virtual void debug_vcycle(const double* b, double* x) = 0;
     virtual void debug_pcg(const double* b, int32_t iters, double* x) = 0;
+    virtual void debug_prepare(double dt) = 0;
     virtual void pass_burst(int32_t reps, double* ms, double* bytes) = 0;
     virtual void bind() = 0;  // make this context's device/stream current for the calling thread
     virtual void set_profiling(int on) = 0;
@@ -274,6 +275,12 @@ class Engine : public EngineBase {
         }
         mf.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
         mf.grid = mf.tma ? mf_grid_tma(r0, r1, (int)sizeof(T), kc) : mf_grid(r1 - r0);
+        if (const char* cap = std::getenv("MGPBD_MF_GRID_CAP")) {  // tests: many tiles per CTA (TMA ring wraps)
+            const int c = std::max(1, std::atoi(cap));
+            mf.grid = std::min(mf.grid, c);
+            mf.vg_grid_cap = c;
+            if (mf64_ok) { mf64.grid = std::min(mf64.grid, c); mf64.vg_grid_cap = c; }
+        }
 
     }
     int l0_nparts() const { return mf_on() ? mf.grid : L[0]->hot().nparts; }
@@ -1008,9 +1015,9 @@ class Engine : public EngineBase {
         d2h(hf, flags.p, 6, st);
         MG_CK(cudaStreamSynchronize(st));
         // <z,r> <= 0: the lazily-set omega is no longer below 2/lambda_max -> re-run the setup at ite 0
-        // of the next frame (reading c13); counted, not an error.
+        // of the next frame (reading c13; cfg.resetup_on_indef); counted, not an error.
         indef_events = hf[4];
-        if (indef_events) stale = true;
+        if (indef_events && cfg.resetup_on_indef) stale = true;
         if (hf[1]) throw Error(MGPBD_E_NONFINITE, "non-finite PCG scalar at (frame " + std::to_string(frame - 1) +
                                                       ", ite " + std::to_string(hf[3] / 4096) + ", pcg " +
                                                       std::to_string(hf[3] % 4096) + ")");
@@ -1160,6 +1167,24 @@ class Engine : public EngineBase {
         cudaGraphExecDestroy(exec);
     }
 
+    void debug_prepare(double dt) override {
+        MG_CK(cudaMemsetAsync(flags.p, 0, 8 * sizeof(int), st));
+        predict(nv, x.p, v.p, x_old.p, w.p, dt, cfg.gravity[0], cfg.gravity[1], cfg.gravity[2], st);  // l.1
+        omega_dev.resize(1);
+        h2d(omega_dev.p, &cfg.omega_relax, 1, st);
+        MG_CK(cudaMemsetAsync(lambda.p, 0, sizeof(double) * m, st));                                // l.2
+        assemble_hot(dt);                                                                            // l.4-6
+        if (stale || !have_hier || frame % cfg.setup_interval == 0) {                               // l.7
+            assemble_setup(dt);
+            setup();
+        }
+        if (cfg.level0_operator == 1 && nL < 2)
+            assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, L[0]->vl, L[0]->val.p,
+                        L[0]->dinv.p, st, r0, r1);
+        refresh();                                                                                   // Eq. 6
+        MG_CK(cudaStreamSynchronize(st));
+    }
+
     void debug_pcg(const double* b, int32_t iters, double* xo) override {
         if (!have_hier) throw Error(MGPBD_E_ARG, "no hierarchy");
         DBuf<double> tmp;
@@ -1235,6 +1260,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->omega_min = 1e-3;
     c->residual_tol = 0.0;
     c->pcg_tol = 0.0;
+    c->resetup_on_indef = 1;
     return MGPBD_OK;
 }
 
@@ -1358,6 +1384,10 @@ mgpbd_status mgpbd_debug_setup_from(mgpbd_ctx* ctx, const double* vals) {
 mgpbd_status mgpbd_debug_vcycle(mgpbd_ctx* ctx, const double* b, double* x) {
     if (ctx && (!b || !x)) return MGPBD_E_ARG;
     return guarded(ctx, [&] { ctx->eng->debug_vcycle(b, x); });
+}
+mgpbd_status mgpbd_debug_prepare(mgpbd_ctx* ctx, double dt) {
+    if (!ctx || !(dt > 0.0)) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->debug_prepare(dt); });
 }
 mgpbd_status mgpbd_debug_pcg(mgpbd_ctx* ctx, const double* b, int32_t iters, double* x) {
     if (ctx && (!b || !x || iters < 0 || iters > mgpbd::SC_KMAX)) return MGPBD_E_ARG;

@@ -369,7 +369,8 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #ifndef MGPBD_VG_CTAS_PER_SM
 #define MGPBD_VG_CTAS_PER_SM 16
 #endif
-        const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
+        int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
+        if (A.vg_grid_cap > 0) grid = std::min(grid, A.vg_grid_cap);
         k_mf_vgather<T, KC, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, x,
                                                       reinterpret_cast<V4<T>*>(A.u));
         MG_LAUNCH_CHECK();

@@ -32,6 +32,7 @@ struct MatFree {
     const T* dinv = nullptr;        // 1 / A_ii from the assembly
     int grid = 1;                   // CTAs of the row kernel = number of dot partials
     bool tma = false;               // TMA-pipelined row kernel (persistent CTAs, bulk copies)
+    int vg_grid_cap = 0;            // > 0: cap on the vertex-gather grid (MGPBD_MF_GRID_CAP, tests only)
 };
 
 int mf_grid(int32_t rows);

@@ -1,6 +1,7 @@
 // Deterministic scans, reductions and small helper kernels.
 #include "util.cuh"
 
+#include <map>
 #include <mutex>
 #include <unordered_map>
 
@@ -218,15 +219,29 @@ void stamp(unsigned long long* buf, int idx, cudaStream_t s) {
     MG_LAUNCH_CHECK();
 }
 
-void ensure_dyn_smem(const void* kernel, size_t bytes) {
+// Raise (never lower) a kernel's dynamic shared-memory limit on the current device.  The cache is keyed
+// by (device, kernel): the attribute is per device, and lowering it would break another live context
+// that launches the same kernel with a larger plan.  Returns false (no throw) when `bytes` cannot be
+// granted.
+static bool raise_dyn_smem(const void* kernel, size_t bytes, bool throw_on_error) {
     static std::mutex mu;
-    static std::unordered_map<const void*, size_t> set;
+    static std::map<std::pair<int, const void*>, size_t> set;
+    int dev = 0;
+    MG_CK(cudaGetDevice(&dev));
     std::lock_guard<std::mutex> lk(mu);
-    size_t& cur = set[kernel];
+    size_t& cur = set[{dev, kernel}];
     if (bytes > cur && bytes > 48 * 1024) {
-        MG_CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) {
+            if (throw_on_error) MG_CK(e);
+            (void)cudaGetLastError();
+            return false;
+        }
         cur = bytes;
     }
+    return true;
 }
+void ensure_dyn_smem(const void* kernel, size_t bytes) { raise_dyn_smem(kernel, bytes, true); }
+bool try_raise_dyn_smem(const void* kernel, size_t bytes) { return raise_dyn_smem(kernel, bytes, false); }
 
 }  // namespace mgpbd

@@ -38,7 +38,8 @@ void group_by_key(const int32_t* key, int64_t n, int64_t nk, DBuf<int64_t>& ptr,
 
 // Raise a kernel's dynamic shared-memory limit to at least `bytes` (thread-safe: contexts of virtual
 // ranks launch from several host threads; the attribute is only ever raised).
-void ensure_dyn_smem(const void* kernel, size_t bytes);
+void ensure_dyn_smem(const void* kernel, size_t bytes);      // raise-only, per (device, kernel); throws
+bool try_raise_dyn_smem(const void* kernel, size_t bytes);   // same, returns false instead of throwing
 
 // Diagnostics: buf[idx] = %globaltimer (one thread; graph-capturable; MGPBD_TRACE_STAGES).
 void stamp(unsigned long long* buf, int idx, cudaStream_t s);

@@ -20,6 +20,7 @@ SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgp
            "mgpbd_get_positions", "mgpbd_get_velocities", "mgpbd_get_lambda", "mgpbd_get_stats",
            "mgpbd_get_level_sizes", "mgpbd_get_level", "mgpbd_get_prolongator", "mgpbd_get_aggregates",
            "mgpbd_get_near_kernel", "mgpbd_debug_setup_from", "mgpbd_debug_vcycle", "mgpbd_debug_pcg",
+           "mgpbd_debug_prepare",
            "mgpbd_pass_burst",
            "mgpbd_last_error", "mgpbd_destroy", "mgpbd_nccl_unique_id", "mgpbd_vgroup_create",
            "mgpbd_vgroup_destroy", "mgpbd_partition_rows", "mgpbd_halo_plan"]
@@ -50,7 +51,8 @@ class Config(C.Structure):
                 ("rank", C.c_int32), ("world", C.c_int32), ("profile", C.c_int32),
                 ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32),
                 ("smoother", C.c_int32), ("cheb_lower", C.c_double), ("backtrack", C.c_int32),
-                ("omega_min", C.c_double), ("residual_tol", C.c_double), ("pcg_tol", C.c_double)]
+                ("omega_min", C.c_double), ("residual_tol", C.c_double), ("pcg_tol", C.c_double),
+                ("resetup_on_indef", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -97,6 +99,7 @@ def lib():
             "mgpbd_debug_setup_from": (C.c_int, [P, P]),
             "mgpbd_debug_vcycle": (C.c_int, [P, P, P]),
             "mgpbd_debug_pcg": (C.c_int, [P, P, i32, P]),
+            "mgpbd_debug_prepare": (C.c_int, [P, f64]),
             "mgpbd_pass_burst": (C.c_int, [P, i32, P, P]),
             "mgpbd_last_error": (C.c_char_p, [P]),
             "mgpbd_nccl_unique_id": (C.c_int, [P]),
@@ -291,6 +294,10 @@ class Context:
     def debug_setup_from(self, vals):
         vals = np.ascontiguousarray(vals, np.float64)
         self._ck(lib().mgpbd_debug_setup_from(self.h, _p(vals)))
+
+    def debug_prepare(self, dt):
+        """Alg. 1 l.1-7 of the next frame without the solve (mgpbd_debug_prepare)."""
+        self._ck(lib().mgpbd_debug_prepare(self.h, float(dt)))
 
     def debug_vcycle(self, b):
         b = np.ascontiguousarray(b, np.float64)

@@ -49,3 +49,19 @@ def test_bench_cli_parses():
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--help"], capture_output=True,
                          text=True, timeout=120)
     assert out.returncode == 0 and "--impl" in out.stdout and "--gpus" in out.stdout
+
+
+def test_gpus_flag_spawns_ranks_and_checks_world():
+    """`bench.py --gpus N` without a launcher runs N ranks under torch.distributed.run (rank 0 prints);
+    under a launcher, WORLD_SIZE != --gpus is an error (the line must not misreport n_gpus)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=300, env=env)
+    assert out.returncode == 0, out.stderr
+    lines = [l for l in out.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["gpus_arg"] == 2
+    bad = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                         capture_output=True, text=True, timeout=120, env={**env, "WORLD_SIZE": "3"})
+    assert bad.returncode == 2 and "WORLD_SIZE" in bad.stderr

@@ -286,3 +286,31 @@ def test_hierarchy_invariants_cloth_and_table1(O, cloth_frame):
     t = GOLD["table1"]
     # loose consistency with Table 1 (cloth C = 1.046, nl = 5): C close to 1, nl small
     assert 1.0 <= h.operator_complexity() < 1.1 and t["nl_min"] <= L <= t["nl_max"]
+
+
+@pytest.mark.parametrize("safety", [1.0, 1.1])
+def test_hierarchy_omega_closed_form(O, safety):
+    """omega_l = 2/(s lambda_max(D^-1 A_l) + lambda_min_est) as orc_hier_build sets it (PAPER.md:318,
+    reading c9), pinned against a closed-form spectrum: A = S T S with T = tridiag(-c, 1, -c) (n x n)
+    and S = diag(sqrt(d)) has D = diag(d) and D^-1 A = S^-1 T S, similar to T, whose largest eigenvalue
+    is 1 + 2c cos(pi/(n+1)).  The Chebyshev interval of level 0 is [0.25 hi, hi], hi = s lambda_max
+    (reading c20)."""
+    n, c = 12, 0.4
+    rng = np.random.default_rng(3)
+    d = rng.uniform(0.5, 4.0, n)
+    T = np.eye(n) - c * (np.eye(n, k=1) + np.eye(n, k=-1))
+    A = np.sqrt(np.outer(d, d)) * T
+    lam = 1.0 + 2.0 * c * np.cos(np.pi / (n + 1))
+    r, cc, v = csr_from_dense_diaglast(A)
+    # gap lambda_2/lambda_1 ~ 0.93: 20000 power iterations converge to machine precision
+    cfg = O.default_config(min_coarse=2, power_iters=20000, lambda_safety=safety)
+    h = O.Hierarchy(r, cc, v, cfg)
+    assert h.n_levels >= 2
+    assert np.isclose(h.omega(0), 2.0 / (safety * lam + 0.1), rtol=1e-12)
+    theta, delta = h.cheb(0)
+    hi = safety * lam
+    assert np.isclose(theta, 0.5 * (hi + 0.25 * hi), rtol=1e-12) and np.isclose(delta, 0.5 * (hi - 0.25 * hi), rtol=1e-12)
+    # lambda_min_est enters additively (PAPER.md:318): another estimate moves omega exactly
+    h2 = O.Hierarchy(r, cc, v, O.default_config(min_coarse=2, power_iters=20000, lambda_safety=safety,
+                                                lambda_min_est=0.5))
+    assert np.isclose(h2.omega(0), 2.0 / (safety * lam + 0.5), rtol=1e-12)

@@ -152,6 +152,8 @@ def test_frame_equals_dense_direct_frame(O, name):
     xr, vr, lr = _python_frame(O, sc, 4, sc.omega_relax)
     assert np.allclose(lam, lr, rtol=1e-9, atol=1e-12 * np.abs(lr).max())
     assert np.allclose(x - sc.pos, xr - sc.pos, rtol=1e-9, atol=1e-12 * np.abs(xr - sc.pos).max())
+    # Alg. 1 l.17: v = (x - x_old)/dt, against the dense-direct frame's own velocity
+    assert np.allclose(v, vr, rtol=1e-9, atol=1e-12 * np.abs(vr).max())
 
 
 def test_single_constraint_closed_form_eq4_eq5(O):
@@ -422,3 +424,24 @@ def test_pcg_tolerance_exit(O, bar_sys):
     xt, _, _ = ht.pcg(b, 40)
     assert np.array_equal(xt, h.pcg(b, K)[0])
     assert np.linalg.norm(b - A @ xt) <= tol * np.linalg.norm(b) * (1 + 1e-12)
+
+
+def test_setup_schedule_literal_and_resetup_on_indefinite(O):
+    """Alg. 1 l.7: setup at ite 0 of frames with frame % setup_interval == 0.  With
+    resetup_on_indef = 0 (the literal paper) nothing else triggers it, even after PCG iterations with
+    <z,r> <= 0; with resetup_on_indef = 1 (reading c13 extension) a frame with such events is followed by
+    a setup.  bar3k with lambda_safety = 1 (literal omega) has events from frame 0 on."""
+    sc = scenes.make("bar3k")
+    ev, su = {}, {}
+    for re in (0, 1):
+        cfg = O.default_config(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters, lambda_safety=1.0,
+                               resetup_on_indef=re)
+        sim = O.Sim(sc, cfg)
+        ev[re], su[re] = [], []
+        for _ in range(4):
+            sim.step(sc.dt, sc.n_iters)
+            ev[re].append(sim.indefinite_events()); su[re].append(sim.setups())
+    assert sum(ev[0]) > 0 and su[0] == [1, 1, 1, 1]
+    for f in range(1, 4):
+        assert su[1][f] - su[1][f - 1] == (1 if ev[1][f - 1] > 0 else 0)
+    assert su[1][-1] > 1
