@@ -14,6 +14,7 @@
 #include <time.h>
 
 #define OMAX(a, b) ((a) > (b) ? (a) : (b))
+#define ORC_RANK_TOL 1e-10  /* QR column drop threshold, relative to the column norm (reading c24) */
 
 static void* xmalloc(size_t n) { void* p = malloc(n ? n : 1); if (!p) abort(); return p; }
 static void* xcalloc(size_t n, size_t s) { void* p = calloc(n ? n : 1, s ? s : 1); if (!p) abort(); return p; }
@@ -566,6 +567,188 @@ int64_t orc_galerkin(int32_t n, const int64_t* rowptr, const int32_t* col, const
     return nnz;
 }
 
+/* ------------------------------------------------------------------------------------------
+ * k > 1 near-kernel vectors ("We repeat this six times to generate
+ * six distinct B"; "use QR decomposition to form the next level, where R of QR
+ * decomposition serves as B at the next level").  Readings c23-c25.
+ * ------------------------------------------------------------------------------------------ */
+
+/* k bootstrapped columns (reading c23): column c is orc_gs_bootstrap's sweep sequence
+ * from x_0[i] = U(stream 3, 0, i + c n) * max|A_ij| (reading c0: index offset c n per column), each
+ * column with its own ||.|| < 1e-14 sqrt(n) => ones fallback.  B is column-major, B[c n + i]. */
+void orc_gs_bootstrap_k(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                        const int32_t* colour, int32_t sweeps, uint64_t seed, int32_t k, double* B) {
+    double mx = 0.0;
+    for (int64_t e = 0; e < rowptr[n]; ++e) mx = OMAX(mx, fabs(val[e]));
+    ci_pair* ord = xmalloc(sizeof(ci_pair) * (size_t)n);
+    for (int32_t i = 0; i < n; ++i) { ord[i].c = colour[i]; ord[i].i = i; }
+    qsort(ord, (size_t)n, sizeof(ci_pair), cmp_ci);
+    for (int32_t c = 0; c < k; ++c) {
+        double* x = B + (int64_t)c * n;
+        for (int32_t i = 0; i < n; ++i) x[i] = orc_uniform(seed, 3, 0, (uint64_t)i + (uint64_t)c * (uint64_t)n) * mx;
+        for (int32_t s = 0; s < sweeps; ++s)
+            for (int32_t t = 0; t < n; ++t) {
+                int32_t i = ord[t].i;
+                double acc = 0.0, d = 0.0;
+                for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                    if (col[e] == i) d = val[e];
+                    else acc += val[e] * x[col[e]];
+                }
+                x[i] = -acc / d;
+            }
+        double nn = 0.0;
+        for (int32_t i = 0; i < n; ++i) nn += x[i] * x[i];
+        if (sqrt(nn) < 1e-14 * sqrt((double)n))
+            for (int32_t i = 0; i < n; ++i) x[i] = 1.0;
+    }
+    free(ord);
+}
+
+/* Inject with k columns (readings c24, c25).  For each aggregate a (members N_a
+ * ascending) the |N_a| x k block B_a = B[N_a, :] is factored B_a = Q_a R_a by modified Gram-Schmidt
+ * with one re-orthogonalisation pass, columns in order 0..k-1: column c is kept iff the norm of its
+ * component orthogonal to the kept columns exceeds rank_tol * ||B_a[:, c]|| (and is > 0); kept columns
+ * get R diagonal = that norm > 0, dropped (rank-deficient) columns only their projections.  Q_a fills
+ * P's rows N_a in r_a consecutive coarse columns off_a .. off_a + r_a - 1 (off = prefix sum of r);
+ * row j of R_a (r_a x k) becomes row off_a + j of B_next (n_next x k, column-major with leading
+ * dimension ld_next).  An aggregate with no kept column (B_a = 0) gets the single column
+ * 1/sqrt(|N_a|) with a zero R row (the k = 1 rule of reading c6).  P is CSR (pptr n+1, pcol, pval;
+ * row i holds r_agg(i) entries, ascending columns).  B is column-major n x k.  Returns n_next; coff
+ * (n_agg + 1) receives the offsets.  With pcol == NULL only coff / n_next are computed. */
+int32_t orc_prolongator_qr(int32_t n, const int32_t* agg, int32_t n_agg, int32_t k, const double* B,
+                           double rank_tol, int32_t* coff, int64_t* pptr, int32_t* pcol, double* pval,
+                           double* B_next, int32_t ld_next) {
+    int64_t* mp = xcalloc((size_t)n_agg + 1, sizeof(int64_t));
+    for (int32_t i = 0; i < n; ++i) mp[agg[i] + 1]++;
+    for (int32_t a = 0; a < n_agg; ++a) mp[a + 1] += mp[a];
+    int32_t* mem = xmalloc(sizeof(int32_t) * (size_t)n);
+    int64_t* f = xmalloc(sizeof(int64_t) * ((size_t)n_agg + 1));
+    memcpy(f, mp, sizeof(int64_t) * ((size_t)n_agg + 1));
+    for (int32_t i = 0; i < n; ++i) mem[f[agg[i]]++] = i;
+    free(f);
+    int32_t maxm = 0;
+    for (int32_t a = 0; a < n_agg; ++a) maxm = (int32_t)OMAX(maxm, mp[a + 1] - mp[a]);
+    double* Q = xmalloc(sizeof(double) * (size_t)maxm * (size_t)k);   /* kept columns, |N_a| each */
+    double* v = xmalloc(sizeof(double) * (size_t)maxm);
+    double* R = xmalloc(sizeof(double) * (size_t)k * (size_t)k);     /* R[j*k + c] */
+    double* Qs = pval ? xmalloc(sizeof(double) * (size_t)n * (size_t)k) : NULL;  /* Q by member slot */
+    int32_t* rk = xmalloc(sizeof(int32_t) * (size_t)n_agg);
+    coff[0] = 0;
+    for (int32_t a = 0; a < n_agg; ++a) {
+        const int64_t m0 = mp[a];
+        const int32_t na = (int32_t)(mp[a + 1] - m0);
+        int32_t r = 0;
+        memset(R, 0, sizeof(double) * (size_t)k * (size_t)k);
+        for (int32_t c = 0; c < k; ++c) {
+            double bn = 0.0;
+            for (int32_t t = 0; t < na; ++t) { v[t] = B[(int64_t)c * n + mem[m0 + t]]; bn += v[t] * v[t]; }
+            bn = sqrt(bn);
+            for (int pass = 0; pass < 2; ++pass)
+                for (int32_t j = 0; j < r; ++j) {
+                    double s = 0.0;
+                    for (int32_t t = 0; t < na; ++t) s += Q[(int64_t)j * na + t] * v[t];
+                    for (int32_t t = 0; t < na; ++t) v[t] -= s * Q[(int64_t)j * na + t];
+                    R[j * k + c] += s;
+                }
+            double vn = 0.0;
+            for (int32_t t = 0; t < na; ++t) vn += v[t] * v[t];
+            vn = sqrt(vn);
+            if (vn > 0.0 && vn > rank_tol * bn) {
+                for (int32_t t = 0; t < na; ++t) Q[(int64_t)r * na + t] = v[t] / vn;
+                R[r * k + c] = vn;
+                ++r;
+            }
+        }
+        if (r == 0) {   /* B_a = 0: uniform column, zero R row (reading c6) */
+            for (int32_t t = 0; t < na; ++t) Q[t] = 1.0 / sqrt((double)na);
+            memset(R, 0, sizeof(double) * (size_t)k);
+            r = 1;
+        }
+        rk[a] = r;
+        coff[a + 1] = coff[a] + r;
+        if (B_next)
+            for (int32_t j = 0; j < r; ++j)
+                for (int32_t c = 0; c < k; ++c) B_next[(int64_t)c * ld_next + coff[a] + j] = R[j * k + c];
+        if (Qs)
+            for (int32_t j = 0; j < r; ++j)
+                for (int32_t t = 0; t < na; ++t) Qs[(int64_t)(m0 + t) * k + j] = Q[(int64_t)j * na + t];
+    }
+    if (pptr) {
+        pptr[0] = 0;
+        for (int32_t i = 0; i < n; ++i) pptr[i + 1] = pptr[i] + rk[agg[i]];
+    }
+    if (pcol && pval) {
+        for (int32_t a = 0; a < n_agg; ++a)
+            for (int64_t t = mp[a]; t < mp[a + 1]; ++t) {
+                const int32_t i = mem[t];
+                for (int32_t j = 0; j < rk[a]; ++j) {
+                    pcol[pptr[i] + j] = coff[a] + j;
+                    pval[pptr[i] + j] = Qs[t * k + j];
+                }
+            }
+    }
+    const int32_t nn = coff[n_agg];
+    free(mp); free(mem); free(Q); free(v); free(R); free(Qs); free(rk);
+    return nn;
+}
+
+/* Galerkin product A_c = P^T A P for a general CSR prolongator (Eq. 6; used with
+ * k > 1): (A_c)_{IJ} = sum_i sum_{j in row i of A} P_{iI} A_ij P_{jJ}.  Coarse row I accumulates over
+ * the fine rows i with P_{iI} != 0 in ascending i, their stored entries in storage order, and P's
+ * row j in storage order; the pattern is every (I, J) reached, off-diagonals ascending, diagonal
+ * last.  All-NULL outputs => count only (returns nnz). */
+int64_t orc_galerkin_p(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                       const int64_t* pptr, const int32_t* pcol, const double* pval, int32_t nc,
+                       int64_t* crowptr, int32_t* ccol, double* cval) {
+    /* P^T by coarse column: fine rows ascending */
+    int64_t* tp = xcalloc((size_t)nc + 1, sizeof(int64_t));
+    for (int64_t e = 0; e < pptr[n]; ++e) tp[pcol[e] + 1]++;
+    for (int32_t I = 0; I < nc; ++I) tp[I + 1] += tp[I];
+    int32_t* ti = xmalloc(sizeof(int32_t) * (size_t)OMAX(pptr[n], 1));
+    double* tv = xmalloc(sizeof(double) * (size_t)OMAX(pptr[n], 1));
+    int64_t* f = xmalloc(sizeof(int64_t) * ((size_t)nc + 1));
+    memcpy(f, tp, sizeof(int64_t) * ((size_t)nc + 1));
+    for (int32_t i = 0; i < n; ++i)
+        for (int64_t e = pptr[i]; e < pptr[i + 1]; ++e) { ti[f[pcol[e]]] = i; tv[f[pcol[e]]++] = pval[e]; }
+    free(f);
+    double* acc = xcalloc((size_t)nc, sizeof(double));
+    uint8_t* mark = xcalloc((size_t)nc, 1);
+    int32_t* touched = xmalloc(sizeof(int32_t) * (size_t)nc);
+    int64_t nnz = 0;
+    if (crowptr) crowptr[0] = 0;
+    for (int32_t I = 0; I < nc; ++I) {
+        int32_t nt = 0;
+        for (int64_t t = tp[I]; t < tp[I + 1]; ++t) {
+            const int32_t i = ti[t];
+            const double pi = tv[t];
+            for (int64_t e = rowptr[i]; e < rowptr[i + 1]; ++e) {
+                const int32_t j = col[e];
+                for (int64_t q = pptr[j]; q < pptr[j + 1]; ++q) {
+                    const int32_t J = pcol[q];
+                    if (!mark[J]) { mark[J] = 1; touched[nt++] = J; acc[J] = 0.0; }
+                    if (cval) acc[J] += pi * val[e] * pval[q];
+                }
+            }
+        }
+        qsort(touched, (size_t)nt, sizeof(int32_t), cmp_i32);
+        int32_t k = 0;
+        for (int32_t t = 0; t < nt; ++t) {
+            const int32_t J = touched[t];
+            if (J == I) continue;
+            if (ccol) ccol[nnz + k] = J;
+            if (cval) cval[nnz + k] = acc[J];
+            ++k;
+        }
+        if (ccol) ccol[nnz + k] = I;
+        if (cval) cval[nnz + k] = mark[I] ? acc[I] : 0.0;
+        nnz += k + 1;
+        for (int32_t t = 0; t < nt; ++t) mark[touched[t]] = 0;
+        if (crowptr) crowptr[I + 1] = nnz;
+    }
+    free(tp); free(ti); free(tv); free(acc); free(mark); free(touched);
+    return nnz;
+}
+
 /* lambda_max(D^-1 A) by the power method (reading c9): v_0 = U(stream 4, l)/||.||;
  * `iters` times: w = D^-1 A v; lambda = ||w||_2; v = w / lambda. */
 double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
@@ -629,13 +812,15 @@ typedef struct {
     int32_t* agg; int32_t n_agg; double* P; double omega;
     double cheb_theta, cheb_delta;  /* Chebyshev interval (reading c20) */
     int32_t* gs_order;              /* multicolour GS: nodes sorted by (colour, index) (reading c22) */
+    /* k > 1 (f2): general CSR prolongator n x n_next (row i: r_agg(i) entries), coarse offsets */
+    int64_t* pptr; int32_t* pcol; double* pval; int32_t* coff;
 } orc_level;
 
 struct orc_hier {
     int L;
     orc_level lv[32];
     double* Lc;          /* Cholesky factor of the coarsest matrix */
-    double* B0;          /* bootstrapped near-kernel vector at level 0 (if coarsened) */
+    double* B0;          /* bootstrapped near-kernel vector(s) at level 0 (if coarsened): n x k column-major */
     int32_t ncolours;
     int stalled;
     orc_config cfg;
@@ -643,6 +828,7 @@ struct orc_hier {
 
 static void level_free(orc_level* v) {
     free(v->rowptr); free(v->col); free(v->val); free(v->agg); free(v->P); free(v->gs_order);
+    free(v->pptr); free(v->pcol); free(v->pval); free(v->coff);
     memset(v, 0, sizeof *v);
 }
 
@@ -676,6 +862,7 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
     memcpy(l0->val, val, sizeof(double) * (size_t)l0->nnz);
     h->L = 1;
     double* B = NULL;
+    const int32_t k = cfg->k_nullspace > 1 ? cfg->k_nullspace : 1;
     int maxl = cfg->max_levels < 32 ? cfg->max_levels : 32;
     for (int l = 0; l + 1 < maxl; ++l) {
         orc_level* a = &h->lv[l];
@@ -689,24 +876,48 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
         if (l == 0) {
             int32_t* colour = xmalloc(sizeof(int32_t) * (size_t)a->n);
             h->ncolours = orc_colour(a->n, a->rowptr, a->col, cfg->seed, colour);
-            B = xmalloc(sizeof(double) * (size_t)a->n);
-            orc_gs_bootstrap(a->n, a->rowptr, a->col, a->val, colour, cfg->bootstrap_sweeps, cfg->seed, B);
+            B = xmalloc(sizeof(double) * (size_t)a->n * (size_t)k);
+            if (k == 1) orc_gs_bootstrap(a->n, a->rowptr, a->col, a->val, colour, cfg->bootstrap_sweeps, cfg->seed, B);
+            else orc_gs_bootstrap_k(a->n, a->rowptr, a->col, a->val, colour, cfg->bootstrap_sweeps, cfg->seed, k, B);
             free(colour);
-            h->B0 = xmalloc(sizeof(double) * (size_t)a->n);
-            memcpy(h->B0, B, sizeof(double) * (size_t)a->n);
+            h->B0 = xmalloc(sizeof(double) * (size_t)a->n * (size_t)k);
+            memcpy(h->B0, B, sizeof(double) * (size_t)a->n * (size_t)k);
         }
         a->agg = agg; a->n_agg = na;
-        a->P = xmalloc(sizeof(double) * (size_t)a->n);
-        double* Bn = xmalloc(sizeof(double) * (size_t)na);
-        orc_prolongator(a->n, agg, na, B, a->P, Bn);
-        free(B); B = Bn;
         orc_level* c = &h->lv[l + 1];
-        c->n = na;
-        c->rowptr = xmalloc(sizeof(int64_t) * ((size_t)na + 1));
-        c->nnz = orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, NULL, NULL);
-        c->col = xmalloc(sizeof(int32_t) * (size_t)c->nnz);
-        c->val = xmalloc(sizeof(double) * (size_t)c->nnz);
-        orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, c->col, c->val);
+        if (k == 1) {
+            a->P = xmalloc(sizeof(double) * (size_t)a->n);
+            double* Bn = xmalloc(sizeof(double) * (size_t)na);
+            orc_prolongator(a->n, agg, na, B, a->P, Bn);
+            free(B); B = Bn;
+            c->n = na;
+            c->rowptr = xmalloc(sizeof(int64_t) * ((size_t)na + 1));
+            c->nnz = orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, NULL, NULL);
+            c->col = xmalloc(sizeof(int32_t) * (size_t)c->nnz);
+            c->val = xmalloc(sizeof(double) * (size_t)c->nnz);
+            orc_galerkin(a->n, a->rowptr, a->col, a->val, agg, a->P, na, c->rowptr, c->col, c->val);
+        } else {  /* k columns (f2): QR injection, general P^T A P on the scalar coarse DOFs (c24, c25) */
+            a->coff = xmalloc(sizeof(int32_t) * ((size_t)na + 1));
+            a->pptr = xmalloc(sizeof(int64_t) * ((size_t)a->n + 1));
+            const int32_t nc = orc_prolongator_qr(a->n, agg, na, k, B, ORC_RANK_TOL, a->coff, a->pptr, NULL, NULL, NULL, 0);
+            if ((double)nc > cfg->stall_ratio * (double)a->n) {  /* coarse DOFs, not aggregates, decide (c7) */
+                free(a->coff); free(a->pptr); free(a->agg);
+                a->coff = NULL; a->pptr = NULL; a->agg = NULL; a->n_agg = 0;
+                h->stalled = 1;
+                break;
+            }
+            a->pcol = xmalloc(sizeof(int32_t) * (size_t)a->pptr[a->n]);
+            a->pval = xmalloc(sizeof(double) * (size_t)a->pptr[a->n]);
+            double* Bn = xmalloc(sizeof(double) * (size_t)nc * (size_t)k);
+            orc_prolongator_qr(a->n, agg, na, k, B, ORC_RANK_TOL, a->coff, a->pptr, a->pcol, a->pval, Bn, nc);
+            free(B); B = Bn;
+            c->n = nc;
+            c->rowptr = xmalloc(sizeof(int64_t) * ((size_t)nc + 1));
+            c->nnz = orc_galerkin_p(a->n, a->rowptr, a->col, a->val, a->pptr, a->pcol, a->pval, nc, c->rowptr, NULL, NULL);
+            c->col = xmalloc(sizeof(int32_t) * (size_t)c->nnz);
+            c->val = xmalloc(sizeof(double) * (size_t)c->nnz);
+            orc_galerkin_p(a->n, a->rowptr, a->col, a->val, a->pptr, a->pcol, a->pval, nc, c->rowptr, c->col, c->val);
+        }
         double lam = orc_power(a->n, a->rowptr, a->col, a->val, cfg->power_iters, cfg->seed, l);
         a->omega = 2.0 / (cfg->lambda_safety * lam + cfg->lambda_min_est);
         if (cfg->smoother == 2) {  /* multicolour GS order of this level (reading c22) */
@@ -737,7 +948,8 @@ int orc_hier_refresh(orc_hier* h, const double* val0) {
     memcpy(h->lv[0].val, val0, sizeof(double) * (size_t)h->lv[0].nnz);
     for (int l = 0; l + 1 < h->L; ++l) {
         orc_level* a = &h->lv[l]; orc_level* c = &h->lv[l + 1];
-        orc_galerkin(a->n, a->rowptr, a->col, a->val, a->agg, a->P, a->n_agg, c->rowptr, c->col, c->val);
+        if (a->pptr) orc_galerkin_p(a->n, a->rowptr, a->col, a->val, a->pptr, a->pcol, a->pval, c->n, c->rowptr, c->col, c->val);
+        else orc_galerkin(a->n, a->rowptr, a->col, a->val, a->agg, a->P, a->n_agg, c->rowptr, c->col, c->val);
     }
     return factor_coarsest(h);
 }
@@ -756,9 +968,31 @@ void orc_hier_get_level(const orc_hier* h, int l, int64_t* rowptr, int32_t* col,
     if (val) memcpy(val, a->val, sizeof(double) * (size_t)a->nnz);
 }
 void orc_hier_get_agg(const orc_hier* h, int l, int32_t* agg) { memcpy(agg, h->lv[l].agg, sizeof(int32_t) * (size_t)h->lv[l].n); }
-void orc_hier_get_P(const orc_hier* h, int l, double* P) { memcpy(P, h->lv[l].P, sizeof(double) * (size_t)h->lv[l].n); }
+void orc_hier_get_P(const orc_hier* h, int l, double* P) { if (h->lv[l].P) memcpy(P, h->lv[l].P, sizeof(double) * (size_t)h->lv[l].n); }
 double orc_hier_omega(const orc_hier* h, int l) { return h->lv[l].omega; }
-void orc_hier_get_B0(const orc_hier* h, double* B) { if (h->B0) memcpy(B, h->B0, sizeof(double) * (size_t)h->lv[0].n); }
+void orc_hier_get_B0(const orc_hier* h, double* B) {
+    const size_t k = h->cfg.k_nullspace > 1 ? (size_t)h->cfg.k_nullspace : 1;
+    if (h->B0) memcpy(B, h->B0, sizeof(double) * (size_t)h->lv[0].n * k);
+}
+/* level-l prolongator as CSR (n_l x n_{l+1}); k = 1 levels are returned in the same form (one entry per
+ * row, column = aggregate).  rowptr == NULL: only *nnz. */
+void orc_hier_get_P_csr(const orc_hier* h, int l, int64_t* nnz, int64_t* rowptr, int32_t* col, double* val) {
+    const orc_level* a = &h->lv[l];
+    if (a->pptr) {
+        *nnz = a->pptr[a->n];
+        if (rowptr) memcpy(rowptr, a->pptr, sizeof(int64_t) * ((size_t)a->n + 1));
+        if (col) memcpy(col, a->pcol, sizeof(int32_t) * (size_t)*nnz);
+        if (val) memcpy(val, a->pval, sizeof(double) * (size_t)*nnz);
+        return;
+    }
+    *nnz = a->n;
+    for (int32_t i = 0; i < a->n; ++i) {
+        if (rowptr) rowptr[i] = i;
+        if (col) col[i] = a->agg[i];
+        if (val) val[i] = a->P[i];
+    }
+    if (rowptr) rowptr[a->n] = a->n;
+}
 int32_t orc_hier_n_colours(const orc_hier* h) { return h->ncolours; }
 
 /* omega-Jacobi sweep x <- x + omega D^-1 (b - A x). */
@@ -828,7 +1062,7 @@ void orc_hier_smooth(const orc_hier* h, int l, const double* b, double* x, int p
 static void vcycle_level(const orc_hier* h, int l, const double* b, double* x) {
     const orc_level* a = &h->lv[l];
     if (l == h->L - 1) { orc_chol_solve(a->n, h->Lc, b, x); return; }
-    int32_t n = a->n, nc = a->n_agg;
+    int32_t n = a->n, nc = h->lv[l + 1].n;
     double* tmp = xmalloc(sizeof(double) * (size_t)n);
     double* d = xmalloc(sizeof(double) * (size_t)n);
     for (int32_t i = 0; i < n; ++i) x[i] = 0.0;
@@ -836,9 +1070,17 @@ static void vcycle_level(const orc_hier* h, int l, const double* b, double* x) {
     orc_spmv(n, a->rowptr, a->col, a->val, x, tmp);
     double* bc = xcalloc((size_t)nc, sizeof(double));
     double* ec = xmalloc(sizeof(double) * (size_t)nc);
-    for (int32_t i = 0; i < n; ++i) bc[a->agg[i]] += a->P[i] * (b[i] - tmp[i]);
-    vcycle_level(h, l + 1, bc, ec);
-    for (int32_t i = 0; i < n; ++i) x[i] += a->P[i] * ec[a->agg[i]];
+    if (a->pptr) {   /* general P (k > 1): b_c = P^T r, x += P e */
+        for (int32_t i = 0; i < n; ++i)
+            for (int64_t q = a->pptr[i]; q < a->pptr[i + 1]; ++q) bc[a->pcol[q]] += a->pval[q] * (b[i] - tmp[i]);
+        vcycle_level(h, l + 1, bc, ec);
+        for (int32_t i = 0; i < n; ++i)
+            for (int64_t q = a->pptr[i]; q < a->pptr[i + 1]; ++q) x[i] += a->pval[q] * ec[a->pcol[q]];
+    } else {
+        for (int32_t i = 0; i < n; ++i) bc[a->agg[i]] += a->P[i] * (b[i] - tmp[i]);
+        vcycle_level(h, l + 1, bc, ec);
+        for (int32_t i = 0; i < n; ++i) x[i] += a->P[i] * ec[a->agg[i]];
+    }
     smooth(h, a, b, x, tmp, d, 1);
     free(tmp); free(d); free(bc); free(ec);
 }

@@ -92,6 +92,16 @@ void orc_prolongator(int32_t n, const int32_t* agg, int32_t n_agg, const double*
 int64_t orc_galerkin(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
                      const int32_t* agg, const double* P, int32_t n_agg,
                      int64_t* crowptr, int32_t* ccol, double* cval /* all NULL => count only */);
+/* k > 1 near kernel (f2; readings c23-c25): k bootstrapped columns (column-major n x k), per-aggregate
+ * MGS thin QR injection into a CSR prolongator, general Galerkin P^T A P. */
+void orc_gs_bootstrap_k(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                        const int32_t* colour, int32_t sweeps, uint64_t seed, int32_t k, double* B);
+int32_t orc_prolongator_qr(int32_t n, const int32_t* agg, int32_t n_agg, int32_t k, const double* B,
+                           double rank_tol, int32_t* coff, int64_t* pptr, int32_t* pcol, double* pval,
+                           double* B_next, int32_t ld_next);
+int64_t orc_galerkin_p(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                       const int64_t* pptr, const int32_t* pcol, const double* pval, int32_t nc,
+                       int64_t* crowptr, int32_t* ccol, double* cval);
 double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
                  int32_t iters, uint64_t seed, int level);
 int orc_cholesky(int32_t n, const double* A /* dense n*n */, double* L /* n*n */);
@@ -114,7 +124,8 @@ void orc_hier_cheb(const orc_hier* h, int l, double* theta, double* delta);
 /* one smoothing pass (the level's configured smoother, cfg.smoother_sweeps steps) on A x = b;
  * post = 1: the post-smoother (GS: reversed colour order) */
 void orc_hier_smooth(const orc_hier* h, int l, const double* b, double* x, int post);
-void orc_hier_get_B0(const orc_hier* h, double* B);
+void orc_hier_get_B0(const orc_hier* h, double* B);   /* n_0 x k, column-major */
+void orc_hier_get_P_csr(const orc_hier* h, int l, int64_t* nnz, int64_t* rowptr, int32_t* col, double* val);
 int32_t orc_hier_n_colours(const orc_hier* h);
 void orc_vcycle(const orc_hier* h, const double* b, double* x);
 int orc_pcg(const orc_hier* h, const double* b, int32_t iters, double* x, double* rz_trace);

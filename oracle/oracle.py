@@ -68,6 +68,10 @@ def lib():
             "orc_prolongator": (None, [i32, P, i32, P, P, P]),
             "orc_galerkin": (i64, [i32, P, P, P, P, P, i32, P, P, P]),
             "orc_power": (f64, [i32, P, P, P, i32, u64, C.c_int]),
+            "orc_gs_bootstrap_k": (None, [i32, P, P, P, P, i32, u64, i32, P]),
+            "orc_prolongator_qr": (i32, [i32, P, i32, i32, P, f64, P, P, P, P, P, i32]),
+            "orc_galerkin_p": (i64, [i32, P, P, P, P, P, P, i32, P, P, P]),
+            "orc_hier_get_P_csr": (None, [P, C.c_int, P, P, P, P]),
             "orc_cholesky": (C.c_int, [i32, P, P]),
             "orc_chol_solve": (None, [i32, P, P, P]),
             "orc_hier_build": (P, [i32, P, P, P, P]),
@@ -275,6 +279,45 @@ def prolongator(agg, n_agg, B):
     return P, Bn
 
 
+def gs_bootstrap_k(rowptr, col, val, colours, k, sweeps=20, seed=1):
+    """k bootstrapped near-kernel columns (n x k array; reading c23)."""
+    rowptr, col, val = _c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)
+    colours = _c(colours, np.int32)
+    n = rowptr.shape[0] - 1
+    B = np.empty(n * k)
+    lib().orc_gs_bootstrap_k(n, _p(rowptr), _p(col), _p(val), _p(colours), sweeps, seed, k, _p(B))
+    return B.reshape(k, n).T.copy()
+
+
+def prolongator_qr(agg, n_agg, B, rank_tol=1e-10):
+    """QR injection with k = B.shape[1] columns (readings c24, c25): (P as CSR (rowptr, col, val), B_next
+    (n_next x k), coarse offsets per aggregate)."""
+    agg = _c(agg, np.int32)
+    B = np.asarray(B, np.float64)
+    n, k = B.shape
+    Bc = _c(B.T, np.float64)          # column-major
+    coff = np.empty(n_agg + 1, np.int32); pptr = np.empty(n + 1, np.int64)
+    nc = lib().orc_prolongator_qr(n, _p(agg), n_agg, k, _p(Bc), rank_tol, _p(coff), _p(pptr), None, None, None, 0)
+    pcol = np.empty(int(pptr[-1]), np.int32); pval = np.empty(int(pptr[-1]))
+    Bn = np.empty(nc * k)
+    lib().orc_prolongator_qr(n, _p(agg), n_agg, k, _p(Bc), rank_tol, _p(coff), _p(pptr), _p(pcol), _p(pval),
+                             _p(Bn), nc)
+    return (pptr, pcol, pval), Bn.reshape(k, nc).T.copy(), coff
+
+
+def galerkin_p(rowptr, col, val, P, nc):
+    """P^T A P for a CSR prolongator P = (pptr, pcol, pval) with nc columns."""
+    rowptr, col, val = _c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)
+    pptr, pcol, pval = _c(P[0], np.int64), _c(P[1], np.int32), _c(P[2], np.float64)
+    n = rowptr.shape[0] - 1
+    crow = np.empty(nc + 1, np.int64)
+    nnz = lib().orc_galerkin_p(n, _p(rowptr), _p(col), _p(val), _p(pptr), _p(pcol), _p(pval), nc, _p(crow), None, None)
+    ccol = np.empty(nnz, np.int32); cval = np.empty(nnz)
+    lib().orc_galerkin_p(n, _p(rowptr), _p(col), _p(val), _p(pptr), _p(pcol), _p(pval), nc, _p(crow), _p(ccol),
+                         _p(cval))
+    return crow, ccol, cval
+
+
 def galerkin(rowptr, col, val, agg, P, n_agg):
     rowptr, col, val = _c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)
     agg, P = _c(agg, np.int32), _c(P, np.float64)
@@ -311,11 +354,13 @@ class Hierarchy:
 
     def __init__(self, rowptr, col, val, cfg: Config | None = None, _handle=None, _owner=None):
         self._owner = _owner
+        self.cfg = cfg if cfg is not None else (getattr(_owner, "cfg", None) if _owner is not None else None)
         if _handle is not None:
             self.h = _handle
             self._own = False
         else:
             cfg = cfg or default_config()
+            self.cfg = cfg
             self._keep = [_c(rowptr, np.int64), _c(col, np.int32), _c(val, np.float64)]
             r, c, v = self._keep
             self.h = lib().orc_hier_build(r.shape[0] - 1, _p(r), _p(c), _p(v), C.byref(cfg))
@@ -369,10 +414,21 @@ class Hierarchy:
         return x
 
     def B0(self):
+        """Level-0 near kernel: n (k = 1) or n x k (k > 1)."""
         n, _ = self.level_size(0)
-        a = np.empty(n)
+        k = max(int(self.cfg.k_nullspace), 1) if self.cfg is not None else 1
+        a = np.empty(n * k)
         lib().orc_hier_get_B0(self.h, _p(a))
-        return a
+        return a if k == 1 else a.reshape(k, n).T.copy()
+
+    def P_csr(self, l):
+        """Level-l prolongator as CSR (rowptr, col, val); k = 1: one entry per row, column = aggregate."""
+        nnz = C.c_int64()
+        lib().orc_hier_get_P_csr(self.h, l, C.byref(nnz), None, None, None)
+        n, _ = self.level_size(l)
+        r = np.empty(n + 1, np.int64); c = np.empty(nnz.value, np.int32); v = np.empty(nnz.value)
+        lib().orc_hier_get_P_csr(self.h, l, C.byref(nnz), _p(r), _p(c), _p(v))
+        return r, c, v
 
     @property
     def n_colours(self) -> int:
