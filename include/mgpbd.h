@@ -72,7 +72,9 @@ typedef struct {
     int32_t precision;        /* 0: fp64 everywhere; 1: fp32 storage of A, h, P and level vectors
                                  with fp64 accumulation, fp64 setup, fp64 scalars and coarsest solve */
     double theta;             /* SOC threshold theta_s, 0.1 */
-    int32_t k_nullspace;      /* near-kernel vectors per aggregate; only 1 is implemented (reading c1) */
+    int32_t k_nullspace;      /* near-kernel vectors per aggregate ("six distinct B"): 1 (default,
+                                 reading c1) or 2..8 (k bootstrapped columns, per-aggregate
+                                 thin QR, block coarse operators; one rank; readings c23-c25) */
     int32_t min_coarse;       /* coarsen while n_l >= min_coarse, 400 */
     int32_t max_levels;       /* 16 */
     double stall_ratio;       /* stop coarsening when n_{l+1}/n_l > stall_ratio, 0.9 */
@@ -196,11 +198,19 @@ MGPBD_API mgpbd_status mgpbd_get_stats(mgpbd_ctx* ctx, mgpbd_stats* out);
 MGPBD_API mgpbd_status mgpbd_get_level_sizes(mgpbd_ctx* ctx, int32_t l, int64_t* n, int64_t* nnz);
 /* CSR of level l (rowptr n+1, cols nnz, vals nnz as fp64): current values of the hot loop. */
 MGPBD_API mgpbd_status mgpbd_get_level(mgpbd_ctx* ctx, int32_t l, int64_t* rowptr, int32_t* cols, double* vals);
-/* Level-l prolongator values P_i (n_l doubles, one per row; column = aggregate of row i). */
+/* Level-l prolongator values P_i (n_l doubles, one per row; column = aggregate of row i); k_nullspace = 1
+ * only (MGPBD_E_ARG otherwise: use mgpbd_get_prolongator_csr). */
 MGPBD_API mgpbd_status mgpbd_get_prolongator(mgpbd_ctx* ctx, int32_t l, double* p_vals);
+/* Level-l prolongator as CSR (n_l x n_{l+1}, columns ascending per row): *nnz always; rowptr (n_l + 1),
+ * col and val (nnz each) when non-NULL.  k_nullspace = 1: one entry per row, column = aggregate, value =
+ * P_i; k > 1 (readings c24/c25): row i holds the r_a (<= k) entries of its aggregate's
+ * thin-QR factor Q_a in columns off_a .. off_a + r_a - 1. */
+MGPBD_API mgpbd_status mgpbd_get_prolongator_csr(mgpbd_ctx* ctx, int32_t l, int64_t* nnz, int64_t* rowptr,
+                                                 int32_t* col, double* val);
 /* Level-l aggregate index per node (n_l int32). */
 MGPBD_API mgpbd_status mgpbd_get_aggregates(mgpbd_ctx* ctx, int32_t l, int32_t* out);
-/* Level-0 near-kernel vector B after the GS bootstrap (n_0 doubles). */
+/* Level-0 near-kernel vector(s) B after the GS bootstrap: n_0 x k_nullspace doubles, column-major (column c
+ * starts at out + c n_0; reading c23). */
 MGPBD_API mgpbd_status mgpbd_get_near_kernel(mgpbd_ctx* ctx, double* out);
 /* Run the setup on caller-given level-0 values (nnz doubles in the pattern's CSR order), then the
  * Galerkin refresh and coarse inversion on the same values (identical-input-bits tests). */

@@ -19,6 +19,7 @@
 #include "vagal.cuh"
 #include "coarse.cuh"
 #include "coarse_res.cuh"
+#include "nullspace.cuh"
 
 namespace mgpbd {
 
@@ -40,6 +41,7 @@ struct EngineBase {
     virtual void level_sizes(int l, int64_t* n, int64_t* nnz) = 0;
     virtual void get_level(int l, int64_t* rowptr, int32_t* col, double* val) = 0;
     virtual void get_prolongator(int l, double* p) = 0;
+    virtual void get_prolongator_csr(int l, int64_t* nnz, int64_t* rowptr, int32_t* col, double* val) = 0;
     virtual void get_aggregates(int l, int32_t* a) = 0;
     virtual void get_near_kernel(double* b) = 0;
     virtual void debug_setup_from(const double* vals) = 0;
@@ -89,6 +91,13 @@ class Engine : public EngineBase {
         // rows this rank processes in the hot loop (partitioned level 0); coarse levels: all rows
         int32_t own0 = 0, own1 = -1;
         int32_t own_n() const { return (own1 < 0 ? n : own1) - own0; }
+        // k > 1 near kernel (f2, nullspace.cuh): general prolongator towards level+1 and the block Galerkin
+        int kk = 1;
+        KProlongator kp;
+        DBuf<T> kQs, kpval, kW, kones;
+        DBuf<double> kW64;
+        DBuf<int64_t> arow, xoff;   // aggregate-level coarse pattern (rows), block offsets per entry
+        DBuf<int32_t> acol, erow;
         void configure(cudaStream_t s) {
             const int32_t nl = own_n();
             vl = choose_vl(n, nnz);
@@ -131,6 +140,7 @@ class Engine : public EngineBase {
     cudaStream_t st = nullptr;
     bool own_stream = false;
     int kind = 2, kc = 2;
+    int kk = 1;  // near-kernel vectors per aggregate (cfg.k_nullspace)
     int32_t nv = 0, m = 0;
     DBuf<int32_t> verts;
     DBuf<double> x, v, x_old, w, sqrtw, alpha, rest, vol, lambda;
@@ -291,6 +301,7 @@ class Engine : public EngineBase {
     Engine(const mgpbd_mesh* mesh, const mgpbd_constraints* cons, const double* inv_mass, const double* comp,
            const mgpbd_config* c) {
         cfg = *c;
+        kk = cfg.k_nullspace;
         MG_CK(cudaSetDevice(cfg.device));
         if (cfg.stream) st = (cudaStream_t)cfg.stream;
         else { MG_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)); own_stream = true; }
@@ -510,7 +521,7 @@ class Engine : public EngineBase {
                     trace("colour", l);
                 }
                 const DBuf<int32_t>& col_ = colours0;
-                B.resize(a.n);
+                B.resize((size_t)a.n * kk);
                 GsOperator gop;
                 const bool gs_mf = cfg.level0_operator == 1 && mf_ready && h64.n && !va_off;
                 if (gs_mf) {  // the sweeps through H H^T + diag(at) (fp64 setup values)
@@ -519,9 +530,11 @@ class Engine : public EngineBase {
                     gop.kc = kc; gop.nv = nv; gop.verts = verts.p; gop.h = h64.p; gop.vptr = vptr.p;
                     gop.vlist = vlist.p; gop.at = at64.p; gop.dinv = a.dinv64.p;
                 }
-                gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed, B.p, st,
-                             gs_mf ? &gop : nullptr);
-                d2d(B0.p, B.p, a.n, st);
+                for (int c = 0; c < kk; ++c)  // k columns: hash index offset c n (reading c23)
+                    gs_bootstrap(a.n, a.rowptr, a.col, a.val64.p, col_.p, ncolours, cfg.bootstrap_sweeps, cfg.seed,
+                                 B.p + (size_t)c * a.n, st, gs_mf ? &gop : nullptr, (uint64_t)c * (uint64_t)a.n);
+                B0.resize((size_t)m * kk);
+                d2d(B0.p, B.p, (size_t)a.n * kk, st);
                 trace("gs_bootstrap", l);
             }
             a.n_agg = na;
@@ -535,6 +548,48 @@ class Engine : public EngineBase {
             }
             DBuf<int32_t> cnt;
             group_by_key(a.agg.p, a.n, na, a.mptr, a.mlist, cnt, st, true);
+            if (kk > 1) {  // k columns: per-aggregate QR injection (readings c24, c25)
+                a.kk = kk;
+                const int32_t nc = qr_prolongator(a.n, na, kk, a.agg.p, a.mptr.p, a.mlist.p, B.p, 1e-10, a.kp, Bn, st);
+                trace("members+qr_prolongator", l);
+                if ((double)nc > cfg.stall_ratio * (double)a.n) { a.kk = 1; break; }  // coarse DOFs decide (c7)
+                galerkin_symbolic(a.n, a.rowptr, a.col, a.agg.p, a.mptr.p, a.mlist.p, na, a.plan, a.arow, a.acol, st);
+                L.emplace_back(new Level());
+                Level& c = *L[l + 1];
+                Level& a2 = *L[l];
+                kgal_expand(na, a2.arow.p, a2.acol.p, a2.kp.coff.p, c.rowptr_own, c.col_own, a2.xoff, a2.erow, st);
+                c.n = nc;
+                c.nnz = read_scalar(c.rowptr_own.p + nc, st);
+                c.rowptr = c.rowptr_own.p; c.col = c.col_own.p;
+                c.configure(st);
+                c.val64.resize(c.nnz); c.dinv64.resize(c.n);
+                a2.kW64.resize((size_t)std::max<int64_t>(a2.plan.T, 1) * kk);
+                kgal_numeric<double>(a2.plan, a2.rowptr, a2.col, a2.val64.p, kk, a2.kp.pptr.p, a2.kp.pval64.p,
+                                     a2.kp.coff.p, a2.agg.p, na, a2.erow.p, a2.acol.p, a2.xoff.p, c.rowptr, nc,
+                                     a2.kW64.p, c.val64.p, c.dinv64.p, st);
+                trace("k-galerkin", l);
+                double lam;
+                if (l == 0 && mf64_ok && mf_ready && h64.n) {
+                    mf64.h = h64.p;
+                    mf64.dinv = a2.dinv64.p;
+                    mf_refresh<double>(mf64, alpha.p, last_dt, a2.dinv64.p, st);
+                    lam = power_method_op(
+                        m, a2.grid,
+                        [&](const double* xv, double* yv, double* pp) {
+                            mf_pass<double>(PASS_POWER, mf64, xv, nullptr, yv, nullptr, 0.0, pp, nullptr, st);
+                            return mf64.grid;
+                        },
+                        cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
+                } else {
+                    lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
+                }
+                set_smoother(a2, lam);
+                trace("power", l);
+                B.swap(Bn);
+                nL = l + 2;
+                pw_v.resize(std::max<size_t>(pw_v.n, (size_t)nc)); pw_w.resize(std::max<size_t>(pw_w.n, (size_t)nc));
+                continue;
+            }
             a.P64.resize(a.n);
             Bn.resize(na);
             prolongator(na, a.mptr.p, a.mlist.p, B.p, a.P64.p, Bn.p, st);
@@ -544,7 +599,7 @@ class Engine : public EngineBase {
             Level& a2 = *L[l];  // re-bind after emplace (unique_ptr: stable)
             // matrix-free level 0: P^T A_0 P from the fp64 gradients (vertex-aggregate form, vagal.cuh) — no
             // CSR Galerkin plan over the 1.4 GB level-0 pattern; the VA plan is the hot loop's as well
-            const bool va_setup = l == 0 && cfg.level0_operator == 1 && mf_ready && h64.n && !va_off;
+            const bool va_setup = l == 0 && cfg.level0_operator == 1 && mf_ready && h64.n && !va_off && kk == 1;
             if (va_setup) {
                 GalerkinPlan& gp = a2.plan;  // not used: drop a CSR plan left by an earlier setup
                 gp.gperm.free_all(); gp.tptr.free_all(); gp.tstart.free_all(); gp.trow.free_all();
@@ -605,7 +660,16 @@ class Engine : public EngineBase {
         for (int l = 0; l < nL; ++l) {
             Level& a = *L[l];
             if (l > 0) { a.val.resize(a.nnz); a.dinv.resize(a.n); alloc_vectors(a); }
-            if (l + 1 < nL) {
+            if (l + 1 < nL && a.kk > 1) {
+                a.kQs.resize((size_t)a.n * a.kk);
+                convert<double, T>(a.kp.Qs64.p, a.kQs.p, (int64_t)a.n * a.kk, st);
+                a.kpval.resize(a.kp.pcol.n);
+                convert<double, T>(a.kp.pval64.p, a.kpval.p, (int64_t)a.kp.pcol.n, st);
+                a.kW.resize((size_t)std::max<int64_t>(a.plan.T, 1) * a.kk);
+                a.kones.resize(a.n);
+                std::vector<T> ones((size_t)a.n, (T)1);
+                h2d(a.kones.p, ones.data(), a.n, st);
+            } else if (l + 1 < nL) {
                 a.P.resize(a.n);
                 convert<double, T>(a.P64.p, a.P.p, a.n, st);
                 a.tval.resize(a.plan.T);
@@ -618,7 +682,7 @@ class Engine : public EngineBase {
             MG_CK(cudaMemsetAsync(a.tval.p, 0, sizeof(T) * (a.plan.T ? a.plan.T : 1), st));
         }
         va_ok = va_built && nL > 1;
-        if (!va_ok && cfg.level0_operator == 1 && nL > 1) {
+        if (!va_ok && cfg.level0_operator == 1 && nL > 1 && kk == 1) {
             va_symbolic(nv, kc, vptr.p, vlist.p, L[0]->agg.p, L[0]->n_agg, L[1]->rowptr, L[1]->col, L[1]->nnz, va, st);
             va_ok = true;
             trace("va_symbolic");
@@ -626,7 +690,7 @@ class Engine : public EngineBase {
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
         ccyc_ok = false;
-        if (use_coarse_kernel && cfg.smoother != 2 && ccyc_from >= 1 && nL >= ccyc_from + 2) {
+        if (use_coarse_kernel && cfg.smoother != 2 && kk == 1 && ccyc_from >= 1 && nL >= ccyc_from + 2) {
             ccyc = CoarseCycle<T>();
             ccyc.K = nL - ccyc_from;
             ccyc.nu = cfg.smoother_sweeps;
@@ -700,6 +764,14 @@ class Engine : public EngineBase {
         for (int l = 0; l + 1 < nL; ++l) {
             Level& a = *L[l];
             Level& c = *L[l + 1];
+            if (a.kk > 1) {  // block Galerkin of the k > 1 hierarchy (nullspace.cuh) from the level's CSR values
+                if (l == 0 && mf_on())  // the hot loop is matrix-free: assemble A_0's values for the product
+                    assemble<T>(kind, m, verts.p, h.p, alpha.p, last_dt, rowptr0.p, col0.p, a.vl, a.val.p, a.dinv.p, st,
+                                r0, r1);
+                kgal_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.kk, a.kp.pptr.p, a.kpval.p, a.kp.coff.p, a.agg.p,
+                                a.n_agg, a.erow.p, a.acol.p, a.xoff.p, c.rowptr, c.n, a.kW.p, c.val.p, c.dinv.p, st);
+                continue;
+            }
             if (l == 0 && va_ok && mf_on()) {  // from h directly (replicated on every rank, no collective)
                 va_numeric<T>(va, kc, h.p, (mf.e0 == 0 && mf.e1 == mf.ninc) ? (const T*)mf.hv : nullptr, a.P.p, a.mptr.p,
                               a.mlist.p, mf.at, a.n_agg, c.rowptr, c.val.p, c.dinv.p, st);
@@ -742,11 +814,18 @@ class Engine : public EngineBase {
             const Csr<T> A = a.hot();
             MG_CK(cudaMemsetAsync(cur, 0, sizeof(T) * a.n, st));
             for (int sw = 0; sw < nu; ++sw) gs_sweep<T>(A, a.gs_ptr.p, a.gs_list.p, a.gs_ncol, false, b, cur, st);
-            pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
             Level& c = *L[l + 1];
-            restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
-            vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
-            prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
+            if (a.kk > 1) {
+                pass(l, PASS_RESID_P, cur, b, a.vt.p, a.kones.p, 0.0);
+                krestrict<T>(c.n, a.kk, a.kp.dof_agg.p, a.kp.coff.p, a.mptr.p, a.mlist.p, a.kQs.p, a.vt.p, c.vb.p, st);
+                vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+                kprolong<T>(o, cn, a.kp.pptr.p, a.kp.pcol.p, a.kpval.p, c.vz.p, cur, st);
+            } else {
+                pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
+                restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
+                vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+                prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
+            }
             for (int sw = 0; sw < nu; ++sw) gs_sweep<T>(A, a.gs_ptr.p, a.gs_list.p, a.gs_ncol, true, b, cur, st);
             d2d(x_out, cur, a.n, st);
             if (dot_r) {  // the partials of r.z and r.r the PCG finalisation expects
@@ -760,12 +839,19 @@ class Engine : public EngineBase {
             pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.sm_omega[sw], a.sm_alpha[sw], sw == 1 ? nullptr : nxt);
             std::swap(cur, nxt);
         }
-        pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
         Level& c = *L[l + 1];
-        restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
-        if (l == 0 && dist) comm->allreduce(c.vb.p, (size_t)c.n, st);  // partial sums of split aggregates
-        vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
-        prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
+        if (a.kk > 1) {  // general P (k > 1): r = b - A x, b_c = P^T r, x += P e
+            pass(l, PASS_RESID_P, cur, b, a.vt.p, a.kones.p, 0.0);
+            krestrict<T>(c.n, a.kk, a.kp.dof_agg.p, a.kp.coff.p, a.mptr.p, a.mlist.p, a.kQs.p, a.vt.p, c.vb.p, st);
+            vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+            kprolong<T>(o, cn, a.kp.pptr.p, a.kp.pcol.p, a.kpval.p, c.vz.p, cur, st);
+        } else {
+            pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
+            restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
+            if (l == 0 && dist) comm->allreduce(c.vb.p, (size_t)c.n, st);  // partial sums of split aggregates
+            vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+            prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
+        }
         for (int sw = 0; sw < nu; ++sw) {
             const bool last = sw == nu - 1;
             T* other = cur == a.vx.p ? a.vy.p : a.vx.p;  // holds x_{sw-1} for sw >= 1
@@ -1093,9 +1179,28 @@ class Engine : public EngineBase {
         }
         MG_CK(cudaStreamSynchronize(st));
     }
+    void get_prolongator_csr(int l, int64_t* nnz, int64_t* rp, int32_t* cl, double* vals) override {
+        check_level(l);
+        if (!have_hier || l >= nL - 1) throw Error(MGPBD_E_ARG, "coarsest level has no prolongator");
+        const Level& a = *L[l];
+        if (a.kk > 1) {
+            *nnz = (int64_t)a.kp.pcol.n;
+            if (rp) d2h(rp, a.kp.pptr.p, (size_t)a.n + 1, st);
+            if (cl) d2h(cl, a.kp.pcol.p, a.kp.pcol.n, st);
+            if (vals) d2h(vals, a.kp.pval64.p, a.kp.pcol.n, st);
+        } else {
+            *nnz = a.n;
+            if (cl) d2h(cl, a.agg.p, a.n, st);
+            if (vals) d2h(vals, a.P64.p, a.n, st);
+            if (rp)
+                for (int64_t i = 0; i <= a.n; ++i) rp[i] = i;
+        }
+        MG_CK(cudaStreamSynchronize(st));
+    }
     void get_prolongator(int l, double* pv) override {
         check_level(l);
         if (!have_hier || l >= nL - 1) throw Error(MGPBD_E_ARG, "coarsest level has no prolongator");
+        if (L[l]->kk > 1) throw Error(MGPBD_E_ARG, "k_nullspace > 1: use mgpbd_get_prolongator_csr");
         d2h(pv, L[l]->P64.p, L[l]->n, st);
         MG_CK(cudaStreamSynchronize(st));
     }
@@ -1107,7 +1212,7 @@ class Engine : public EngineBase {
     }
     void get_near_kernel(double* bout) override {
         if (!have_hier || nL < 2) throw Error(MGPBD_E_ARG, "no bootstrapped near kernel (single-level hierarchy)");
-        d2h(bout, B0.p, m, st);
+        d2h(bout, B0.p, (size_t)m * kk, st);
         MG_CK(cudaStreamSynchronize(st));
     }
     void debug_setup_from(const double* vals) override {
@@ -1277,7 +1382,9 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cons->n_cons <= 0 || !cons->verts) return fail("bad constraint set");
     if ((int64_t)cons->n_cons * cons->kind >= ((int64_t)1 << 31)) return fail("too many constraints");
     if (cfg->precision != 0 && cfg->precision != 1) return fail("precision must be 0 (fp64) or 1 (fp32)");
-    if (cfg->k_nullspace != 1) return fail("only k_nullspace = 1 is implemented (reading c1)");
+    if (cfg->k_nullspace < 1 || cfg->k_nullspace > 8) return fail("k_nullspace must be in 1..8 (reading c1; f2)");
+    if (cfg->k_nullspace > 1 && (cfg->world > 1 || cfg->vgroup || cfg->nccl_id))
+        return fail("k_nullspace > 1 runs on one rank");
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail("bad rank/world");
     if (cfg->world > 1 && !cfg->nccl_id && !cfg->vgroup) return fail("world > 1 needs nccl_id or vgroup");
     if (cfg->level0_operator != 0 && cfg->level0_operator != 1) return fail("level0_operator must be 0 or 1");
@@ -1364,6 +1471,11 @@ mgpbd_status mgpbd_get_level_sizes(mgpbd_ctx* ctx, int32_t l, int64_t* n, int64_
 }
 mgpbd_status mgpbd_get_level(mgpbd_ctx* ctx, int32_t l, int64_t* rowptr, int32_t* cols, double* vals) {
     return guarded(ctx, [&] { ctx->eng->get_level(l, rowptr, cols, vals); });
+}
+mgpbd_status mgpbd_get_prolongator_csr(mgpbd_ctx* ctx, int32_t l, int64_t* nnz, int64_t* rowptr, int32_t* col,
+                                       double* val) {
+    if (!nnz) return MGPBD_E_ARG;
+    return guarded(ctx, [&] { ctx->eng->get_prolongator_csr(l, nnz, rowptr, col, val); });
 }
 mgpbd_status mgpbd_get_prolongator(mgpbd_ctx* ctx, int32_t l, double* p) {
     if (ctx && !p) return MGPBD_E_ARG;

@@ -196,9 +196,9 @@ __global__ void k_absmax_parts(int64_t nnz, const double* __restrict__ val, doub
         if (threadIdx.x == 0) parts[blockIdx.x] = v;
     }
 }
-__global__ void k_gs_init(int32_t n, uint64_t base, const double* __restrict__ maxabs, double* __restrict__ x) {
+__global__ void k_gs_init(int32_t n, uint64_t base, uint64_t off, const double* __restrict__ maxabs, double* __restrict__ x) {
     int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) x[i] = hunit(hkey(base, (uint64_t)i)) * (*maxabs);
+    if (i < n) x[i] = hunit(hkey(base, (uint64_t)i + off)) * (*maxabs);
 }
 // one colour class of a GS sweep on A x = 0: x_i = -(sum_{j != i} A_ij x_j) / A_ii
 __global__ void k_gs_colour(int64_t cnt, const int32_t* __restrict__ rows, const int64_t* __restrict__ rowptr,
@@ -536,14 +536,15 @@ int32_t colour(int32_t n, const int64_t* rowptr, const int32_t* col, uint64_t se
 }
 
 void gs_bootstrap(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, const int32_t* colours,
-                  int32_t ncolours, int32_t sweeps, uint64_t seed, double* B, cudaStream_t s, const GsOperator* op) {
+                  int32_t ncolours, int32_t sweeps, uint64_t seed, double* B, cudaStream_t s, const GsOperator* op,
+                  uint64_t idx_offset) {
     int64_t nnz = read_scalar(rowptr + n, s);
     DBuf<double> parts, mx;
     parts.resize(1024); mx.resize(2);
     k_absmax_parts<<<1024, 256, 0, s>>>(nnz, val, parts.p);
     MG_LAUNCH_CHECK();
     finalize_max(parts.p, 1024, mx.p, s);
-    k_gs_init<<<g1(n), 256, 0, s>>>(n, hkey_base(seed, 3, 0), mx.p, B);
+    k_gs_init<<<g1(n), 256, 0, s>>>(n, hkey_base(seed, 3, 0), idx_offset, mx.p, B);
     MG_LAUNCH_CHECK();
     DBuf<int64_t> cptr; DBuf<int32_t> clist, cnt;
     group_by_key(colours, n, ncolours, cptr, clist, cnt, s, /*sort=*/false);

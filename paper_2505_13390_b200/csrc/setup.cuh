@@ -39,9 +39,10 @@ struct GsOperator {
 // vertices' u — rows of one colour share no vertex (they are not coupled in A), so the updates are
 // race-free and the result is Gauss-Seidel's (rounding aside) at ~1/4 of the CSR sweep's bytes.  The
 // CSR values still give x_0's scale max |A_ij| (reading c0).
+// idx_offset: the hash index of x_0[i] is i + idx_offset (column c of a k > 1 bootstrap: c n, reading c23).
 void gs_bootstrap(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, const int32_t* colours,
                   int32_t ncolours, int32_t sweeps, uint64_t seed, double* B, cudaStream_t s,
-                  const GsOperator* op = nullptr);
+                  const GsOperator* op = nullptr, uint64_t idx_offset = 0);
 
 // Inject (k = 1): P_i = B_i / ||B_agg(i)||, B_next[a] = ||B_a|| (members ascending).
 void prolongator(int32_t n_agg, const int64_t* mptr, const int32_t* mlist, const double* B, double* P,

@@ -20,7 +20,7 @@ SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgp
            "mgpbd_get_positions", "mgpbd_get_velocities", "mgpbd_get_lambda", "mgpbd_get_stats",
            "mgpbd_get_level_sizes", "mgpbd_get_level", "mgpbd_get_prolongator", "mgpbd_get_aggregates",
            "mgpbd_get_near_kernel", "mgpbd_debug_setup_from", "mgpbd_debug_vcycle", "mgpbd_debug_pcg",
-           "mgpbd_debug_prepare",
+           "mgpbd_debug_prepare", "mgpbd_get_prolongator_csr",
            "mgpbd_pass_burst",
            "mgpbd_last_error", "mgpbd_destroy", "mgpbd_nccl_unique_id", "mgpbd_vgroup_create",
            "mgpbd_vgroup_destroy", "mgpbd_partition_rows", "mgpbd_halo_plan"]
@@ -94,6 +94,7 @@ def lib():
             "mgpbd_get_level_sizes": (C.c_int, [P, i32, P, P]),
             "mgpbd_get_level": (C.c_int, [P, i32, P, P, P]),
             "mgpbd_get_prolongator": (C.c_int, [P, i32, P]),
+            "mgpbd_get_prolongator_csr": (C.c_int, [P, i32, P, P, P, P]),
             "mgpbd_get_aggregates": (C.c_int, [P, i32, P]),
             "mgpbd_get_near_kernel": (C.c_int, [P, P]),
             "mgpbd_debug_setup_from": (C.c_int, [P, P]),
@@ -280,6 +281,15 @@ class Context:
         self._ck(lib().mgpbd_get_prolongator(self.h, l, _p(out)))
         return out
 
+    def prolongator_csr(self, l):
+        """Level-l prolongator as CSR (rowptr, col, val) — k_nullspace > 1 (and k = 1 in the same form)."""
+        nnz = C.c_int64()
+        self._ck(lib().mgpbd_get_prolongator_csr(self.h, l, C.byref(nnz), None, None, None))
+        n, _ = self.level_size(l)
+        r = np.empty(n + 1, np.int64); c = np.empty(nnz.value, np.int32); v = np.empty(nnz.value)
+        self._ck(lib().mgpbd_get_prolongator_csr(self.h, l, C.byref(nnz), _p(r), _p(c), _p(v)))
+        return r, c, v
+
     def aggregates(self, l):
         n, _ = self.level_size(l)
         out = np.empty(n, np.int32)
@@ -287,9 +297,11 @@ class Context:
         return out
 
     def near_kernel(self):
-        out = np.empty(self.m)
+        """n (k = 1) or n x k (k_nullspace > 1) bootstrapped near-kernel vectors of level 0."""
+        k = max(int(self.cfg.k_nullspace), 1)
+        out = np.empty(self.m * k)
         self._ck(lib().mgpbd_get_near_kernel(self.h, _p(out)))
-        return out
+        return out if k == 1 else out.reshape(k, self.m).T.copy()
 
     def debug_setup_from(self, vals):
         vals = np.ascontiguousarray(vals, np.float64)

@@ -67,7 +67,7 @@ def test_config_default_and_create_validation(libpath):
     with pytest.raises(mgpbd.MgpbdError):                           # empty constraint set
         mgpbd.Context(2, np.zeros((0, 2), np.int32), X, np.ones(2), np.ones(0))
     for kw in (dict(smoother=3), dict(level0_operator=2), dict(pcg_tol=-1.0), dict(pcg_iters=5000),
-               dict(k_nullspace=6), dict(precision=2), dict(smoother_sweeps=0)):
+               dict(k_nullspace=9), dict(k_nullspace=0), dict(precision=2), dict(smoother_sweeps=0)):
         with pytest.raises(mgpbd.MgpbdError) as e:
             mgpbd.Context(2, np.array([[0, 1]], np.int32), X, np.ones(2), np.ones(1), **kw)
         assert e.value.status == mgpbd.E_ARG, kw                     # host validation, no device work

@@ -1,0 +1,102 @@
+"""GPU parity of the k > 1 near-kernel variant (readings c23-c25)
+against the oracle: setup on identical input bits (aggregates and patterns bit-exact, k bootstrapped columns,
+QR prolongator, block coarse operators, omega), V-cycle / MGPCG on the identical hierarchy, and whole
+frames (matrix-free and CSR level 0, fp64 and fp32)."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2505_13390_b200 import mgpbd, scenes
+
+pytestmark = pytest.mark.gpu
+
+CASES = ["bar3k", "block_small", "cloth64"]
+
+
+def make_scene(name):
+    if name == "cloth64":
+        return scenes.cloth(64, dt=3e-3, n_iters=5)
+    return scenes.make(name)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, float), np.asarray(b, float)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def ocfg(sc, k, **kw):
+    return O.default_config(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters, k_nullspace=k, **kw)
+
+
+def oracle_setup(sc, k):
+    sim = O.Sim(sc, ocfg(sc, k))
+    sim.step(sc.dt, 1)
+    r, c, v = sim.A()
+    return r, c, v, O.Hierarchy(r, c, v, ocfg(sc, k))
+
+
+@pytest.mark.parametrize("k", [6, 3])
+@pytest.mark.parametrize("name", CASES)
+def test_setup_identical_input_bits_k(name, k):
+    sc = make_scene(name)
+    r, c, v, h = oracle_setup(sc, k)
+    ctx = mgpbd.Context.from_scene(sc, k_nullspace=k)
+    ctx.debug_setup_from(v)
+    st = ctx.stats()
+    assert st.n_levels == h.n_levels >= 2
+    assert rel(ctx.near_kernel(), h.B0()) <= 1e-10
+    for l in range(h.n_levels):
+        rg, cg, vg = ctx.level(l)
+        ro, co, vo = h.level(l)
+        assert np.array_equal(rg, ro) and np.array_equal(cg, co), l
+        assert np.abs(vg - vo).max() <= 1e-11 * np.abs(vo).max(), l
+        if l + 1 < h.n_levels:
+            assert np.array_equal(ctx.aggregates(l), h.agg(l)), l
+            pg, po = ctx.prolongator_csr(l), h.P_csr(l)
+            assert np.array_equal(pg[0], po[0]) and np.array_equal(pg[1], po[1]), l
+            assert np.abs(pg[2] - po[2]).max() <= 1e-11, l
+            assert np.isclose(st.omega[l], h.omega(l), rtol=1e-10), l
+    ctx.close()
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_vcycle_and_pcg_identical_hierarchy_k6(name):
+    sc = make_scene(name)
+    r, c, v, h = oracle_setup(sc, 6)
+    ctx = mgpbd.Context.from_scene(sc, k_nullspace=6)
+    ctx.debug_setup_from(v)
+    b = np.random.default_rng(0).normal(size=sc.n_cons)
+    assert rel(ctx.debug_vcycle(b), h.vcycle(b)) <= 1e-10
+    for K in (1, 3, 10):
+        xo, rc, _ = h.pcg(b, K)
+        assert rel(ctx.debug_pcg(b, K), xo) <= 1e-8, K
+    ctx.close()
+
+
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp64", "fp32"])
+@pytest.mark.parametrize("op", [0, 1], ids=["csr", "matfree"])
+@pytest.mark.parametrize("name", CASES)
+def test_frame_k6(name, op, precision):
+    sc = make_scene(name)
+    sim = O.Sim(sc, ocfg(sc, 6))
+    assert sim.step(sc.dt, sc.n_iters) == 0
+    ctx = mgpbd.Context.from_scene(sc, k_nullspace=6, level0_operator=op, precision=precision)
+    ctx.step(sc.dt, sc.n_iters)
+    xo, vo, lo = sim.state()
+    tol = 1e-6 if precision == 0 else 1e-3
+    assert rel(ctx.lambdas(), lo) <= tol
+    assert rel(ctx.positions() - sc.pos, xo - sc.pos) <= tol
+    assert rel(ctx.velocities(), vo) <= tol
+    st = ctx.stats()
+    assert st.n_levels == sim.hierarchy().n_levels
+    if precision == 0:
+        assert st.indefinite_events == sim.indefinite_events()
+    ctx.close()
+
+
+def test_k_nullspace_argument_checks():
+    sc = scenes.make("cloth16")
+    with pytest.raises(mgpbd.MgpbdError):
+        mgpbd.Context.from_scene(sc, k_nullspace=9)
+    with pytest.raises(mgpbd.MgpbdError):
+        mgpbd.Context.from_scene(sc, k_nullspace=0)
