@@ -128,7 +128,10 @@ __device__ __forceinline__ void dense_solve(const Lanes& w, int32_t n, const Sli
 
 template <class T>
 __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_constant__ CoarseCycle<T> c,
-                                                             const __grid_constant__ ResPlan plan) {
+                                                             const __grid_constant__ ResPlan plan, int mode,
+                                                             int kstop) {
+    // mode 0: the whole cycle; 1: down phase of levels 0..kstop-1 (ends with b of level kstop); 2: up phase
+    // from level kstop-1 (z of level kstop given) — levels >= kstop then run on the cluster tail kernel
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
@@ -166,8 +169,9 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
     const int K = sc.K, nu = sc.nu;
     auto slice = [&](int k) { return Slice<T>{smem, slv[k]}; };
     T* cur[16];
+    const int kdown = mode == 0 ? K - 1 : kstop;
     // ---- down
-    for (int k = 0; k + 1 < K; ++k) {
+    for (int k = 0; k < kdown && mode != 2; ++k) {
         const CoarseLevel<T>& L = sc.L[k];
         const Slice<T> S = slice(k);
         const T* __restrict__ b = L.b;
@@ -198,13 +202,15 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
         restrict_t(w, L, S, sc.L[k + 1].b);
         grid.sync(); mark();
     }
+    if (mode == 1) return;
     // ---- coarsest
-    dense_solve(w, sc.L[K - 1].n, slice(K - 1), sc.L[K - 1].b, sc.L[K - 1].z);
+    if (mode == 0) dense_solve(w, sc.L[K - 1].n, slice(K - 1), sc.L[K - 1].b, sc.L[K - 1].z);
     // ---- up
-    for (int k = K - 2; k >= 0; --k) {
+    for (int k = mode == 0 ? K - 2 : kstop - 1; k >= 0; --k) {
         const CoarseLevel<T>& L = sc.L[k];
         const Slice<T> S = slice(k);
-        T* __restrict__ cu = cur[k];
+        // the buffer the down phase left the pre-smoothed x in (mode 2: recomputed from nu)
+        T* __restrict__ cu = mode == 2 ? ((nu >= 2 && ((nu - 2) & 1)) ? L.y : L.x) : cur[k];
         T* ot = cu == L.x ? L.y : L.x;
         const T* __restrict__ zc = sc.L[k + 1].z;
         const T* __restrict__ P = L.P;
@@ -240,7 +246,7 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
 template <class T>
 bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vector<ResLevel>& lv,
                      std::vector<ResCopy>& copies, std::vector<int32_t>& ncopies, std::vector<uint32_t>& tx,
-                     uint32_t& smem, cudaStream_t s) {
+                     uint32_t& smem, cudaStream_t s, bool with_coarsest) {
     const int K = c.K;
     if (K < 2 || K > 16) return false;
     std::vector<std::vector<int32_t>> rb(K), ab(K);
@@ -308,7 +314,7 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
                 ok = ok && add(d.o_agg, L.agg, d.r0, 4, (size_t)rows);
                 ok = ok && add(d.o_mp, L.mptr, d.a0, 8, (size_t)(d.a1 - d.a0) + 1);
                 ok = ok && add(d.o_ml, L.mlist, d.m0, 4, (size_t)mem);
-            } else {
+            } else if (with_coarsest) {
                 ok = ok && add(d.o_val, c.Ainv, (int64_t)d.r0 * L.n, 8, (size_t)rows * L.n);
             }
             if (!ok) return false;
@@ -321,7 +327,7 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
 }
 
 template <class T>
-void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s) {
+void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s, int mode, int kstop) {
     ensure_dyn_smem((const void*)k_coarse_vcycle_res<T>, plan.smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.G);
@@ -333,7 +339,7 @@ void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_
     attr_[0].val.cooperative = 1;
     cfg.attrs = attr_;
     cfg.numAttrs = 1;
-    MG_CK(cudaLaunchKernelEx(&cfg, k_coarse_vcycle_res<T>, c, plan));
+    MG_CK(cudaLaunchKernelEx(&cfg, k_coarse_vcycle_res<T>, c, plan, mode, kstop));
     MG_LAUNCH_CHECK();
 }
 
@@ -351,8 +357,8 @@ int coarse_res_blocks_per_sm(uint32_t smem) {
 #define MG_INST(T)                                                                                             \
     template bool coarse_res_plan<T>(const CoarseCycle<T>&, int, uint32_t, std::vector<ResLevel>&,             \
                                      std::vector<ResCopy>&, std::vector<int32_t>&, std::vector<uint32_t>&,     \
-                                     uint32_t&, cudaStream_t);                                                 \
-    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t);                \
+                                     uint32_t&, cudaStream_t, bool);                                           \
+    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t, int, int);      \
     template int coarse_res_blocks_per_sm<T>(uint32_t);
 MG_INST(float)
 MG_INST(double)

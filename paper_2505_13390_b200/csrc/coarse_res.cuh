@@ -40,13 +40,17 @@ struct ResPlan {
 
 // Host: build the plan for cycle `c` (host copies of each level's rowptr / mptr are downloaded).
 // Returns false if some CTA's slices exceed `smem_cap` bytes (then the global kernel is used).
+// with_coarsest = false: the last level of `c` gets no slices (the cycle is split around the cluster tail,
+// coarse_tail.cuh, whose first level is c's last).
 template <class T>
 bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vector<ResLevel>& lv,
                      std::vector<ResCopy>& copies, std::vector<int32_t>& ncopies, std::vector<uint32_t>& tx,
-                     uint32_t& smem, cudaStream_t s);
+                     uint32_t& smem, cudaStream_t s, bool with_coarsest = true);
 
+// mode 0: the whole cycle; 1: down phase of levels 0..kstop-1 (leaves b of level kstop); 2: up phase from
+// level kstop-1 (reads z of level kstop).
 template <class T>
-void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s);
+void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s, int mode = 0, int kstop = 0);
 // CTAs of k_coarse_vcycle_res<T> that fit on one SM with `smem` dynamic bytes (0: the resident plan
 // cannot be launched cooperatively at one CTA per SM; the caller falls back to the global kernel)
 template <class T>

@@ -20,6 +20,7 @@
 #include "coarse.cuh"
 #include "coarse_res.cuh"
 #include "nullspace.cuh"
+#include "coarse_tail.cuh"
 
 namespace mgpbd {
 
@@ -223,6 +224,17 @@ class Engine : public EngineBase {
     DBuf<uint32_t> res_tx;
     bool res_ok = false;
     bool use_res = std::getenv("MGPBD_NO_RES_COARSE") == nullptr;
+    // smallest levels on one thread-block cluster (coarse_tail.cuh); the levels above it run as the down /
+    // up halves of the resident kernel over a truncated cycle.  MGPBD_NO_TAIL=1 disables
+    TailPlan tail;
+    bool tail_ok = false;
+    bool use_tail = std::getenv("MGPBD_NO_TAIL") == nullptr;
+    CoarseCycle<T> ccyc_top;
+    ResPlan res_top;
+    DBuf<ResLevel> rt_lv;
+    DBuf<ResCopy> rt_cp;
+    DBuf<int32_t> rt_nc;
+    DBuf<uint32_t> rt_tx;
     int ccyc_from = std::getenv("MGPBD_COARSE_FROM") ? std::atoi(std::getenv("MGPBD_COARSE_FROM")) : 1;
     bool mf_on() const { return cfg.level0_operator == 1 && mf_ready; }
 
@@ -735,15 +747,58 @@ class Engine : public EngineBase {
                 }
             }
         }
+        tail_ok = false;
+        if (ccyc_ok && res_ok && use_tail) setup_tail();
         if (tracing)
-            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B\n", nL,
-                         !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u);
+            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, tail %s\n", nL,
+                         !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u,
+                         tail_ok ? ("from cycle level " + std::to_string(tail.first) + " on " + std::to_string(tail.CT) +
+                                    " CTAs, " + std::to_string(tail.smem) + " B").c_str() : "off");
         invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
         stale = false;
         (void)l0;
         MG_CK(cudaStreamSynchronize(st));
         trace("hot buffers");
+    }
+
+    // Cluster tail of the coarse cycle: plan it on 16 (else 8) CTAs; the top part of the cycle becomes a
+    // truncated cycle (levels 0..first of ccyc, the last one only receiving b / providing z) run by the
+    // resident kernel's down and up halves.
+    void setup_tail() {
+        int sms = 148;
+        MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
+        const uint32_t cap = 220u * 1024u;
+        for (int CT : {16, 8}) {
+            if (coarse_tail_plan<T>(ccyc, 1, CT, cap, tail, st) && coarse_tail_launchable<T>(CT, tail.smem)) {
+                tail_ok = true;
+                break;
+            }
+        }
+        if (!tail_ok) return;
+        ccyc_top = ccyc;
+        ccyc_top.K = tail.first + 1;
+        std::vector<ResLevel> lv;
+        std::vector<ResCopy> cp;
+        std::vector<int32_t> nc;
+        std::vector<uint32_t> tx;
+        uint32_t smem = 0;
+        if (!coarse_res_plan<T>(ccyc_top, sms, cap, lv, cp, nc, tx, smem, st, /*with_coarsest=*/false) ||
+            coarse_res_blocks_per_sm<T>(smem) < 1) {
+            tail_ok = false;
+            return;
+        }
+        rt_lv.resize(lv.size()); h2d(rt_lv.p, lv.data(), lv.size(), st);
+        rt_cp.resize(cp.size()); h2d(rt_cp.p, cp.data(), cp.size(), st);
+        rt_nc.resize(nc.size()); h2d(rt_nc.p, nc.data(), nc.size(), st);
+        rt_tx.resize(tx.size()); h2d(rt_tx.p, tx.data(), tx.size(), st);
+        res_top.G = sms;
+        res_top.smem = smem;
+        res_top.lv = rt_lv.p;
+        res_top.copies = rt_cp.p;
+        res_top.ncopies = rt_nc.p;
+        res_top.txbytes = rt_tx.p;
+        MG_CK(cudaStreamSynchronize(st));
     }
 
     // MGPBD_TRACE=1: host wall time of the setup phases (stream synchronised at every mark).
@@ -802,8 +857,15 @@ class Engine : public EngineBase {
             return;
         }
         if (l == ccyc_from && ccyc_ok && b == a.vb.p && x_out == a.vz.p) {
-            if (res_ok) coarse_vcycle_res<T>(ccyc, res_plan, st);
-            else coarse_vcycle<T>(ccyc, st);
+            if (tail_ok) {  // grid-wide down half, cluster tail, grid-wide up half
+                coarse_vcycle_res<T>(ccyc_top, res_top, st, 1, tail.first);
+                coarse_tail_run<T>(ccyc, tail, st);
+                coarse_vcycle_res<T>(ccyc_top, res_top, st, 2, tail.first);
+            } else if (res_ok) {
+                coarse_vcycle_res<T>(ccyc, res_plan, st);
+            } else {
+                coarse_vcycle<T>(ccyc, st);
+            }
             return;
         }
         const int nu = cfg.smoother_sweeps;
