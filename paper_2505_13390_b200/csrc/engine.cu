@@ -708,8 +708,8 @@ class Engine : public EngineBase {
             ccyc.nu = cfg.smoother_sweeps;
             ccyc.Ainv = Ainv.p;
             if (std::getenv("MGPBD_TRACE_COARSE")) {
-                ctrace.resize(64);
-                MG_CK(cudaMemsetAsync(ctrace.p, 0, 64 * sizeof(unsigned long long), st));
+                ctrace.resize(128);  // [0, 32): grid-wide kernel (down half), [32, 64): cluster tail, [64, 96): up half
+                MG_CK(cudaMemsetAsync(ctrace.p, 0, 128 * sizeof(unsigned long long), st));
                 ccyc.trace = ctrace.p;
             }
             for (int l = ccyc_from; l < nL; ++l) {
@@ -860,7 +860,9 @@ class Engine : public EngineBase {
             if (tail_ok) {  // grid-wide down half, cluster tail, grid-wide up half
                 coarse_vcycle_res<T>(ccyc_top, res_top, st, 1, tail.first);
                 coarse_tail_run<T>(ccyc, tail, st);
-                coarse_vcycle_res<T>(ccyc_top, res_top, st, 2, tail.first);
+                CoarseCycle<T> up = ccyc_top;
+                if (up.trace) up.trace += 64;
+                coarse_vcycle_res<T>(up, res_top, st, 2, tail.first);
             } else if (res_ok) {
                 coarse_vcycle_res<T>(ccyc, res_plan, st);
             } else {
@@ -1125,12 +1127,22 @@ class Engine : public EngineBase {
                          us(0, 1), us(1, 2), us(2, 3), us(3, 4), us(6, 7), us(7, 8), us(8, 9), us(4, 5));
         }
         if (ccyc.trace) {  // phase times of the last coarse V-cycle (MGPBD_TRACE_COARSE)
-            unsigned long long tt[64];
-            d2h(tt, ctrace.p, 64, st);
+            unsigned long long tt[128];
+            d2h(tt, ctrace.p, 128, st);
             MG_CK(cudaStreamSynchronize(st));
-            std::fprintf(stderr, "[mgpbd coarse] K=%d phases (us):", ccyc.K);
-            for (int k = 1; k < 64 && tt[k] > tt[k - 1]; ++k) std::fprintf(stderr, " %.2f", (tt[k] - tt[k - 1]) * 1e-3);
-            std::fprintf(stderr, "\n");
+            const char* names[3] = {"grid", "tail", "up"};
+            unsigned long long prev_end = 0;
+            for (int part = 0; part < 3; ++part) {
+                const unsigned long long* p = tt + 32 * part;
+                if (!p[0]) continue;
+                int nmark = 1;
+                while (nmark < 32 && p[nmark] >= p[nmark - 1] && p[nmark]) ++nmark;
+                std::fprintf(stderr, "[mgpbd coarse] K=%d %s (gap %.2f us, %.2f us total) phases (us):", ccyc.K, names[part],
+                             prev_end ? (double)(p[0] - prev_end) * 1e-3 : 0.0, (double)(p[nmark - 1] - p[0]) * 1e-3);
+                for (int k = 1; k < nmark; ++k) std::fprintf(stderr, " %.2f", (p[k] - p[k - 1]) * 1e-3);
+                std::fprintf(stderr, "\n");
+                prev_end = p[nmark - 1];
+            }
         }
         frame++;
         n_b = iters_run;
