@@ -197,6 +197,12 @@ class Engine : public EngineBase {
     // matrix-free level-0 operator (cfg.level0_operator == 1, matfree.cuh)
     MatFree<T> mf;
     DBuf<T> mf_hv, mf_at, mf_u;
+    // padded vertex-major layout shared by mf and mf64 (matfree.cuh)
+    DBuf<int64_t> mf_ppos;
+    DBuf<int32_t> mf_vsrc, mf_vj32, mf_jbase;
+    DBuf<uint16_t> mf_vj16, mf_v16;
+    DBuf<int32_t> mf_vbase;
+    int64_t mf_npad = 0;
     // fp64 matrix-free operator for the setup's level-0 power method (reading c18: setup in fp64)
     MatFree<double> mf64;
     DBuf<double> mf64_hv, mf64_at, mf64_u;
@@ -263,6 +269,51 @@ class Engine : public EngineBase {
         }
         dsc.resize(4);
     }
+    // Padded vertex-major incidence layout of the hot vertex gather (matfree.cuh): vertex v's incidences
+    // (vlist order) at ppos[v] .. ppos[v] + deg(v), zero-padded to a multiple of 4; constraint indices as
+    // 16-bit offsets from the vertex's smallest one when every vertex spans < 65536 constraints.
+    std::vector<int64_t> ppos_h;
+    void build_padded_layout(const std::vector<int64_t>& hp) {
+        const int64_t ninc = hp[nv];
+        std::vector<int32_t> vl((size_t)ninc);
+        d2h(vl.data(), vlist.p, (size_t)ninc, st);
+        MG_CK(cudaStreamSynchronize(st));
+        ppos_h.assign((size_t)nv + 1, 0);
+        for (int32_t v = 0; v < nv; ++v) ppos_h[v + 1] = ppos_h[v] + ((hp[v + 1] - hp[v] + 3) & ~(int64_t)3);
+        mf_npad = ppos_h[nv];
+        std::vector<int32_t> src((size_t)mf_npad, -1), jb((size_t)nv, 0), j32((size_t)mf_npad, 0);
+        bool fits16 = true;
+        for (int32_t v = 0; v < nv; ++v) {
+            int32_t jmin = INT32_MAX, jmax = -1;
+            for (int64_t e = hp[v]; e < hp[v + 1]; ++e) {
+                const int32_t j = vl[e] / kc;
+                jmin = std::min(jmin, j); jmax = std::max(jmax, j);
+                src[ppos_h[v] + (e - hp[v])] = vl[e];
+                j32[ppos_h[v] + (e - hp[v])] = j;
+            }
+            jb[v] = jmax < 0 ? 0 : jmin;
+            if (jmax >= 0 && jmax - jmin >= 65536) fits16 = false;
+            for (int64_t p = ppos_h[v] + (hp[v + 1] - hp[v]); p < ppos_h[v + 1]; ++p) j32[p] = jb[v];  // pads: x[jbase]
+        }
+        if (std::getenv("MGPBD_NO_VJ16")) fits16 = false;
+        mf_ppos.resize((size_t)nv + 1); h2d(mf_ppos.p, ppos_h.data(), (size_t)nv + 1, st);
+        mf_vsrc.resize((size_t)mf_npad); h2d(mf_vsrc.p, src.data(), (size_t)mf_npad, st);
+        mf_jbase.resize((size_t)nv); h2d(mf_jbase.p, jb.data(), (size_t)nv, st);
+        if (fits16) {
+            std::vector<uint16_t> j16((size_t)mf_npad);
+            for (int32_t v = 0; v < nv; ++v)
+                for (int64_t p = ppos_h[v]; p < ppos_h[v + 1]; ++p) j16[p] = (uint16_t)(j32[p] - jb[v]);
+            mf_vj16.resize((size_t)mf_npad); h2d(mf_vj16.p, j16.data(), (size_t)mf_npad, st);
+            mf_vj32.free_all();
+        } else {
+            mf_vj32.resize((size_t)mf_npad); h2d(mf_vj32.p, j32.data(), (size_t)mf_npad, st);
+            mf_vj16.free_all();
+            std::vector<int32_t> zero((size_t)nv, 0);
+            h2d(mf_jbase.p, zero.data(), (size_t)nv, st);   // absolute indices
+        }
+        MG_CK(cudaStreamSynchronize(st));
+    }
+
     void setup_matfree() {
         // vertices touched by this rank's rows: their incidences reference only owned or halo rows
         std::vector<int32_t> hv_((size_t)(r1 - r0) * kc);
@@ -279,7 +330,11 @@ class Engine : public EngineBase {
         mf.v0 = vmax < 0 ? 0 : vmin; mf.v1 = vmax < 0 ? 0 : vmax + 1;
         mf.verts = verts.p; mf.h = h.p; mf.vptr = vptr.p; mf.vlist = vlist.p;
         mf.ninc = hp[nv]; mf.e0 = hp[mf.v0]; mf.e1 = hp[mf.v1];
-        mf_hv.resize(3 * (size_t)mf.ninc); mf_at.resize(m); mf_u.resize(4 * (size_t)nv);
+        build_padded_layout(hp);
+        mf.ppos = mf_ppos.p; mf.npad = mf_npad; mf.vsrc = mf_vsrc.p; mf.jbase = mf_jbase.p;
+        mf.vj16 = mf_vj16.n ? mf_vj16.p : nullptr; mf.vj32 = mf_vj32.n ? mf_vj32.p : nullptr;
+        mf.p0 = ppos_h[mf.v0]; mf.p1 = ppos_h[mf.v1];
+        mf_hv.resize(3 * (size_t)mf_npad); mf_at.resize(m); mf_u.resize(4 * (size_t)nv);
         MG_CK(cudaMemsetAsync(mf_u.p, 0, sizeof(T) * 4 * (size_t)nv, st));
         mf.hv = mf_hv.p; mf.at = mf_at.p; mf.u = mf_u.p;
         mf.dinv = L[0]->dinv.p;
@@ -288,7 +343,10 @@ class Engine : public EngineBase {
             mf64.kc = kc; mf64.m = m; mf64.row0 = 0; mf64.row1 = m; mf64.v0 = 0; mf64.v1 = nv;
             mf64.verts = verts.p; mf64.vptr = vptr.p; mf64.vlist = vlist.p;
             mf64.ninc = hp[nv]; mf64.e0 = 0; mf64.e1 = hp[nv];
-            mf64_hv.resize(3 * (size_t)mf64.ninc); mf64_at.resize(m); mf64_u.resize(4 * (size_t)nv);
+            mf64.ppos = mf_ppos.p; mf64.npad = mf_npad; mf64.vsrc = mf_vsrc.p; mf64.jbase = mf_jbase.p;
+            mf64.vj16 = mf.vj16; mf64.vj32 = mf.vj32;
+            mf64.p0 = 0; mf64.p1 = mf_npad;
+            mf64_hv.resize(3 * (size_t)mf_npad); mf64_at.resize(m); mf64_u.resize(4 * (size_t)nv);
             MG_CK(cudaMemsetAsync(mf64_u.p, 0, sizeof(double) * 4 * (size_t)nv, st));
             mf64.hv = mf64_hv.p; mf64.at = mf64_at.p; mf64.u = mf64_u.p;
             mf64.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
@@ -296,7 +354,19 @@ class Engine : public EngineBase {
             mf64_ok = true;
         }
         mf.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
-        mf.grid = mf.tma ? mf_grid_tma(r0, r1, (int)sizeof(T), kc) : mf_grid(r1 - r0);
+        int vbytes = 4;
+        if (mf.tma && !std::getenv("MGPBD_NO_V16")) {  // 16-bit vertex offsets per TMA tile (8 B per row saved)
+            std::vector<int32_t> hvt((size_t)m * kc);
+            d2h(hvt.data(), verts.p, hvt.size(), st);
+            MG_CK(cudaStreamSynchronize(st));
+            if (mf_build_v16(r0, r1, kc, hvt, mf_v16, mf_vbase, st)) {
+                mf.v16 = mf_v16.p; mf.vbase = mf_vbase.p;
+                vbytes = 2;
+                if (mf64_ok) { mf64.v16 = mf_v16.p; mf64.vbase = mf_vbase.p; }   // same tiling (one rank: r0 = 0)
+            }
+        }
+        if (mf64_ok && mf64.tma) mf64.grid = mf_grid_tma(0, m, 8, kc, vbytes);
+        mf.grid = mf.tma ? mf_grid_tma(r0, r1, (int)sizeof(T), kc, vbytes) : mf_grid(r1 - r0);
         if (const char* cap = std::getenv("MGPBD_MF_GRID_CAP")) {  // tests: many tiles per CTA (TMA ring wraps)
             const int c = std::max(1, std::atoi(cap));
             mf.grid = std::min(mf.grid, c);
@@ -409,9 +479,11 @@ class Engine : public EngineBase {
         if (mf_on()) {
             // matrix-free: vertex gather (hv planes, vlist, vptr, u write) + row gather (verts, h, at,
             // u read once per vertex); x is read by both kernels
-            const double nvr = (double)(mf.v1 - mf.v0), ne = (double)(mf.e1 - mf.e0);
-            mat = ne * (3 * s + 4) + 8.0 * (nvr + 1) + nvr * 4 * s                      // gather
-                  + mrows * (4.0 * kc + 3.0 * kc * s + s) + nvr * 4 * s + mrows * s;    // rows
+            // padded slots: 3 planes + the 16/32-bit constraint index; per vertex ppos, jbase, u
+            const double nvr = (double)(mf.v1 - mf.v0), np = (double)(mf.p1 - mf.p0);
+            const double jb = mf.vj16 ? 2.0 : 4.0;
+            mat = np * (3 * s + jb) + 8.0 * (nvr + 1) + (mf.vj16 ? 4.0 * nvr : 0.0) + nvr * 4 * s   // gather
+                  + mrows * ((mf.v16 ? 2.0 : 4.0) * kc + 3.0 * kc * s + s) + nvr * 4 * s + mrows * s;  // rows
         }
         double vec;
         switch (mode) {
@@ -629,7 +701,8 @@ class Engine : public EngineBase {
             c.configure(st);
             c.val64.resize(c.nnz); c.dinv64.resize(c.n);
             if (va_setup) {
-                va_symbolic(nv, kc, vptr.p, vlist.p, a2.agg.p, na, c.rowptr, c.col, c.nnz, va, st);
+                va_symbolic(nv, kc, vptr.p, vlist.p, a2.agg.p, na, c.rowptr, c.col, c.nnz, va, st,
+                            mf_ppos.n ? mf_ppos.p : nullptr, mf_npad);
                 va_numeric<double>(va, kc, h64.p, nullptr, a2.P64.p, a2.mptr.p, a2.mlist.p, at64.p, na, c.rowptr, c.val64.p,
                                    c.dinv64.p, st);
                 va_built = true;
@@ -695,7 +768,8 @@ class Engine : public EngineBase {
         }
         va_ok = va_built && nL > 1;
         if (!va_ok && cfg.level0_operator == 1 && nL > 1 && kk == 1) {
-            va_symbolic(nv, kc, vptr.p, vlist.p, L[0]->agg.p, L[0]->n_agg, L[1]->rowptr, L[1]->col, L[1]->nnz, va, st);
+            va_symbolic(nv, kc, vptr.p, vlist.p, L[0]->agg.p, L[0]->n_agg, L[1]->rowptr, L[1]->col, L[1]->nnz, va, st,
+                        mf_ppos.n ? mf_ppos.p : nullptr, mf_npad);
             va_ok = true;
             trace("va_symbolic");
         }
@@ -828,7 +902,7 @@ class Engine : public EngineBase {
                 continue;
             }
             if (l == 0 && va_ok && mf_on()) {  // from h directly (replicated on every rank, no collective)
-                va_numeric<T>(va, kc, h.p, (mf.e0 == 0 && mf.e1 == mf.ninc) ? (const T*)mf.hv : nullptr, a.P.p, a.mptr.p,
+                va_numeric<T>(va, kc, h.p, (mf.p0 == 0 && mf.p1 == mf.npad) ? (const T*)mf.hv : nullptr, a.P.p, a.mptr.p,
                               a.mlist.p, mf.at, a.n_agg, c.rowptr, c.val.p, c.dinv.p, st);
                 mark_stage(1);
                 continue;
@@ -1018,7 +1092,7 @@ class Engine : public EngineBase {
         mark_stage(4);
         timed(PH_UPD, [&] {
             if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
-            if (mf_on() && !dist && mf.e0 == 0 && mf.e1 == mf.ninc)  // hv covers every incidence
+            if (mf_on() && !dist && mf.p0 == 0 && mf.p1 == mf.npad)  // hv covers every incidence
                 mf_update<T>(mf, xs.p, sqrtw.p, omega_dev.p, x.p, st);                       // l.9, l.11
             else
                 update_positions<T>(nv, kc, vptr.p, vlist.p, h.p, sqrtw.p, xs.p, omega_dev.p, x.p, st);

@@ -1,5 +1,7 @@
 // Matrix-free level-0 operator, see matfree.cuh.
 #include <algorithm>
+#include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include "matfree.cuh"
@@ -19,20 +21,21 @@ struct alignas(4 * sizeof(T)) V4 {
     T x, y, z, w;
 };
 
-// hv[plane][e] = h[vlist[e]][plane] for the incidences of vertices [v0, v1); at_i = alpha_i / dt^2 for
-// all rows; dinv_i = 1 / (sum_s |h_{i,s}|^2 + at_i) for rows [r0, r1) — the assembly's diagonal formula
-// (mesh.cu k_assemble), so the smoother does not need the assembled matrix.
+// hv[plane][p] = h[vsrc[p]][plane] (0 on pad slots) for the padded slots [p0, p1) of the vertices
+// [v0, v1); at_i = alpha_i / dt^2 for all rows; dinv_i = 1 / (sum_s |h_{i,s}|^2 + at_i) for rows [r0, r1) —
+// the assembly's diagonal formula (mesh.cu k_assemble), so the smoother does not need the assembled matrix.
 template <class T, int KC>
-__global__ void k_mf_refresh(int64_t e0, int64_t e1, int64_t ninc, const int32_t* __restrict__ vlist,
+__global__ void k_mf_refresh(int64_t p0, int64_t p1, int64_t npad, const int32_t* __restrict__ vsrc,
                              const T* __restrict__ h, T* __restrict__ hv, int32_t m, int32_t r0, int32_t r1,
                              const double* __restrict__ alpha, double dt2, T* __restrict__ at,
                              T* __restrict__ dinv) {
     const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t e = e0 + tid; e < e1; e += nt) {
-        const T* p = h + (int64_t)vlist[e] * 3;
-        hv[e] = p[0];
-        hv[ninc + e] = p[1];
-        hv[2 * ninc + e] = p[2];
+    for (int64_t p = p0 + tid; p < p1; p += nt) {
+        const int32_t code = vsrc[p];
+        const T* q = h + (int64_t)(code < 0 ? 0 : code) * 3;
+        hv[p] = code < 0 ? (T)0 : q[0];
+        hv[npad + p] = code < 0 ? (T)0 : q[1];
+        hv[2 * npad + p] = code < 0 ? (T)0 : q[2];
     }
     for (int64_t i = tid; i < m; i += nt) {
         const double a = alpha[i] / dt2;
@@ -50,107 +53,150 @@ __global__ void k_mf_refresh(int64_t e0, int64_t e1, int64_t ninc, const int32_t
     }
 }
 
-// u_v = sum over v's incidences of h_{j,s} x_j: G lanes per vertex, lane partials in incidence order
-// strided by G, fixed butterfly (deterministic).
-template <class T, int KC, int G>
-__global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, int64_t ninc,
-                                                      const int64_t* __restrict__ vptr,
-                                                      const int32_t* __restrict__ vlist, const T* __restrict__ hv,
+// One 16-byte chunk of a vertex's padded incidence list: VW = 16 / sizeof(T) incidences of the three h planes
+// and their constraint indices (16- or 32-bit).
+template <class T, bool J16>
+struct Chunk {
+    static constexpr int VW = 16 / (int)sizeof(T);
+    T hx[VW], hy[VW], hz[VW];
+    int32_t j[VW];
+    __device__ __forceinline__ void load(const T* __restrict__ hx_, const T* __restrict__ hy_, const T* __restrict__ hz_,
+                                         const uint16_t* __restrict__ j16, const int32_t* __restrict__ j32, int64_t p,
+                                         bool in) {
+        using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+        if (in) {
+            const VT a = __ldcs(reinterpret_cast<const VT*>(hx_ + p));   // streamed once per pass: evict first
+            const VT b = __ldcs(reinterpret_cast<const VT*>(hy_ + p));
+            const VT c = __ldcs(reinterpret_cast<const VT*>(hz_ + p));
+            memcpy(hx, &a, 16); memcpy(hy, &b, 16); memcpy(hz, &c, 16);
+            if constexpr (J16 && VW == 4) {
+                const uint2 w = __ldcs(reinterpret_cast<const uint2*>(j16 + p));
+                j[0] = (int32_t)(w.x & 0xFFFFu); j[1] = (int32_t)(w.x >> 16);
+                j[2] = (int32_t)(w.y & 0xFFFFu); j[3] = (int32_t)(w.y >> 16);
+            } else if constexpr (J16) {
+                const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(j16 + p));
+                j[0] = (int32_t)(w & 0xFFFFu); j[1] = (int32_t)(w >> 16);
+            } else if constexpr (VW == 4) {
+                const int4 w = __ldcs(reinterpret_cast<const int4*>(j32 + p));
+                j[0] = w.x; j[1] = w.y; j[2] = w.z; j[3] = w.w;
+            } else {
+                const int2 w = __ldcs(reinterpret_cast<const int2*>(j32 + p));
+                j[0] = w.x; j[1] = w.y;
+            }
+        } else {
+#pragma unroll
+            for (int w = 0; w < VW; ++w) { hx[w] = hy[w] = hz[w] = (T)0; j[w] = 0; }
+        }
+    }
+};
+
+// u_v = sum over v's incidences of h_{j,s} x_j over the padded vertex-major layout: G lanes per vertex, each
+// lane streams 16-byte chunks (UN per round: all loads, then all x gathers, then the sums), fixed butterfly
+// (deterministic).  Accumulation in the storage precision unless MGPBD_VG_ACC64 (fp32 -> fp64 conversions
+// are quarter-rate on sm_100a; DESIGN.md §2 reading c18 records the measured cost and parity impact).
+#ifndef MGPBD_VG_ACC64
+#define MGPBD_VG_ACC64 0
+#endif
+template <class T, int G, int UN, bool J16>
+__global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
+                                                      const int64_t* __restrict__ ppos,
+                                                      const uint16_t* __restrict__ vj16,
+                                                      const int32_t* __restrict__ vj32,
+                                                      const int32_t* __restrict__ jbase, const T* __restrict__ hv,
                                                       const T* __restrict__ x, V4<T>* __restrict__ u) {
     // programmatic dependent launch: the row kernel may start streaming its static operands now; it
     // waits (griddepcontrol.wait) for this grid's u before gathering it
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    using CH = Chunk<T, J16>;
+    constexpr int VW = CH::VW;
     constexpr int PER_WARP = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const T* __restrict__ hx = hv;
-    const T* __restrict__ hy = hv + ninc;
-    const T* __restrict__ hz = hv + 2 * ninc;
-    // warp-uniform trip count: the butterfly below needs the whole warp
-    for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {
+    const T* __restrict__ hy = hv + npad;
+    const T* __restrict__ hz = hv + 2 * npad;
+    for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {  // warp-uniform
         const int64_t v = base + sub;
-        T a0 = (T)0, a1 = (T)0, a2 = (T)0;
+        using AC = typename std::conditional<MGPBD_VG_ACC64 != 0, double, T>::type;
+        AC a0 = (AC)0, a1 = (AC)0, a2 = (AC)0;
         if (v < v1) {
-            // chunks of UN incidences per lane: all index/h loads, then all x gathers, then the FMAs,
-            // so a chunk costs two dependent round trips instead of two per incidence
-#ifndef MGPBD_VG_UN
-#define MGPBD_VG_UN 6  // swept on B200 (profiles/r1/sweep_level0_pass.txt): 6 > 4 > 8 > 2
-#endif
-            constexpr int UN = MGPBD_VG_UN;
-            const int64_t e0 = vptr[v], e1 = vptr[v + 1];
-            for (int64_t eb = e0 + sl; eb < e1; eb += G * UN) {
-                int32_t cj[UN];
-                T px[UN], py[UN], pz[UN], xv[UN];
+            const int64_t p0 = ppos[v], p1 = ppos[v + 1];
+            const int32_t jb = J16 ? jbase[v] : 0;
+            for (int64_t pb = p0 + (int64_t)sl * VW; pb < p1; pb += (int64_t)G * VW * UN) {
+                CH c[UN];
 #pragma unroll
                 for (int q = 0; q < UN; ++q) {
-                    const int64_t e = eb + q * G;
-                    const bool in = e < e1;
-                    cj[q] = in ? vlist[e] / KC : -1;
-                    px[q] = in ? hx[e] : (T)0;
-                    py[q] = in ? hy[e] : (T)0;
-                    pz[q] = in ? hz[e] : (T)0;
+                    const int64_t p = pb + (int64_t)q * G * VW;
+                    c[q].load(hx, hy, hz, vj16, vj32, p, p < p1);
                 }
+                T xv[UN][VW];
 #pragma unroll
-                for (int q = 0; q < UN; ++q) xv[q] = cj[q] >= 0 ? x[cj[q]] : (T)0;
+                for (int q = 0; q < UN; ++q)
 #pragma unroll
-                for (int q = 0; q < UN; ++q) {
-                    a0 += px[q] * xv[q];
-                    a1 += py[q] * xv[q];
-                    a2 += pz[q] * xv[q];
-                }
+                    for (int w = 0; w < VW; ++w) xv[q][w] = x[jb + c[q].j[w]];
+#pragma unroll
+                for (int q = 0; q < UN; ++q)
+#pragma unroll
+                    for (int w = 0; w < VW; ++w) {
+                        a0 += (AC)c[q].hx[w] * (AC)xv[q][w];
+                        a1 += (AC)c[q].hy[w] * (AC)xv[q][w];
+                        a2 += (AC)c[q].hz[w] * (AC)xv[q][w];
+                    }
             }
         }
         a0 = group_sum_t<G>(a0);
         a1 = group_sum_t<G>(a1);
         a2 = group_sum_t<G>(a2);
-        if (v < v1 && sl == 0) u[v] = V4<T>{a0, a1, a2, (T)0};
+        if (v < v1 && sl == 0) u[v] = V4<T>{(T)a0, (T)a1, (T)a2, (T)0};
     }
 }
 
 // Eq. 5 position update from the vertex-major gradients: x_v += omega sqrt(w_v) sum_{(j,s) at v}
-// h_{j,s} dl_j, G lanes per vertex over the vertex's contiguous incidences in hv (coalesced planes
-// instead of one scattered 12-byte record per incidence), fp64 lane partials, fixed butterfly.
-template <class T, int KC, int G>
-__global__ void __launch_bounds__(MF_BS) k_mf_update(int32_t v0, int32_t v1, int64_t ninc,
-                                                     const int64_t* __restrict__ vptr,
-                                                     const int32_t* __restrict__ vlist, const T* __restrict__ hv,
+// h_{j,s} dl_j over the same padded layout (fp64 lane partials, fixed butterfly).
+template <class T, int G, int UN, bool J16>
+__global__ void __launch_bounds__(MF_BS) k_mf_update(int32_t v0, int32_t v1, int64_t npad,
+                                                     const int64_t* __restrict__ ppos,
+                                                     const uint16_t* __restrict__ vj16,
+                                                     const int32_t* __restrict__ vj32,
+                                                     const int32_t* __restrict__ jbase, const T* __restrict__ hv,
                                                      const T* __restrict__ dl, const double* __restrict__ sqrtw,
                                                      const double* __restrict__ omega_p, double* __restrict__ x) {
+    using CH = Chunk<T, J16>;
+    constexpr int VW = CH::VW;
     constexpr int PER_WARP = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     const T* __restrict__ hx = hv;
-    const T* __restrict__ hy = hv + ninc;
-    const T* __restrict__ hz = hv + 2 * ninc;
+    const T* __restrict__ hy = hv + npad;
+    const T* __restrict__ hz = hv + 2 * npad;
     for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {  // warp-uniform
         const int64_t v = base + sub;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
         if (v < v1) {
-            constexpr int UN = 4;
-            const int64_t e0 = vptr[v], e1 = vptr[v + 1];
-            for (int64_t eb = e0 + sl; eb < e1; eb += G * UN) {
-                int32_t cj[UN];
-                T px[UN], py[UN], pz[UN];
-                double dv[UN];
+            const int64_t p0 = ppos[v], p1 = ppos[v + 1];
+            const int32_t jb = J16 ? jbase[v] : 0;
+            for (int64_t pb = p0 + (int64_t)sl * VW; pb < p1; pb += (int64_t)G * VW * UN) {
+                CH c[UN];
 #pragma unroll
                 for (int q = 0; q < UN; ++q) {
-                    const int64_t e = eb + q * G;
-                    const bool in = e < e1;
-                    cj[q] = in ? vlist[e] / KC : -1;
-                    px[q] = in ? hx[e] : (T)0;
-                    py[q] = in ? hy[e] : (T)0;
-                    pz[q] = in ? hz[e] : (T)0;
+                    const int64_t p = pb + (int64_t)q * G * VW;
+                    c[q].load(hx, hy, hz, vj16, vj32, p, p < p1);
                 }
+                double dv[UN][VW];
 #pragma unroll
-                for (int q = 0; q < UN; ++q) dv[q] = cj[q] >= 0 ? (double)dl[cj[q]] : 0.0;
+                for (int q = 0; q < UN; ++q)
 #pragma unroll
-                for (int q = 0; q < UN; ++q) {
-                    a0 += (double)px[q] * dv[q];
-                    a1 += (double)py[q] * dv[q];
-                    a2 += (double)pz[q] * dv[q];
-                }
+                    for (int w = 0; w < VW; ++w) dv[q][w] = (double)dl[jb + c[q].j[w]];
+#pragma unroll
+                for (int q = 0; q < UN; ++q)
+#pragma unroll
+                    for (int w = 0; w < VW; ++w) {
+                        a0 += (double)c[q].hx[w] * dv[q][w];
+                        a1 += (double)c[q].hy[w] * dv[q][w];
+                        a2 += (double)c[q].hz[w] * dv[q][w];
+                    }
             }
         }
         a0 = group_sum<G>(a0);
@@ -237,11 +283,12 @@ constexpr int MF_R = MGPBD_MF_R;  // rows per tile (= threads per CTA)
 #endif
 constexpr int MF_STAGES = MGPBD_MF_STAGES;  // ring depth (overridable at build time for tuning sweeps)
 
-template <class T, int KC>
+template <class T, int KC, bool V16>
 struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 128 or 256)
+    static constexpr uint32_t VB = V16 ? 2 : 4;  // bytes per vertex index (16-bit: offset from the tile's base)
     static constexpr uint32_t H = 0;
     static constexpr uint32_t V = H + MF_R * KC * 3 * sizeof(T);
-    static constexpr uint32_t X = V + MF_R * KC * sizeof(int32_t);
+    static constexpr uint32_t X = V + MF_R * KC * VB;
     static constexpr uint32_t AT = X + MF_R * sizeof(T);
     static constexpr uint32_t D = AT + MF_R * sizeof(T);
     static constexpr uint32_t B = D + MF_R * sizeof(T);
@@ -250,16 +297,17 @@ struct TileLayout {  // byte offsets inside one stage (every section 16-B aligne
     static constexpr uint32_t BYTES = XP + MF_R * sizeof(T);
 };
 
-template <class T, int KC, int MODE>
+template <class T, int KC, int MODE, bool V16>
 __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1, int32_t tbase, int32_t ntiles,
-                                                      const int32_t* __restrict__ verts, const T* __restrict__ h,
+                                                      const void* __restrict__ verts_, const int32_t* __restrict__ vbase,
+                                                      const T* __restrict__ h,
                                                       const V4<T>* __restrict__ u, const T* __restrict__ at,
                                                       const T* __restrict__ dinv, const T* __restrict__ x,
                                                       const T* __restrict__ b, T* __restrict__ y,
                                                       const T* __restrict__ aux, double omega, double alpha,
                                                       const T* __restrict__ xprev, double* __restrict__ parts,
                                                       double* __restrict__ parts2) {
-    using LY = TileLayout<T, KC>;
+    using LY = TileLayout<T, KC, V16>;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[MF_STAGES];
     constexpr bool ND = MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER;
@@ -279,13 +327,13 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
         const int32_t i0 = tbase + tile * MF_R;
         const int32_t rows = min(MF_R, row1 - i0);
         auto rnd = [](uint32_t by) { return (by + 15u) & ~15u; };
-        const uint32_t bh = rnd(rows * KC * 3 * sizeof(T)), bv = rnd(rows * KC * sizeof(int32_t)),
+        const uint32_t bh = rnd(rows * KC * 3 * sizeof(T)), bv = rnd(rows * KC * LY::VB),
                        bs = rnd(rows * sizeof(T));
         uint32_t tot = bh + bv + 2 * bs + (ND ? bs : 0) + (NB ? bs : 0) + (NA ? bs : 0) + (NP ? bs : 0);
         uint64_t* bar = &bars[j % MF_STAGES];
         mbar_expect_tx(bar, tot);
         bulk_g2s(st + LY::H, h + (int64_t)i0 * KC * 3, bh, bar);
-        bulk_g2s(st + LY::V, verts + (int64_t)i0 * KC, bv, bar);
+        bulk_g2s(st + LY::V, reinterpret_cast<const unsigned char*>(verts_) + (int64_t)i0 * KC * LY::VB, bv, bar);
         bulk_g2s(st + LY::X, x + i0, bs, bar);
         bulk_g2s(st + LY::AT, at + i0, bs, bar);
         if (ND) bulk_g2s(st + LY::D, dinv + i0, bs, bar);
@@ -308,9 +356,16 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
             int vi[KC];
             T hi[KC][3];
             {
-                const int32_t* sv = reinterpret_cast<const int32_t*>(st + LY::V) + t * KC;
+                if (V16) {
+                    const uint16_t* sv = reinterpret_cast<const uint16_t*>(st + LY::V) + t * KC;
+                    const int32_t vb = vbase[blockIdx.x + j * gridDim.x];
 #pragma unroll
-                for (int k = 0; k < KC; ++k) vi[k] = sv[k];
+                    for (int k = 0; k < KC; ++k) vi[k] = vb + (int32_t)sv[k];
+                } else {
+                    const int32_t* sv = reinterpret_cast<const int32_t*>(st + LY::V) + t * KC;
+#pragma unroll
+                    for (int k = 0; k < KC; ++k) vi[k] = sv[k];
+                }
                 load_record<T, KC>(reinterpret_cast<const T*>(st + LY::H) + t * KC * 3, hi);
             }
             const T xi = reinterpret_cast<const T*>(st + LY::X)[t];
@@ -361,28 +416,39 @@ template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
                 double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
     if (A.v1 > A.v0) {
-#ifndef MGPBD_VG_G4
-#define MGPBD_VG_G4 4
+        // G lanes per vertex, UN 16-byte chunks per lane per round (~23 incidences per vertex on tets = 6 float4
+        // chunks, ~6 on cloth = 2); build-time overridable for tuning sweeps
+#ifndef MGPBD_VG_G
+#define MGPBD_VG_G 4
 #endif
-        constexpr int G = KC == 4 ? MGPBD_VG_G4 : 2;  // ~23 (tets) / ~6 (cloth) incidences per vertex
+#ifndef MGPBD_VG_UN
+#define MGPBD_VG_UN 2
+#endif
+        constexpr int G = KC == 4 ? MGPBD_VG_G : 2;
+        constexpr int UN = KC == 4 ? MGPBD_VG_UN : 1;
         const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
 #ifndef MGPBD_VG_CTAS_PER_SM
 #define MGPBD_VG_CTAS_PER_SM 16
 #endif
         int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
         if (A.vg_grid_cap > 0) grid = std::min(grid, A.vg_grid_cap);
-        k_mf_vgather<T, KC, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, x,
-                                                      reinterpret_cast<V4<T>*>(A.u));
+        if (A.vj16)
+            k_mf_vgather<T, G, UN, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase,
+                                                                A.hv, x, reinterpret_cast<V4<T>*>(A.u));
+        else
+            k_mf_vgather<T, G, UN, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase,
+                                                                 A.hv, x, reinterpret_cast<V4<T>*>(A.u));
         MG_LAUNCH_CHECK();
     }
     const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
     if (A.tma) {
         const int32_t tbase = A.row0 & ~3;  // 16-B aligned vector offsets
         const int32_t ntiles = (A.row1 - tbase + MF_R - 1) / MF_R;
-        const size_t smem = (size_t)MF_STAGES * TileLayout<T, KC>::BYTES;
-#define MG_MFT(M)                                                                                               \
+#define MG_MFT(M) { if (A.v16) MG_MFT2(M, true) else MG_MFT2(M, false) }
+#define MG_MFT2(M, V16)                                                                                         \
     {                                                                                                           \
-        ensure_dyn_smem((const void*)k_mf_rows_tma<T, KC, M>, smem);                                           \
+        const size_t smem = (size_t)MF_STAGES * TileLayout<T, KC, V16>::BYTES;                                  \
+        ensure_dyn_smem((const void*)k_mf_rows_tma<T, KC, M, V16>, smem);                                      \
         cudaLaunchConfig_t lc = {};                                                                             \
         lc.gridDim = dim3(A.grid);                                                                              \
         lc.blockDim = dim3(MF_R);                                                                               \
@@ -393,7 +459,8 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         la[0].val.programmaticStreamSerializationAllowed = 1;                                                   \
         lc.attrs = la;                                                                                          \
         lc.numAttrs = 1;                                                                                        \
-        MG_CK(cudaLaunchKernelEx(&lc, k_mf_rows_tma<T, KC, M>, A.row0, A.row1, tbase, ntiles, A.verts, A.h, u,   \
+        MG_CK(cudaLaunchKernelEx(&lc, k_mf_rows_tma<T, KC, M, V16>, A.row0, A.row1, tbase, ntiles,              \
+                                 V16 ? (const void*)A.v16 : (const void*)A.verts, A.vbase, A.h, u,              \
                                  (const T*)A.at, (const T*)A.dinv, x, b, y, aux, omega, alpha, xprev, parts,    \
                                  parts2));                                                                      \
     }
@@ -406,6 +473,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
             default: throw Error(-1, "mf_pass: bad mode");
         }
 #undef MG_MFT
+#undef MG_MFT2
         MG_LAUNCH_CHECK();
         return;
     }
@@ -430,10 +498,34 @@ int mf_grid(int32_t rows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)rows + MF_BS - 1) / MF_BS, 148 * 8));
 }
 
-int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc) {
+bool mf_build_v16(int32_t row0, int32_t row1, int kc, const std::vector<int32_t>& hverts, DBuf<uint16_t>& v16,
+                  DBuf<int32_t>& vbase, cudaStream_t s) {
     const int32_t tbase = row0 & ~3;
     const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + MF_R - 1) / MF_R);
-    const size_t stage = (size_t)MF_R * ((size_t)kc * 3 * tsize + (size_t)kc * 4 + 6 * (size_t)tsize);
+    const int64_t m = (int64_t)hverts.size() / kc;
+    std::vector<int32_t> vb((size_t)ntiles, 0);
+    std::vector<uint16_t> o((size_t)m * kc, 0);
+    for (int64_t t = 0; t < ntiles; ++t) {
+        const int64_t i0 = tbase + t * MF_R, i1 = std::min<int64_t>(i0 + MF_R, row1);
+        int32_t lo = INT32_MAX, hi = -1;
+        for (int64_t e = i0 * kc; e < i1 * kc; ++e) { lo = std::min(lo, hverts[e]); hi = std::max(hi, hverts[e]); }
+        if (hi < 0) continue;
+        if (hi - lo >= 65536) return false;
+        vb[t] = lo;
+        for (int64_t e = i0 * kc; e < i1 * kc; ++e) o[e] = (uint16_t)(hverts[e] - lo);
+    }
+    v16.resize((size_t)m * kc);
+    h2d(v16.p, o.data(), (size_t)m * kc, s);
+    vbase.resize((size_t)ntiles);
+    h2d(vbase.p, vb.data(), (size_t)ntiles, s);
+    MG_CK(cudaStreamSynchronize(s));
+    return true;
+}
+
+int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc, int vbytes) {
+    const int32_t tbase = row0 & ~3;
+    const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + MF_R - 1) / MF_R);
+    const size_t stage = (size_t)MF_R * ((size_t)kc * 3 * tsize + (size_t)kc * vbytes + 6 * (size_t)tsize);
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (MF_STAGES * stage + 1024)));
     int dev = 0, sms = 148;
     MG_CK(cudaGetDevice(&dev));
@@ -443,14 +535,14 @@ int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc) {
 
 template <class T>
 void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cudaStream_t s) {
-    const int64_t work = std::max<int64_t>(A.e1 - A.e0, A.m);
+    const int64_t work = std::max<int64_t>(A.p1 - A.p0, A.m);
     if (work <= 0) return;
     const int grid = (int)std::min<int64_t>((work + 255) / 256, 148 * 16);
     if (A.kc == 4)
-        k_mf_refresh<T, 4><<<grid, 256, 0, s>>>(A.e0, A.e1, A.ninc, A.vlist, A.h, A.hv, A.m, A.row0, A.row1, alpha,
+        k_mf_refresh<T, 4><<<grid, 256, 0, s>>>(A.p0, A.p1, A.npad, A.vsrc, A.h, A.hv, A.m, A.row0, A.row1, alpha,
                                                 dt * dt, A.at, dinv);
     else
-        k_mf_refresh<T, 2><<<grid, 256, 0, s>>>(A.e0, A.e1, A.ninc, A.vlist, A.h, A.hv, A.m, A.row0, A.row1, alpha,
+        k_mf_refresh<T, 2><<<grid, 256, 0, s>>>(A.p0, A.p1, A.npad, A.vsrc, A.h, A.hv, A.m, A.row0, A.row1, alpha,
                                                 dt * dt, A.at, dinv);
     MG_LAUNCH_CHECK();
 }
@@ -465,13 +557,17 @@ void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const 
 template <class T>
 void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const double* omega, double* x, cudaStream_t s) {
     if (A.v1 <= A.v0) return;
-    constexpr int G = 4;
-    const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
-    const int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * 16);
-    if (A.kc == 4)
-        k_mf_update<T, 4, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, dl, sqrtw, omega, x);
-    else
-        k_mf_update<T, 2, G><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.ninc, A.vptr, A.vlist, A.hv, dl, sqrtw, omega, x);
+    if (A.kc == 4) {  // same lane split as the vertex gather (G = 4, UN = 2: ~60 registers)
+        constexpr int G = 4;
+        const int grid = (int)std::min<int64_t>(((int64_t)(A.v1 - A.v0) * G + MF_BS - 1) / MF_BS, 148 * 16);
+        if (A.vj16) k_mf_update<T, G, 2, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
+        else k_mf_update<T, G, 2, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
+    } else {
+        constexpr int G = 2;
+        const int grid = (int)std::min<int64_t>(((int64_t)(A.v1 - A.v0) * G + MF_BS - 1) / MF_BS, 148 * 16);
+        if (A.vj16) k_mf_update<T, G, 1, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
+        else k_mf_update<T, G, 1, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
+    }
     MG_LAUNCH_CHECK();
 }
 

@@ -26,18 +26,36 @@ struct MatFree {
     const int32_t* vlist = nullptr; // constraint*kc + slot, ascending per vertex
     int64_t ninc = 0;               // vptr[nv]
     int64_t e0 = 0, e1 = 0;         // vptr[v0], vptr[v1]
-    T* hv = nullptr;                // vertex-major copy of h: [x | y | z] planes of ninc values
+    // padded vertex-major layout of the hot gathers: vertex v's incidences (vlist order) start at ppos[v], a
+    // multiple of 4, and are zero-padded to a multiple of 4, so every lane streams 16-byte vectors
+    const int64_t* ppos = nullptr;  // nv + 1
+    int64_t npad = 0;               // ppos[nv]
+    int64_t p0 = 0, p1 = 0;         // ppos[v0], ppos[v1]
+    const int32_t* vsrc = nullptr;  // npad: incidence code (constraint*kc + slot) of each padded slot, -1 = pad
+    const uint16_t* vj16 = nullptr; // npad: constraint index - jbase[v] (when every vertex spans < 65536 rows)
+    const int32_t* vj32 = nullptr;  // npad: constraint index (otherwise)
+    const int32_t* jbase = nullptr; // nv
+    T* hv = nullptr;                // vertex-major copy of h: [x | y | z] planes of npad values (padded layout)
     T* at = nullptr;                // alpha_i / dt^2 (m)
     T* u = nullptr;                 // 4 values per vertex (xyz, pad)
     const T* dinv = nullptr;        // 1 / A_ii from the assembly
     int grid = 1;                   // CTAs of the row kernel = number of dot partials
     bool tma = false;               // TMA-pipelined row kernel (persistent CTAs, bulk copies)
     int vg_grid_cap = 0;            // > 0: cap on the vertex-gather grid (MGPBD_MF_GRID_CAP, tests only)
+    // TMA row kernel: vertex ids as 16-bit offsets from a per-tile base (tiles of the kernel's tiling from
+    // row0 & ~3) when every tile spans < 65536 vertices; nullptr = the 32-bit verts
+    const uint16_t* v16 = nullptr;  // m x kc
+    const int32_t* vbase = nullptr; // per tile
 };
+
+// Build the 16-bit vertex-offset copy of verts (host copy hverts, m x kc) for the TMA tiling of rows
+// [row0, row1).  Returns false (buffers untouched) if a tile spans >= 65536 vertices.
+bool mf_build_v16(int32_t row0, int32_t row1, int kc, const std::vector<int32_t>& hverts, DBuf<uint16_t>& v16,
+                  DBuf<int32_t>& vbase, cudaStream_t s);
 
 int mf_grid(int32_t rows);
 // persistent grid of the TMA row kernel for rows [row0, row1) (T of tsize bytes, kc vertices)
-int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc);
+int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc, int vbytes = 4);
 
 
 // Per outer iteration, after the constraint evaluation: hv (vertex-major h), at (all rows) and the

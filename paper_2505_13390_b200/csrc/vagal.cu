@@ -19,11 +19,15 @@ inline int g1(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n
 // per vertex: incidences re-sorted by aggregate (stable: codes stay ascending inside an aggregate),
 // number of distinct aggregates
 __global__ void k_va_sort(int32_t nv, int kc, const int64_t* __restrict__ vptr, const int32_t* __restrict__ vlist,
-                          const int32_t* __restrict__ agg, int32_t* __restrict__ vlist2, int32_t* __restrict__ vpos,
-                          int32_t* __restrict__ pcnt) {
+                          const int32_t* __restrict__ agg, const int64_t* __restrict__ ppos,
+                          int32_t* __restrict__ vlist2, int32_t* __restrict__ vpos, int32_t* __restrict__ pcnt) {
     for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += gridDim.x * blockDim.x) {
         const int64_t e0 = vptr[v], e1 = vptr[v + 1];
-        for (int64_t e = e0; e < e1; ++e) { vlist2[e] = vlist[e]; if (vpos) vpos[e] = (int32_t)e; }
+        // vpos: position of the incidence in the hot vertex-major copy (padded layout when ppos is given)
+        for (int64_t e = e0; e < e1; ++e) {
+            vlist2[e] = vlist[e];
+            if (vpos) vpos[e] = (int32_t)(ppos ? ppos[v] + (e - e0) : e);
+        }
         for (int64_t a = e0 + 1; a < e1; ++a) {
             const int32_t c = vlist2[a];
             const int32_t pa = vpos ? vpos[a] : 0;
@@ -288,7 +292,7 @@ void va_coarse_pattern(int32_t nv, int kc, const int64_t* vptr, const int32_t* v
     DBuf<int64_t> vpp, ptr;
     vl2.resize(ninc);
     pcnt.resize(nv);
-    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, vl2.p, nullptr, pcnt.p);
+    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, nullptr, vl2.p, nullptr, pcnt.p);
     MG_LAUNCH_CHECK();
     vpp.resize((size_t)nv + 1);
     scan_exclusive<int32_t>(pcnt.p, vpp.p, nv, s);
@@ -327,8 +331,10 @@ void va_at(int32_t m, const double* alpha, double dt, double* at, cudaStream_t s
 }
 
 void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg, int32_t n_agg,
-                 const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s) {
+                 const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s,
+                 const int64_t* ppos, int64_t hv_stride) {
     const int64_t ninc = read_scalar(vptr + nv, s);
+    plan.hv_stride = ppos ? hv_stride : ninc;
     plan.cnnz = cnnz;
     plan.vlist2.resize(ninc);
     plan.vpos.resize(ninc);
@@ -337,7 +343,7 @@ void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, 
     DBuf<int64_t> vpp, coff;
     DBuf<int2> pq;
     pcnt.resize(nv);
-    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, plan.vlist2.p, plan.vpos.p, pcnt.p);
+    k_va_sort<<<g1(nv), 256, 0, s>>>(nv, kc, vptr, vlist, agg, ppos, plan.vlist2.p, plan.vpos.p, pcnt.p);
     MG_LAUNCH_CHECK();
     vpp.resize((size_t)nv + 1);
     scan_exclusive<int32_t>(pcnt.p, vpp.p, nv, s);
@@ -380,7 +386,7 @@ void va_numeric(VaPlan& plan, int kc, const T* h, const T* hv, const T* P, const
     if (plan.npairs) {
 #define MG_VAG(KC, HV)                                                                                      \
     k_va_g<T, KC, HV><<<g1(plan.npairs), 256, 0, s>>>(plan.npairs, plan.pstart.p, plan.vlist2.p, plan.vpos.p, h, \
-                                                      hv, plan.ninc, P, G)
+                                                      hv, plan.hv_stride, P, G)
         if (kc == 4) { if (hv) MG_VAG(4, true); else MG_VAG(4, false); }
         else { if (hv) MG_VAG(2, true); else MG_VAG(2, false); }
 #undef MG_VAG

@@ -15,8 +15,9 @@ namespace mgpbd {
 
 struct VaPlan {
     int64_t npairs = 0, ncontrib = 0, cnnz = 0, ninc = 0;
+    int64_t hv_stride = 0;  // plane stride of the vertex-major copy hv (padded layout: npad)
     DBuf<int32_t> vlist2;   // incidence codes (constraint*kc + slot) per vertex sorted by (agg, code)
-    DBuf<int32_t> vpos;     // ninc: position in vlist (and in the matrix-free hv planes) of vlist2[e]
+    DBuf<int32_t> vpos;     // ninc: position of vlist2[e] in the matrix-free hv planes (padded layout) or vlist
     DBuf<int32_t> pstart;   // npairs + 1: incidence range of (vertex, aggregate) pair p in vlist2
     DBuf<int64_t> cptr;     // cnnz + 1: products of coarse entry k
     DBuf<int2> cpq;         // ncontrib: (p, q) pair indices, grouped by coarse entry, ascending (v, p, q)
@@ -35,8 +36,11 @@ void va_coarse_pattern(int32_t nv, int kc, const int64_t* vptr, const int32_t* v
 void va_at(int32_t m, const double* alpha, double dt, double* at, cudaStream_t s);
 
 // Setup time, after aggregation and the coarse pattern of level 1.
+// ppos / hv_stride: the matrix-free operator's padded vertex-major layout (matfree.cuh) that va_numeric's
+// hv argument uses (nullptr: hv indexed like vlist).
 void va_symbolic(int32_t nv, int kc, const int64_t* vptr, const int32_t* vlist, const int32_t* agg, int32_t n_agg,
-                 const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s);
+                 const int64_t* crowptr, const int32_t* ccol, int64_t cnnz, VaPlan& plan, cudaStream_t s,
+                 const int64_t* ppos = nullptr, int64_t hv_stride = 0);
 
 // Every outer iteration: cval = A_1 values from the current h (m x kc x 3), P and at = alpha/dt^2 (all
 // m rows); cdinv = 1/diag.  hv (optional, nullptr = read h): the matrix-free operator's vertex-major

@@ -1,6 +1,6 @@
 """Run a few frames of a config through the C-ABI (for ncu launch lists / captures).
 
-  python tools/profile_frames.py --config cloth256 --frames 2 [--precision fp32]
+  python tools/profile_frames.py --config cloth256 --frames 2 [--precision fp32] [--resetup-at 1 5]
 """
 import argparse
 import os
@@ -18,11 +18,16 @@ def main():
     ap.add_argument("--frames", type=int, default=2)
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--n-iters", type=int, default=0)
+    ap.add_argument("--resetup-at", type=int, nargs="*", default=[],
+                    help="mark the hierarchy stale before these frames (setup from that frame's state)")
+    ap.add_argument("--no-profile", action="store_true", help="graph replay instead of eager profiled launches")
     a = ap.parse_args()
     sc = scenes.make(a.config)
     n_iters = a.n_iters or sc.n_iters
-    ctx = mgpbd.Context.from_scene(sc, precision=1 if a.precision == "fp32" else 0, profile=1)
+    ctx = mgpbd.Context.from_scene(sc, precision=1 if a.precision == "fp32" else 0, profile=0 if a.no_profile else 1)
     for f in range(a.frames):
+        if f in a.resetup_at:
+            ctx.setup_hierarchy()
         t = time.perf_counter()
         ctx.step(sc.dt, n_iters)
         s = ctx.stats()
