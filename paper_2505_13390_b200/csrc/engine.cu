@@ -366,6 +366,10 @@ class Engine : public EngineBase {
             }
         }
         if (mf64_ok && mf64.tma) mf64.grid = mf_grid_tma(0, m, 8, kc, vbytes);
+        if (mf.tma && std::getenv("MGPBD_VG_TMA")) {  // TMA-pipelined vertex gather (measured slower in fp32: off)
+            mf.vg_ts = mf_vg_plan(ppos_h, mf.v0, mf.v1, (int)sizeof(T), mf.vj16 != nullptr, &mf.vg_grid);
+            if (mf64_ok) mf64.vg_ts = mf_vg_plan(ppos_h, 0, nv, 8, mf.vj16 != nullptr, &mf64.vg_grid);
+        }
         mf.grid = mf.tma ? mf_grid_tma(r0, r1, (int)sizeof(T), kc, vbytes) : mf_grid(r1 - r0);
         if (const char* cap = std::getenv("MGPBD_MF_GRID_CAP")) {  // tests: many tiles per CTA (TMA ring wraps)
             const int c = std::max(1, std::atoi(cap));

@@ -15,6 +15,14 @@ namespace mgpbd {
 namespace {
 
 constexpr int MF_BS = 256;
+#ifndef MGPBD_MF_R
+#define MGPBD_MF_R 128  // swept on B200 (profiles/r1/sweep_level0_pass.txt): 128 rows, 3 stages, 6 CTAs/SM
+#endif
+constexpr int MF_R = MGPBD_MF_R;  // rows per tile (= threads per CTA)
+#ifndef MGPBD_MF_STAGES
+#define MGPBD_MF_STAGES 3
+#endif
+constexpr int MF_STAGES = MGPBD_MF_STAGES;  // ring depth (overridable at build time for tuning sweeps)
 
 template <class T>
 struct alignas(4 * sizeof(T)) V4 {
@@ -60,27 +68,33 @@ struct Chunk {
     static constexpr int VW = 16 / (int)sizeof(T);
     T hx[VW], hy[VW], hz[VW];
     int32_t j[VW];
+    // SM: the chunk lives in shared memory (plain loads); otherwise global, streamed (evict-first)
+    template <bool SM = false>
     __device__ __forceinline__ void load(const T* __restrict__ hx_, const T* __restrict__ hy_, const T* __restrict__ hz_,
                                          const uint16_t* __restrict__ j16, const int32_t* __restrict__ j32, int64_t p,
                                          bool in) {
         using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+        auto ld = [](const auto* q) {
+            if constexpr (SM) return *q;
+            else return __ldcs(q);
+        };
         if (in) {
-            const VT a = __ldcs(reinterpret_cast<const VT*>(hx_ + p));   // streamed once per pass: evict first
-            const VT b = __ldcs(reinterpret_cast<const VT*>(hy_ + p));
-            const VT c = __ldcs(reinterpret_cast<const VT*>(hz_ + p));
+            const VT a = ld(reinterpret_cast<const VT*>(hx_ + p));
+            const VT b = ld(reinterpret_cast<const VT*>(hy_ + p));
+            const VT c = ld(reinterpret_cast<const VT*>(hz_ + p));
             memcpy(hx, &a, 16); memcpy(hy, &b, 16); memcpy(hz, &c, 16);
             if constexpr (J16 && VW == 4) {
-                const uint2 w = __ldcs(reinterpret_cast<const uint2*>(j16 + p));
+                const uint2 w = ld(reinterpret_cast<const uint2*>(j16 + p));
                 j[0] = (int32_t)(w.x & 0xFFFFu); j[1] = (int32_t)(w.x >> 16);
                 j[2] = (int32_t)(w.y & 0xFFFFu); j[3] = (int32_t)(w.y >> 16);
             } else if constexpr (J16) {
-                const unsigned int w = __ldcs(reinterpret_cast<const unsigned int*>(j16 + p));
+                const unsigned int w = ld(reinterpret_cast<const unsigned int*>(j16 + p));
                 j[0] = (int32_t)(w & 0xFFFFu); j[1] = (int32_t)(w >> 16);
             } else if constexpr (VW == 4) {
-                const int4 w = __ldcs(reinterpret_cast<const int4*>(j32 + p));
+                const int4 w = ld(reinterpret_cast<const int4*>(j32 + p));
                 j[0] = w.x; j[1] = w.y; j[2] = w.z; j[3] = w.w;
             } else {
-                const int2 w = __ldcs(reinterpret_cast<const int2*>(j32 + p));
+                const int2 w = ld(reinterpret_cast<const int2*>(j32 + p));
                 j[0] = w.x; j[1] = w.y;
             }
         } else {
@@ -149,6 +163,119 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
         a1 = group_sum_t<G>(a1);
         a2 = group_sum_t<G>(a2);
         if (v < v1 && sl == 0) u[v] = V4<T>{(T)a0, (T)a1, (T)a2, (T)0};
+    }
+}
+
+// TMA-pipelined vertex gather: persistent CTAs stream tiles of VGT consecutive vertices — their padded slot
+// ranges of the three h planes, the constraint offsets and the vertex's slot offsets — into a MF_STAGES-deep
+// shared-memory ring with 1-D bulk copies, so the HBM stream never waits on the dependent x gathers; G lanes
+// per vertex read 16-byte chunks from shared memory and gather x from L2 (same sums, same order as
+// k_mf_vgather).
+#ifndef MGPBD_VGT
+#define MGPBD_VGT 32
+#endif
+constexpr int VGT = MGPBD_VGT;       // vertices per tile
+constexpr int VG_BS = 128;           // threads per CTA
+
+template <class T, bool J16>
+struct VgLayout {                    // one stage for tiles of at most TS slots
+    uint32_t hx, hy, hz, j, pp, bytes;
+    __host__ __device__ VgLayout(int32_t TS) {
+        const uint32_t ph = (uint32_t)TS * sizeof(T);
+        hx = 0; hy = ph; hz = 2 * ph; j = 3 * ph;
+        const uint32_t jb = (uint32_t)TS * (J16 ? 2u : 4u) + 16u;
+        pp = j + ((jb + 15u) & ~15u);
+        bytes = pp + (uint32_t)((VGT + 4) * 8);
+    }
+};
+
+template <class T, int G, bool J16>
+__global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1, int32_t ntiles, int32_t TS,
+                                                          int64_t npad, const int64_t* __restrict__ ppos,
+                                                          const uint16_t* __restrict__ vj16,
+                                                          const int32_t* __restrict__ vj32,
+                                                          const int32_t* __restrict__ jbase, const T* __restrict__ hv,
+                                                          const T* __restrict__ x, V4<T>* __restrict__ u) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    extern __shared__ __align__(128) unsigned char smem[];
+    __shared__ __align__(8) uint64_t bars[MF_STAGES];
+    const VgLayout<T, J16> LY(TS);
+    const int t = threadIdx.x;
+    if (t == 0) {
+        for (int k = 0; k < MF_STAGES; ++k) mbar_init(&bars[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const T* __restrict__ hx = hv;
+    const T* __restrict__ hy = hv + npad;
+    const T* __restrict__ hz = hv + 2 * npad;
+    const unsigned char* jsrc = J16 ? reinterpret_cast<const unsigned char*>(vj16) : reinterpret_cast<const unsigned char*>(vj32);
+    constexpr uint32_t JB = J16 ? 2u : 4u;
+    auto issue = [&](int jt) {
+        const int tile = blockIdx.x + jt * gridDim.x;
+        unsigned char* st = smem + (size_t)(jt % MF_STAGES) * LY.bytes;
+        const int32_t va = v0 + tile * VGT, vb = min(va + VGT, v1);
+        const int64_t pa = ppos[va], pb = ppos[vb];
+        const uint32_t ns = (uint32_t)(pb - pa);
+        const uintptr_t ja = reinterpret_cast<uintptr_t>(jsrc + pa * JB), ja0 = ja & ~(uintptr_t)15;
+        const uint32_t jbytes = (uint32_t)(((ja - ja0) + (uintptr_t)ns * JB + 15) & ~(uintptr_t)15);
+        const uintptr_t pp = reinterpret_cast<uintptr_t>(ppos + va), pp0 = pp & ~(uintptr_t)15;
+        const uint32_t pbytes = (uint32_t)(((pp - pp0) + (uintptr_t)(vb - va + 1) * 8 + 15) & ~(uintptr_t)15);
+        uint64_t* bar = &bars[jt % MF_STAGES];
+        mbar_expect_tx(bar, 3 * ns * (uint32_t)sizeof(T) + jbytes + pbytes);
+        if (ns) {
+            bulk_g2s(st + LY.hx, hx + pa, ns * (uint32_t)sizeof(T), bar);
+            bulk_g2s(st + LY.hy, hy + pa, ns * (uint32_t)sizeof(T), bar);
+            bulk_g2s(st + LY.hz, hz + pa, ns * (uint32_t)sizeof(T), bar);
+        }
+        bulk_g2s(st + LY.j, reinterpret_cast<const void*>(ja0), jbytes, bar);
+        bulk_g2s(st + LY.pp, reinterpret_cast<const void*>(pp0), pbytes, bar);
+    };
+    const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (t == 0)
+        for (int jt = 0; jt < MF_STAGES && jt < my_tiles; ++jt) issue(jt);
+    using CH = Chunk<T, J16>;
+    constexpr int VW = CH::VW;
+    const int g = t / G, sl = t % G;
+    for (int jt = 0; jt < my_tiles; ++jt) {
+        mbar_wait(&bars[jt % MF_STAGES], (uint32_t)((jt / MF_STAGES) & 1));
+        const unsigned char* st = smem + (size_t)(jt % MF_STAGES) * LY.bytes;
+        const int tile = blockIdx.x + jt * gridDim.x;
+        const int32_t va = v0 + tile * VGT, vb = min(va + VGT, v1);
+        const uintptr_t pp = reinterpret_cast<uintptr_t>(ppos + va);
+        const int64_t* spp = reinterpret_cast<const int64_t*>(st + LY.pp) + ((pp & 15) >> 3);
+        const int64_t pa = spp[0];
+        const uint32_t jlead = (uint32_t)(reinterpret_cast<uintptr_t>(jsrc + pa * JB) & 15);
+        const T* shx = reinterpret_cast<const T*>(st + LY.hx);
+        const T* shy = reinterpret_cast<const T*>(st + LY.hy);
+        const T* shz = reinterpret_cast<const T*>(st + LY.hz);
+        const unsigned char* sj = st + LY.j + jlead;
+        for (int vi = g; vi < VGT; vi += VG_BS / G) {   // uniform trip count: the butterfly needs the group
+            const int32_t v = va + vi;
+            T a0 = (T)0, a1 = (T)0, a2 = (T)0;
+            if (v < vb) {
+                const int64_t s0 = spp[vi] - pa, s1 = spp[vi + 1] - pa;
+                const int32_t jb = J16 ? jbase[v] : 0;
+                for (int64_t sb = s0 + (int64_t)sl * VW; sb < s1; sb += (int64_t)G * VW) {
+                    CH c;
+                    c.template load<true>(shx, shy, shz, reinterpret_cast<const uint16_t*>(sj),
+                                          reinterpret_cast<const int32_t*>(sj), sb, true);
+#pragma unroll
+                    for (int w = 0; w < VW; ++w) {
+                        const T xv = x[jb + c.j[w]];
+                        a0 += c.hx[w] * xv;
+                        a1 += c.hy[w] * xv;
+                        a2 += c.hz[w] * xv;
+                    }
+                }
+            }
+            a0 = group_sum_t<G>(a0);
+            a1 = group_sum_t<G>(a1);
+            a2 = group_sum_t<G>(a2);
+            if (v < vb && sl == 0) u[v] = V4<T>{a0, a1, a2, (T)0};
+        }
+        __syncthreads();   // every thread is done with this stage: refill it
+        if (t == 0 && jt + MF_STAGES < my_tiles) issue(jt + MF_STAGES);
     }
 }
 
@@ -274,14 +401,6 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 // TMA-pipelined row kernel: persistent CTAs stream MF_R-row tiles of the constraint records (vertex
 // ids, h) and per-row operands into shared memory with 1-D bulk copies (cp.async.bulk, completion on
 // an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
-#ifndef MGPBD_MF_R
-#define MGPBD_MF_R 128  // swept on B200 (profiles/r1/sweep_level0_pass.txt): 128 rows, 3 stages, 6 CTAs/SM
-#endif
-constexpr int MF_R = MGPBD_MF_R;  // rows per tile (= threads per CTA)
-#ifndef MGPBD_MF_STAGES
-#define MGPBD_MF_STAGES 3
-#endif
-constexpr int MF_STAGES = MGPBD_MF_STAGES;  // ring depth (overridable at build time for tuning sweeps)
 
 template <class T, int KC, bool V16>
 struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 128 or 256)
@@ -432,7 +551,23 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #endif
         int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
         if (A.vg_grid_cap > 0) grid = std::min(grid, A.vg_grid_cap);
-        if (A.vj16)
+        if (A.vg_ts > 0) {  // TMA-pipelined vertex gather
+            constexpr int GT = KC == 4 ? 4 : 2;
+            const int32_t ntiles = (A.v1 - A.v0 + VGT - 1) / VGT;
+            int tg = std::min(ntiles, A.vg_grid);
+            if (A.vg_grid_cap > 0) tg = std::min(tg, A.vg_grid_cap);
+            if (A.vj16) {
+                const size_t sm = (size_t)MF_STAGES * VgLayout<T, true>(A.vg_ts).bytes;
+                ensure_dyn_smem((const void*)k_mf_vgather_tma<T, GT, true>, sm);
+                k_mf_vgather_tma<T, GT, true><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
+                                                                   A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
+            } else {
+                const size_t sm = (size_t)MF_STAGES * VgLayout<T, false>(A.vg_ts).bytes;
+                ensure_dyn_smem((const void*)k_mf_vgather_tma<T, GT, false>, sm);
+                k_mf_vgather_tma<T, GT, false><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
+                                                                    A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
+            }
+        } else if (A.vj16)
             k_mf_vgather<T, G, UN, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase,
                                                                 A.hv, x, reinterpret_cast<V4<T>*>(A.u));
         else
@@ -496,6 +631,21 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 
 int mf_grid(int32_t rows) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(((int64_t)rows + MF_BS - 1) / MF_BS, 148 * 8));
+}
+
+int mf_vg_plan(const std::vector<int64_t>& ppos, int32_t v0, int32_t v1, int tsize, bool j16, int* grid) {
+    int64_t ts = 4;
+    for (int64_t v = v0; v < v1; v += VGT) ts = std::max<int64_t>(ts, ppos[std::min<int64_t>(v + VGT, v1)] - ppos[v]);
+    if (ts > (1 << 20)) return 0;
+    const uint32_t bytes = tsize == 4 ? (j16 ? VgLayout<float, true>((int32_t)ts).bytes : VgLayout<float, false>((int32_t)ts).bytes)
+                                      : (j16 ? VgLayout<double, true>((int32_t)ts).bytes : VgLayout<double, false>((int32_t)ts).bytes);
+    const int per_sm = (int)std::min<size_t>(16, (227 * 1024) / ((size_t)MF_STAGES * bytes + 1024));
+    if (per_sm < 1) return 0;
+    int dev = 0, sms = 148;
+    MG_CK(cudaGetDevice(&dev));
+    MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    *grid = sms * per_sm;
+    return (int)ts;
 }
 
 bool mf_build_v16(int32_t row0, int32_t row1, int kc, const std::vector<int32_t>& hverts, DBuf<uint16_t>& v16,

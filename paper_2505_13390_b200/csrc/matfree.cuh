@@ -46,7 +46,13 @@ struct MatFree {
     // row0 & ~3) when every tile spans < 65536 vertices; nullptr = the 32-bit verts
     const uint16_t* v16 = nullptr;  // m x kc
     const int32_t* vbase = nullptr; // per tile
+    // TMA-pipelined vertex gather: slots per vertex tile (> 0 enables it) and its persistent grid
+    int vg_ts = 0, vg_grid = 0;
 };
+
+// Plan of the TMA vertex gather over vertices [v0, v1) of the padded layout (host ppos): returns the stage
+// capacity in slots (0: not usable) and the persistent grid in *grid.
+int mf_vg_plan(const std::vector<int64_t>& ppos, int32_t v0, int32_t v1, int tsize, bool j16, int* grid);
 
 // Build the 16-bit vertex-offset copy of verts (host copy hverts, m x kc) for the TMA tiling of rows
 // [row0, row1).  Returns false (buffers untouched) if a tile spans >= 65536 vertices.
