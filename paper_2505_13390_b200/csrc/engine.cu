@@ -808,7 +808,10 @@ class Engine : public EngineBase {
                 std::vector<int32_t> nc;
                 std::vector<uint32_t> tx;
                 uint32_t smem = 0;
-                const uint32_t cap = 220u * 1024u;  // 227 KB minus the static descriptor copy
+                // 227 KB minus the static descriptor copy; MGPBD_RES_CAP (bytes, tests) lowers it to force the
+                // global-kernel fallback
+                const uint32_t cap = std::getenv("MGPBD_RES_CAP") ? (uint32_t)std::atol(std::getenv("MGPBD_RES_CAP"))
+                                                                    : 220u * 1024u;
                 if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st) &&
                     coarse_res_blocks_per_sm<T>(smem) >= 1) {  // else the global coarse kernel
                     res_lv.resize(lv.size()); h2d(res_lv.p, lv.data(), lv.size(), st);

@@ -1,0 +1,67 @@
+"""Every kernel-variant switch selects another implementation of the same operators: a frame
+under each switch against the oracle (fp64, 1e-6; reading p1: 3 outer iterations keep the oracle's own rounding
+sensitivity far below the bar).  block_small with min_coarse = 30 has 4 levels, so the persistent coarse
+kernels, the cluster tail and the coarsest inverse all run."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2505_13390_b200 import mgpbd, scenes
+
+pytestmark = pytest.mark.gpu
+
+MF_SWITCHES = ["", "MGPBD_NO_GRAPH=1", "MGPBD_NO_TMA=1", "MGPBD_NO_RES_COARSE=1", "MGPBD_NO_COARSE_KERNEL=1",
+               "MGPBD_COARSE_FROM=2", "MGPBD_NO_GJ_COOP=1", "MGPBD_NO_VA_SETUP=1", "MGPBD_NO_POWER_COOP=1",
+               "MGPBD_NO_TAIL=1", "MGPBD_NO_VJ16=1", "MGPBD_NO_V16=1", "MGPBD_VG_TMA=1", "MGPBD_MF_GRID_CAP=2",
+               "MGPBD_RES_CAP=4096"]
+CSR_SWITCHES = ["", "MGPBD_NO_BAND=1", "MGPBD_NO_ROWS=1", "MGPBD_NO_BAND=1 MGPBD_NO_ROWS=1"]
+ITERS = 3
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(b)
+
+
+@pytest.fixture(scope="module")
+def ref():
+    sc = scenes.make("block_small")
+    sim = O.Sim(sc, O.default_config(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters, min_coarse=30))
+    assert sim.step(sc.dt, ITERS) == 0
+    assert sim.hierarchy().n_levels >= 4
+    return sc, sim
+
+
+def run(monkeypatch, sc, switch, op, precision=0):
+    for kv in switch.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, level0_operator=op, min_coarse=30)
+    ctx.step(sc.dt, ITERS)
+    out = ctx.lambdas(), ctx.positions(), ctx.stats().n_levels
+    ctx.close()
+    return out
+
+
+@pytest.mark.parametrize("switch", MF_SWITCHES)
+def test_matrix_free_switch(monkeypatch, ref, switch):
+    sc, sim = ref
+    xo, _, lo = sim.state()
+    lg, xg, nl = run(monkeypatch, sc, switch, 1)
+    assert nl == sim.hierarchy().n_levels
+    assert rel(lg, lo) <= 1e-6 and rel(xg - sc.pos, xo - sc.pos) <= 1e-6, switch
+
+
+@pytest.mark.parametrize("switch", CSR_SWITCHES)
+def test_csr_switch(monkeypatch, ref, switch):
+    sc, sim = ref
+    xo, _, lo = sim.state()
+    lg, xg, _ = run(monkeypatch, sc, switch, 0)
+    assert rel(lg, lo) <= 1e-6 and rel(xg - sc.pos, xo - sc.pos) <= 1e-6, switch
+
+
+@pytest.mark.parametrize("switch", ["", "MGPBD_NO_TAIL=1", "MGPBD_NO_VJ16=1 MGPBD_NO_V16=1"])
+def test_fp32_switch(monkeypatch, ref, switch):
+    sc, sim = ref
+    xo, _, lo = sim.state()
+    lg, xg, _ = run(monkeypatch, sc, switch, 1, precision=1)
+    assert rel(lg, lo) <= 1e-3 and rel(xg - sc.pos, xo - sc.pos) <= 1e-3, switch
