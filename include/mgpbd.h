@@ -117,6 +117,8 @@ typedef struct {
     double pcg_tol;           /* MGPCG convergence exit: the solve stops (remaining iterations become no-ops,
                                  decided on the device) at the first iteration k with ||r_k|| <= pcg_tol *
                                  ||b||; 0 = off: exactly pcg_iters iterations (reading c10) */
+    double residual_abs;      /* Alg. 1 l.12 with an absolute eps ("||b|| < 1e-4"): stop the frame
+                                 after the first outer iteration with ||b|| < residual_abs; 0 = off */
     int32_t resetup_on_indef; /* 1 (default): a frame in which a PCG iteration saw <z,r> <= 0 marks the
                                  hierarchy stale, so the setup re-runs at ite 0 of the next frame (reading
                                  c13 extension); 0: the literal lazy schedule of PAPER.md:215
@@ -125,7 +127,8 @@ typedef struct {
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16
-#define MGPBD_MAX_ITERS 256
+#define MGPBD_MAX_ITERS 256            /* outer iterations recorded in mgpbd_stats.b_norm */
+#define MGPBD_MAX_FRAME_ITERS 1000000  /* outer iterations per frame ("maxiter (1e5)") */
 
 typedef struct {
     int32_t n_levels;
@@ -135,7 +138,8 @@ typedef struct {
     int32_t n_colours;                 /* colours of the level-0 GS bootstrap */
     int32_t setup_ran;                 /* setup ran in the last frame */
     int32_t n_b;                       /* outer iterations recorded in b_norm */
-    double b_norm[MGPBD_MAX_ITERS];    /* ||b||_2 per outer iteration of the last frame */
+    double b_norm[MGPBD_MAX_ITERS];    /* ||b||_2 per outer iteration of the last frame (the first
+                                          MGPBD_MAX_ITERS; n_b counts them, b_last is the final one) */
     int64_t frame;                     /* frames stepped so far */
     /* profile == 1 only: summed CUDA-event time of the level-0 matrix-pass kernels (smoother
        sweeps, residual, PCG SpMV) in the last frame, their launch count and algorithmic bytes */
@@ -155,6 +159,8 @@ typedef struct {
        constraint evaluation + assembly / matrix-free refresh, Galerkin refresh + coarsest inverse,
        V-cycles, the rest of MGPCG, position / lambda update */
     double ms_assemble, ms_galerkin, ms_vcycle, ms_pcg_other, ms_update;
+    int32_t iters_run;                 /* outer iterations the last frame ran (< n_iters after an l.12 exit) */
+    double b_last;                     /* ||b||_2 of its last outer iteration */
 } mgpbd_stats;
 
 /* Fill *cfg with the defaults listed above.  Never fails for a non-NULL cfg. */
@@ -173,7 +179,7 @@ MGPBD_API mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constrai
 /* Mark the hierarchy stale: it is rebuilt at ite 0 of the next mgpbd_step (Alg. 1 l.7). */
 MGPBD_API mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx);
 
-/* One frame of Algorithm 1 with n_iters outer iterations (1..MGPBD_MAX_ITERS) and time step dt > 0.
+/* One frame of Algorithm 1 with n_iters outer iterations (1..MGPBD_MAX_FRAME_ITERS) and time step dt > 0.
  * Setup runs at ite 0 when frame % setup_interval == 0 or the hierarchy is stale.  Synchronises at
  * the end and checks the device flags: MGPBD_E_NONFINITE (NaN/Inf PCG scalar), MGPBD_E_INDEFINITE
  * (non-SPD coarsest matrix).  <z,r> <= 0 in PCG is counted (mgpbd_stats.indefinite_events), not

@@ -25,7 +25,7 @@ void orc_config_default(orc_config* c) {
     c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
     c->smoother = 0; c->cheb_lower = 0.25;
     c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0; c->pcg_tol = 0.0;
-    c->resetup_on_indef = 1; c->k_nullspace = 1;
+    c->resetup_on_indef = 1; c->residual_abs = 0.0; c->k_nullspace = 1;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -1241,6 +1241,7 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
         for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->x[k] += omega * s->dx[k];              /* l.11 */
         s->iters_used = ite + 1;
         if (s->cfg.residual_tol > 0.0 && bn < s->cfg.residual_tol * b0) break;                 /* l.12 */
+        if (s->cfg.residual_abs > 0.0 && bn < s->cfg.residual_abs) break;
     }
     s->omega_last = omega;
     for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->v[k] = (s->x[k] - s->x_old[k]) / dt;      /* l.17 */

@@ -42,6 +42,7 @@ typedef struct {
     int32_t resetup_on_indef;/* 1: a frame with a PCG iteration <z,r> <= 0 marks the hierarchy stale, so setup
                                 re-runs at ite 0 of the next frame (reading c13 extension); 0: the literal
                                 schedule of PAPER.md:215 (setup only every setup_interval frames).  Default 1 */
+    double residual_abs;     /* Alg. 1 l.12 absolute eps ("||b|| < 1e-4"): break once ||b|| < it; 0 = off */
     int32_t k_nullspace;     /* near-kernel vectors per aggregate ("six distinct B"; reading c1):
                                 1 (default) or up to 6 */
 } orc_config;

@@ -32,7 +32,7 @@ class Config(C.Structure):
                 ("gravity", C.c_double * 3), ("seed", C.c_uint64), ("smoother", C.c_int32),
                 ("cheb_lower", C.c_double), ("backtrack", C.c_int32), ("omega_min", C.c_double),
                 ("residual_tol", C.c_double), ("pcg_tol", C.c_double), ("resetup_on_indef", C.c_int32),
-                ("k_nullspace", C.c_int32)]
+                ("residual_abs", C.c_double), ("k_nullspace", C.c_int32)]
 
 
 _lib = None

@@ -433,7 +433,7 @@ class Engine : public EngineBase {
         if (cfg.world > 1 || cfg.vgroup || cfg.nccl_id) setup_partition();
         h.resize((size_t)m * kc * 3); b0.resize(m);
         r.resize(m); p.resize(m); q.resize(m); xs.resize(m);
-        scal.resize(2 * 4096); flags.resize(8); bn.resize(MGPBD_MAX_ITERS);
+        scal.resize(2 * 4096); flags.resize(8); bn.resize(MGPBD_MAX_FRAME_ITERS);
         parts1.resize(148 * 8); parts2.resize(148 * 8);
         pw_ss.resize(4);
         MG_CK(cudaMemsetAsync(flags.p, 0, 8 * sizeof(int), st));
@@ -1113,7 +1113,7 @@ class Engine : public EngineBase {
     // One graph serves every outer iteration (the iteration index reaches the kernels through flags[7]),
     // so after a setup only the second outer iteration pays the capture + instantiation.
     void run_iter(int ite) {
-        set_outer_index(flags.p, ite, st);
+        set_outer_index(flags.p, std::min(ite, 500000), st);  // error tags ite*4096 + k stay within int32
         if (!use_graphs || cfg.profile) { iter_body(ite); return; }  // events need eager launches
         if (graphs.empty()) graphs.resize(1);
         IterGraph& g = graphs[0];
@@ -1184,12 +1184,14 @@ class Engine : public EngineBase {
                             L[0]->dinv.p, st, r0, r1);
             run_iter(ite);  // Eq. 6 refresh, l.8 MGPCG, l.9-11 update
             iters_run = ite + 1;
-            if (cfg.residual_tol > 0.0) {  // l.12: ||b|| < eps, eps = residual_tol ||b_0|| (reading c21)
+            if (cfg.residual_tol > 0.0 || cfg.residual_abs > 0.0) {
+                // l.12: ||b|| < eps, eps = residual_tol ||b_0|| (reading c21) or residual_abs
                 double b2[2];
                 d2h(b2, bn.p, 1, st);
                 d2h(b2 + 1, bn.p + ite, 1, st);
                 MG_CK(cudaStreamSynchronize(st));
-                if (b2[1] < cfg.residual_tol * cfg.residual_tol * b2[0]) break;
+                if (cfg.residual_tol > 0.0 && b2[1] < cfg.residual_tol * cfg.residual_tol * b2[0]) break;
+                if (cfg.residual_abs > 0.0 && b2[1] < cfg.residual_abs * cfg.residual_abs) break;
             }
         }
         velocity(nv, x.p, x_old.p, v.p, dt, st);                                                     // l.17
@@ -1286,9 +1288,14 @@ class Engine : public EngineBase {
         s->n_colours = ncolours;
         s->setup_ran = setup_ran;
         s->n_b = n_b;
-        if (n_b) d2h(s->b_norm, bn.p, n_b, st);
+        const int nb = std::min(n_b, (int)MGPBD_MAX_ITERS);
+        s->n_b = nb;
+        s->iters_run = n_b;
+        if (nb) d2h(s->b_norm, bn.p, nb, st);
+        if (n_b) d2h(&s->b_last, bn.p + n_b - 1, 1, st);
         MG_CK(cudaStreamSynchronize(st));
-        for (int i = 0; i < n_b; ++i) s->b_norm[i] = std::sqrt(s->b_norm[i]);
+        for (int i = 0; i < nb; ++i) s->b_norm[i] = std::sqrt(s->b_norm[i]);
+        s->b_last = std::sqrt(s->b_last);
         s->frame = frame;
         s->l0_pass_ms = l0_ms;
         s->l0_pass_launches = cfg.profile ? l0_launches : 0;
@@ -1520,6 +1527,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->omega_min = 1e-3;
     c->residual_tol = 0.0;
     c->pcg_tol = 0.0;
+    c->residual_abs = 0.0;
     c->resetup_on_indef = 1;
     return MGPBD_OK;
 }
@@ -1549,7 +1557,8 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
         return fail("the Gauss-Seidel smoother needs level0_operator = 0 and one rank");
     if (cfg->smoother_sweeps > 8) return fail("smoother_sweeps must be <= 8");
     if (cfg->backtrack != 0 && cfg->backtrack != 1) return fail("backtrack must be 0 or 1");
-    if (!(cfg->omega_min > 0.0) || !(cfg->residual_tol >= 0.0)) return fail("bad omega_min / residual_tol");
+    if (!(cfg->omega_min > 0.0) || !(cfg->residual_tol >= 0.0) || !(cfg->residual_abs >= 0.0))
+        return fail("bad omega_min / residual_tol / residual_abs");
     if (cfg->smoother == 1 && !(cfg->cheb_lower > 0.0 && cfg->cheb_lower < 1.0)) return fail("cheb_lower must be in (0, 1)");
     if (!(cfg->pcg_tol >= 0.0)) return fail("pcg_tol must be >= 0");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > mgpbd::SC_KMAX || cfg->setup_interval < 1 ||
@@ -1590,8 +1599,8 @@ mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx) {
 }
 
 mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters) {
-    if (ctx && (!(dt > 0.0) || n_iters < 1 || n_iters > MGPBD_MAX_ITERS)) {
-        ctx->err = "dt must be > 0 and 1 <= n_iters <= MGPBD_MAX_ITERS";
+    if (ctx && (!(dt > 0.0) || n_iters < 1 || n_iters > MGPBD_MAX_FRAME_ITERS)) {
+        ctx->err = "dt must be > 0 and 1 <= n_iters <= MGPBD_MAX_FRAME_ITERS";
         return MGPBD_E_ARG;
     }
     return guarded(ctx, [&] { ctx->eng->step(dt, n_iters); });

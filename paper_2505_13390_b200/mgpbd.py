@@ -13,7 +13,7 @@ LIB_PATH = os.path.join(HERE, "libmgpbd.so")
 
 OK, E_ARG, E_CUDA, E_NCCL, E_OOM, E_INDEFINITE, E_NONFINITE, E_STALL = 0, -1, -2, -3, -4, -5, -6, -7
 DISTANCE, TET_ARAP = 2, 4
-MAX_LEVELS, MAX_ITERS = 16, 256
+MAX_LEVELS, MAX_ITERS, MAX_FRAME_ITERS = 16, 256, 1000000
 
 SYMBOLS = ["mgpbd_config_default", "mgpbd_create", "mgpbd_setup_hierarchy", "mgpbd_step", "mgpbd_set_state",
            "mgpbd_set_profiling",
@@ -52,7 +52,7 @@ class Config(C.Structure):
                 ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32),
                 ("smoother", C.c_int32), ("cheb_lower", C.c_double), ("backtrack", C.c_int32),
                 ("omega_min", C.c_double), ("residual_tol", C.c_double), ("pcg_tol", C.c_double),
-                ("resetup_on_indef", C.c_int32)]
+                ("residual_abs", C.c_double), ("resetup_on_indef", C.c_int32)]
 
 
 class Stats(C.Structure):
@@ -65,7 +65,7 @@ class Stats(C.Structure):
                 ("rank", C.c_int32), ("world", C.c_int32), ("row_begin", C.c_int32), ("row_end", C.c_int32),
                 ("halo_rows", C.c_int64), ("omega_relax", C.c_double), ("ms_assemble", C.c_double),
                 ("ms_galerkin", C.c_double), ("ms_vcycle", C.c_double), ("ms_pcg_other", C.c_double),
-                ("ms_update", C.c_double)]
+                ("ms_update", C.c_double), ("iters_run", C.c_int32), ("b_last", C.c_double)]
 
 
 _lib = None

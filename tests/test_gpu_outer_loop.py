@@ -81,3 +81,22 @@ def test_pcg_tolerance_exit(name):
     xg = ctx.debug_pcg(b, 30)
     assert rel(xg, xo) <= 1e-9
     assert np.linalg.norm(b - A @ xg) <= tol * np.linalg.norm(b) * (1 + 1e-9)
+
+
+@pytest.mark.parametrize("name", ["cloth16", "bar3k"])
+def test_absolute_residual_exit_frame(name):
+    """Alg. 1 l.12 with the absolute eps of the paper's cloth runs ("||b|| < 1e-4"): both sides
+    stop after the same outer iteration and agree on the frame."""
+    sc = scenes.make(name)
+    probe = O.Sim(sc)
+    probe.step(sc.dt, 10)
+    nb = probe.b_norms(10)
+    eps = 1.001 * nb[:5].min()                          # reached within the first 5 iterations
+    ctx = mgpbd.Context.from_scene(sc, residual_abs=eps)
+    sim = O.Sim(sc, O.default_config(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters, residual_abs=eps))
+    ctx.step(sc.dt, 10)
+    sim.step(sc.dt, 10)
+    st = ctx.stats()
+    assert st.iters_run == sim.iters_used() <= 5 and st.b_last < eps
+    xo, _, lo = sim.state()
+    assert rel(ctx.lambdas(), lo) <= 1e-6 and rel(ctx.positions() - sc.pos, xo - sc.pos) <= 1e-6

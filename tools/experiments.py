@@ -1,6 +1,6 @@
 """Convergence / scaling experiments of SURVEY.md §8(f) row f3 on the synthetic scenes (GPU, C-ABI).
 
-  python tools/experiments.py [linearity] [lazy] [smoother]
+  python tools/experiments.py [linearity] [lazy] [smoother] [cloth_tol]
 
 * linearity — time per outer iteration vs problem size (Fig. 8a: "linearly scaled up
   with resolution"): cloth N x N and block slabs of growing length; least-squares line and R^2.
@@ -8,6 +8,9 @@
   relative residual ||b_last|| / ||b_0|| per frame, frames with a setup, device time.
 * smoother — omega-Jacobi vs Chebyshev ("omega-Jacobi has the best performance for
   softbody, and Chebyshev has the best performance for cloth") at the same number of matrix passes.
+* cloth_tol — the paper's cloth hanging test (Fig. cloth, Table 1: N = 64/128/256/512, dt 3 ms,
+  stiffness 1e9, "maxiter (1e5) ... ||b|| < 1e-4"): outer iterations and device time per frame until
+  ||b|| < 1e-4 (absolute, Alg. 1 l.12), capped at MAXIT.
 Prints one JSON object per experiment.
 """
 import json
@@ -100,7 +103,24 @@ def smoother():
     print(json.dumps({"experiment": "smoother", **res}), flush=True)
 
 
+def cloth_tol(maxit=20000, frames=2):
+    out = []
+    for n in (64, 128, 256, 512):
+        sc = scenes.cloth(n, dt=3e-3, n_iters=20)
+        ctx = mgpbd.Context.from_scene(sc, precision=0, residual_abs=1e-4)
+        rows = []
+        for f in range(frames):
+            ctx.step(sc.dt, maxit)
+            st = ctx.stats()
+            rows.append({"frame": f, "iters": st.iters_run, "b_first": st.b_norm[0], "b_last": st.b_last,
+                         "ms": st.ms_frame, "converged": st.b_last < 1e-4})
+        ctx.close()
+        out.append({"N": n, "constraints": sc.n_cons, "frames": rows})
+        print(json.dumps({"experiment": "cloth_tol", "N": n, "frames": rows}), flush=True)
+    return out
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["linearity", "lazy", "smoother"]
     for w in which:
-        {"linearity": linearity, "lazy": lazy, "smoother": smoother}[w]()
+        {"linearity": linearity, "lazy": lazy, "smoother": smoother, "cloth_tol": cloth_tol}[w]()
