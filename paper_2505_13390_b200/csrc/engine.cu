@@ -200,8 +200,8 @@ class Engine : public EngineBase {
     // padded vertex-major layout shared by mf and mf64 (matfree.cuh)
     DBuf<int64_t> mf_ppos;
     DBuf<int32_t> mf_vsrc, mf_vj32, mf_jbase;
-    DBuf<uint16_t> mf_vj16, mf_v16;
-    DBuf<int32_t> mf_vbase;
+    DBuf<uint16_t> mf_vj16, mf_v16, mf64_v16;
+    DBuf<int32_t> mf_vbase, mf64_vbase;
     int64_t mf_npad = 0;
     // fp64 matrix-free operator for the setup's level-0 power method (reading c18: setup in fp64)
     MatFree<double> mf64;
@@ -359,13 +359,16 @@ class Engine : public EngineBase {
             std::vector<int32_t> hvt((size_t)m * kc);
             d2h(hvt.data(), verts.p, hvt.size(), st);
             MG_CK(cudaStreamSynchronize(st));
-            if (mf_build_v16(r0, r1, kc, hvt, mf_v16, mf_vbase, st)) {
+            if (mf_build_v16(r0, r1, kc, (int)sizeof(T), hvt, mf_v16, mf_vbase, st)) {
                 mf.v16 = mf_v16.p; mf.vbase = mf_vbase.p;
                 vbytes = 2;
-                if (mf64_ok) { mf64.v16 = mf_v16.p; mf64.vbase = mf_vbase.p; }   // same tiling (one rank: r0 = 0)
+                // the fp64 twin (one rank: r0 = 0) has its own tiling when its tile height differs (cloth)
+                if (mf64_ok && mf_build_v16(0, m, kc, 8, hvt, mf64_v16, mf64_vbase, st)) {
+                    mf64.v16 = mf64_v16.p; mf64.vbase = mf64_vbase.p;
+                }
             }
         }
-        if (mf64_ok && mf64.tma) mf64.grid = mf_grid_tma(0, m, 8, kc, vbytes);
+        if (mf64_ok && mf64.tma) mf64.grid = mf_grid_tma(0, m, 8, kc, mf64.v16 ? 2 : 4);
         if (mf.tma && std::getenv("MGPBD_VG_TMA")) {  // TMA-pipelined vertex gather (measured slower in fp32: off)
             mf.vg_ts = mf_vg_plan(ppos_h, mf.v0, mf.v1, (int)sizeof(T), mf.vj16 != nullptr, &mf.vg_grid);
             if (mf64_ok) mf64.vg_ts = mf_vg_plan(ppos_h, 0, nv, 8, mf.vj16 != nullptr, &mf64.vg_grid);

@@ -18,7 +18,13 @@ constexpr int MF_BS = 256;
 #ifndef MGPBD_MF_R
 #define MGPBD_MF_R 128  // swept on B200 (profiles/r1/sweep_level0_pass.txt): 128 rows, 3 stages, 6 CTAs/SM
 #endif
-constexpr int MF_R = MGPBD_MF_R;  // rows per tile (= threads per CTA)
+constexpr int MF_R = MGPBD_MF_R;  // rows per tile (= threads per CTA) of tetrahedra
+#ifndef MGPBD_MF_R2
+#define MGPBD_MF_R2 256  // fp32 distance constraints (2 vertices per row), swept on cloth2048 (profiles/r2):
+#endif                   // 220 us per pass vs 228 (128 rows) and 237 (512); fp64 keeps 128 (429 vs 463 us)
+template <class T, int KC>
+__host__ __device__ constexpr int mf_r() { return (KC == 2 && sizeof(T) == 4) ? MGPBD_MF_R2 : MF_R; }
+inline int mf_r(int kc, int tsize) { return (kc == 2 && tsize == 4) ? MGPBD_MF_R2 : MF_R; }
 #ifndef MGPBD_MF_STAGES
 #define MGPBD_MF_STAGES 3
 #endif
@@ -403,21 +409,22 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 // an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
 
 template <class T, int KC, bool V16>
-struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for MF_R = 128 or 256)
+struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for R = 128 or 256)
+    static constexpr int R = mf_r<T, KC>();
     static constexpr uint32_t VB = V16 ? 2 : 4;  // bytes per vertex index (16-bit: offset from the tile's base)
     static constexpr uint32_t H = 0;
-    static constexpr uint32_t V = H + MF_R * KC * 3 * sizeof(T);
-    static constexpr uint32_t X = V + MF_R * KC * VB;
-    static constexpr uint32_t AT = X + MF_R * sizeof(T);
-    static constexpr uint32_t D = AT + MF_R * sizeof(T);
-    static constexpr uint32_t B = D + MF_R * sizeof(T);
-    static constexpr uint32_t AUX = B + MF_R * sizeof(T);
-    static constexpr uint32_t XP = AUX + MF_R * sizeof(T);
-    static constexpr uint32_t BYTES = XP + MF_R * sizeof(T);
+    static constexpr uint32_t V = H + R * KC * 3 * sizeof(T);
+    static constexpr uint32_t X = V + R * KC * VB;
+    static constexpr uint32_t AT = X + R * sizeof(T);
+    static constexpr uint32_t D = AT + R * sizeof(T);
+    static constexpr uint32_t B = D + R * sizeof(T);
+    static constexpr uint32_t AUX = B + R * sizeof(T);
+    static constexpr uint32_t XP = AUX + R * sizeof(T);
+    static constexpr uint32_t BYTES = XP + R * sizeof(T);
 };
 
 template <class T, int KC, int MODE, bool V16>
-__global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1, int32_t tbase, int32_t ntiles,
+__global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int32_t row1, int32_t tbase, int32_t ntiles,
                                                       const void* __restrict__ verts_, const int32_t* __restrict__ vbase,
                                                       const T* __restrict__ h,
                                                       const V4<T>* __restrict__ u, const T* __restrict__ at,
@@ -427,6 +434,7 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
                                                       const T* __restrict__ xprev, double* __restrict__ parts,
                                                       double* __restrict__ parts2) {
     using LY = TileLayout<T, KC, V16>;
+    constexpr int MF_RK = LY::R;
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bars[MF_STAGES];
     constexpr bool ND = MODE == PASS_JACOBI || MODE == PASS_JACOBI_DOT || MODE == PASS_POWER;
@@ -443,8 +451,8 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
     auto issue = [&](int j) {
         const int tile = blockIdx.x + j * gridDim.x;
         unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
-        const int32_t i0 = tbase + tile * MF_R;
-        const int32_t rows = min(MF_R, row1 - i0);
+        const int32_t i0 = tbase + tile * MF_RK;
+        const int32_t rows = min(MF_RK, row1 - i0);
         auto rnd = [](uint32_t by) { return (by + 15u) & ~15u; };
         const uint32_t bh = rnd(rows * KC * 3 * sizeof(T)), bv = rnd(rows * KC * LY::VB),
                        bs = rnd(rows * sizeof(T));
@@ -470,7 +478,7 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
     for (int j = 0; j < my_tiles; ++j) {
         mbar_wait(&bars[j % MF_STAGES], (uint32_t)((j / MF_STAGES) & 1));
         const unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
-        const int32_t i = tbase + (blockIdx.x + j * gridDim.x) * MF_R + t;
+        const int32_t i = tbase + (blockIdx.x + j * gridDim.x) * MF_RK + t;
         if (i >= row0 && i < row1) {
             int vi[KC];
             T hi[KC][3];
@@ -522,10 +530,10 @@ __global__ void __launch_bounds__(MF_R) k_mf_rows_tma(int32_t row0, int32_t row1
     }
     if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
         __shared__ double sh[32];
-        const double t1 = block_sum<MF_R>(acc1, sh);
+        const double t1 = block_sum<MF_RK>(acc1, sh);
         if (threadIdx.x == 0) parts[blockIdx.x] = t1;
         if (MODE == PASS_JACOBI_DOT) {
-            const double t2 = block_sum<MF_R>(acc2, sh);
+            const double t2 = block_sum<MF_RK>(acc2, sh);
             if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
         }
     }
@@ -578,7 +586,8 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
     const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
     if (A.tma) {
         const int32_t tbase = A.row0 & ~3;  // 16-B aligned vector offsets
-        const int32_t ntiles = (A.row1 - tbase + MF_R - 1) / MF_R;
+        constexpr int R = mf_r<T, KC>();
+        const int32_t ntiles = (A.row1 - tbase + R - 1) / R;
 #define MG_MFT(M) { if (A.v16) MG_MFT2(M, true) else MG_MFT2(M, false) }
 #define MG_MFT2(M, V16)                                                                                         \
     {                                                                                                           \
@@ -586,7 +595,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         ensure_dyn_smem((const void*)k_mf_rows_tma<T, KC, M, V16>, smem);                                      \
         cudaLaunchConfig_t lc = {};                                                                             \
         lc.gridDim = dim3(A.grid);                                                                              \
-        lc.blockDim = dim3(MF_R);                                                                               \
+        lc.blockDim = dim3(R);                                                                                  \
         lc.dynamicSmemBytes = smem;                                                                             \
         lc.stream = s;                                                                                          \
         cudaLaunchAttribute la[1];                                                                              \
@@ -648,15 +657,16 @@ int mf_vg_plan(const std::vector<int64_t>& ppos, int32_t v0, int32_t v1, int tsi
     return (int)ts;
 }
 
-bool mf_build_v16(int32_t row0, int32_t row1, int kc, const std::vector<int32_t>& hverts, DBuf<uint16_t>& v16,
-                  DBuf<int32_t>& vbase, cudaStream_t s) {
+bool mf_build_v16(int32_t row0, int32_t row1, int kc, int tsize, const std::vector<int32_t>& hverts,
+                  DBuf<uint16_t>& v16, DBuf<int32_t>& vbase, cudaStream_t s) {
     const int32_t tbase = row0 & ~3;
-    const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + MF_R - 1) / MF_R);
+    const int R = mf_r(kc, tsize);
+    const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + R - 1) / R);
     const int64_t m = (int64_t)hverts.size() / kc;
     std::vector<int32_t> vb((size_t)ntiles, 0);
     std::vector<uint16_t> o((size_t)m * kc, 0);
     for (int64_t t = 0; t < ntiles; ++t) {
-        const int64_t i0 = tbase + t * MF_R, i1 = std::min<int64_t>(i0 + MF_R, row1);
+        const int64_t i0 = tbase + t * R, i1 = std::min<int64_t>(i0 + R, row1);
         int32_t lo = INT32_MAX, hi = -1;
         for (int64_t e = i0 * kc; e < i1 * kc; ++e) { lo = std::min(lo, hverts[e]); hi = std::max(hi, hverts[e]); }
         if (hi < 0) continue;
@@ -674,8 +684,9 @@ bool mf_build_v16(int32_t row0, int32_t row1, int kc, const std::vector<int32_t>
 
 int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc, int vbytes) {
     const int32_t tbase = row0 & ~3;
-    const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + MF_R - 1) / MF_R);
-    const size_t stage = (size_t)MF_R * ((size_t)kc * 3 * tsize + (size_t)kc * vbytes + 6 * (size_t)tsize);
+    const int R = mf_r(kc, tsize);
+    const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + R - 1) / R);
+    const size_t stage = (size_t)R * ((size_t)kc * 3 * tsize + (size_t)kc * vbytes + 6 * (size_t)tsize);
     const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (MF_STAGES * stage + 1024)));
     int dev = 0, sms = 148;
     MG_CK(cudaGetDevice(&dev));

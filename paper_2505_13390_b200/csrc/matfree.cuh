@@ -56,8 +56,8 @@ int mf_vg_plan(const std::vector<int64_t>& ppos, int32_t v0, int32_t v1, int tsi
 
 // Build the 16-bit vertex-offset copy of verts (host copy hverts, m x kc) for the TMA tiling of rows
 // [row0, row1).  Returns false (buffers untouched) if a tile spans >= 65536 vertices.
-bool mf_build_v16(int32_t row0, int32_t row1, int kc, const std::vector<int32_t>& hverts, DBuf<uint16_t>& v16,
-                  DBuf<int32_t>& vbase, cudaStream_t s);
+bool mf_build_v16(int32_t row0, int32_t row1, int kc, int tsize, const std::vector<int32_t>& hverts,
+                  DBuf<uint16_t>& v16, DBuf<int32_t>& vbase, cudaStream_t s);
 
 int mf_grid(int32_t rows);
 // persistent grid of the TMA row kernel for rows [row0, row1) (T of tsize bytes, kc vertices)
