@@ -75,6 +75,15 @@ class NcclComm : public Comm {
         }
         MG_NCCL(ncclGroupEnd());
     }
+    void allgather_blocks(void* base, size_t elem, const std::vector<int32_t>& bounds, cudaStream_t s) override {
+        char* b = static_cast<char*>(base);
+        MG_NCCL(ncclGroupStart());
+        for (int r = 0; r < w_; ++r) {
+            const size_t n = (size_t)(bounds[r + 1] - bounds[r]) * elem;
+            if (n) MG_NCCL(ncclBroadcast(b + (size_t)bounds[r] * elem, b + (size_t)bounds[r] * elem, n, ncclUint8, r, comm_, s));
+        }
+        MG_NCCL(ncclGroupEnd());
+    }
     bool graph_capturable() const override { return true; }
 
    private:
@@ -147,6 +156,20 @@ class VirtualComm : public Comm {
                 MG_CK(cudaMemcpyAsync(static_cast<char*>(base) + (size_t)x.recv.a * elem,
                                       static_cast<const char*>(g_->ptr[x.peer]) + (size_t)x.recv.a * elem,
                                       (size_t)x.recv.size() * elem, cudaMemcpyDeviceToDevice, s));
+        MG_CK(cudaStreamSynchronize(s));
+        g_->barrier();
+    }
+    void allgather_blocks(void* base, size_t elem, const std::vector<int32_t>& bounds, cudaStream_t s) override {
+        MG_CK(cudaStreamSynchronize(s));
+        g_->ptr[r_] = base;
+        g_->barrier();
+        for (int q = 0; q < g_->world; ++q) {
+            const size_t n = (size_t)(bounds[q + 1] - bounds[q]) * elem;
+            if (q != r_ && n)
+                MG_CK(cudaMemcpyAsync(static_cast<char*>(base) + (size_t)bounds[q] * elem,
+                                      static_cast<const char*>(g_->ptr[q]) + (size_t)bounds[q] * elem, n,
+                                      cudaMemcpyDeviceToDevice, s));
+        }
         MG_CK(cudaStreamSynchronize(s));
         g_->barrier();
     }

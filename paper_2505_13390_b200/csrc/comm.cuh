@@ -43,6 +43,9 @@ class Comm {
     // exchange: for each peer, send [ptr+send.a, ptr+send.b) and receive into [ptr+recv.a, ...)
     struct Xfer { int peer; Range send, recv; };
     virtual void exchange(void* base, size_t elem, const std::vector<Xfer>& xs, cudaStream_t s) = 0;
+    // every rank's block [bounds[r], bounds[r+1]) of a full-length buffer replaces the others' copies
+    // (variable-size allgather in place: one broadcast per root in a group)
+    virtual void allgather_blocks(void* base, size_t elem, const std::vector<int32_t>& bounds, cudaStream_t s) = 0;
     virtual bool graph_capturable() const = 0;
 };
 

@@ -192,6 +192,7 @@ class Engine : public EngineBase {
     int32_t r0 = 0, r1 = 0;
     int64_t nnz_own = 0, halo_elems = 0;
     std::vector<Comm::Xfer> xfers;
+    std::vector<int32_t> part_bounds;  // level-0 row blocks of all ranks
     int64_t tb0 = 0, te0 = -1;  // Galerkin segments of the owned rows (level 0 -> 1)
     DBuf<double> dsc;           // rank-local dot results before the allreduce
     // matrix-free level-0 operator (cfg.level0_operator == 1, matfree.cuh)
@@ -253,6 +254,7 @@ class Engine : public EngineBase {
         d2h(hrp.data(), rowptr0.p, (size_t)m + 1, st);
         MG_CK(cudaStreamSynchronize(st));
         const std::vector<int32_t> bounds = partition_rows(hrp.data(), m, W);
+        part_bounds = bounds;
         std::vector<int32_t> mn(W), mx(W);
         for (int q = 0; q < W; ++q) row_range_window(rowptr0.p, col0.p, bounds[q], bounds[q + 1], &mn[q], &mx[q], st);
         const auto plan = halo_plan(bounds, mn, mx);
@@ -1101,7 +1103,7 @@ class Engine : public EngineBase {
         timed(PH_PCG, [&] { pcg(cfg.pcg_iters, ite); });                                             // l.8
         mark_stage(4);
         timed(PH_UPD, [&] {
-            if (dist) comm->allreduce(xs.p, (size_t)m, st);  // dlambda of every row on every rank
+            if (dist) comm->allgather_blocks(xs.p, sizeof(T), part_bounds, st);  // dlambda of every row, every rank
             if (mf_on() && !dist && mf.p0 == 0 && mf.p1 == mf.npad)  // hv covers every incidence
                 mf_update<T>(mf, xs.p, sqrtw.p, omega_dev.p, x.p, st);                       // l.9, l.11
             else
