@@ -236,6 +236,8 @@ class Engine : public EngineBase {
     TailPlan tail;
     bool tail_ok = false;
     bool use_tail = std::getenv("MGPBD_NO_TAIL") == nullptr;
+    // the V-cycle's first two level-0 smoothing steps as one pass (MGPBD_NO_FUSE_J0=1 disables)
+    bool fuse_jacobi0 = std::getenv("MGPBD_NO_FUSE_J0") == nullptr;
     CoarseCycle<T> ccyc_top;
     ResPlan res_top;
     DBuf<ResLevel> rt_lv;
@@ -534,18 +536,18 @@ class Engine : public EngineBase {
     }
 
     void l0_pass(int mode, const T* xin, const T* b, T* y, const T* aux, double omega, double alpha = 0.0,
-                 const T* xprev = nullptr) {
+                 const T* xprev = nullptr, double x0_omega = 0.0) {
         const Level& l0 = *L[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         if (cfg.profile) { e0 = prof_event(); MG_CK(cudaEventRecord(e0, st)); }
-        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
+        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev, x0_omega);
         else csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
         if (cfg.profile) {
             e1 = prof_event();
             MG_CK(cudaEventRecord(e1, st));
             (capturing ? capturing->ev : prof_pairs).emplace_back(e0, e1);
             l0_launches++;
-            l0_bytes_acc += pass_bytes(mode);
+            l0_bytes_acc += pass_bytes(mode) - (x0_omega != 0.0 ? (double)sizeof(T) * (r1 - r0) : 0.0);  // x not read
         }
     }
 
@@ -984,10 +986,17 @@ class Engine : public EngineBase {
             }
             return;
         }
-        vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.sm_omega[0], cur + o, st);  // step 0 from x = 0
-        for (int sw = 1; sw < nu; ++sw) {  // x_{sw+1} over x_{sw-1} (x_0 = 0: no xprev)
-            pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.sm_omega[sw], a.sm_alpha[sw], sw == 1 ? nullptr : nxt);
+        if (l == 0 && nu == 2 && fuse_jacobi0 && mf_on() && !dist && mf.tma && mf.vg_ts == 0) {
+            // steps 0 and 1 in one matrix pass: x_1 = omega_0 D^-1 b is formed inside the gathers (no k_jacobi0
+            // launch, no x_1 stream); same expressions, same result
+            l0_pass(PASS_JACOBI, nullptr, b, nxt, nullptr, a.sm_omega[1], a.sm_alpha[1], nullptr, a.sm_omega[0]);
             std::swap(cur, nxt);
+        } else {
+            vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.sm_omega[0], cur + o, st);  // step 0 from x = 0
+            for (int sw = 1; sw < nu; ++sw) {  // x_{sw+1} over x_{sw-1} (x_0 = 0: no xprev)
+                pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.sm_omega[sw], a.sm_alpha[sw], sw == 1 ? nullptr : nxt);
+                std::swap(cur, nxt);
+            }
         }
         Level& c = *L[l + 1];
         if (a.kk > 1) {  // general P (k > 1): r = b - A x, b_c = P^T r, x += P e

@@ -117,13 +117,16 @@ struct Chunk {
 #ifndef MGPBD_VG_ACC64
 #define MGPBD_VG_ACC64 0
 #endif
-template <class T, int G, int UN, bool J16>
+// XJ: x is not materialised — x_j = omega0 D^-1_jj b_j (the V-cycle's first smoothing step from x = 0,
+// k_jacobi0's expression), gathered from dinv and b.
+template <class T, int G, int UN, bool J16, bool XJ>
 __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
                                                       const int64_t* __restrict__ ppos,
                                                       const uint16_t* __restrict__ vj16,
                                                       const int32_t* __restrict__ vj32,
                                                       const int32_t* __restrict__ jbase, const T* __restrict__ hv,
-                                                      const T* __restrict__ x, V4<T>* __restrict__ u) {
+                                                      const T* __restrict__ x, V4<T>* __restrict__ u,
+                                                      const T* __restrict__ xd, const T* __restrict__ xb, double xom) {
     // programmatic dependent launch: the row kernel may start streaming its static operands now; it
     // waits (griddepcontrol.wait) for this grid's u before gathering it
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -154,7 +157,11 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
 #pragma unroll
                 for (int q = 0; q < UN; ++q)
 #pragma unroll
-                    for (int w = 0; w < VW; ++w) xv[q][w] = x[jb + c[q].j[w]];
+                    for (int w = 0; w < VW; ++w) {
+                        const int32_t jj = jb + c[q].j[w];
+                        if (XJ) xv[q][w] = (T)(xom * (double)xd[jj] * (double)xb[jj]);
+                        else xv[q][w] = x[jj];
+                    }
 #pragma unroll
                 for (int q = 0; q < UN; ++q)
 #pragma unroll
@@ -432,7 +439,8 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
                                                       const T* __restrict__ b, T* __restrict__ y,
                                                       const T* __restrict__ aux, double omega, double alpha,
                                                       const T* __restrict__ xprev, double* __restrict__ parts,
-                                                      double* __restrict__ parts2) {
+                                                      double* __restrict__ parts2, double xom) {
+    // xom != 0 (PASS_JACOBI only): x is not materialised, x_i = xom D^-1_ii b_i (see k_mf_vgather XJ)
     using LY = TileLayout<T, KC, V16>;
     constexpr int MF_RK = LY::R;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -456,12 +464,13 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         auto rnd = [](uint32_t by) { return (by + 15u) & ~15u; };
         const uint32_t bh = rnd(rows * KC * 3 * sizeof(T)), bv = rnd(rows * KC * LY::VB),
                        bs = rnd(rows * sizeof(T));
-        uint32_t tot = bh + bv + 2 * bs + (ND ? bs : 0) + (NB ? bs : 0) + (NA ? bs : 0) + (NP ? bs : 0);
+        const bool XJ = xom != 0.0;
+        uint32_t tot = bh + bv + (XJ ? 0 : bs) + bs + (ND ? bs : 0) + (NB ? bs : 0) + (NA ? bs : 0) + (NP ? bs : 0);
         uint64_t* bar = &bars[j % MF_STAGES];
         mbar_expect_tx(bar, tot);
         bulk_g2s(st + LY::H, h + (int64_t)i0 * KC * 3, bh, bar);
         bulk_g2s(st + LY::V, reinterpret_cast<const unsigned char*>(verts_) + (int64_t)i0 * KC * LY::VB, bv, bar);
-        bulk_g2s(st + LY::X, x + i0, bs, bar);
+        if (!XJ) bulk_g2s(st + LY::X, x + i0, bs, bar);
         bulk_g2s(st + LY::AT, at + i0, bs, bar);
         if (ND) bulk_g2s(st + LY::D, dinv + i0, bs, bar);
         if (NB) bulk_g2s(st + LY::B, b + i0, bs, bar);
@@ -495,7 +504,9 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
                 }
                 load_record<T, KC>(reinterpret_cast<const T*>(st + LY::H) + t * KC * 3, hi);
             }
-            const T xi = reinterpret_cast<const T*>(st + LY::X)[t];
+            const T xi = xom != 0.0 ? (T)(xom * (double)reinterpret_cast<const T*>(st + LY::D)[t] *
+                                          (double)reinterpret_cast<const T*>(st + LY::B)[t])
+                                    : reinterpret_cast<const T*>(st + LY::X)[t];
             T acc = reinterpret_cast<const T*>(st + LY::AT)[t] * xi;
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
@@ -541,7 +552,9 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
 
 template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-                double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
+                double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev, double xom) {
+    if (xom != 0.0 && (mode != PASS_JACOBI || !A.tma || A.vg_ts > 0))
+        throw Error(-1, "mf_pass: implicit x (x0_omega) needs PASS_JACOBI and the TMA row kernel");
     if (A.v1 > A.v0) {
         // G lanes per vertex, UN 16-byte chunks per lane per round (~23 incidences per vertex on tets = 6 float4
         // chunks, ~6 on cloth = 2); build-time overridable for tuning sweeps
@@ -575,12 +588,14 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
                 k_mf_vgather_tma<T, GT, false><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
                                                                     A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
             }
-        } else if (A.vj16)
-            k_mf_vgather<T, G, UN, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase,
-                                                                A.hv, x, reinterpret_cast<V4<T>*>(A.u));
-        else
-            k_mf_vgather<T, G, UN, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase,
-                                                                 A.hv, x, reinterpret_cast<V4<T>*>(A.u));
+        } else {
+#define MG_VG(J, X)                                                                                     \
+    k_mf_vgather<T, G, UN, J, X><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, \
+                                                        x, reinterpret_cast<V4<T>*>(A.u), A.dinv, b, xom)
+            if (A.vj16) { if (xom != 0.0) MG_VG(true, true); else MG_VG(true, false); }
+            else { if (xom != 0.0) MG_VG(false, true); else MG_VG(false, false); }
+#undef MG_VG
+        }
         MG_LAUNCH_CHECK();
     }
     const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
@@ -606,7 +621,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         MG_CK(cudaLaunchKernelEx(&lc, k_mf_rows_tma<T, KC, M, V16>, A.row0, A.row1, tbase, ntiles,              \
                                  V16 ? (const void*)A.v16 : (const void*)A.verts, A.vbase, A.h, u,              \
                                  (const T*)A.at, (const T*)A.dinv, x, b, y, aux, omega, alpha, xprev, parts,    \
-                                 parts2));                                                                      \
+                                 parts2, xom));                                                                 \
     }
         switch (mode) {
             case PASS_JACOBI: MG_MFT(PASS_JACOBI); break;
@@ -710,9 +725,9 @@ void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cu
 
 template <class T>
 void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-             double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev) {
-    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev);
-    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev);
+             double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev, double xom) {
+    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom);
+    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom);
 }
 
 template <class T>
@@ -736,7 +751,7 @@ void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const doub
     template void mf_update<T>(const MatFree<T>&, const T*, const double*, const double*, double*, cudaStream_t); \
     template void mf_refresh<T>(const MatFree<T>&, const double*, double, T*, cudaStream_t);                     \
     template void mf_pass<T>(int, const MatFree<T>&, const T*, const T*, T*, const T*, double, double*, double*, \
-                             cudaStream_t, double, const T*);
+                             cudaStream_t, double, const T*, double);
 MG_INST(float)
 MG_INST(double)
 #undef MG_INST

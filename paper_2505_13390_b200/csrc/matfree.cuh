@@ -76,8 +76,11 @@ void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const doub
 
 // One level-0 pass of `mode` (PASS_JACOBI, PASS_JACOBI_DOT, PASS_RESID_P, PASS_SPMV_DOT, PASS_POWER);
 // same arguments and outputs as csr_pass, A.grid partials.
+// x0_omega != 0 (PASS_JACOBI, TMA row kernel): x is not read — x_i = x0_omega D^-1_ii b_i, the first smoothing
+// step from x = 0 fused into the second (the V-cycle's k_jacobi0 expression, bit for bit).
 template <class T>
 void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-             double* parts, double* parts2, cudaStream_t s, double alpha = 0.0, const T* xprev = nullptr);
+             double* parts, double* parts2, cudaStream_t s, double alpha = 0.0, const T* xprev = nullptr,
+             double x0_omega = 0.0);
 
 }  // namespace mgpbd
