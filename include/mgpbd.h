@@ -186,9 +186,11 @@ MGPBD_API mgpbd_status mgpbd_setup_hierarchy(mgpbd_ctx* ctx);
  * returned. */
 MGPBD_API mgpbd_status mgpbd_step(mgpbd_ctx* ctx, double dt, int32_t n_iters);
 
-/* Enable (1) / disable (0) CUDA-event timing of the level-0 matrix passes (mgpbd_stats.l0_pass_*).
- * While enabled the per-iteration CUDA graphs are not used: the same kernels launch eagerly between
- * event records.  Errors: MGPBD_E_ARG for a NULL context. */
+/* CUDA-event timing of the level-0 matrix passes (mgpbd_stats.l0_pass_*): 0 off; 1 eager — the
+ * per-iteration CUDA graphs are not used, the same kernels launch eagerly between event records (and the
+ * phase times ms_* are recorded); 2 in-graph — the pass events are captured as nodes of the replayed
+ * per-iteration graph (the launch configuration the bench times); each replay overwrites them, so the last
+ * replay's pass durations stand for every outer iteration.  Errors: MGPBD_E_ARG for a NULL context. */
 MGPBD_API mgpbd_status mgpbd_set_profiling(mgpbd_ctx* ctx, int32_t on);
 
 /* Upload a new state (3*n_verts each; vel may be NULL = unchanged). */

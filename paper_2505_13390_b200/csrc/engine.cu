@@ -539,12 +539,18 @@ class Engine : public EngineBase {
                  const T* xprev = nullptr, double x0_omega = 0.0) {
         const Level& l0 = *L[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (cfg.profile) { e0 = prof_event(); MG_CK(cudaEventRecord(e0, st)); }
+        // inside stream capture a plain record is only a dependency: cudaEventRecordExternal makes it an event
+        // record node whose timestamp the replay writes
+        auto rec = [&](cudaEvent_t e) {
+            if (capturing) MG_CK(cudaEventRecordWithFlags(e, st, cudaEventRecordExternal));
+            else MG_CK(cudaEventRecord(e, st));
+        };
+        if (cfg.profile) { e0 = prof_event(); rec(e0); }
         if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev, x0_omega);
         else csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
         if (cfg.profile) {
             e1 = prof_event();
-            MG_CK(cudaEventRecord(e1, st));
+            rec(e1);
             (capturing ? capturing->ev : prof_pairs).emplace_back(e0, e1);
             l0_launches++;
             l0_bytes_acc += pass_bytes(mode) - (x0_omega != 0.0 ? (double)sizeof(T) * (r1 - r0) : 0.0);  // x not read
@@ -1122,13 +1128,22 @@ class Engine : public EngineBase {
         mark_stage(5);
     }
 
-    void set_profiling(int on) override { cfg.profile = on ? 1 : 0; }
+    // 1: eager launches with CUDA events around every level-0 pass and phase; 2: the same pass events captured
+    // as nodes of the per-iteration graph (the replayed frame as the bench times it; each replay overwrites
+    // the events, so the last replay's pass durations stand for every outer iteration of the frame)
+    bool graph_profile = false;
+    void set_profiling(int on) override {
+        const bool gp = on == 2;
+        if (gp != graph_profile || (on != 0) != (cfg.profile != 0)) invalidate_graphs();
+        graph_profile = gp;
+        cfg.profile = on ? 1 : 0;
+    }
 
     // One graph serves every outer iteration (the iteration index reaches the kernels through flags[7]),
     // so after a setup only the second outer iteration pays the capture + instantiation.
     void run_iter(int ite) {
         set_outer_index(flags.p, std::min(ite, 500000), st);  // error tags ite*4096 + k stay within int32
-        if (!use_graphs || cfg.profile) { iter_body(ite); return; }  // events need eager launches
+        if (!use_graphs || (cfg.profile && !graph_profile)) { iter_body(ite); return; }  // eager event timing
         if (graphs.empty()) graphs.resize(1);
         IterGraph& g = graphs[0];
         if (!g.seen) {  // first use after a (re)build: eager

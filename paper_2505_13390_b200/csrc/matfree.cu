@@ -119,8 +119,14 @@ struct Chunk {
 #endif
 // XJ: x is not materialised — x_j = omega0 D^-1_jj b_j (the V-cycle's first smoothing step from x = 0,
 // k_jacobi0's expression), gathered from dinv and b.
+#ifndef MGPBD_VG_MINB
+#define MGPBD_VG_MINB 1
+#endif
+#ifndef MGPBD_VG_PREFETCH
+#define MGPBD_VG_PREFETCH 1
+#endif
 template <class T, int G, int UN, bool J16, bool XJ>
-__global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
+__global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
                                                       const int64_t* __restrict__ ppos,
                                                       const uint16_t* __restrict__ vj16,
                                                       const int32_t* __restrict__ vj32,
@@ -139,13 +145,23 @@ __global__ void __launch_bounds__(MF_BS) k_mf_vgather(int32_t v0, int32_t v1, in
     const T* __restrict__ hx = hv;
     const T* __restrict__ hy = hv + npad;
     const T* __restrict__ hz = hv + 2 * npad;
+    // the next vertex's slot range and index base are fetched one round ahead (one dependent round trip less
+    // per vertex)
+    int64_t p0n = 0, p1n = 0;
+    int32_t jbn = 0;
+    auto fetch = [&](int64_t vv) {
+        if (vv < v1) { p0n = ppos[vv]; p1n = ppos[vv + 1]; jbn = J16 ? jbase[vv] : 0; }
+    };
+    if (MGPBD_VG_PREFETCH) fetch(v0 + warp * PER_WARP + sub);
     for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {  // warp-uniform
         const int64_t v = base + sub;
         using AC = typename std::conditional<MGPBD_VG_ACC64 != 0, double, T>::type;
         AC a0 = (AC)0, a1 = (AC)0, a2 = (AC)0;
+        if (!MGPBD_VG_PREFETCH) fetch(v);
+        const int64_t p0 = p0n, p1 = p1n;
+        const int32_t jb = jbn;
+        if (MGPBD_VG_PREFETCH) fetch(v + nwarps * PER_WARP);
         if (v < v1) {
-            const int64_t p0 = ppos[v], p1 = ppos[v + 1];
-            const int32_t jb = J16 ? jbase[v] : 0;
             for (int64_t pb = p0 + (int64_t)sl * VW; pb < p1; pb += (int64_t)G * VW * UN) {
                 CH c[UN];
 #pragma unroll

@@ -236,8 +236,9 @@ class Context:
     def step(self, dt, n_iters):
         self._ck(lib().mgpbd_step(self.h, float(dt), int(n_iters)))
 
-    def set_profiling(self, on: bool):
-        self._ck(lib().mgpbd_set_profiling(self.h, 1 if on else 0))
+    def set_profiling(self, on):
+        """False/0 off, True/1 eager event timing, 2 events captured inside the replayed graphs."""
+        self._ck(lib().mgpbd_set_profiling(self.h, int(on)))
 
     def set_state(self, pos, vel=None):
         pos = np.ascontiguousarray(pos, np.float64)
