@@ -4,6 +4,7 @@
 #include <algorithm>
 
 #include "coarse_res.cuh"
+#include "coarse_tail_body.cuh"
 #include "comm.cuh"
 #include "tma.cuh"
 #include "util.cuh"
@@ -129,9 +130,14 @@ __device__ __forceinline__ void dense_solve(const Lanes& w, int32_t n, const Sli
 template <class T>
 __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_constant__ CoarseCycle<T> c,
                                                              const __grid_constant__ ResPlan plan, int mode,
-                                                             int kstop) {
+                                                             int kstop, const __grid_constant__ TailArgs<T> ta,
+                                                             uint32_t tail_base) {
     // mode 0: the whole cycle; 1: down phase of levels 0..kstop-1 (ends with b of level kstop); 2: up phase
-    // from level kstop-1 (z of level kstop given) — levels >= kstop then run on the cluster tail kernel
+    // from level kstop-1 (z of level kstop given) — levels >= kstop then run on the cluster tail kernel;
+    // 3: 1, then the tail on the first cluster of this (cooperative + cluster) launch, then 2 — one launch
+    __shared__ TailLevel tail_lv[TAIL_MAXL];
+    __shared__ __align__(8) uint64_t tail_bar;
+    __shared__ __align__(8) uint64_t tail_pbars[2];
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
@@ -155,6 +161,8 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
         for (int k = 0; k < plan.ncopies[cta]; ++k) bulk_g2s(smem + cp[k].dst, cp[k].src, cp[k].bytes, &bar);
     }
     __syncthreads();
+    // mode 3: the first cluster also stages its static tail data now, behind the grid levels' work
+    if (mode == 3 && blockIdx.x < (unsigned)ta.CT) tail_detail::coarse_tail_load<T>(ta, smem + tail_base, tail_lv, tail_bar, tail_pbars);
     mbar_wait(&bar, 0);
     int tix = 0;
     auto mark = [&]() {
@@ -203,6 +211,10 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
         grid.sync(); mark();
     }
     if (mode == 1) return;
+    if (mode == 3) {  // the tail levels on the first cluster while the other CTAs wait at the grid barrier
+        if (blockIdx.x < (unsigned)ta.CT) tail_detail::coarse_tail_body<T>(ta, smem + tail_base, tail_lv, tail_bar, tail_pbars);
+        grid.sync(); mark();
+    }
     // ---- coarsest
     if (mode == 0) dense_solve(w, sc.L[K - 1].n, slice(K - 1), sc.L[K - 1].b, sc.L[K - 1].z);
     // ---- up
@@ -327,20 +339,56 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
 }
 
 template <class T>
-void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s, int mode, int kstop) {
-    ensure_dyn_smem((const void*)k_coarse_vcycle_res<T>, plan.smem);
+void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s, int mode, int kstop,
+                       const TailArgs<T>* tail, uint32_t tail_base, uint32_t tail_smem) {
+    const uint32_t smem = mode == 3 ? tail_base + tail_smem : plan.smem;
+    ensure_dyn_smem((const void*)k_coarse_vcycle_res<T>, smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.G);
     cfg.blockDim = dim3(RB);
-    cfg.dynamicSmemBytes = plan.smem;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr_[1];
+    cudaLaunchAttribute attr_[2];
     attr_[0].id = cudaLaunchAttributeCooperative;
     attr_[0].val.cooperative = 1;
+    attr_[1].id = cudaLaunchAttributeClusterDimension;
+    attr_[1].val.clusterDim.x = mode == 3 ? (unsigned)tail->CT : 1u;
+    attr_[1].val.clusterDim.y = 1; attr_[1].val.clusterDim.z = 1;
     cfg.attrs = attr_;
-    cfg.numAttrs = 1;
-    MG_CK(cudaLaunchKernelEx(&cfg, k_coarse_vcycle_res<T>, c, plan, mode, kstop));
+    cfg.numAttrs = mode == 3 ? 2 : 1;
+    TailArgs<T> ta;
+    if (tail) ta = *tail;
+    MG_CK(cudaLaunchKernelEx(&cfg, k_coarse_vcycle_res<T>, c, plan, mode, kstop, ta, tail_base));
     MG_LAUNCH_CHECK();
+}
+
+// Co-resident CTAs of a cooperative launch of the fused (mode 3) kernel in clusters of CT with `smem` bytes
+// (a multiple of CT; 0: not launchable).
+template <class T>
+int coarse_res_fused_grid(int CT, uint32_t smem) {
+    if (!try_raise_dyn_smem((const void*)k_coarse_vcycle_res<T>, smem)) return 0;
+    if (CT > 8 && cudaFuncSetAttribute((const void*)k_coarse_vcycle_res<T>, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                                       1) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(CT);
+    cfg.blockDim = dim3(RB);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CT; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;
+    at[1].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, (const void*)k_coarse_vcycle_res<T>, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return 0;
+    }
+    return nc * CT;
 }
 
 template <class T>
@@ -358,7 +406,9 @@ int coarse_res_blocks_per_sm(uint32_t smem) {
     template bool coarse_res_plan<T>(const CoarseCycle<T>&, int, uint32_t, std::vector<ResLevel>&,             \
                                      std::vector<ResCopy>&, std::vector<int32_t>&, std::vector<uint32_t>&,     \
                                      uint32_t&, cudaStream_t, bool);                                           \
-    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t, int, int);      \
+    template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t, int, int,         \
+                                       const TailArgs<T>*, uint32_t, uint32_t);                                \
+    template int coarse_res_fused_grid<T>(int, uint32_t);                                                      \
     template int coarse_res_blocks_per_sm<T>(uint32_t);
 MG_INST(float)
 MG_INST(double)

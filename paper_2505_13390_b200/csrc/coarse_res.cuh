@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "coarse.cuh"
+#include "coarse_tail.cuh"
 
 namespace mgpbd {
 
@@ -48,9 +49,15 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
                      uint32_t& smem, cudaStream_t s, bool with_coarsest = true);
 
 // mode 0: the whole cycle; 1: down phase of levels 0..kstop-1 (leaves b of level kstop); 2: up phase from
-// level kstop-1 (reads z of level kstop).
+// level kstop-1 (reads z of level kstop); 3: 1 + the cluster tail (coarse_tail.cuh) on the launch's first
+// cluster + 2, in ONE cooperative launch with cluster dimensions (tail: its arguments, its shared-memory
+// region at tail_base of tail_smem bytes).
 template <class T>
-void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s, int mode = 0, int kstop = 0);
+void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_t s, int mode = 0, int kstop = 0,
+                       const TailArgs<T>* tail = nullptr, uint32_t tail_base = 0, uint32_t tail_smem = 0);
+// co-resident CTAs of the mode-3 launch in clusters of CT with `smem` bytes (multiple of CT; 0: none)
+template <class T>
+int coarse_res_fused_grid(int CT, uint32_t smem);
 // CTAs of k_coarse_vcycle_res<T> that fit on one SM with `smem` dynamic bytes (0: the resident plan
 // cannot be launched cooperatively at one CTA per SM; the caller falls back to the global kernel)
 template <class T>

@@ -5,6 +5,7 @@
 #include <cstdlib>
 
 #include "coarse_tail.cuh"
+#include "coarse_tail_body.cuh"
 #include "comm.cuh"
 #include "tma.cuh"
 #include "util.cuh"
@@ -15,233 +16,16 @@ namespace mgpbd {
 
 namespace {
 
-constexpr int TB = 1024;        // threads per CTA
-constexpr int TVL = 8;          // lanes per row
-constexpr int TCH = 5;          // nonzeros per lane per chunk
-constexpr int TRPW = 32 / TVL;  // rows per warp
-constexpr int TWARPS = TB / 32;
-
-template <class U>
-__device__ __forceinline__ U* sp(unsigned char* sm, uint32_t off) { return reinterpret_cast<U*>(sm + off); }
-
-template <class T>
-struct Tail {
-    unsigned char* sm;
-    cg::cluster_group cl;
-    int CT, me;
-    int lane, sub, sl, warp;
-
-    // store value v at element `idx` of the buffer at smem offset `off` in every CTA of the cluster
-    // (the 8 lanes of a row group share the CT stores)
-    __device__ __forceinline__ void bcast_row(uint32_t off, int32_t idx, T v) {
-        T* loc = sp<T>(sm, off) + idx;
-        for (int r = sl; r < CT; r += TVL) *cl.map_shared_rank(loc, r) = v;
-    }
-    __device__ __forceinline__ void bcast_elem(uint32_t off, int32_t idx, T v, int r) {
-        *cl.map_shared_rank(sp<T>(sm, off) + idx, r) = v;
-    }
-
-    // sum_k A_ik x[col_k] for own row i of level D (matrix and x in local shared memory)
-    __device__ __forceinline__ double row_sum(const TailLevel& D, bool valid, int32_t i, uint32_t xoff) const {
-        const int64_t* rp = sp<int64_t>(sm, D.o_rp);
-        const uint16_t* col = sp<uint16_t>(sm, D.o_col);
-        const T* val = sp<T>(sm, D.o_val);
-        const T* x = sp<T>(sm, xoff);
-        const int64_t a = valid ? rp[i - D.r0] - D.e0 : 0, e = valid ? rp[i - D.r0 + 1] - D.e0 : 0;
-        const int maxlen = __reduce_max_sync(0xffffffffu, (int)(e - a));
-        T part = (T)0;
-        for (int off = 0; off < maxlen; off += TVL * TCH) {
-            T v[TCH], xv[TCH];
-#pragma unroll
-            for (int q = 0; q < TCH; ++q) {
-                const int64_t k = a + off + q * TVL + sl;
-                const bool in = k < e;
-                v[q] = in ? val[k] : (T)0;
-                xv[q] = in ? x[col[k]] : (T)0;
-            }
-#pragma unroll
-            for (int q = 0; q < TCH; ++q) part += v[q] * xv[q];
-        }
-        return (double)group_sum_t<TVL>(part);
-    }
-};
+constexpr int TB = tail_detail::TB;
 
 template <class T>
 __global__ void __launch_bounds__(TB, 1) k_coarse_tail(const __grid_constant__ TailArgs<T> A) {
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
     __shared__ TailLevel L[TAIL_MAXL];
-    Tail<T> W{smem, cg::this_cluster(), A.CT, 0, 0, 0, 0, 0};
-    W.me = (int)W.cl.block_rank();
-    W.lane = threadIdx.x & 31; W.sub = W.lane / TVL; W.sl = W.lane % TVL; W.warp = threadIdx.x >> 5;
-    const int me = W.me;
-    {
-        const int* src = reinterpret_cast<const int*>(A.lv + (size_t)me * TAIL_MAXL);
-        int* dst = reinterpret_cast<int*>(L);
-        for (int k = threadIdx.x; k < (int)(TAIL_MAXL * sizeof(TailLevel) / sizeof(int)); k += TB) dst[k] = src[k];
-    }
-    if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(&bar, A.txbytes[me]);
-        const TailCopy* cp = A.copies + (size_t)me * TAIL_MAXC;
-        for (int k = 0; k < A.ncopies[me]; ++k) bulk_g2s(smem + cp[k].dst, cp[k].src, cp[k].bytes, &bar);
-    }
-    __syncthreads();
-    mbar_wait(&bar, 0);
-    int tix = 0;
-    auto sync = [&]() {
-        W.cl.sync();
-        if (A.trace && me == 0 && threadIdx.x == 0 && tix < 64) {
-            unsigned long long t;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-            A.trace[tix] = t;
-        }
-        ++tix;
-    };
-    sync();  // every CTA of the cluster is resident and loaded before the first DSMEM store
-    const int KT = A.KT, nu = A.nu;
-    uint32_t cur[TAIL_MAXL];   // buffer holding the pre-smoothed x of each level after the down phase
-    // ---------------------------------------------------------------- down
-    {   // x_1 = omega_0 D^-1 b on the first tail level (own rows) -> every CTA's X
-        const TailLevel& D = L[0];
-        const T* b = sp<T>(smem, D.o_b);
-        const T* d = sp<T>(smem, D.o_dinv);
-        const int32_t own = D.r1 - D.r0;
-        for (int q = threadIdx.x; q < own * A.CT; q += TB) {
-            const int32_t i = q / A.CT;
-            const T y = (T)(A.sm_omega[0][0] * (double)d[i] * (double)b[i]);
-            W.bcast_elem(D.o_X, D.r0 + i, y, q % A.CT);
-        }
-        sync();
-    }
-    for (int t = 0; t + 1 < KT; ++t) {
-        const TailLevel& D = L[t];
-        const T* b = sp<T>(smem, D.o_b);
-        const T* d = sp<T>(smem, D.o_dinv);
-        uint32_t in = D.o_X, out = D.o_Y;
-        for (int s = 1; s < nu; ++s) {   // pre-smoothing steps 1..nu-1 (step 0 = x_1 above / in restrict)
-            const double om = A.sm_omega[t][s], al = A.sm_alpha[t][s];
-            for (int32_t base = D.r0 + W.warp * TRPW; base < D.r1; base += TWARPS * TRPW) {
-                const int32_t i = base + W.sub;
-                const bool valid = i < D.r1;
-                const double sum = W.row_sum(D, valid, i, in);
-                if (valid) {
-                    const int32_t li = i - D.r0;
-                    const double xi = (double)sp<T>(smem, in)[i];
-                    double y = xi + om * (double)d[li] * ((double)b[li] - sum);
-                    if (al != 0.0) y += al * (xi - (s == 1 ? 0.0 : (double)sp<T>(smem, out)[i]));
-                    W.bcast_row(out, i, (T)y);
-                }
-            }
-            sync();
-            const uint32_t tt = in; in = out; out = tt;
-        }
-        cur[t] = in;
-        // residual * P -> the owner of the aggregate's slot (one DSMEM store per row)
-        {
-            const T* P = sp<T>(smem, D.o_P);
-            const int32_t* push = sp<int32_t>(smem, D.o_push);
-            for (int32_t base = D.r0 + W.warp * TRPW; base < D.r1; base += TWARPS * TRPW) {
-                const int32_t i = base + W.sub;
-                const bool valid = i < D.r1;
-                const double sum = W.row_sum(D, valid, i, in);
-                if (valid && W.sl == 0) {
-                    const int32_t li = i - D.r0;
-                    const int32_t code = push[li];
-                    T* dst = sp<T>(smem, D.o_slot) + (code & 0xFFFFFF);
-                    *W.cl.map_shared_rank(dst, (unsigned)code >> 24) = (T)((double)P[li] * ((double)b[li] - sum));
-                }
-            }
-            sync();
-        }
-        // restriction over the own aggregates (members ascending) = own rows of level t+1
-        {
-            const TailLevel& N = L[t + 1];
-            const int64_t* mp = sp<int64_t>(smem, D.o_mp);
-            const T* slot = sp<T>(smem, D.o_slot);
-            T* bn = sp<T>(smem, N.o_b);
-            const bool coarsest = t + 2 == KT;
-            const T* dn = coarsest ? nullptr : sp<T>(smem, N.o_dinv);
-            const double om0 = A.sm_omega[t + 1][0];
-            for (int32_t base = D.a0 + W.warp * TRPW; base < D.a1; base += TWARPS * TRPW) {
-                const int32_t a = base + W.sub;
-                double sum = 0.0;
-                if (a < D.a1) {
-                    const int64_t s0 = mp[a - D.a0] - D.m0, s1 = mp[a - D.a0 + 1] - D.m0;
-                    for (int64_t q = s0 + W.sl; q < s1; q += TVL) sum += (double)slot[q];
-                }
-                sum = group_sum<TVL>(sum);
-                if (a < D.a1) {
-                    if (W.sl == 0) bn[a - N.r0] = (T)sum;
-                    // next level: its first smoothing step x_1 = omega_0 D^-1 b (or, coarsest, b itself)
-                    const T y = coarsest ? (T)sum : (T)(om0 * (double)dn[a - N.r0] * sum);
-                    W.bcast_row(N.o_X, a, y);
-                }
-            }
-            sync();
-        }
-    }
-    // ---------------------------------------------------------------- coarsest: z = A_c^-1 b (fp64 rows)
-    {
-        const TailLevel& C = L[KT - 1];
-        const double* Ai = sp<double>(smem, C.o_Ainv);
-        const T* bc = sp<T>(smem, C.o_X);
-        for (int32_t i = C.r0 + W.warp; i < C.r1; i += TWARPS) {
-            double s = 0.0;
-            for (int32_t j = W.lane; j < C.n; j += 32) s += Ai[(int64_t)(i - C.r0) * C.n + j] * (double)bc[j];
-            s = group_sum<32>(s);
-            // 32 lanes share the CT stores
-            const T zi = (T)s;
-            for (int r = W.lane; r < A.CT; r += 32) W.bcast_elem(C.o_Y, i, zi, r);
-        }
-        sync();
-    }
-    // ---------------------------------------------------------------- up
-    uint32_t zbuf = L[KT - 1].o_Y;   // full z of the level below
-    for (int t = KT - 2; t >= 0; --t) {
-        const TailLevel& D = L[t];
-        const T* b = sp<T>(smem, D.o_b);
-        const T* d = sp<T>(smem, D.o_dinv);
-        const T* P = sp<T>(smem, D.o_P);
-        const int32_t* agg = sp<int32_t>(smem, D.o_agg);
-        const T* zc = sp<T>(smem, zbuf);
-        const uint32_t c0 = cur[t], other = c0 == D.o_X ? D.o_Y : D.o_X;
-        {   // prolongation x_0 = x + P z_c[agg] (own rows) -> every CTA
-            const int32_t own = D.r1 - D.r0;
-            const T* xc = sp<T>(smem, c0);
-            for (int q = threadIdx.x; q < own * A.CT; q += TB) {
-                const int32_t li = q / A.CT;
-                const T y = (T)((double)xc[D.r0 + li] + (double)P[li] * (double)zc[agg[li]]);
-                W.bcast_elem(other, D.r0 + li, y, q % A.CT);
-            }
-            sync();
-        }
-        uint32_t in = other, out = c0;
-        for (int s = 0; s < nu; ++s) {
-            const double om = A.sm_omega[t][s], al = A.sm_alpha[t][s];
-            const bool last = s == nu - 1;
-            for (int32_t base = D.r0 + W.warp * TRPW; base < D.r1; base += TWARPS * TRPW) {
-                const int32_t i = base + W.sub;
-                const bool valid = i < D.r1;
-                const double sum = W.row_sum(D, valid, i, in);
-                if (valid) {
-                    const int32_t li = i - D.r0;
-                    const double xi = (double)sp<T>(smem, in)[i];
-                    double y = xi + om * (double)d[li] * ((double)b[li] - sum);
-                    if (al != 0.0 && s > 0) y += al * (xi - (double)sp<T>(smem, out)[i]);
-                    if (last && t == 0) {
-                        if (W.sl == 0) A.z_top[i] = (T)y;
-                    } else {
-                        W.bcast_row(out, i, (T)y);
-                    }
-                }
-            }
-            if (!(last && t == 0)) sync();
-            const uint32_t tt = in; in = out; out = tt;
-        }
-        zbuf = in;   // the buffer the last step wrote
-    }
+    __shared__ __align__(8) uint64_t pbars[2];
+    tail_detail::coarse_tail_load<T>(A, smem, L, bar, pbars);
+    tail_detail::coarse_tail_body<T>(A, smem, L, bar, pbars);
 }
 
 }  // namespace
@@ -303,7 +87,9 @@ bool coarse_tail_plan(const CoarseCycle<T>& c, int min_first, int CT, uint32_t s
         bool fits16 = true;
         for (int k = first; k + 1 < K; ++k) fits16 = fits16 && c.L[k].n <= 65536;
         if (!fits16) continue;
-        // row partitions: nnz-balanced (coarsest: even)
+        // row partitions: nnz-balanced (coarsest: even), interior bounds rounded to 16-byte multiples so every
+        // CTA's own range can be broadcast as one bulk copy
+        const int32_t VEC = (int32_t)(16 / ts);
         std::vector<std::vector<int32_t>> rb(KT);
         for (int t = 0; t < KT; ++t) {
             const int k = first + t;
@@ -312,6 +98,8 @@ bool coarse_tail_plan(const CoarseCycle<T>& c, int min_first, int CT, uint32_t s
                 rb[t].resize(CT + 1);
                 for (int g = 0; g <= CT; ++g) rb[t][g] = (int32_t)((int64_t)c.L[k].n * g / CT);
             }
+            for (int g = 1; g < CT; ++g)
+                rb[t][g] = std::max(rb[t][g - 1], std::min(c.L[k].n, (rb[t][g] + VEC / 2) / VEC * VEC));
         }
         // smem layout per CTA
         std::vector<TailLevel> lv((size_t)CT * TAIL_MAXL);
@@ -356,8 +144,9 @@ bool coarse_tail_plan(const CoarseCycle<T>& c, int min_first, int CT, uint32_t s
         };
         for (int t = 0; t < KT; ++t) {
             const int k = first + t;
-            common_alloc(oX[t], (size_t)c.L[k].n * ts);
-            common_alloc(oY[t], (size_t)c.L[k].n * ts);
+            const size_t npad = ((size_t)c.L[k].n + VEC - 1) / VEC * VEC;   // the last CTA's range rounds up
+            common_alloc(oX[t], npad * ts);
+            common_alloc(oY[t], npad * ts);
             if (t + 1 < KT) {
                 int64_t mx = 0;
                 for (int g = 0; g < CT; ++g) mx = std::max(mx, mp[k][rb[t + 1][g + 1]] - mp[k][rb[t + 1][g]]);
@@ -411,14 +200,21 @@ bool coarse_tail_plan(const CoarseCycle<T>& c, int min_first, int CT, uint32_t s
                     ok = ok && add(d.o_mp, Lk.mptr, d.a0, 8, (size_t)(d.a1 - d.a0) + 1);
                     (void)mem;
                     d.o_slot = oS[t];
-                    if (t == 0) ok = ok && add(d.o_b, Lk.b, d.r0, ts, (size_t)rows);
-                    else alloc(d.o_b, ts, (size_t)rows);
+                    alloc(d.o_b, ts, (size_t)rows);   // t = 0: read from b_top by the kernel (not static)
                 } else {
                     ok = ok && add(d.o_Ainv, c.Ainv, (int64_t)d.r0 * Lk.n, 8, (size_t)rows * Lk.n);
                     alloc(d.o_b, ts, (size_t)rows);
                 }
                 d.o_X = oX[t];   // full-length vectors (global row index), common offsets
                 d.o_Y = oY[t];
+                auto obytes = [&](int gg) {
+                    const int32_t a = rb[t][gg], b = rb[t][gg + 1];
+                    return (uint32_t)(((int64_t)(b - a) * (int64_t)ts + 15) & ~(int64_t)15);
+                };
+                d.ob = obytes(g);
+                d.rx = 0;
+                for (int gg = 0; gg < CT; ++gg)
+                    if (gg != g) d.rx += obytes(gg);
             }
             ncp[g] = nc;
             smem = std::max(smem, cursor);
@@ -427,6 +223,7 @@ bool coarse_tail_plan(const CoarseCycle<T>& c, int min_first, int CT, uint32_t s
         if (!ok) continue;
         plan.first = first;
         plan.CT = CT;
+        plan.bulk = std::getenv("MGPBD_TAIL_SCALAR_BCAST") ? 0 : 1;
         plan.smem = smem;
         plan.lv.resize(lv.size()); h2d(plan.lv.p, lv.data(), lv.size(), s);
         plan.copies.resize(cps.size()); h2d(plan.copies.p, cps.data(), cps.size(), s);
@@ -436,6 +233,28 @@ bool coarse_tail_plan(const CoarseCycle<T>& c, int min_first, int CT, uint32_t s
         return true;
     }
     return false;
+}
+
+template <class T>
+TailArgs<T> coarse_tail_args(const CoarseCycle<T>& c, const TailPlan& plan) {
+    TailArgs<T> a;
+    a.KT = c.K - plan.first;
+    a.nu = c.nu;
+    a.CT = plan.CT;
+    a.lv = plan.lv.p;
+    a.copies = plan.copies.p;
+    a.ncopies = plan.ncopies.p;
+    a.txbytes = plan.txbytes.p;
+    a.b_top = c.L[plan.first].b;
+    a.z_top = c.L[plan.first].z;
+    for (int t = 0; t < a.KT && t < TAIL_MAXL; ++t)
+        for (int q = 0; q < 8; ++q) {
+            a.sm_omega[t][q] = c.L[plan.first + t].sm_omega[q];
+            a.sm_alpha[t][q] = c.L[plan.first + t].sm_alpha[q];
+        }
+    a.trace = c.trace ? c.trace + 32 : nullptr;
+    a.bulk = plan.bulk;
+    return a;
 }
 
 template <class T>
@@ -456,6 +275,7 @@ void coarse_tail_run(const CoarseCycle<T>& c, const TailPlan& plan, cudaStream_t
             a.sm_alpha[t][q] = c.L[plan.first + t].sm_alpha[q];
         }
     a.trace = c.trace ? c.trace + 32 : nullptr;
+    a.bulk = plan.bulk;
     ensure_dyn_smem((const void*)k_coarse_tail<T>, plan.smem);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(plan.CT);
@@ -474,7 +294,8 @@ void coarse_tail_run(const CoarseCycle<T>& c, const TailPlan& plan, cudaStream_t
 #define MG_INST(T)                                                                                               \
     template bool coarse_tail_plan<T>(const CoarseCycle<T>&, int, int, uint32_t, TailPlan&, cudaStream_t);     \
     template bool coarse_tail_launchable<T>(int, uint32_t);                                                      \
-    template void coarse_tail_run<T>(const CoarseCycle<T>&, const TailPlan&, cudaStream_t);
+    template void coarse_tail_run<T>(const CoarseCycle<T>&, const TailPlan&, cudaStream_t);                     \
+    template TailArgs<T> coarse_tail_args<T>(const CoarseCycle<T>&, const TailPlan&);
 MG_INST(float)
 MG_INST(double)
 #undef MG_INST

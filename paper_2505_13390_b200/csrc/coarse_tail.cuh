@@ -34,6 +34,8 @@ struct TailLevel {                // one CTA's share of one tail level (smem byt
     int64_t m0 = 0;               // mptr[a0]
     uint32_t o_rp = 0, o_col = 0, o_val = 0, o_dinv = 0, o_P = 0, o_agg = 0, o_push = 0, o_mp = 0;
     uint32_t o_slot = 0, o_b = 0, o_X = 0, o_Y = 0, o_Ainv = 0;
+    uint32_t ob = 0;              // bulk broadcast: bytes of this CTA's own rows (16-byte multiple)
+    uint32_t rx = 0;              //   and the bytes it receives from the other CTAs per broadcast
 };
 struct TailCopy {
     const void* src;
@@ -54,11 +56,13 @@ struct TailArgs {
     double sm_omega[TAIL_MAXL][8];
     double sm_alpha[TAIL_MAXL][8];
     unsigned long long* trace = nullptr;
+    int bulk = 0;                      // 1: broadcasts as cp.async.bulk shared::cta -> shared::cluster copies
 };
 
 struct TailPlan {
     int first = 0;                     // cycle index of the first tail level (levels first..K-1)
     int CT = 0;
+    int bulk = 0;                      // row ranges 16-byte aligned: bulk DSMEM broadcasts
     uint32_t smem = 0;
     DBuf<TailLevel> lv;
     DBuf<TailCopy> copies;
@@ -80,5 +84,8 @@ bool coarse_tail_launchable(int CT, uint32_t smem);
 // z_first = V(b_first) over the tail levels.
 template <class T>
 void coarse_tail_run(const CoarseCycle<T>& c, const TailPlan& plan, cudaStream_t s);
+// The kernel arguments of the tail (for the fused grid + cluster kernel, coarse_res.cuh mode 3).
+template <class T>
+TailArgs<T> coarse_tail_args(const CoarseCycle<T>& c, const TailPlan& plan);
 
 }  // namespace mgpbd

@@ -241,6 +241,19 @@ class Engine : public EngineBase {
     bool fuse_jacobi0 = std::getenv("MGPBD_FUSE_J0") != nullptr;
     CoarseCycle<T> ccyc_top;
     ResPlan res_top;
+    // fused variant: ONE cooperative launch with cluster dimensions runs the grid down half, the tail on its
+    // first cluster and the up half (no kernel boundaries); MGPBD_NO_FUSED_TAIL=1 keeps the three launches
+    TailPlan tail_f;
+    bool fused_ok = false;
+    bool use_fused = std::getenv("MGPBD_NO_FUSED_TAIL") == nullptr;
+    CoarseCycle<T> ccyc_f;
+    ResPlan res_f;
+    TailArgs<T> targs_f;
+    uint32_t tail_base_f = 0;
+    DBuf<ResLevel> rf_lv;
+    DBuf<ResCopy> rf_cp;
+    DBuf<int32_t> rf_nc;
+    DBuf<uint32_t> rf_tx;
     DBuf<ResLevel> rt_lv;
     DBuf<ResCopy> rt_cp;
     DBuf<int32_t> rt_nc;
@@ -847,8 +860,11 @@ class Engine : public EngineBase {
         if (tracing)
             std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, tail %s\n", nL,
                          !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u,
-                         tail_ok ? ("from cycle level " + std::to_string(tail.first) + " on " + std::to_string(tail.CT) +
-                                    " CTAs, " + std::to_string(tail.smem) + " B").c_str() : "off");
+                         tail_ok ? (std::string(fused_ok ? "fused, " : "split, ") + "from cycle level " +
+                                    std::to_string(fused_ok ? tail_f.first : tail.first) + " on " +
+                                    std::to_string(fused_ok ? tail_f.CT : tail.CT) + " CTAs, " +
+                                    std::to_string(fused_ok ? tail_f.smem : tail.smem) + " B" +
+                                    (fused_ok ? ", grid " + std::to_string(res_f.G) : std::string())).c_str() : "off");
         invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
         stale = false;
@@ -860,10 +876,44 @@ class Engine : public EngineBase {
     // Cluster tail of the coarse cycle: plan it on 16 (else 8) CTAs; the top part of the cycle becomes a
     // truncated cycle (levels 0..first of ccyc, the last one only receiving b / providing z) run by the
     // resident kernel's down and up halves.
+    bool setup_fused_tail() {
+        const uint32_t cap = 220u * 1024u;
+        for (int CT : {16, 8}) {
+            if (!coarse_tail_plan<T>(ccyc, 1, CT, 110u * 1024u, tail_f, st)) continue;
+            const int G = coarse_res_fused_grid<T>(CT, cap);
+            if (G < CT) continue;
+            CoarseCycle<T> top = ccyc;
+            top.K = tail_f.first + 1;
+            std::vector<ResLevel> lv;
+            std::vector<ResCopy> cp;
+            std::vector<int32_t> nc;
+            std::vector<uint32_t> tx;
+            uint32_t smem = 0;
+            const uint32_t tcap = cap - ((tail_f.smem + 127u) & ~127u);
+            if (!coarse_res_plan<T>(top, G, tcap, lv, cp, nc, tx, smem, st, /*with_coarsest=*/false)) continue;
+            tail_base_f = (smem + 127u) & ~127u;
+            if (coarse_res_fused_grid<T>(CT, tail_base_f + tail_f.smem) < G) continue;
+            rf_lv.resize(lv.size()); h2d(rf_lv.p, lv.data(), lv.size(), st);
+            rf_cp.resize(cp.size()); h2d(rf_cp.p, cp.data(), cp.size(), st);
+            rf_nc.resize(nc.size()); h2d(rf_nc.p, nc.data(), nc.size(), st);
+            rf_tx.resize(tx.size()); h2d(rf_tx.p, tx.data(), tx.size(), st);
+            res_f.G = G;
+            res_f.smem = smem;
+            res_f.lv = rf_lv.p; res_f.copies = rf_cp.p; res_f.ncopies = rf_nc.p; res_f.txbytes = rf_tx.p;
+            ccyc_f = top;
+            targs_f = coarse_tail_args<T>(ccyc, tail_f);
+            MG_CK(cudaStreamSynchronize(st));
+            return true;
+        }
+        return false;
+    }
+
     void setup_tail() {
         int sms = 148;
         MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
         const uint32_t cap = 220u * 1024u;
+        fused_ok = use_fused && setup_fused_tail();
+        if (fused_ok) { tail_ok = true; return; }
         for (int CT : {16, 8}) {
             if (coarse_tail_plan<T>(ccyc, 1, CT, cap, tail, st) && coarse_tail_launchable<T>(CT, tail.smem)) {
                 tail_ok = true;
@@ -952,7 +1002,9 @@ class Engine : public EngineBase {
             return;
         }
         if (l == ccyc_from && ccyc_ok && b == a.vb.p && x_out == a.vz.p) {
-            if (tail_ok) {  // grid-wide down half, cluster tail, grid-wide up half
+            if (fused_ok) {  // one cooperative + cluster launch: grid down half, tail on cluster 0, grid up half
+                coarse_vcycle_res<T>(ccyc_f, res_f, st, 3, tail_f.first, &targs_f, tail_base_f, tail_f.smem);
+            } else if (tail_ok) {  // grid-wide down half, cluster tail, grid-wide up half
                 coarse_vcycle_res<T>(ccyc_top, res_top, st, 1, tail.first);
                 coarse_tail_run<T>(ccyc, tail, st);
                 CoarseCycle<T> up = ccyc_top;
