@@ -127,6 +127,136 @@ __device__ __forceinline__ void dense_solve(const Lanes& w, int32_t n, const Sli
     }
 }
 
+// The solo tail (coarse_res.cuh SoloLevel): cycle levels js..K-1 of `c` by this CTA alone.  Same operators,
+// smoothing steps and lane structure (8 lanes per row, fixed butterfly) as the grid phases; reads b of level
+// js from global memory and writes its z there.
+template <class T>
+__device__ void solo_cycle(const Lanes& w, const CoarseCycle<T>& c, const ResPlan& plan, int js, unsigned char* sm) {
+    const int K = c.K, nu = c.nu, nl = K - js;
+    auto P_ = [&](uint32_t off) { return reinterpret_cast<T*>(sm + off); };
+    auto rowsum = [&](const SoloLevel& S, int32_t i, bool valid, const T* x) {
+        const int64_t* rp = reinterpret_cast<const int64_t*>(sm + S.o_rp);
+        const int32_t* col = reinterpret_cast<const int32_t*>(sm + S.o_col);
+        const T* val = reinterpret_cast<const T*>(sm + S.o_val);
+        const int64_t a = valid ? rp[i] : 0, e = valid ? rp[i + 1] : 0;
+        const int maxlen = __reduce_max_sync(0xffffffffu, (int)(e - a));
+        T part = (T)0;
+        for (int off = 0; off < maxlen; off += RCHUNK) {
+            T v[RSCH], xv[RSCH];
+#pragma unroll
+            for (int q = 0; q < RSCH; ++q) {
+                const int64_t k = a + off + q * RSVL + w.sl;
+                const bool in = k < e;
+                v[q] = in ? val[k] : (T)0;
+                xv[q] = in ? x[col[k]] : (T)0;
+            }
+#pragma unroll
+            for (int q = 0; q < RSCH; ++q) part += v[q] * xv[q];
+        }
+        return (double)group_sum_t<RSVL>(part);
+    };
+    // smoother step over all rows: out = x + alpha (x - xprev) + omega D^-1 (b - A x); xprev == nullptr: 0
+    auto sweep = [&](const SoloLevel& S, const T* x, const T* xprev, double om, double al, T* out) {
+        const T* d = P_(S.o_dinv);
+        const T* b = P_(S.o_b);
+        for (int32_t base = w.warp * RRPW; base < S.n; base += RWARPS * RRPW) {
+            const int32_t i = base + w.sub;
+            const bool valid = i < S.n;
+            const double sum = rowsum(S, i, valid, x);
+            if (valid && w.sl == 0) {
+                const double xi = (double)x[i];
+                double y = xi + om * (double)d[i] * ((double)b[i] - sum);
+                if (al != 0.0) y += al * (xi - (xprev ? (double)xprev[i] : 0.0));
+                out[i] = (T)y;
+            }
+        }
+        __syncthreads();
+    };
+    {   // rhs of the first solo level
+        T* b0 = P_(plan.solo[0].o_b);
+        for (int32_t i = threadIdx.x; i < plan.solo[0].n; i += blockDim.x) b0[i] = c.L[js].b[i];
+        __syncthreads();
+    }
+    T* curs[SOLO_MAXL];
+    for (int t = 0; t + 1 < nl; ++t) {
+        const SoloLevel& S = plan.solo[t];
+        const CoarseLevel<T>& L = c.L[js + t];
+        T* X = P_(S.o_x);
+        T* Y = P_(S.o_y);
+        const T* d = P_(S.o_dinv);
+        const T* b = P_(S.o_b);
+        for (int32_t i = threadIdx.x; i < S.n; i += blockDim.x) X[i] = (T)(L.sm_omega[0] * (double)d[i] * (double)b[i]);
+        __syncthreads();
+        T* cu = X;
+        T* ot = Y;
+        for (int s = 1; s < nu; ++s) {
+            sweep(S, cu, s == 1 ? nullptr : ot, L.sm_omega[s], L.sm_alpha[s], ot);
+            T* tt = cu; cu = ot; ot = tt;
+        }
+        curs[t] = cu;
+        {   // t_i = P_i (b_i - (A x)_i)
+            const T* Pv = P_(S.o_P);
+            T* tv = P_(S.o_t);
+            for (int32_t base = w.warp * RRPW; base < S.n; base += RWARPS * RRPW) {
+                const int32_t i = base + w.sub;
+                const bool valid = i < S.n;
+                const double sum = rowsum(S, i, valid, cu);
+                if (valid && w.sl == 0) tv[i] = (T)((double)Pv[i] * ((double)b[i] - sum));
+            }
+            __syncthreads();
+        }
+        {   // b_next[a] = sum over the members of a (ascending) of t
+            const SoloLevel& N = plan.solo[t + 1];
+            const int64_t* mp = reinterpret_cast<const int64_t*>(sm + S.o_mp);
+            const int32_t* ml = reinterpret_cast<const int32_t*>(sm + S.o_ml);
+            const T* tv = P_(S.o_t);
+            T* bn = P_(N.o_b);
+            for (int32_t base = w.warp * RRPW; base < N.n; base += RWARPS * RRPW) {
+                const int32_t a = base + w.sub;
+                double sum = 0.0;
+                if (a < N.n)
+                    for (int64_t e = mp[a] + w.sl; e < mp[a + 1]; e += RSVL) sum += (double)tv[ml[e]];
+                sum = group_sum<RSVL>(sum);
+                if (a < N.n && w.sl == 0) bn[a] = (T)sum;
+            }
+            __syncthreads();
+        }
+    }
+    {   // coarsest: z = A_c^-1 b (fp64 rows)
+        const SoloLevel& C = plan.solo[nl - 1];
+        const double* Ai = reinterpret_cast<const double*>(sm + C.o_val);
+        const T* bc = P_(C.o_b);
+        T* zc = P_(C.o_z);
+        for (int32_t i = w.warp; i < C.n; i += RWARPS) {
+            double s = 0.0;
+            for (int32_t j = w.lane; j < C.n; j += 32) s += Ai[(int64_t)i * C.n + j] * (double)bc[j];
+            s = group_sum<32>(s);
+            if (w.lane == 0) zc[i] = (T)s;
+        }
+        __syncthreads();
+    }
+    for (int t = nl - 2; t >= 0; --t) {
+        const SoloLevel& S = plan.solo[t];
+        const CoarseLevel<T>& L = c.L[js + t];
+        T* cu = curs[t];
+        T* ot = cu == P_(S.o_x) ? P_(S.o_y) : P_(S.o_x);
+        const T* zc = P_(plan.solo[t + 1].o_z);
+        const T* Pv = P_(S.o_P);
+        const int32_t* agg = reinterpret_cast<const int32_t*>(sm + S.o_agg);
+        for (int32_t i = threadIdx.x; i < S.n; i += blockDim.x)
+            ot[i] = (T)((double)cu[i] + (double)Pv[i] * (double)zc[agg[i]]);
+        __syncthreads();
+        T* in = ot;
+        T* out = cu;
+        for (int s = 0; s < nu; ++s) {
+            const bool last = s == nu - 1;
+            T* dst = last ? (t == 0 ? c.L[js].z : P_(S.o_z)) : out;
+            sweep(S, in, s == 0 ? nullptr : out, L.sm_omega[s], s == 0 ? 0.0 : L.sm_alpha[s], dst);
+            if (!last) { T* tt = in; in = out; out = tt; }
+        }
+    }
+}
+
 template <class T>
 __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_constant__ CoarseCycle<T> c,
                                                              const __grid_constant__ ResPlan plan, int mode,
@@ -177,7 +307,9 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
     const int K = sc.K, nu = sc.nu;
     auto slice = [&](int k) { return Slice<T>{smem, slv[k]}; };
     T* cur[16];
-    const int kdown = mode == 0 ? K - 1 : kstop;
+    const bool solo_on = mode == 0 && plan.solo[0].n > 0;   // cycle levels solo..K-1 on CTA 0 alone
+    const int solo = solo_on ? plan.solo_first : 0;
+    const int kdown = mode == 0 ? (solo_on ? solo : K - 1) : kstop;
     // ---- down
     for (int k = 0; k < kdown && mode != 2; ++k) {
         const CoarseLevel<T>& L = sc.L[k];
@@ -211,14 +343,18 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
         grid.sync(); mark();
     }
     if (mode == 1) return;
+    if (solo_on) {  // the smallest levels on CTA 0, whole in its shared memory, __syncthreads between phases
+        if (blockIdx.x == 0) solo_cycle<T>(w, sc, plan, solo, smem);
+        grid.sync(); mark();
+    }
     if (mode == 3) {  // the tail levels on the first cluster while the other CTAs wait at the grid barrier
         if (blockIdx.x < (unsigned)ta.CT) tail_detail::coarse_tail_body<T>(ta, smem + tail_base, tail_lv, tail_bar, tail_pbars);
         grid.sync(); mark();
     }
     // ---- coarsest
-    if (mode == 0) dense_solve(w, sc.L[K - 1].n, slice(K - 1), sc.L[K - 1].b, sc.L[K - 1].z);
+    if (mode == 0 && !solo_on) dense_solve(w, sc.L[K - 1].n, slice(K - 1), sc.L[K - 1].b, sc.L[K - 1].z);
     // ---- up
-    for (int k = mode == 0 ? K - 2 : kstop - 1; k >= 0; --k) {
+    for (int k = mode == 0 ? (solo_on ? solo - 1 : K - 2) : kstop - 1; k >= 0; --k) {
         const CoarseLevel<T>& L = sc.L[k];
         const Slice<T> S = slice(k);
         // the buffer the down phase left the pre-smoothed x in (mode 2: recomputed from nu)
@@ -258,7 +394,7 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
 template <class T>
 bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vector<ResLevel>& lv,
                      std::vector<ResCopy>& copies, std::vector<int32_t>& ncopies, std::vector<uint32_t>& tx,
-                     uint32_t& smem, cudaStream_t s, bool with_coarsest) {
+                     uint32_t& smem, cudaStream_t s, bool with_coarsest, ResPlan* solo_out) {
     const int K = c.K;
     if (K < 2 || K > 16) return false;
     std::vector<std::vector<int32_t>> rb(K), ab(K);
@@ -330,6 +466,58 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
                 ok = ok && add(d.o_val, c.Ainv, (int64_t)d.r0 * L.n, 8, (size_t)rows * L.n);
             }
             if (!ok) return false;
+        }
+        if (g == 0 && solo_out && with_coarsest) {   // the solo tail in CTA 0 (coarse_res.cuh)
+            const size_t ts = sizeof(T);
+            auto level_bytes = [&](int k) -> size_t {
+                const CoarseLevel<T>& L = c.L[k];
+                if (k + 1 == K) return (size_t)L.n * L.n * 8 + 2 * (size_t)L.n * ts + 64;
+                const size_t nnz = (size_t)rp[k][L.n];
+                return ((size_t)L.n + 1) * 8 + nnz * (4 + ts) + (size_t)L.n * (2 * ts + 8) + ((size_t)L.n_agg + 1) * 8 +
+                       5 * (size_t)L.n * ts + 16 * 16;
+            };
+            int js = K;
+            size_t tot = 0;
+            for (int k = K - 1; k >= 0; --k) {
+                if (k + 1 < K && c.L[k].n > 8192) break;
+                if (cursor + tot + level_bytes(k) > smem_cap || K - k > SOLO_MAXL) break;
+                tot += level_bytes(k);
+                js = k;
+            }
+            solo_out->solo_first = 0;
+            if (js <= K - 2) {
+                uint32_t save_cursor = cursor;
+                int save_nc = nc;
+                uint32_t save_tx = tx[g];
+                bool ok = true;
+                for (int k = js; k < K && ok; ++k) {
+                    const CoarseLevel<T>& L = c.L[k];
+                    SoloLevel& d = solo_out->solo[k - js];
+                    d = SoloLevel();
+                    d.n = L.n;
+                    auto vec = [&](uint32_t& off) { off = (cursor + 15u) & ~15u; cursor = off + (uint32_t)((size_t)L.n * ts); };
+                    if (k + 1 < K) {
+                        const int64_t nnz = rp[k][L.n];
+                        ok = ok && add(d.o_rp, L.rowptr, 0, 8, (size_t)L.n + 1);
+                        ok = ok && add(d.o_col, L.col, 0, 4, (size_t)nnz);
+                        ok = ok && add(d.o_val, L.val, 0, ts, (size_t)nnz);
+                        ok = ok && add(d.o_dinv, L.dinv, 0, ts, (size_t)L.n);
+                        ok = ok && add(d.o_P, L.P, 0, ts, (size_t)L.n);
+                        ok = ok && add(d.o_agg, L.agg, 0, 4, (size_t)L.n);
+                        ok = ok && add(d.o_mp, L.mptr, 0, 8, (size_t)L.n_agg + 1);
+                        ok = ok && add(d.o_ml, L.mlist, 0, 4, (size_t)L.n);
+                        vec(d.o_x); vec(d.o_y); vec(d.o_t);
+                    } else {
+                        ok = ok && add(d.o_val, c.Ainv, 0, 8, (size_t)L.n * L.n);
+                    }
+                    vec(d.o_b); vec(d.o_z);
+                }
+                if (ok && cursor <= smem_cap) {
+                    solo_out->solo_first = js;
+                } else {
+                    cursor = save_cursor; nc = save_nc; tx[g] = save_tx;
+                }
+            }
         }
         ncopies[g] = nc;
         smem = std::max(smem, cursor);
@@ -405,7 +593,7 @@ int coarse_res_blocks_per_sm(uint32_t smem) {
 #define MG_INST(T)                                                                                             \
     template bool coarse_res_plan<T>(const CoarseCycle<T>&, int, uint32_t, std::vector<ResLevel>&,             \
                                      std::vector<ResCopy>&, std::vector<int32_t>&, std::vector<uint32_t>&,     \
-                                     uint32_t&, cudaStream_t, bool);                                           \
+                                     uint32_t&, cudaStream_t, bool, ResPlan*);                                 \
     template void coarse_vcycle_res<T>(const CoarseCycle<T>&, const ResPlan&, cudaStream_t, int, int,         \
                                        const TailArgs<T>*, uint32_t, uint32_t);                                \
     template int coarse_res_fused_grid<T>(int, uint32_t);                                                      \

@@ -28,7 +28,18 @@ struct ResCopy {
     uint32_t bytes;      // multiple of 16
 };
 
-constexpr int RES_MAXC = 64;  // bulk copies per CTA
+constexpr int RES_MAXC = 128;  // bulk copies per CTA
+
+// "Solo" tail: the smallest levels (cycle levels solo_first..K-1, the coarsest inverse included) held whole in
+// CTA 0's shared memory and cycled by that CTA alone with __syncthreads between phases while the other CTAs
+// wait at one grid barrier — no grid barrier per phase.  Offsets are CTA-0 shared-memory byte offsets of
+// element 0 of each whole-level array.
+struct SoloLevel {
+    int32_t n = 0;
+    uint32_t o_rp = 0, o_col = 0, o_val = 0, o_dinv = 0, o_P = 0, o_agg = 0, o_mp = 0, o_ml = 0;
+    uint32_t o_b = 0, o_x = 0, o_y = 0, o_t = 0, o_z = 0;   // vectors (not copied)
+};
+constexpr int SOLO_MAXL = 8;
 
 struct ResPlan {
     int G = 0;                       // CTAs (one per SM)
@@ -37,16 +48,20 @@ struct ResPlan {
     const ResCopy* copies = nullptr; // [G][RES_MAXC]
     const int32_t* ncopies = nullptr;
     const uint32_t* txbytes = nullptr;
+    int solo_first = 0;              // > 0: cycle levels solo_first..K-1 run on CTA 0 alone (mode 0)
+    SoloLevel solo[SOLO_MAXL];
 };
 
 // Host: build the plan for cycle `c` (host copies of each level's rowptr / mptr are downloaded).
 // Returns false if some CTA's slices exceed `smem_cap` bytes (then the global kernel is used).
 // with_coarsest = false: the last level of `c` gets no slices (the cycle is split around the cluster tail,
 // coarse_tail.cuh, whose first level is c's last).
+// solo = true: also plan the solo tail (the longest suffix of levels, at least one above the coarsest, whose
+// whole data fits CTA 0 next to its slices); plan.solo_first / plan.solo are filled through *solo_out.
 template <class T>
 bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vector<ResLevel>& lv,
                      std::vector<ResCopy>& copies, std::vector<int32_t>& ncopies, std::vector<uint32_t>& tx,
-                     uint32_t& smem, cudaStream_t s, bool with_coarsest = true);
+                     uint32_t& smem, cudaStream_t s, bool with_coarsest = true, ResPlan* solo_out = nullptr);
 
 // mode 0: the whole cycle; 1: down phase of levels 0..kstop-1 (leaves b of level kstop); 2: up phase from
 // level kstop-1 (reads z of level kstop); 3: 1 + the cluster tail (coarse_tail.cuh) on the launch's first

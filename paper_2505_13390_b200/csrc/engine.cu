@@ -839,8 +839,17 @@ class Engine : public EngineBase {
                 // global-kernel fallback
                 const uint32_t cap = std::getenv("MGPBD_RES_CAP") ? (uint32_t)std::atol(std::getenv("MGPBD_RES_CAP"))
                                                                     : 220u * 1024u;
-                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st) &&
+                ResPlan solo_plan;
+                // solo tail: correct but issue-bound on one SM (~2.5 us per phase for a 548-row level, measured):
+                // opt-in with MGPBD_SOLO=1
+                const bool want_solo = std::getenv("MGPBD_SOLO") != nullptr;
+                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st, true, want_solo ? &solo_plan : nullptr) &&
                     coarse_res_blocks_per_sm<T>(smem) >= 1) {  // else the global coarse kernel
+                    res_plan = ResPlan();
+                    if (want_solo && solo_plan.solo_first <= ccyc.K - 2 && solo_plan.solo[0].n > 0) {
+                        res_plan.solo_first = solo_plan.solo_first;
+                        for (int q = 0; q < SOLO_MAXL; ++q) res_plan.solo[q] = solo_plan.solo[q];
+                    }
                     res_lv.resize(lv.size()); h2d(res_lv.p, lv.data(), lv.size(), st);
                     res_cp.resize(cp.size()); h2d(res_cp.p, cp.data(), cp.size(), st);
                     res_nc.resize(nc.size()); h2d(res_nc.p, nc.data(), nc.size(), st);
@@ -856,10 +865,13 @@ class Engine : public EngineBase {
             }
         }
         tail_ok = false;
-        if (ccyc_ok && res_ok && use_tail) setup_tail();
+        fused_ok = false;
+        const bool solo_ok = res_ok && res_plan.solo[0].n > 0;
+        if (ccyc_ok && res_ok && use_tail && !solo_ok) setup_tail();
         if (tracing)
-            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, tail %s\n", nL,
+            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, solo from %d, tail %s\n", nL,
                          !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u,
+                         solo_ok ? res_plan.solo_first : -1,
                          tail_ok ? (std::string(fused_ok ? "fused, " : "split, ") + "from cycle level " +
                                     std::to_string(fused_ok ? tail_f.first : tail.first) + " on " +
                                     std::to_string(fused_ok ? tail_f.CT : tail.CT) + " CTAs, " +

@@ -14,7 +14,7 @@ MF_SWITCHES = ["", "MGPBD_NO_GRAPH=1", "MGPBD_NO_TMA=1", "MGPBD_NO_RES_COARSE=1"
                "MGPBD_COARSE_FROM=2", "MGPBD_NO_GJ_COOP=1", "MGPBD_NO_VA_SETUP=1", "MGPBD_NO_POWER_COOP=1",
                "MGPBD_NO_TAIL=1", "MGPBD_NO_VJ16=1", "MGPBD_NO_V16=1", "MGPBD_VG_TMA=1", "MGPBD_MF_GRID_CAP=2",
                "MGPBD_RES_CAP=4096", "MGPBD_FUSE_J0=1", "MGPBD_NO_FUSED_TAIL=1",
-               "MGPBD_TAIL_SCALAR_BCAST=1"]
+               "MGPBD_TAIL_SCALAR_BCAST=1", "MGPBD_SOLO=1", "MGPBD_SOLO=1 MGPBD_NO_TAIL=1"]
 CSR_SWITCHES = ["", "MGPBD_NO_BAND=1", "MGPBD_NO_ROWS=1", "MGPBD_NO_BAND=1 MGPBD_NO_ROWS=1"]
 ITERS = 3
 
@@ -60,7 +60,8 @@ def test_csr_switch(monkeypatch, ref, switch):
     assert rel(lg, lo) <= 1e-6 and rel(xg - sc.pos, xo - sc.pos) <= 1e-6, switch
 
 
-@pytest.mark.parametrize("switch", ["", "MGPBD_NO_TAIL=1", "MGPBD_NO_FUSED_TAIL=1", "MGPBD_TAIL_SCALAR_BCAST=1",
+@pytest.mark.parametrize("switch", ["", "MGPBD_SOLO=1", "MGPBD_NO_TAIL=1", "MGPBD_NO_FUSED_TAIL=1",
+                                    "MGPBD_TAIL_SCALAR_BCAST=1",
                                     "MGPBD_NO_VJ16=1 MGPBD_NO_V16=1"])
 def test_fp32_switch(monkeypatch, ref, switch):
     sc, sim = ref

@@ -11,7 +11,8 @@ name = sys.argv[1] if len(sys.argv) > 1 else "block1.67M"
 sc = scenes.make(name)
 b = np.random.default_rng(7).normal(size=sc.n_cons)
 resetup = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # frames stepped before (B-type hierarchy: 2)
-VARIANTS = {"fused": {}, "split": {"MGPBD_NO_FUSED_TAIL": "1"}, "none": {"MGPBD_NO_TAIL": "1"}}
+VARIANTS = {"solo": {"MGPBD_SOLO": "1"}, "fused": {}, "split": {"MGPBD_NO_FUSED_TAIL": "1"},
+            "none": {"MGPBD_NO_TAIL": "1"}}
 state = None
 if resetup:  # a later state (B-type hierarchy), identical for every variant: stepped once by an fp64 context
     os.environ["MGPBD_NO_TAIL"] = "1"
@@ -23,7 +24,7 @@ if resetup:  # a later state (B-type hierarchy), identical for every variant: st
 for prec in (0, 1):
     out = {}
     for name_v, env in VARIANTS.items():
-        for k in ("MGPBD_NO_TAIL", "MGPBD_NO_FUSED_TAIL"):
+        for k in ("MGPBD_NO_TAIL", "MGPBD_NO_FUSED_TAIL", "MGPBD_SOLO"):
             os.environ.pop(k, None)
         os.environ.update(env)
         ctx = mgpbd.Context.from_scene(sc, precision=prec)
@@ -33,7 +34,7 @@ for prec in (0, 1):
         ctx.debug_prepare(sc.dt)
         out[name_v] = (ctx.debug_vcycle(b), ctx.debug_pcg(b, 5))
         ctx.close()
-    for v in ("fused", "split"):
+    for v in ("solo", "fused", "split"):
         rv = np.linalg.norm(out[v][0] - out["none"][0]) / np.linalg.norm(out["none"][0])
         rp = np.linalg.norm(out[v][1] - out["none"][1]) / np.linalg.norm(out["none"][1])
         print(f"{name} prec {prec}: {v} tail vs no tail: V-cycle {rv:.3e}, 5-step PCG {rp:.3e}", flush=True)
