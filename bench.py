@@ -136,6 +136,7 @@ def frame_errors(ctx, sim, sc):
 
 def config_dict(sc, args, world, extra=None):
     d = {"workload": sc.name, "n_cons": sc.n_cons, "n_verts": sc.n_verts, "n_iters": sc.n_iters,
+         "k_nullspace": args.k_nullspace,
          "pcg_iters": sc.pcg_iters, "setup_interval": 20, "precision": args.precision,
          "accumulation": "fp64", "l2": "inputs larger than L2 (level-0 matrix streamed from HBM every pass)",
          "parallelism": (f"level-0 rows partitioned over {world} GPUs (NCCL halos + allreduce), coarse "
@@ -219,7 +220,7 @@ def run_ours(args):
     elif args.partitioned:
         part = dict(rank=0, world=1, nccl_id=mgpbd.nccl_unique_id())   # partitioned path, 1-rank NCCL
     ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=0,
-                                   level0_operator=args.level0_operator, **part)
+                                   level0_operator=args.level0_operator, k_nullspace=args.k_nullspace, **part)
     for _ in range(args.warmup):
         ctx.step(sc.dt, sc.n_iters)
     st0 = ctx.stats()
@@ -362,7 +363,7 @@ def run_ours(args):
         # and the GPU's error on that same frame (a fresh context in the bench configuration)
         ms_o, per_iter, setup, sim = oracle_at_config(sc, args.cpu_iters)
         ctx0 = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream,
-                                        level0_operator=args.level0_operator)
+                                        level0_operator=args.level0_operator, k_nullspace=args.k_nullspace)
         ctx0.step(sc.dt, args.cpu_iters)
         err = frame_errors(ctx0, sim, sc)
         ctx0.close()
@@ -395,6 +396,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-iters", type=int, default=1,
                     help="outer iterations of the oracle's frame-0 sample at the full configuration")
+    ap.add_argument("--k-nullspace", type=int, default=1,
+                    help="near-kernel vectors per aggregate (SURVEY.md §8(f) f2; 1 = the paper's hierarchies, reading c1)")
     ap.add_argument("--level0-operator", type=int, default=1, choices=[0, 1],
                     help="1: matrix-free level 0 (default), 0: assembled-CSR level-0 passes")
     ap.add_argument("--partitioned", action="store_true",

@@ -124,6 +124,13 @@ typedef struct {
                                  c13 extension); 0: the literal lazy schedule of PAPER.md:215
                                  (setup only every setup_interval frames).  With lambda_safety = 1 this is
                                  the paper's literal mode */
+    int32_t omega_refresh_iters; /* 0 (default): the smoother weights are fixed at setup (lazy).
+                                 > 0: at ite 0 of every frame WITHOUT a setup, this many further power
+                                 iterations per level on the current fp64 level matrices, started from the
+                                 iterate the previous setup / refresh left, re-derive lambda_max and the
+                                 smoother coefficients (reading c26).
+                                 Costs the fp64 Galerkin refresh + the iterations + one graph re-capture
+                                 per frame */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16

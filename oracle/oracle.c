@@ -25,7 +25,7 @@ void orc_config_default(orc_config* c) {
     c->lambda_min_est = 0.1; c->lambda_safety = 1.1; c->smoother_sweeps = 2; c->pcg_iters = 10; c->omega_relax = 0.1;
     c->smoother = 0; c->cheb_lower = 0.25;
     c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0; c->pcg_tol = 0.0;
-    c->resetup_on_indef = 1; c->residual_abs = 0.0; c->k_nullspace = 1;
+    c->resetup_on_indef = 1; c->residual_abs = 0.0; c->k_nullspace = 1; c->omega_refresh_iters = 0;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -751,14 +751,10 @@ int64_t orc_galerkin_p(int32_t n, const int64_t* rowptr, const int32_t* col, con
 
 /* lambda_max(D^-1 A) by the power method (reading c9): v_0 = U(stream 4, l)/||.||;
  * `iters` times: w = D^-1 A v; lambda = ||w||_2; v = w / lambda. */
-double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
-                 int32_t iters, uint64_t seed, int level) {
-    double* v = xmalloc(sizeof(double) * (size_t)n);
+/* `iters` power iterations from the normalised vector v (updated in place: the last normalised iterate). */
+double orc_power_from(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, int32_t iters,
+                      double* v) {
     double* w = xmalloc(sizeof(double) * (size_t)n);
-    double nn = 0.0;
-    for (int32_t i = 0; i < n; ++i) { v[i] = orc_uniform(seed, 4, level, (uint64_t)i); nn += v[i] * v[i]; }
-    nn = sqrt(nn);
-    for (int32_t i = 0; i < n; ++i) v[i] /= nn;
     double lam = 0.0;
     for (int32_t it = 0; it < iters; ++it) {
         orc_spmv(n, rowptr, col, val, v, w);
@@ -768,7 +764,23 @@ double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const dou
         if (lam == 0.0) break;
         for (int32_t i = 0; i < n; ++i) v[i] = w[i] / lam;
     }
-    free(v); free(w);
+    free(w);
+    return lam;
+}
+
+static void power_start(int32_t n, uint64_t seed, int level, double* v) {
+    double nn = 0.0;
+    for (int32_t i = 0; i < n; ++i) { v[i] = orc_uniform(seed, 4, level, (uint64_t)i); nn += v[i] * v[i]; }
+    nn = sqrt(nn);
+    for (int32_t i = 0; i < n; ++i) v[i] /= nn;
+}
+
+double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
+                 int32_t iters, uint64_t seed, int level) {
+    double* v = xmalloc(sizeof(double) * (size_t)n);
+    power_start(n, seed, level, v);
+    const double lam = orc_power_from(n, rowptr, col, val, iters, v);
+    free(v);
     return lam;
 }
 
@@ -814,6 +826,7 @@ typedef struct {
     int32_t* gs_order;              /* multicolour GS: nodes sorted by (colour, index) (reading c22) */
     /* k > 1 (f2): general CSR prolongator n x n_next (row i: r_agg(i) entries), coarse offsets */
     int64_t* pptr; int32_t* pcol; double* pval; int32_t* coff;
+    double* pw_v;                   /* last normalised power iterate of D^-1 A (omega refresh start) */
 } orc_level;
 
 struct orc_hier {
@@ -828,7 +841,7 @@ struct orc_hier {
 
 static void level_free(orc_level* v) {
     free(v->rowptr); free(v->col); free(v->val); free(v->agg); free(v->P); free(v->gs_order);
-    free(v->pptr); free(v->pcol); free(v->pval); free(v->coff);
+    free(v->pptr); free(v->pcol); free(v->pval); free(v->coff); free(v->pw_v);
     memset(v, 0, sizeof *v);
 }
 
@@ -918,7 +931,9 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
             c->val = xmalloc(sizeof(double) * (size_t)c->nnz);
             orc_galerkin_p(a->n, a->rowptr, a->col, a->val, a->pptr, a->pcol, a->pval, nc, c->rowptr, c->col, c->val);
         }
-        double lam = orc_power(a->n, a->rowptr, a->col, a->val, cfg->power_iters, cfg->seed, l);
+        a->pw_v = xmalloc(sizeof(double) * (size_t)a->n);
+        power_start(a->n, cfg->seed, l, a->pw_v);
+        double lam = orc_power_from(a->n, a->rowptr, a->col, a->val, cfg->power_iters, a->pw_v);
         a->omega = 2.0 / (cfg->lambda_safety * lam + cfg->lambda_min_est);
         if (cfg->smoother == 2) {  /* multicolour GS order of this level (reading c22) */
             int32_t* colour = xmalloc(sizeof(int32_t) * (size_t)a->n);
@@ -940,6 +955,25 @@ orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, c
     free(B);
     factor_coarsest(h);
     return h;
+}
+
+/* Smoother parameters of every level from `iters` further power iterations on the CURRENT level matrices,
+ * started from the last normalised iterate (reading c26: the optional per-frame omega refresh).  Same formulas
+ * as orc_hier_build. */
+static void set_smoother_params(orc_level* a, const orc_config* cfg, double lam) {
+    a->omega = 2.0 / (cfg->lambda_safety * lam + cfg->lambda_min_est);
+    const double hi = cfg->lambda_safety * lam, lo = cfg->cheb_lower * hi;
+    a->cheb_theta = 0.5 * (hi + lo);
+    a->cheb_delta = 0.5 * (hi - lo);
+}
+void orc_hier_refresh_omega(orc_hier* h, int32_t iters) {
+    if (iters <= 0) return;
+    for (int l = 0; l + 1 < h->L; ++l) {
+        orc_level* a = &h->lv[l];
+        if (!a->pw_v) continue;
+        const double lam = orc_power_from(a->n, a->rowptr, a->col, a->val, iters, a->pw_v);
+        set_smoother_params(a, &h->cfg, lam);
+    }
 }
 
 /* Solving phase: recompute A_{l+1} = P_l^T A_l P_l with the cached P (values of the
@@ -1234,7 +1268,10 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
             s->n_setups++;
             s->setup_ms = wall_ms() - t0;
             if (factor_coarsest(s->h) != 0) rc = -5;
-        } else if (orc_hier_refresh(s->h, s->val) != 0) rc = -5;
+        } else {
+            if (orc_hier_refresh(s->h, s->val) != 0) rc = -5;
+            if (ite == 0 && s->cfg.omega_refresh_iters > 0) orc_hier_refresh_omega(s->h, s->cfg.omega_refresh_iters);
+        }
         s->n_indef += orc_pcg(s->h, s->b, s->cfg.pcg_iters, s->dl, NULL);                         /* l.8 */
         orc_apply_dx(m, s->kind, s->verts, n, s->w, s->g, s->dl, s->dx);                         /* l.9 */
         for (int32_t j = 0; j < m; ++j) s->lambda[j] += s->dl[j];                               /* l.10 */

@@ -43,6 +43,9 @@ typedef struct {
                                 re-runs at ite 0 of the next frame (reading c13 extension); 0: the literal
                                 schedule of PAPER.md:215 (setup only every setup_interval frames).  Default 1 */
     double residual_abs;     /* Alg. 1 l.12 absolute eps ("||b|| < 1e-4"): break once ||b|| < it; 0 = off */
+    int32_t omega_refresh_iters; /* > 0: at ite 0 of frames without a setup, omega_l / the Chebyshev interval are
+                                    re-estimated by this many power iterations on the current level matrices from
+                                    the last normalised iterate (reading c26); 0 = omega only at setup */
     int32_t k_nullspace;     /* near-kernel vectors per aggregate ("six distinct B"; reading c1):
                                 1 (default) or up to 6 */
 } orc_config;
@@ -103,6 +106,8 @@ int32_t orc_prolongator_qr(int32_t n, const int32_t* agg, int32_t n_agg, int32_t
 int64_t orc_galerkin_p(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
                        const int64_t* pptr, const int32_t* pcol, const double* pval, int32_t nc,
                        int64_t* crowptr, int32_t* ccol, double* cval);
+double orc_power_from(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val, int32_t iters,
+                      double* v /* normalised start, in/out */);
 double orc_power(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
                  int32_t iters, uint64_t seed, int level);
 int orc_cholesky(int32_t n, const double* A /* dense n*n */, double* L /* n*n */);
@@ -113,6 +118,7 @@ typedef struct orc_hier orc_hier;
 orc_hier* orc_hier_build(int32_t n, const int64_t* rowptr, const int32_t* col, const double* val,
                          const orc_config* cfg);
 int orc_hier_refresh(orc_hier* h, const double* val0); /* new A_0 values: Galerkin + coarse factor */
+void orc_hier_refresh_omega(orc_hier* h, int32_t iters);   /* reading c26: per-frame omega refresh */
 void orc_hier_free(orc_hier* h);
 int orc_hier_levels(const orc_hier* h);
 void orc_hier_level_size(const orc_hier* h, int l, int32_t* n, int64_t* nnz);

@@ -32,7 +32,8 @@ class Config(C.Structure):
                 ("gravity", C.c_double * 3), ("seed", C.c_uint64), ("smoother", C.c_int32),
                 ("cheb_lower", C.c_double), ("backtrack", C.c_int32), ("omega_min", C.c_double),
                 ("residual_tol", C.c_double), ("pcg_tol", C.c_double), ("resetup_on_indef", C.c_int32),
-                ("residual_abs", C.c_double), ("k_nullspace", C.c_int32)]
+                ("residual_abs", C.c_double), ("omega_refresh_iters", C.c_int32),
+                ("k_nullspace", C.c_int32)]
 
 
 _lib = None
@@ -68,6 +69,8 @@ def lib():
             "orc_prolongator": (None, [i32, P, i32, P, P, P]),
             "orc_galerkin": (i64, [i32, P, P, P, P, P, i32, P, P, P]),
             "orc_power": (f64, [i32, P, P, P, i32, u64, C.c_int]),
+            "orc_power_from": (f64, [i32, P, P, P, i32, P]),
+            "orc_hier_refresh_omega": (None, [P, i32]),
             "orc_gs_bootstrap_k": (None, [i32, P, P, P, P, i32, u64, i32, P]),
             "orc_prolongator_qr": (i32, [i32, P, i32, i32, P, f64, P, P, P, P, P, i32]),
             "orc_galerkin_p": (i64, [i32, P, P, P, P, P, P, i32, P, P, P]),
@@ -433,6 +436,10 @@ class Hierarchy:
     @property
     def n_colours(self) -> int:
         return int(lib().orc_hier_n_colours(self.h))
+
+    def refresh_omega(self, iters):
+        """Reading c26: omega / Chebyshev parameters from `iters` further power iterations on the current levels."""
+        lib().orc_hier_refresh_omega(self.h, int(iters))
 
     def refresh(self, val0) -> int:
         v = _c(val0, np.float64)

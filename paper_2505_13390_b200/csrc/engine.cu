@@ -98,6 +98,7 @@ class Engine : public EngineBase {
         DBuf<T> kQs, kpval, kW, kones;
         DBuf<double> kW64;
         DBuf<int64_t> arow, xoff;   // aggregate-level coarse pattern (rows), block offsets per entry
+        DBuf<double> pwv;           // last normalised power iterate (start of the omega refresh, c26)
         DBuf<int32_t> acol, erow;
         void configure(cudaStream_t s) {
             const int32_t nl = own_n();
@@ -214,6 +215,8 @@ class Engine : public EngineBase {
     bool mf_ready = false;      // h is current and describes level 0 (false after debug_setup_from)
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
+    int64_t omega_refreshes = 0;
+    bool va_setup0 = false;  // the last setup formed level 1 through the VA plan (fp64 omega refresh follows it)
     bool va_off = std::getenv("MGPBD_NO_VA_SETUP") != nullptr;  // CSR Galerkin at setup (comparison)
     double last_dt = 0.0;
     DBuf<double> omega_dev;     // relaxation omega of Alg. 1 l.11 (device scalar: backtracking, c21)
@@ -606,6 +609,140 @@ class Engine : public EngineBase {
         }
     }
 
+    void keep_power_iterate(Level& a) {
+        a.pwv.resize(a.n);
+        d2d(a.pwv.p, pw_v.p, a.n, st);
+    }
+
+    // Reading c26 (cfg.omega_refresh_iters > 0): at ite 0 of a frame without a setup,
+    // lambda_max(D^-1 A_l) of every smoothed level is re-estimated on the CURRENT matrices with
+    // omega_refresh_iters further power iterations started from the iterate the setup (or the previous
+    // refresh) left, and the smoother coefficients and coarse-kernel tables follow.  The level matrices are
+    // the fp64 ones the setup uses (A_0 from assemble_setup, the coarse levels by the fp64 Galerkin product
+    // over the setup's aggregates / P), so the estimate matches the oracle's orc_hier_refresh_omega.
+    void omega_refresh(double dt) {
+        const int32_t iters = cfg.omega_refresh_iters;
+        assemble_setup(dt);
+        const bool mf0 = mf64_ok && mf_ready && h64.n;
+        if (va_setup0) {
+            at64.resize(m);
+            va_at(m, alpha.p, last_dt, at64.p, st);
+        }
+        for (int l = 0; l + 1 < nL; ++l) {  // fp64 Galerkin values of levels 1..nL-1 (Eq. 6)
+            Level& a = *L[l];
+            Level& c = *L[l + 1];
+            if (a.kk > 1)
+                kgal_numeric<double>(a.plan, a.rowptr, a.col, a.val64.p, a.kk, a.kp.pptr.p, a.kp.pval64.p, a.kp.coff.p,
+                                     a.agg.p, a.n_agg, a.erow.p, a.acol.p, a.xoff.p, c.rowptr, c.n, a.kW64.p, c.val64.p,
+                                     c.dinv64.p, st);
+            else if (l == 0 && va_setup0)
+                va_numeric<double>(va, kc, h64.p, nullptr, a.P64.p, a.mptr.p, a.mlist.p, at64.p, a.n_agg, c.rowptr,
+                                   c.val64.p, c.dinv64.p, st);
+            else
+                galerkin_numeric<double>(a.plan, a.rowptr, a.col, a.val64.p, a.P64.p, a.n_agg, c.rowptr, c.nnz,
+                                         a.tval64.p, c.val64.p, c.dinv64.p, st);
+        }
+        for (int l = 0; l + 1 < nL; ++l) {
+            Level& a = *L[l];
+            if (!a.pwv.n) continue;
+            double lam;
+            if (l == 0 && mf0) {
+                mf64.h = h64.p;
+                mf64.dinv = a.dinv64.p;
+                mf_refresh<double>(mf64, alpha.p, last_dt, a.dinv64.p, st);
+                lam = power_method_op(
+                    m, a.grid,
+                    [&](const double* xv, double* yv, double* pp) {
+                        mf_pass<double>(PASS_POWER, mf64, xv, nullptr, yv, nullptr, 0.0, pp, nullptr, st);
+                        return mf64.grid;
+                    },
+                    iters, cfg.seed, l, a.pwv.p, pw_w.p, parts1.p, pw_ss.p, st, false);
+            } else {
+                lam = power_method(a.setup_csr(), iters, cfg.seed, l, a.pwv.p, pw_w.p, parts1.p, pw_ss.p, st, false);
+            }
+            set_smoother(a, lam);
+        }
+        plan_coarse();
+        invalidate_graphs();  // the smoother coefficients are launch arguments of the captured iteration
+        omega_refreshes++;
+    }
+
+    // The coarse-cycle kernels' tables (levels, smoother coefficients, resident / tail plans) from the current
+    // hierarchy: at setup, and after a per-frame omega refresh (reading c26).
+    void plan_coarse() {
+        ccyc_ok = false;
+        if (use_coarse_kernel && cfg.smoother != 2 && kk == 1 && ccyc_from >= 1 && nL >= ccyc_from + 2) {
+            ccyc = CoarseCycle<T>();
+            ccyc.K = nL - ccyc_from;
+            ccyc.nu = cfg.smoother_sweeps;
+            ccyc.Ainv = Ainv.p;
+            if (std::getenv("MGPBD_TRACE_COARSE")) {
+                ctrace.resize(128);  // [0, 32): grid-wide kernel (down half), [32, 64): cluster tail, [64, 96): up half
+                MG_CK(cudaMemsetAsync(ctrace.p, 0, 128 * sizeof(unsigned long long), st));
+                ccyc.trace = ctrace.p;
+            }
+            for (int l = ccyc_from; l < nL; ++l) {
+                Level& a = *L[l];
+                CoarseLevel<T>& c = ccyc.L[l - ccyc_from];
+                c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p; c.omega = a.omega;
+                for (int k = 0; k < 8; ++k) { c.sm_omega[k] = a.sm_omega[k]; c.sm_alpha[k] = a.sm_alpha[k]; }
+                if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_agg = a.n_agg; }
+                c.t = a.vt.p; c.b = a.vb.p; c.z = a.vz.p; c.x = a.vx.p; c.y = a.vy.p;
+            }
+            ccyc_ok = true;
+            res_ok = false;
+            if (use_res) {
+                int sms = 148;
+                MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
+                std::vector<ResLevel> lv;
+                std::vector<ResCopy> cp;
+                std::vector<int32_t> nc;
+                std::vector<uint32_t> tx;
+                uint32_t smem = 0;
+                // 227 KB minus the static descriptor copy; MGPBD_RES_CAP (bytes, tests) lowers it to force the
+                // global-kernel fallback
+                const uint32_t cap = std::getenv("MGPBD_RES_CAP") ? (uint32_t)std::atol(std::getenv("MGPBD_RES_CAP"))
+                                                                    : 220u * 1024u;
+                ResPlan solo_plan;
+                // solo tail: correct but issue-bound on one SM (~2.5 us per phase for a 548-row level, measured):
+                // opt-in with MGPBD_SOLO=1 (DESIGN.md §6.3)
+                const bool want_solo = std::getenv("MGPBD_SOLO") != nullptr;
+                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st, true, want_solo ? &solo_plan : nullptr) &&
+                    coarse_res_blocks_per_sm<T>(smem) >= 1) {  // else the global coarse kernel
+                    res_plan = ResPlan();
+                    if (want_solo && solo_plan.solo_first <= ccyc.K - 2 && solo_plan.solo[0].n > 0) {
+                        res_plan.solo_first = solo_plan.solo_first;
+                        for (int q = 0; q < SOLO_MAXL; ++q) res_plan.solo[q] = solo_plan.solo[q];
+                    }
+                    res_lv.resize(lv.size()); h2d(res_lv.p, lv.data(), lv.size(), st);
+                    res_cp.resize(cp.size()); h2d(res_cp.p, cp.data(), cp.size(), st);
+                    res_nc.resize(nc.size()); h2d(res_nc.p, nc.data(), nc.size(), st);
+                    res_tx.resize(tx.size()); h2d(res_tx.p, tx.data(), tx.size(), st);
+                    res_plan.G = sms;
+                    res_plan.smem = smem;
+                    res_plan.lv = res_lv.p;
+                    res_plan.copies = res_cp.p;
+                    res_plan.ncopies = res_nc.p;
+                    res_plan.txbytes = res_tx.p;
+                    res_ok = true;
+                }
+            }
+        }
+        tail_ok = false;
+        fused_ok = false;
+        const bool solo_ok = res_ok && res_plan.solo[0].n > 0;
+        if (ccyc_ok && res_ok && use_tail && !solo_ok) setup_tail();
+        if (tracing)
+            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, solo from %d, tail %s\n", nL,
+                         !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u,
+                         solo_ok ? res_plan.solo_first : -1,
+                         tail_ok ? (std::string(fused_ok ? "fused, " : "split, ") + "from cycle level " +
+                                    std::to_string(fused_ok ? tail_f.first : tail.first) + " on " +
+                                    std::to_string(fused_ok ? tail_f.CT : tail.CT) + " CTAs, " +
+                                    std::to_string(fused_ok ? tail_f.smem : tail.smem) + " B" +
+                                    (fused_ok ? ", grid " + std::to_string(res_f.G) : std::string())).c_str() : "off");
+    }
+
     // ------------------------------------------------------------------ setup (Fig. setup-pipline)
     void setup() {
         Level& l0 = *L[0];
@@ -698,6 +835,7 @@ class Engine : public EngineBase {
                 } else {
                     lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
                 }
+                keep_power_iterate(a2);
                 set_smoother(a2, lam);
                 trace("power", l);
                 B.swap(Bn);
@@ -763,6 +901,7 @@ class Engine : public EngineBase {
             } else {
                 lam = power_method(a2.setup_csr(), cfg.power_iters, cfg.seed, l, pw_v.p, pw_w.p, parts1.p, pw_ss.p, st);
             }
+            keep_power_iterate(a2);
             set_smoother(a2, lam);
             trace("power", l);
             B.swap(Bn);
@@ -798,6 +937,7 @@ class Engine : public EngineBase {
             MG_CK(cudaMemsetAsync(a.tval.p, 0, sizeof(T) * (a.plan.T ? a.plan.T : 1), st));
         }
         va_ok = va_built && nL > 1;
+        va_setup0 = va_built && nL > 1;
         if (!va_ok && cfg.level0_operator == 1 && nL > 1 && kk == 1) {
             va_symbolic(nv, kc, vptr.p, vlist.p, L[0]->agg.p, L[0]->n_agg, L[1]->rowptr, L[1]->col, L[1]->nnz, va, st,
                         mf_ppos.n ? mf_ppos.p : nullptr, mf_npad);
@@ -806,77 +946,7 @@ class Engine : public EngineBase {
         }
         Ainv.resize((size_t)cl.n * cl.n);
         inv_work.resize((size_t)cl.n * cl.n + 64 * (size_t)cl.n + 1024);
-        ccyc_ok = false;
-        if (use_coarse_kernel && cfg.smoother != 2 && kk == 1 && ccyc_from >= 1 && nL >= ccyc_from + 2) {
-            ccyc = CoarseCycle<T>();
-            ccyc.K = nL - ccyc_from;
-            ccyc.nu = cfg.smoother_sweeps;
-            ccyc.Ainv = Ainv.p;
-            if (std::getenv("MGPBD_TRACE_COARSE")) {
-                ctrace.resize(128);  // [0, 32): grid-wide kernel (down half), [32, 64): cluster tail, [64, 96): up half
-                MG_CK(cudaMemsetAsync(ctrace.p, 0, 128 * sizeof(unsigned long long), st));
-                ccyc.trace = ctrace.p;
-            }
-            for (int l = ccyc_from; l < nL; ++l) {
-                Level& a = *L[l];
-                CoarseLevel<T>& c = ccyc.L[l - ccyc_from];
-                c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p; c.omega = a.omega;
-                for (int k = 0; k < 8; ++k) { c.sm_omega[k] = a.sm_omega[k]; c.sm_alpha[k] = a.sm_alpha[k]; }
-                if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_agg = a.n_agg; }
-                c.t = a.vt.p; c.b = a.vb.p; c.z = a.vz.p; c.x = a.vx.p; c.y = a.vy.p;
-            }
-            ccyc_ok = true;
-            res_ok = false;
-            if (use_res) {
-                int sms = 148;
-                MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device));
-                std::vector<ResLevel> lv;
-                std::vector<ResCopy> cp;
-                std::vector<int32_t> nc;
-                std::vector<uint32_t> tx;
-                uint32_t smem = 0;
-                // 227 KB minus the static descriptor copy; MGPBD_RES_CAP (bytes, tests) lowers it to force the
-                // global-kernel fallback
-                const uint32_t cap = std::getenv("MGPBD_RES_CAP") ? (uint32_t)std::atol(std::getenv("MGPBD_RES_CAP"))
-                                                                    : 220u * 1024u;
-                ResPlan solo_plan;
-                // solo tail: correct but issue-bound on one SM (~2.5 us per phase for a 548-row level, measured):
-                // opt-in with MGPBD_SOLO=1 (DESIGN.md §6.3)
-                const bool want_solo = std::getenv("MGPBD_SOLO") != nullptr;
-                if (coarse_res_plan<T>(ccyc, sms, cap, lv, cp, nc, tx, smem, st, true, want_solo ? &solo_plan : nullptr) &&
-                    coarse_res_blocks_per_sm<T>(smem) >= 1) {  // else the global coarse kernel
-                    res_plan = ResPlan();
-                    if (want_solo && solo_plan.solo_first <= ccyc.K - 2 && solo_plan.solo[0].n > 0) {
-                        res_plan.solo_first = solo_plan.solo_first;
-                        for (int q = 0; q < SOLO_MAXL; ++q) res_plan.solo[q] = solo_plan.solo[q];
-                    }
-                    res_lv.resize(lv.size()); h2d(res_lv.p, lv.data(), lv.size(), st);
-                    res_cp.resize(cp.size()); h2d(res_cp.p, cp.data(), cp.size(), st);
-                    res_nc.resize(nc.size()); h2d(res_nc.p, nc.data(), nc.size(), st);
-                    res_tx.resize(tx.size()); h2d(res_tx.p, tx.data(), tx.size(), st);
-                    res_plan.G = sms;
-                    res_plan.smem = smem;
-                    res_plan.lv = res_lv.p;
-                    res_plan.copies = res_cp.p;
-                    res_plan.ncopies = res_nc.p;
-                    res_plan.txbytes = res_tx.p;
-                    res_ok = true;
-                }
-            }
-        }
-        tail_ok = false;
-        fused_ok = false;
-        const bool solo_ok = res_ok && res_plan.solo[0].n > 0;
-        if (ccyc_ok && res_ok && use_tail && !solo_ok) setup_tail();
-        if (tracing)
-            std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, solo from %d, tail %s\n", nL,
-                         !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u,
-                         solo_ok ? res_plan.solo_first : -1,
-                         tail_ok ? (std::string(fused_ok ? "fused, " : "split, ") + "from cycle level " +
-                                    std::to_string(fused_ok ? tail_f.first : tail.first) + " on " +
-                                    std::to_string(fused_ok ? tail_f.CT : tail.CT) + " CTAs, " +
-                                    std::to_string(fused_ok ? tail_f.smem : tail.smem) + " B" +
-                                    (fused_ok ? ", grid " + std::to_string(res_f.G) : std::string())).c_str() : "off");
+        plan_coarse();
         invalidate_graphs();  // buffers of the hierarchy changed
         have_hier = true;
         stale = false;
@@ -1272,6 +1342,8 @@ class Engine : public EngineBase {
                 s1 = ev();
                 MG_CK(cudaEventRecord(s1, st));
                 setup_ran = 1;
+            } else if (ite == 0 && cfg.omega_refresh_iters > 0 && have_hier && nL > 1) {  // reading c26
+                omega_refresh(dt);
             }
             if (cfg.level0_operator == 1 && nL < 2)  // single level: A_0 is the coarsest, inverted densely
                 assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, L[0]->vl, L[0]->val.p,
@@ -1538,6 +1610,8 @@ class Engine : public EngineBase {
         if (stale || !have_hier || frame % cfg.setup_interval == 0) {                               // l.7
             assemble_setup(dt);
             setup();
+        } else if (cfg.omega_refresh_iters > 0 && have_hier && nL > 1) {
+            omega_refresh(dt);  // reading c26
         }
         if (cfg.level0_operator == 1 && nL < 2)
             assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, L[0]->vl, L[0]->val.p,
@@ -1623,6 +1697,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->pcg_tol = 0.0;
     c->residual_abs = 0.0;
     c->resetup_on_indef = 1;
+    c->omega_refresh_iters = 0;
     return MGPBD_OK;
 }
 
@@ -1655,6 +1730,7 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
         return fail("bad omega_min / residual_tol / residual_abs");
     if (cfg->smoother == 1 && !(cfg->cheb_lower > 0.0 && cfg->cheb_lower < 1.0)) return fail("cheb_lower must be in (0, 1)");
     if (!(cfg->pcg_tol >= 0.0)) return fail("pcg_tol must be >= 0");
+    if (cfg->omega_refresh_iters < 0 || cfg->omega_refresh_iters > 10000) return fail("omega_refresh_iters must be in 0..10000");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > mgpbd::SC_KMAX || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
         cfg->max_dense_coarse < 1)

@@ -682,12 +682,14 @@ void diag_inv(int32_t n, const int64_t* rowptr, const T* val, T* dinv, cudaStrea
 
 double power_method_op(int32_t n, int dot_grid, const std::function<int(const double*, double*, double*)>& apply,
                        int32_t iters, uint64_t seed, int level, double* v, double* w, double* parts, double* ss,
-                       cudaStream_t s) {
-    k_power_init<<<g1(n), 256, 0, s>>>(n, hkey_base(seed, 4, level), v);
-    MG_LAUNCH_CHECK();
-    dot_parts<double>(n, v, v, parts, dot_grid, s);
-    finalize_sum(parts, dot_grid, ss, s);
-    scale_by_inv_sqrt<double>(n, v, v, ss, s);
+                       cudaStream_t s, bool init) {
+    if (init) {
+        k_power_init<<<g1(n), 256, 0, s>>>(n, hkey_base(seed, 4, level), v);
+        MG_LAUNCH_CHECK();
+        dot_parts<double>(n, v, v, parts, dot_grid, s);
+        finalize_sum(parts, dot_grid, ss, s);
+        scale_by_inv_sqrt<double>(n, v, v, ss, s);
+    }
     for (int it = 0; it < iters; ++it) {
         const int np = apply(v, w, parts);
         finalize_sum(parts, np, ss, s);
@@ -713,27 +715,29 @@ __global__ void __launch_bounds__(PWT) k_power_coop(int32_t n, const int64_t* __
                                                     const int32_t* __restrict__ col, const double* __restrict__ val,
                                                     const double* __restrict__ dinv, int32_t iters, uint64_t base,
                                                     double* __restrict__ v, double* __restrict__ w,
-                                                    double* __restrict__ parts, double* __restrict__ out) {
+                                                    double* __restrict__ parts, double* __restrict__ out, int init) {
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
     __shared__ double inv_s;
     const int lane = threadIdx.x & 31;
     const int64_t tid = (int64_t)blockIdx.x * PWT + threadIdx.x, nt = (int64_t)gridDim.x * PWT;
     const int64_t gw = tid >> 5, nw = nt >> 5;
-    double acc = 0.0;
-    for (int64_t i = tid; i < n; i += nt) {
-        const double x = hunit(hkey(base, (uint64_t)i));
-        v[i] = x;
-        acc += x * x;
+    double acc = 0.0, t = 0.0, ss = 0.0;
+    if (init) {  // v_0 = U(stream 4)/|.|
+        for (int64_t i = tid; i < n; i += nt) {
+            const double x = hunit(hkey(base, (uint64_t)i));
+            v[i] = x;
+            acc += x * x;
+        }
+        t = block_sum<PWT>(acc, sh);
+        if (threadIdx.x == 0) parts[blockIdx.x] = t;
+        grid.sync();
+        ss = pw_total(parts, gridDim.x, sh);
+        if (threadIdx.x == 0) { const double lam = sqrt(ss); inv_s = lam > 0.0 ? 1.0 / lam : 0.0; }
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += nt) v[i] = v[i] * inv_s;
+        grid.sync();
     }
-    double t = block_sum<PWT>(acc, sh);
-    if (threadIdx.x == 0) parts[blockIdx.x] = t;
-    grid.sync();
-    double ss = pw_total(parts, gridDim.x, sh);
-    if (threadIdx.x == 0) { const double lam = sqrt(ss); inv_s = lam > 0.0 ? 1.0 / lam : 0.0; }
-    __syncthreads();
-    for (int64_t i = tid; i < n; i += nt) v[i] = v[i] * inv_s;
-    grid.sync();
     for (int32_t it = 0; it < iters; ++it) {
         acc = 0.0;
         for (int64_t i = gw; i < n; i += nw) {
@@ -760,7 +764,7 @@ __global__ void __launch_bounds__(PWT) k_power_coop(int32_t n, const int64_t* __
 }  // namespace
 
 double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
-                    double* parts, double* ss, cudaStream_t s) {
+                    double* parts, double* ss, cudaStream_t s, bool init) {
     if (A.n > 0 && A.n <= (1 << 18) && std::getenv("MGPBD_NO_POWER_COOP") == nullptr) {
         static const int grid = [] {
             int dev = 0, sms = 0, occ = 0;
@@ -772,8 +776,9 @@ double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int leve
         // parts holds >= 1024 doubles (the engine's partial-sum buffer)
         const int g = (int)std::max<int64_t>(1, std::min<int64_t>(std::min(grid, 1024), ((int64_t)A.n * 32 + PWT - 1) / PWT));
         const uint64_t base = hkey_base(seed, 4, level);
+        int init_i = init ? 1 : 0;
         void* args[] = {(void*)&A.n, (void*)&A.rowptr, (void*)&A.col, (void*)&A.val, (void*)&A.dinv,
-                        (void*)&iters, (void*)&base, (void*)&v, (void*)&w, (void*)&parts, (void*)&ss};
+                        (void*)&iters, (void*)&base, (void*)&v, (void*)&w, (void*)&parts, (void*)&ss, (void*)&init_i};
         MG_CK(cudaLaunchCooperativeKernel((const void*)k_power_coop, g, PWT, args, 0, s));
         MG_LAUNCH_CHECK();
         const double lam2 = read_scalar(ss, s);
@@ -785,7 +790,7 @@ double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int leve
             csr_pass<double>(PASS_POWER, A, x, nullptr, y, nullptr, 0.0, pp, nullptr, s);
             return A.nparts;
         },
-        iters, seed, level, v, w, parts, ss, s);
+        iters, seed, level, v, w, parts, ss, s, init);
 }
 
 #define MG_INST(T)                                                                                             \

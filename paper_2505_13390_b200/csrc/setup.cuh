@@ -78,10 +78,12 @@ void diag_inv(int32_t n, const int64_t* rowptr, const T* val, T* dinv, cudaStrea
 // lambda_max(D^-1 A) by the power method (reading c9); returns lambda (host sync).
 // Same iteration with the operator given as apply(v, w, parts): w = D^-1 A v and the partials of
 // |w|^2; returns the number of partials written.  (Level 0 uses the matrix-free operator.)
+// init = false: start from the normalised vector already in v (the per-frame omega refresh, reading c26).
+// On return v holds the last normalised iterate.
 double power_method_op(int32_t n, int dot_grid, const std::function<int(const double*, double*, double*)>& apply,
                        int32_t iters, uint64_t seed, int level, double* v, double* w, double* parts, double* ss,
-                       cudaStream_t s);
+                       cudaStream_t s, bool init = true);
 double power_method(const Csr<double>& A, int32_t iters, uint64_t seed, int level, double* v, double* w,
-                    double* parts, double* ss, cudaStream_t s);
+                    double* parts, double* ss, cudaStream_t s, bool init = true);
 
 }  // namespace mgpbd

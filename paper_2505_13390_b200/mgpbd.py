@@ -52,7 +52,8 @@ class Config(C.Structure):
                 ("nccl_id", C.c_void_p), ("vgroup", C.c_void_p), ("level0_operator", C.c_int32),
                 ("smoother", C.c_int32), ("cheb_lower", C.c_double), ("backtrack", C.c_int32),
                 ("omega_min", C.c_double), ("residual_tol", C.c_double), ("pcg_tol", C.c_double),
-                ("residual_abs", C.c_double), ("resetup_on_indef", C.c_int32)]
+                ("residual_abs", C.c_double), ("resetup_on_indef", C.c_int32),
+                ("omega_refresh_iters", C.c_int32)]
 
 
 class Stats(C.Structure):

@@ -314,3 +314,57 @@ def test_hierarchy_omega_closed_form(O, safety):
     h2 = O.Hierarchy(r, cc, v, O.default_config(min_coarse=2, power_iters=20000, lambda_safety=safety,
                                                 lambda_min_est=0.5))
     assert np.isclose(h2.omega(0), 2.0 / (safety * lam + 0.5), rtol=1e-12)
+
+
+@pytest.mark.parametrize("smoother", [0, 1])
+def test_refresh_omega_closed_form(O, smoother):
+    """Reading c26 (optional per-frame omega refresh): after the level-0 values change (same pattern),
+    orc_hier_refresh_omega re-estimates lambda_max(D^-1 A_l) on the refreshed levels from the stored
+    iterate.  Level 0 is pinned to the closed form of the tridiagonal family (see the test above, c: 0.4 ->
+    0.3); level 1 to the library eigenvalues of its refreshed Galerkin matrix; 0 iterations leave omega."""
+    n = 40
+    rng = np.random.default_rng(5)
+    d = rng.uniform(0.5, 4.0, n)
+
+    def A_of(c):
+        T = np.eye(n) - c * (np.eye(n, k=1) + np.eye(n, k=-1))
+        return np.sqrt(np.outer(d, d)) * T
+
+    r, cc, v = csr_from_dense_diaglast(A_of(0.4))
+    cfg = O.default_config(min_coarse=2, power_iters=200, lambda_safety=1.1, smoother=smoother)
+    h = O.Hierarchy(r, cc, v, cfg)
+    assert h.n_levels >= 3
+    om0 = [h.omega(l) for l in range(h.n_levels - 1)]
+    r2, c2, v2 = csr_from_dense_diaglast(A_of(0.3))
+    assert np.array_equal(r2, r) and np.array_equal(c2, cc)
+    assert h.refresh(v2) == 0
+    h.refresh_omega(0)
+    assert [h.omega(l) for l in range(h.n_levels - 1)] == om0
+    h.refresh_omega(60000)
+    lam0 = 1.0 + 2.0 * 0.3 * np.cos(np.pi / (n + 1))
+    assert np.isclose(h.omega(0), 2.0 / (1.1 * lam0 + 0.1), rtol=1e-10)
+    A1 = dense(*h.level(1))
+    d1 = np.sqrt(np.diag(A1))
+    lam1 = np.linalg.eigvalsh(A1 / np.outer(d1, d1)).max()
+    assert np.isclose(h.omega(1), 2.0 / (1.1 * lam1 + 0.1), rtol=1e-10)
+    theta, delta = h.cheb(0)
+    hi = 1.1 * lam0
+    assert np.isclose(theta, 0.5 * (hi + 0.25 * hi), rtol=1e-10) and np.isclose(delta, 0.5 * (hi - 0.25 * hi), rtol=1e-10)
+
+
+def test_sim_omega_refresh_schedule(O):
+    """omega_refresh_iters > 0 re-derives omega at ite 0 of the frames without a setup only; 0 (default)
+    keeps the setup's omega until the next setup (PAPER.md:320 lazy setup)."""
+    sc = scenes.make("bar3k")
+    base = dict(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters, setup_interval=100, resetup_on_indef=0)
+    s0 = O.Sim(sc, O.default_config(**base))
+    s1 = O.Sim(sc, O.default_config(omega_refresh_iters=20, **base))
+    om = []
+    for f in range(3):
+        assert s0.step(sc.dt, 4) == 0 and s1.step(sc.dt, 4) == 0
+        h0, h1 = s0.hierarchy(), s1.hierarchy()
+        om.append(([h0.omega(l) for l in range(h0.n_levels - 1)], [h1.omega(l) for l in range(h1.n_levels - 1)]))
+    assert s0.setups() == 1 and s1.setups() == 1
+    assert om[0][0] == om[0][1]                 # frame 0: the setup, identical on both
+    assert om[1][0] == om[0][0] and om[2][0] == om[0][0]
+    assert om[1][1] != om[0][1] and om[2][1] != om[1][1]
