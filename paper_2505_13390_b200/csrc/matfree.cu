@@ -75,14 +75,25 @@ struct Chunk {
     T hx[VW], hy[VW], hz[VW];
     int32_t j[VW];
     // SM: the chunk lives in shared memory (plain loads); otherwise global, streamed (evict-first)
-    template <bool SM = false>
+    // POL: global loads carry the L2 policy `pol` (MGPBD_L2POL) instead of the streaming hint
+    template <bool SM = false, bool POL = false>
     __device__ __forceinline__ void load(const T* __restrict__ hx_, const T* __restrict__ hy_, const T* __restrict__ hz_,
                                          const uint16_t* __restrict__ j16, const int32_t* __restrict__ j32, int64_t p,
-                                         bool in) {
+                                         bool in, uint64_t pol = 0) {
         using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-        auto ld = [](const auto* q) {
-            if constexpr (SM) return *q;
-            else return __ldcs(q);
+        auto ld = [pol](const auto* q) {
+            using Q = typename std::remove_cv<typename std::remove_pointer<decltype(q)>::type>::type;
+            if constexpr (SM) {
+                return *q;
+            } else if constexpr (POL) {
+                Q r;
+                if constexpr (sizeof(Q) == 16) { const uint4 w = ldg16_pol(q, pol); memcpy(&r, &w, 16); }
+                else if constexpr (sizeof(Q) == 8) { const uint2 w = ldg8_pol(q, pol); memcpy(&r, &w, 8); }
+                else { const uint32_t w = ldg4_pol(q, pol); memcpy(&r, &w, 4); }
+                return r;
+            } else {
+                return __ldcs(q);
+            }
         };
         if (in) {
             const VT a = ld(reinterpret_cast<const VT*>(hx_ + p));
@@ -125,6 +136,13 @@ struct Chunk {
 #ifndef MGPBD_VG_PREFETCH
 #define MGPBD_VG_PREFETCH 1
 #endif
+// L2 policy of the level-0 pass's two gradient streams (hv in the vertex gather, h in the row kernel; each
+// ~80 MB fp32 on block1.67M, read 50 times per outer iteration): 0 = streaming (evict-first loads in the
+// gather, default bulk copies), 1 = gather stream evict_last + row stream evict_first, 2 = the reverse,
+// 3 = gather stream evict_last, row stream default.
+#ifndef MGPBD_L2POL
+#define MGPBD_L2POL 0
+#endif
 template <class T, int G, int UN, bool J16, bool XJ>
 __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
                                                       const int64_t* __restrict__ ppos,
@@ -145,6 +163,7 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
     const T* __restrict__ hx = hv;
     const T* __restrict__ hy = hv + npad;
     const T* __restrict__ hz = hv + 2 * npad;
+    const uint64_t pol = MGPBD_L2POL == 1 || MGPBD_L2POL == 3 ? l2_policy_last() : MGPBD_L2POL == 2 ? l2_policy_first() : 0;
     // the next vertex's slot range and index base are fetched one round ahead (one dependent round trip less
     // per vertex)
     int64_t p0n = 0, p1n = 0;
@@ -167,7 +186,7 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
 #pragma unroll
                 for (int q = 0; q < UN; ++q) {
                     const int64_t p = pb + (int64_t)q * G * VW;
-                    c[q].load(hx, hy, hz, vj16, vj32, p, p < p1);
+                    c[q].template load<false, (MGPBD_L2POL != 0)>(hx, hy, hz, vj16, vj32, p, p < p1, pol);
                 }
                 T xv[UN][VW];
 #pragma unroll
@@ -484,8 +503,15 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         uint32_t tot = bh + bv + (XJ ? 0 : bs) + bs + (ND ? bs : 0) + (NB ? bs : 0) + (NA ? bs : 0) + (NP ? bs : 0);
         uint64_t* bar = &bars[j % MF_STAGES];
         mbar_expect_tx(bar, tot);
-        bulk_g2s(st + LY::H, h + (int64_t)i0 * KC * 3, bh, bar);
-        bulk_g2s(st + LY::V, reinterpret_cast<const unsigned char*>(verts_) + (int64_t)i0 * KC * LY::VB, bv, bar);
+        if constexpr (MGPBD_L2POL == 1 || MGPBD_L2POL == 2) {
+            const uint64_t pol = MGPBD_L2POL == 1 ? l2_policy_first() : l2_policy_last();
+            bulk_g2s_pol(st + LY::H, h + (int64_t)i0 * KC * 3, bh, bar, pol);
+            bulk_g2s_pol(st + LY::V, reinterpret_cast<const unsigned char*>(verts_) + (int64_t)i0 * KC * LY::VB, bv, bar,
+                         pol);
+        } else {
+            bulk_g2s(st + LY::H, h + (int64_t)i0 * KC * 3, bh, bar);
+            bulk_g2s(st + LY::V, reinterpret_cast<const unsigned char*>(verts_) + (int64_t)i0 * KC * LY::VB, bv, bar);
+        }
         if (!XJ) bulk_g2s(st + LY::X, x + i0, bs, bar);
         bulk_g2s(st + LY::AT, at + i0, bs, bar);
         if (ND) bulk_g2s(st + LY::D, dinv + i0, bs, bar);

@@ -538,10 +538,53 @@ void launch_pass_mode(const Csr<T>& A, const T* x, const T* b, T* y, const T* au
     MG_LAUNCH_CHECK();
 }
 
-template <class T>
+// Streaming vector kernels: one 16-byte chunk (W elements) per thread, every load of the chunk issued before
+// any arithmetic; V = false (an operand not 16-byte aligned, e.g. a rank's row offset) falls back to W = 1.
+template <class T, bool V>
+struct Chunk16 {
+    static constexpr int W = V ? 16 / (int)sizeof(T) : 1;
+    using VT = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    // element range of chunk c: [c W, min(n, c W + W))
+    __device__ static __forceinline__ bool full(int64_t c, int64_t n) { return (c + 1) * W <= n; }
+    __device__ static __forceinline__ void ld(const T* __restrict__ a, int64_t c, int64_t n, T (&o)[W]) {
+        if (V && full(c, n)) {
+            const VT v = *reinterpret_cast<const VT*>(a + c * W);
+            memcpy(o, &v, 16);
+        } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w) o[w] = c * W + w < n ? a[c * W + w] : (T)0;
+        }
+    }
+    __device__ static __forceinline__ void st(T* __restrict__ a, int64_t c, int64_t n, const T (&o)[W]) {
+        if (V && full(c, n)) {
+            VT v;
+            memcpy(&v, o, 16);
+            *reinterpret_cast<VT*>(a + c * W) = v;
+        } else {
+#pragma unroll
+            for (int w = 0; w < W; ++w)
+                if (c * W + w < n) a[c * W + w] = o[w];
+        }
+    }
+};
+inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+template <class T, bool V>
+inline int chunk_grid(int64_t n) {
+    const int64_t items = (n + Chunk16<T, V>::W - 1) / Chunk16<T, V>::W;
+    return (int)std::max<int64_t>(1, (items + PB - 1) / PB);
+}
+
+template <class T, bool V>
 __global__ void k_jacobi0(int32_t n, const T* __restrict__ dinv, const T* __restrict__ b, double omega, T* __restrict__ y) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = (T)(omega * (double)dinv[i] * (double)b[i]);
+    using C = Chunk16<T, V>;
+    const int64_t c = blockIdx.x * (int64_t)PB + threadIdx.x;
+    if (c * C::W >= n) return;
+    T d[C::W], bb[C::W], o[C::W];
+    C::ld(dinv, c, n, d);
+    C::ld(b, c, n, bb);
+#pragma unroll
+    for (int w = 0; w < C::W; ++w) o[w] = (T)(omega * (double)d[w] * (double)bb[w]);
+    C::st(y, c, n, o);
 }
 
 // bc[a] = sum_{i in a, ascending} t[i]: 8 lanes per aggregate, each lane's members in chunks of 4 with
@@ -571,11 +614,36 @@ __global__ void k_restrict(int32_t nc, const int64_t* __restrict__ mptr, const i
     }
 }
 
-template <class T>
+template <class T, bool V>
 __global__ void k_prolong(int32_t n, const int32_t* __restrict__ agg, const T* __restrict__ P, const T* __restrict__ e,
                           T* __restrict__ x) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        x[i] = (T)((double)x[i] + (double)P[i] * (double)e[agg[i]]);
+    using C = Chunk16<T, V>;
+    constexpr int W = C::W;
+    const int64_t c = blockIdx.x * (int64_t)PB + threadIdx.x;
+    if (c * W >= n) return;
+    T xv[W], pv[W], ev[W];
+    int32_t ag[W];
+    C::ld(x, c, n, xv);
+    C::ld(P, c, n, pv);
+    if (V && C::full(c, n)) {  // W 32-bit aggregate ids: 16 (fp32) or 8 bytes (fp64)
+        if constexpr (W == 4) {
+            const int4 a4 = *reinterpret_cast<const int4*>(agg + c * W);
+            memcpy(ag, &a4, 16);
+        } else if constexpr (W == 2) {
+            const int2 a2 = *reinterpret_cast<const int2*>(agg + c * W);
+            memcpy(ag, &a2, 8);
+        } else {
+            ag[0] = agg[c];
+        }
+    } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) ag[w] = c * W + w < n ? agg[c * W + w] : 0;
+    }
+#pragma unroll
+    for (int w = 0; w < W; ++w) ev[w] = e[ag[w]];
+#pragma unroll
+    for (int w = 0; w < W; ++w) xv[w] = (T)((double)xv[w] + (double)pv[w] * (double)ev[w]);
+    C::st(x, c, n, xv);
 }
 
 // Convergence exit of MGPCG (pcg_tol > 0): true if the solve is frozen at iteration k, i.e. it was
@@ -616,10 +684,15 @@ __global__ void k_pcg_xr(int32_t n, const T* __restrict__ p, const T* __restrict
 // Finalisation of <r,z> (and <r,r>) fused into the p update: every CTA reduces the partials in the same
 // fixed order (identical value everywhere), CTA 0 publishes the scalar and raises the flags of
 // k_fin_rz; saves one launch per PCG iteration.
-template <class T>
+template <class T, bool V>
 __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ p, double* __restrict__ scal, int k,
                             const double* __restrict__ prz, const double* __restrict__ prr, int np, int* flags,
                             int tag) {
+    using CK = Chunk16<T, V>;
+    constexpr int W = CK::W;
+    const int64_t ci = blockIdx.x * (int64_t)PB + threadIdx.x;
+    T zv[W], pv[W];
+    if (ci * W < n) { CK::ld(z, ci, n, zv); CK::ld(p, ci, n, pv); }  // issued before the partial sums
     __shared__ double sh[32];
     __shared__ double rz_s;
     double a = 0.0, c = 0.0;
@@ -655,16 +728,25 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
         const double prev = scal[2 * (k - 1)];
         beta = prev != 0.0 ? rz_s / prev : 0.0;
     }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        p[i] = (T)((double)z[i] + beta * (double)p[i]);
+    if (ci * W >= n) return;
+#pragma unroll
+    for (int w = 0; w < W; ++w) pv[w] = (T)((double)zv[w] + beta * (double)pv[w]);
+    CK::st(p, ci, n, pv);
 }
 
 // <p,q> finalisation fused into the x / r update (see k_pcg_p_fin)
-template <class T>
+template <class T, bool V>
 __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
                              T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
                              int np, int* flags, int tag) {
     if (scal[SC_DONE] != 0.0) return;
+    using CK = Chunk16<T, V>;
+    constexpr int W = CK::W;
+    const int64_t ci = blockIdx.x * (int64_t)PB + threadIdx.x;
+    T xv[W], pv[W], rv[W], qv[W];
+    if (ci * W < n) {  // issued before the partial sums
+        CK::ld(x, ci, n, xv); CK::ld(p, ci, n, pv); CK::ld(r, ci, n, rv); CK::ld(q, ci, n, qv);
+    }
     __shared__ double sh[32];
     __shared__ double pq_s;
     double a = 0.0;
@@ -680,10 +762,14 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
     }
     __syncthreads();
     const double alpha = pq_s != 0.0 ? scal[2 * k] / pq_s : 0.0;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        x[i] = (T)((double)x[i] + alpha * (double)p[i]);
-        r[i] = (T)((double)r[i] - alpha * (double)q[i]);
+    if (ci * W >= n) return;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+        xv[w] = (T)((double)xv[w] + alpha * (double)pv[w]);
+        rv[w] = (T)((double)rv[w] - alpha * (double)qv[w]);
     }
+    CK::st(x, ci, n, xv);
+    CK::st(r, ci, n, rv);
 }
 
 // One colour of a multicolour Gauss-Seidel sweep (reading c22): for the rows of colour c
@@ -1281,7 +1367,10 @@ void csr_pass(int mode, const Csr<T>& A, const T* x, const T* b, T* y, const T* 
 template <class T>
 void vec_jacobi0(int32_t n, const T* dinv, const T* b, double omega, T* y, cudaStream_t s) {
     if (!n) return;
-    k_jacobi0<T><<<vgrid(n), PB, 0, s>>>(n, dinv, b, omega, y);
+    if (al16(dinv) && al16(b) && al16(y))
+        k_jacobi0<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, dinv, b, omega, y);
+    else
+        k_jacobi0<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, dinv, b, omega, y);
     MG_LAUNCH_CHECK();
 }
 template <class T>
@@ -1294,7 +1383,10 @@ void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, con
 template <class T>
 void prolong_add(int32_t n, const int32_t* agg, const T* P, const T* e, T* x, cudaStream_t s) {
     if (!n) return;
-    k_prolong<T><<<vgrid(n), PB, 0, s>>>(n, agg, P, e, x);
+    if (al16(agg) && al16(P) && al16(x))
+        k_prolong<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, agg, P, e, x);
+    else
+        k_prolong<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, agg, P, e, x);
     MG_LAUNCH_CHECK();
 }
 template <class T>
@@ -1315,13 +1407,20 @@ void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaSt
 template <class T>
 void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const double* prz, const double* prr, int np,
                       int* flags, int tag, cudaStream_t s) {
-    k_pcg_p_fin<T><<<vgrid(std::max<int32_t>(n, 1)), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag);
+    // every CTA must run (CTA 0 publishes the scalars even for n = 0): the grid covers at least one chunk
+    if (al16(z) && al16(p))
+        k_pcg_p_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag);
+    else
+        k_pcg_p_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag);
     MG_LAUNCH_CHECK();
 }
 template <class T>
 void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
                        int* flags, int tag, cudaStream_t s) {
-    k_pcg_xr_fin<T><<<vgrid(std::max<int32_t>(n, 1)), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag);
+    if (al16(p) && al16(q) && al16(x) && al16(r))
+        k_pcg_xr_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag);
+    else
+        k_pcg_xr_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag);
     MG_LAUNCH_CHECK();
 }
 template <class T>

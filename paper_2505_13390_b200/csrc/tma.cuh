@@ -27,4 +27,42 @@ static __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint
                  : "memory");
 }
 
+// L2 eviction-priority policies (createpolicy) and the hinted loads / bulk copies that carry them: the level-0
+// pass keeps one of its two gradient streams L2-resident across the 50 passes of an outer iteration
+// (MGPBD_L2POL, matfree.cu).
+static __device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+static __device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+static __device__ __forceinline__ uint4 ldg16_pol(const void* q, uint64_t pol) {
+    uint4 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(q), "l"(pol));
+    return r;
+}
+static __device__ __forceinline__ uint2 ldg8_pol(const void* q, uint64_t pol) {
+    uint2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(r.x), "=r"(r.y) : "l"(q), "l"(pol));
+    return r;
+}
+static __device__ __forceinline__ uint32_t ldg4_pol(const void* q, uint64_t pol) {
+    uint32_t r;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(q), "l"(pol));
+    return r;
+}
+static __device__ __forceinline__ void bulk_g2s_pol(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                    uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 }  // namespace mgpbd

@@ -8,6 +8,9 @@
   relative residual ||b_last|| / ||b_0|| per frame, frames with a setup, device time.
 * smoother — omega-Jacobi vs Chebyshev ("omega-Jacobi has the best performance for
   softbody, and Chebyshev has the best performance for cloth") at the same number of matrix passes.
+* omega_refresh — indefinite MGPCG steps through the lazy window (reading c26): bar50k and block1.67M
+  frames in the literal lazy schedule (no early re-setup), omega_refresh_iters 0 / 10 / 50, lambda_safety 1 / 1.1:
+  indefinite PCG iterations per frame, residual reduction, device time.
 * cloth_tol — the paper's cloth hanging test (Fig. cloth, Table 1: N = 64/128/256/512, dt 3 ms,
   stiffness 1e9, "maxiter (1e5) ... ||b|| < 1e-4"): outer iterations and device time per frame until
   ||b|| < 1e-4 (absolute, Alg. 1 l.12), capped at MAXIT.
@@ -120,7 +123,29 @@ def cloth_tol(maxit=20000, frames=2):
     return out
 
 
+def omega_refresh(frames=20):
+    for name in ("bar50k", "block1.67M"):
+        sc = scenes.make(name)
+        for safety in (1.0, 1.1):
+            for k in (0, 10, 50):
+                ctx = mgpbd.Context.from_scene(sc, precision=1, lambda_safety=safety, resetup_on_indef=0,
+                                               omega_refresh_iters=k)
+                ev, rel, ms = [], [], []
+                for f in range(frames):
+                    ctx.step(sc.dt, sc.n_iters)
+                    st = ctx.stats()
+                    ev.append(st.indefinite_events)
+                    rel.append(st.b_last / max(st.b_norm[0], 1e-300))
+                    ms.append(st.ms_frame)
+                ctx.close()
+                print(json.dumps({"experiment": "omega_refresh", "config": name, "lambda_safety": safety,
+                                  "omega_refresh_iters": k, "frames": frames, "indefinite_events": ev,
+                                  "total_events": int(sum(ev)), "mean_rel_residual": statistics.mean(rel),
+                                  "ms_frame_median": statistics.median(ms)}), flush=True)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["linearity", "lazy", "smoother"]
     for w in which:
-        {"linearity": linearity, "lazy": lazy, "smoother": smoother, "cloth_tol": cloth_tol}[w]()
+        {"linearity": linearity, "lazy": lazy, "smoother": smoother, "cloth_tol": cloth_tol,
+         "omega_refresh": omega_refresh}[w]()
