@@ -11,7 +11,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libmgpbd.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["util.cu", "mesh.cu", "solve.cu", "setup.cu", "comm.cu", "matfree.cu", "vagal.cu", "coarse.cu", "coarse_res.cu", "nullspace.cu", "coarse_tail.cu", "engine.cu"]
+SOURCES = ["util.cu", "mesh.cu", "solve.cu", "setup.cu", "comm.cu", "matfree.cu", "vagal.cu", "coarse.cu", "coarse_res.cu", "nullspace.cu", "coarse_tail.cu", "subcycle.cu", "engine.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "-I", INCLUDE,

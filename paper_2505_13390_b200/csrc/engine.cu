@@ -21,6 +21,7 @@
 #include "coarse_res.cuh"
 #include "nullspace.cuh"
 #include "coarse_tail.cuh"
+#include "subcycle.cuh"
 
 namespace mgpbd {
 
@@ -216,6 +217,12 @@ class Engine : public EngineBase {
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
     int64_t omega_refreshes = 0;
+    // dense bottom of the cycle (reading c27; MGPBD_DENSE_CUT = max rows, 0 = off)
+    int dense_cut = std::getenv("MGPBD_DENSE_CUT") ? std::atoi(std::getenv("MGPBD_DENSE_CUT")) : 1024;
+    int lcut = -1;
+    bool sub_ok = false;
+    SubCycle<T> subc;
+    DBuf<double> Mcut;
     bool va_setup0 = false;  // the last setup formed level 1 through the VA plan (fp64 omega refresh follows it)
     bool va_off = std::getenv("MGPBD_NO_VA_SETUP") != nullptr;  // CSR Galerkin at setup (comparison)
     double last_dt = 0.0;
@@ -669,24 +676,62 @@ class Engine : public EngineBase {
 
     // The coarse-cycle kernels' tables (levels, smoother coefficients, resident / tail plans) from the current
     // hierarchy: at setup, and after a per-frame omega refresh (reading c26).
+    // Reading c27: the first coarse level l >= 1 with at most `dense_cut` rows (and levels below it) becomes the
+    // hot cycle's dense bottom z = M b, M rebuilt from the sub-cycle at every refresh (subcycle.cuh).
+    void plan_subcycle() {
+        sub_ok = false;
+        lcut = -1;
+        if (dense_cut <= 0 || kk != 1 || cfg.smoother == 2 || nL < 3) return;
+        for (int l = 1; l + 1 < nL; ++l)
+            if (L[l]->n <= dense_cut) { lcut = l; break; }
+        if (lcut < 0 || nL - lcut > SUB_MAXL) { lcut = -1; return; }
+        subc = SubCycle<T>();
+        subc.K = nL - lcut;
+        subc.nu = cfg.smoother_sweeps;
+        subc.Ainv = Ainv.p;
+        for (int l = lcut; l < nL; ++l) {
+            Level& a = *L[l];
+            SubLevel<T>& c = subc.L[l - lcut];
+            c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p;
+            for (int k = 0; k < 8; ++k) { c.om[k] = a.sm_omega[k]; c.al[k] = a.sm_alpha[k]; }
+            if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; }
+        }
+        if (!subcycle_plan<T>(subc, 200u * 1024u)) { lcut = -1; return; }
+        Mcut.resize((size_t)L[lcut]->n * L[lcut]->n);
+        sub_ok = true;
+    }
+    // the hot cycle's bottom level (dense solve) and its matrix
+    int lc() const { return sub_ok ? lcut : nL - 1; }
+    const double* bottom_inv() const { return sub_ok ? Mcut.p : Ainv.p; }
+
     void plan_coarse() {
+        plan_subcycle();
+        plan_coarse_kernels();
+        if (sub_ok && ccyc_ok && use_res && !res_ok) {  // the dense bottom's slices do not fit: plain bottom
+            sub_ok = false;
+            lcut = -1;
+            plan_coarse_kernels();
+        }
+    }
+
+    void plan_coarse_kernels() {
         ccyc_ok = false;
-        if (use_coarse_kernel && cfg.smoother != 2 && kk == 1 && ccyc_from >= 1 && nL >= ccyc_from + 2) {
+        if (use_coarse_kernel && cfg.smoother != 2 && kk == 1 && ccyc_from >= 1 && lc() >= ccyc_from + 1) {
             ccyc = CoarseCycle<T>();
-            ccyc.K = nL - ccyc_from;
+            ccyc.K = lc() + 1 - ccyc_from;
             ccyc.nu = cfg.smoother_sweeps;
-            ccyc.Ainv = Ainv.p;
+            ccyc.Ainv = bottom_inv();
             if (std::getenv("MGPBD_TRACE_COARSE")) {
                 ctrace.resize(128);  // [0, 32): grid-wide kernel (down half), [32, 64): cluster tail, [64, 96): up half
                 MG_CK(cudaMemsetAsync(ctrace.p, 0, 128 * sizeof(unsigned long long), st));
                 ccyc.trace = ctrace.p;
             }
-            for (int l = ccyc_from; l < nL; ++l) {
+            for (int l = ccyc_from; l <= lc(); ++l) {
                 Level& a = *L[l];
                 CoarseLevel<T>& c = ccyc.L[l - ccyc_from];
                 c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p; c.omega = a.omega;
                 for (int k = 0; k < 8; ++k) { c.sm_omega[k] = a.sm_omega[k]; c.sm_alpha[k] = a.sm_alpha[k]; }
-                if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_agg = a.n_agg; }
+                if (l < lc()) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_agg = a.n_agg; }
                 c.t = a.vt.p; c.b = a.vb.p; c.z = a.vz.p; c.x = a.vx.p; c.y = a.vy.p;
             }
             ccyc_ok = true;
@@ -1072,6 +1117,7 @@ class Engine : public EngineBase {
         }
         mark_stage(2);
         coarse_invert<T>(L[nL - 1]->hot(), inv_work.p, Ainv.p, flags.p, st);
+        if (sub_ok) subcycle_matrix<T>(subc, Mcut.p, st);  // reading c27
     }
 
     // ------------------------------------------------------------------ V-cycle
@@ -1079,8 +1125,8 @@ class Engine : public EngineBase {
     // produces the partials of r.z and r.r.
     void vcycle(int l, const T* b, T* x_out, const T* dot_r) {
         Level& a = *L[l];
-        if (l == nL - 1) {
-            coarse_gemv<T>(a.n, Ainv.p, b, x_out, st);
+        if (l == lc()) {  // coarsest: its inverse; or the dense bottom M of reading c27
+            coarse_gemv<T>(a.n, bottom_inv(), b, x_out, st);
             return;
         }
         if (l == ccyc_from && ccyc_ok && b == a.vb.p && x_out == a.vz.p) {

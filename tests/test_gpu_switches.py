@@ -14,7 +14,9 @@ MF_SWITCHES = ["", "MGPBD_NO_GRAPH=1", "MGPBD_NO_TMA=1", "MGPBD_NO_RES_COARSE=1"
                "MGPBD_COARSE_FROM=2", "MGPBD_NO_GJ_COOP=1", "MGPBD_NO_VA_SETUP=1", "MGPBD_NO_POWER_COOP=1",
                "MGPBD_NO_TAIL=1", "MGPBD_NO_VJ16=1", "MGPBD_NO_V16=1", "MGPBD_VG_TMA=1", "MGPBD_MF_GRID_CAP=2",
                "MGPBD_RES_CAP=4096", "MGPBD_FUSE_J0=1", "MGPBD_NO_FUSED_TAIL=1",
-               "MGPBD_TAIL_SCALAR_BCAST=1", "MGPBD_SOLO=1", "MGPBD_SOLO=1 MGPBD_NO_TAIL=1"]
+               "MGPBD_TAIL_SCALAR_BCAST=1", "MGPBD_SOLO=1", "MGPBD_SOLO=1 MGPBD_NO_TAIL=1",
+               "MGPBD_DENSE_CUT=0", "MGPBD_DENSE_CUT=64", "MGPBD_DENSE_CUT=100000",
+               "MGPBD_DENSE_CUT=64 MGPBD_NO_TAIL=1", "MGPBD_DENSE_CUT=64 MGPBD_NO_RES_COARSE=1"]
 CSR_SWITCHES = ["", "MGPBD_NO_BAND=1", "MGPBD_NO_ROWS=1", "MGPBD_NO_BAND=1 MGPBD_NO_ROWS=1"]
 ITERS = 3
 
@@ -61,6 +63,7 @@ def test_csr_switch(monkeypatch, ref, switch):
 
 
 @pytest.mark.parametrize("switch", ["", "MGPBD_SOLO=1", "MGPBD_NO_TAIL=1", "MGPBD_NO_FUSED_TAIL=1",
+                                    "MGPBD_DENSE_CUT=0", "MGPBD_DENSE_CUT=100000",
                                     "MGPBD_TAIL_SCALAR_BCAST=1",
                                     "MGPBD_NO_VJ16=1 MGPBD_NO_V16=1"])
 def test_fp32_switch(monkeypatch, ref, switch):
@@ -68,3 +71,30 @@ def test_fp32_switch(monkeypatch, ref, switch):
     xo, _, lo = sim.state()
     lg, xg, _ = run(monkeypatch, sc, switch, 1, precision=1)
     assert rel(lg, lo) <= 1e-3 and rel(xg - sc.pos, xo - sc.pos) <= 1e-3, switch
+
+
+@pytest.mark.parametrize("precision,tol", [(0, 1e-12), (1, 1e-4)], ids=["fp64", "fp32"])
+def test_dense_bottom_equals_level_by_level_cycle(monkeypatch, precision, tol):
+    """Reading c27: the V-cycle whose bottom levels are applied as the explicit sub-cycle matrix M equals the
+    level-by-level cycle on the same hierarchy (identical inputs, deterministic setup) up to rounding, for a
+    cut at every coarse level (MGPBD_DENSE_CUT rows) and through the resident, global and per-level kernels."""
+    sc = scenes.make("block_small")
+    rng = np.random.default_rng(7)
+    b = rng.normal(size=sc.n_cons)
+    out = {}
+    for cut in (0, 64, 400, 100000):
+        for extra in ("", "MGPBD_NO_RES_COARSE=1", "MGPBD_NO_COARSE_KERNEL=1"):
+            monkeypatch.setenv("MGPBD_DENSE_CUT", str(cut))
+            for k in ("MGPBD_NO_RES_COARSE", "MGPBD_NO_COARSE_KERNEL"):
+                monkeypatch.delenv(k, raising=False)
+            if extra:
+                monkeypatch.setenv(extra.split("=")[0], "1")
+            ctx = mgpbd.Context.from_scene(sc, precision=precision, min_coarse=30)
+            ctx.debug_prepare(sc.dt)
+            out[(cut, extra)] = (ctx.debug_vcycle(b), ctx.stats().n_levels)
+            ctx.close()
+    z0, nl = out[(0, "")]
+    assert nl >= 4
+    for key, (z, n) in out.items():
+        assert n == nl
+        assert rel(z, z0) <= tol, (key, rel(z, z0))
