@@ -67,6 +67,11 @@ __global__ void k_mf_refresh(int64_t p0, int64_t p1, int64_t npad, const int32_t
     }
 }
 
+// timing experiments only (tools/pass_sweep.sh; results are wrong): 1 = no x gather in the vertex gather,
+// 2 = no h planes (only the constraint offsets streamed)
+#ifndef MGPBD_VG_EXPT
+#define MGPBD_VG_EXPT 0
+#endif
 // One 16-byte chunk of a vertex's padded incidence list: VW = 16 / sizeof(T) incidences of the three h planes
 // and their constraint indices (16- or 32-bit).
 template <class T, bool J16>
@@ -96,10 +101,15 @@ struct Chunk {
             }
         };
         if (in) {
-            const VT a = ld(reinterpret_cast<const VT*>(hx_ + p));
-            const VT b = ld(reinterpret_cast<const VT*>(hy_ + p));
-            const VT c = ld(reinterpret_cast<const VT*>(hz_ + p));
-            memcpy(hx, &a, 16); memcpy(hy, &b, 16); memcpy(hz, &c, 16);
+            if (MGPBD_VG_EXPT == 2 && !SM) {
+#pragma unroll
+                for (int w = 0; w < VW; ++w) hx[w] = hy[w] = hz[w] = (T)(p + w);
+            } else {
+                const VT a = ld(reinterpret_cast<const VT*>(hx_ + p));
+                const VT b = ld(reinterpret_cast<const VT*>(hy_ + p));
+                const VT c = ld(reinterpret_cast<const VT*>(hz_ + p));
+                memcpy(hx, &a, 16); memcpy(hy, &b, 16); memcpy(hz, &c, 16);
+            }
             if constexpr (J16 && VW == 4) {
                 const uint2 w = ld(reinterpret_cast<const uint2*>(j16 + p));
                 j[0] = (int32_t)(w.x & 0xFFFFu); j[1] = (int32_t)(w.x >> 16);
@@ -136,6 +146,21 @@ struct Chunk {
 #ifndef MGPBD_VG_PREFETCH
 #define MGPBD_VG_PREFETCH 1
 #endif
+// 2 (default): contiguous vertex range per CTA of a persistent grid (x values reused from L1 across the
+// constraints a vertex plane shares with the next: 45.9 -> 43.4 us per fp32 pass, profiles/r2/sweep_vgather.txt);
+// 1: the same with the ranges of the CTAs co-resident on an SM adjacent; 0: grid-stride
+#ifndef MGPBD_VG_BLOCKED
+#define MGPBD_VG_BLOCKED 2
+#endif
+inline int vg_sms() {
+    static const int n = [] {
+        int dev = 0, sms = 148;
+        MG_CK(cudaGetDevice(&dev));
+        MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        return sms;
+    }();
+    return n;
+}
 // L2 policy of the level-0 pass's two gradient streams (hv in the vertex gather, h in the row kernel; each
 // ~80 MB fp32 on block1.67M, read 50 times per outer iteration): 0 = streaming (evict-first loads in the
 // gather, default bulk copies), 1 = gather stream evict_last + row stream evict_first, 2 = the reverse,
@@ -150,7 +175,7 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
                                                       const int32_t* __restrict__ vj32,
                                                       const int32_t* __restrict__ jbase, const T* __restrict__ hv,
                                                       const T* __restrict__ x, V4<T>* __restrict__ u,
-                                                      const T* __restrict__ xd, const T* __restrict__ xb, double xom) {
+                                                      const T* __restrict__ xd, const T* __restrict__ xb, double xom, int nsm) {
     // programmatic dependent launch: the row kernel may start streaming its static operands now; it
     // waits (griddepcontrol.wait) for this grid's u before gathering it
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -158,8 +183,28 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
     constexpr int VW = CH::VW;
     constexpr int PER_WARP = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // vertices of this warp: base = first, first + step, ... < vend.  Grid-stride over the whole range, or
+    // (MGPBD_VG_BLOCKED, persistent grid) one contiguous range per CTA, the CTAs resident on one SM holding
+    // adjacent ranges (CTA i runs on SM i mod S), so an SM sweeps ~n_v / S consecutive vertices and the x values
+    // of the constraints between two vertex planes are reused from its L1
+    int64_t first, step, vend;
+    if (MGPBD_VG_BLOCKED) {
+        const int S = gridDim.x < (unsigned)nsm ? (int)gridDim.x : nsm;
+        const int per = (int)gridDim.x / S;
+        const int r = MGPBD_VG_BLOCKED == 2 ? (int)blockIdx.x : (int)(blockIdx.x % S) * per + (int)(blockIdx.x / S);
+        const int64_t wpc = blockDim.x >> 5;
+        const int64_t chunk = ((v1 - v0 + (int64_t)gridDim.x - 1) / gridDim.x + wpc * PER_WARP - 1) / (wpc * PER_WARP) * (wpc * PER_WARP);
+        const int64_t cs = v0 + (int64_t)r * chunk;
+        vend = cs + chunk < v1 ? cs + chunk : v1;
+        first = cs + (int64_t)(threadIdx.x >> 5) * PER_WARP;
+        step = wpc * PER_WARP;
+    } else {
+        const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+        first = v0 + warp * PER_WARP;
+        step = nwarps * PER_WARP;
+        vend = v1;
+    }
     const T* __restrict__ hx = hv;
     const T* __restrict__ hy = hv + npad;
     const T* __restrict__ hz = hv + 2 * npad;
@@ -169,18 +214,18 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
     int64_t p0n = 0, p1n = 0;
     int32_t jbn = 0;
     auto fetch = [&](int64_t vv) {
-        if (vv < v1) { p0n = ppos[vv]; p1n = ppos[vv + 1]; jbn = J16 ? jbase[vv] : 0; }
+        if (vv < vend) { p0n = ppos[vv]; p1n = ppos[vv + 1]; jbn = J16 ? jbase[vv] : 0; }
     };
-    if (MGPBD_VG_PREFETCH) fetch(v0 + warp * PER_WARP + sub);
-    for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {  // warp-uniform
+    if (MGPBD_VG_PREFETCH) fetch(first + sub);
+    for (int64_t base = first; base < vend; base += step) {  // warp-uniform
         const int64_t v = base + sub;
         using AC = typename std::conditional<MGPBD_VG_ACC64 != 0, double, T>::type;
         AC a0 = (AC)0, a1 = (AC)0, a2 = (AC)0;
         if (!MGPBD_VG_PREFETCH) fetch(v);
         const int64_t p0 = p0n, p1 = p1n;
         const int32_t jb = jbn;
-        if (MGPBD_VG_PREFETCH) fetch(v + nwarps * PER_WARP);
-        if (v < v1) {
+        if (MGPBD_VG_PREFETCH) fetch(v + step);
+        if (v < vend) {
             for (int64_t pb = p0 + (int64_t)sl * VW; pb < p1; pb += (int64_t)G * VW * UN) {
                 CH c[UN];
 #pragma unroll
@@ -194,7 +239,8 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
 #pragma unroll
                     for (int w = 0; w < VW; ++w) {
                         const int32_t jj = jb + c[q].j[w];
-                        if (XJ) xv[q][w] = (T)(xom * (double)xd[jj] * (double)xb[jj]);
+                        if (MGPBD_VG_EXPT == 1) xv[q][w] = (T)jj;   // timing experiment: no x gather
+                        else if (XJ) xv[q][w] = (T)(xom * (double)xd[jj] * (double)xb[jj]);
                         else xv[q][w] = x[jj];
                     }
 #pragma unroll
@@ -210,12 +256,12 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
         a0 = group_sum_t<G>(a0);
         a1 = group_sum_t<G>(a1);
         a2 = group_sum_t<G>(a2);
-        if (v < v1 && sl == 0) u[v] = V4<T>{(T)a0, (T)a1, (T)a2, (T)0};
+        if (v < vend && sl == 0) u[v] = V4<T>{(T)a0, (T)a1, (T)a2, (T)0};
     }
 }
 
 // TMA-pipelined vertex gather: persistent CTAs stream tiles of VGT consecutive vertices — their padded slot
-// ranges of the three h planes, the constraint offsets and the vertex's slot offsets — into a MF_STAGES-deep
+// ranges of the three h planes, the constraint offsets and the vertex's slot offsets — into a VG_STAGES-deep
 // shared-memory ring with 1-D bulk copies, so the HBM stream never waits on the dependent x gathers; G lanes
 // per vertex read 16-byte chunks from shared memory and gather x from L2 (same sums, same order as
 // k_mf_vgather).
@@ -223,7 +269,14 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
 #define MGPBD_VGT 32
 #endif
 constexpr int VGT = MGPBD_VGT;       // vertices per tile
-constexpr int VG_BS = 128;           // threads per CTA
+#ifndef MGPBD_VG_BS
+#define MGPBD_VG_BS 128
+#endif
+#ifndef MGPBD_VG_STAGES
+#define MGPBD_VG_STAGES 3
+#endif
+constexpr int VG_BS = MGPBD_VG_BS;   // threads per CTA
+constexpr int VG_STAGES = MGPBD_VG_STAGES;
 
 template <class T, bool J16>
 struct VgLayout {                    // one stage for tiles of at most TS slots
@@ -246,11 +299,11 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
                                                           const T* __restrict__ x, V4<T>* __restrict__ u) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     extern __shared__ __align__(128) unsigned char smem[];
-    __shared__ __align__(8) uint64_t bars[MF_STAGES];
+    __shared__ __align__(8) uint64_t bars[VG_STAGES];
     const VgLayout<T, J16> LY(TS);
     const int t = threadIdx.x;
     if (t == 0) {
-        for (int k = 0; k < MF_STAGES; ++k) mbar_init(&bars[k], 1);
+        for (int k = 0; k < VG_STAGES; ++k) mbar_init(&bars[k], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -261,7 +314,7 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
     constexpr uint32_t JB = J16 ? 2u : 4u;
     auto issue = [&](int jt) {
         const int tile = blockIdx.x + jt * gridDim.x;
-        unsigned char* st = smem + (size_t)(jt % MF_STAGES) * LY.bytes;
+        unsigned char* st = smem + (size_t)(jt % VG_STAGES) * LY.bytes;
         const int32_t va = v0 + tile * VGT, vb = min(va + VGT, v1);
         const int64_t pa = ppos[va], pb = ppos[vb];
         const uint32_t ns = (uint32_t)(pb - pa);
@@ -269,7 +322,7 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
         const uint32_t jbytes = (uint32_t)(((ja - ja0) + (uintptr_t)ns * JB + 15) & ~(uintptr_t)15);
         const uintptr_t pp = reinterpret_cast<uintptr_t>(ppos + va), pp0 = pp & ~(uintptr_t)15;
         const uint32_t pbytes = (uint32_t)(((pp - pp0) + (uintptr_t)(vb - va + 1) * 8 + 15) & ~(uintptr_t)15);
-        uint64_t* bar = &bars[jt % MF_STAGES];
+        uint64_t* bar = &bars[jt % VG_STAGES];
         mbar_expect_tx(bar, 3 * ns * (uint32_t)sizeof(T) + jbytes + pbytes);
         if (ns) {
             bulk_g2s(st + LY.hx, hx + pa, ns * (uint32_t)sizeof(T), bar);
@@ -281,13 +334,13 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
     };
     const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     if (t == 0)
-        for (int jt = 0; jt < MF_STAGES && jt < my_tiles; ++jt) issue(jt);
+        for (int jt = 0; jt < VG_STAGES && jt < my_tiles; ++jt) issue(jt);
     using CH = Chunk<T, J16>;
     constexpr int VW = CH::VW;
     const int g = t / G, sl = t % G;
     for (int jt = 0; jt < my_tiles; ++jt) {
-        mbar_wait(&bars[jt % MF_STAGES], (uint32_t)((jt / MF_STAGES) & 1));
-        const unsigned char* st = smem + (size_t)(jt % MF_STAGES) * LY.bytes;
+        mbar_wait(&bars[jt % VG_STAGES], (uint32_t)((jt / VG_STAGES) & 1));
+        const unsigned char* st = smem + (size_t)(jt % VG_STAGES) * LY.bytes;
         const int tile = blockIdx.x + jt * gridDim.x;
         const int32_t va = v0 + tile * VGT, vb = min(va + VGT, v1);
         const uintptr_t pp = reinterpret_cast<uintptr_t>(ppos + va);
@@ -304,17 +357,30 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
             if (v < vb) {
                 const int64_t s0 = spp[vi] - pa, s1 = spp[vi + 1] - pa;
                 const int32_t jb = J16 ? jbase[v] : 0;
-                for (int64_t sb = s0 + (int64_t)sl * VW; sb < s1; sb += (int64_t)G * VW) {
-                    CH c;
-                    c.template load<true>(shx, shy, shz, reinterpret_cast<const uint16_t*>(sj),
-                                          reinterpret_cast<const int32_t*>(sj), sb, true);
+                // rounds of VUN chunks per lane: all chunks from shared memory, then all their x gathers (one L2
+                // round trip per round), then the products
+                constexpr int VUN = 2;
+                for (int64_t sb = s0 + (int64_t)sl * VW; sb < s1; sb += (int64_t)G * VW * VUN) {
+                    CH c[VUN];
 #pragma unroll
-                    for (int w = 0; w < VW; ++w) {
-                        const T xv = x[jb + c.j[w]];
-                        a0 += c.hx[w] * xv;
-                        a1 += c.hy[w] * xv;
-                        a2 += c.hz[w] * xv;
+                    for (int q = 0; q < VUN; ++q) {
+                        const int64_t sq = sb + (int64_t)q * G * VW;
+                        c[q].template load<true>(shx, shy, shz, reinterpret_cast<const uint16_t*>(sj),
+                                                 reinterpret_cast<const int32_t*>(sj), sq, sq < s1);
                     }
+                    T xv[VUN][VW];
+#pragma unroll
+                    for (int q = 0; q < VUN; ++q)
+#pragma unroll
+                        for (int w = 0; w < VW; ++w) xv[q][w] = x[jb + c[q].j[w]];
+#pragma unroll
+                    for (int q = 0; q < VUN; ++q)
+#pragma unroll
+                        for (int w = 0; w < VW; ++w) {
+                            a0 += c[q].hx[w] * xv[q][w];
+                            a1 += c[q].hy[w] * xv[q][w];
+                            a2 += c[q].hz[w] * xv[q][w];
+                        }
                 }
             }
             a0 = group_sum_t<G>(a0);
@@ -323,7 +389,7 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
             if (v < vb && sl == 0) u[v] = V4<T>{a0, a1, a2, (T)0};
         }
         __syncthreads();   // every thread is done with this stage: refill it
-        if (t == 0 && jt + MF_STAGES < my_tiles) issue(jt + MF_STAGES);
+        if (t == 0 && jt + VG_STAGES < my_tiles) issue(jt + VG_STAGES);
     }
 }
 
@@ -450,6 +516,9 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 // ids, h) and per-row operands into shared memory with 1-D bulk copies (cp.async.bulk, completion on
 // an mbarrier), MF_STAGES deep, so the HBM stream never waits on the dependent u gathers.
 
+#ifndef MGPBD_ROWS_PIPE
+#define MGPBD_ROWS_PIPE 1
+#endif
 template <class T, int KC, bool V16>
 struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for R = 128 or 256)
     static constexpr int R = mf_r<T, KC>();
@@ -526,35 +595,49 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
     // just before this grid (programmatic dependent launch): wait for it before the first gather
     asm volatile("griddepcontrol.wait;" ::: "memory");
     double acc1 = 0.0, acc2 = 0.0;
-    for (int j = 0; j < my_tiles; ++j) {
+    // u of tile j is gathered one tile ahead (MGPBD_ROWS_PIPE): while tile j's products run, the L2 round trip of
+    // tile j + 1's gathers is in flight (its stage has landed: the ring is MF_STAGES >= 2 deep)
+    auto rowof = [&](int j) { return tbase + (blockIdx.x + j * gridDim.x) * MF_RK + t; };
+    auto gather_u = [&](int j, V4<T> (&uo)[KC]) {
         mbar_wait(&bars[j % MF_STAGES], (uint32_t)((j / MF_STAGES) & 1));
         const unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
-        const int32_t i = tbase + (blockIdx.x + j * gridDim.x) * MF_RK + t;
+        const int32_t i = rowof(j);
         if (i >= row0 && i < row1) {
             int vi[KC];
-            T hi[KC][3];
-            {
-                if (V16) {
-                    const uint16_t* sv = reinterpret_cast<const uint16_t*>(st + LY::V) + t * KC;
-                    const int32_t vb = vbase[blockIdx.x + j * gridDim.x];
+            if (V16) {
+                const uint16_t* sv = reinterpret_cast<const uint16_t*>(st + LY::V) + t * KC;
+                const int32_t vb = vbase[blockIdx.x + j * gridDim.x];
 #pragma unroll
-                    for (int k = 0; k < KC; ++k) vi[k] = vb + (int32_t)sv[k];
-                } else {
-                    const int32_t* sv = reinterpret_cast<const int32_t*>(st + LY::V) + t * KC;
+                for (int k = 0; k < KC; ++k) vi[k] = vb + (int32_t)sv[k];
+            } else {
+                const int32_t* sv = reinterpret_cast<const int32_t*>(st + LY::V) + t * KC;
 #pragma unroll
-                    for (int k = 0; k < KC; ++k) vi[k] = sv[k];
-                }
-                load_record<T, KC>(reinterpret_cast<const T*>(st + LY::H) + t * KC * 3, hi);
+                for (int k = 0; k < KC; ++k) vi[k] = sv[k];
             }
+#pragma unroll
+            for (int k = 0; k < KC; ++k) uo[k] = u[vi[k]];
+        }
+    };
+    V4<T> uc[KC];
+    if (MGPBD_ROWS_PIPE && my_tiles > 0) gather_u(0, uc);
+    for (int j = 0; j < my_tiles; ++j) {
+        V4<T> un[KC];
+        if (MGPBD_ROWS_PIPE) {
+            if (j + 1 < my_tiles) gather_u(j + 1, un);
+        } else {
+            gather_u(j, uc);
+        }
+        const unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
+        const int32_t i = rowof(j);
+        if (i >= row0 && i < row1) {
+            T hi[KC][3];
+            load_record<T, KC>(reinterpret_cast<const T*>(st + LY::H) + t * KC * 3, hi);
             const T xi = xom != 0.0 ? (T)(xom * (double)reinterpret_cast<const T*>(st + LY::D)[t] *
                                           (double)reinterpret_cast<const T*>(st + LY::B)[t])
                                     : reinterpret_cast<const T*>(st + LY::X)[t];
             T acc = reinterpret_cast<const T*>(st + LY::AT)[t] * xi;
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const V4<T> uu = u[vi[k]];
-                acc += hi[k][0] * uu.x + hi[k][1] * uu.y + hi[k][2] * uu.z;
-            }
+            for (int k = 0; k < KC; ++k) acc += hi[k][0] * uc[k].x + hi[k][1] * uc[k].y + hi[k][2] * uc[k].z;
             const double s = (double)acc;
             const double di = ND ? (double)reinterpret_cast<const T*>(st + LY::D)[t] : 0.0;
             const double bi = NB ? (double)reinterpret_cast<const T*>(st + LY::B)[t] : 0.0;
@@ -580,6 +663,10 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         }
         __syncthreads();  // every thread is done with this stage: refill it
         if (t == 0 && j + MF_STAGES < my_tiles) issue(j + MF_STAGES);
+        if (MGPBD_ROWS_PIPE) {
+#pragma unroll
+            for (int k = 0; k < KC; ++k) uc[k] = un[k];
+        }
     }
     if (MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT || MODE == PASS_POWER) {
         __shared__ double sh[32];
@@ -607,12 +694,24 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #define MGPBD_VG_UN 2
 #endif
         constexpr int G = KC == 4 ? MGPBD_VG_G : 2;
-        constexpr int UN = KC == 4 ? MGPBD_VG_UN : 1;
+#ifndef MGPBD_VG_UN64
+#define MGPBD_VG_UN64 3
+#endif
+        // fp64 chunks hold 2 incidences: 3 per lane per round cover a tet vertex (78.6 vs 87.2 us per pass at 2)
+        constexpr int UN = KC == 4 ? (sizeof(T) == 8 ? MGPBD_VG_UN64 : MGPBD_VG_UN) : 1;
         const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
 #ifndef MGPBD_VG_CTAS_PER_SM
 #define MGPBD_VG_CTAS_PER_SM 16
 #endif
         int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
+        if (MGPBD_VG_BLOCKED) {  // persistent: the resident CTAs only
+            static const int resident = [] {
+                int occ = 1;
+                MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mf_vgather<T, G, UN, true, false>, MF_BS, 0));
+                return std::max(1, occ);
+            }();
+            grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, (int64_t)vg_sms() * resident);
+        }
         if (A.vg_grid_cap > 0) grid = std::min(grid, A.vg_grid_cap);
         if (A.vg_ts > 0) {  // TMA-pipelined vertex gather
             constexpr int GT = KC == 4 ? 4 : 2;
@@ -620,12 +719,12 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
             int tg = std::min(ntiles, A.vg_grid);
             if (A.vg_grid_cap > 0) tg = std::min(tg, A.vg_grid_cap);
             if (A.vj16) {
-                const size_t sm = (size_t)MF_STAGES * VgLayout<T, true>(A.vg_ts).bytes;
+                const size_t sm = (size_t)VG_STAGES * VgLayout<T, true>(A.vg_ts).bytes;
                 ensure_dyn_smem((const void*)k_mf_vgather_tma<T, GT, true>, sm);
                 k_mf_vgather_tma<T, GT, true><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
                                                                    A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
             } else {
-                const size_t sm = (size_t)MF_STAGES * VgLayout<T, false>(A.vg_ts).bytes;
+                const size_t sm = (size_t)VG_STAGES * VgLayout<T, false>(A.vg_ts).bytes;
                 ensure_dyn_smem((const void*)k_mf_vgather_tma<T, GT, false>, sm);
                 k_mf_vgather_tma<T, GT, false><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
                                                                     A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
@@ -633,7 +732,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         } else {
 #define MG_VG(J, X)                                                                                     \
     k_mf_vgather<T, G, UN, J, X><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, \
-                                                        x, reinterpret_cast<V4<T>*>(A.u), A.dinv, b, xom)
+                                                        x, reinterpret_cast<V4<T>*>(A.u), A.dinv, b, xom, vg_sms())
             if (A.vj16) { if (xom != 0.0) MG_VG(true, true); else MG_VG(true, false); }
             else { if (xom != 0.0) MG_VG(false, true); else MG_VG(false, false); }
 #undef MG_VG
@@ -705,7 +804,7 @@ int mf_vg_plan(const std::vector<int64_t>& ppos, int32_t v0, int32_t v1, int tsi
     if (ts > (1 << 20)) return 0;
     const uint32_t bytes = tsize == 4 ? (j16 ? VgLayout<float, true>((int32_t)ts).bytes : VgLayout<float, false>((int32_t)ts).bytes)
                                       : (j16 ? VgLayout<double, true>((int32_t)ts).bytes : VgLayout<double, false>((int32_t)ts).bytes);
-    const int per_sm = (int)std::min<size_t>(16, (227 * 1024) / ((size_t)MF_STAGES * bytes + 1024));
+    const int per_sm = (int)std::min<size_t>(std::min(16, 2048 / VG_BS), (227 * 1024) / ((size_t)VG_STAGES * bytes + 1024));
     if (per_sm < 1) return 0;
     int dev = 0, sms = 148;
     MG_CK(cudaGetDevice(&dev));
