@@ -519,6 +519,9 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 #ifndef MGPBD_ROWS_PIPE
 #define MGPBD_ROWS_PIPE 1
 #endif
+#ifndef MGPBD_ROWS_BLOCKED
+#define MGPBD_ROWS_BLOCKED 1
+#endif
 template <class T, int KC, bool V16>
 struct TileLayout {  // byte offsets inside one stage (every section 16-B aligned for R = 128 or 256)
     static constexpr int R = mf_r<T, KC>();
@@ -559,9 +562,12 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    // tile j of this CTA = blockIdx.x + j * gridDim.x; rows [tbase + tile*R, +R) clipped to row1
+    // tile j of this CTA: blockIdx.x + j gridDim.x (round robin), or (MGPBD_ROWS_BLOCKED) blockIdx.x tpc + j over
+    // a contiguous range of tpc tiles; rows [tbase + tile R, +R) clipped to row1
+    const int tpc = (ntiles + (int)gridDim.x - 1) / (int)gridDim.x;
+    auto tile_of = [&](int j) { return MGPBD_ROWS_BLOCKED ? (int)blockIdx.x * tpc + j : (int)blockIdx.x + j * (int)gridDim.x; };
     auto issue = [&](int j) {
-        const int tile = blockIdx.x + j * gridDim.x;
+        const int tile = tile_of(j);
         unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
         const int32_t i0 = tbase + tile * MF_RK;
         const int32_t rows = min(MF_RK, row1 - i0);
@@ -588,7 +594,8 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         if (NA) bulk_g2s(st + LY::AUX, aux + i0, bs, bar);
         if (NP) bulk_g2s(st + LY::XP, xprev + i0, bs, bar);
     };
-    const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const int my_tiles = MGPBD_ROWS_BLOCKED ? max(0, min(tpc, ntiles - (int)blockIdx.x * tpc))
+                                            : (blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0);
     if (t == 0)
         for (int j = 0; j < MF_STAGES && j < my_tiles; ++j) issue(j);
     // everything above reads only data of earlier kernels; u comes from the vertex gather launched
@@ -597,7 +604,7 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
     double acc1 = 0.0, acc2 = 0.0;
     // u of tile j is gathered one tile ahead (MGPBD_ROWS_PIPE): while tile j's products run, the L2 round trip of
     // tile j + 1's gathers is in flight (its stage has landed: the ring is MF_STAGES >= 2 deep)
-    auto rowof = [&](int j) { return tbase + (blockIdx.x + j * gridDim.x) * MF_RK + t; };
+    auto rowof = [&](int j) { return tbase + tile_of(j) * MF_RK + t; };
     auto gather_u = [&](int j, V4<T> (&uo)[KC]) {
         mbar_wait(&bars[j % MF_STAGES], (uint32_t)((j / MF_STAGES) & 1));
         const unsigned char* st = smem + (size_t)(j % MF_STAGES) * LY::BYTES;
@@ -606,7 +613,7 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
             int vi[KC];
             if (V16) {
                 const uint16_t* sv = reinterpret_cast<const uint16_t*>(st + LY::V) + t * KC;
-                const int32_t vb = vbase[blockIdx.x + j * gridDim.x];
+                const int32_t vb = vbase[tile_of(j)];
 #pragma unroll
                 for (int k = 0; k < KC; ++k) vi[k] = vb + (int32_t)sv[k];
             } else {
