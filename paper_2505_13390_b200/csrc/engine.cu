@@ -217,6 +217,11 @@ class Engine : public EngineBase {
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
     int64_t omega_refreshes = 0;
+    // level-0 x1 of the next V-cycle already formed by the PCG x / r update (one launch less per iteration)
+    bool l0_x1_ready = false;
+    bool x1_fusable() const {
+        return !dist && nL > 1 && cfg.smoother != 2 && !fuse_jacobi0 && std::getenv("MGPBD_NO_X1_FUSE") == nullptr;
+    }
     // dense bottom of the cycle (reading c27; MGPBD_DENSE_CUT = max rows, 0 = off)
     int dense_cut = std::getenv("MGPBD_DENSE_CUT") ? std::atoi(std::getenv("MGPBD_DENSE_CUT")) : 1024;
     int lcut = -1;
@@ -1179,7 +1184,9 @@ class Engine : public EngineBase {
             l0_pass(PASS_JACOBI, nullptr, b, nxt, nullptr, a.sm_omega[1], a.sm_alpha[1], nullptr, a.sm_omega[0]);
             std::swap(cur, nxt);
         } else {
-            vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.sm_omega[0], cur + o, st);  // step 0 from x = 0
+            if (!(l == 0 && l0_x1_ready && b == r.p))  // (else formed by the previous x / r update)
+                vec_jacobi0<T>(cn, a.dinv.p + o, b + o, a.sm_omega[0], cur + o, st);  // step 0 from x = 0
+            if (l == 0) l0_x1_ready = false;
             for (int sw = 1; sw < nu; ++sw) {  // x_{sw+1} over x_{sw-1} (x_0 = 0: no xprev)
                 pass(l, PASS_JACOBI, cur, b, nxt, nullptr, a.sm_omega[sw], a.sm_alpha[sw], sw == 1 ? nullptr : nxt);
                 std::swap(cur, nxt);
@@ -1249,8 +1256,11 @@ class Engine : public EngineBase {
                 pcg_commit_pq(dsc.p + 2, scal.p, k, flags.p, tag, st);
                 pcg_update_xr<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, st);
             } else {
+                // the next iteration's V-cycle starts with x1 = omega_0 D^-1 r: formed here from the new r
+                const bool x1 = k + 1 < iters && x1_fusable();
                 pcg_update_xr_fin<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, parts1.p, l0_nparts(),
-                                     flags.p, tag, st);
+                                     flags.p, tag, st, l0.dinv.p + o, l0.sm_omega[0], x1 ? l0.vx.p + o : nullptr);
+                l0_x1_ready = x1;
             }
         }
     }

@@ -738,14 +738,15 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
 template <class T, bool V>
 __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
                              T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
-                             int np, int* flags, int tag) {
+                             int np, int* flags, int tag, const T* __restrict__ dinv, double om0, T* __restrict__ x1) {
     if (scal[SC_DONE] != 0.0) return;
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
     const int64_t ci = blockIdx.x * (int64_t)PB + threadIdx.x;
-    T xv[W], pv[W], rv[W], qv[W];
+    T xv[W], pv[W], rv[W], qv[W], dv[W];
     if (ci * W < n) {  // issued before the partial sums
         CK::ld(x, ci, n, xv); CK::ld(p, ci, n, pv); CK::ld(r, ci, n, rv); CK::ld(q, ci, n, qv);
+        if (x1) CK::ld(dinv, ci, n, dv);
     }
     __shared__ double sh[32];
     __shared__ double pq_s;
@@ -770,6 +771,11 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
     }
     CK::st(x, ci, n, xv);
     CK::st(r, ci, n, rv);
+    if (x1) {  // the next V-cycle's step 0 (k_jacobi0's expression on the new residual)
+#pragma unroll
+        for (int w = 0; w < W; ++w) dv[w] = (T)(om0 * (double)dv[w] * (double)rv[w]);
+        CK::st(x1, ci, n, dv);
+    }
 }
 
 // One colour of a multicolour Gauss-Seidel sweep (reading c22): for the rows of colour c
@@ -1416,11 +1422,11 @@ void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const do
 }
 template <class T>
 void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
-                       int* flags, int tag, cudaStream_t s) {
-    if (al16(p) && al16(q) && al16(x) && al16(r))
-        k_pcg_xr_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag);
+                       int* flags, int tag, cudaStream_t s, const T* dinv, double om0, T* x1) {
+    if (al16(p) && al16(q) && al16(x) && al16(r) && (!x1 || (al16(x1) && al16(dinv))))
+        k_pcg_xr_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1);
     else
-        k_pcg_xr_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag);
+        k_pcg_xr_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1);
     MG_LAUNCH_CHECK();
 }
 template <class T>
@@ -1524,7 +1530,7 @@ void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s
     template void pcg_update_p_fin<T>(int32_t, const T*, T*, double*, int, const double*, const double*, int,  \
                                       int*, int, cudaStream_t);                                               \
     template void pcg_update_xr_fin<T>(int32_t, const T*, const T*, T*, T*, double*, int, const double*, int,  \
-                                       int*, int, cudaStream_t);                                              \
+                                       int*, int, cudaStream_t, const T*, double, T*);                        \
     template void dot_parts<T>(int32_t, const T*, const T*, double*, int, cudaStream_t);                       \
     template void scale_by_inv_sqrt<T>(int32_t, const T*, T*, const double*, cudaStream_t);                    \
     template void coarse_invert<T>(const Csr<T>&, double*, double*, int*, cudaStream_t);                       \
