@@ -697,11 +697,11 @@ class Engine : public EngineBase {
         for (int l = lcut; l < nL; ++l) {
             Level& a = *L[l];
             SubLevel<T>& c = subc.L[l - lcut];
-            c.n = a.n; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p;
+            c.n = a.n; c.nnz = (int32_t)a.nnz; c.rowptr = a.rowptr; c.col = a.col; c.val = a.val.p; c.dinv = a.dinv.p;
             for (int k = 0; k < 8; ++k) { c.om[k] = a.sm_omega[k]; c.al[k] = a.sm_alpha[k]; }
-            if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; }
+            if (l + 1 < nL) { c.agg = a.agg.p; c.P = a.P.p; c.mptr = a.mptr.p; c.mlist = a.mlist.p; c.n_next = a.n_agg; }
         }
-        if (!subcycle_plan<T>(subc, 200u * 1024u)) { lcut = -1; return; }
+        if (!subcycle_plan<T>(subc, 224u * 1024u)) { lcut = -1; return; }
         Mcut.resize((size_t)L[lcut]->n * L[lcut]->n);
         sub_ok = true;
     }

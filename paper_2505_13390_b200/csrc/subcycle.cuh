@@ -32,8 +32,11 @@ struct SubLevel {
     const T* P = nullptr;
     const int64_t* mptr = nullptr;
     const int32_t* mlist = nullptr;
+    int32_t nnz = 0, n_next = 0;   // entries; rows of the next level (= aggregates)
     // shared-memory element offsets (units of T, per column block) of this level's b and pre-smoothed x
     uint32_t o_b = 0, o_xs = 0;
+    // staged copies (byte offsets; SubCycle::staged): rowptr / mptr as int32, col, val, dinv, P, agg, mlist
+    uint32_t s_rp = 0, s_col = 0, s_val = 0, s_dinv = 0, s_P = 0, s_agg = 0, s_mp = 0, s_ml = 0;
 };
 
 template <class T>
@@ -43,6 +46,9 @@ struct SubCycle {
     const double* Ainv = nullptr; // coarsest inverse, row-major n_{K-1}^2
     uint32_t o_s0 = 0, o_s1 = 0, o_s2 = 0;  // three scratch vectors (max n each)
     uint32_t smem = 0;            // dynamic shared memory bytes per CTA
+    bool staged = false;          // the level CSR / P / aggregates / members and Ainv copied into shared memory
+    uint32_t s_ainv = 0;          // byte offset of the staged Ainv
+    uint32_t vec_bytes = 0;       // bytes of the vector section (offset of the staged data)
     SubLevel<T> L[SUB_MAXL];
 };
 
