@@ -157,7 +157,8 @@ class Engine : public EngineBase {
     bool have_hier = false;
     DBuf<double> Ainv, inv_work;
     DBuf<T> r, p, q, xs;
-    DBuf<double> scal, parts1, parts2, bn, B0, pw_v, pw_w, pw_ss;
+    DBuf<double> scal, parts1, parts2, bn, B0, pw_v, pw_w, pw_ss, mf_fin;
+    DBuf<unsigned> mf_fin_ctr;
     DBuf<int> flags;
     int32_t ncolours = 0;
     int64_t frame = 0;
@@ -219,6 +220,10 @@ class Engine : public EngineBase {
     int64_t omega_refreshes = 0;
     // level-0 x1 of the next V-cycle already formed by the PCG x / r update (one launch less per iteration)
     bool l0_x1_ready = false;
+    // the row kernel's last CTA sums the PCG dot partials (MatFree::fin) on this path
+    const double* fin_ready() const {
+        return (!dist && nL > 1 && mf_on() && mf.tma && mf.fin && cfg.smoother != 2) ? mf.fin : nullptr;
+    }
     bool x1_fusable() const {
         return !dist && nL > 1 && cfg.smoother != 2 && !fuse_jacobi0 && std::getenv("MGPBD_NO_X1_FUSE") == nullptr;
     }
@@ -412,6 +417,15 @@ class Engine : public EngineBase {
             mf.grid = std::min(mf.grid, c);
             mf.vg_grid_cap = c;
             if (mf64_ok) { mf64.grid = std::min(mf64.grid, c); mf64.vg_grid_cap = c; }
+        }
+        // opt-in (MGPBD_FIN_IN_ROWS=1): the row kernel's last CTA sums the PCG dot partials; measured 0.2 ms/frame
+        // slower (the arrival atomics lengthen every dot pass) than the redundant per-CTA sums of the update kernels
+        if (mf.tma && !dist && std::getenv("MGPBD_FIN_IN_ROWS") != nullptr) {
+            mf_fin.resize(4);
+            mf_fin_ctr.resize(1);
+            MG_CK(cudaMemsetAsync(mf_fin_ctr.p, 0, sizeof(unsigned), st));
+            mf.fin = mf_fin.p;
+            mf.fin_ctr = mf_fin_ctr.p;
         }
 
     }
@@ -781,7 +795,8 @@ class Engine : public EngineBase {
         tail_ok = false;
         fused_ok = false;
         const bool solo_ok = res_ok && res_plan.solo[0].n > 0;
-        if (ccyc_ok && res_ok && use_tail && !solo_ok) setup_tail();
+        // (the dense bottom of c27 leaves too little for a cluster tail to win: grid-only cycle)
+        if (ccyc_ok && res_ok && use_tail && !solo_ok && !sub_ok) setup_tail();
         if (tracing)
             std::fprintf(stderr, "[mgpbd trace] levels %d coarse kernel %s from level %d, smem %u B, solo from %d, tail %s\n", nL,
                          !ccyc_ok ? "off" : res_ok ? "resident" : "global", ccyc_from, res_ok ? res_plan.smem : 0u,
@@ -1245,7 +1260,7 @@ class Engine : public EngineBase {
                 pcg_commit_rz(dsc.p, scal.p, k, flags.p, tag, st);
                 pcg_update_p<T>(cn, z + o, p.p + o, scal.p, k, st);
             } else {
-                pcg_update_p_fin<T>(cn, z + o, p.p + o, scal.p, k, parts1.p, parts2.p, np, flags.p, tag, st);
+                pcg_update_p_fin<T>(cn, z + o, p.p + o, scal.p, k, parts1.p, parts2.p, np, flags.p, tag, st, fin_ready());
             }
             if (k == 0) mark_stage(8);
             pass(0, PASS_SPMV_DOT, p.p, nullptr, q.p, nullptr, 0.0);
@@ -1259,7 +1274,8 @@ class Engine : public EngineBase {
                 // the next iteration's V-cycle starts with x1 = omega_0 D^-1 r: formed here from the new r
                 const bool x1 = k + 1 < iters && x1_fusable();
                 pcg_update_xr_fin<T>(cn, p.p + o, q.p + o, xs.p + o, r.p + o, scal.p, k, parts1.p, l0_nparts(),
-                                     flags.p, tag, st, l0.dinv.p + o, l0.sm_omega[0], x1 ? l0.vx.p + o : nullptr);
+                                     flags.p, tag, st, l0.dinv.p + o, l0.sm_omega[0], x1 ? l0.vx.p + o : nullptr,
+                                     fin_ready());
                 l0_x1_ready = x1;
             }
         }

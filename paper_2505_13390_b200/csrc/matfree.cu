@@ -546,7 +546,8 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
                                                       const T* __restrict__ b, T* __restrict__ y,
                                                       const T* __restrict__ aux, double omega, double alpha,
                                                       const T* __restrict__ xprev, double* __restrict__ parts,
-                                                      double* __restrict__ parts2, double xom) {
+                                                      double* __restrict__ parts2, double xom, double* __restrict__ fin,
+                                                      unsigned* __restrict__ fin_ctr) {
     // xom != 0 (PASS_JACOBI only): x is not materialised, x_i = xom D^-1_ii b_i (see k_mf_vgather XJ)
     using LY = TileLayout<T, KC, V16>;
     constexpr int MF_RK = LY::R;
@@ -683,6 +684,30 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
             const double t2 = block_sum<MF_RK>(acc2, sh);
             if (threadIdx.x == 0) parts2[blockIdx.x] = t2;
         }
+        if ((MODE == PASS_JACOBI_DOT || MODE == PASS_SPMV_DOT) && fin) {
+            // the last CTA to arrive sums every CTA's partial in index order (deterministic) for the PCG update
+            __shared__ int last;
+            if (threadIdx.x == 0) {
+                __threadfence();
+                last = atomicAdd(fin_ctr, 1u) == gridDim.x - 1;
+            }
+            __syncthreads();
+            if (last) {
+                __threadfence();
+                double a = 0.0, c = 0.0;
+                for (int i = threadIdx.x; i < (int)gridDim.x; i += MF_RK) {
+                    a += __ldcg(parts + i);
+                    if (MODE == PASS_JACOBI_DOT) c += __ldcg(parts2 + i);
+                }
+                a = block_sum<MF_RK>(a, sh);
+                if (MODE == PASS_JACOBI_DOT) c = block_sum<MF_RK>(c, sh);
+                if (threadIdx.x == 0) {
+                    if (MODE == PASS_JACOBI_DOT) { fin[0] = a; fin[1] = c; }
+                    else fin[2] = a;
+                    *fin_ctr = 0u;
+                }
+            }
+        }
     }
 }
 
@@ -769,7 +794,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         MG_CK(cudaLaunchKernelEx(&lc, k_mf_rows_tma<T, KC, M, V16>, A.row0, A.row1, tbase, ntiles,              \
                                  V16 ? (const void*)A.v16 : (const void*)A.verts, A.vbase, A.h, u,              \
                                  (const T*)A.at, (const T*)A.dinv, x, b, y, aux, omega, alpha, xprev, parts,    \
-                                 parts2, xom));                                                                 \
+                                 parts2, xom, A.fin, A.fin_ctr));                                               \
     }
         switch (mode) {
             case PASS_JACOBI: MG_MFT(PASS_JACOBI); break;

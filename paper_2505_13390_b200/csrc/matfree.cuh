@@ -42,6 +42,10 @@ struct MatFree {
     int grid = 1;                   // CTAs of the row kernel = number of dot partials
     bool tma = false;               // TMA-pipelined row kernel (persistent CTAs, bulk copies)
     int vg_grid_cap = 0;            // > 0: cap on the vertex-gather grid (MGPBD_MF_GRID_CAP, tests only)
+    // != nullptr: the row kernel's last CTA also sums the dot partials (fixed order): JACOBI_DOT -> fin[0] (parts),
+    // fin[1] (parts2); SPMV_DOT -> fin[2]; fin_ctr = arrival counter (0 between launches)
+    double* fin = nullptr;
+    unsigned* fin_ctr = nullptr;
     // TMA row kernel: vertex ids as 16-bit offsets from a per-tile base (tiles of the kernel's tiling from
     // row0 & ~3) when every tile spans < 65536 vertices; nullptr = the 32-bit verts
     const uint16_t* v16 = nullptr;  // m x kc

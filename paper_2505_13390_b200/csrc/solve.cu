@@ -687,7 +687,7 @@ __global__ void k_pcg_xr(int32_t n, const T* __restrict__ p, const T* __restrict
 template <class T, bool V>
 __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ p, double* __restrict__ scal, int k,
                             const double* __restrict__ prz, const double* __restrict__ prr, int np, int* flags,
-                            int tag) {
+                            int tag, const double* __restrict__ fin) {
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
     const int64_t ci = blockIdx.x * (int64_t)PB + threadIdx.x;
@@ -696,9 +696,14 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
     __shared__ double sh[32];
     __shared__ double rz_s;
     double a = 0.0, c = 0.0;
-    for (int i = threadIdx.x; i < np; i += PB) { a += prz[i]; c += prr[i]; }
-    a = block_sum<PB>(a, sh);
-    c = block_sum<PB>(c, sh);
+    if (fin) {  // already summed by the producing row kernel's last CTA
+        a = fin[0];
+        c = fin[1];
+    } else {
+        for (int i = threadIdx.x; i < np; i += PB) { a += prz[i]; c += prr[i]; }
+        a = block_sum<PB>(a, sh);
+        c = block_sum<PB>(c, sh);
+    }
     __shared__ int conv;
     if (threadIdx.x == 0) conv = pcg_converged(scal, k, c) ? 1 : 0;
     __syncthreads();
@@ -738,7 +743,8 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
 template <class T, bool V>
 __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
                              T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
-                             int np, int* flags, int tag, const T* __restrict__ dinv, double om0, T* __restrict__ x1) {
+                             int np, int* flags, int tag, const T* __restrict__ dinv, double om0, T* __restrict__ x1,
+                             const double* __restrict__ fin) {
     if (scal[SC_DONE] != 0.0) return;
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
@@ -751,8 +757,12 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
     __shared__ double sh[32];
     __shared__ double pq_s;
     double a = 0.0;
-    for (int i = threadIdx.x; i < np; i += PB) a += ppq[i];
-    a = block_sum<PB>(a, sh);
+    if (fin) {
+        a = fin[2];
+    } else {
+        for (int i = threadIdx.x; i < np; i += PB) a += ppq[i];
+        a = block_sum<PB>(a, sh);
+    }
     if (threadIdx.x == 0) {
         pq_s = a;
         if (blockIdx.x == 0) {
@@ -1412,21 +1422,21 @@ void pcg_update_p(int32_t n, const T* z, T* p, const double* scal, int k, cudaSt
 }
 template <class T>
 void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const double* prz, const double* prr, int np,
-                      int* flags, int tag, cudaStream_t s) {
+                      int* flags, int tag, cudaStream_t s, const double* fin) {
     // every CTA must run (CTA 0 publishes the scalars even for n = 0): the grid covers at least one chunk
     if (al16(z) && al16(p))
-        k_pcg_p_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag);
+        k_pcg_p_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
     else
-        k_pcg_p_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag);
+        k_pcg_p_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
     MG_LAUNCH_CHECK();
 }
 template <class T>
 void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
-                       int* flags, int tag, cudaStream_t s, const T* dinv, double om0, T* x1) {
+                       int* flags, int tag, cudaStream_t s, const T* dinv, double om0, T* x1, const double* fin) {
     if (al16(p) && al16(q) && al16(x) && al16(r) && (!x1 || (al16(x1) && al16(dinv))))
-        k_pcg_xr_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1);
+        k_pcg_xr_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
     else
-        k_pcg_xr_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1);
+        k_pcg_xr_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
     MG_LAUNCH_CHECK();
 }
 template <class T>
@@ -1528,9 +1538,9 @@ void coarse_gemv(int32_t n, const double* Ainv, const T* b, T* x, cudaStream_t s
     template void gs_sweep<T>(const Csr<T>&, const int64_t*, const int32_t*, int, bool, const T*, T*, cudaStream_t); \
     template void pcg_update_xr<T>(int32_t, const T*, const T*, T*, T*, const double*, int, cudaStream_t);     \
     template void pcg_update_p_fin<T>(int32_t, const T*, T*, double*, int, const double*, const double*, int,  \
-                                      int*, int, cudaStream_t);                                               \
+                                      int*, int, cudaStream_t, const double*);                                \
     template void pcg_update_xr_fin<T>(int32_t, const T*, const T*, T*, T*, double*, int, const double*, int,  \
-                                       int*, int, cudaStream_t, const T*, double, T*);                        \
+                                       int*, int, cudaStream_t, const T*, double, T*, const double*);         \
     template void dot_parts<T>(int32_t, const T*, const T*, double*, int, cudaStream_t);                       \
     template void scale_by_inv_sqrt<T>(int32_t, const T*, T*, const double*, cudaStream_t);                    \
     template void coarse_invert<T>(const Csr<T>&, double*, double*, int*, cudaStream_t);                       \

@@ -88,10 +88,12 @@ void gs_sweep(const Csr<T>& A, const int64_t* gs_ptr, const int32_t* gs_list, in
 // pcg_finalize_* + pcg_update_* pairs)
 template <class T>
 void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const double* prz, const double* prr, int np,
-                      int* flags, int tag, cudaStream_t s);
+                      int* flags, int tag, cudaStream_t s, const double* fin = nullptr);
 template <class T>
 void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
-                       int* flags, int tag, cudaStream_t s, const T* dinv = nullptr, double om0 = 0.0, T* x1 = nullptr);
+                       int* flags, int tag, cudaStream_t s, const T* dinv = nullptr, double om0 = 0.0, T* x1 = nullptr,
+                       const double* fin = nullptr);
+// (fin != nullptr: the partial sums were already summed by the producing matrix-free row kernel, MatFree::fin)
 // (x1 != nullptr: also x1 = om0 D^-1 r_new, the next V-cycle's first smoothing step from x = 0)
 // alpha = rz[k]/pq[k] (0 if pq == 0); x += alpha p; r -= alpha q
 template <class T> void pcg_update_xr(int32_t n, const T* p, const T* q, T* x, T* r, const double* scal, int k,
