@@ -220,6 +220,7 @@ class Engine : public EngineBase {
     int64_t omega_refreshes = 0;
     // level-0 x1 of the next V-cycle already formed by the PCG x / r update (one launch less per iteration)
     bool l0_x1_ready = false;
+    bool vc_trace = false;  // stage stamps inside the first level-0 V-cycle of an iteration (MGPBD_TRACE_STAGES)
     // the row kernel's last CTA sums the PCG dot partials (MatFree::fin) on this path
     const double* fin_ready() const {
         return (!dist && nL > 1 && mf_on() && mf.tma && mf.fin && cfg.smoother != 2) ? mf.fin : nullptr;
@@ -392,6 +393,7 @@ class Engine : public EngineBase {
             mf64_ok = true;
         }
         mf.tma = std::getenv("MGPBD_NO_TMA") == nullptr;
+        mf.vg_pdl = std::getenv("MGPBD_NO_VG_PDL") == nullptr;  // 94.77 -> 94.64 ms/frame (tools/ab_frames.py)
         int vbytes = 4;
         if (mf.tma && !std::getenv("MGPBD_NO_V16")) {  // 16-bit vertex offsets per TMA tile (8 B per row saved)
             std::vector<int32_t> hvt((size_t)m * kc);
@@ -1207,6 +1209,7 @@ class Engine : public EngineBase {
                 std::swap(cur, nxt);
             }
         }
+        if (l == 0 && vc_trace) mark_stage(10);
         Level& c = *L[l + 1];
         if (a.kk > 1) {  // general P (k > 1): r = b - A x, b_c = P^T r, x += P e
             pass(l, PASS_RESID_P, cur, b, a.vt.p, a.kones.p, 0.0);
@@ -1215,10 +1218,14 @@ class Engine : public EngineBase {
             kprolong<T>(o, cn, a.kp.pptr.p, a.kp.pcol.p, a.kpval.p, c.vz.p, cur, st);
         } else {
             pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
+            if (l == 0 && vc_trace) mark_stage(11);
             restrict_members<T>(a.n_agg, a.mptr.p, a.mlist.p, a.vt.p, c.vb.p, st);
             if (l == 0 && dist) comm->allreduce(c.vb.p, (size_t)c.n, st);  // partial sums of split aggregates
+            if (l == 0 && vc_trace) mark_stage(12);
             vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+            if (l == 0 && vc_trace) mark_stage(13);
             prolong_add<T>(cn, a.agg.p + o, a.P.p + o, c.vz.p, cur + o, st);
+            if (l == 0 && vc_trace) mark_stage(14);
         }
         for (int sw = 0; sw < nu; ++sw) {
             const bool last = sw == nu - 1;
@@ -1227,6 +1234,7 @@ class Engine : public EngineBase {
             const T* xprev = sw == 0 ? nullptr : other;
             if (last && dot_r) pass(l, PASS_JACOBI_DOT, cur, b, dst, dot_r, a.sm_omega[sw], a.sm_alpha[sw], xprev);
             else pass(l, PASS_JACOBI, cur, b, dst, nullptr, a.sm_omega[sw], a.sm_alpha[sw], xprev);
+            if (l == 0 && vc_trace) mark_stage(15 + std::min(sw, 1));
             cur = dst;
         }
     }
@@ -1249,7 +1257,9 @@ class Engine : public EngineBase {
                 dot_parts<T>(m, r.p, r.p, parts2.p, l0.grid, st);
             } else {
                 if (k == 0) mark_stage(6);
+                vc_trace = k == 0 && trace_stages;
                 timed(PH_VC, [&] { vcycle(0, r.p, z, r.p); });
+                vc_trace = false;
                 if (k == 0) mark_stage(7);
             }
             const int np = nL == 1 ? l0.grid : l0_nparts();
@@ -1278,6 +1288,7 @@ class Engine : public EngineBase {
                                      fin_ready());
                 l0_x1_ready = x1;
             }
+            if (k == 0) mark_stage(17);
         }
     }
 
@@ -1438,14 +1449,19 @@ class Engine : public EngineBase {
         MG_CK(cudaStreamSynchronize(st));
         launches_last = g_kernel_launches;
         if (trace_stages && stamps.n) {  // stage times of the last outer iteration
-            unsigned long long tt[10];
-            d2h(tt, stamps.p, 10, st);
+            unsigned long long tt[18];
+            d2h(tt, stamps.p, 18, st);
             MG_CK(cudaStreamSynchronize(st));
             auto us = [&](int a, int b) { return (double)(tt[b] - tt[a]) * 1e-3; };
             std::fprintf(stderr,
                          "[mgpbd stages] refresh: VA %.1f levels %.1f coarsest-inverse %.1f | pcg %.1f (first "
-                         "iteration: V-cycle %.1f, p-update %.1f, SpMV %.1f) | update %.1f us\n",
-                         us(0, 1), us(1, 2), us(2, 3), us(3, 4), us(6, 7), us(7, 8), us(8, 9), us(4, 5));
+                         "iteration: V-cycle %.1f, p-update %.1f, SpMV %.1f, x/r-update %.1f) | update %.1f us\n",
+                         us(0, 1), us(1, 2), us(2, 3), us(3, 4), us(6, 7), us(7, 8), us(8, 9), us(9, 17), us(4, 5));
+            if (tt[10] && tt[16])
+                std::fprintf(stderr,
+                             "[mgpbd stages] level-0 V-cycle: pre-smoothing %.1f, residual %.1f, restriction %.1f, coarse "
+                             "levels %.1f, prolongation %.1f, post step 1 %.1f, post step 2 %.1f us\n",
+                             us(6, 10), us(10, 11), us(11, 12), us(12, 13), us(13, 14), us(14, 15), us(15, 16));
         }
         if (ccyc.trace) {  // phase times of the last coarse V-cycle (MGPBD_TRACE_COARSE)
             unsigned long long tt[128];

@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
         if (vv < vend) { p0n = ppos[vv]; p1n = ppos[vv + 1]; jbn = J16 ? jbase[vv] : 0; }
     };
     if (MGPBD_VG_PREFETCH) fetch(first + sub);
+    // launched with programmatic dependent launch (MatFree::vg_pdl): everything above reads static data; x is
+    // the previous kernel's output (no-op otherwise)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (int64_t base = first; base < vend; base += step) {  // warp-uniform
         const int64_t v = base + sub;
         using AC = typename std::conditional<MGPBD_VG_ACC64 != 0, double, T>::type;
@@ -671,6 +674,7 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         }
         __syncthreads();  // every thread is done with this stage: refill it
         if (t == 0 && j + MF_STAGES < my_tiles) issue(j + MF_STAGES);
+        if (j + 1 == my_tiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // last tile done
         if (MGPBD_ROWS_PIPE) {
 #pragma unroll
             for (int k = 0; k < KC; ++k) uc[k] = un[k];
@@ -763,8 +767,20 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
             }
         } else {
 #define MG_VG(J, X)                                                                                     \
-    k_mf_vgather<T, G, UN, J, X><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, \
-                                                        x, reinterpret_cast<V4<T>*>(A.u), A.dinv, b, xom, vg_sms())
+    do {                                                                                                \
+        cudaLaunchConfig_t lc = {};                                                                     \
+        lc.gridDim = dim3(grid);                                                                        \
+        lc.blockDim = dim3(MF_BS);                                                                      \
+        lc.stream = s;                                                                                  \
+        cudaLaunchAttribute la[1];                                                                      \
+        la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                  \
+        la[0].val.programmaticStreamSerializationAllowed = 1;                                           \
+        lc.attrs = la;                                                                                  \
+        lc.numAttrs = A.vg_pdl ? 1 : 0;                                                                 \
+        MG_CK(cudaLaunchKernelEx(&lc, k_mf_vgather<T, G, UN, J, X>, A.v0, A.v1, A.npad, A.ppos, A.vj16, \
+                                 A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u), (const T*)A.dinv, \
+                                 b, xom, vg_sms()));                                                    \
+    } while (0)
             if (A.vj16) { if (xom != 0.0) MG_VG(true, true); else MG_VG(true, false); }
             else { if (xom != 0.0) MG_VG(false, true); else MG_VG(false, false); }
 #undef MG_VG

@@ -44,6 +44,7 @@ struct MatFree {
     int vg_grid_cap = 0;            // > 0: cap on the vertex-gather grid (MGPBD_MF_GRID_CAP, tests only)
     // != nullptr: the row kernel's last CTA also sums the dot partials (fixed order): JACOBI_DOT -> fin[0] (parts),
     // fin[1] (parts2); SPMV_DOT -> fin[2]; fin_ctr = arrival counter (0 between launches)
+    bool vg_pdl = false;            // vertex gather launched with programmatic dependent launch (MGPBD_VG_PDL)
     double* fin = nullptr;
     unsigned* fin_ctr = nullptr;
     // TMA row kernel: vertex ids as 16-bit offsets from a per-tile base (tiles of the kernel's tiling from

@@ -569,9 +569,14 @@ struct Chunk16 {
 };
 inline bool al16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 template <class T, bool V>
-inline int chunk_grid(int64_t n) {
+inline int chunk_grid(int64_t n, int cpt = 1) {
     const int64_t items = (n + Chunk16<T, V>::W - 1) / Chunk16<T, V>::W;
-    return (int)std::max<int64_t>(1, (items + PB - 1) / PB);
+    return (int)std::max<int64_t>(1, (items + (int64_t)PB * cpt - 1) / ((int64_t)PB * cpt));
+}
+// chunks per thread of the PCG update kernels (MGPBD_VEC_CPT: 1 or 4)
+inline int vec_cpt() {
+    static const int c = std::getenv("MGPBD_VEC_CPT") ? std::atoi(std::getenv("MGPBD_VEC_CPT")) : 4;
+    return c == 1 ? 1 : 4;
 }
 
 template <class T, bool V>
@@ -589,10 +594,10 @@ __global__ void k_jacobi0(int32_t n, const T* __restrict__ dinv, const T* __rest
 
 // bc[a] = sum_{i in a, ascending} t[i]: 8 lanes per aggregate, each lane's members in chunks of 4 with
 // all list loads issued before the t gathers; lane partials + fixed-order butterfly (deterministic)
-template <class T>
+template <class T, int G>
 __global__ void k_restrict(int32_t nc, const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
                            const T* __restrict__ t, T* __restrict__ bc) {
-    constexpr int G = 8, PER = 32 / G, UN = 4;
+    constexpr int PER = 32 / G, UN = 4;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -684,15 +689,20 @@ __global__ void k_pcg_xr(int32_t n, const T* __restrict__ p, const T* __restrict
 // Finalisation of <r,z> (and <r,r>) fused into the p update: every CTA reduces the partials in the same
 // fixed order (identical value everywhere), CTA 0 publishes the scalar and raises the flags of
 // k_fin_rz; saves one launch per PCG iteration.
-template <class T, bool V>
+template <class T, bool V, int CPT>
 __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ p, double* __restrict__ scal, int k,
                             const double* __restrict__ prz, const double* __restrict__ prr, int np, int* flags,
                             int tag, const double* __restrict__ fin) {
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
-    const int64_t ci = blockIdx.x * (int64_t)PB + threadIdx.x;
-    T zv[W], pv[W];
-    if (ci * W < n) { CK::ld(z, ci, n, zv); CK::ld(p, ci, n, pv); }  // issued before the partial sums
+    // CPT chunks per thread (chunk c of the block strided by PB: coalesced), all loaded before the partial sums,
+    // which every CTA reduces redundantly (fewer CTAs: less of that L2 traffic)
+    T zv[CPT][W], pv[CPT][W];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        const int64_t ci = ((int64_t)blockIdx.x * CPT + c) * PB + threadIdx.x;
+        if (ci * W < n) { CK::ld(z, ci, n, zv[c]); CK::ld(p, ci, n, pv[c]); }
+    }
     __shared__ double sh[32];
     __shared__ double rz_s;
     double a = 0.0, c = 0.0;
@@ -733,14 +743,18 @@ __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ 
         const double prev = scal[2 * (k - 1)];
         beta = prev != 0.0 ? rz_s / prev : 0.0;
     }
-    if (ci * W >= n) return;
 #pragma unroll
-    for (int w = 0; w < W; ++w) pv[w] = (T)((double)zv[w] + beta * (double)pv[w]);
-    CK::st(p, ci, n, pv);
+    for (int c = 0; c < CPT; ++c) {
+        const int64_t ci = ((int64_t)blockIdx.x * CPT + c) * PB + threadIdx.x;
+        if (ci * W >= n) break;
+#pragma unroll
+        for (int w = 0; w < W; ++w) pv[c][w] = (T)((double)zv[c][w] + beta * (double)pv[c][w]);
+        CK::st(p, ci, n, pv[c]);
+    }
 }
 
 // <p,q> finalisation fused into the x / r update (see k_pcg_p_fin)
-template <class T, bool V>
+template <class T, bool V, int CPT>
 __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __restrict__ q, T* __restrict__ x,
                              T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
                              int np, int* flags, int tag, const T* __restrict__ dinv, double om0, T* __restrict__ x1,
@@ -748,11 +762,14 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
     if (scal[SC_DONE] != 0.0) return;
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
-    const int64_t ci = blockIdx.x * (int64_t)PB + threadIdx.x;
-    T xv[W], pv[W], rv[W], qv[W], dv[W];
-    if (ci * W < n) {  // issued before the partial sums
-        CK::ld(x, ci, n, xv); CK::ld(p, ci, n, pv); CK::ld(r, ci, n, rv); CK::ld(q, ci, n, qv);
-        if (x1) CK::ld(dinv, ci, n, dv);
+    T xv[CPT][W], pv[CPT][W], rv[CPT][W], qv[CPT][W], dv[CPT][W];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {  // issued before the partial sums
+        const int64_t ci = ((int64_t)blockIdx.x * CPT + c) * PB + threadIdx.x;
+        if (ci * W < n) {
+            CK::ld(x, ci, n, xv[c]); CK::ld(p, ci, n, pv[c]); CK::ld(r, ci, n, rv[c]); CK::ld(q, ci, n, qv[c]);
+            if (x1) CK::ld(dinv, ci, n, dv[c]);
+        }
     }
     __shared__ double sh[32];
     __shared__ double pq_s;
@@ -773,18 +790,22 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
     }
     __syncthreads();
     const double alpha = pq_s != 0.0 ? scal[2 * k] / pq_s : 0.0;
-    if (ci * W >= n) return;
 #pragma unroll
-    for (int w = 0; w < W; ++w) {
-        xv[w] = (T)((double)xv[w] + alpha * (double)pv[w]);
-        rv[w] = (T)((double)rv[w] - alpha * (double)qv[w]);
-    }
-    CK::st(x, ci, n, xv);
-    CK::st(r, ci, n, rv);
-    if (x1) {  // the next V-cycle's step 0 (k_jacobi0's expression on the new residual)
+    for (int c = 0; c < CPT; ++c) {
+        const int64_t ci = ((int64_t)blockIdx.x * CPT + c) * PB + threadIdx.x;
+        if (ci * W >= n) break;
 #pragma unroll
-        for (int w = 0; w < W; ++w) dv[w] = (T)(om0 * (double)dv[w] * (double)rv[w]);
-        CK::st(x1, ci, n, dv);
+        for (int w = 0; w < W; ++w) {
+            xv[c][w] = (T)((double)xv[c][w] + alpha * (double)pv[c][w]);
+            rv[c][w] = (T)((double)rv[c][w] - alpha * (double)qv[c][w]);
+        }
+        CK::st(x, ci, n, xv[c]);
+        CK::st(r, ci, n, rv[c]);
+        if (x1) {  // the next V-cycle's step 0 (k_jacobi0's expression on the new residual)
+#pragma unroll
+            for (int w = 0; w < W; ++w) dv[c][w] = (T)(om0 * (double)dv[c][w] * (double)rv[c][w]);
+            CK::st(x1, ci, n, dv[c]);
+        }
     }
 }
 
@@ -1393,7 +1414,7 @@ template <class T>
 void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, const T* t, T* bc, cudaStream_t s) {
     if (!nc) return;
     int g = (int)std::min<int64_t>(((int64_t)nc * 32 + PB - 1) / PB, 148 * 8);
-    k_restrict<T><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
+    k_restrict<T, 8><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
     MG_LAUNCH_CHECK();
 }
 template <class T>
@@ -1424,19 +1445,27 @@ template <class T>
 void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const double* prz, const double* prr, int np,
                       int* flags, int tag, cudaStream_t s, const double* fin) {
     // every CTA must run (CTA 0 publishes the scalars even for n = 0): the grid covers at least one chunk
-    if (al16(z) && al16(p))
-        k_pcg_p_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
-    else
-        k_pcg_p_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
+    const int cpt = vec_cpt();
+    if (al16(z) && al16(p)) {
+        if (cpt == 4) k_pcg_p_fin<T, true, 4><<<chunk_grid<T, true>(n, 4), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
+        else k_pcg_p_fin<T, true, 1><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
+    } else {
+        k_pcg_p_fin<T, false, 1><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
+    }
     MG_LAUNCH_CHECK();
 }
 template <class T>
 void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* scal, int k, const double* ppq, int np,
                        int* flags, int tag, cudaStream_t s, const T* dinv, double om0, T* x1, const double* fin) {
-    if (al16(p) && al16(q) && al16(x) && al16(r) && (!x1 || (al16(x1) && al16(dinv))))
-        k_pcg_xr_fin<T, true><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
-    else
-        k_pcg_xr_fin<T, false><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
+    const int cpt = vec_cpt();
+    if (al16(p) && al16(q) && al16(x) && al16(r) && (!x1 || (al16(x1) && al16(dinv)))) {
+        if (cpt == 4)
+            k_pcg_xr_fin<T, true, 4><<<chunk_grid<T, true>(n, 4), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
+        else
+            k_pcg_xr_fin<T, true, 1><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
+    } else {
+        k_pcg_xr_fin<T, false, 1><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
+    }
     MG_LAUNCH_CHECK();
 }
 template <class T>
