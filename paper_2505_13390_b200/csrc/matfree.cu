@@ -152,6 +152,32 @@ struct Chunk {
 #ifndef MGPBD_VG_BLOCKED
 #define MGPBD_VG_BLOCKED 2
 #endif
+// Vertices of the calling warp over [v0, v1): base = first, first + step, ... < vend (MGPBD_VG_BLOCKED: one
+// contiguous range per CTA of a persistent grid, see k_mf_vgather; else grid-stride)
+struct VRange {
+    int64_t first, step, vend;
+};
+template <int PER_WARP>
+__device__ __forceinline__ VRange warp_vertices(int32_t v0, int32_t v1, int nsm) {
+    VRange r;
+    if (MGPBD_VG_BLOCKED) {
+        const int S = gridDim.x < (unsigned)nsm ? (int)gridDim.x : nsm;
+        const int per = (int)gridDim.x / S;
+        const int c = MGPBD_VG_BLOCKED == 2 ? (int)blockIdx.x : (int)(blockIdx.x % S) * per + (int)(blockIdx.x / S);
+        const int64_t wpc = blockDim.x >> 5;
+        const int64_t chunk = ((v1 - v0 + (int64_t)gridDim.x - 1) / gridDim.x + wpc * PER_WARP - 1) / (wpc * PER_WARP) * (wpc * PER_WARP);
+        const int64_t cs = v0 + (int64_t)c * chunk;
+        r.vend = cs + chunk < v1 ? cs + chunk : v1;
+        r.first = cs + (int64_t)(threadIdx.x >> 5) * PER_WARP;
+        r.step = wpc * PER_WARP;
+    } else {
+        const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+        r.first = v0 + warp * PER_WARP;
+        r.step = (((int64_t)gridDim.x * blockDim.x) >> 5) * PER_WARP;
+        r.vend = v1;
+    }
+    return r;
+}
 inline int vg_sms() {
     static const int n = [] {
         int dev = 0, sms = 148;
@@ -187,24 +213,8 @@ __global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0,
     // (MGPBD_VG_BLOCKED, persistent grid) one contiguous range per CTA, the CTAs resident on one SM holding
     // adjacent ranges (CTA i runs on SM i mod S), so an SM sweeps ~n_v / S consecutive vertices and the x values
     // of the constraints between two vertex planes are reused from its L1
-    int64_t first, step, vend;
-    if (MGPBD_VG_BLOCKED) {
-        const int S = gridDim.x < (unsigned)nsm ? (int)gridDim.x : nsm;
-        const int per = (int)gridDim.x / S;
-        const int r = MGPBD_VG_BLOCKED == 2 ? (int)blockIdx.x : (int)(blockIdx.x % S) * per + (int)(blockIdx.x / S);
-        const int64_t wpc = blockDim.x >> 5;
-        const int64_t chunk = ((v1 - v0 + (int64_t)gridDim.x - 1) / gridDim.x + wpc * PER_WARP - 1) / (wpc * PER_WARP) * (wpc * PER_WARP);
-        const int64_t cs = v0 + (int64_t)r * chunk;
-        vend = cs + chunk < v1 ? cs + chunk : v1;
-        first = cs + (int64_t)(threadIdx.x >> 5) * PER_WARP;
-        step = wpc * PER_WARP;
-    } else {
-        const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-        const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-        first = v0 + warp * PER_WARP;
-        step = nwarps * PER_WARP;
-        vend = v1;
-    }
+    const VRange vr = warp_vertices<PER_WARP>(v0, v1, nsm);
+    const int64_t first = vr.first, step = vr.step, vend = vr.vend;
     const T* __restrict__ hx = hv;
     const T* __restrict__ hy = hv + npad;
     const T* __restrict__ hz = hv + 2 * npad;
@@ -405,20 +415,19 @@ __global__ void __launch_bounds__(MF_BS) k_mf_update(int32_t v0, int32_t v1, int
                                                      const int32_t* __restrict__ vj32,
                                                      const int32_t* __restrict__ jbase, const T* __restrict__ hv,
                                                      const T* __restrict__ dl, const double* __restrict__ sqrtw,
-                                                     const double* __restrict__ omega_p, double* __restrict__ x) {
+                                                     const double* __restrict__ omega_p, double* __restrict__ x, int nsm) {
     using CH = Chunk<T, J16>;
     constexpr int VW = CH::VW;
     constexpr int PER_WARP = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const VRange vr = warp_vertices<PER_WARP>(v0, v1, nsm);  // (the vertex gather's blocked ranges: dl reuse in L1)
     const T* __restrict__ hx = hv;
     const T* __restrict__ hy = hv + npad;
     const T* __restrict__ hz = hv + 2 * npad;
-    for (int64_t base = v0 + warp * PER_WARP; base < v1; base += nwarps * PER_WARP) {  // warp-uniform
+    for (int64_t base = vr.first; base < vr.vend; base += vr.step) {  // warp-uniform
         const int64_t v = base + sub;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        if (v < v1) {
+        if (v < vr.vend) {
             const int64_t p0 = ppos[v], p1 = ppos[v + 1];
             const int32_t jb = J16 ? jbase[v] : 0;
             for (int64_t pb = p0 + (int64_t)sl * VW; pb < p1; pb += (int64_t)G * VW * UN) {
@@ -446,7 +455,7 @@ __global__ void __launch_bounds__(MF_BS) k_mf_update(int32_t v0, int32_t v1, int
         a0 = group_sum<G>(a0);
         a1 = group_sum<G>(a1);
         a2 = group_sum<G>(a2);
-        if (v < v1 && sl == 0) {
+        if (v < vr.vend && sl == 0) {
             const double sw = sqrtw[v], om = *omega_p;
             x[3 * v] += om * (sw * a0);
             x[3 * v + 1] += om * (sw * a1);
@@ -919,19 +928,30 @@ void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const 
     else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom);
 }
 
+// grid of the vertex-major update: the resident CTAs only when the ranges are blocked (persistent), else grid-stride
+static int update_grid(const void* k, int64_t threads) {
+    int grid = (int)std::min<int64_t>((threads + MF_BS - 1) / MF_BS, 148 * 16);
+    if (MGPBD_VG_BLOCKED) {
+        int occ = 1;
+        MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, MF_BS, 0));
+        grid = (int)std::min<int64_t>((threads + MF_BS - 1) / MF_BS, (int64_t)vg_sms() * std::max(1, occ));
+    }
+    return std::max(grid, 1);
+}
+
 template <class T>
 void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const double* omega, double* x, cudaStream_t s) {
     if (A.v1 <= A.v0) return;
     if (A.kc == 4) {  // same lane split as the vertex gather (G = 4, UN = 2: ~60 registers)
         constexpr int G = 4;
-        const int grid = (int)std::min<int64_t>(((int64_t)(A.v1 - A.v0) * G + MF_BS - 1) / MF_BS, 148 * 16);
-        if (A.vj16) k_mf_update<T, G, 2, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
-        else k_mf_update<T, G, 2, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
+        const int grid = update_grid((const void*)k_mf_update<T, G, 2, true>, (int64_t)(A.v1 - A.v0) * G);
+        if (A.vj16) k_mf_update<T, G, 2, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
+        else k_mf_update<T, G, 2, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
     } else {
         constexpr int G = 2;
-        const int grid = (int)std::min<int64_t>(((int64_t)(A.v1 - A.v0) * G + MF_BS - 1) / MF_BS, 148 * 16);
-        if (A.vj16) k_mf_update<T, G, 1, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
-        else k_mf_update<T, G, 1, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x);
+        const int grid = update_grid((const void*)k_mf_update<T, G, 1, true>, (int64_t)(A.v1 - A.v0) * G);
+        if (A.vj16) k_mf_update<T, G, 1, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
+        else k_mf_update<T, G, 1, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
     }
     MG_LAUNCH_CHECK();
 }

@@ -247,13 +247,20 @@ __device__ bool polar_newton(const double F[9], double R[9]) {
         C[6] = X[1] * X[5] - X[2] * X[4]; C[7] = X[2] * X[3] - X[0] * X[5]; C[8] = X[0] * X[4] - X[1] * X[3];
         const double det = X[0] * C[0] + X[1] * C[1] + X[2] * C[2];
         if (!(det > 0.0)) return false;
-        double g = 1.0;
+        // X <- a X + c C.  Any a, c > 0 keep the polar factor of X (X = U H -> U (a H + c det H^-1)), so the
+        // scaled steps take g, a, c from single-precision norms (fast sqrt / divide): only the final unscaled
+        // steps, whose fixed point needs a + c det = 1 exactly, use the fp64 divide
+        double a = 0.5, c;
         if (scale) {
-            double nx = 0.0, nc = 0.0;
-            for (int k = 0; k < 9; ++k) { nx += X[k] * X[k]; nc += C[k] * C[k]; }
-            g = sqrt(sqrt(nc / (nx * det * det)));   // (||X^-1||_F / ||X||_F)^(1/2)
+            float nx = 0.0f, nc = 0.0f;
+            for (int k = 0; k < 9; ++k) { nx += (float)X[k] * (float)X[k]; nc += (float)C[k] * (float)C[k]; }
+            const float detf = (float)det;
+            const float g = sqrtf(sqrtf(nc / (nx * detf * detf)));   // (||X^-1||_F / ||X||_F)^(1/2)
+            a = 0.5 * (double)g;
+            c = (double)(0.5f / (g * detf));
+        } else {
+            c = 0.5 / det;
         }
-        const double a = 0.5 * g, c = 0.5 / (g * det);
         double d2 = 0.0, n2 = 0.0;
         for (int k = 0; k < 9; ++k) {
             const double xn = a * X[k] + c * C[k];
