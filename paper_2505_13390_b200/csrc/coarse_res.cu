@@ -275,6 +275,11 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
     __shared__ ResLevel slv[16];  // this CTA's slice descriptors (read after every barrier)
     const Lanes w;
     const int cta = blockIdx.x;
+    if (c.trace && blockIdx.x == 0 && threadIdx.x == 0) {  // kernel entry (before the shared-memory staging)
+        unsigned long long t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        c.trace[96 + (mode == 2 ? 2 : 0)] = t0;
+    }
     {
         const int* src = reinterpret_cast<const int*>(&c);
         int* dst = reinterpret_cast<int*>(&sc);
@@ -294,6 +299,7 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
     // mode 3: the first cluster also stages its static tail data now, behind the grid levels' work
     if (mode == 3 && blockIdx.x < (unsigned)ta.CT) tail_detail::coarse_tail_load<T>(ta, smem + tail_base, tail_lv, tail_bar, tail_pbars);
     mbar_wait(&bar, 0);
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // (PDL launch: the previous kernel's b is complete)
     int tix = 0;
     auto mark = [&]() {
         if (c.trace && blockIdx.x == 0 && threadIdx.x == 0 && tix < 64) {
@@ -536,14 +542,26 @@ void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_
     cfg.blockDim = dim3(RB);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr_[2];
+    cudaLaunchAttribute attr_[3];
     attr_[0].id = cudaLaunchAttributeCooperative;
     attr_[0].val.cooperative = 1;
-    attr_[1].id = cudaLaunchAttributeClusterDimension;
-    attr_[1].val.clusterDim.x = mode == 3 ? (unsigned)tail->CT : 1u;
-    attr_[1].val.clusterDim.y = 1; attr_[1].val.clusterDim.z = 1;
+    int na = 1;
+    if (mode == 3) {
+        attr_[na].id = cudaLaunchAttributeClusterDimension;
+        attr_[na].val.clusterDim.x = (unsigned)tail->CT;
+        attr_[na].val.clusterDim.y = 1; attr_[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    // programmatic dependent launch (MGPBD_COARSE_PDL): the CTAs stage their static slices while the preceding
+    // kernel (the level-0 restriction) finishes; griddepcontrol.wait precedes the first read of b
+    static const bool pdl = std::getenv("MGPBD_COARSE_PDL") != nullptr;
+    if (pdl && (mode == 0 || mode == 1 || mode == 3)) {
+        attr_[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr_[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
     cfg.attrs = attr_;
-    cfg.numAttrs = mode == 3 ? 2 : 1;
+    cfg.numAttrs = na;
     TailArgs<T> ta;
     if (tail) ta = *tail;
     MG_CK(cudaLaunchKernelEx(&cfg, k_coarse_vcycle_res<T>, c, plan, mode, kstop, ta, tail_base));

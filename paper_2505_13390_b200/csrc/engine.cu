@@ -1474,8 +1474,10 @@ class Engine : public EngineBase {
                 if (!p[0]) continue;
                 int nmark = 1;
                 while (nmark < 32 && p[nmark] >= p[nmark - 1] && p[nmark]) ++nmark;
-                std::fprintf(stderr, "[mgpbd coarse] K=%d %s (gap %.2f us, %.2f us total) phases (us):", ccyc.K, names[part],
-                             prev_end ? (double)(p[0] - prev_end) * 1e-3 : 0.0, (double)(p[nmark - 1] - p[0]) * 1e-3);
+                const unsigned long long entry = tt[96 + part];
+                std::fprintf(stderr, "[mgpbd coarse] K=%d %s (gap %.2f us, staging %.2f us, %.2f us total) phases (us):",
+                             ccyc.K, names[part], prev_end ? (double)(p[0] - prev_end) * 1e-3 : 0.0,
+                             entry && entry <= p[0] ? (double)(p[0] - entry) * 1e-3 : 0.0, (double)(p[nmark - 1] - p[0]) * 1e-3);
                 for (int k = 1; k < nmark; ++k) std::fprintf(stderr, " %.2f", (p[k] - p[k - 1]) * 1e-3);
                 std::fprintf(stderr, "\n");
                 prev_end = p[nmark - 1];

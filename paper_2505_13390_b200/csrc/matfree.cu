@@ -152,6 +152,13 @@ struct Chunk {
 #ifndef MGPBD_VG_BLOCKED
 #define MGPBD_VG_BLOCKED 2
 #endif
+// threads per CTA of the register vertex gather: fp32 one 1024-thread CTA per SM (its 32 warps share one contiguous
+// vertex range: 41.5 -> 40.6 us per pass), fp64 256 (its 3-chunk rounds need more than 64 registers)
+#ifndef MGPBD_VG_THREADS
+#define MGPBD_VG_THREADS 1024
+#endif
+template <class T>
+constexpr int vg_threads() { return sizeof(T) == 4 ? MGPBD_VG_THREADS : 256; }
 // Vertices of the calling warp over [v0, v1): base = first, first + step, ... < vend (MGPBD_VG_BLOCKED: one
 // contiguous range per CTA of a persistent grid, see k_mf_vgather; else grid-stride)
 struct VRange {
@@ -195,7 +202,7 @@ inline int vg_sms() {
 #define MGPBD_L2POL 0
 #endif
 template <class T, int G, int UN, bool J16, bool XJ>
-__global__ void __launch_bounds__(MF_BS, MGPBD_VG_MINB) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
+__global__ void __launch_bounds__(vg_threads<T>(), MGPBD_VG_MINB) k_mf_vgather(int32_t v0, int32_t v1, int64_t npad,
                                                       const int64_t* __restrict__ ppos,
                                                       const uint16_t* __restrict__ vj16,
                                                       const int32_t* __restrict__ vj32,
@@ -531,6 +538,9 @@ __global__ void __launch_bounds__(MF_BS, 2048 / MF_BS) k_mf_rows(int32_t row0, i
 #ifndef MGPBD_ROWS_PIPE
 #define MGPBD_ROWS_PIPE 1
 #endif
+#ifndef MGPBD_ROWS_TRIGGER
+#define MGPBD_ROWS_TRIGGER 0
+#endif
 #ifndef MGPBD_ROWS_BLOCKED
 #define MGPBD_ROWS_BLOCKED 1
 #endif
@@ -683,7 +693,9 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
         }
         __syncthreads();  // every thread is done with this stage: refill it
         if (t == 0 && j + MF_STAGES < my_tiles) issue(j + MF_STAGES);
-        if (j + 1 == my_tiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // last tile done
+        // dependents (the next pass's PDL vertex gather) may launch once this CTA's last tile is done
+        // (MGPBD_ROWS_TRIGGER=1; default 0: only at grid completion — the early trigger cost 3 us per back-to-back pass)
+        if (MGPBD_ROWS_TRIGGER && j + 1 == my_tiles) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
         if (MGPBD_ROWS_PIPE) {
 #pragma unroll
             for (int k = 0; k < KC; ++k) uc[k] = un[k];
@@ -748,14 +760,14 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #ifndef MGPBD_VG_CTAS_PER_SM
 #define MGPBD_VG_CTAS_PER_SM 16
 #endif
-        int grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, 148 * MGPBD_VG_CTAS_PER_SM);
+        int grid = (int)std::min<int64_t>((thr + vg_threads<T>() - 1) / vg_threads<T>(), 148 * MGPBD_VG_CTAS_PER_SM);
         if (MGPBD_VG_BLOCKED) {  // persistent: the resident CTAs only
             static const int resident = [] {
                 int occ = 1;
-                MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mf_vgather<T, G, UN, true, false>, MF_BS, 0));
+                MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_mf_vgather<T, G, UN, true, false>, vg_threads<T>(), 0));
                 return std::max(1, occ);
             }();
-            grid = (int)std::min<int64_t>((thr + MF_BS - 1) / MF_BS, (int64_t)vg_sms() * resident);
+            grid = (int)std::min<int64_t>((thr + vg_threads<T>() - 1) / vg_threads<T>(), (int64_t)vg_sms() * resident);
         }
         if (A.vg_grid_cap > 0) grid = std::min(grid, A.vg_grid_cap);
         if (A.vg_ts > 0) {  // TMA-pipelined vertex gather
@@ -779,7 +791,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
     do {                                                                                                \
         cudaLaunchConfig_t lc = {};                                                                     \
         lc.gridDim = dim3(grid);                                                                        \
-        lc.blockDim = dim3(MF_BS);                                                                      \
+        lc.blockDim = dim3(vg_threads<T>());                                                                 \
         lc.stream = s;                                                                                  \
         cudaLaunchAttribute la[1];                                                                      \
         la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                                  \

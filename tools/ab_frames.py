@@ -19,9 +19,12 @@ from paper_2505_13390_b200 import mgpbd, scenes
 sc = scenes.make(os.environ["AB_CONFIG"])
 ctx = mgpbd.Context.from_scene(sc, precision=1, setup_interval=1000, resetup_on_indef=0)
 ms = []
-for f in range(3 + int(os.environ["AB_FRAMES"])):
+rs = int(os.environ["AB_RESETUP"])
+for f in range(rs + 3 + int(os.environ["AB_FRAMES"])):
+    if rs and f == rs:
+        ctx.setup_hierarchy()   # hierarchy B (deterministic for one build: env variants compare on the same B)
     ctx.step(sc.dt, sc.n_iters)
-    if f >= 3:
+    if f >= rs + 3:
         ms.append(ctx.stats().ms_frame)
 st = ctx.stats()
 print(f"median {statistics.median(ms):.3f} ms/frame  min {min(ms):.3f}  levels {[st.n[l] for l in range(st.n_levels)]}", flush=True)
@@ -32,10 +35,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="block1.67M")
     ap.add_argument("--frames", type=int, default=8)
+    ap.add_argument("--resetup-at", type=int, default=0,
+                    help="re-setup before this frame (B-type hierarchy; identical across env variants of one build, "
+                         "not across builds)")
     ap.add_argument("variants", nargs="*")
     a = ap.parse_args()
     for var in a.variants or [""]:
-        env = dict(os.environ, AB_CONFIG=a.config, AB_FRAMES=str(a.frames))
+        env = dict(os.environ, AB_CONFIG=a.config, AB_FRAMES=str(a.frames), AB_RESETUP=str(a.resetup_at))
         for kv in var.split():
             k, v = kv.split("=", 1)
             env[k] = v
