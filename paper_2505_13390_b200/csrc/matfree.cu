@@ -912,7 +912,10 @@ int mf_grid_tma(int32_t row0, int32_t row1, int tsize, int kc, int vbytes) {
     const int R = mf_r(kc, tsize);
     const int64_t ntiles = std::max<int64_t>(1, ((int64_t)row1 - tbase + R - 1) / R);
     const size_t stage = (size_t)R * ((size_t)kc * 3 * tsize + (size_t)kc * vbytes + 6 * (size_t)tsize);
-    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(8, (227 * 1024) / (MF_STAGES * stage + 1024)));
+#ifndef MGPBD_ROWS_PER_SM
+#define MGPBD_ROWS_PER_SM 8
+#endif
+    const int per_sm = (int)std::max<size_t>(1, std::min<size_t>(MGPBD_ROWS_PER_SM, (227 * 1024) / (MF_STAGES * stage + 1024)));
     int dev = 0, sms = 148;
     MG_CK(cudaGetDevice(&dev));
     MG_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
