@@ -219,8 +219,10 @@ def run_ours(args):
         part = dict(rank=rank, world=world, nccl_id=obj[0])
     elif args.partitioned:
         part = dict(rank=0, world=1, nccl_id=mgpbd.nccl_unique_id())   # partitioned path, 1-rank NCCL
+    # k > 1: coarse DOFs shrink by ~k/aggregate size per level, the stall rule (c7) leaves a larger coarsest level
+    kx = dict(max_dense_coarse=8192) if args.k_nullspace > 1 else {}
     ctx = mgpbd.Context.from_scene(sc, precision=prec, device=local, stream=stream.cuda_stream, profile=0,
-                                   level0_operator=args.level0_operator, k_nullspace=args.k_nullspace, **part)
+                                   level0_operator=args.level0_operator, k_nullspace=args.k_nullspace, **part, **kx)
     for _ in range(args.warmup):
         ctx.step(sc.dt, sc.n_iters)
     st0 = ctx.stats()

@@ -91,7 +91,7 @@ typedef struct {
     uint64_t seed;            /* hash seed (reading c0), 1 */
     int32_t device;           /* CUDA device ordinal */
     void* stream;             /* cudaStream_t, NULL = context-owned stream */
-    int32_t max_dense_coarse; /* largest coarsest level inverted densely, 8192 */
+    int32_t max_dense_coarse; /* largest coarsest level inverted densely (default 2048; MGPBD_E_STALL above) */
     int32_t rank, world;      /* row partition of level 0 over `world` ranks, 0 <= rank < world */
     int32_t profile;          /* 1: record CUDA events around the level-0 matrix passes */
     const void* nccl_id;      /* world > 1: 128-byte ncclUniqueId shared by all ranks (mgpbd_nccl_unique_id on

@@ -1,5 +1,6 @@
 // k > 1 near-kernel setup and transfer kernels, see nullspace.cuh.
 #include <algorithm>
+#include <cstdint>
 #include <vector>
 
 #include "nullspace.cuh"
@@ -11,7 +12,9 @@ namespace {
 
 constexpr int KMAX = 8;
 
-inline int g1(int64_t n, int bs = 256) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, 148 * 64)); }
+// one thread per item (the kernels below are not grid-stride): the grid must cover every item — a cap here left
+// items beyond 148 x 64 x 256 uncomputed (k = 6 on blockslab32 and larger: garbage block Galerkin values)
+inline int g1(int64_t n, int bs = 256) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + bs - 1) / bs, INT32_MAX)); }
 
 // Warp per aggregate: MGS thin QR of the |N_a| x k block (members in mlist order = ascending node index),
 // one re-orthogonalisation pass, drop test |v_perp| <= tol |B_a[:,c]| (reading c24), zero block -> uniform

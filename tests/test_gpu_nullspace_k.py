@@ -103,3 +103,31 @@ def test_k_nullspace_argument_checks():
         mgpbd.Context.from_scene(sc, k_nullspace=9)
     with pytest.raises(mgpbd.MgpbdError):
         mgpbd.Context.from_scene(sc, k_nullspace=0)
+
+
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp64", "fp32"])
+def test_k6_block_galerkin_at_scale(precision):
+    """k = 6 on blockslab32 (393K rows: more level-0 Galerkin segments than 148 x 64 x 256 threads, the size at which
+    a capped one-thread-per-item grid once left part of the block product uncomputed): the device's level-1 block
+    operator equals the library product P^T A_0 P of the device's own A_0 and P (scipy), its diagonal is positive,
+    and frames run finite."""
+    import scipy.sparse as sp
+    sc = scenes.make("blockslab32")
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, k_nullspace=6)
+    ctx.debug_prepare(sc.dt)
+    r0, c0, v0 = ctx.level(0)
+    pr, pc, pv = ctx.prolongator_csr(0)
+    r1, c1, v1 = ctx.level(1)
+    n0, n1 = len(r0) - 1, len(r1) - 1
+    A0 = sp.csr_matrix((v0, c0, r0), shape=(n0, n0))
+    P = sp.csr_matrix((pv, pc, pr), shape=(n0, n1))
+    ref = (P.T @ A0 @ P).tocsr()
+    got = sp.csr_matrix((v1, c1, r1), shape=(n1, n1))
+    err = abs(got - ref).max() / abs(ref).max()
+    print(f"k=6 blockslab32 fp{'32' if precision else '64'}: n1 {n1}, |A1 - P^T A0 P| / max {err:.2e}")
+    assert err <= (1e-12 if precision == 0 else 2e-6)
+    assert (v1[r1[1:] - 1] > 0).all()
+    ctx.step(sc.dt, 2)
+    st = ctx.stats()
+    assert np.isfinite(st.b_norm[1])   # (the frame re-runs the setup on its own predicted state)
+    ctx.close()
