@@ -39,7 +39,7 @@ def test_gs_vcycle_pcg_identical_hierarchy(name, sweeps):
 
 # fp32 + GS on the squashed block: the GS update replaces x_i by a quotient of nearly cancelling
 # fp32-stored terms, and the frame deviates 2.2e-3 from fp64 (the GPU's own fp64 GS frame matches the
-# oracle to 1e-12); tools/debug_gs32.py measures it.  The omega-Jacobi default stays at ~1e-4.
+# oracle to 1e-12; the case below pins the 5e-3 bound).  The omega-Jacobi default stays at ~1e-4.
 CASES = [(n, 0, 1e-6) for n in ("cloth16", "cloth64", "bar3k", "block_small")] + \
         [(n, 1, 1e-3) for n in ("cloth16", "cloth64", "bar3k")] + [("block_small", 1, 5e-3)]
 

@@ -167,7 +167,7 @@ def test_virtual_ranks_match_single_gpu(name, world, precision):
     sc = scenes.make(name) if name != "cloth64" else scenes.cloth(64, dt=3e-3, n_iters=5)
     # fp64: three frames across a lazy re-setup, to rounding.  fp32: one frame at the whole-frame fp32
     # bound (1e-3); fp32 frames of the squashed block are chaotic in the rounding (single-GPU fp32 vs
-    # fp64 already differ by 1e-2 in lambda after two frames, tools/debug_prec.py), so later frames of
+    # fp64 already differ by 1e-2 in lambda after two frames; reading p1 in DESIGN.md), so later frames of
     # two fp32 runs with different summation orders are not comparable element-wise.
     frames = 3 if precision == 0 else 1
     ctx = mgpbd.Context.from_scene(sc, precision=precision, setup_interval=2)
