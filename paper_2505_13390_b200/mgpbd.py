@@ -251,8 +251,8 @@ class Context:
         self._ck(lib().mgpbd_get_positions(self.h, _p(out)))
         return out
 
-    def velocities(self):
-        out = np.empty((self.n, 3))
+    def velocities(self, out=None):
+        out = np.empty((self.n, 3)) if out is None else out
         self._ck(lib().mgpbd_get_velocities(self.h, _p(out)))
         return out
 
