@@ -271,6 +271,7 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
     cg::grid_group grid = cg::this_grid();
     extern __shared__ __align__(128) unsigned char smem[];
     __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar_late;
     __shared__ CoarseCycle<T> sc;
     __shared__ ResLevel slv[16];  // this CTA's slice descriptors (read after every barrier)
     const Lanes w;
@@ -289,11 +290,22 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
         for (int k = threadIdx.x; k < (int)(16 * sizeof(ResLevel) / sizeof(int)); k += blockDim.x) ld[k] = ls[k];
     }
     if (threadIdx.x == 0) {  // this CTA's slices of every level -> shared memory
+        // two completion barriers: the first cycle level's slices (bar) and the rest (bar_late, flagged by the
+        // plan in bit 31 of the byte count), so the first phases start before the deeper levels have landed
         mbar_init(&bar, 1);
+        mbar_init(&bar_late, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        mbar_expect_tx(&bar, plan.txbytes[cta]);
         const ResCopy* cp = plan.copies + (size_t)cta * RES_MAXC;
-        for (int k = 0; k < plan.ncopies[cta]; ++k) bulk_g2s(smem + cp[k].dst, cp[k].src, cp[k].bytes, &bar);
+        uint32_t early = 0, late = 0;
+        for (int k = 0; k < plan.ncopies[cta]; ++k) {
+            const uint32_t by = cp[k].bytes & RES_BYTES_MASK;
+            if (cp[k].bytes & RES_LATE) late += by;
+            else early += by;
+        }
+        mbar_expect_tx(&bar, early);
+        mbar_expect_tx(&bar_late, late);
+        for (int k = 0; k < plan.ncopies[cta]; ++k)
+            bulk_g2s(smem + cp[k].dst, cp[k].src, cp[k].bytes & RES_BYTES_MASK, (cp[k].bytes & RES_LATE) ? &bar_late : &bar);
     }
     __syncthreads();
     // mode 3: the first cluster also stages its static tail data now, behind the grid levels' work
@@ -316,8 +328,14 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
     const bool solo_on = mode == 0 && plan.solo[0].n > 0;   // cycle levels solo..K-1 on CTA 0 alone
     const int solo = solo_on ? plan.solo_first : 0;
     const int kdown = mode == 0 ? (solo_on ? solo : K - 1) : kstop;
+    bool late_ready = false;
+    auto wait_late = [&]() {
+        if (!late_ready) { mbar_wait(&bar_late, 0); late_ready = true; }
+    };
+    if (mode == 2) wait_late();
     // ---- down
     for (int k = 0; k < kdown && mode != 2; ++k) {
+        if (k == 1) wait_late();
         const CoarseLevel<T>& L = sc.L[k];
         const Slice<T> S = slice(k);
         const T* __restrict__ b = L.b;
@@ -349,6 +367,7 @@ __global__ void __launch_bounds__(RB, 1) k_coarse_vcycle_res(const __grid_consta
         grid.sync(); mark();
     }
     if (mode == 1) return;
+    wait_late();
     if (solo_on) {  // the smallest levels on CTA 0, whole in its shared memory, __syncthreads between phases
         if (blockIdx.x == 0) solo_cycle<T>(w, sc, plan, solo, smem);
         grid.sync(); mark();
@@ -433,6 +452,7 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
     for (int g = 0; g < G; ++g) {
         uint32_t cursor = 0;
         int nc = 0;
+        bool late_lv = false;  // copies of cycle levels >= 1 (and the solo tail) complete on the kernel's second barrier
         auto add = [&](uint32_t& off, const void* base, int64_t elem_off, size_t esz, size_t count) -> bool {
             const uintptr_t src = reinterpret_cast<uintptr_t>(base) + (uintptr_t)(elem_off * (int64_t)esz);
             const uintptr_t al = src & ~(uintptr_t)15;
@@ -443,12 +463,13 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
             if (bytes == 0) { cursor = dst; return true; }
             const uint32_t nb = (uint32_t)((lead + bytes + 15) & ~(size_t)15);
             if (nc >= RES_MAXC) return false;
-            copies[(size_t)g * RES_MAXC + nc++] = ResCopy{reinterpret_cast<const void*>(al), dst, nb};
+            copies[(size_t)g * RES_MAXC + nc++] = ResCopy{reinterpret_cast<const void*>(al), dst, nb | (late_lv ? RES_LATE : 0u)};
             cursor = dst + nb;
             tx[g] += nb;
             return true;
         };
         for (int k = 0; k < K; ++k) {
+            late_lv = k > 0;
             const CoarseLevel<T>& L = c.L[k];
             ResLevel& d = lv[(size_t)g * 16 + k];
             d.r0 = rb[k][g]; d.r1 = rb[k][g + 1];
@@ -473,6 +494,7 @@ bool coarse_res_plan(const CoarseCycle<T>& c, int G, uint32_t smem_cap, std::vec
             }
             if (!ok) return false;
         }
+        late_lv = true;
         if (g == 0 && solo_out && with_coarsest) {   // the solo tail in CTA 0 (coarse_res.cuh)
             const size_t ts = sizeof(T);
             auto level_bytes = [&](int k) -> size_t {

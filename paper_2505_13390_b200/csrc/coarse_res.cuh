@@ -25,8 +25,10 @@ struct ResLevel {        // one CTA's share of one coarse level
 struct ResCopy {
     const void* src;     // 16-byte aligned
     uint32_t dst;        // shared-memory byte offset, 16-byte aligned
-    uint32_t bytes;      // multiple of 16
+    uint32_t bytes;      // multiple of 16; bit 31 (RES_LATE): a copy of cycle level >= 1 (second barrier)
 };
+constexpr uint32_t RES_LATE = 0x80000000u;
+constexpr uint32_t RES_BYTES_MASK = 0x7fffffffu;
 
 constexpr int RES_MAXC = 128;  // bulk copies per CTA
 
