@@ -131,6 +131,10 @@ typedef struct {
                                  smoother coefficients (reading c26).
                                  Costs the fp64 Galerkin refresh + the iterations + one graph re-capture
                                  per frame */
+    double time_budget_ms;    /* Alg. 1 l.12 "timeBudgetExhausted": stop the frame after the first
+                                 outer iteration that completes more than this many ms (device time, CUDA events)
+                                 after the frame started (one host synchronisation per outer iteration); 0 = off.
+                                 Machine-dependent by definition (reading c21) */
 } mgpbd_config;
 
 #define MGPBD_MAX_LEVELS 16

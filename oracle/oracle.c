@@ -26,6 +26,7 @@ void orc_config_default(orc_config* c) {
     c->smoother = 0; c->cheb_lower = 0.25;
     c->backtrack = 0; c->omega_min = 1e-3; c->residual_tol = 0.0; c->pcg_tol = 0.0;
     c->resetup_on_indef = 1; c->residual_abs = 0.0; c->k_nullspace = 1; c->omega_refresh_iters = 0;
+    c->time_budget_ms = 0.0;
     c->gravity[0] = 0.0; c->gravity[1] = -9.8; c->gravity[2] = 0.0; c->seed = 1;
 }
 
@@ -1250,6 +1251,8 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
     s->n_b = 0;
     /* omega of l.11: user-specified, or halved whenever ||b|| rises (reading c21) */
     double omega = s->cfg.omega_relax, bprev = -1.0, b0 = 0.0;
+    struct timespec tf0;
+    clock_gettime(CLOCK_MONOTONIC, &tf0);
     for (int32_t ite = 0; ite < n_iters; ++ite) {
         if (s->kind == 2) orc_eval_distance(m, s->verts, s->x, s->rest_len, s->C, s->g);          /* l.4 */
         else orc_eval_arap(m, s->verts, s->x, s->Dm_inv, s->C, s->g);
@@ -1279,6 +1282,12 @@ int orc_sim_step(orc_sim* s, double dt, int32_t n_iters) {
         s->iters_used = ite + 1;
         if (s->cfg.residual_tol > 0.0 && bn < s->cfg.residual_tol * b0) break;                 /* l.12 */
         if (s->cfg.residual_abs > 0.0 && bn < s->cfg.residual_abs) break;
+        if (s->cfg.time_budget_ms > 0.0) {                                                       /* l.12 budget */
+            struct timespec tn;
+            clock_gettime(CLOCK_MONOTONIC, &tn);
+            const double ms = (double)(tn.tv_sec - tf0.tv_sec) * 1e3 + (double)(tn.tv_nsec - tf0.tv_nsec) * 1e-6;
+            if (ms > s->cfg.time_budget_ms) break;
+        }
     }
     s->omega_last = omega;
     for (int64_t k = 0; k < 3 * (int64_t)n; ++k) s->v[k] = (s->x[k] - s->x_old[k]) / dt;      /* l.17 */

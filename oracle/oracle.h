@@ -48,6 +48,9 @@ typedef struct {
                                     the last normalised iterate (reading c26); 0 = omega only at setup */
     int32_t k_nullspace;     /* near-kernel vectors per aggregate ("six distinct B"; reading c1):
                                 1 (default) or up to 6 */
+    double time_budget_ms;   /* Alg. 1 l.12 "timeBudgetExhausted": break after the first outer iteration
+                                that ends more than this many ms (wall clock) after the frame started; 0 = off.
+                                Machine-dependent by definition (reading c21) */
 } orc_config;
 
 void orc_config_default(orc_config* c);

@@ -33,7 +33,7 @@ class Config(C.Structure):
                 ("cheb_lower", C.c_double), ("backtrack", C.c_int32), ("omega_min", C.c_double),
                 ("residual_tol", C.c_double), ("pcg_tol", C.c_double), ("resetup_on_indef", C.c_int32),
                 ("residual_abs", C.c_double), ("omega_refresh_iters", C.c_int32),
-                ("k_nullspace", C.c_int32)]
+                ("k_nullspace", C.c_int32), ("time_budget_ms", C.c_double)]
 
 
 _lib = None

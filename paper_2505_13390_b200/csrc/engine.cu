@@ -1442,6 +1442,14 @@ class Engine : public EngineBase {
                 if (cfg.residual_tol > 0.0 && b2[1] < cfg.residual_tol * cfg.residual_tol * b2[0]) break;
                 if (cfg.residual_abs > 0.0 && b2[1] < cfg.residual_abs * cfg.residual_abs) break;
             }
+            if (cfg.time_budget_ms > 0.0) {  // l.12 timeBudgetExhausted: device time since the frame started
+                cudaEvent_t ei = ev();
+                MG_CK(cudaEventRecord(ei, st));
+                MG_CK(cudaEventSynchronize(ei));
+                float el = 0.0f;
+                MG_CK(cudaEventElapsedTime(&el, f0, ei));
+                if ((double)el > cfg.time_budget_ms) break;
+            }
         }
         velocity(nv, x.p, x_old.p, v.p, dt, st);                                                     // l.17
         f1 = ev();
@@ -1788,6 +1796,7 @@ mgpbd_status mgpbd_config_default(mgpbd_config* c) {
     c->residual_abs = 0.0;
     c->resetup_on_indef = 1;
     c->omega_refresh_iters = 0;
+    c->time_budget_ms = 0.0;
     return MGPBD_OK;
 }
 
@@ -1821,6 +1830,7 @@ mgpbd_status mgpbd_create(const mgpbd_mesh* mesh, const mgpbd_constraints* cons,
     if (cfg->smoother == 1 && !(cfg->cheb_lower > 0.0 && cfg->cheb_lower < 1.0)) return fail("cheb_lower must be in (0, 1)");
     if (!(cfg->pcg_tol >= 0.0)) return fail("pcg_tol must be >= 0");
     if (cfg->omega_refresh_iters < 0 || cfg->omega_refresh_iters > 10000) return fail("omega_refresh_iters must be in 0..10000");
+    if (!(cfg->time_budget_ms >= 0.0)) return fail("time_budget_ms must be >= 0");
     if (cfg->smoother_sweeps < 1 || cfg->pcg_iters < 0 || cfg->pcg_iters > mgpbd::SC_KMAX || cfg->setup_interval < 1 ||
         cfg->min_coarse < 1 || cfg->max_levels < 1 || cfg->power_iters < 0 || cfg->bootstrap_sweeps < 0 ||
         cfg->max_dense_coarse < 1)

@@ -100,3 +100,23 @@ def test_absolute_residual_exit_frame(name):
     assert st.iters_run == sim.iters_used() <= 5 and st.b_last < eps
     xo, _, lo = sim.state()
     assert rel(ctx.lambdas(), lo) <= 1e-6 and rel(ctx.positions() - sc.pos, xo - sc.pos) <= 1e-6
+
+
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp64", "fp32"])
+def test_time_budget_exit_frame(precision):
+    """Alg. 1 l.12 "timeBudgetExhausted" (reading c21): a budget below one outer iteration stops after it — equal to the
+    oracle's 1-iteration frame — and a budget above the frame keeps every iteration."""
+    sc = scenes.make("bar3k")
+    tol = 1e-6 if precision == 0 else 1e-3
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, time_budget_ms=1e-6)
+    ctx.step(sc.dt, 8)
+    assert ctx.stats().iters_run == 1
+    sim = O.Sim(sc, O.default_config(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters))
+    sim.step(sc.dt, 1)
+    xo, _, lo = sim.state()
+    assert rel(ctx.lambdas(), lo) <= tol and rel(ctx.positions() - sc.pos, xo - sc.pos) <= tol
+    ctx.close()
+    ctx = mgpbd.Context.from_scene(sc, precision=precision, time_budget_ms=1e7)
+    ctx.step(sc.dt, 8)
+    assert ctx.stats().iters_run == 8
+    ctx.close()

@@ -445,3 +445,23 @@ def test_setup_schedule_literal_and_resetup_on_indefinite(O):
     for f in range(1, 4):
         assert su[1][f] - su[1][f - 1] == (1 if ev[1][f - 1] > 0 else 0)
     assert su[1][-1] > 1
+
+
+def test_time_budget_exit(O):
+    """Alg. 1 l.12 "timeBudgetExhausted" (reading c21): a budget every iteration exceeds stops the frame
+    after its first outer iteration — the frame then equals a 1-iteration frame — and a budget none reaches leaves
+    the fixed-count frame unchanged."""
+    from paper_2505_13390_b200 import scenes
+    sc = scenes.make("bar_small")
+    base = dict(omega_relax=sc.omega_relax, pcg_iters=sc.pcg_iters)
+    one = O.Sim(sc, O.default_config(**base))
+    assert one.step(sc.dt, 1) == 0
+    tiny = O.Sim(sc, O.default_config(time_budget_ms=1e-9, **base))
+    assert tiny.step(sc.dt, 6) == 0 and tiny.iters_used() == 1
+    for a, b in zip(tiny.state(), one.state()):
+        assert np.array_equal(a, b)
+    full = O.Sim(sc, O.default_config(**base))
+    huge = O.Sim(sc, O.default_config(time_budget_ms=1e9, **base))
+    assert full.step(sc.dt, 6) == 0 and huge.step(sc.dt, 6) == 0 and huge.iters_used() == 6
+    for a, b in zip(huge.state(), full.state()):
+        assert np.array_equal(a, b)
