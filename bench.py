@@ -254,6 +254,8 @@ def run_ours(args):
         e1.record(stream)
         barrier()
     t_ms = e0.elapsed_time(e1)
+    st1 = ctx.stats()   # the hierarchy the window ended on (re-setups inside the window change it)
+    levels_end = [(int(st1.n[l]), int(st1.nnz[l])) for l in range(st1.n_levels)]
     # phase breakdown + eager pass timing: the same frames again with CUDA events around every level-0 pass
     # and phase (the per-iteration graphs are bypassed; kernels are identical)
     ctx.set_profiling(True)
@@ -326,8 +328,8 @@ def run_ours(args):
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32" if prec else "f64", "data": "synthetic",
         "config": config_dict(sc, args, world, {
-            "nnz_A0": levels[0][1] if levels else None, "levels": levels,
-            "op_complexity": st0.op_complexity,
+            "nnz_A0": levels[0][1] if levels else None, "levels": levels_end, "levels_at_window_start": levels,
+            "op_complexity": st1.op_complexity,
             "ms_setup_frame_extra": (statistics.mean(setup_ms) if setup_ms else None),
             "setups_in_window": len(setup_ms),
             "indefinite_events_in_window": indef,
