@@ -3,6 +3,7 @@
 
 #include <cooperative_groups.h>
 #include <cstdlib>
+#include <string>
 
 #include <algorithm>
 #include <cstdint>
@@ -594,10 +595,10 @@ __global__ void k_jacobi0(int32_t n, const T* __restrict__ dinv, const T* __rest
 
 // bc[a] = sum_{i in a, ascending} t[i]: 8 lanes per aggregate, each lane's members in chunks of 4 with
 // all list loads issued before the t gathers; lane partials + fixed-order butterfly (deterministic)
-template <class T, int G>
+template <class T, int G, int UN = 4>
 __global__ void k_restrict(int32_t nc, const int64_t* __restrict__ mptr, const int32_t* __restrict__ mlist,
                            const T* __restrict__ t, T* __restrict__ bc) {
-    constexpr int PER = 32 / G, UN = 4;
+    constexpr int PER = 32 / G;
     const int lane = threadIdx.x & 31, sub = lane / G, sl = lane % G;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -1413,8 +1414,12 @@ void vec_jacobi0(int32_t n, const T* dinv, const T* b, double omega, T* y, cudaS
 template <class T>
 void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, const T* t, T* bc, cudaStream_t s) {
     if (!nc) return;
-    int g = (int)std::min<int64_t>(((int64_t)nc * 32 + PB - 1) / PB, 148 * 8);
-    k_restrict<T, 8><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
+    // 16 lanes per aggregate, 4 member loads in flight per lane (tools/ab_frames.py on hierarchy B: 68.27 ms/frame
+    // with 8 x 4, 67.91 with 16 x 4; 4 x 4/8, 8 x 8, 16 x 2, 32 x 2/4 between or slower); MGPBD_RESTRICT_G8=1: 8 x 4
+    static const bool g8 = std::getenv("MGPBD_RESTRICT_G8") != nullptr;
+    const int g = (int)std::min<int64_t>(((int64_t)nc * (g8 ? 8 : 16) * 4 + PB - 1) / PB, 148 * 8);
+    if (g8) k_restrict<T, 8, 4><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
+    else k_restrict<T, 16, 4><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
     MG_LAUNCH_CHECK();
 }
 template <class T>
