@@ -577,7 +577,7 @@ inline int chunk_grid(int64_t n, int cpt = 1) {
 // chunks per thread of the PCG update kernels (MGPBD_VEC_CPT: 1 or 4)
 inline int vec_cpt() {
     static const int c = std::getenv("MGPBD_VEC_CPT") ? std::atoi(std::getenv("MGPBD_VEC_CPT")) : 4;
-    return c == 1 ? 1 : 4;
+    return c == 1 || c == 2 || c == 8 ? c : 4;
 }
 
 template <class T, bool V>
@@ -1452,8 +1452,9 @@ void pcg_update_p_fin(int32_t n, const T* z, T* p, double* scal, int k, const do
     // every CTA must run (CTA 0 publishes the scalars even for n = 0): the grid covers at least one chunk
     const int cpt = vec_cpt();
     if (al16(z) && al16(p)) {
-        if (cpt == 4) k_pcg_p_fin<T, true, 4><<<chunk_grid<T, true>(n, 4), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
-        else k_pcg_p_fin<T, true, 1><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
+#define MG_PF(C) k_pcg_p_fin<T, true, C><<<chunk_grid<T, true>(n, C), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin)
+        switch (cpt) { case 1: MG_PF(1); break; case 2: MG_PF(2); break; case 8: MG_PF(8); break; default: MG_PF(4); }
+#undef MG_PF
     } else {
         k_pcg_p_fin<T, false, 1><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, z, p, scal, k, prz, prr, np, flags, tag, fin);
     }
@@ -1464,10 +1465,9 @@ void pcg_update_xr_fin(int32_t n, const T* p, const T* q, T* x, T* r, double* sc
                        int* flags, int tag, cudaStream_t s, const T* dinv, double om0, T* x1, const double* fin) {
     const int cpt = vec_cpt();
     if (al16(p) && al16(q) && al16(x) && al16(r) && (!x1 || (al16(x1) && al16(dinv)))) {
-        if (cpt == 4)
-            k_pcg_xr_fin<T, true, 4><<<chunk_grid<T, true>(n, 4), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
-        else
-            k_pcg_xr_fin<T, true, 1><<<chunk_grid<T, true>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
+#define MG_XR(C) k_pcg_xr_fin<T, true, C><<<chunk_grid<T, true>(n, C), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin)
+        switch (cpt) { case 1: MG_XR(1); break; case 2: MG_XR(2); break; case 8: MG_XR(8); break; default: MG_XR(4); }
+#undef MG_XR
     } else {
         k_pcg_xr_fin<T, false, 1><<<chunk_grid<T, false>(n), PB, 0, s>>>(n, p, q, x, r, scal, k, ppq, np, flags, tag, dinv, om0, x1, fin);
     }
