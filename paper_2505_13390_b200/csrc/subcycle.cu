@@ -8,8 +8,14 @@ namespace mgpbd {
 
 namespace {
 
-constexpr int SB = 512;   // threads per CTA
-constexpr int CB = 4;     // unit-vector columns per CTA pass
+#ifndef MGPBD_SUB_SB
+#define MGPBD_SUB_SB 512
+#endif
+#ifndef MGPBD_SUB_CB
+#define MGPBD_SUB_CB 4
+#endif
+constexpr int SB = MGPBD_SUB_SB;   // threads per CTA
+constexpr int CB = MGPBD_SUB_CB;   // unit-vector columns per CTA pass
 
 // Level data as the kernel reads it: staged in shared memory (32-bit offsets) or in global memory.
 template <class T, bool ST>
