@@ -282,7 +282,7 @@ def run_ours(args):
         g_frames_ms += s.ms_frame - s.ms_setup
     ctx.set_profiling(False)
     burst = None
-    if world == 1:  # the same pass replayed as one CUDA graph: no launch gaps
+    if world == 1 and not args.partitioned:  # the same pass replayed as one CUDA graph: no launch gaps
         b_ms, b_bytes = ctx.pass_burst(50)
         burst = (b_bytes / 1e9) / (b_ms / 1e3)
     if dist:

@@ -218,6 +218,10 @@ class Engine : public EngineBase {
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
     int64_t omega_refreshes = 0;
+    // halo exchange overlapped with the interior vertex gather (partitioned matrix-free level 0; MGPBD_NO_HALO_OVERLAP)
+    bool halo_overlap = std::getenv("MGPBD_NO_HALO_OVERLAP") == nullptr;
+    cudaStream_t st_comm = nullptr;
+    cudaEvent_t ev_xa = nullptr, ev_xb = nullptr;
     // level-0 x1 of the next V-cycle already formed by the PCG x / r update (one launch less per iteration)
     bool l0_x1_ready = false;
     bool vc_trace = false;  // stage stamps inside the first level-0 V-cycle of an iteration (MGPBD_TRACE_STAGES)
@@ -373,6 +377,25 @@ class Engine : public EngineBase {
         mf.ppos = mf_ppos.p; mf.npad = mf_npad; mf.vsrc = mf_vsrc.p; mf.jbase = mf_jbase.p;
         mf.vj16 = mf_vj16.n ? mf_vj16.p : nullptr; mf.vj32 = mf_vj32.n ? mf_vj32.p : nullptr;
         mf.p0 = ppos_h[mf.v0]; mf.p1 = ppos_h[mf.v1];
+        if (dist && mf.v1 > mf.v0) {  // longest run of vertices whose incidences are all owned rows [r0, r1)
+            std::vector<int32_t> vl_((size_t)hp[nv]);
+            d2h(vl_.data(), vlist.p, vl_.size(), st);
+            MG_CK(cudaStreamSynchronize(st));
+            int32_t best0 = 0, best1 = 0, run0 = -1;
+            for (int32_t v = mf.v0; v <= mf.v1; ++v) {
+                bool interior = v < mf.v1;
+                for (int64_t e = v < mf.v1 ? hp[v] : 0; interior && e < hp[v + 1]; ++e) {
+                    const int32_t j = vl_[e] / kc;
+                    interior = j >= r0 && j < r1;
+                }
+                if (interior && run0 < 0) run0 = v;
+                if (!interior && run0 >= 0) {
+                    if (v - run0 > best1 - best0) { best0 = run0; best1 = v; }
+                    run0 = -1;
+                }
+            }
+            mf.vi0 = best0; mf.vi1 = best1;
+        }
         mf_hv.resize(3 * (size_t)mf_npad); mf_at.resize(m); mf_u.resize(4 * (size_t)nv);
         MG_CK(cudaMemsetAsync(mf_u.p, 0, sizeof(T) * 4 * (size_t)nv, st));
         mf.hv = mf_hv.p; mf.at = mf_at.p; mf.u = mf_u.p;
@@ -508,6 +531,9 @@ class Engine : public EngineBase {
         invalidate_graphs();
         for (auto e : ev_pool) cudaEventDestroy(e);
         cudaStreamSynchronize(st);
+        if (st_comm) { cudaStreamSynchronize(st_comm); cudaStreamDestroy(st_comm); }
+        if (ev_xa) cudaEventDestroy(ev_xa);
+        if (ev_xb) cudaEventDestroy(ev_xb);
         g_alloc_stream = nullptr;  // members are freed after this body: plain cudaFree from here on
         if (own_stream && st) cudaStreamDestroy(st);
     }
@@ -581,7 +607,7 @@ class Engine : public EngineBase {
     }
 
     void l0_pass(int mode, const T* xin, const T* b, T* y, const T* aux, double omega, double alpha = 0.0,
-                 const T* xprev = nullptr, double x0_omega = 0.0) {
+                 const T* xprev = nullptr, double x0_omega = 0.0, const std::function<void()>* mid = nullptr) {
         const Level& l0 = *L[0];
         cudaEvent_t e0 = nullptr, e1 = nullptr;
         // inside stream capture a plain record is only a dependency: cudaEventRecordExternal makes it an event
@@ -591,7 +617,7 @@ class Engine : public EngineBase {
             else MG_CK(cudaEventRecord(e, st));
         };
         if (cfg.profile) { e0 = prof_event(); rec(e0); }
-        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev, x0_omega);
+        if (mf_on()) mf_pass<T>(mode, mf, xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev, x0_omega, mid);
         else csr_pass<T>(mode, l0.hot(), xin, b, y, aux, omega, parts1.p, parts2.p, st, alpha, xprev);
         if (cfg.profile) {
             e1 = prof_event();
@@ -606,6 +632,22 @@ class Engine : public EngineBase {
     void pass(int l, int mode, const T* xin, const T* b, T* y, const T* aux, double omega, double alpha = 0.0,
               const T* xprev = nullptr) {
         if (l == 0) {
+            if (dist && mf_on() && halo_overlap && mf.vi1 > mf.vi0 && !xfers.empty()) {
+                // partitioned matrix-free level 0: the halo exchange runs on a side stream while the interior
+                // vertices (no halo incidence) are gathered; the boundary vertices and the rows wait for it
+                if (!st_comm) {
+                    MG_CK(cudaStreamCreateWithFlags(&st_comm, cudaStreamNonBlocking));
+                    MG_CK(cudaEventCreateWithFlags(&ev_xa, cudaEventDisableTiming));
+                    MG_CK(cudaEventCreateWithFlags(&ev_xb, cudaEventDisableTiming));
+                }
+                MG_CK(cudaEventRecord(ev_xa, st));
+                MG_CK(cudaStreamWaitEvent(st_comm, ev_xa, 0));
+                comm->exchange(const_cast<T*>(xin), sizeof(T), xfers, st_comm);
+                MG_CK(cudaEventRecord(ev_xb, st_comm));
+                const std::function<void()> mid = [&] { MG_CK(cudaStreamWaitEvent(st, ev_xb, 0)); };
+                l0_pass(mode, xin, b, y, aux, omega, alpha, xprev, 0.0, &mid);
+                return;
+            }
             // partitioned level 0: bring the halo columns of x from the owning ranks first
             if (dist) comm->exchange(const_cast<T*>(xin), sizeof(T), xfers, st);
             l0_pass(mode, xin, b, y, aux, omega, alpha, xprev);

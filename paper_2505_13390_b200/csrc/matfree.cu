@@ -738,10 +738,13 @@ __global__ void __launch_bounds__(mf_r<T, KC>()) k_mf_rows_tma(int32_t row0, int
 
 template <class T, int KC>
 void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-                double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev, double xom) {
+                double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev, double xom,
+                const std::function<void()>* mid) {
     if (xom != 0.0 && (mode != PASS_JACOBI || !A.tma || A.vg_ts > 0))
         throw Error(-1, "mf_pass: implicit x (x0_omega) needs PASS_JACOBI and the TMA row kernel");
-    if (A.v1 > A.v0) {
+    // the vertex gather over [gv0, gv1)
+    auto gather = [&](int32_t gv0, int32_t gv1) {
+        if (gv1 <= gv0) return;
         // G lanes per vertex, UN 16-byte chunks per lane per round (~23 incidences per vertex on tets = 6 float4
         // chunks, ~6 on cloth = 2); build-time overridable for tuning sweeps
 #ifndef MGPBD_VG_G
@@ -756,7 +759,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #endif
         // fp64 chunks hold 2 incidences: 3 per lane per round cover a tet vertex (78.6 vs 87.2 us per pass at 2)
         constexpr int UN = KC == 4 ? (sizeof(T) == 8 ? MGPBD_VG_UN64 : MGPBD_VG_UN) : 1;
-        const int64_t thr = (int64_t)(A.v1 - A.v0) * G;
+        const int64_t thr = (int64_t)(gv1 - gv0) * G;
 #ifndef MGPBD_VG_CTAS_PER_SM
 #define MGPBD_VG_CTAS_PER_SM 16
 #endif
@@ -772,18 +775,18 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         if (A.vg_grid_cap > 0) grid = std::min(grid, A.vg_grid_cap);
         if (A.vg_ts > 0) {  // TMA-pipelined vertex gather
             constexpr int GT = KC == 4 ? 4 : 2;
-            const int32_t ntiles = (A.v1 - A.v0 + VGT - 1) / VGT;
+            const int32_t ntiles = (gv1 - gv0 + VGT - 1) / VGT;
             int tg = std::min(ntiles, A.vg_grid);
             if (A.vg_grid_cap > 0) tg = std::min(tg, A.vg_grid_cap);
             if (A.vj16) {
                 const size_t sm = (size_t)VG_STAGES * VgLayout<T, true>(A.vg_ts).bytes;
                 ensure_dyn_smem((const void*)k_mf_vgather_tma<T, GT, true>, sm);
-                k_mf_vgather_tma<T, GT, true><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
+                k_mf_vgather_tma<T, GT, true><<<tg, VG_BS, sm, s>>>(gv0, gv1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
                                                                    A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
             } else {
                 const size_t sm = (size_t)VG_STAGES * VgLayout<T, false>(A.vg_ts).bytes;
                 ensure_dyn_smem((const void*)k_mf_vgather_tma<T, GT, false>, sm);
-                k_mf_vgather_tma<T, GT, false><<<tg, VG_BS, sm, s>>>(A.v0, A.v1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
+                k_mf_vgather_tma<T, GT, false><<<tg, VG_BS, sm, s>>>(gv0, gv1, ntiles, A.vg_ts, A.npad, A.ppos, A.vj16,
                                                                     A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u));
             }
         } else {
@@ -798,7 +801,7 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
         la[0].val.programmaticStreamSerializationAllowed = 1;                                           \
         lc.attrs = la;                                                                                  \
         lc.numAttrs = A.vg_pdl ? 1 : 0;                                                                 \
-        MG_CK(cudaLaunchKernelEx(&lc, k_mf_vgather<T, G, UN, J, X>, A.v0, A.v1, A.npad, A.ppos, A.vj16, \
+        MG_CK(cudaLaunchKernelEx(&lc, k_mf_vgather<T, G, UN, J, X>, gv0, gv1, A.npad, A.ppos, A.vj16, \
                                  A.vj32, A.jbase, A.hv, x, reinterpret_cast<V4<T>*>(A.u), (const T*)A.dinv, \
                                  b, xom, vg_sms()));                                                    \
     } while (0)
@@ -807,6 +810,17 @@ void mf_pass_kc(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, con
 #undef MG_VG
         }
         MG_LAUNCH_CHECK();
+    };
+    // mid (partitioned level 0, MatFree::vi0/vi1): the interior vertices — no halo incidence — are gathered while the
+    // halo exchange runs; mid() joins it, then the boundary vertices
+    if (mid && A.vi1 > A.vi0 && A.vg_ts == 0) {
+        gather(A.vi0, A.vi1);
+        (*mid)();
+        gather(A.v0, A.vi0);
+        gather(A.vi1, A.v1);
+    } else {
+        if (mid) (*mid)();
+        gather(A.v0, A.v1);
     }
     const V4<T>* u = reinterpret_cast<const V4<T>*>(A.u);
     if (A.tma) {
@@ -938,9 +952,10 @@ void mf_refresh(const MatFree<T>& A, const double* alpha, double dt, T* dinv, cu
 
 template <class T>
 void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
-             double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev, double xom) {
-    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom);
-    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom);
+             double* parts, double* parts2, cudaStream_t s, double alpha, const T* xprev, double xom,
+             const std::function<void()>* mid) {
+    if (A.kc == 4) mf_pass_kc<T, 4>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom, mid);
+    else mf_pass_kc<T, 2>(mode, A, x, b, y, aux, omega, parts, parts2, s, alpha, xprev, xom, mid);
 }
 
 // grid of the vertex-major update: the resident CTAs only when the ranges are blocked (persistent), else grid-stride
@@ -975,7 +990,7 @@ void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const doub
     template void mf_update<T>(const MatFree<T>&, const T*, const double*, const double*, double*, cudaStream_t); \
     template void mf_refresh<T>(const MatFree<T>&, const double*, double, T*, cudaStream_t);                     \
     template void mf_pass<T>(int, const MatFree<T>&, const T*, const T*, T*, const T*, double, double*, double*, \
-                             cudaStream_t, double, const T*, double);
+                             cudaStream_t, double, const T*, double, const std::function<void()>*);
 MG_INST(float)
 MG_INST(double)
 #undef MG_INST

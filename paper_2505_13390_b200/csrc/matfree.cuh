@@ -8,6 +8,7 @@
 // followed by the same per-row epilogues as the CSR passes (PASS_* in solve.cuh).  The assembled CSR
 // is still built every outer iteration: the Galerkin refresh (Eq. 6) and the smoother diagonal use it.
 #pragma once
+#include <functional>
 #include <vector>
 
 #include "common.cuh"
@@ -44,6 +45,7 @@ struct MatFree {
     int vg_grid_cap = 0;            // > 0: cap on the vertex-gather grid (MGPBD_MF_GRID_CAP, tests only)
     // != nullptr: the row kernel's last CTA also sums the dot partials (fixed order): JACOBI_DOT -> fin[0] (parts),
     // fin[1] (parts2); SPMV_DOT -> fin[2]; fin_ctr = arrival counter (0 between launches)
+    int32_t vi0 = 0, vi1 = 0;       // interior vertices of a partitioned level 0 (no halo incidence), vi0 >= vi1: none
     bool vg_pdl = false;            // vertex gather launched with programmatic dependent launch (MGPBD_VG_PDL)
     double* fin = nullptr;
     unsigned* fin_ctr = nullptr;
@@ -84,8 +86,10 @@ void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const doub
 // x0_omega != 0 (PASS_JACOBI, TMA row kernel): x is not read — x_i = x0_omega D^-1_ii b_i, the first smoothing
 // step from x = 0 fused into the second (the V-cycle's k_jacobi0 expression, bit for bit).
 template <class T>
+// mid != nullptr (partitioned level 0): called between the gather of the interior vertices [vi0, vi1) and the
+// boundary vertices — the caller joins the halo exchange there, which therefore overlaps the interior gather.
 void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const T* aux, double omega,
              double* parts, double* parts2, cudaStream_t s, double alpha = 0.0, const T* xprev = nullptr,
-             double x0_omega = 0.0);
+             double x0_omega = 0.0, const std::function<void()>* mid = nullptr);
 
 }  // namespace mgpbd

@@ -217,3 +217,17 @@ def test_nccl_single_rank_partitioned_path(precision):
     ctx.close()
     frames_tol = 1e-9 if precision == 0 else 1e-3
     assert rel(x - sc.pos, x1 - sc.pos) <= frames_tol and rel(lam, l1) <= frames_tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_overlap_is_bitwise_the_sequential_exchange(monkeypatch, world):
+    """The halo exchange overlapped with the interior vertex gather (side stream, boundary vertices after the join)
+    computes every vertex sum and row exactly as exchange-then-pass: bit-identical frames."""
+    sc = scenes.make("block_small")
+    monkeypatch.delenv("MGPBD_NO_HALO_OVERLAP", raising=False)
+    a = _run_virtual(sc, world, 2, 4, precision=0, setup_interval=2)
+    monkeypatch.setenv("MGPBD_NO_HALO_OVERLAP", "1")
+    b = _run_virtual(sc, world, 2, 4, precision=0, setup_interval=2)
+    for (xa, la, *_), (xb, lb, *_) in zip(a, b):
+        assert np.array_equal(xa, xb) and np.array_equal(la, lb)
