@@ -300,7 +300,13 @@ __global__ void k_eval_distance(int32_t m, const int32_t* __restrict__ verts, co
 // ARAP (Eq. 8, literal squared form, reading c15): C = ||F - R||_F^2, G = 2(F - R) D_m^-T,
 // grad_{1..3} = columns of G, grad_0 = -sum; h_k = sqrt(w_{v_k}) grad_k.
 template <class T>
-__global__ void __launch_bounds__(128, 8) k_eval_arap(int32_t m, const int32_t* __restrict__ verts, const double* __restrict__ x,
+#ifndef MGPBD_EVAL_BS
+#define MGPBD_EVAL_BS 128
+#endif
+#ifndef MGPBD_EVAL_MINB
+#define MGPBD_EVAL_MINB 8
+#endif
+__global__ void __launch_bounds__(MGPBD_EVAL_BS, MGPBD_EVAL_MINB) k_eval_arap(int32_t m, const int32_t* __restrict__ verts, const double* __restrict__ x,
                             const double* __restrict__ Dminv, const double* __restrict__ sqrtw,
                             const double* __restrict__ alpha, double dt2, const double* __restrict__ lambda,
                             T* __restrict__ h, T* __restrict__ b) {
@@ -548,7 +554,7 @@ void eval_constraints(int kind, int32_t m, const int32_t* verts, const double* x
     if (kind == 2)
         k_eval_distance<T><<<grid1d(m), 256, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b);
     else
-        k_eval_arap<T><<<grid1d(m, 128), 128, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b);
+        k_eval_arap<T><<<grid1d(m, MGPBD_EVAL_BS), MGPBD_EVAL_BS, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b);
     MG_LAUNCH_CHECK();
 }
 
