@@ -218,6 +218,9 @@ class Engine : public EngineBase {
     VaPlan va;                  // level-0 -> 1 Galerkin from h (vagal.cuh), rebuilt at every setup
     bool va_ok = false;
     int64_t omega_refreshes = 0;
+    bool eval_hv = std::getenv("MGPBD_NO_EVAL_HV") == nullptr;  // evaluation writes the vertex-major operator data
+    DBuf<int32_t> mf_inv;
+    bool npad_fits() const { return mf_npad < ((int64_t)1 << 31); }
     // halo exchange overlapped with the interior vertex gather (partitioned matrix-free level 0; MGPBD_NO_HALO_OVERLAP)
     bool halo_overlap = std::getenv("MGPBD_NO_HALO_OVERLAP") == nullptr;
     cudaStream_t st_comm = nullptr;
@@ -341,6 +344,12 @@ class Engine : public EngineBase {
         if (std::getenv("MGPBD_NO_VJ16")) fits16 = false;
         mf_ppos.resize((size_t)nv + 1); h2d(mf_ppos.p, ppos_h.data(), (size_t)nv + 1, st);
         mf_vsrc.resize((size_t)mf_npad); h2d(mf_vsrc.p, src.data(), (size_t)mf_npad, st);
+        {   // padded slot of every incidence code (constraint j, slot k) -> j kc + k: the evaluation writes hv directly
+            std::vector<int32_t> inv((size_t)ninc, 0);
+            for (int64_t p = 0; p < mf_npad; ++p)
+                if (src[p] >= 0) inv[src[p]] = (int32_t)p;
+            mf_inv.resize((size_t)ninc); h2d(mf_inv.p, inv.data(), (size_t)ninc, st);
+        }
         mf_jbase.resize((size_t)nv); h2d(mf_jbase.p, jb.data(), (size_t)nv, st);
         if (fits16) {
             std::vector<uint16_t> j16((size_t)mf_npad);
@@ -397,6 +406,7 @@ class Engine : public EngineBase {
             mf.vi0 = best0; mf.vi1 = best1;
         }
         mf_hv.resize(3 * (size_t)mf_npad); mf_at.resize(m); mf_u.resize(4 * (size_t)nv);
+        MG_CK(cudaMemsetAsync(mf_hv.p, 0, sizeof(T) * 3 * (size_t)mf_npad, st));  // pad slots stay 0 (EvalHv)
         MG_CK(cudaMemsetAsync(mf_u.p, 0, sizeof(T) * 4 * (size_t)nv, st));
         mf.hv = mf_hv.p; mf.at = mf_at.p; mf.u = mf_u.p;
         mf.dinv = L[0]->dinv.p;
@@ -1336,12 +1346,18 @@ class Engine : public EngineBase {
 
     void assemble_hot(double dt) {
         Level& l0 = *L[0];
-        eval_constraints<T>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h.p, b0.p, st);
+        // one rank, matrix-free: the evaluation also writes hv / at / D^-1 (no k_mf_refresh pass over h)
+        const bool fused = cfg.level0_operator == 1 && !dist && eval_hv && mf.p0 == 0 && mf.p1 == mf_npad &&
+                           mf_inv.n == (size_t)m * kc && npad_fits();
+        EvalHv<T> e;
+        if (fused) { e.inv = mf_inv.p; e.hv = mf_hv.p; e.npad = mf_npad; e.at = mf_at.p; e.dinv = l0.dinv.p; }
+        eval_constraints<T>(kind, m, verts.p, x.p, rest.p, sqrtw.p, alpha.p, dt, lambda.p, h.p, b0.p, st,
+                            fused ? &e : nullptr);
         // (all constraints are evaluated on every rank: h of the halo constraints is needed locally)
         last_dt = dt;
         if (cfg.level0_operator == 1) {
             // matrix-free level 0: no assembled matrix in the hot loop (diagonal and A_1 from h)
-            mf_refresh<T>(mf, alpha.p, dt, l0.dinv.p, st);
+            if (!fused) mf_refresh<T>(mf, alpha.p, dt, l0.dinv.p, st);
             mf_ready = true;
         } else {
             assemble<T>(kind, m, verts.p, h.p, alpha.p, dt, rowptr0.p, col0.p, l0.vl, l0.val.p, l0.dinv.p, st, r0, r1);

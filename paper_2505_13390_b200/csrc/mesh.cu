@@ -277,11 +277,28 @@ __device__ bool polar_newton(const double F[9], double R[9]) {
     return false;
 }
 
-template <class T>
+// the vertex-major operator data of row j from its KC x 3 gradient record o (EvalHv; k_mf_refresh's arithmetic)
+template <class T, int KC>
+__device__ __forceinline__ void write_hv(const EvalHv<T>& e, int32_t j, const T (&o)[KC * 3], double a) {
+    double d = 0.0;
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+        const int64_t p = e.inv[(int64_t)j * KC + k];
+        e.hv[p] = o[3 * k];
+        e.hv[e.npad + p] = o[3 * k + 1];
+        e.hv[2 * e.npad + p] = o[3 * k + 2];
+        d += (double)o[3 * k] * o[3 * k] + (double)o[3 * k + 1] * o[3 * k + 1] + (double)o[3 * k + 2] * o[3 * k + 2];
+    }
+    d += a;
+    e.at[j] = (T)a;
+    e.dinv[j] = (T)(1.0 / (double)(T)d);
+}
+
+template <class T, bool HV = false>
 __global__ void k_eval_distance(int32_t m, const int32_t* __restrict__ verts, const double* __restrict__ x,
                                 const double* __restrict__ L, const double* __restrict__ sqrtw,
                                 const double* __restrict__ alpha, double dt2, const double* __restrict__ lambda,
-                                T* __restrict__ h, T* __restrict__ b) {
+                                T* __restrict__ h, T* __restrict__ b, const EvalHv<T> ehv) {
     int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     int2 ab = reinterpret_cast<const int2*>(verts)[j];
@@ -292,24 +309,26 @@ __global__ void k_eval_distance(int32_t m, const int32_t* __restrict__ verts, co
     double u0 = d0 * il, u1 = d1 * il, u2 = d2 * il;
     double wa = sqrtw[ab.x], wb = sqrtw[ab.y];
     T* hj = h + 6 * (int64_t)j;
-    hj[0] = (T)(wa * u0); hj[1] = (T)(wa * u1); hj[2] = (T)(wa * u2);
-    hj[3] = (T)(-wb * u0); hj[4] = (T)(-wb * u1); hj[5] = (T)(-wb * u2);
-    b[j] = (T)(-C - (alpha[j] / dt2) * lambda[j]);
+    const T o[6] = {(T)(wa * u0), (T)(wa * u1), (T)(wa * u2), (T)(-wb * u0), (T)(-wb * u1), (T)(-wb * u2)};
+    for (int k = 0; k < 6; ++k) hj[k] = o[k];
+    const double a = alpha[j] / dt2;
+    if (HV) write_hv<T, 2>(ehv, j, o, a);
+    b[j] = (T)(-C - a * lambda[j]);
 }
 
 // ARAP (Eq. 8, literal squared form, reading c15): C = ||F - R||_F^2, G = 2(F - R) D_m^-T,
 // grad_{1..3} = columns of G, grad_0 = -sum; h_k = sqrt(w_{v_k}) grad_k.
-template <class T>
 #ifndef MGPBD_EVAL_BS
 #define MGPBD_EVAL_BS 128
 #endif
 #ifndef MGPBD_EVAL_MINB
 #define MGPBD_EVAL_MINB 8
 #endif
+template <class T, bool HV>
 __global__ void __launch_bounds__(MGPBD_EVAL_BS, MGPBD_EVAL_MINB) k_eval_arap(int32_t m, const int32_t* __restrict__ verts, const double* __restrict__ x,
                             const double* __restrict__ Dminv, const double* __restrict__ sqrtw,
                             const double* __restrict__ alpha, double dt2, const double* __restrict__ lambda,
-                            T* __restrict__ h, T* __restrict__ b) {
+                            T* __restrict__ h, T* __restrict__ b, const EvalHv<T> ehv) {
     int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= m) return;
     int4 tv = reinterpret_cast<const int4*>(verts)[j];
@@ -331,8 +350,14 @@ __global__ void __launch_bounds__(MGPBD_EVAL_BS, MGPBD_EVAL_MINB) k_eval_arap(in
         }
     T* hj = h + 12 * (int64_t)j;
     double C = 0.0;
+    const double aj = alpha[j] / dt2;
     if (!finite) {
         for (int k = 0; k < 12; ++k) hj[k] = (T)0;
+        if (HV) {
+            T z[12];
+            for (int k = 0; k < 12; ++k) z[k] = (T)0;
+            write_hv<T, 4>(ehv, j, z, aj);
+        }
     } else {
         double R[9], E[9];
         if (!polar_newton(F, R)) polar_rotation(F, R);
@@ -356,8 +381,9 @@ __global__ void __launch_bounds__(MGPBD_EVAL_BS, MGPBD_EVAL_MINB) k_eval_arap(in
             double2* d = reinterpret_cast<double2*>(hj);
             for (int k = 0; k < 6; ++k) d[k] = make_double2((double)o[2 * k], (double)o[2 * k + 1]);
         }
+        if (HV) write_hv<T, 4>(ehv, j, o, aj);
     }
-    b[j] = (T)(-C - (alpha[j] / dt2) * lambda[j]);
+    b[j] = (T)(-C - aj * lambda[j]);
 }
 
 // ----------------------------------------------------------------------------- assembly
@@ -548,13 +574,19 @@ void build_pattern(const int32_t* verts, int32_t m, int kc, int32_t nv, const in
 template <class T>
 void eval_constraints(int kind, int32_t m, const int32_t* verts, const double* x, const double* rest,
                       const double* sqrtw, const double* alpha, double dt, const double* lambda, T* h, T* b,
-                      cudaStream_t s) {
+                      cudaStream_t s, const EvalHv<T>* hvout) {
     if (!m) return;
     double dt2 = dt * dt;
-    if (kind == 2)
-        k_eval_distance<T><<<grid1d(m), 256, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b);
-    else
-        k_eval_arap<T><<<grid1d(m, MGPBD_EVAL_BS), MGPBD_EVAL_BS, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b);
+    const EvalHv<T> e = hvout ? *hvout : EvalHv<T>();
+    if (kind == 2) {
+        if (hvout) k_eval_distance<T, true><<<grid1d(m), 256, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b, e);
+        else k_eval_distance<T, false><<<grid1d(m), 256, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b, e);
+    } else {
+        if (hvout)
+            k_eval_arap<T, true><<<grid1d(m, MGPBD_EVAL_BS), MGPBD_EVAL_BS, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b, e);
+        else
+            k_eval_arap<T, false><<<grid1d(m, MGPBD_EVAL_BS), MGPBD_EVAL_BS, 0, s>>>(m, verts, x, rest, sqrtw, alpha, dt2, lambda, h, b, e);
+    }
     MG_LAUNCH_CHECK();
 }
 
@@ -619,7 +651,8 @@ void sqrt_vec(int32_t n, const double* w, double* out, cudaStream_t s) {
 
 #define MG_INST(T)                                                                                          \
     template void eval_constraints<T>(int, int32_t, const int32_t*, const double*, const double*, const double*, \
-                                      const double*, double, const double*, T*, T*, cudaStream_t);           \
+                                      const double*, double, const double*, T*, T*, cudaStream_t,            \
+                                      const EvalHv<T>*);                                                     \
     template void assemble<T>(int, int32_t, const int32_t*, const T*, const double*, double, const int64_t*,  \
                               const int32_t*, int, T*, T*, cudaStream_t, int32_t, int32_t);                  \
     template void update_positions<T>(int32_t, int, const int64_t*, const int32_t*, const T*, const double*,  \

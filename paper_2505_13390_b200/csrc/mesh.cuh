@@ -18,10 +18,21 @@ void build_pattern(const int32_t* verts, int32_t m, int kc, int32_t nv, const in
                    const int32_t* vlist, DBuf<int64_t>& rowptr, DBuf<int32_t>& col, cudaStream_t s);
 
 // Constraint evaluation (Alg. 1 l.4 + l.6): scaled gradients h = sqrt(w) grad C and b = -C - at*lambda.
+// EvalHv (optional, one rank, every row): the kernel also writes the matrix-free operator's per-outer-iteration data
+// that k_mf_refresh would build from h — the vertex-major planes hv[plane npad + inv[j kc + k]] = h_{j,k,plane}
+// (inv: padded slot of incidence (j, k)), at_j = alpha_j / dt^2 and dinv_j with k_mf_refresh's expression.
+template <class T>
+struct EvalHv {
+    const int32_t* inv = nullptr;
+    T* hv = nullptr;
+    int64_t npad = 0;
+    T* at = nullptr;
+    T* dinv = nullptr;
+};
 template <class T>
 void eval_constraints(int kind, int32_t m, const int32_t* verts, const double* x, const double* rest,
                       const double* sqrtw, const double* alpha, double dt, const double* lambda,
-                      T* h, T* b, cudaStream_t s);
+                      T* h, T* b, cudaStream_t s, const EvalHv<T>* hvout = nullptr);
 
 // Numeric re-assembly (Alg. 1 l.5) into the fixed pattern; also dinv = 1/A_ii.
 template <class T>
