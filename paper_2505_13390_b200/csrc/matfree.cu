@@ -415,8 +415,12 @@ __global__ void __launch_bounds__(VG_BS) k_mf_vgather_tma(int32_t v0, int32_t v1
 
 // Eq. 5 position update from the vertex-major gradients: x_v += omega sqrt(w_v) sum_{(j,s) at v}
 // h_{j,s} dl_j over the same padded layout (fp64 lane partials, fixed butterfly).
+#ifndef MGPBD_UPD_THREADS
+#define MGPBD_UPD_THREADS 256
+#endif
+constexpr int UPD_BS = MGPBD_UPD_THREADS;   // threads per CTA of the Eq. 5 update (build switch)
 template <class T, int G, int UN, bool J16>
-__global__ void __launch_bounds__(MF_BS) k_mf_update(int32_t v0, int32_t v1, int64_t npad,
+__global__ void __launch_bounds__(UPD_BS) k_mf_update(int32_t v0, int32_t v1, int64_t npad,
                                                      const int64_t* __restrict__ ppos,
                                                      const uint16_t* __restrict__ vj16,
                                                      const int32_t* __restrict__ vj32,
@@ -960,11 +964,11 @@ void mf_pass(int mode, const MatFree<T>& A, const T* x, const T* b, T* y, const 
 
 // grid of the vertex-major update: the resident CTAs only when the ranges are blocked (persistent), else grid-stride
 static int update_grid(const void* k, int64_t threads) {
-    int grid = (int)std::min<int64_t>((threads + MF_BS - 1) / MF_BS, 148 * 16);
+    int grid = (int)std::min<int64_t>((threads + UPD_BS - 1) / UPD_BS, 148 * 16);
     if (MGPBD_VG_BLOCKED) {
         int occ = 1;
-        MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, MF_BS, 0));
-        grid = (int)std::min<int64_t>((threads + MF_BS - 1) / MF_BS, (int64_t)vg_sms() * std::max(1, occ));
+        MG_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, UPD_BS, 0));
+        grid = (int)std::min<int64_t>((threads + UPD_BS - 1) / UPD_BS, (int64_t)vg_sms() * std::max(1, occ));
     }
     return std::max(grid, 1);
 }
@@ -975,13 +979,13 @@ void mf_update(const MatFree<T>& A, const T* dl, const double* sqrtw, const doub
     if (A.kc == 4) {  // same lane split as the vertex gather (G = 4, UN = 2: ~60 registers)
         constexpr int G = 4;
         const int grid = update_grid((const void*)k_mf_update<T, G, 2, true>, (int64_t)(A.v1 - A.v0) * G);
-        if (A.vj16) k_mf_update<T, G, 2, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
-        else k_mf_update<T, G, 2, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
+        if (A.vj16) k_mf_update<T, G, 2, true><<<grid, UPD_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
+        else k_mf_update<T, G, 2, false><<<grid, UPD_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
     } else {
         constexpr int G = 2;
         const int grid = update_grid((const void*)k_mf_update<T, G, 1, true>, (int64_t)(A.v1 - A.v0) * G);
-        if (A.vj16) k_mf_update<T, G, 1, true><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
-        else k_mf_update<T, G, 1, false><<<grid, MF_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
+        if (A.vj16) k_mf_update<T, G, 1, true><<<grid, UPD_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
+        else k_mf_update<T, G, 1, false><<<grid, UPD_BS, 0, s>>>(A.v0, A.v1, A.npad, A.ppos, A.vj16, A.vj32, A.jbase, A.hv, dl, sqrtw, omega, x, vg_sms());
     }
     MG_LAUNCH_CHECK();
 }
