@@ -15,9 +15,15 @@ namespace mgpbd {
 
 namespace {
 
+#ifndef MGPBD_RES_SVL
+#define MGPBD_RES_SVL 8
+#endif
+#ifndef MGPBD_RES_SCH
+#define MGPBD_RES_SCH 5
+#endif
 constexpr int RB = 1024;  // threads per CTA (one CTA per SM)
-constexpr int RSVL = 8;   // lanes per row
-constexpr int RSCH = 5;   // nonzeros per lane per chunk
+constexpr int RSVL = MGPBD_RES_SVL;   // lanes per row (build switch, sweeps)
+constexpr int RSCH = MGPBD_RES_SCH;   // nonzeros per lane per chunk
 constexpr int RRPW = 32 / RSVL;
 constexpr int RCHUNK = RSVL * RSCH;
 constexpr int RWARPS = RB / 32;

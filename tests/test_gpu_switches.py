@@ -98,3 +98,22 @@ def test_dense_bottom_equals_level_by_level_cycle(monkeypatch, precision, tol):
     for key, (z, n) in out.items():
         assert n == nl
         assert rel(z, z0) <= tol, (key, rel(z, z0))
+
+
+@pytest.mark.parametrize("precision", [0, 1], ids=["fp64", "fp32"])
+@pytest.mark.parametrize("switch", ["MGPBD_NO_EVAL_HV=1", "MGPBD_NO_HALO_OVERLAP=1", "MGPBD_NO_X1_FUSE=1"])
+def test_fusions_are_bitwise(monkeypatch, precision, switch):
+    """Fusions that move work between kernels without changing any arithmetic give bit-identical frames: the
+    evaluation writing the vertex-major data (vs k_mf_refresh), the V-cycle's first step formed by the x/r update
+    (vs k_jacobi0), the overlapped halo exchange (one rank: no halo, same path)."""
+    sc = scenes.make("block_small")
+    outs = []
+    for sw in ("", switch):
+        for kv in sw.split():
+            k, v = kv.split("=")
+            monkeypatch.setenv(k, v)
+        ctx = mgpbd.Context.from_scene(sc, precision=precision, min_coarse=30)
+        ctx.step(sc.dt, ITERS)
+        outs.append((ctx.lambdas(), ctx.positions()))
+        ctx.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1]), switch
