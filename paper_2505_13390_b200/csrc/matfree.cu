@@ -147,7 +147,7 @@ struct Chunk {
 #define MGPBD_VG_PREFETCH 1
 #endif
 // 2 (default): contiguous vertex range per CTA of a persistent grid (x values reused from L1 across the
-// constraints a vertex plane shares with the next: 45.9 -> 43.4 us per fp32 pass, profiles/r2/sweep_vgather.txt);
+// constraints a vertex plane shares with the next: 45.9 -> 43.4 us per fp32 pass, profiles/r2/experiments_log.txt);
 // 1: the same with the ranges of the CTAs co-resident on an SM adjacent; 0: grid-stride
 #ifndef MGPBD_VG_BLOCKED
 #define MGPBD_VG_BLOCKED 2
