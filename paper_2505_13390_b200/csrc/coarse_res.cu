@@ -582,7 +582,7 @@ void coarse_vcycle_res(const CoarseCycle<T>& c, const ResPlan& plan, cudaStream_
     }
     // programmatic dependent launch (MGPBD_COARSE_PDL): the CTAs stage their static slices while the preceding
     // kernel (the level-0 restriction) finishes; griddepcontrol.wait precedes the first read of b
-    static const bool pdl = std::getenv("MGPBD_COARSE_PDL") != nullptr;
+    const bool pdl = std::getenv("MGPBD_COARSE_PDL") != nullptr;
     if (pdl && (mode == 0 || mode == 1 || mode == 3)) {
         attr_[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr_[na].val.programmaticStreamSerializationAllowed = 1;

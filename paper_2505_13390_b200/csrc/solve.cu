@@ -576,7 +576,8 @@ inline int chunk_grid(int64_t n, int cpt = 1) {
 }
 // chunks per thread of the PCG update kernels (MGPBD_VEC_CPT: 1 or 4)
 inline int vec_cpt() {
-    static const int c = std::getenv("MGPBD_VEC_CPT") ? std::atoi(std::getenv("MGPBD_VEC_CPT")) : 4;
+    const char* e = std::getenv("MGPBD_VEC_CPT");  // read per call (launch/capture time): tests toggle it
+    const int c = e ? std::atoi(e) : 4;
     return c == 1 || c == 2 || c == 8 ? c : 4;
 }
 
@@ -1416,7 +1417,7 @@ void restrict_members(int32_t nc, const int64_t* mptr, const int32_t* mlist, con
     if (!nc) return;
     // 16 lanes per aggregate, 4 member loads in flight per lane (tools/ab_frames.py on hierarchy B: 68.27 ms/frame
     // with 8 x 4, 67.91 with 16 x 4; 4 x 4/8, 8 x 8, 16 x 2, 32 x 2/4 between or slower); MGPBD_RESTRICT_G8=1: 8 x 4
-    static const bool g8 = std::getenv("MGPBD_RESTRICT_G8") != nullptr;
+    const bool g8 = std::getenv("MGPBD_RESTRICT_G8") != nullptr;
     const int g = (int)std::min<int64_t>(((int64_t)nc * (g8 ? 8 : 16) * 4 + PB - 1) / PB, 148 * 8);
     if (g8) k_restrict<T, 8, 4><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
     else k_restrict<T, 16, 4><<<g, PB, 0, s>>>(nc, mptr, mlist, t, bc);
@@ -1503,7 +1504,7 @@ template <class T>
 void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cudaStream_t s) {
     const int32_t n = A.n;
     size_t bytes = (size_t)n * n * sizeof(double);
-    static const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
+    const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
     // (the one-CTA scalar Gauss-Jordan in shared memory is n barrier-separated steps: 241 us at n = 102
     // against ~40 us for the cooperative blocked kernel, so it only serves as the MGPBD_NO_GJ_COOP path)
     if (!coop && bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
