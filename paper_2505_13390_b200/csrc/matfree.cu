@@ -209,9 +209,6 @@ __global__ void __launch_bounds__(vg_threads<T>(), MGPBD_VG_MINB) k_mf_vgather(i
                                                       const int32_t* __restrict__ jbase, const T* __restrict__ hv,
                                                       const T* __restrict__ x, V4<T>* __restrict__ u,
                                                       const T* __restrict__ xd, const T* __restrict__ xb, double xom, int nsm) {
-    // programmatic dependent launch: the row kernel may start streaming its static operands now; it
-    // waits (griddepcontrol.wait) for this grid's u before gathering it
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     using CH = Chunk<T, J16>;
     constexpr int VW = CH::VW;
     constexpr int PER_WARP = 32 / G;
@@ -237,6 +234,11 @@ __global__ void __launch_bounds__(vg_threads<T>(), MGPBD_VG_MINB) k_mf_vgather(i
     // launched with programmatic dependent launch (MatFree::vg_pdl): everything above reads static data; x is
     // the previous kernel's output (no-op otherwise)
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // programmatic dependent launch: the row kernel may start streaming its operands now (it waits in
+    // griddepcontrol.wait for this grid's u before gathering it).  Released after this grid's own wait, so
+    // that everything launched before it (the kernel that wrote x, b) is complete when the row kernel's
+    // pre-wait prologue reads it, whichever kernel released this grid early (MG_VEC_TRIGGER, solve.cu)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     for (int64_t base = first; base < vend; base += step) {  // warp-uniform
         const int64_t v = base + sub;
         using AC = typename std::conditional<MGPBD_VG_ACC64 != 0, double, T>::type;

@@ -581,8 +581,21 @@ inline int vec_cpt() {
     return c == 1 || c == 2 || c == 8 ? c : 4;
 }
 
+// The PCG vector kernels that precede a level-0 pass (Jacobi-0, prolongation, p update, x / r update) release
+// the pass's PDL-launched vertex gather at their start: its persistent CTAs (one per SM, the whole register
+// file) become resident as this grid's CTAs leave each SM, run their static prologue and wait in
+// griddepcontrol.wait for this grid's completion (MGPBD_VEC_TRIGGER=0: released at exit).
+#ifndef MGPBD_VEC_TRIGGER
+#define MGPBD_VEC_TRIGGER 1
+#endif
+#define MG_VEC_TRIGGER()                                                                 \
+    do {                                                                                 \
+        if (MGPBD_VEC_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    } while (0)
+
 template <class T, bool V>
 __global__ void k_jacobi0(int32_t n, const T* __restrict__ dinv, const T* __restrict__ b, double omega, T* __restrict__ y) {
+    MG_VEC_TRIGGER();
     using C = Chunk16<T, V>;
     const int64_t c = blockIdx.x * (int64_t)PB + threadIdx.x;
     if (c * C::W >= n) return;
@@ -624,6 +637,7 @@ __global__ void k_restrict(int32_t nc, const int64_t* __restrict__ mptr, const i
 template <class T, bool V>
 __global__ void k_prolong(int32_t n, const int32_t* __restrict__ agg, const T* __restrict__ P, const T* __restrict__ e,
                           T* __restrict__ x) {
+    MG_VEC_TRIGGER();
     using C = Chunk16<T, V>;
     constexpr int W = C::W;
     const int64_t c = blockIdx.x * (int64_t)PB + threadIdx.x;
@@ -695,6 +709,7 @@ template <class T, bool V, int CPT>
 __global__ void k_pcg_p_fin(int32_t n, const T* __restrict__ z, T* __restrict__ p, double* __restrict__ scal, int k,
                             const double* __restrict__ prz, const double* __restrict__ prr, int np, int* flags,
                             int tag, const double* __restrict__ fin) {
+    MG_VEC_TRIGGER();
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
     // CPT chunks per thread (chunk c of the block strided by PB: coalesced), all loaded before the partial sums,
@@ -761,6 +776,7 @@ __global__ void k_pcg_xr_fin(int32_t n, const T* __restrict__ p, const T* __rest
                              T* __restrict__ r, double* __restrict__ scal, int k, const double* __restrict__ ppq,
                              int np, int* flags, int tag, const T* __restrict__ dinv, double om0, T* __restrict__ x1,
                              const double* __restrict__ fin) {
+    MG_VEC_TRIGGER();
     if (scal[SC_DONE] != 0.0) return;
     using CK = Chunk16<T, V>;
     constexpr int W = CK::W;
