@@ -1171,6 +1171,7 @@ class Engine : public EngineBase {
                                 r0, r1);
                 kgal_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.kk, a.kp.pptr.p, a.kpval.p, a.kp.coff.p, a.agg.p,
                                 a.n_agg, a.erow.p, a.acol.p, a.xoff.p, c.rowptr, c.n, a.kW.p, c.val.p, c.dinv.p, st);
+                if (l == 0) mark_stage(1);
                 continue;
             }
             if (l == 0 && va_ok && mf_on()) {  // from h directly (replicated on every rank, no collective)
@@ -1184,10 +1185,12 @@ class Engine : public EngineBase {
                                     c.val.p, nullptr, st, tb0, te0);
                 comm->allreduce(c.val.p, (size_t)c.nnz, st);
                 diag_inv<T>(c.n, c.rowptr, c.val.p, c.dinv.p, st);
+                mark_stage(1);
                 continue;
             }
             galerkin_numeric<T>(a.plan, a.rowptr, a.col, a.val.p, a.P.p, a.n_agg, c.rowptr, c.nnz, a.tval.p, c.val.p,
                                 c.dinv.p, st);
+            if (l == 0) mark_stage(1);  // (stage stamps: level-0 product done)
         }
         mark_stage(2);
         coarse_invert<T>(L[nL - 1]->hot(), inv_work.p, Ainv.p, flags.p, st);
@@ -1265,9 +1268,13 @@ class Engine : public EngineBase {
         Level& c = *L[l + 1];
         if (a.kk > 1) {  // general P (k > 1): r = b - A x, b_c = P^T r, x += P e
             pass(l, PASS_RESID_P, cur, b, a.vt.p, a.kones.p, 0.0);
+            if (l == 0 && vc_trace) mark_stage(11);
             krestrict<T>(c.n, a.kk, a.kp.dof_agg.p, a.kp.coff.p, a.mptr.p, a.mlist.p, a.kQs.p, a.vt.p, c.vb.p, st);
+            if (l == 0 && vc_trace) mark_stage(12);
             vcycle(l + 1, c.vb.p, c.vz.p, nullptr);
+            if (l == 0 && vc_trace) mark_stage(13);
             kprolong<T>(o, cn, a.kp.pptr.p, a.kp.pcol.p, a.kpval.p, c.vz.p, cur, st);
+            if (l == 0 && vc_trace) mark_stage(14);
         } else {
             pass(l, PASS_RESID_P, cur, b, a.vt.p, a.P.p, 0.0);
             if (l == 0 && vc_trace) mark_stage(11);
