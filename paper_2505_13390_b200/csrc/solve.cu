@@ -1054,6 +1054,61 @@ __global__ void __launch_bounds__(256) k_gj_update(int32_t n, double* __restrict
     }
 }
 
+// The same panel update for large n (the k > 1 hierarchies' coarsest levels of 2-8K rows, where the cooperative
+// kernel recomputes R = P K in every 32 x 32 tile and streams its operands at two shared loads per FMA): 64 x 64
+// output tile per CTA, thread (tx, ty) of 16 x 16 owns rows ty + 16a and columns tx + 16b (a, b < 4), so each
+// k step is 8 shared loads (broadcast / consecutive) for 16 FMAs.  Columns j in K take P in place of R, so the
+// same accumulation gives C P there.  Same outputs as k_gj_update (sums over t in the same order).
+__global__ void __launch_bounds__(256) k_gj_update64(int32_t n, double* __restrict__ W, int32_t k0, int32_t bs,
+                                                     const double* __restrict__ P, const double* __restrict__ C,
+                                                     const double* __restrict__ R) {
+    __shared__ double Cs[64][GJB + 1];
+    __shared__ double Rs[GJB][64 + 1];
+    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+    const int32_t i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+    for (int q = t; q < 64 * GJB; q += 256) {
+        const int r = q / GJB, u = q % GJB;  // C tile: row r, column u (coalesced over u)
+        const int32_t i = i0 + r;
+        Cs[r][u] = (i < n && u < bs && !(i >= k0 && i < k0 + bs)) ? C[(int64_t)i * bs + u] : 0.0;
+        const int u2 = q / 64, c = q % 64;  // R tile: row u2, column c (coalesced over c)
+        const int32_t j = j0 + c;
+        double rv = 0.0;
+        if (u2 < bs && j < n) rv = (j >= k0 && j < k0 + bs) ? P[u2 * bs + (j - k0)] : R[(int64_t)u2 * n + j];
+        Rs[u2][c] = rv;
+    }
+    __syncthreads();
+    double acc[4][4] = {};
+#pragma unroll 8
+    for (int u = 0; u < GJB; ++u) {
+        double cv[4], rv[4];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) cv[a] = Cs[ty + 16 * a][u];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rv[b] = Rs[u][tx + 16 * b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) acc[a][b] += cv[a] * rv[b];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int32_t i = i0 + ty + 16 * a;
+        if (i >= n) continue;
+        const bool iK = i >= k0 && i < k0 + bs;
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int32_t j = j0 + tx + 16 * b;
+            if (j >= n) continue;
+            const bool jK = j >= k0 && j < k0 + bs;
+            double* w = &W[(int64_t)i * n + j];
+            if (!iK && !jK) *w -= acc[a][b];
+            else if (iK && !jK) *w = R[(int64_t)(i - k0) * n + j];
+            else if (!iK && jK) *w = -acc[a][b];
+            else *w = P[(i - k0) * bs + (j - k0)];
+        }
+    }
+}
+
 // Blocked Gauss-Jordan inverse as ONE cooperative kernel (one grid barrier per 32-wide panel instead of
 // three launches).  Ping-pong between two n x n buffers so no tile reads a value another CTA writes in
 // the same panel.  Every CTA inverts the 32x32 pivot block itself (all 256 threads, 4 entries each,
@@ -1207,6 +1262,11 @@ void tile_config(int32_t n, int64_t nnz, const int64_t* rowptr, int& vlr, int& g
     MG_CK(cudaStreamSynchronize(s));
     tile_nnz = std::max(1, h);
     if ((size_t)tile_nnz * sizeof(double) > 200 * 1024) vlr = 0;  // fall back to the warp-per-row kernel
+    // rows of >= 128 entries on average (vlr 16 / 32): the warp-per-row kernel k_pass, 32 lanes per row, streams
+    // them far faster than the tile kernel, whose per-tile shared-memory products (25-50 KB) leave 4 CTAs per SM
+    // with 3 serialised latencies per tile (k = 6 coarse levels of 200-600 entries per row: the 2-outer-iteration
+    // frame 100.8 -> 61.1 ms, profiles/r2/experiments_log.txt); MGPBD_TILE_LONG_ROWS=1 keeps the tile kernel
+    if (vlr >= 16 && !std::getenv("MGPBD_TILE_LONG_ROWS")) vlr = 0;
 }
 
 namespace {
@@ -1520,10 +1580,13 @@ template <class T>
 void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cudaStream_t s) {
     const int32_t n = A.n;
     size_t bytes = (size_t)n * n * sizeof(double);
-    const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr;
+    // n >= MGPBD_GJ_BIG_N (default 1024): the 3-kernel panel loop with the register-tiled update (k_gj_update64)
+    const char* bn = std::getenv("MGPBD_GJ_BIG_N");
+    const bool big = n >= (bn ? std::atoi(bn) : 1024);
+    const bool coop = std::getenv("MGPBD_NO_GJ_COOP") == nullptr && !big;
     // (the one-CTA scalar Gauss-Jordan in shared memory is n barrier-separated steps: 241 us at n = 102
     // against ~40 us for the cooperative blocked kernel, so it only serves as the MGPBD_NO_GJ_COOP path)
-    if (!coop && bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
+    if (!coop && !big && bytes <= 160 * 1024) {  // small: whole matrix in one CTA's shared memory
         if (bytes > 48 * 1024)
             ensure_dyn_smem((const void*)k_coarse_inv<T>, bytes);
         k_coarse_inv<T><<<1, 1024, bytes, s>>>(n, A.rowptr, A.col, A.val, work, Ainv, flags, 1);
@@ -1567,7 +1630,8 @@ void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cuda
         k_gj_panel<<<(int)std::min<int64_t>((2 * (int64_t)n * bs + 255) / 256, 148 * 8), 256, 0, s>>>(n, Ainv, k0, bs, P,
                                                                                                    Cb, Rb);
         MG_LAUNCH_CHECK();
-        k_gj_update<<<ug, 256, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
+        if (big) k_gj_update64<<<dim3((n + 63) / 64, (n + 63) / 64), 256, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
+        else k_gj_update<<<ug, 256, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
         MG_LAUNCH_CHECK();
     }
 }

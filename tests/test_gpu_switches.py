@@ -16,8 +16,9 @@ MF_SWITCHES = ["", "MGPBD_NO_GRAPH=1", "MGPBD_NO_TMA=1", "MGPBD_NO_RES_COARSE=1"
                "MGPBD_RES_CAP=4096", "MGPBD_FUSE_J0=1", "MGPBD_NO_FUSED_TAIL=1",
                "MGPBD_TAIL_SCALAR_BCAST=1", "MGPBD_SOLO=1", "MGPBD_SOLO=1 MGPBD_NO_TAIL=1",
                "MGPBD_DENSE_CUT=0", "MGPBD_DENSE_CUT=64", "MGPBD_DENSE_CUT=100000",
-               "MGPBD_DENSE_CUT=64 MGPBD_NO_TAIL=1", "MGPBD_DENSE_CUT=64 MGPBD_NO_RES_COARSE=1", "MGPBD_NO_X1_FUSE=1", "MGPBD_FIN_IN_ROWS=1", "MGPBD_NO_VG_PDL=1", "MGPBD_VEC_CPT=1", "MGPBD_RESTRICT_G8=1", "MGPBD_NO_EVAL_HV=1"]
-CSR_SWITCHES = ["", "MGPBD_NO_BAND=1", "MGPBD_NO_ROWS=1", "MGPBD_NO_BAND=1 MGPBD_NO_ROWS=1"]
+               "MGPBD_DENSE_CUT=64 MGPBD_NO_TAIL=1", "MGPBD_DENSE_CUT=64 MGPBD_NO_RES_COARSE=1", "MGPBD_NO_X1_FUSE=1", "MGPBD_FIN_IN_ROWS=1", "MGPBD_NO_VG_PDL=1", "MGPBD_VEC_CPT=1", "MGPBD_RESTRICT_G8=1", "MGPBD_NO_EVAL_HV=1",
+               "MGPBD_GJ_BIG_N=0", "MGPBD_TILE_LONG_ROWS=1"]
+CSR_SWITCHES = ["", "MGPBD_NO_BAND=1", "MGPBD_NO_ROWS=1", "MGPBD_NO_BAND=1 MGPBD_NO_ROWS=1", "MGPBD_GJ_BIG_N=0"]
 ITERS = 3
 
 
