@@ -1056,17 +1056,41 @@ __global__ void __launch_bounds__(256) k_gj_update(int32_t n, double* __restrict
 
 // The same panel update for large n (the k > 1 hierarchies' coarsest levels of 2-8K rows, where the cooperative
 // kernel recomputes R = P K in every 32 x 32 tile and streams its operands at two shared loads per FMA): 64 x 64
-// output tile per CTA, thread (tx, ty) of 16 x 16 owns rows ty + 16a and columns tx + 16b (a, b < 4), so each
-// k step is 8 shared loads (broadcast / consecutive) for 16 FMAs.  Columns j in K take P in place of R, so the
-// same accumulation gives C P there.  Same outputs as k_gj_update (sums over t in the same order).
-__global__ void __launch_bounds__(256) k_gj_update64(int32_t n, double* __restrict__ W, int32_t k0, int32_t bs,
-                                                     const double* __restrict__ P, const double* __restrict__ C,
-                                                     const double* __restrict__ R) {
+// output tile per CTA of 512 threads, thread (tx, ty) of 32 x 16 owns rows ty + 16a (a < 4) and columns tx + 32b
+// (b < 2), so each k step is 6 shared loads (broadcast / consecutive) for 8 FMAs; the thread's old W values are
+// loaded before the staging.  Columns j in K take P in place of R, so the same accumulation gives C P there.  Same
+// outputs as k_gj_update (sums over t in the same order).  n = 7656 (k = 6 bench hierarchy), per inverse: 118 ms
+// with 256 threads x 16 outputs, 110 with the early W loads, 94 with 512 threads at 2 CTAs per SM (1 CTA per SM
+// at 108 registers: 148; 3 CTAs at 40 registers: 100).
+#ifndef MGPBD_GJ_PREFETCH
+#define MGPBD_GJ_PREFETCH 1
+#endif
+#ifndef MGPBD_GJU_T
+#define MGPBD_GJU_T 512
+#endif
+#ifndef MGPBD_GJU_MINB
+#define MGPBD_GJU_MINB 2
+#endif
+constexpr int GJU_T = MGPBD_GJU_T;           // threads per CTA: 256 (4 x 4 outputs each) or 512 (4 x 2)
+constexpr int GJU_CX = GJU_T == 512 ? 32 : 16;  // thread columns
+constexpr int GJU_NB = 64 / GJU_CX;             // columns per thread
+__global__ void __launch_bounds__(GJU_T, MGPBD_GJU_MINB) k_gj_update64(int32_t n, double* __restrict__ W, int32_t k0, int32_t bs,
+                                                       const double* __restrict__ P, const double* __restrict__ C,
+                                                       const double* __restrict__ R) {
     __shared__ double Cs[64][GJB + 1];
     __shared__ double Rs[GJB][64 + 1];
-    const int t = threadIdx.x, tx = t & 15, ty = t >> 4;
+    const int t = threadIdx.x, tx = t % GJU_CX, ty = t / GJU_CX;
     const int32_t i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-    for (int q = t; q < 64 * GJB; q += 256) {
+    // the old values this thread updates are loaded first: their HBM latency overlaps the staging + products
+    double wold[4][GJU_NB];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < GJU_NB; ++b) {
+            const int32_t i = i0 + ty + 16 * a, j = j0 + tx + GJU_CX * b;
+            wold[a][b] = (MGPBD_GJ_PREFETCH && i < n && j < n) ? W[(int64_t)i * n + j] : 0.0;
+        }
+    for (int q = t; q < 64 * GJB; q += GJU_T) {
         const int r = q / GJB, u = q % GJB;  // C tile: row r, column u (coalesced over u)
         const int32_t i = i0 + r;
         Cs[r][u] = (i < n && u < bs && !(i >= k0 && i < k0 + bs)) ? C[(int64_t)i * bs + u] : 0.0;
@@ -1077,18 +1101,18 @@ __global__ void __launch_bounds__(256) k_gj_update64(int32_t n, double* __restri
         Rs[u2][c] = rv;
     }
     __syncthreads();
-    double acc[4][4] = {};
+    double acc[4][GJU_NB] = {};
 #pragma unroll 8
     for (int u = 0; u < GJB; ++u) {
-        double cv[4], rv[4];
+        double cv[4], rv[GJU_NB];
 #pragma unroll
         for (int a = 0; a < 4; ++a) cv[a] = Cs[ty + 16 * a][u];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) rv[b] = Rs[u][tx + 16 * b];
+        for (int b = 0; b < GJU_NB; ++b) rv[b] = Rs[u][tx + GJU_CX * b];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-            for (int b = 0; b < 4; ++b) acc[a][b] += cv[a] * rv[b];
+            for (int b = 0; b < GJU_NB; ++b) acc[a][b] += cv[a] * rv[b];
     }
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -1096,12 +1120,12 @@ __global__ void __launch_bounds__(256) k_gj_update64(int32_t n, double* __restri
         if (i >= n) continue;
         const bool iK = i >= k0 && i < k0 + bs;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int32_t j = j0 + tx + 16 * b;
+        for (int b = 0; b < GJU_NB; ++b) {
+            const int32_t j = j0 + tx + GJU_CX * b;
             if (j >= n) continue;
             const bool jK = j >= k0 && j < k0 + bs;
             double* w = &W[(int64_t)i * n + j];
-            if (!iK && !jK) *w -= acc[a][b];
+            if (!iK && !jK) *w = (MGPBD_GJ_PREFETCH ? wold[a][b] : *w) - acc[a][b];
             else if (iK && !jK) *w = R[(int64_t)(i - k0) * n + j];
             else if (!iK && jK) *w = -acc[a][b];
             else *w = P[(i - k0) * bs + (j - k0)];
@@ -1630,7 +1654,7 @@ void coarse_invert(const Csr<T>& A, double* work, double* Ainv, int* flags, cuda
         k_gj_panel<<<(int)std::min<int64_t>((2 * (int64_t)n * bs + 255) / 256, 148 * 8), 256, 0, s>>>(n, Ainv, k0, bs, P,
                                                                                                    Cb, Rb);
         MG_LAUNCH_CHECK();
-        if (big) k_gj_update64<<<dim3((n + 63) / 64, (n + 63) / 64), 256, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
+        if (big) k_gj_update64<<<dim3((n + 63) / 64, (n + 63) / 64), GJU_T, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
         else k_gj_update<<<ug, 256, 0, s>>>(n, Ainv, k0, bs, P, Cb, Rb);
         MG_LAUNCH_CHECK();
     }
