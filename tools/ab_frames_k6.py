@@ -1,3 +1,11 @@
+"""A/B frame timing of the k = 6 near-kernel path on block1.67M (GPU box).
+
+Each variant (environment switches, e.g. MGPBD_GJ_BIG_N=100000 or MGPBD_TILE_LONG_ROWS=1) runs in its own process:
+frame 0 builds the hierarchy (no re-setups after it), then 3 more frames of 2 outer iterations each; prints the
+per-frame device times and the level sizes.
+
+  python tools/ab_frames_k6.py "" "MGPBD_TILE_LONG_ROWS=1"
+"""
 import os, subprocess, sys
 CH = r'''
 import sys; sys.path.insert(0, ".")
